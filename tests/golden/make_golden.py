@@ -1,0 +1,163 @@
+"""Generate golden vectors from the REAL reference (run in the build container).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Imports ``vecpomdp`` from /root/reference/pkg/src (read-only, never copied)
+and writes small ``.npz`` fixtures next to this script.  The GPU box has no
+/root/reference, so tests only ever read the committed fixtures.
+
+Cases (see SURVEY.md section 4 "parity ladder" and Appendix C):
+* rng_*       -- RowRng / BoundRng draws (rng.py:26-120)
+* formulas    -- softmax / LSE / sample_actions / match_or_append_pairs /
+                 aggregate_leaves / action_q_values examples
+* plan_*      -- full ``plan()`` trees on MARS, Tiger and (reference solver
+                 driving the oracle's new models) Synthetic and Light-Dark
+* episode_*   -- closed-loop ``run_episode`` records
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import vecpomdp as ref  # noqa: E402
+from vecpomdp.envs import MarsModel, tiger_model  # noqa: E402
+
+import oracle  # noqa: E402  (only for the two NEW models the reference lacks)
+
+
+def tree_arrays(tree, full_prefs: bool) -> dict:
+    out = {
+        "parent_action": tree.parent_action.astype(np.int32),
+        "parent_obs": tree.parent_obs.astype(np.int64),
+        "depth": tree.depth.astype(np.int16),
+        "action_parent_belief": tree.action_parent_belief.astype(np.int32),
+        "action_id": tree.action_id.astype(np.int16),
+        "action_reward_sum": tree.action_reward_sum.copy(),
+        "action_visits": tree.action_visits.astype(np.int32),
+        "prefs_row_sum": tree.prefs.sum(axis=1),
+        "prefs_root": tree.prefs[0].copy(),
+    }
+    if full_prefs:
+        out["prefs"] = tree.prefs.copy()
+    return out
+
+
+def gen_rng():
+    out = {}
+    rows = np.concatenate([np.arange(64), np.array([1000, 123456, 2**31 - 1, 2**40 + 7])]).astype(np.int64)
+    seeds = [0, 1, 42, 2**63 + 5, 123456789]
+    keys, uni, uni3, nor = [], [], [], []
+    for s in seeds:
+        r = ref.RowRng.from_seed(s)
+        for path in [(), (0,), (1, 0), (3, 5, 7), (2, 11)]:
+            d = r.derive(*path)
+            keys.append(int(d.key))
+            uni.append(d.uniform(rows))
+            uni3.append(d.uniform(rows, 3))
+            nor.append(d.normal(rows, 2))
+    out["rows"] = rows
+    out["keys"] = np.array(keys, dtype=np.uint64)
+    out["uniform"] = np.stack(uni)
+    out["uniform_k3"] = np.stack(uni3)
+    out["normal_k2"] = np.stack(nor)
+    out["uniform1"] = np.array([ref.RowRng.from_seed(12).derive(4).uniform1()])
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), **out)
+
+
+def gen_formulas():
+    g = np.random.default_rng(7)
+    out = {}
+    rows = g.normal(size=(40, 13)) * 3.0
+    out["lse_in"] = rows
+    out["lse_eta2"] = ref.log_sum_exp_rows(rows, 2.0)
+    out["softmax_eta2"] = ref.softmax_rows(rows, 2.0)
+    # sample_actions with groups (multi-group path) and single group path
+    pol = ref.softmax_rows(g.normal(size=(5, 7)), 1.5)
+    groups = g.integers(0, 5, size=300)
+    rng = ref.RowRng.from_seed(3).derive(9)
+    out["sa_pol"] = pol
+    out["sa_groups"] = groups
+    out["sa_multi"] = ref.sample_actions(pol, rng.bind(np.arange(300)), groups=groups)
+    out["sa_single"] = ref.sample_actions(pol[:1], rng.bind(np.arange(300)), groups=np.zeros(300, dtype=np.int64))
+    # match_or_append_pairs on 10^4 random pairs
+    ex = np.unique(g.integers(0, 50, size=(300, 2)), axis=0)
+    g.shuffle(ex)
+    q = g.integers(0, 60, size=(10_000, 2))
+    rows_out, n_new = ref.match_or_append_pairs(ex, q)
+    out["moa_existing"], out["moa_query"], out["moa_rows"], out["moa_new"] = ex, q, rows_out, np.array([n_new])
+    np.savez_compressed(os.path.join(HERE, "formulas.npz"), **out)
+
+
+def make_model(kind: str, seed: int):
+    if kind.startswith("mars"):
+        n, m = map(int, kind[4:].split("_"))
+        return MarsModel(n=n, m=m, layout_seed=seed)
+    if kind == "tiger":
+        return tiger_model()
+    if kind == "synthetic":
+        return oracle.SyntheticModel(n_actions=16, n_obs=8, seed=seed)
+    if kind == "lightdark":
+        return oracle.LightDarkModel()
+    raise ValueError(kind)
+
+
+# (name, model kind, n_parallel, iterations, seeds, full_prefs)
+PLAN_CASES = [
+    ("plan_mars4_3", "mars4_3", 64, 6, [0, 1, 2], True),
+    ("plan_mars7_8_c1", "mars7_8", 1024, 8, [0, 1], False),
+    ("plan_mars7_8_small", "mars7_8", 96, 5, [3], True),
+    ("plan_tiger", "tiger", 256, 8, [0, 1], True),
+    ("plan_synthetic", "synthetic", 256, 6, [0, 1], True),
+    ("plan_lightdark", "lightdark", 128, 5, [0, 1], True),
+]
+
+
+def gen_plans():
+    manifest = {}
+    for name, kind, n_par, iters, seeds, full in PLAN_CASES:
+        arrays = {}
+        meta = []
+        for s in seeds:
+            model = make_model(kind, s)
+            belief = ref.ParticleBelief.from_model(model, 2000, ref.RowRng.from_seed(s).derive(3))
+            cfg = ref.SolverConfig(n_parallel=n_par, iterations=iters, eta=2.0)
+            out = ref.plan(belief, model, cfg, ref.RowRng.from_seed(s).derive(1, 0))
+            for k, v in tree_arrays(out.tree, full).items():
+                arrays[f"s{s}_{k}"] = v
+            meta.append({"seed": s, "chosen_action": out.chosen_action, "iterations_run": out.iterations_run,
+                         "final_d_max": out.final_d_max, "tree_stats": out.tree_stats})
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+        manifest[name] = {"kind": kind, "n_parallel": n_par, "iterations": iters, "particles": 2000,
+                          "eta": 2.0, "runs": meta}
+    return manifest
+
+
+def gen_episodes():
+    out = {}
+    cfg = ref.SolverConfig(n_parallel=64, iterations=4, particles=500)
+    recs = []
+    for s in range(3):
+        rec = ref.run_episode(MarsModel(n=4, m=3, layout_seed=s), cfg, seed=s)
+        recs.append({"seed": s, "return": rec.discounted_return, "steps": rec.steps,
+                     "reason": rec.terminal_reason, "degenerate": rec.degenerate_updates})
+    out["episode_mars4_3"] = recs
+    return out
+
+
+if __name__ == "__main__":
+    gen_rng()
+    gen_formulas()
+    manifest = {"plans": gen_plans(), "episodes": gen_episodes(),
+                "numpy": np.__version__, "reference": "/root/reference/pkg/src/vecpomdp @ 0.1.0"}
+    with open(os.path.join(HERE, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=1, sort_keys=True)
+    print("wrote golden fixtures to", HERE)

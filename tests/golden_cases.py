@@ -1,0 +1,62 @@
+"""Shared helpers: rebuild the golden plan cases with the oracle or the device.
+
+The case list mirrors tests/golden/make_golden.py (which ran the REAL
+reference).  Nothing here reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+import oracle
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+
+INT_COLUMNS = ("parent_action", "parent_obs", "depth", "action_parent_belief", "action_id", "action_visits")
+
+
+def manifest() -> dict:
+    with open(os.path.join(GOLDEN, "manifest.json")) as f:
+        return json.load(f)
+
+
+def load(name: str) -> dict:
+    with np.load(os.path.join(GOLDEN, name + ".npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def oracle_model(kind: str, seed: int):
+    if kind.startswith("mars"):
+        n, m = map(int, kind[4:].split("_"))
+        return oracle.MarsModel(n=n, m=m, layout_seed=seed)
+    if kind == "tiger":
+        return oracle.tiger_model()
+    if kind == "synthetic":
+        return oracle.SyntheticModel(n_actions=16, n_obs=8, seed=seed)
+    if kind == "lightdark":
+        return oracle.LightDarkModel()
+    raise ValueError(kind)
+
+
+def plan_inputs(case: dict, seed: int, model=None):
+    """(model, belief, config, rng) exactly as make_golden.py built them."""
+    model = model or oracle_model(case["kind"], seed)
+    belief = oracle.ParticleBelief.from_model(model, case["particles"], oracle.RowRng.from_seed(seed).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=case["n_parallel"], iterations=case["iterations"], eta=case["eta"])
+    rng = oracle.RowRng.from_seed(seed).derive(1, 0)
+    return model, belief, cfg, rng
+
+
+def tree_columns(tables: dict) -> dict:
+    """Golden-comparable columns from a dict of full tables."""
+    out = {k: np.asarray(tables[k]) for k in INT_COLUMNS}
+    out["action_reward_sum"] = np.asarray(tables["action_reward_sum"], dtype=np.float64)
+    prefs = np.asarray(tables["prefs"], dtype=np.float64)
+    out["prefs"] = prefs
+    out["prefs_row_sum"] = prefs.sum(axis=1)
+    out["prefs_root"] = prefs[0]
+    return out

@@ -1,0 +1,99 @@
+"""Pin the CPU oracle against golden vectors produced by the real reference.
+
+CPU-only.  If any of these fail the oracle is not trustworthy and every GPU
+parity claim built on it is void.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_cases import INT_COLUMNS, load, manifest, plan_inputs, tree_columns
+
+
+def test_rng_streams_match_reference():
+    g = load("rng")
+    rows = g["rows"]
+    i = 0
+    for s in [0, 1, 42, 2**63 + 5, 123456789]:
+        r = oracle.RowRng.from_seed(s)
+        for path in [(), (0,), (1, 0), (3, 5, 7), (2, 11)]:
+            d = r.derive(*path)
+            assert int(d.key) == int(g["keys"][i])
+            np.testing.assert_array_equal(d.uniform(rows), g["uniform"][i])
+            np.testing.assert_array_equal(d.uniform(rows, 3), g["uniform_k3"][i])
+            np.testing.assert_array_equal(d.normal(rows, 2), g["normal_k2"][i])
+            i += 1
+    assert oracle.RowRng.from_seed(12).derive(4).uniform1() == g["uniform1"][0]
+
+
+def test_rng_contract_examples():
+    # pkg/tests/test_rng.py:6-61 restated against the oracle
+    with pytest.raises(ValueError):
+        oracle.RowRng.from_seed(1).derive(-1)
+    rng = oracle.RowRng.from_seed(9).derive(1)
+    np.testing.assert_array_equal(rng.uniform(np.arange(4)), rng.uniform(np.arange(4096))[:4])
+    b = oracle.RowRng.from_seed(3).derive(7).bind([5, 6])
+    np.testing.assert_array_equal(b.uniform(), oracle.RowRng.from_seed(3).derive(7).uniform(np.array([5, 6])))
+
+
+def test_formula_vectors():
+    g = load("formulas")
+    np.testing.assert_array_equal(oracle.log_sum_exp_rows(g["lse_in"], 2.0), g["lse_eta2"])
+    np.testing.assert_array_equal(oracle.softmax_rows(g["lse_in"], 2.0), g["softmax_eta2"])
+    rng = oracle.RowRng.from_seed(3).derive(9)
+    got = oracle.sample_actions(g["sa_pol"], rng.bind(np.arange(300)), groups=g["sa_groups"])
+    np.testing.assert_array_equal(got, g["sa_multi"])
+    got1 = oracle.sample_actions(g["sa_pol"][:1], rng.bind(np.arange(300)), groups=np.zeros(300, dtype=np.int64))
+    np.testing.assert_array_equal(got1, g["sa_single"])
+    rows, n_new = oracle.match_or_append_pairs(g["moa_existing"], g["moa_query"])
+    np.testing.assert_array_equal(rows, g["moa_rows"])
+    assert n_new == int(g["moa_new"][0])
+
+
+def test_spec_appendix_c_examples():
+    # SPEC.md:154-157, 163-166, 227-230, 285-288, 294-297, 303-306
+    rows, n_new = oracle.match_or_append_pairs(np.zeros((0, 2)), [(0, 3), (0, 3), (0, 5)])
+    assert list(rows) == [0, 0, 1] and n_new == 2
+    rows, n_new = oracle.match_or_append_pairs([(0, 3)], [(0, 3)])
+    assert list(rows) == [0] and n_new == 0
+    t = oracle.ColumnarTree(4)
+    t.append_actions([0, 0, 0], [2, 2, 2], [1.0, 1.0, 4.0])
+    assert t.action_visits[0] == 3 and t.action_reward_sum[0] == 6.0
+    np.testing.assert_allclose(oracle.softmax_rows([[0.0, np.log(2.0)]], 1.0), [[1 / 3, 2 / 3]])
+    np.testing.assert_allclose(oracle.softmax_rows([[1.0] * 4], 2.0), [[0.25] * 4])
+    assert abs(oracle.log_sum_exp_rows([[3.0] * 4], 2.0)[0] - (3.0 + np.log(4) / 2)) < 1e-12
+    assert abs(oracle.log_sum_exp_rows([[1.0, 2.0]], 1.0)[0] - 2.31326) < 1e-5
+    lv = oracle.aggregate_leaves(oracle.LeafResult(np.array([7, 7]), np.array([4.0, 6.0])))
+    assert lv.values[0] == 5.0 and lv.visit_weights[0] == 2.0
+
+
+@pytest.mark.parametrize("name", sorted(manifest()["plans"]))
+def test_oracle_plan_matches_reference(name):
+    case = manifest()["plans"][name]
+    g = load(name)
+    for run in case["runs"]:
+        s = run["seed"]
+        model, belief, cfg, rng = plan_inputs(case, s)
+        out = oracle.plan(belief, model, cfg, rng)
+        assert out.chosen_action == run["chosen_action"]
+        assert out.tree_stats == run["tree_stats"]
+        assert out.final_d_max == run["final_d_max"]
+        cols = tree_columns(out.tree.tables())
+        for k in INT_COLUMNS:
+            np.testing.assert_array_equal(cols[k], g[f"s{s}_{k}"].astype(cols[k].dtype), err_msg=k)
+        np.testing.assert_array_equal(cols["action_reward_sum"], g[f"s{s}_action_reward_sum"])
+        np.testing.assert_array_equal(cols["prefs_root"], g[f"s{s}_prefs_root"])
+        np.testing.assert_allclose(cols["prefs_row_sum"], g[f"s{s}_prefs_row_sum"], rtol=0, atol=1e-12)
+        if f"s{s}_prefs" in g:
+            np.testing.assert_array_equal(cols["prefs"], g[f"s{s}_prefs"])
+        out.tree.validate()
+
+
+def test_oracle_episode_matches_reference():
+    recs = manifest()["episodes"]["episode_mars4_3"]
+    cfg = oracle.SolverConfig(n_parallel=64, iterations=4, particles=500)
+    for r in recs:
+        got = oracle.run_episode(oracle.MarsModel(n=4, m=3, layout_seed=r["seed"]), cfg, seed=r["seed"])
+        assert got.steps == r["steps"] and got.terminal_reason == r["reason"]
+        assert got.discounted_return == r["return"]
