@@ -1,0 +1,339 @@
+"""Benchmark of the PORPP planning step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): one planning
+step ``plan()`` on RockSample(11,11) = MarsModel(n=11, m=11), |A| = 256,
+n_parallel = 16 384 simulations per iteration, 10 iterations (d_max 1..10),
+eta = 2.0, a 10 000-particle belief.  A "step" is one whole planning step.
+
+* ``value``  -- simulations/s with the belief already resident in HBM: each
+  step is tree reset + 10 x (root draw, search, backup) + root argmax, timed
+  with CUDA events on the planner's stream; the per-step tree arena (~1 GB)
+  exceeds the 126 MB L2, so no explicit flush is needed.
+* ``e2e``    -- the same metric through the public ``plan()`` call with the
+  particle StateBatch on the host (pack + pinned H2D + D2H of the action).
+* ``roofline`` -- the dominant kernel's algorithmic bytes per launch over its
+  CUDA-event duration (profiled pass of the same steps) vs MEASURED_PEAKS.
+* ``cpu_baseline`` -- the CPU oracle (numpy port of the reference) timed on
+  this host, one core, on one planning step of the same workload.
+* ``--impl reference`` -- the reference algorithm on the host CPU (the oracle
+  port; /root/reference is not on the GPU box): one concurrent plan() per core.
+
+Multi-GPU (torchrun, N > 1): every rank plans its own replica of the
+workload (different seeds); the value is the sum over ranks, timed as the
+max over ranks ("replicas", scaling "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOAD = {"problem": "mars", "n": 11, "m": 11, "n_parallel": 16384, "iterations": 10, "eta": 2.0,
+            "particles": 10_000}
+METRIC = "belief-tree simulations/sec per planning step"
+UNIT = "simulations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-parallel", type=int, default=WORKLOAD["n_parallel"])
+    ap.add_argument("--iterations", type=int, default=WORKLOAD["iterations"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(args, world):
+    return {"workload": f"RockSample(11,11)=MarsModel(11,11) plan(), n_parallel={args.n_parallel}, "
+                        f"iterations={args.iterations}",
+            "problem": "MarsModel(n=11, m=11)", "actions": 256, "n_parallel": args.n_parallel,
+            "iterations": args.iterations, "eta": WORKLOAD["eta"], "particles": WORKLOAD["particles"],
+            "simulations_per_step": args.n_parallel * args.iterations,
+            "episode_steps_per_step": args.n_parallel * sum(range(1, args.iterations + 1)),
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "per-step tree arena (~1 GB) > 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- algorithmic bytes
+
+
+def level_counts(work, d_max):
+    """Per-level U_l (distinct beliefs), P_l (distinct actions) from the device lists."""
+    fc = work.fcount.cpu().numpy()[: d_max + 1].astype(np.int64)
+    pc = work.pcount.cpu().numpy()[:d_max].astype(np.int64)
+    return fc, pc
+
+
+def bytes_level_sample(n, A, S, fc, pc, psi_bytes=4):
+    """K1 per launch (level l): frontier slot + hash slot (4 + 32/distinct), state in/out
+    (2S), obs/reward/action/slot writes (20), PSI row + LSE + stamp per distinct belief,
+    one probed sector per distinct (b, a)."""
+    out = []
+    for lvl in range(len(pc)):
+        u, p = fc[lvl], pc[lvl]
+        out.append(n * (4 + 2 * S + 20) + u * (psi_bytes * A + 32 + 32 + 32) + 32 * p)
+    return out
+
+
+# ---------------------------------------------------------------- b200 arm
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_27191_b200 as vp
+    from paper_2510_27191_b200 import _lib
+    from paper_2510_27191_b200.rng import key_of
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seed = 1000 + rank
+    model = vp.MarsModel(n=WORKLOAD["n"], m=WORKLOAD["m"], layout_seed=seed)
+    belief = vp.ParticleBelief.from_model(model, WORKLOAD["particles"], vp.RowRng.from_seed(seed).derive(3))
+    cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=args.n_parallel, iterations=args.iterations)
+    planner = vp.Planner(args.precision)
+    dm = vp.device_model(model)
+    particles, cumw, m = planner.upload_belief(dm, belief)
+    rngs = [vp.RowRng.from_seed(seed).derive(1, t) for t in range(args.warmup + args.steps)]
+
+    def step(t):
+        d, tree, work = planner.prepare(model, cfg)
+        return planner.run(d, tree, work, particles, cumw, m, model.spec, cfg, key_of(rngs[t]))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for t in range(args.warmup):
+        step(t)
+    barrier()
+    clocks = ClockSampler(local)
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    outs = [step(args.warmup + t) for t in range(args.steps)]
+    ev1.record()
+    barrier()
+    launches = _lib.launch_count() - launches0
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    sims = args.n_parallel * args.iterations * args.steps * world
+    value = sims / (elapsed_ms / 1e3)
+
+    # e2e through the public API with host buffers
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(args.steps):
+        out = vp.plan(belief, model, cfg, rngs[args.warmup + t], precision=args.precision)
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e = sims / (e2e_ms / 1e3)
+    h2d = belief.states.x.shape[0] * dm.state_bytes + 8 * len(belief.weights)
+
+    # profiled pass of the same steps: per-kernel-kind device time and the dominant kernel
+    _lib.profile_enable(True)
+    prof_steps = min(args.steps, 3)
+    for t in range(prof_steps):
+        step(args.warmup + t)
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    kinds = {k: v for k, v in prof.items() if v[1]}
+    total_ms = sum(v[0] for v in kinds.values())
+    top = max(kinds, key=lambda k: kinds[k][0])
+    # algorithmic bytes of level_sample for one step, from the recorded per-level lists
+    d, tree, work = planner.prepare(model, cfg)
+    res = planner.run(d, tree, work, particles, cumw, m, model.spec, cfg, key_of(rngs[args.warmup]))
+    fc, pc = level_counts(work, args.iterations)
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    ls_ms, ls_n = kinds.get("level_sample", (0.0, 0))
+    roof = None
+    if ls_n:
+        # bytes of the last iteration's levels (the only ones whose lists survive) scaled per launch
+        per_launch = bytes_level_sample(args.n_parallel, 256, dm.state_bytes, fc, pc,
+                                        4 if args.precision == "fp32" else 8)
+        avg_bytes = float(np.mean(per_launch))
+        avg_ms = ls_ms / ls_n
+        ach = avg_bytes / (avg_ms / 1e3) / 1e9
+        roof = {"kernel": "k_level_sample", "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                "bytes_per_launch": avg_bytes, "avg_launch_us": round(avg_ms * 1e3, 2),
+                "share_of_step": round(ls_ms / total_ms, 3) if total_ms else None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+    kernel_table = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
+                    for k, v in kinds.items()}
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+            "data": "synthetic (MARS belief sampled from the model; no dataset)",
+            "config": workload_config(args, world),
+            "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
+                    "ms_per_step": round(e2e_ms / args.steps, 4)},
+            "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
+            "kernels": kernel_table, "dominant_kernel": top,
+            "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1),
+            "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- CPU (oracle port of the reference)
+
+
+def _cpu_plan(seed, n_parallel, iterations):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle
+
+    model = oracle.MarsModel(n=WORKLOAD["n"], m=WORKLOAD["m"], layout_seed=seed)
+    belief = oracle.ParticleBelief.from_model(model, WORKLOAD["particles"], oracle.RowRng.from_seed(seed).derive(3))
+    cfg = oracle.SolverConfig(eta=WORKLOAD["eta"], n_parallel=n_parallel, iterations=iterations)
+    t0 = time.perf_counter()
+    out = oracle.plan(belief, model, cfg, oracle.RowRng.from_seed(seed).derive(1, 0))
+    return time.perf_counter() - t0, out.tree_stats
+
+
+def cpu_baseline(args) -> dict:
+    """One core, whole planning steps of the same workload until the budget is used."""
+    times = []
+    t_start = time.perf_counter()
+    while not times or (time.perf_counter() - t_start < args.cpu_budget_s and len(times) < 3):
+        dt, _ = _cpu_plan(1000 + len(times), args.n_parallel, args.iterations)
+        times.append(dt)
+    sims = args.n_parallel * args.iterations
+    return {"value": round(sims * len(times) / sum(times), 1), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(times)} full planning step(s) of the same workload on 1 core "
+                      f"({sum(times):.1f} s; oracle/ numpy port of vecpomdp.plan)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    try:  # each process holds one reference tree (~1 GB at the default workload)
+        import psutil
+
+        cores = max(1, min(cores, int(psutil.virtual_memory().available // (2 << 30))))
+    except ImportError:
+        pass
+    # keep each step bounded: every core runs one whole planning step of the workload
+    ctx = mp.get_context("spawn")
+    os.environ["OMP_NUM_THREADS"] = "1"  # inherited by the spawned workers
+    with ctx.Pool(cores) as pool:
+        for w in range(args.warmup):
+            pool.starmap(_cpu_plan, [(2000 + w * cores + c, args.n_parallel, args.iterations) for c in range(cores)])
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            pool.starmap(_cpu_plan, [(3000 + s * cores + c, args.n_parallel, args.iterations) for c in range(cores)])
+        dt = time.perf_counter() - t0
+    sims = args.n_parallel * args.iterations * cores * args.steps
+    value = sims / dt
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, 1), "impl": "reference",
+            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"each step: {cores} concurrent full planning steps (one per core) of "
+                                       f"the workload, oracle/ numpy port of vecpomdp.plan"},
+            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

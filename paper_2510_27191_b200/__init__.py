@@ -1,0 +1,30 @@
+"""B200-native PORPP planning step (arXiv 2510.27191), drop-in for ``vecpomdp.plan``.
+
+The public names mirror the reference package (pkg/src/vecpomdp/__init__.py:
+10-48): ``plan``/``search``/``backup``/``SolverConfig``/``RowRng``/... with the
+tree, search and backup executed by hand-written sm_100a kernels behind the
+C ABI in include/vpb200.h (libvpb200.so, loaded through ``_lib``).  There is
+no CPU fallback: without the library or a CUDA device every compute entry
+point raises.
+"""
+
+from . import _lib
+from .backup import backup, log_sum_exp_rows
+from .belief import ParticleBelief, SirUpdate, sir_update, systematic_resample
+from .core import ProblemModel, ProblemSpec, StepResult
+from .envs import (LightDarkModel, MarsModel, SyntheticModel, TabularModel, TabularPOMDP, device_model,
+                   problem_from_config, tiger_model)
+from .rng import BoundRng, RowRng
+from .search import LeafResult, SearchBatch, sample_actions, search, softmax_rows
+from .solver import Planner, PlanOutcome, RunRecord, SolverConfig, get_planner, plan, run_episode
+from .tree import DeviceTree, init_tree
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BoundRng", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "ParticleBelief", "PlanOutcome",
+    "Planner", "ProblemModel", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
+    "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
+    "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",
+    "sir_update", "softmax_rows", "systematic_resample", "tiger_model",
+]

@@ -1,0 +1,197 @@
+"""ctypes binding of the C ABI in include/vpb200.h (libvpb200.so, sm_100a).
+
+This is the "reference-side FFI" of the drop-in: the reference planner is pure
+Python (/root/reference/pkg/src/vecpomdp), so the natural binding is ctypes.
+There is no fallback: if the library is missing or CUDA is unavailable every
+entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvpb200.so")
+
+VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
+VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
+VP_PSI_F32, VP_PSI_F64 = 0, 1
+VP_SCAN_TILE = 1024
+ABI_VERSION = 1
+
+p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
+    C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
+    C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
+
+
+class VpModel(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("action_count", C.c_int32), ("obs_arity", C.c_int32),
+        ("state_bytes", C.c_int32), ("discount", C.c_double),
+        ("mars_n", C.c_int32), ("mars_m", C.c_int32), ("mars_ops", C.c_int32), ("mars_pad", C.c_int32),
+        ("mars_half_eff", C.c_double), ("mars_rock_at", C.c_void_p),
+        ("mars_rock_x", C.c_int16 * 64), ("mars_rock_y", C.c_int16 * 64),
+        ("tab_states", C.c_int32), ("tab_obs", C.c_int32),
+        ("tab_cum_t", C.c_void_p), ("tab_cum_z", C.c_void_p), ("tab_reward", C.c_void_p),
+        ("tab_terminal", C.c_void_p),
+        ("syn_branching", C.c_int32), ("syn_term_per_mille", C.c_int32),
+        ("syn_obs_accuracy", C.c_double), ("syn_salt", C.c_uint64),
+        ("ld_step", C.c_double), ("ld_light_x", C.c_double), ("ld_goal_radius", C.c_double),
+        ("ld_sigma0", C.c_double), ("ld_sigma_slope", C.c_double), ("ld_bin_width", C.c_double),
+        ("ld_bins", C.c_int32), ("ld_pad", C.c_int32),
+    ]
+
+
+class VpTree(C.Structure):
+    _fields_ = [
+        ("cap_beliefs", C.c_int32), ("cap_actions", C.c_int32), ("action_count", C.c_int32),
+        ("psi_dtype", C.c_int32), ("exact", C.c_int32), ("pad0", C.c_int32),
+        ("hmask_a", C.c_uint64), ("hmask_b", C.c_uint64),
+        ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_depth", C.c_void_p),
+        ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p), ("b_weight", C.c_void_p),
+        ("b_stamp", C.c_void_p),
+        ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),
+        ("a_visits", C.c_void_p), ("a_num", C.c_void_p), ("a_den", C.c_void_p), ("a_stamp", C.c_void_p),
+        ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
+        ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("eta", C.c_double),
+    ]
+
+
+class VpWork(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("max_levels", C.c_int32), ("states", C.c_void_p),
+        ("slot_a", C.c_void_p), ("slot_b", C.c_void_p), ("obs", C.c_void_p), ("reward", C.c_void_p),
+        ("action", C.c_void_p), ("flist", C.c_void_p), ("fcount", C.c_void_p), ("plist", C.c_void_p),
+        ("pcount", C.c_void_p), ("level_base", C.c_void_p), ("scan_status", C.c_void_p),
+        ("scan_ticket", C.c_void_p), ("leaf_belief", C.c_void_p), ("leaf_value", C.c_void_p),
+        ("trace_action", C.c_void_p), ("trace_obs", C.c_void_p), ("trace_anode", C.c_void_p),
+        ("trace_belief", C.c_void_p),
+    ]
+
+
+class VpSearchArgs(C.Structure):
+    _fields_ = [
+        ("search_key", C.c_uint64), ("depth0", C.c_int32), ("d_max", C.c_int32),
+        ("stamp_base", C.c_uint32), ("iteration", C.c_int32),
+        ("inject_actions", C.c_void_p), ("start_beliefs", C.c_void_p),
+    ]
+
+
+# (name, restype, argtypes) -- exactly the exports of include/vpb200.h
+_SIGNATURES = [
+    ("vp_abi_version", C.c_int32, []),
+    ("vp_status_string", C.c_char_p, [C.c_int32]),
+    ("vp_last_cuda_error", C.c_int32, []),
+    ("vp_abi_layout", C.c_int32, [p_i32, C.c_int32]),
+    ("vp_profile_enable", C.c_int32, [C.c_int32]),
+    ("vp_profile_read", C.c_int32, [p_f64, C.POINTER(C.c_int64), C.c_int32]),
+    ("vp_launch_count", C.c_int64, []),
+    ("vp_tree_init", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
+    ("vp_tree_rehash", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
+    ("vp_tree_counts", C.c_int32, [C.POINTER(VpTree), p_i32, C.c_void_p]),
+    ("vp_draw_root_states", C.c_int32,
+     [C.POINTER(VpModel), C.POINTER(VpWork), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]),
+    ("vp_search", C.c_int32,
+     [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpSearchArgs), C.c_void_p]),
+    ("vp_backup", C.c_int32,
+     [C.POINTER(VpTree), C.POINTER(VpWork), C.c_int32, C.c_int32, C.c_double, C.c_uint32, C.c_void_p]),
+    ("vp_root_argmax", C.c_int32, [C.POINTER(VpTree), C.c_void_p, C.c_void_p]),
+    ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_rng_normal", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_model_step", C.c_int32,
+     [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+      C.c_void_p]),
+    ("vp_model_heuristic", C.c_int32, [C.POINTER(VpModel), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_lse_rows", C.c_int32,
+     [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
+    ("vp_sample_rows", C.c_int32,
+     [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_int32,
+      C.c_void_p, C.c_void_p]),
+]
+
+EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)
+
+KERNEL_KINDS = ("draw", "level_sample", "assign_actions", "accum_probe", "assign_beliefs", "leaf",
+                "backup_leaves", "backup_q", "backup_v", "parent_lists", "argmax", "tree_init", "rehash")
+
+
+def profile_enable(on: bool):
+    load().vp_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kind: (total_ms, launches)} for launches recorded since profile_enable(True)."""
+    k = len(KERNEL_KINDS)
+    ms = (C.c_double * k)()
+    cnt = (C.c_int64 * k)()
+    load().vp_profile_read(ms, cnt, k)
+    return {name: (ms[i], int(cnt[i])) for i, name in enumerate(KERNEL_KINDS)}
+
+
+def launch_count() -> int:
+    return int(load().vp_launch_count())
+
+
+class CapacityError(RuntimeError):
+    """Device arena or hash index too small (VP_ERR_CAPACITY)."""
+
+
+class LibraryMissing(ImportError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA context is created here)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryMissing(
+            f"{path} not found: build the sm_100a library first (`make` or "
+            "`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+    lib = C.CDLL(path)
+    for name, res, args in _SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.vp_abi_version() != ABI_VERSION:
+        raise LibraryMissing(f"ABI mismatch: library {lib.vp_abi_version()} vs binding {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def layout_mismatches() -> list:
+    """Compare the ctypes mirrors with the library's own sizeof/offsetof."""
+    lib = load()
+    m = lib.vp_abi_layout(None, 0)
+    buf = (C.c_int32 * m)()
+    lib.vp_abi_layout(buf, m)
+    mine = [C.sizeof(VpModel), C.sizeof(VpTree), C.sizeof(VpWork), C.sizeof(VpSearchArgs),
+            VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
+            VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16]
+    names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
+             "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
+             "vp_search_args.start_beliefs", "sizeof(Slot)"]
+    return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
+
+
+def check(status: int, what: str = ""):
+    """Map a vp_status to the reference's exception convention."""
+    if status == VP_OK:
+        return
+    msg = f"{what}: {load().vp_status_string(status).decode()}"
+    if status == VP_ERR_INVALID:
+        raise ValueError(msg)
+    if status == VP_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if status == VP_ERR_MODEL:
+        raise TypeError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args):
+    check(getattr(load(), name)(*args), name)

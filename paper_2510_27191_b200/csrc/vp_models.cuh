@@ -1,0 +1,245 @@
+// vp_models.cuh -- device generative models G(s, a) -> (s', o, r) and leaf
+// heuristics.  Each model replays its host definition operation for
+// operation so that integer outputs are bit-identical:
+//   MARS      /root/reference/pkg/src/vecpomdp/envs/mars.py:146-180, 223-243
+//   TABULAR   /root/reference/pkg/src/vecpomdp/envs/tabular.py:106-130
+//   SYNTHETIC oracle/envs.py SyntheticModel   (new; integer hash dynamics)
+//   LIGHTDARK oracle/envs.py LightDarkModel   (new; continuous observations)
+// The per-row model stream is `mkey` = level_rng.derive(1) (search.py:113-115)
+// and the logical row id is the global simulation index.
+#pragma once
+
+#include "vp_common.cuh"
+
+namespace vp {
+
+// ------------------------------------------------------------------ MARS
+// 16-byte packed record: agent columns/rows (x == n means departed), rock
+// quality bits (bit i set while rock i is good), terminal flag.
+struct __align__(16) MarsState {
+  uint8_t x0, y0, x1, y1;
+  uint32_t term;
+  u64 rocks;
+};
+
+struct MarsModel {
+  typedef MarsState State;
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
+                                              u32& obs, double& rew) {
+    const int n = M.mars_n, P = M.mars_ops;
+    const int op[2] = {a / P, a % P};
+    const State in = s;
+    const bool gone[2] = {in.x0 == n, in.x1 == n};
+    int x[2] = {in.x0, in.x1}, y[2] = {in.y0, in.y1};
+    u64 rocks = in.rocks;
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+    // moves N/E/S/W for both agents (mars.py:95-111, 154-155)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!gone[k] && op[k] < 4) {
+        const int dx = (op[k] == 1) - (op[k] == 3);
+        const int dy = (op[k] == 2) - (op[k] == 0);
+        const int tx = x[k] + dx, ty = y[k] + dy;
+        const bool departs = tx == n;
+        const bool inside = tx >= 0 && tx < n && ty >= 0 && ty < n;
+        if (departs || inside) {
+          x[k] = tx;
+          if (!departs) y[k] = ty;
+        }
+        if (departs) part[k] = 10.0;
+      }
+    }
+    // samples, agent 0 first (mars.py:113-127, 156-157)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!gone[k] && op[k] == 4) {
+        part[2 + k] = -10.0;
+        const int rk = M.mars_rock_at[x[k] * n + y[k]];
+        if (rk >= 0 && ((rocks >> rk) & 1ull)) {
+          part[2 + k] = 10.0;
+          rocks &= ~(1ull << rk);
+        }
+      }
+    }
+    // sensor readings from post-sample rocks (mars.py:129-144, 158-165)
+    int reading[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double u = uniform1(fold(mkey, (u64)k), row);
+      reading[k] = 2;  // NULL
+      if (!gone[k] && op[k] >= 5) {
+        const int rk = op[k] - 5;
+        const double ddx = (double)(x[k] - M.mars_rock_x[rk]);
+        const double ddy = (double)(y[k] - M.mars_rock_y[rk]);
+        const double d = sqrt(ddx * ddx + ddy * ddy);
+        const double acc = 0.5 * (1.0 + exp2(-d / M.mars_half_eff));
+        const bool correct = u < acc;
+        const bool truth = (rocks >> rk) & 1ull;
+        reading[k] = (truth == correct) ? 0 : 1;
+      }
+    }
+    obs = (u32)(reading[0] * 3 + reading[1]);
+    rew = (((0.0 + part[0]) + part[1]) + part[2]) + part[3];
+    const bool term = in.term || (x[0] == n && x[1] == n);
+    if (term) obs = (u32)M.obs_arity;
+    if (in.term) {
+      rew = 0.0;
+      return;  // absorbing: state unchanged (mars.py:174-179)
+    }
+    s.x0 = (uint8_t)x[0]; s.y0 = (uint8_t)y[0];
+    s.x1 = (uint8_t)x[1]; s.y1 = (uint8_t)y[1];
+    s.rocks = rocks;
+    s.term = term ? 1u : 0u;
+  }
+
+  static __device__ __forceinline__ double heuristic(const vp_model& M, const State& s) {
+    // mars.py:223-243
+    if (s.term) return 0.0;
+    const int n = M.mars_n;
+    const double g = M.discount;
+    const int xs[2] = {s.x0, s.x1}, ys[2] = {s.y0, s.y1};
+    const bool act[2] = {xs[0] < n, xs[1] < n};
+    double h = 0.0;
+    h += act[0] ? 10.0 * pow(g, (double)(n - xs[0] - 1)) : 0.0;
+    h += act[1] ? 10.0 * pow(g, (double)(n - xs[1] - 1)) : 0.0;
+    if (!(act[0] || act[1])) return h;
+    auto term_i = [&](int i) -> double {
+      int best = 0x3fffffff;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!act[k]) continue;
+        const int dd = abs(xs[k] - M.mars_rock_x[i]) + abs(ys[k] - M.mars_rock_y[i]);
+        best = dd < best ? dd : best;
+      }
+      const double good = ((s.rocks >> i) & 1ull) ? 10.0 : 0.0;
+      return good * pow(g, (double)best);
+    };
+    h += pairwise_sum(term_i, 0, M.mars_m);
+    return h;
+  }
+};
+
+// ------------------------------------------------------------------ TABULAR
+struct __align__(8) TabularState {
+  int32_t idx;
+  int32_t term;
+};
+
+struct TabularModel {
+  typedef TabularState State;
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
+                                              u32& obs, double& rew) {
+    const int S = M.tab_states, O = M.tab_obs;
+    const int cur = s.idx;
+    const double us = uniform1(fold(mkey, 0), row);
+    const double* ct = M.tab_cum_t + ((size_t)a * S + cur) * S;
+    int nxt = 0;
+    for (int j = 0; j < S; ++j) nxt += ct[j] < us;
+    nxt = nxt < S - 1 ? nxt : S - 1;
+    const double uo = uniform1(fold(mkey, 1), row);
+    const double* cz = M.tab_cum_z + ((size_t)a * S + nxt) * O;
+    int o = 0;
+    for (int j = 0; j < O; ++j) o += cz[j] < uo;
+    o = o < O - 1 ? o : O - 1;
+    rew = M.tab_reward[(size_t)cur * M.action_count + a];
+    const bool term = M.tab_terminal[nxt] || s.term;
+    obs = term ? (u32)M.obs_arity : (u32)o;
+    if (s.term) {
+      rew = 0.0;
+      return;
+    }
+    s.idx = nxt;
+    s.term = term ? 1 : 0;
+  }
+  static __device__ __forceinline__ double heuristic(const vp_model&, const State&) { return 0.0; }
+};
+
+// ------------------------------------------------------------------ SYNTHETIC
+struct __align__(16) SyntheticState {
+  u64 word;
+  uint32_t term;
+  uint32_t pad;
+};
+constexpr u64 kSynAct = 0xD1B54A32D192ED03ull;
+constexpr u64 kSynBranch = 0xABC98388FB8FAC03ull;
+constexpr u64 kSynReward = 0x8CB92BA72F3D8DD7ull;
+constexpr u64 kSynHeur = 0x9FB21C651E98DF25ull;
+
+struct SyntheticModel {
+  typedef SyntheticState State;
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
+                                              u32& obs, double& rew) {
+    const double ut = uniform1(fold(mkey, 0), row);
+    const double uo = uniform1(fold(mkey, 1), row);
+    const double un = uniform1(fold(mkey, 2), row);
+    const u64 w = s.word, ua = (u64)a;
+    const u64 branch = (u64)(int64_t)floor(ut * (double)M.syn_branching);
+    const u64 nxt = mix64(w + (ua + 1) * kSynAct + branch * kSynBranch + M.syn_salt);
+    rew = unit53(mix64(w ^ (ua * kSynReward + M.syn_salt))) * 2.0 - 1.0;
+    const int no = M.obs_arity;
+    const int true_obs = (int)((nxt >> 17) % (u64)no);
+    int noise = (int)floor(un * (double)no);
+    noise = noise < no - 1 ? noise : no - 1;
+    int o = uo < M.syn_obs_accuracy ? true_obs : noise;
+    const bool term = s.term || (int)((nxt >> 40) % 1000ull) < M.syn_term_per_mille;
+    obs = term ? (u32)no : (u32)o;
+    if (s.term) {
+      rew = 0.0;
+      return;
+    }
+    s.word = nxt;
+    s.term = term ? 1u : 0u;
+  }
+  static __device__ __forceinline__ double heuristic(const vp_model&, const State& s) {
+    if (s.term) return 0.0;
+    return 0.5 * unit53(mix64(s.word + kSynHeur));
+  }
+};
+
+// ------------------------------------------------------------------ LIGHT-DARK
+struct __align__(8) LightDarkState {
+  double x, y;
+  uint32_t term;
+  uint32_t pad;
+};
+
+struct LightDarkModel {
+  typedef LightDarkState State;
+  static __device__ __forceinline__ int bin(const vp_model& M, double v) {
+    double b = floor(v / M.ld_bin_width) + (double)(M.ld_bins / 2);
+    b = b < 0.0 ? 0.0 : b;
+    const double hi = (double)(M.ld_bins - 1);
+    b = b > hi ? hi : b;
+    return (int)b;
+  }
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
+                                              u32& obs, double& rew) {
+    // moves E, NE, N, NW, W, SW, S, SE, then DECLARE
+    const int dxs[9] = {1, 1, 0, -1, -1, -1, 0, 1, 0};
+    const int dys[9] = {0, 1, 1, 1, 0, -1, -1, -1, 0};
+    const double nx = s.x + (double)dxs[a] * M.ld_step;
+    const double ny = s.y + (double)dys[a] * M.ld_step;
+    const bool declare = a == 8;
+    const bool inside = s.x * s.x + s.y * s.y <= M.ld_goal_radius * M.ld_goal_radius;
+    rew = declare ? (inside ? 100.0 : -100.0) : -1.0;
+    const u64 nk = fold(mkey, 0);
+    const double z0 = normal_j(nk, row, 1), z1 = normal_j(nk, row, 2);
+    const double sigma = M.ld_sigma0 + M.ld_sigma_slope * fabs(nx - M.ld_light_x);
+    const int o = bin(M, nx + sigma * z0) * M.ld_bins + bin(M, ny + sigma * z1);
+    const bool term = s.term || declare;
+    obs = term ? (u32)M.obs_arity : (u32)o;
+    if (s.term) {
+      rew = 0.0;
+      return;
+    }
+    s.x = nx;
+    s.y = ny;
+    s.term = term ? 1u : 0u;
+  }
+  static __device__ __forceinline__ double heuristic(const vp_model&, const State& s) {
+    if (s.term) return 0.0;
+    return -(fabs(s.x) + fabs(s.y));
+  }
+};
+
+}  // namespace vp

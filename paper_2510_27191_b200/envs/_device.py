@@ -1,0 +1,247 @@
+"""Device descriptors (vp_model) and packed state records for problem models.
+
+A ``DeviceModel`` binds one ProblemModel instance to:
+* a ``VpModel`` ctypes struct (include/vpb200.h) with its constant tables
+  uploaded to HBM (kept alive here);
+* the packed per-row state record the kernels use (csrc/vp_models.cuh):
+
+    MARS       16 B  {u8 x0, y0, x1, y1; u32 terminal; u64 rock bits}
+    TABULAR     8 B  {i32 state index; i32 terminal}
+    SYNTHETIC  16 B  {u64 word; u32 terminal; u32 pad}
+    LIGHTDARK  24 B  {f64 x; f64 y; u32 terminal; u32 pad}
+
+Models are recognised either by a ``device_descriptor()`` method or, for
+objects of the reference package (vecpomdp.envs.MarsModel / TabularModel),
+by their public attributes, so the reference's own model objects plan on
+the device unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from .. import _lib
+from ..core import check_step_inputs, StepResult
+from ..rng import key_of
+
+MARS_DTYPE = np.dtype([("x0", "u1"), ("y0", "u1"), ("x1", "u1"), ("y1", "u1"), ("term", "<u4"), ("rocks", "<u8")])
+TAB_DTYPE = np.dtype([("idx", "<i4"), ("term", "<i4")])
+SYN_DTYPE = np.dtype([("word", "<u8"), ("term", "<u4"), ("pad", "<u4")])
+LD_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("term", "<u4"), ("pad", "<u4")])
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch
+
+
+class DeviceModel:
+    """Descriptor + packer for one model instance."""
+
+    def __init__(self, kind: int, spec, state_dtype: np.dtype, pack, unpack=None):
+        self.kind = kind
+        self.spec = spec
+        self.state_dtype = state_dtype
+        self._pack = pack
+        self._unpack = unpack
+        self.desc = _lib.VpModel()
+        self.desc.kind = kind
+        self.desc.action_count = spec.action_count
+        self.desc.obs_arity = spec.observation_arity
+        self.desc.state_bytes = state_dtype.itemsize
+        self.desc.discount = float(spec.discount)
+        self.tables = []  # device tensors referenced by desc
+
+    @property
+    def state_bytes(self) -> int:
+        return self.state_dtype.itemsize
+
+    def upload(self, arr: np.ndarray):
+        torch = _torch()
+        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+        self.tables.append(t)
+        return t.data_ptr()
+
+    def pack(self, states) -> np.ndarray:
+        return self._pack(states)
+
+    def unpack(self, records: np.ndarray):
+        if self._unpack is None:
+            raise TypeError("this model's states cannot be rebuilt from device records")
+        return self._unpack(records)
+
+    def states_to_device(self, states):
+        torch = _torch()
+        rec = self.pack(states)
+        return torch.from_numpy(rec.view(np.uint8).reshape(-1)).cuda()
+
+    # -- device-backed ProblemModel pieces (used by the product model classes)
+    def step(self, states, actions, rng):
+        """step_batch on the device via vp_model_step (test hook + env step)."""
+        torch = _torch()
+        check_step_inputs(self.spec, states, actions)
+        n = len(states)
+        if n == 0:
+            return StepResult(states, np.zeros(0, dtype=np.int64), np.zeros(0))
+        st = self.states_to_device(states)
+        acts = torch.as_tensor(np.asarray(actions, dtype=np.int32)).cuda()
+        rows = torch.as_tensor(np.asarray(rng.rows, dtype=np.int64)).cuda()
+        obs = torch.empty(n, dtype=torch.int32, device="cuda")
+        rew = torch.empty(n, dtype=torch.float64, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        _lib.call("vp_model_step", C.byref(self.desc), st.data_ptr(), acts.data_ptr(), key_of(rng.rng),
+                  rows.data_ptr(), n, obs.data_ptr(), rew.data_ptr(), stream)
+        rec = st.cpu().numpy().view(self.state_dtype)
+        o = obs.cpu().numpy().view(np.uint32).astype(np.int64)
+        return StepResult(self.unpack(rec), o, rew.cpu().numpy())
+
+    def heuristic(self, states) -> np.ndarray:
+        torch = _torch()
+        n = len(states)
+        if n == 0:
+            return np.zeros(0)
+        st = self.states_to_device(states)
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("vp_model_heuristic", C.byref(self.desc), st.data_ptr(), n, out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        return out.cpu().numpy()
+
+
+# ------------------------------------------------------------------ MARS
+
+
+def _rock_bits(rocks: np.ndarray) -> np.ndarray:
+    r = np.asarray(rocks, dtype=bool)
+    if r.shape[1] > 64:
+        raise ValueError("MARS device records hold at most 64 rocks")
+    shifts = np.arange(r.shape[1], dtype=np.uint64)
+    return np.bitwise_or.reduce(r.astype(np.uint64) << shifts[None, :], axis=1) if r.shape[1] else \
+        np.zeros(len(r), dtype=np.uint64)
+
+
+def mars_pack(states) -> np.ndarray:
+    x = np.asarray(states.x)
+    y = np.asarray(states.y)
+    rec = np.zeros(len(x), dtype=MARS_DTYPE)
+    rec["x0"], rec["y0"], rec["x1"], rec["y1"] = x[:, 0], y[:, 0], x[:, 1], y[:, 1]
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    rec["rocks"] = _rock_bits(states.rocks)
+    return rec
+
+
+def mars_descriptor(model, unpack=None) -> DeviceModel:
+    """vp_model for a MarsModel (reference envs/mars.py:44-80 attributes)."""
+    n, m = int(model.n), int(model.m)
+    if n > 254 or m > 64:
+        raise ValueError("MARS device model supports n <= 254 and m <= 64")
+    dm = DeviceModel(_lib.VP_MODEL_MARS, model.spec, MARS_DTYPE, mars_pack, unpack)
+    d = dm.desc
+    d.mars_n, d.mars_m, d.mars_ops = n, m, int(model.per_agent_ops)
+    d.mars_half_eff = float(model.half_efficiency_distance)
+    rock_at = np.asarray(model.rock_at, dtype=np.int64).astype(np.int8).reshape(-1)  # [x, y] -> x*n + y
+    d.mars_rock_at = dm.upload(rock_at)
+    for i in range(m):
+        d.mars_rock_x[i] = int(model.rock_x[i])
+        d.mars_rock_y[i] = int(model.rock_y[i])
+    return dm
+
+
+# ------------------------------------------------------------------ TABULAR
+
+
+def tab_pack(states) -> np.ndarray:
+    rec = np.zeros(len(states.idx), dtype=TAB_DTYPE)
+    rec["idx"] = np.asarray(states.idx)
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    return rec
+
+
+def tabular_descriptor(model, unpack=None) -> DeviceModel:
+    """vp_model for a TabularModel (reference envs/tabular.py:79-92)."""
+    p = model.pomdp
+    t = np.asarray(p.transitions, dtype=np.float64)
+    z = np.asarray(p.observations, dtype=np.float64)
+    dm = DeviceModel(_lib.VP_MODEL_TABULAR, model.spec, TAB_DTYPE, tab_pack, unpack)
+    d = dm.desc
+    d.tab_states = t.shape[1]
+    d.tab_obs = z.shape[2]
+    d.tab_cum_t = dm.upload(np.cumsum(t, axis=2).reshape(-1))
+    d.tab_cum_z = dm.upload(np.cumsum(z, axis=2).reshape(-1))
+    d.tab_reward = dm.upload(np.asarray(p.rewards, dtype=np.float64).reshape(-1))
+    d.tab_terminal = dm.upload(np.asarray(p.terminal_states, dtype=np.uint8))
+    return dm
+
+
+# ------------------------------------------------------------------ SYNTHETIC
+
+
+def syn_pack(states) -> np.ndarray:
+    rec = np.zeros(len(states.word), dtype=SYN_DTYPE)
+    rec["word"] = np.asarray(states.word, dtype=np.uint64)
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    return rec
+
+
+def synthetic_descriptor(model, unpack=None) -> DeviceModel:
+    dm = DeviceModel(_lib.VP_MODEL_SYNTHETIC, model.spec, SYN_DTYPE, syn_pack, unpack)
+    d = dm.desc
+    d.syn_branching = int(model.branching)
+    d.syn_term_per_mille = int(model.term_per_mille)
+    d.syn_obs_accuracy = float(model.obs_accuracy)
+    d.syn_salt = int(model.salt) & ((1 << 64) - 1)
+    return dm
+
+
+# ------------------------------------------------------------------ LIGHTDARK
+
+
+def ld_pack(states) -> np.ndarray:
+    rec = np.zeros(len(states.x), dtype=LD_DTYPE)
+    rec["x"] = np.asarray(states.x, dtype=np.float64)
+    rec["y"] = np.asarray(states.y, dtype=np.float64)
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    return rec
+
+
+def lightdark_descriptor(model, unpack=None) -> DeviceModel:
+    dm = DeviceModel(_lib.VP_MODEL_LIGHTDARK, model.spec, LD_DTYPE, ld_pack, unpack)
+    d = dm.desc
+    d.ld_step, d.ld_light_x, d.ld_goal_radius = float(model.step), float(model.light_x), float(model.goal_radius)
+    d.ld_sigma0, d.ld_sigma_slope = float(model.sigma0), float(model.sigma_slope)
+    d.ld_bin_width, d.ld_bins = float(model.bin_width), int(model.bins)
+    return dm
+
+
+_BY_NAME = {
+    "MarsModel": mars_descriptor,
+    "TabularModel": tabular_descriptor,
+    "SyntheticModel": synthetic_descriptor,
+    "LightDarkModel": lightdark_descriptor,
+}
+_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_model(model) -> DeviceModel:
+    """The (cached) DeviceModel of any supported ProblemModel instance."""
+    try:
+        return _CACHE[model]
+    except (KeyError, TypeError):
+        pass
+    if hasattr(model, "device_descriptor"):
+        dm = model.device_descriptor()
+    else:
+        build = _BY_NAME.get(type(model).__name__)
+        if build is None:
+            raise TypeError(f"no device model for {type(model).__name__}; supported: {sorted(_BY_NAME)}")
+        dm = build(model)
+    try:
+        _CACHE[model] = dm
+    except TypeError:
+        pass
+    return dm

@@ -1,0 +1,288 @@
+"""The planning step on the B200: ``plan(belief, model, config, rng) -> PlanOutcome``.
+
+Drop-in for /root/reference/pkg/src/vecpomdp/solver.py:79-113 (same
+arguments, same SolverConfig validation and budget semantics, same
+PlanOutcome).  Per iteration the host only derives three 64-bit keys
+(Appendix A of SURVEY.md) and issues three C-ABI calls; everything else --
+root-state draw, D search levels, leaf aggregation, D backup levels -- is
+queued on the current CUDA stream without synchronisation.  The host syncs
+once at the end (root argmax, 4 bytes) or once per iteration in wall-time
+budget mode (the reference checks perf_counter after every iteration).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .backup import run_backup
+from .belief import ParticleBelief, sir_update
+from .envs._device import device_model
+from .rng import RowRng, fold, key_of
+from .search import Workspace, run_search
+from .tree import DeviceTree, TreeHandle
+
+NS_ENV, NS_PLAN, NS_SIR, NS_INIT_BELIEF = 0, 1, 2, 3
+SITE_DRAW, SITE_SEARCH = 0, 1
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Planner parameters (solver.py:33-60); exactly one budget must be set."""
+
+    eta: float = 2.0
+    n_parallel: int = 1024
+    planning_seconds: float | None = None
+    iterations: int | None = None
+    d_max_cap: int = 90
+    seed: int = 0
+    particles: int = 10_000
+    max_sir_retries: int = 3
+
+    def __post_init__(self):
+        if self.eta <= 0:
+            raise ValueError("eta must be positive")
+        if self.n_parallel < 1:
+            raise ValueError("n_parallel must be >= 1")
+        if self.d_max_cap < 1:
+            raise ValueError("d_max_cap must be >= 1")
+        if (self.planning_seconds is None) == (self.iterations is None):
+            raise ValueError("set exactly one of planning_seconds / iterations")
+        if self.planning_seconds is not None and self.planning_seconds <= 0:
+            raise ValueError("planning_seconds must be positive")
+        if self.iterations is not None and self.iterations < 1:
+            raise ValueError("iterations must be >= 1")
+        if self.particles < 1:
+            raise ValueError("particles must be >= 1")
+
+
+@dataclass
+class PlanOutcome:
+    chosen_action: int
+    iterations_run: int
+    final_d_max: int
+    tree_stats: dict
+    tree: object = field(repr=False, default=None)
+    traces: list | None = field(repr=False, default=None)
+
+
+def initial_prefs(model, eta: float):
+    """Zero rows for a uniform reference, else log(pi0)/eta (solver.py:72-76)."""
+    ref = np.asarray(model.reference_log_probs(), dtype=np.float64)
+    if np.allclose(ref, ref[0]):
+        return None
+    return ref / eta
+
+
+def _validate_config(config):
+    # accept the reference's SolverConfig (or any duck-typed one) and re-check it
+    SolverConfig(config.eta, config.n_parallel, config.planning_seconds, config.iterations, config.d_max_cap,
+                 getattr(config, "seed", 0), getattr(config, "particles", 1), getattr(config, "max_sir_retries", 3))
+
+
+class Planner:
+    """Reusable device storage for repeated planning steps (one per stream).
+
+    The reference rebuilds its tree every step (solver.py:91, SPEC tree
+    freshness); so does this planner -- but into storage kept from the last
+    step, so a closed-loop episode allocates once.
+    """
+
+    def __init__(self, precision: str = "fp32", exact: bool = False, mem_fraction: float = 0.6):
+        self.precision, self.exact, self.mem_fraction = precision, exact, mem_fraction
+        self.tree: DeviceTree | None = None
+        self.work: Workspace | None = None
+        self._cap_cache = {}
+        self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
+
+    def _capacity(self, n: int, config, A: int):
+        """Worst-case node counts for the whole plan, bounded by a memory budget."""
+        torch = _torch()
+        cap_levels = config.d_max_cap
+        if config.iterations is not None:
+            total = sum(min(i + 1, cap_levels) for i in range(config.iterations))
+            levels = min(config.iterations, cap_levels)
+        else:
+            total = sum(min(i + 1, cap_levels) for i in range(16))
+            levels = cap_levels
+        need = 1 + n * total
+        elem = 4 if self.precision == "fp32" else 8
+        per_belief = A * elem + 8 * 3 + 4 * 4 + 64  # PSI row + columns + hash slots
+        free, _ = torch.cuda.mem_get_info()
+        budget = int(free * self.mem_fraction) // (per_belief + 48 + 64)
+        return min(need, max(budget, 1 + n * levels)), levels
+
+    def prepare(self, model, config, trace: bool = False):
+        dm = device_model(model)
+        A = model.spec.action_count
+        n = config.n_parallel
+        ck = (n, config.iterations, config.d_max_cap, A)
+        if ck not in self._cap_cache:
+            self._cap_cache[ck] = self._capacity(n, config, A)
+        cap, levels = self._cap_cache[ck]
+        init = initial_prefs(model, config.eta)
+        t = self.tree
+        if t is None or t.action_count != A or t.precision != self.precision or t.exact != self.exact:
+            t = self.tree = DeviceTree(A, init, eta=config.eta, precision=self.precision, exact=self.exact,
+                                       cap_beliefs=cap, cap_actions=cap)
+        else:
+            if t.cap_beliefs < cap:
+                t = self.tree = DeviceTree(A, init, eta=config.eta, precision=self.precision, exact=self.exact,
+                                           cap_beliefs=cap, cap_actions=cap)
+            else:
+                t.reset(init, config.eta)
+        w = self.work
+        if w is None or not w.fits(n, levels, dm.state_bytes, trace):
+            w = self.work = Workspace(n, levels, dm.state_bytes, trace)
+        return dm, t, w
+
+    def upload_belief(self, dm, belief):
+        """Pack the particle StateBatch and copy it (and the weight CDF) to HBM."""
+        torch = _torch()
+        weights = np.asarray(belief.weights, dtype=np.float64)
+        rec = dm.pack(belief.states)
+        particles = torch.from_numpy(rec.view(np.uint8).reshape(-1)).pin_memory().cuda(non_blocking=True)
+        # sequential fp64 cumsum exactly as belief.py:42
+        cumw = torch.from_numpy(np.cumsum(weights)).pin_memory().cuda(non_blocking=True)
+        return particles, cumw, len(weights)
+
+    def plan(self, belief, model, config, rng, *, keep_tree: bool = False, inject_actions=None,
+             trace: bool = False) -> PlanOutcome:
+        _validate_config(config)
+        dm, tree, work = self.prepare(model, config, trace)
+        particles, cumw, m = self.upload_belief(dm, belief)
+        return self.run(dm, tree, work, particles, cumw, m, model.spec, config, key_of(rng),
+                        keep_tree=keep_tree, inject_actions=inject_actions, trace=trace)
+
+    def run(self, dm, tree, work, particles, cumw, m: int, spec, config, key: int, *, keep_tree: bool = False,
+            inject_actions=None, trace: bool = False) -> PlanOutcome:
+        """Iterations of one planning step from HBM-resident particles."""
+        torch = _torch()
+        n = config.n_parallel
+        stream = torch.cuda.current_stream().cuda_stream
+        ub_b, ub_a = 1, 0
+        d_max, done, last = 1, 0, 0
+        traces = [] if trace else None
+        t0 = time.perf_counter()
+        while True:
+            it_key = fold(key, done)
+            if ub_b + n * d_max > tree.cap_beliefs or ub_a + n * d_max > tree.cap_actions:
+                nb, na, _ = tree.counts()
+                ub_b, ub_a = nb, na
+                tree.ensure_capacity(nb + n * d_max, na + n * d_max)
+            _lib.call("vp_draw_root_states", C.byref(dm.desc), C.byref(work.struct), particles.data_ptr(),
+                      cumw.data_ptr(), m, fold(it_key, SITE_DRAW), stream)
+            inject = None
+            if inject_actions is not None:
+                arr = np.asarray(inject_actions[done], dtype=np.int32).reshape(d_max, n)
+                inject = torch.from_numpy(arr.reshape(-1)).cuda()
+            stamp = tree.next_stamp_base(work.max_levels)
+            run_search(tree, dm, work, fold(it_key, SITE_SEARCH), 0, d_max, stamp, done, inject)
+            run_backup(tree, work, 0, d_max, spec.discount, stamp)
+            if trace:
+                traces.append({"levels": work.traces(0, d_max),
+                               "leaf_beliefs": work.leaf_belief.cpu().numpy().astype(np.int64),
+                               "heuristic_values": work.leaf_value.cpu().numpy().copy()})
+            ub_b += n * d_max
+            ub_a += n * d_max
+            done += 1
+            last = d_max
+            if config.iterations is not None:
+                if done >= config.iterations:
+                    break
+            else:
+                torch.cuda.current_stream().synchronize()
+                if time.perf_counter() - t0 >= config.planning_seconds:
+                    break
+            d_max = min(d_max + 1, config.d_max_cap)
+        _lib.call("vp_root_argmax", C.byref(tree.struct), self._out.data_ptr(), stream)
+        _lib.call("vp_tree_counts", C.byref(tree.struct), tree._host_counts, stream)  # syncs once
+        chosen = int(self._out.item())
+        nb, na, overflow = (int(v) for v in tree._host_counts)
+        if overflow:
+            raise _lib.CapacityError("device tree overflowed its arena during plan()")
+        held = tree if keep_tree else TreeHandle(tree)
+        if keep_tree:
+            self.tree = None  # hand the storage to the caller
+        return PlanOutcome(chosen, done, last, {"belief_rows": nb, "action_rows": na}, held, traces)
+
+
+_PLANNERS: dict = {}
+
+
+def get_planner(precision: str = "fp32", exact: bool = False) -> Planner:
+    torch = _torch()
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, precision, bool(exact))
+    p = _PLANNERS.get(key)
+    if p is None:
+        p = _PLANNERS[key] = Planner(precision, exact)
+    return p
+
+
+def plan(belief, model, config, rng, *, precision: str = "fp32", exact: bool = False, keep_tree: bool = False,
+         inject_actions=None, trace: bool = False) -> PlanOutcome:
+    """One planning step on the device (solver.py:79-113).
+
+    ``precision`` selects the PSI storage/compute type: "fp32" (default,
+    the fast path) or "fp64"; ``exact=True`` (fp64 only) additionally follows
+    numpy's operation order in softmax / LSE so whole-plan trees reproduce the
+    reference bit for bit in every integer field.
+    """
+    return get_planner(precision, exact).plan(belief, model, config, rng, keep_tree=keep_tree,
+                                              inject_actions=inject_actions, trace=trace)
+
+
+@dataclass
+class RunRecord:
+    run_index: int
+    seed: int
+    discounted_return: float
+    steps: int
+    terminal_reason: str
+    plan_wall_times: list
+    counters: dict
+    degenerate_updates: int
+
+
+def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str = "fp32",
+                exact: bool = False) -> RunRecord:
+    """Plan / execute / filter loop (solver.py:130-194) around the device plan."""
+    spec = model.spec
+    root = RowRng.from_seed(seed)
+    env_rng = root.derive(NS_ENV)
+    env_state = model.sample_initial_states(1, env_rng.derive(0))
+    belief = ParticleBelief.from_model(model, config.particles, root.derive(NS_INIT_BELIEF))
+    belief = ParticleBelief(model.reconcile_belief(belief.states, env_state), belief.weights)
+    total, counters, times, degenerate, t, reason = 0.0, {}, [], 0, 0, "truncated"
+    while t < spec.max_steps:
+        t0 = time.perf_counter()
+        outcome = plan(belief, model, config, root.derive(NS_PLAN, t), precision=precision, exact=exact)
+        times.append(time.perf_counter() - t0)
+        a = outcome.chosen_action
+        res = model.step_batch(env_state, np.array([a], dtype=np.int64), env_rng.derive(1 + t).bind([0]))
+        total += spec.discount ** t * float(res.rewards[0])
+        for k, v in model.step_metrics(env_state, a, res).items():
+            counters[k] = counters.get(k, 0.0) + float(v)
+        env_state = res.next_states
+        t += 1
+        if bool(env_state.terminal[0]):
+            reason = "terminal"
+            break
+        upd = sir_update(belief, model, a, int(res.observations[0]), root.derive(NS_SIR, t),
+                         max_retries=config.max_sir_retries)
+        degenerate += int(upd.degenerate)
+        env_state = model.refresh_executed(env_state)
+        belief = ParticleBelief(model.reconcile_belief(upd.belief.states, env_state), upd.belief.weights)
+    return RunRecord(run_index, seed, total, t, reason, times, counters, degenerate)

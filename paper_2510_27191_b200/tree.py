@@ -1,0 +1,271 @@
+"""Structure-of-arrays belief tree resident in HBM (device mirror of
+/root/reference/pkg/src/vecpomdp/tree.py:100-378).
+
+Layout (all device tensors, row-indexed):
+
+    B   b_parent_action i32 | b_parent_obs u32 | b_depth i32
+    PSI psi [cap_beliefs, |A|] fp32 (fast) or fp64 (parity), row-major
+        b_lse f64 (cached LSE of the row) | b_value, b_weight f64 (backup scratch)
+    A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32
+        a_num, a_den f64 (backup scratch)
+    two open-addressing hash indexes of 16-byte slots, load factor <= 1/2:
+        (belief << 32 | action) -> action row, (action row << 32 | obs) -> belief row
+
+Row 0 is the root (parent fields -1).  New rows are numbered in
+first-occurrence order of each batch (tree.py:10-12) by the device scans.
+Host-facing accessors download on demand and mirror the reference
+properties and ``serialize()`` text format (tree.py:298-320).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .core import ROOT_SENTINEL
+
+PRECISIONS = {"fp32": _lib.VP_PSI_F32, "fp64": _lib.VP_PSI_F64}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch
+
+
+def _pow2_at_least(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def _stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+class DeviceTree:
+    """B / A / PSI tables of one planning step on the current CUDA device."""
+
+    def __init__(self, action_count: int, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32",
+                 exact: bool = False, cap_beliefs: int = 4096, cap_actions: int = 4096):
+        if action_count < 1:
+            raise ValueError("action_count must be >= 1")
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+        if exact and precision != "fp64":
+            raise ValueError("exact (numpy-order) mode requires precision='fp64'")
+        torch = _torch()
+        self.action_count = action_count
+        self.precision = precision
+        self.exact = bool(exact)
+        self.eta = float(eta)
+        self.generation = 0
+        self._stamp_cursor = 0
+        self.last_search = None
+        self._psi_dtype = torch.float32 if precision == "fp32" else torch.float64
+        self._counters = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self._init_lse = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self._init_prefs = torch.zeros(action_count, dtype=torch.float64, device="cuda")
+        self._host_counts = (C.c_int32 * 3)()
+        self.cap_beliefs = 0
+        self.cap_actions = 0
+        self._allocate(max(16, cap_beliefs), max(16, cap_actions))
+        self.reset(init_prefs, eta)
+
+    # ------------------------------------------------------------------ storage
+    def _allocate(self, cap_b: int, cap_a: int, keep_b: int = 0, keep_a: int = 0):
+        torch = _torch()
+        dev = "cuda"
+        A = self.action_count
+
+        def col(old, shape, dtype, keep):
+            new = torch.empty(shape, dtype=dtype, device=dev)
+            if old is not None and keep:
+                new[:keep] = old[:keep]
+            return new
+
+        g = lambda name: getattr(self, name, None)  # noqa: E731
+        self.b_parent_action = col(g("b_parent_action"), cap_b, torch.int32, keep_b)
+        self.b_parent_obs = col(g("b_parent_obs"), cap_b, torch.int32, keep_b)
+        self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
+        self.psi = col(g("psi"), (cap_b, A), self._psi_dtype, keep_b)
+        self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
+        self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b)
+        self.b_weight = col(g("b_weight"), cap_b, torch.float64, keep_b)
+        self.b_stamp = col(g("b_stamp"), cap_b, torch.int32, keep_b)
+        self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
+        self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
+        self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a)
+        self.a_visits = col(g("a_visits"), cap_a, torch.int32, keep_a)
+        self.a_num = col(g("a_num"), cap_a, torch.float64, keep_a)
+        self.a_den = col(g("a_den"), cap_a, torch.float64, keep_a)
+        self.a_stamp = col(g("a_stamp"), cap_a, torch.int32, keep_a)
+        ha = _pow2_at_least(2 * cap_a)
+        hb = _pow2_at_least(2 * cap_b)
+        self.hash_a = torch.empty((ha, 2), dtype=torch.int64, device=dev)
+        self.hash_b = torch.empty((hb, 2), dtype=torch.int64, device=dev)
+        self.cap_beliefs, self.cap_actions = cap_b, cap_a
+        s = _lib.VpTree()
+        s.cap_beliefs, s.cap_actions, s.action_count = cap_b, cap_a, A
+        s.psi_dtype = PRECISIONS[self.precision]
+        s.exact = int(self.exact)
+        s.hmask_a, s.hmask_b = ha - 1, hb - 1
+        for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_weight",
+                     "b_stamp", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_num", "a_den",
+                     "a_stamp", "hash_a", "hash_b"):
+            setattr(s, name, getattr(self, name).data_ptr())
+        s.counters = self._counters.data_ptr()
+        s.init_prefs = self._init_prefs.data_ptr()
+        s.init_lse = self._init_lse.data_ptr()
+        s.eta = self.eta
+        self.struct = s
+
+    def set_eta(self, eta: float):
+        if eta <= 0:
+            raise ValueError("eta must be positive")
+        self.eta = float(eta)
+        self.struct.eta = self.eta
+
+    def reset(self, init_prefs=None, eta: float | None = None):
+        """Fresh tree (tree.py:103-132): root row, no actions, init PSI row."""
+        torch = _torch()
+        if eta is not None:
+            self.set_eta(eta)
+        A = self.action_count
+        base = np.zeros(A) if init_prefs is None else np.asarray(init_prefs, dtype=np.float64)
+        if base.shape != (A,) or not np.all(np.isfinite(base)):
+            raise ValueError("init_prefs must be a finite vector of length |A|")
+        self.init_prefs = base
+        self._init_prefs.copy_(torch.from_numpy(base))
+        self.generation += 1
+        self._stamp_cursor = 0
+        self.last_search = None
+        _lib.call("vp_tree_init", C.byref(self.struct), _stream())
+
+    def counts(self):
+        """(n_beliefs, n_actions, overflow) -- synchronises the stream."""
+        _lib.call("vp_tree_counts", C.byref(self.struct), self._host_counts, _stream())
+        return int(self._host_counts[0]), int(self._host_counts[1]), int(self._host_counts[2])
+
+    def ensure_capacity(self, need_beliefs: int, need_actions: int):
+        """Grow (geometric, tree.py:90-97) so the next search cannot overflow."""
+        if need_beliefs <= self.cap_beliefs and need_actions <= self.cap_actions:
+            return False
+        nb, na, _ = self.counts()
+        cap_b = max(self.cap_beliefs, 16)
+        while cap_b < need_beliefs:
+            cap_b *= 2
+        cap_a = max(self.cap_actions, 16)
+        while cap_a < need_actions:
+            cap_a *= 2
+        self._allocate(cap_b, cap_a, keep_b=nb, keep_a=na)
+        _lib.call("vp_tree_rehash", C.byref(self.struct), _stream())
+        return True
+
+    def next_stamp_base(self, levels: int) -> int:
+        base = self._stamp_cursor
+        self._stamp_cursor += levels + 3
+        return base
+
+    # ------------------------------------------------------------------ reference-style accessors
+    @property
+    def n_beliefs(self) -> int:
+        return self.counts()[0]
+
+    @property
+    def n_actions(self) -> int:
+        return self.counts()[1]
+
+    def tables(self) -> dict:
+        """All columns as host numpy arrays (int64 / float64 like the reference)."""
+        nb, na, _ = self.counts()
+        obs = self.b_parent_obs[:nb].cpu().numpy().view(np.uint32).astype(np.int64)
+        if nb:
+            obs[0] = ROOT_SENTINEL
+        return {
+            "parent_action": self.b_parent_action[:nb].cpu().numpy().astype(np.int64),
+            "parent_obs": obs,
+            "depth": self.b_depth[:nb].cpu().numpy().astype(np.int64),
+            "prefs": self.psi[:nb].cpu().numpy().astype(np.float64),
+            "action_parent_belief": self.a_parent_belief[:na].cpu().numpy().astype(np.int64),
+            "action_id": self.a_action[:na].cpu().numpy().astype(np.int64),
+            "action_reward_sum": self.a_reward[:na].cpu().numpy().copy(),
+            "action_visits": self.a_visits[:na].cpu().numpy().astype(np.int64),
+        }
+
+    parent_action = property(lambda s: s.tables()["parent_action"])
+    parent_obs = property(lambda s: s.tables()["parent_obs"])
+    depth = property(lambda s: s.tables()["depth"])
+    prefs = property(lambda s: s.tables()["prefs"])
+    action_parent_belief = property(lambda s: s.tables()["action_parent_belief"])
+    action_id = property(lambda s: s.tables()["action_id"])
+    action_reward_sum = property(lambda s: s.tables()["action_reward_sum"])
+    action_visits = property(lambda s: s.tables()["action_visits"])
+
+    def root_prefs(self) -> np.ndarray:
+        return self.psi[0].cpu().numpy().astype(np.float64)
+
+    def stats(self) -> dict:
+        nb, na, _ = self.counts()
+        return {"belief_rows": nb, "action_rows": na}
+
+    def validate(self):
+        """Full-table invariants (tree.py:269-291) on the downloaded tables."""
+        t = self.tables()
+        nb, na = len(t["depth"]), len(t["action_id"])
+        assert nb >= 1 and t["parent_action"][0] == ROOT_SENTINEL
+        assert t["parent_obs"][0] == ROOT_SENTINEL and t["depth"][0] == 0
+        if nb > 1:
+            pa = t["parent_action"][1:]
+            assert pa.min() >= 0 and pa.max() < na
+            keys = (pa << 32) | t["parent_obs"][1:]
+            assert len(np.unique(keys)) == nb - 1, "duplicate belief edge"
+            assert np.all(t["depth"][1:] == t["depth"][t["action_parent_belief"][pa]] + 1)
+        if na:
+            pb = t["action_parent_belief"]
+            assert pb.min() >= 0 and pb.max() < nb
+            assert len(np.unique((pb << 32) | t["action_id"])) == na, "duplicate action edge"
+            assert t["action_visits"].min() >= 1
+            assert np.all(np.isfinite(t["action_reward_sum"]))
+        assert np.all(np.isfinite(t["prefs"]))
+
+    def serialize(self) -> str:
+        """Text dump in the reference format (tree.py:298-320)."""
+        t = self.tables()
+        out = ["B\t%d\t%d\t%d\t%d" % (i, t["parent_action"][i], t["parent_obs"][i], t["depth"][i])
+               for i in range(len(t["depth"]))]
+        out += ["A\t%d\t%d\t%d\t%r\t%d" % (i, t["action_parent_belief"][i], t["action_id"][i],
+                                          float(t["action_reward_sum"][i]), t["action_visits"][i])
+                for i in range(len(t["action_id"]))]
+        out += ["P\t%d\t%d\t%s" % (i, i, "\t".join(repr(float(v)) for v in t["prefs"][i]))
+                for i in range(len(t["depth"]))]
+        return "\n".join(out) + "\n"
+
+
+class TreeHandle:
+    """What ``PlanOutcome.tree`` holds when the planner reuses pooled storage:
+    valid until the pool's next ``plan()`` resets the tree (then it raises
+    instead of silently showing the next step's tree)."""
+
+    def __init__(self, tree: DeviceTree):
+        self._tree = tree
+        self._generation = tree.generation
+
+    def __getattr__(self, name):
+        tree = self.__dict__["_tree"]
+        if tree.generation != self.__dict__["_generation"]:
+            raise RuntimeError("this plan's device tree was recycled by a later plan() call; "
+                               "pass keep_tree=True to keep it")
+        return getattr(tree, name)
+
+
+def init_tree(spec, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32", exact: bool = False,
+              cap_beliefs: int = 4096, cap_actions: int = 4096) -> DeviceTree:
+    """Device counterpart of tree.init_tree (tree.py:370-378)."""
+    return DeviceTree(spec.action_count, init_prefs, eta=eta, precision=precision, exact=exact,
+                      cap_beliefs=cap_beliefs, cap_actions=cap_actions)

@@ -1,0 +1,133 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads and exports
+every symbol include/vpb200.h declares, the ctypes mirrors match the C
+layout, and the host-side pieces (key derivation, model layouts, packing,
+config validation) agree with the oracle.  No CUDA call is made here."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2510_27191_b200 as vp
+from paper_2510_27191_b200 import _lib
+from paper_2510_27191_b200.envs import _device
+from paper_2510_27191_b200.rng import fold, mix64_int
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_exports():
+    txt = open(os.path.join(REPO, "include", "vpb200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*)\s+(vp_\w+)\s*\(", txt, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    declared = header_exports()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTED_SYMBOLS) == declared
+    assert lib.vp_abi_version() == _lib.ABI_VERSION
+
+
+def test_ctypes_layout_matches_c():
+    assert _lib.layout_mismatches() == []
+
+
+def test_status_mapping():
+    with pytest.raises(ValueError):
+        _lib.check(_lib.VP_ERR_INVALID, "x")
+    with pytest.raises(_lib.CapacityError):
+        _lib.check(_lib.VP_ERR_CAPACITY, "x")
+    with pytest.raises(TypeError):
+        _lib.check(_lib.VP_ERR_MODEL, "x")
+    _lib.check(_lib.VP_OK)
+
+
+def test_host_key_derivation_matches_oracle():
+    for seed in [0, 1, 12345, 2**63 + 11]:
+        a = vp.RowRng.from_seed(seed)
+        b = oracle.RowRng.from_seed(seed)
+        assert int(a.key) == int(b.key)
+        for path in [(1, 0), (3,), (2, 7, 9)]:
+            assert int(a.derive(*path).key) == int(b.derive(*path).key)
+        k = int(b.key)
+        assert fold(k, 5) == int(oracle.rng.fold_word(b.key, 5))
+        rows = np.arange(100)
+        np.testing.assert_array_equal(a.uniform(rows, 3), b.uniform(rows, 3))
+        np.testing.assert_array_equal(a.normal(rows), b.normal(rows))
+    assert mix64_int(0) == 0
+
+
+def test_product_models_match_oracle_host_parts():
+    for n, m, s in [(4, 3, 0), (7, 8, 1), (11, 11, 2), (15, 15, 5)]:
+        a, b = vp.MarsModel(n, m, layout_seed=s), oracle.MarsModel(n, m, layout_seed=s)
+        np.testing.assert_array_equal(a.rock_x, b.rock_x)
+        np.testing.assert_array_equal(a.rock_y, b.rock_y)
+        assert a.spec.action_count == b.spec.action_count
+        sa = a.sample_initial_states(50, vp.RowRng.from_seed(s).derive(3))
+        sb = b.sample_initial_states(50, oracle.RowRng.from_seed(s).derive(3))
+        np.testing.assert_array_equal(sa.rocks, sb.rocks)
+    sy, so = vp.SyntheticModel(seed=4), oracle.SyntheticModel(seed=4)
+    np.testing.assert_array_equal(sy.sample_initial_states(20, vp.RowRng.from_seed(1)).word,
+                                  so.sample_initial_states(20, oracle.RowRng.from_seed(1)).word)
+    la, lb = vp.LightDarkModel(), oracle.LightDarkModel()
+    np.testing.assert_array_equal(la.sample_initial_states(20, vp.RowRng.from_seed(1)).x,
+                                  lb.sample_initial_states(20, oracle.RowRng.from_seed(1)).x)
+    ta, tb = vp.tiger_model(), oracle.tiger_model()
+    np.testing.assert_array_equal(ta.pomdp.transitions, tb.pomdp.transitions)
+    np.testing.assert_array_equal(ta.pomdp.observations, tb.pomdp.observations)
+    np.testing.assert_array_equal(ta.pomdp.rewards, tb.pomdp.rewards)
+
+
+def test_state_packing_roundtrip():
+    m = vp.MarsModel(7, 8, layout_seed=0)
+    st = m.sample_initial_states(33, vp.RowRng.from_seed(2))
+    st.x[3, 1] = 7
+    st.terminal[5] = True
+    rec = _device.mars_pack(st)
+    assert rec.dtype.itemsize == 16
+    back = m._unpack(rec)
+    np.testing.assert_array_equal(back.x, st.x)
+    np.testing.assert_array_equal(back.y, st.y)
+    np.testing.assert_array_equal(back.rocks, st.rocks)
+    np.testing.assert_array_equal(back.terminal, st.terminal)
+    assert _device.TAB_DTYPE.itemsize == 8 and _device.SYN_DTYPE.itemsize == 16 and _device.LD_DTYPE.itemsize == 24
+
+
+def test_solver_config_contract():
+    with pytest.raises(ValueError):
+        vp.SolverConfig(iterations=None)
+    with pytest.raises(ValueError):
+        vp.SolverConfig(iterations=3, planning_seconds=1.0)
+    with pytest.raises(ValueError):
+        vp.SolverConfig(iterations=3, eta=0.0)
+    with pytest.raises(ValueError):
+        vp.SolverConfig(iterations=0)
+    assert vp.SolverConfig(iterations=2).n_parallel == 1024
+
+
+def test_initial_prefs_rule():
+    from paper_2510_27191_b200.solver import initial_prefs
+
+    assert initial_prefs(vp.MarsModel(4, 3), 2.0) is None
+
+    class Skewed(vp.MarsModel):
+        def reference_log_probs(self):
+            p = np.linspace(1, 2, self.spec.action_count)
+            return np.log(p / p.sum())
+
+    ip = initial_prefs(Skewed(4, 3), 2.0)
+    assert ip.shape == (64,) and np.all(np.isfinite(ip))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(REPO, "paper_2510_27191_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(root, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f

@@ -1,0 +1,175 @@
+"""Whole-planning-step parity of the device path (L1-L3 of SURVEY.md section 4).
+
+* fp64 parity mode (numpy operation order): full ``plan()`` trees equal the
+  REFERENCE's golden trees in every integer column; floats within 1e-9.
+* fp32 fast mode with the oracle's sampled actions injected ("identical
+  injected sample streams"): tree structure bit-exact, PSI / values within
+  1e-5 relative (scale-aware).
+* structural invariants and visit conservation at the C1 configuration.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2510_27191_b200 as vp
+from golden_cases import INT_COLUMNS, load, manifest, plan_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def product_model(kind, seed):
+    if kind.startswith("mars"):
+        n, m = map(int, kind[4:].split("_"))
+        return vp.MarsModel(n, m, layout_seed=seed)
+    return {"tiger": vp.tiger_model, "synthetic": lambda: vp.SyntheticModel(seed=seed),
+            "lightdark": vp.LightDarkModel}[kind]()
+
+
+def scale_close(got, want, rel):
+    """|x - y| <= rel * max(|y|, max |row|) (hard part 2)."""
+    got, want = np.asarray(got), np.asarray(want)
+    if want.ndim == 2:
+        scale = np.maximum(np.abs(want), np.abs(want).max(axis=1, keepdims=True))
+    else:
+        scale = np.abs(want)
+    return np.all(np.abs(got - want) <= rel * np.maximum(scale, 1.0))
+
+
+@pytest.mark.parametrize("name", sorted(manifest()["plans"]))
+def test_fp64_exact_plan_equals_reference_tree(name):
+    case = manifest()["plans"][name]
+    g = load(name)
+    for run in case["runs"]:
+        s = run["seed"]
+        om, belief, cfg, rng = plan_inputs(case, s)
+        out = vp.plan(belief, om, cfg, rng, precision="fp64", exact=True, keep_tree=True)
+        assert out.tree_stats == run["tree_stats"], (name, s)
+        t = out.tree.tables()
+        for k in INT_COLUMNS:
+            np.testing.assert_array_equal(t[k], g[f"s{s}_{k}"].astype(np.int64), err_msg=f"{name} s{s} {k}")
+        np.testing.assert_allclose(t["action_reward_sum"], g[f"s{s}_action_reward_sum"], rtol=1e-12, atol=1e-9)
+        np.testing.assert_allclose(t["prefs"][0], g[f"s{s}_prefs_root"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(t["prefs"].sum(axis=1), g[f"s{s}_prefs_row_sum"], rtol=1e-9, atol=1e-8)
+        if f"s{s}_prefs" in g:
+            assert scale_close(t["prefs"], g[f"s{s}_prefs"], 1e-9)
+        assert out.chosen_action == run["chosen_action"]
+        out.tree.validate()
+
+
+def _oracle_traces(case, seed):
+    om, belief, cfg, rng = plan_inputs(case, seed)
+    traces = []
+    ref = oracle.plan(belief, om, cfg, rng, traces=traces)
+    inject = [np.stack([lv["actions"] for lv in it["levels"]]) for it in traces]
+    return om, belief, cfg, rng, ref, traces, inject
+
+
+@pytest.mark.parametrize("name", ["plan_mars4_3", "plan_mars7_8_small", "plan_tiger", "plan_synthetic",
+                                  "plan_lightdark"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_injected_streams_structure_exact_values_close(name, precision):
+    case = manifest()["plans"][name]
+    s = case["runs"][0]["seed"]
+    om, belief, cfg, rng, ref, traces, inject = _oracle_traces(case, s)
+    out = vp.plan(belief, om, cfg, rng, precision=precision, inject_actions=inject, keep_tree=True, trace=True)
+    want = ref.tree.tables()
+    got = out.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    # per-level traces identical (observations / node ids)
+    for it_d, it_o in zip(out.traces, traces):
+        for lv_d, lv_o in zip(it_d["levels"], it_o["levels"]):
+            np.testing.assert_array_equal(lv_d["observations"], lv_o["observations"])
+            np.testing.assert_array_equal(lv_d["action_nodes"], lv_o["action_nodes"])
+            np.testing.assert_array_equal(lv_d["next_beliefs"], lv_o["next_beliefs"])
+    np.testing.assert_allclose(got["action_reward_sum"], want["action_reward_sum"], rtol=1e-12, atol=1e-9)
+    rel = 1e-5 if precision == "fp32" else 1e-10
+    assert scale_close(got["prefs"], want["prefs"], rel)
+
+
+def test_c1_fp32_invariants_and_conservation():
+    # RockSample(7,8) C1: n_parallel 1024, 8 iterations
+    case = manifest()["plans"]["plan_mars7_8_c1"]
+    for run in case["runs"]:
+        s = run["seed"]
+        om, belief, cfg, rng = plan_inputs(case, s)
+        out = vp.plan(belief, om, cfg, rng, precision="fp32", keep_tree=True)
+        t = out.tree
+        t.validate()
+        tab = t.tables()
+        n = cfg.n_parallel
+        assert tab["action_visits"].sum() == n * sum(range(1, cfg.iterations + 1))
+        assert out.final_d_max == cfg.iterations and out.iterations_run == cfg.iterations
+        # tree size within a few percent of the reference run (sampling is fp32, so not identical)
+        nb_ref = run["tree_stats"]["belief_rows"]
+        assert abs(out.tree_stats["belief_rows"] - nb_ref) < 0.05 * nb_ref
+
+
+def test_capacity_growth_matches_preallocated():
+    case = manifest()["plans"]["plan_mars4_3"]
+    s = case["runs"][0]["seed"]
+    om, belief, cfg, rng = plan_inputs(case, s)
+    base = vp.plan(belief, om, cfg, rng, precision="fp64", exact=True, keep_tree=True).tree.tables()
+    planner = vp.Planner("fp64", exact=True)
+    planner._capacity = lambda n, config, A: (64, config.iterations)  # force repeated growth + rehash
+    out = planner.plan(belief, om, cfg, rng, keep_tree=True)
+    got = out.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], base[k], err_msg=k)
+    assert out.tree.cap_beliefs >= len(got["depth"])
+
+
+def test_search_backup_api_from_interior_frontier():
+    """Reference API: search from depth-1 beliefs, then backup to the root."""
+    om = oracle.MarsModel(4, 3, layout_seed=0)
+    belief = oracle.ParticleBelief.from_model(om, 500, oracle.RowRng.from_seed(0).derive(3))
+    rng = oracle.RowRng.from_seed(0).derive(1, 0)
+    # grow a small tree with the oracle plan then replay it onto the device tree
+    cfg = oracle.SolverConfig(n_parallel=32, iterations=2)
+    ref = oracle.plan(belief, om, cfg, rng)
+    tree_o = ref.tree
+    states = belief.sample_states(32, rng.derive(9))
+    start = tree_o.nodes_at_depth(1)[0][:1].repeat(32)
+    batch_o = oracle.SearchBatch(start, states, depth=1)
+    # device tree with identical content via injected replay of the same plan
+    traces = []
+    oracle.plan(belief, om, cfg, rng, traces=traces)
+    inject = [np.stack([lv["actions"] for lv in it["levels"]]) for it in traces]
+    dev = vp.plan(belief, om, cfg, rng, precision="fp64", exact=True, keep_tree=True, inject_actions=inject).tree
+    leaves_o = oracle.search(tree_o, om, batch_o, 3, 2.0, rng.derive(77))
+    oracle.backup(tree_o, leaves_o, 3, 2.0, om.spec.discount)
+    leaves_d = vp.search(dev, om, vp.SearchBatch(start, states, depth=1), 3, 2.0, vp.RowRng(rng.derive(77).key))
+    np.testing.assert_array_equal(leaves_d.leaf_belief_indices, leaves_o.leaf_belief_indices)
+    np.testing.assert_allclose(leaves_d.heuristic_values, leaves_o.heuristic_values, rtol=1e-13)
+    vp.backup(dev, leaves_d, 3, 2.0, om.spec.discount)
+    want, got = tree_o.tables(), dev.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    assert scale_close(got["prefs"], want["prefs"], 1e-10)
+
+
+def test_tiger_decision_quality_vs_reference_solver():
+    """Root decision of the fp32 device planner agrees with the reference
+    planner on Tiger beliefs (SPEC.md:628 uses n_p = 1024)."""
+    om = oracle.tiger_model()
+    agree = 0
+    cases = 0
+    for p_left in (0.5, 0.2, 0.03, 0.97, 0.85):
+        m = 2000
+        k = int(round(p_left * m))
+        states = oracle.TabularStates(np.array([0] * k + [1] * (m - k)), np.zeros(m, dtype=bool))
+        belief = oracle.ParticleBelief(states, np.full(m, 1.0 / m))
+        cfg = oracle.SolverConfig(n_parallel=1024, iterations=10)
+        for s in range(3):
+            rng = oracle.RowRng.from_seed(s).derive(1, 0)
+            a_ref = oracle.plan(belief, om, cfg, rng).chosen_action
+            a_dev = vp.plan(belief, om, cfg, rng, precision="fp32").chosen_action
+            agree += a_ref == a_dev
+            cases += 1
+        if p_left >= 0.97:
+            assert a_dev == 2  # confident tiger-left: open right
+        if p_left <= 0.03:
+            assert a_dev == 1
+    assert agree >= cases - 2
