@@ -196,8 +196,9 @@ def sample_actions(policies_or_prefs, uniforms, groups=None, *, eta: float = 1.0
     dt = torch.float64 if precision == "fp64" else torch.float32
     dev_rows = torch.from_numpy(rows).to(dt).cuda()
     out = torch.empty(len(u), dtype=torch.int32, device="cuda")
+    dev_g = torch.from_numpy(g).cuda()  # keep every operand alive until the kernel has run
+    dev_u = torch.from_numpy(u).cuda()
     _lib.call("vp_sample_rows", dev_rows.data_ptr(), 1 if precision == "fp64" else 0, int(exact), rows.shape[0],
-              rows.shape[1], float(eta), torch.from_numpy(g).cuda().data_ptr(),
-              torch.from_numpy(u).cuda().data_ptr(), len(u), out.data_ptr(),
+              rows.shape[1], float(eta), dev_g.data_ptr(), dev_u.data_ptr(), len(u), out.data_ptr(),
               torch.cuda.current_stream().cuda_stream)
     return out.cpu().numpy().astype(np.int64)
