@@ -81,7 +81,7 @@ typedef struct vp_tree {
   int32_t action_count;
   int32_t psi_dtype;          /* vp_psi_dtype                               */
   int32_t exact;              /* 1: numpy-order softmax/LSE (fp64 parity)   */
-  int32_t pad0;
+  int32_t psi_stride;         /* elements per PSI row (|A| padded to 16 B)  */
   uint64_t hmask_a, hmask_b;  /* hash capacity - 1 (power of two)          */
   /* belief table B + PSI */
   int32_t* b_parent_action;   /* -1 for the root                            */
@@ -92,6 +92,7 @@ typedef struct vp_tree {
   double* b_value;            /* backup scratch V                           */
   double* b_weight;           /* backup scratch N                           */
   uint32_t* b_stamp;          /* per-(iteration, level) visit stamp         */
+  uint8_t* b_flags;           /* bit 0: PSI row still equals init (lazy)    */
   /* action table A */
   int32_t* a_parent_belief;
   int32_t* a_action;
@@ -106,6 +107,7 @@ typedef struct vp_tree {
   int32_t* counters;          /* [0] n_beliefs [1] n_actions [2] overflow    */
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
+  void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
   double eta;
 } vp_tree;
 
@@ -135,7 +137,7 @@ typedef struct vp_work {
   int32_t* trace_belief;
 } vp_work;
 
-#define VP_SCAN_TILE 1024
+#define VP_SCAN_TILE 128
 
 /* One search call (search.py:86-119). */
 typedef struct vp_search_args {
@@ -207,8 +209,9 @@ int32_t vp_model_heuristic(const vp_model* model, const void* states, int32_t n,
 int32_t vp_lse_rows(const void* rows, int32_t dtype, int32_t exact, int32_t count,
                     int32_t width, double eta, double* out, void* stream);
 /* Categorical draws from softmax(eta * rows[group[i]]) with uniforms u[i]. */
+/* `lse` (fast mode): per-row LSE from vp_lse_rows, as the tree caches it. */
 int32_t vp_sample_rows(const void* rows, int32_t dtype, int32_t exact, int32_t count,
-                       int32_t width, double eta, const int32_t* group,
+                       int32_t width, double eta, const double* lse, const int32_t* group,
                        const double* u, int32_t n, int32_t* out, void* stream);
 
 #ifdef __cplusplus

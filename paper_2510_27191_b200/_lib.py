@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libvpb200.so")
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
 VP_PSI_F32, VP_PSI_F64 = 0, 1
-VP_SCAN_TILE = 1024
+VP_SCAN_TILE = 128
 ABI_VERSION = 1
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
@@ -46,15 +46,15 @@ class VpModel(C.Structure):
 class VpTree(C.Structure):
     _fields_ = [
         ("cap_beliefs", C.c_int32), ("cap_actions", C.c_int32), ("action_count", C.c_int32),
-        ("psi_dtype", C.c_int32), ("exact", C.c_int32), ("pad0", C.c_int32),
+        ("psi_dtype", C.c_int32), ("exact", C.c_int32), ("psi_stride", C.c_int32),
         ("hmask_a", C.c_uint64), ("hmask_b", C.c_uint64),
         ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_depth", C.c_void_p),
         ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p), ("b_weight", C.c_void_p),
-        ("b_stamp", C.c_void_p),
+        ("b_stamp", C.c_void_p), ("b_flags", C.c_void_p),
         ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),
         ("a_visits", C.c_void_p), ("a_num", C.c_void_p), ("a_den", C.c_void_p), ("a_stamp", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
-        ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("eta", C.c_double),
+        ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p), ("eta", C.c_double),
     ]
 
 
@@ -106,8 +106,8 @@ _SIGNATURES = [
     ("vp_lse_rows", C.c_int32,
      [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
     ("vp_sample_rows", C.c_int32,
-     [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_int32,
-      C.c_void_p, C.c_void_p]),
+     [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+      C.c_int32, C.c_void_p, C.c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)

@@ -10,7 +10,12 @@
 // launches per level over the per-level distinct lists recorded by search:
 //   Q / PSI scatter over the level's action nodes, LSE over its beliefs.
 // Nothing here is a dense contraction: every kernel is HBM / latency bound.
+//
+// PSI rows are created lazily: a new belief only gets a "fresh" flag (its row
+// equals the initial row); the sampler draws fresh beliefs from one shared
+// initial CDF, and the backup materialises a row the first time it updates it.
 #include <cstdio>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <cfloat>
@@ -25,37 +30,35 @@ namespace vp {
 
 static thread_local cudaError_t g_last_cuda = cudaSuccess;
 
-template <class T>
-struct Compute;
-template <>
-struct Compute<float> {
-  typedef float T;
-};
-template <>
-struct Compute<double> {
-  typedef double T;
-};
-__device__ __forceinline__ float exp_ct(float x) { return __expf(x); }
-__device__ __forceinline__ double exp_ct(double x) { return exp(x); }
+constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ Slot* slots(void* p) { return reinterpret_cast<Slot*>(p); }
 
-// ------------------------------------------------------------------ LSE / sampling
+// ------------------------------------------------------------------ exp helpers (fast mode)
+// The fast sampler and the fast LSE evaluate exp(eta * psi - shift) as
+// exp2(fma(eta*log2e, psi, -shift*log2e)); float uses ex2.approx, double exp2.
+__device__ __forceinline__ float fexp2(float x) { return exp2f(x); }
+__device__ __forceinline__ double fexp2(double x) { return exp2(x); }
+__device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double ffma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// ------------------------------------------------------------------ LSE
 
 // Fast LSE: warp per row, max then sum of exp (backup.py:34-41 formula).
 template <class PsiT>
 __device__ double warp_lse_fast(const PsiT* row, int A, double eta) {
-  typedef typename Compute<PsiT>::T CT;
+  typedef PsiT CT;
   const int lane = lane_id();
   const CT e = (CT)eta;
   CT m = -(CT)INFINITY;
   for (int a = lane; a < A; a += 32) {
-    const CT z = e * (CT)row[a];
+    const CT z = e * row[a];
     m = z > m ? z : m;
   }
   m = warp_max(m);
+  const CT e2 = (CT)(eta * 1.4426950408889634), m2 = m * (CT)1.4426950408889634;
   CT s = 0;
-  for (int a = lane; a < A; a += 32) s += exp_ct(e * (CT)row[a] - m);
+  for (int a = lane; a < A; a += 32) s += fexp2(ffma(e2, row[a], -m2));
   s = warp_sum(s);
   return (double)m / eta + log((double)s) / eta;
 }
@@ -68,6 +71,8 @@ __device__ double lse_exact(const double* row, int A, double eta) {
   const double s = pairwise_sum(ex, 0, A);
   return m / eta + log(s) / eta;
 }
+
+// ------------------------------------------------------------------ categorical draws
 
 // numpy-order inverse CDF draw (search.py:46-54 then 77-79, 83).
 __device__ int sample_exact(const double* row, int A, double eta, double u) {
@@ -84,51 +89,91 @@ __device__ int sample_exact(const double* row, int A, double eta, double u) {
   return A - 1;
 }
 
-// Warp-cooperative draw for the 32 rows of a warp.  For every distinct belief
-// among the warp's pending rows the warp streams the PSI row once (coalesced),
-// builds the unnormalised CDF exp(eta (PSI - LSE)) in shared memory with a
-// warp scan, and every row of that belief binary-searches it.
-template <class PsiT, class LseF>
-__device__ int warp_sample_fast(const PsiT* psi, int A, double eta, int b, double u, bool active,
-                                typename Compute<PsiT>::T* pre, const LseF& lse_of) {
-  typedef typename Compute<PsiT>::T CT;
-  const int lane = lane_id();
-  u32 todo = __ballot_sync(FULL, active);
-  int action = 0;
-  while (todo) {
-    const int leader = __ffs(todo) - 1;
-    const int bs = __shfl_sync(FULL, b, leader);
-    const PsiT* row = psi + (size_t)bs * A;
-    const CT shift = (CT)(eta * lse_of(bs));
-    const CT e = (CT)eta;
-    CT carry = 0;
-    for (int base = 0; base < A; base += 32) {
-      const int a = base + lane;
-      CT x = 0;
-      if (a < A) x = exp_ct(e * (CT)row[a] - shift);
-      const CT v = warp_inclusive_scan(x);
-      if (a < A) pre[a] = carry + v;
-      carry += __shfl_sync(FULL, v, 31);
-    }
-    __syncwarp();
-    const bool mine = active && ((todo >> lane) & 1u) && b == bs;
-    if (mine) {
-      const CT target = (CT)u * carry;
-      int lo = 0, hi = A;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (pre[mid] > target) hi = mid;
-        else lo = mid + 1;
-      }
-      action = lo < A ? lo : A - 1;
-    }
-    todo &= ~__ballot_sync(FULL, mine);
-    __syncwarp();
+// Fast draw: the probabilities are exp(eta (psi - LSE)), normalised by the
+// row's cached LSE, accumulated left to right until the running sum exceeds u
+// (clamp |A|-1, search.py:83).  The scalar and the vectorised (staged shared
+// memory) versions perform the identical floating-point sequence.
+template <class CT>
+__device__ __forceinline__ int scan_cdf_scalar(const CT* row, int A, CT e2, CT sh2, CT u) {
+  CT cum = 0;
+  for (int a = 0; a < A; ++a) {
+    cum += fexp2(ffma(e2, row[a], -sh2));
+    if (cum > u) return a;
   }
-  return action;
+  return A - 1;
+}
+template <class CT>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  typedef float4 T;
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void get(const T& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+};
+template <>
+struct Vec16<double> {
+  typedef double2 T;
+  static constexpr int N = 2;
+  static __device__ __forceinline__ void get(const T& v, double* o) { o[0] = v.x; o[1] = v.y; }
+};
+template <class CT>
+__device__ __forceinline__ int scan_cdf_vec(const CT* row, int A, CT e2, CT sh2, CT u) {
+  typedef Vec16<CT> V;
+  CT cum = 0;
+  const typename V::T* rv = reinterpret_cast<const typename V::T*>(row);
+  for (int a0 = 0; a0 < A; a0 += V::N) {
+    CT x[V::N];
+    V::get(rv[a0 / V::N], x);
+#pragma unroll
+    for (int j = 0; j < V::N; ++j) {
+      if (a0 + j < A) {
+        cum += fexp2(ffma(e2, x[j], -sh2));
+        if (cum > u) return a0 + j;
+      }
+    }
+  }
+  return A - 1;
+}
+// First index whose (initial-row) CDF value exceeds u.
+template <class CT>
+__device__ __forceinline__ int search_cdf(const CT* cdf, int A, CT u) {
+  int lo = 0, hi = A;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cdf[mid] > u) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo < A ? lo : A - 1;
 }
 
-// ------------------------------------------------------------------ warp claim
+// ------------------------------------------------------------------ TMA bulk staging
+
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// ------------------------------------------------------------------ warp helpers
 
 // Warp-aggregated probe/claim: lanes with equal keys elect their lowest lane
 // (= smallest row, rows are contiguous per warp) to touch the table once.
@@ -158,6 +203,16 @@ __device__ __forceinline__ void warp_list_once(u32* stamp, int node, u32 value, 
   }
 }
 
+// Write the initial PSI row into belief b if it is still lazily fresh.
+template <class PsiT>
+__device__ __forceinline__ void warp_materialise(const vp_tree& T, int b) {
+  if (!(T.b_flags[b] & 1)) return;
+  PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
+  for (int a = lane_id(); a < T.action_count; a += 32) row[a] = (PsiT)T.init_prefs[a];
+  __syncwarp();
+  if (lane_id() == 0) T.b_flags[b] = 0;
+}
+
 // ------------------------------------------------------------------ tree init / rehash
 
 template <class PsiT, bool Exact>
@@ -177,12 +232,21 @@ __global__ void k_tree_init(vp_tree T) {
     if (threadIdx.x == 0) {
       T.init_lse[0] = v;
       T.b_lse[0] = v;
+      // CDF of the initial row with the sampler's exact arithmetic
+      PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
+      const PsiT e2 = (PsiT)(T.eta * 1.4426950408889634), sh2 = (PsiT)(T.eta * v * 1.4426950408889634);
+      PsiT cum = 0;
+      for (int a = 0; a < A; ++a) {
+        cum += fexp2(ffma(e2, psi[a], -sh2));
+        cdf[a] = cum;
+      }
       T.b_parent_action[0] = -1;
       T.b_parent_obs[0] = 0xffffffffu;
       T.b_depth[0] = 0;
       T.b_value[0] = 0.0;
       T.b_weight[0] = 0.0;
       T.b_stamp[0] = 0;
+      T.b_flags[0] = 0;
       T.counters[0] = 1;
       T.counters[1] = 0;
       T.counters[2] = 0;
@@ -225,51 +289,32 @@ __global__ void k_draw(vp_work W, const typename Model::State* particles, const 
 
 // ------------------------------------------------------------------ K1 level_sample
 
-template <class Model, class PsiT, bool Exact>
-__global__ void __launch_bounds__(256) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S,
-                                                      int level, u64 lkey, u32 stamp) {
-  typedef typename Compute<PsiT>::T CT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+struct StageCfg {
+  int rows;     // G: PSI rows staged per warp per batch
+  int stride;   // staged row stride in PsiT elements (odd multiple of 16 bytes)
+};
+
+// Frontier belief of row r at `level` (hash_b slot written by K3 of level-1).
+__device__ __forceinline__ int frontier_of(const vp_tree& T, const vp_work& W, const vp_search_args& S, int level,
+                                           int r) {
+  if (level == S.depth0) return S.start_beliefs ? S.start_beliefs[r] : 0;
+  const u32 sl = (u32)W.slot_b[r] & ~kExistBit;
+  const int b = (int)slots(T.hash_b)[sl].id;
+  if (W.trace_belief) W.trace_belief[(size_t)(level - 1) * W.n + r] = b;
+  return b;
+}
+
+// Model step + claim of (b, a) in hash_a; shared tail of both K1 variants.
+template <class Model>
+__device__ __forceinline__ void step_and_claim(const vp_tree& T, const vp_model& M, const vp_work& W, int level,
+                                               u64 lkey, int r, bool active, int b, int a) {
   const int n = W.n;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = r < n;
-  const int A = T.action_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level] = T.counters[1];
-
-  // frontier belief of this row
-  int b = 0;
-  if (active) {
-    if (level == S.depth0) {
-      b = S.start_beliefs ? S.start_beliefs[r] : 0;
-    } else {
-      const u32 sl = (u32)W.slot_b[r] & ~kExistBit;
-      b = (int)slots(T.hash_b)[sl].id;
-      if (W.trace_belief) W.trace_belief[(size_t)(level - 1) * n + r] = b;
-    }
-  }
-  warp_list_once(T.b_stamp, b, stamp, active, &W.fcount[level], W.flist + (size_t)level * n);
-
-  // action draw: level_rng.derive(0) bound to the row (search.py:110-112)
-  const u64 akey = fold(lkey, 0);
-  const double u = active ? uniform1(akey, (u64)r) : 0.0;
-  int a;
-  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
-  if (S.inject_actions) {
-    a = active ? S.inject_actions[(size_t)level * n + r] : 0;
-  } else if constexpr (Exact) {
-    a = active ? sample_exact(reinterpret_cast<const double*>(psi) + (size_t)b * A, A, T.eta, u) : 0;
-  } else {
-    CT* pre = reinterpret_cast<CT*>(smem_raw) + (size_t)(threadIdx.x >> 5) * A;
-    const double* lse = T.b_lse;
-    a = warp_sample_fast<PsiT>(psi, A, T.eta, b, u, active, pre, [&](int bb) { return lse[bb]; });
-  }
-  // generative step G(s, a) with level_rng.derive(1) (search.py:113-115)
   u64 key = 0;
   if (active) {
     typename Model::State st = reinterpret_cast<typename Model::State*>(W.states)[r];
     u32 o;
     double rw;
-    Model::step(M, st, a, fold(lkey, 1), (u64)r, o, rw);
+    Model::step(M, st, a, fold(lkey, 1), (u64)r, o, rw);  // level_rng.derive(1) (search.py:113-115)
     reinterpret_cast<typename Model::State*>(W.states)[r] = st;
     W.obs[r] = o;
     W.reward[r] = rw;
@@ -284,47 +329,131 @@ __global__ void __launch_bounds__(256) k_level_sample(vp_tree T, vp_model M, vp_
   if (active) W.slot_a[r] = (int)word;
 }
 
+// Fast mode (fp32 or fp64 PSI).  Rows of the warp whose belief is fresh draw
+// from the shared initial CDF; the distinct non-fresh beliefs' PSI rows are
+// staged into shared memory with TMA bulk copies (one cp.async.bulk per row,
+// completion on a per-warp mbarrier), then every lane scans its own row.
+template <class Model, class PsiT>
+__global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S, int level,
+                                                      u64 lkey, u32 stamp, StageCfg sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) u64 s_bar[4];
+  const int n = W.n;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = r < n;
+  const int A = T.action_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level] = T.counters[1];
+  u64* bar = &s_bar[warp];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int b = active ? frontier_of(T, W, S, level, r) : 0;
+  warp_list_once(T.b_stamp, b, stamp, active, &W.fcount[level], W.flist + (size_t)level * n);
+  const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;  // level_rng.derive(0) (search.py:110)
+
+  int a = 0;
+  if (S.inject_actions) {
+    a = active ? S.inject_actions[(size_t)level * n + r] : 0;
+  } else {
+    const bool fresh = active && (T.b_flags[b] & 1);
+    const bool need = active && !fresh;
+    if (fresh) a = search_cdf(reinterpret_cast<const PsiT*>(T.init_cdf), A, (PsiT)u);
+    const u32 grp = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
+    const int my_leader = __ffs(grp) - 1;
+    const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
+    const int K = __popc(leaders);
+    const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
+    const double lse = need ? T.b_lse[b] : 0.0;
+    const PsiT e2 = (PsiT)(T.eta * 1.4426950408889634), sh2 = (PsiT)(T.eta * lse * 1.4426950408889634);
+    PsiT* stage = reinterpret_cast<PsiT*>(smem_raw) + (size_t)warp * sc.rows * sc.stride;
+    const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+    const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
+    u32 phase = 0;
+    u32 pending = leaders;
+    for (int s0 = 0; s0 < K; s0 += sc.rows) {
+      const int cnt = min(sc.rows, K - s0);
+      fence_async_smem();
+      if (lane == 0) mbar_expect_tx(bar, row_bytes * (u32)cnt);
+      __syncwarp();
+      // the j-th pending leader copies its belief's row into stage slot j
+      const bool copier = need && lane == my_leader && my_slot >= s0 && my_slot < s0 + cnt;
+      if (copier) bulk_g2s(stage + (size_t)(my_slot - s0) * sc.stride, psi + (size_t)b * T.psi_stride, row_bytes,
+                           bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      if (need && my_slot >= s0 && my_slot < s0 + cnt)
+        a = scan_cdf_vec<PsiT>(stage + (size_t)(my_slot - s0) * sc.stride, A, e2, sh2, (PsiT)u);
+      __syncwarp();
+    }
+    (void)pending;
+  }
+  step_and_claim<Model>(T, M, W, level, lkey, r, active, b, a);
+}
+
+// fp64 parity mode: thread per row, numpy operation order, no staging.
+template <class Model>
+__global__ void __launch_bounds__(128) k_level_sample_exact(vp_tree T, vp_model M, vp_work W, vp_search_args S,
+                                                            int level, u64 lkey, u32 stamp) {
+  const int n = W.n;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = r < n;
+  const int A = T.action_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level] = T.counters[1];
+  const int b = active ? frontier_of(T, W, S, level, r) : 0;
+  warp_list_once(T.b_stamp, b, stamp, active, &W.fcount[level], W.flist + (size_t)level * n);
+  const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;
+  int a = 0;
+  if (active) {
+    if (S.inject_actions) {
+      a = S.inject_actions[(size_t)level * n + r];
+    } else {
+      const double* row = (T.b_flags[b] & 1) ? T.init_prefs
+                                             : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
+      a = sample_exact(row, A, T.eta, u);
+    }
+  }
+  step_and_claim<Model>(T, M, W, level, lkey, r, active, b, a);
+}
+
 // ------------------------------------------------------------------ K2/K4 first-occurrence scans
 
-// Number the rows that won their key this level, in row order, and write
-// the new nodes' columns.  WhichTable: 0 = actions, 1 = beliefs.
-template <class PsiT, int WhichTable>
-__global__ void __launch_bounds__(256) k_assign(vp_tree T, vp_work W, int level, u32 epoch) {
+// Number the rows that won their key this level, in row order (one row per
+// thread, one tile per block, tiles chained by decoupled look-back), and
+// write the new nodes' columns.  WhichTable: 0 = actions, 1 = beliefs.
+template <int WhichTable>
+__global__ void __launch_bounds__(VP_SCAN_TILE) k_assign(vp_tree T, vp_work W, int level, u32 epoch) {
   __shared__ u32 s_tile;
-  __shared__ u32 s_warp[8];
+  __shared__ u32 s_warp[VP_SCAN_TILE / 32];
   __shared__ u32 s_excl;
+  constexpr int NW = VP_SCAN_TILE / 32;
   const int n = W.n;
   Slot* tab = slots(WhichTable ? T.hash_b : T.hash_a);
   const int* slot_of = WhichTable ? W.slot_b : W.slot_a;
   if (threadIdx.x == 0) s_tile = atomicAdd(&W.scan_ticket[0], 1u);
   __syncthreads();
   const int tile = (int)s_tile;
-  const int r0 = tile * VP_SCAN_TILE + threadIdx.x * 4;
-  u32 slotv[4];
-  bool win[4];
-  u32 cnt = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int r = r0 + j;
-    win[j] = false;
-    slotv[j] = 0;
-    if (r < n) {
-      const u32 w = (u32)slot_of[r];
-      slotv[j] = w & ~kExistBit;
-      if (!(w & kExistBit)) win[j] = ld_volatile_u32(&tab[slotv[j]].id) == (kPending | (u32)r);
-    }
-    cnt += win[j];
+  const int r = tile * VP_SCAN_TILE + threadIdx.x;
+  u32 sl = 0;
+  bool win = false;
+  if (r < n) {
+    const u32 w = (u32)slot_of[r];
+    sl = w & ~kExistBit;
+    if (!(w & kExistBit)) win = ld_volatile_u32(&tab[sl].id) == (kPending | (u32)r);
   }
-  // block exclusive scan of cnt
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const u32 incl = warp_inclusive_scan(cnt);
-  if (lane == 31) s_warp[warp] = incl;
+  const u32 ballot = __ballot_sync(FULL, win);
+  const u32 below = __popc(ballot & ((1u << lane) - 1u));
+  if (lane == 0) s_warp[warp] = __popc(ballot);
   __syncthreads();
   if (warp == 0) {
-    u32 v = lane < 8 ? s_warp[lane] : 0;
+    const u32 v = lane < NW ? s_warp[lane] : 0;
     const u32 vi = warp_inclusive_scan(v);
-    if (lane < 8) s_warp[lane] = vi - v;  // exclusive per warp
-    const u32 agg = __shfl_sync(FULL, vi, 7);
+    if (lane < NW) s_warp[lane] = vi - v;
+    const u32 agg = __shfl_sync(FULL, vi, NW - 1);
     if (lane == 0) {
       const u32 excl = tile_lookback(reinterpret_cast<u64*>(W.scan_status), tile, agg, epoch);
       s_excl = excl;
@@ -337,65 +466,41 @@ __global__ void __launch_bounds__(256) k_assign(vp_tree T, vp_work W, int level,
     }
   }
   __syncthreads();
-  const int base = W.level_base[2 * level + WhichTable];
-  u32 off = s_excl + s_warp[warp] + incl - cnt;
+  if (!win) return;
+  const int id = W.level_base[2 * level + WhichTable] + (int)(s_excl + s_warp[warp] + below);
+  Slot& s = tab[sl];
+  s.id = (u32)id;
   const int cap = WhichTable ? T.cap_beliefs : T.cap_actions;
-  int new_id[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    new_id[j] = -1;
-    if (!win[j]) continue;
-    const int id = base + (int)off++;
-    new_id[j] = id;
-    Slot& s = tab[slotv[j]];
-    s.id = (u32)id;
-    if (id >= cap) {
-      T.counters[2] = 1;  // overflow: host grows and fails the plan loudly
-      new_id[j] = -1;
-      continue;
-    }
-    const u64 key = s.key;
-    if (WhichTable == 0) {
-      T.a_parent_belief[id] = (int)(key >> 32);
-      T.a_action[id] = (int)(u32)key;
-      T.a_reward[id] = 0.0;
-      T.a_visits[id] = 0;
-      T.a_num[id] = 0.0;
-      T.a_den[id] = 0.0;
-      T.a_stamp[id] = 0;
-    } else {
-      const int pa = (int)(key >> 32);
-      T.b_parent_action[id] = pa;
-      T.b_parent_obs[id] = (u32)key;
-      T.b_depth[id] = T.b_depth[T.a_parent_belief[pa]] + 1;
-      T.b_lse[id] = T.init_lse[0];
-      T.b_value[id] = 0.0;
-      T.b_weight[id] = 0.0;
-      T.b_stamp[id] = 0;
-    }
+  if (id >= cap) {
+    T.counters[2] = 1;  // overflow: the host fails the plan loudly
+    return;
   }
-  if (WhichTable == 1) {
-    // warp-cooperative PSI row init for each new belief of this warp
-    PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-    const int A = T.action_count;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      u32 m = __ballot_sync(FULL, new_id[j] >= 0);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const int id = __shfl_sync(FULL, new_id[j], src);
-        PsiT* row = psi + (size_t)id * A;
-        for (int a = lane; a < A; a += 32) row[a] = (PsiT)T.init_prefs[a];
-      }
-    }
+  const u64 key = s.key;
+  if (WhichTable == 0) {
+    T.a_parent_belief[id] = (int)(key >> 32);
+    T.a_action[id] = (int)(u32)key;
+    T.a_reward[id] = 0.0;
+    T.a_visits[id] = 0;
+    T.a_num[id] = 0.0;
+    T.a_den[id] = 0.0;
+    T.a_stamp[id] = 0;
+  } else {
+    const int pa = (int)(key >> 32);
+    T.b_parent_action[id] = pa;
+    T.b_parent_obs[id] = (u32)key;
+    T.b_depth[id] = T.b_depth[T.a_parent_belief[pa]] + 1;
+    T.b_lse[id] = T.init_lse[0];
+    T.b_value[id] = 0.0;
+    T.b_weight[id] = 0.0;
+    T.b_stamp[id] = 0;
+    T.b_flags[id] = 1;  // PSI row lazily equal to the initial row (tree.py:253)
   }
 }
 
 // ------------------------------------------------------------------ K3 accum_probe
 
-__global__ void __launch_bounds__(256) k_accum_probe(vp_tree T, vp_work W, int level, u32 stamp) {
-  __shared__ double s_rew[256];
+__global__ void __launch_bounds__(128) k_accum_probe(vp_tree T, vp_work W, int level, u32 stamp) {
+  __shared__ double s_rew[128];
   const int n = W.n;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = r < n;
@@ -416,8 +521,7 @@ __global__ void __launch_bounds__(256) k_accum_probe(vp_tree T, vp_work W, int l
   __syncwarp();
   const u32 grp = __match_any_sync(FULL, ok ? (u32)id : 0xffffffffu);
   const int leader = __ffs(grp) - 1;
-  const int lane = lane_id();
-  if (ok && lane == leader) {
+  if (ok && lane_id() == leader) {
     double sum = 0.0;
     u32 g = grp;
     const int wbase = threadIdx.x & ~31;
@@ -441,22 +545,16 @@ __global__ void __launch_bounds__(256) k_accum_probe(vp_tree T, vp_work W, int l
 // ------------------------------------------------------------------ leaves
 
 template <class Model>
-__global__ void __launch_bounds__(256) k_leaf(vp_tree T, vp_model M, vp_work W, vp_search_args S, int dmax,
+__global__ void __launch_bounds__(128) k_leaf(vp_tree T, vp_model M, vp_work W, vp_search_args S, int dmax,
                                               u32 stamp) {
-  __shared__ double s_h[256];
+  __shared__ double s_h[128];
   const int n = W.n;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = r < n;
   int b = 0;
   double h = 0.0;
   if (active) {
-    if (dmax == S.depth0) {
-      b = S.start_beliefs ? S.start_beliefs[r] : 0;
-    } else {
-      const u32 sl = (u32)W.slot_b[r] & ~kExistBit;
-      b = (int)slots(T.hash_b)[sl].id;
-      if (W.trace_belief) W.trace_belief[(size_t)(dmax - 1) * n + r] = b;
-    }
+    b = frontier_of(T, W, S, dmax, r);
     h = Model::heuristic(M, reinterpret_cast<const typename Model::State*>(W.states)[r]);
     W.leaf_belief[r] = b;
     W.leaf_value[r] = h;
@@ -485,7 +583,10 @@ __global__ void __launch_bounds__(256) k_leaf(vp_tree T, vp_model M, vp_work W, 
 
 // Leaves: V = mean heuristic, N = batch count (backup.py:44-51, 82-87), then
 // feed the parent action's visit-weighted child mean (backup.py:64-68).
-__global__ void k_backup_leaves(vp_tree T, vp_work W, int dmax) {
+// Warps with spare work materialise the fresh PSI rows of level `mat`
+// (the parents the next launch updates).
+template <class PsiT>
+__global__ void k_backup_leaves(vp_tree T, vp_work W, int dmax, int mat) {
   const int cnt = W.fcount[dmax];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const int b = W.flist[(size_t)dmax * W.n + i];
@@ -499,6 +600,18 @@ __global__ void k_backup_leaves(vp_tree T, vp_work W, int dmax) {
       atomicAdd(&T.a_den[pa], w);
     }
   }
+  if (mat >= 0) {
+    const int mc = W.fcount[mat];
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
+  }
+}
+
+template <class PsiT>
+__global__ void k_materialise(vp_tree T, vp_work W, int lvl) {
+  const int mc = W.fcount[lvl];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)lvl * W.n + i]);
 }
 
 // Level d: actions of level d-1 -> Q -> PSI[b, a] += Q - LSE_pre(b)
@@ -507,7 +620,6 @@ template <class PsiT>
 __global__ void k_backup_q(vp_tree T, vp_work W, int lvl, double gamma) {
   const int cnt = W.pcount[lvl];
   PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-  const int A = T.action_count;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const int a = W.plist[(size_t)lvl * W.n + i];
     const double vis = (double)T.a_visits[a];
@@ -515,26 +627,27 @@ __global__ void k_backup_q(vp_tree T, vp_work W, int lvl, double gamma) {
     T.a_num[a] = 0.0;
     T.a_den[a] = 0.0;
     const int b = T.a_parent_belief[a];
-    PsiT* cell = psi + (size_t)b * A + T.a_action[a];
+    PsiT* cell = psi + (size_t)b * T.psi_stride + T.a_action[a];
     *cell = (PsiT)((double)*cell + (q - T.b_lse[b]));
     atomicAdd(&T.b_weight[b], vis);
   }
 }
 
 // Level d: beliefs of level d-1 -> V = LSE_post (backup.py:109), cached as
-// the next LSE_pre, then their own parent action's child mean (level d-1).
+// the next LSE_pre, then their own parent action's child mean (level d-1);
+// spare warps materialise the fresh rows of level `mat` = d-2.
 template <class PsiT, bool Exact>
-__global__ void k_backup_v(vp_tree T, vp_work W, int lvl) {
+__global__ void k_backup_v(vp_tree T, vp_work W, int lvl, int mat) {
   const int cnt = W.fcount[lvl];
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   const int A = T.action_count;
   const int lane = lane_id();
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
   if constexpr (Exact) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
       const int b = W.flist[(size_t)lvl * W.n + i];
-      const double v = lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * A, A, T.eta);
+      const double v = lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta);
       T.b_lse[b] = v;
       const double w = T.b_weight[b];
       T.b_weight[b] = 0.0;
@@ -545,9 +658,9 @@ __global__ void k_backup_v(vp_tree T, vp_work W, int lvl) {
       }
     }
   } else {
-    for (int i = gwarp; i < cnt; i += nwarps) {
+    for (int i = gw; i < cnt; i += nw) {
       const int b = W.flist[(size_t)lvl * W.n + i];
-      const double v = warp_lse_fast<PsiT>(psi + (size_t)b * A, A, T.eta);
+      const double v = warp_lse_fast<PsiT>(psi + (size_t)b * T.psi_stride, A, T.eta);
       if (lane == 0) {
         T.b_lse[b] = v;
         const double w = T.b_weight[b];
@@ -559,6 +672,10 @@ __global__ void k_backup_v(vp_tree T, vp_work W, int lvl) {
         }
       }
     }
+  }
+  if (mat >= 0) {
+    const int mc = W.fcount[mat];
+    for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
   }
 }
 
@@ -658,21 +775,16 @@ __global__ void k_lse_rows(const PsiT* rows, int count, int width, double eta, d
   }
 }
 template <class PsiT, bool Exact>
-__global__ void k_sample_rows(const PsiT* rows, int width, double eta, const int32_t* group, const double* u,
-                              int n, int32_t* out) {
-  typedef typename Compute<PsiT>::T CT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void k_sample_rows(const PsiT* rows, int width, double eta, const double* lse, const int32_t* group,
+                              const double* u, int n, int32_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < n;
-  const int g = active ? group[i] : 0;
-  const double ui = active ? u[i] : 0.0;
+  if (i >= n) return;
+  const int g = group[i];
   if constexpr (Exact) {
-    if (active) out[i] = sample_exact(reinterpret_cast<const double*>(rows) + (size_t)g * width, width, eta, ui);
+    out[i] = sample_exact(reinterpret_cast<const double*>(rows) + (size_t)g * width, width, eta, u[i]);
   } else {
-    CT* pre = reinterpret_cast<CT*>(smem_raw) + (size_t)(threadIdx.x >> 5) * width;
-    auto lse_of = [&](int bb) { return warp_lse_fast<PsiT>(rows + (size_t)bb * width, width, eta); };
-    const int a = warp_sample_fast<PsiT>(rows, width, eta, g, ui, active, pre, lse_of);
-    if (active) out[i] = a;
+    const PsiT e2 = (PsiT)(eta * 1.4426950408889634), sh2 = (PsiT)(eta * lse[g] * 1.4426950408889634);
+    out[i] = scan_cdf_scalar<PsiT>(rows + (size_t)g * width, width, e2, sh2, (PsiT)u[i]);
   }
 }
 
@@ -762,34 +874,63 @@ static bool state_size_ok(const vp_model& M) {
   return M.state_bytes == (int)sizeof(typename Model::State);
 }
 
+static int stage_budget_bytes() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VP_STAGE_KB");
+    v = (e ? atoi(e) : 200) * 1024;
+    if (v < 16 * 1024) v = 16 * 1024;
+    if (v > 220 * 1024) v = 220 * 1024;
+  }
+  return v;
+}
+
+template <class PsiT>
+static StageCfg stage_cfg(int A) {
+  int chunks = (int)(((size_t)A * sizeof(PsiT) + 15) / 16);
+  if ((chunks & 1) == 0) ++chunks;  // odd number of 16-B chunks: conflict-free LDS.128 across rows
+  StageCfg c;
+  c.stride = chunks * 16 / (int)sizeof(PsiT);
+  const int per_warp = stage_budget_bytes() / 4;
+  c.rows = std::max(1, std::min(32, per_warp / (chunks * 16)));
+  return c;
+}
+
 template <class Model, class PsiT, bool Exact>
 static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                           cudaStream_t st) {
-  typedef typename Compute<PsiT>::T CT;
   const int n = W.n;
-  const int grid = blocks_for(n, 256);
+  const int grid = blocks_for(n, 128);
   const int tiles = blocks_for(n, VP_SCAN_TILE);
   if (cudaMemsetAsync(W.fcount, 0, sizeof(int32_t) * (W.max_levels + 1), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(W.pcount, 0, sizeof(int32_t) * W.max_levels, st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * tiles, st) != cudaSuccess) return VP_ERR_CUDA;
+  StageCfg sc{0, 0};
   size_t smem = 0;
-  if (!Exact) {
-    smem = (size_t)8 * T.action_count * sizeof(CT);
-    if (smem > 48 * 1024) {
-      if (smem > 220 * 1024) return VP_ERR_INVALID;
-      cudaFuncSetAttribute(k_level_sample<Model, PsiT, Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+  if constexpr (!Exact) {
+    sc = stage_cfg<PsiT>(T.action_count);
+    smem = (size_t)4 * sc.rows * sc.stride * sizeof(PsiT);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      if (cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return VP_ERR_CUDA;
+      configured = smem;
     }
   }
   for (int l = S.depth0; l < S.d_max; ++l) {
     const u64 lkey = fold(S.search_key, (u64)l);
     const u32 stamp = S.stamp_base + (u32)l + 1u;
-    { Launch L_(KK_LEVEL_SAMPLE, st); k_level_sample<Model, PsiT, Exact><<<grid, 256, smem, st>>>(T, M, W, S, l, lkey, stamp); }
-    { Launch L_(KK_ASSIGN_ACTIONS, st); k_assign<PsiT, 0><<<tiles, 256, 0, st>>>(T, W, l, (u32)(2 * l + 1)); }
-    { Launch L_(KK_ACCUM_PROBE, st); k_accum_probe<<<grid, 256, 0, st>>>(T, W, l, stamp); }
-    { Launch L_(KK_ASSIGN_BELIEFS, st); k_assign<PsiT, 1><<<tiles, 256, 0, st>>>(T, W, l, (u32)(2 * l + 2)); }
+    {
+      Launch L_(KK_LEVEL_SAMPLE, st);
+      if constexpr (Exact) k_level_sample_exact<Model><<<grid, 128, 0, st>>>(T, M, W, S, l, lkey, stamp);
+      else k_level_sample<Model, PsiT><<<grid, 128, smem, st>>>(T, M, W, S, l, lkey, stamp, sc);
+    }
+    { Launch L_(KK_ASSIGN_ACTIONS, st); k_assign<0><<<tiles, VP_SCAN_TILE, 0, st>>>(T, W, l, (u32)(2 * l + 1)); }
+    { Launch L_(KK_ACCUM_PROBE, st); k_accum_probe<<<grid, 128, 0, st>>>(T, W, l, stamp); }
+    { Launch L_(KK_ASSIGN_BELIEFS, st); k_assign<1><<<tiles, VP_SCAN_TILE, 0, st>>>(T, W, l, (u32)(2 * l + 2)); }
   }
-  { Launch L_(KK_LEAF, st); k_leaf<Model><<<grid, 256, 0, st>>>(T, M, W, S, S.d_max, S.stamp_base + (u32)S.d_max + 1u); }
+  { Launch L_(KK_LEAF, st); k_leaf<Model><<<grid, 128, 0, st>>>(T, M, W, S, S.d_max, S.stamp_base + (u32)S.d_max + 1u); }
   return check_launch();
 }
 
@@ -798,16 +939,21 @@ static int32_t run_backup(const vp_tree& T, const vp_work& W, int depth0, int dm
                           cudaStream_t st) {
   const int n = W.n;
   const int grid = blocks_for(n, 256);
-  const int vgrid = Exact ? grid : std::min(blocks_for((long long)n * 32, 256), 148 * 32);
-  { Launch L_(KK_BACKUP_LEAVES, st); k_backup_leaves<<<grid, 256, 0, st>>>(T, W, dmax); }
+  const int wgrid = std::min(blocks_for((long long)n * 32, 256), 148 * 32);
+  const int vgrid = Exact ? std::max(grid, wgrid) : wgrid;
+  if (dmax < 1) return VP_OK;
+  // lists of level L exist (recorded by search) for depth0 <= L <= dmax
+  auto recorded = [&](int L) { return L >= depth0 && L >= 0 ? L : -1; };
+  { Launch L_(KK_BACKUP_LEAVES, st); k_backup_leaves<PsiT><<<wgrid, 256, 0, st>>>(T, W, dmax, recorded(dmax - 1)); }
   for (int d = dmax; d >= 1; --d) {
     if (d <= depth0) {
       if (cudaMemsetAsync(W.pcount + (d - 1), 0, sizeof(int32_t), st) != cudaSuccess) return VP_ERR_CUDA;
       if (cudaMemsetAsync(W.fcount + (d - 1), 0, sizeof(int32_t), st) != cudaSuccess) return VP_ERR_CUDA;
       { Launch L_(KK_PARENT_LISTS, st); k_parent_lists<<<grid, 256, 0, st>>>(T, W, d, stamp_base + 0x40000000u + (u32)d); }
+      { Launch L_(KK_PARENT_LISTS, st); k_materialise<PsiT><<<wgrid, 256, 0, st>>>(T, W, d - 1); }
     }
     { Launch L_(KK_BACKUP_Q, st); k_backup_q<PsiT><<<grid, 256, 0, st>>>(T, W, d - 1, gamma); }
-    { Launch L_(KK_BACKUP_V, st); k_backup_v<PsiT, Exact><<<vgrid, 256, 0, st>>>(T, W, d - 1); }
+    { Launch L_(KK_BACKUP_V, st); k_backup_v<PsiT, Exact><<<vgrid, 256, 0, st>>>(T, W, d - 1, d >= 2 ? recorded(d - 2) : -1); }
   }
   return check_launch();
 }
@@ -1026,20 +1172,16 @@ int32_t vp_lse_rows(const void* rows, int32_t dtype, int32_t exact, int32_t coun
 }
 
 int32_t vp_sample_rows(const void* rows, int32_t dtype, int32_t exact, int32_t count, int32_t width, double eta,
-                       const int32_t* group, const double* u, int32_t n, int32_t* out, void* stream) {
+                       const double* lse, const int32_t* group, const double* u, int32_t n, int32_t* out,
+                       void* stream) {
   if (count < 1 || width < 1 || eta <= 0 || n < 0) return VP_ERR_INVALID;
+  if (!exact && !lse) return VP_ERR_INVALID;
   if (!n) return VP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   return dispatch_psi(dtype, exact, [&](auto z, auto ex) -> int32_t {
     typedef decltype(z) PsiT;
-    const size_t smem = decltype(ex)::value ? 0 : (size_t)8 * width * sizeof(PsiT);
-    if (smem > 48 * 1024) {
-      if (smem > 220 * 1024) return VP_ERR_INVALID;
-      cudaFuncSetAttribute(k_sample_rows<PsiT, decltype(ex)::value>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-    }
-    k_sample_rows<PsiT, decltype(ex)::value><<<blocks_for(n, 256), 256, smem, st>>>(
-        reinterpret_cast<const PsiT*>(rows), width, eta, group, u, n, out);
+    k_sample_rows<PsiT, decltype(ex)::value><<<blocks_for(n, 256), 256, 0, st>>>(
+        reinterpret_cast<const PsiT*>(rows), width, eta, lse, group, u, n, out);
     return check_launch();
   });
 }

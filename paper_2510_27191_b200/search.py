@@ -195,10 +195,17 @@ def sample_actions(policies_or_prefs, uniforms, groups=None, *, eta: float = 1.0
     g = np.zeros(len(u), dtype=np.int32) if groups is None else np.asarray(groups, dtype=np.int32)
     dt = torch.float64 if precision == "fp64" else torch.float32
     dev_rows = torch.from_numpy(rows).to(dt).cuda()
+    dtype_code = 1 if precision == "fp64" else 0
+    if not exact:
+        from .backup import log_sum_exp_rows
+
+        lse = torch.from_numpy(np.atleast_1d(log_sum_exp_rows(rows.astype(np.float64) if precision == "fp64"
+                                                              else rows.astype(np.float32).astype(np.float64),
+                                                              eta, precision=precision, exact=False))).cuda()
     out = torch.empty(len(u), dtype=torch.int32, device="cuda")
     dev_g = torch.from_numpy(g).cuda()  # keep every operand alive until the kernel has run
     dev_u = torch.from_numpy(u).cuda()
-    _lib.call("vp_sample_rows", dev_rows.data_ptr(), 1 if precision == "fp64" else 0, int(exact), rows.shape[0],
-              rows.shape[1], float(eta), dev_g.data_ptr(), dev_u.data_ptr(), len(u), out.data_ptr(),
-              torch.cuda.current_stream().cuda_stream)
+    _lib.call("vp_sample_rows", dev_rows.data_ptr(), dtype_code, int(exact), rows.shape[0], rows.shape[1],
+              float(eta), None if exact else lse.data_ptr(), dev_g.data_ptr(), dev_u.data_ptr(), len(u),
+              out.data_ptr(), torch.cuda.current_stream().cuda_stream)
     return out.cpu().numpy().astype(np.int64)

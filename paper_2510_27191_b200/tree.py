@@ -4,7 +4,8 @@
 Layout (all device tensors, row-indexed):
 
     B   b_parent_action i32 | b_parent_obs u32 | b_depth i32
-    PSI psi [cap_beliefs, |A|] fp32 (fast) or fp64 (parity), row-major
+    PSI psi [cap_beliefs, stride] fp32 (fast) or fp64 (parity), row-major,
+        rows padded to 16 B; b_flags bit 0 = row still lazily equal to init
         b_lse f64 (cached LSE of the row) | b_value, b_weight f64 (backup scratch)
     A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32
         a_num, a_den f64 (backup scratch)
@@ -71,6 +72,10 @@ class DeviceTree:
         self._counters = torch.zeros(4, dtype=torch.int32, device="cuda")
         self._init_lse = torch.zeros(1, dtype=torch.float64, device="cuda")
         self._init_prefs = torch.zeros(action_count, dtype=torch.float64, device="cuda")
+        # PSI rows padded to 16 bytes so they can be TMA bulk-copied (csrc K1)
+        per16 = 4 if precision == "fp32" else 2
+        self.psi_stride = (action_count + per16 - 1) // per16 * per16
+        self._init_cdf = torch.zeros(action_count, dtype=self._psi_dtype, device="cuda")
         self._host_counts = (C.c_int32 * 3)()
         self.cap_beliefs = 0
         self.cap_actions = 0
@@ -93,11 +98,12 @@ class DeviceTree:
         self.b_parent_action = col(g("b_parent_action"), cap_b, torch.int32, keep_b)
         self.b_parent_obs = col(g("b_parent_obs"), cap_b, torch.int32, keep_b)
         self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
-        self.psi = col(g("psi"), (cap_b, A), self._psi_dtype, keep_b)
+        self.psi = col(g("psi"), (cap_b, self.psi_stride), self._psi_dtype, keep_b)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
         self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b)
         self.b_weight = col(g("b_weight"), cap_b, torch.float64, keep_b)
         self.b_stamp = col(g("b_stamp"), cap_b, torch.int32, keep_b)
+        self.b_flags = col(g("b_flags"), cap_b, torch.uint8, keep_b)
         self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
         self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
         self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a)
@@ -115,13 +121,15 @@ class DeviceTree:
         s.psi_dtype = PRECISIONS[self.precision]
         s.exact = int(self.exact)
         s.hmask_a, s.hmask_b = ha - 1, hb - 1
+        s.psi_stride = self.psi_stride
         for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_weight",
-                     "b_stamp", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_num", "a_den",
+                     "b_stamp", "b_flags", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_num", "a_den",
                      "a_stamp", "hash_a", "hash_b"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
         s.init_lse = self._init_lse.data_ptr()
+        s.init_cdf = self._init_cdf.data_ptr()
         s.eta = self.eta
         self.struct = s
 
@@ -187,11 +195,14 @@ class DeviceTree:
         obs = self.b_parent_obs[:nb].cpu().numpy().view(np.uint32).astype(np.int64)
         if nb:
             obs[0] = ROOT_SENTINEL
+        prefs = self.psi[:nb, : self.action_count].cpu().numpy().astype(np.float64)
+        fresh = (self.b_flags[:nb].cpu().numpy() & 1).astype(bool)
+        prefs[fresh] = self.init_prefs  # lazily initialised rows (tree.py:253)
         return {
             "parent_action": self.b_parent_action[:nb].cpu().numpy().astype(np.int64),
             "parent_obs": obs,
             "depth": self.b_depth[:nb].cpu().numpy().astype(np.int64),
-            "prefs": self.psi[:nb].cpu().numpy().astype(np.float64),
+            "prefs": prefs,
             "action_parent_belief": self.a_parent_belief[:na].cpu().numpy().astype(np.int64),
             "action_id": self.a_action[:na].cpu().numpy().astype(np.int64),
             "action_reward_sum": self.a_reward[:na].cpu().numpy().copy(),
@@ -208,7 +219,7 @@ class DeviceTree:
     action_visits = property(lambda s: s.tables()["action_visits"])
 
     def root_prefs(self) -> np.ndarray:
-        return self.psi[0].cpu().numpy().astype(np.float64)
+        return self.psi[0, : self.action_count].cpu().numpy().astype(np.float64)
 
     def stats(self) -> dict:
         nb, na, _ = self.counts()
