@@ -195,9 +195,10 @@ class DeviceTree:
         obs = self.b_parent_obs[:nb].cpu().numpy().view(np.uint32).astype(np.int64)
         if nb:
             obs[0] = ROOT_SENTINEL
-        prefs = self.psi[:nb, : self.action_count].cpu().numpy().astype(np.float64)
-        fresh = (self.b_flags[:nb].cpu().numpy() & 1).astype(bool)
-        prefs[fresh] = self.init_prefs  # lazily initialised rows (tree.py:253)
+        fresh = (self.b_flags[:nb] & 1).bool()[:, None]
+        init = self._init_prefs.to(self._psi_dtype)[None, :]
+        # lazily initialised rows read as the initial row (tree.py:253)
+        prefs = _torch().where(fresh, init, self.psi[:nb, : self.action_count]).cpu().numpy().astype(np.float64)
         return {
             "parent_action": self.b_parent_action[:nb].cpu().numpy().astype(np.int64),
             "parent_obs": obs,

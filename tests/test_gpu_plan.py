@@ -102,9 +102,10 @@ def test_c1_fp32_invariants_and_conservation():
         n = cfg.n_parallel
         assert tab["action_visits"].sum() == n * sum(range(1, cfg.iterations + 1))
         assert out.final_d_max == cfg.iterations and out.iterations_run == cfg.iterations
-        # tree size within a few percent of the reference run (sampling is fp32, so not identical)
+        # fp32 draws diverge from the fp64 reference after the first CDF-edge flip, so only
+        # the scale is comparable (same-seed reference trees vary 13k-19k across plan keys)
         nb_ref = run["tree_stats"]["belief_rows"]
-        assert abs(out.tree_stats["belief_rows"] - nb_ref) < 0.05 * nb_ref
+        assert 0.6 * nb_ref < out.tree_stats["belief_rows"] < 1.6 * nb_ref
 
 
 def test_capacity_growth_matches_preallocated():
@@ -173,3 +174,46 @@ def test_tiger_decision_quality_vs_reference_solver():
         if p_left <= 0.03:
             assert a_dev == 1
     assert agree >= cases - 2
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("kind,n_par", [("mars7_8", 2048), ("mars11_11", 4096), ("tiger", 1024),
+                                        ("synthetic", 2048), ("lightdark", 1024)])
+def test_fast_sampler_draws_follow_softmax_of_tree(kind, n_par, precision):
+    """In-kernel fast draws (fresh rows via the shared initial CDF, other rows
+    TMA-staged) equal the inverse CDF of softmax(eta * PSI) of the tree at the
+    start of the iteration, for every row of every level."""
+    seed = 3
+    om = {"mars7_8": lambda: oracle.MarsModel(7, 8, layout_seed=seed),
+          "mars11_11": lambda: oracle.MarsModel(11, 11, layout_seed=seed),
+          "tiger": oracle.tiger_model, "synthetic": lambda: oracle.SyntheticModel(seed=seed),
+          "lightdark": oracle.LightDarkModel}[kind]()
+    belief = oracle.ParticleBelief.from_model(om, 2000, oracle.RowRng.from_seed(seed).derive(3))
+    rng = oracle.RowRng.from_seed(seed).derive(1, 0)
+    k = 5
+    before = vp.plan(belief, om, oracle.SolverConfig(n_parallel=n_par, iterations=k - 1), rng,
+                     precision=precision, keep_tree=True).tree.tables()
+    out = vp.plan(belief, om, oracle.SolverConfig(n_parallel=n_par, iterations=k), rng, precision=precision,
+                  keep_tree=True, trace=True)
+    prefs = before["prefs"]
+    last = out.traces[-1]["levels"]
+    search_rng = rng.derive(k - 1).derive(1)
+    rows = np.arange(n_par)
+    mism = total = 0
+    belief_ids = np.zeros(n_par, dtype=np.int64)
+    for lvl, tr in enumerate(last):
+        u = search_rng.derive(lvl).derive(0).uniform(rows)
+        known = belief_ids < len(prefs)  # beliefs created this iteration are fresh (init row)
+        rowp = np.where(known[:, None], prefs[np.minimum(belief_ids, len(prefs) - 1)], 0.0)
+        pol = oracle.softmax_rows(rowp, 2.0)
+        cum = np.cumsum(pol, axis=1)
+        want = np.minimum((cum <= u[:, None]).sum(axis=1), prefs.shape[1] - 1)
+        got = tr["actions"]
+        bad = np.flatnonzero(got != want)
+        tol = 2e-5 if precision == "fp32" else 1e-12
+        for i in bad:
+            assert np.min(np.abs(cum[i] - u[i])) < tol, (lvl, i, got[i], want[i])
+        mism += len(bad)
+        total += n_par
+        belief_ids = tr["next_beliefs"]
+    assert mism <= max(3, 1e-3 * total)
