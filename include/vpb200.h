@@ -148,7 +148,29 @@ typedef struct vp_search_args {
   int32_t iteration;
   const int32_t* inject_actions; /* [d_max * n] level-major, or NULL       */
   const int32_t* start_beliefs;  /* [n] frontier at depth0, NULL = root     */
+  const uint64_t* search_key_dev; /* device copy of search_key, or NULL     */
 } vp_search_args;
+
+/* A whole fixed-iteration planning step (solver.py:79-113) enqueued by one
+ * call; with use_graph it is captured once into a CUDA graph and replayed
+ * (re-captured whenever a pointer / size / model parameter changes).  Host
+ * buffers must be pinned; the caller synchronises the stream and then reads
+ * out_host = {chosen action, n_beliefs, n_actions, overflow}. */
+typedef struct vp_plan_args {
+  int32_t iterations;          /* fixed-iteration budget (>= 1)             */
+  int32_t d_max_cap;
+  int32_t m;                   /* particles                                 */
+  int32_t use_graph;
+  double gamma;
+  const void* particles_host;  /* [m * state_bytes] pinned, or NULL         */
+  void* particles_dev;
+  const double* cumw_host;     /* [m] cumsum(weights) pinned, or NULL       */
+  double* cumw_dev;
+  const uint64_t* keys_host;   /* [2*iterations] (draw, search) keys, pinned*/
+  uint64_t* keys_dev;
+  int32_t* out_host;           /* [4] pinned                                */
+  int32_t* out_dev;            /* [4]                                       */
+} vp_plan_args;
 
 /* ---- library ---------------------------------------------------------- */
 int32_t vp_abi_version(void);
@@ -192,6 +214,8 @@ int32_t vp_search(const vp_tree* tree, const vp_model* model, const vp_work* wor
 /* Level-synchronous backup d = d_max..depth0+1 (backup.py:75-114). */
 int32_t vp_backup(const vp_tree* tree, const vp_work* work, int32_t depth0,
                   int32_t d_max, double gamma, uint32_t stamp_base, void* stream);
+int32_t vp_plan(const vp_tree* tree, const vp_model* model, const vp_work* work,
+                const vp_plan_args* args, void* stream);
 /* argmax of PSI[0] with lowest-id ties (solver.py:112) into out_dev[0]. */
 int32_t vp_root_argmax(const vp_tree* tree, int32_t* out_dev, void* stream);
 

@@ -74,7 +74,18 @@ class VpSearchArgs(C.Structure):
     _fields_ = [
         ("search_key", C.c_uint64), ("depth0", C.c_int32), ("d_max", C.c_int32),
         ("stamp_base", C.c_uint32), ("iteration", C.c_int32),
-        ("inject_actions", C.c_void_p), ("start_beliefs", C.c_void_p),
+        ("inject_actions", C.c_void_p), ("start_beliefs", C.c_void_p), ("search_key_dev", C.c_void_p),
+    ]
+
+
+class VpPlanArgs(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32), ("d_max_cap", C.c_int32), ("m", C.c_int32), ("use_graph", C.c_int32),
+        ("gamma", C.c_double),
+        ("particles_host", C.c_void_p), ("particles_dev", C.c_void_p),
+        ("cumw_host", C.c_void_p), ("cumw_dev", C.c_void_p),
+        ("keys_host", C.c_void_p), ("keys_dev", C.c_void_p),
+        ("out_host", C.c_void_p), ("out_dev", C.c_void_p),
     ]
 
 
@@ -94,6 +105,8 @@ _SIGNATURES = [
      [C.POINTER(VpModel), C.POINTER(VpWork), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]),
     ("vp_search", C.c_int32,
      [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpSearchArgs), C.c_void_p]),
+    ("vp_plan", C.c_int32,
+     [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpPlanArgs), C.c_void_p]),
     ("vp_backup", C.c_int32,
      [C.POINTER(VpTree), C.POINTER(VpWork), C.c_int32, C.c_int32, C.c_double, C.c_uint32, C.c_void_p]),
     ("vp_root_argmax", C.c_int32, [C.POINTER(VpTree), C.c_void_p, C.c_void_p]),
@@ -172,10 +185,12 @@ def layout_mismatches() -> list:
     lib.vp_abi_layout(buf, m)
     mine = [C.sizeof(VpModel), C.sizeof(VpTree), C.sizeof(VpWork), C.sizeof(VpSearchArgs),
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
-            VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16]
+            VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
+            VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
-             "vp_search_args.start_beliefs", "sizeof(Slot)"]
+             "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
+             "vp_tree.init_cdf"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

@@ -188,6 +188,35 @@ __device__ __forceinline__ u32 tile_lookback(u64* status, int tile, u32 agg, u32
   return excl;
 }
 
+// Warp-parallel variant (called by all 32 lanes of one warp): each round
+// inspects 32 predecessors at once, so a tile waits ~tiles/32 L2 round trips
+// instead of one per predecessor.
+__device__ __forceinline__ u32 tile_lookback_warp(u64* status, int tile, u32 agg, u32 epoch) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, tile == 0 ? kFlagInc : kFlagAgg, agg));
+  if (tile == 0) return 0;
+  u32 excl = 0;
+  int base = tile - 1;
+  while (true) {
+    const int j = base - lane;
+    const u64 s = j >= 0 ? ld_acquire_u64(&status[j]) : pack_status(epoch, kFlagInc, 0);
+    const bool valid = (u32)(s >> 32) == epoch;
+    const u32 inc = __ballot_sync(0xffffffffu, valid && ((s >> 30) & 3) == kFlagInc);
+    const u32 bad = __ballot_sync(0xffffffffu, !valid);
+    const int limit = inc ? __ffs(inc) - 1 : 31;
+    const u32 upto = limit == 31 ? 0xffffffffu : ((2u << limit) - 1u);
+    if (bad & upto) continue;  // a needed predecessor has not published yet
+    u32 v = lane <= limit ? (u32)(s & 0x3fffffffu) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, kFlagInc, excl + agg));
+  return excl;
+}
+
 // ---------------------------------------------------------------- numpy-order sums
 
 // numpy pairwise_sum for float64 (8 accumulators, 128-element blocks,

@@ -273,10 +273,11 @@ __global__ void k_rehash(vp_tree T) {
 // ------------------------------------------------------------------ root draw
 
 template <class Model>
-__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key) {
+__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key,
+                       const u64* key_dev) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= W.n) return;
-  const double u = uniform1(key, (u64)r);
+  const double u = uniform1(key_dev ? *key_dev : key, (u64)r);
   int lo = 0, hi = m;  // first index with cum > u  (searchsorted side=right)
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
@@ -335,7 +336,8 @@ __device__ __forceinline__ void step_and_claim(const vp_tree& T, const vp_model&
 // completion on a per-warp mbarrier), then every lane scans its own row.
 template <class Model, class PsiT>
 __global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S, int level,
-                                                      u64 lkey, u32 stamp, StageCfg sc) {
+                                                      u32 stamp, StageCfg sc) {
+  const u64 lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);  // search.py:107
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) u64 s_bar[4];
   const int n = W.n;
@@ -397,7 +399,8 @@ __global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_
 // fp64 parity mode: thread per row, numpy operation order, no staging.
 template <class Model>
 __global__ void __launch_bounds__(128) k_level_sample_exact(vp_tree T, vp_model M, vp_work W, vp_search_args S,
-                                                            int level, u64 lkey, u32 stamp) {
+                                                            int level, u32 stamp) {
+  const u64 lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);
   const int n = W.n;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = r < n;
@@ -454,8 +457,8 @@ __global__ void __launch_bounds__(VP_SCAN_TILE) k_assign(vp_tree T, vp_work W, i
     const u32 vi = warp_inclusive_scan(v);
     if (lane < NW) s_warp[lane] = vi - v;
     const u32 agg = __shfl_sync(FULL, vi, NW - 1);
+    const u32 excl = tile_lookback_warp(reinterpret_cast<u64*>(W.scan_status), tile, agg, epoch);
     if (lane == 0) {
-      const u32 excl = tile_lookback(reinterpret_cast<u64*>(W.scan_status), tile, agg, epoch);
       s_excl = excl;
       const int ntiles = (n + VP_SCAN_TILE - 1) / VP_SCAN_TILE;
       if (tile == ntiles - 1) {
@@ -516,6 +519,10 @@ __global__ void __launch_bounds__(128) k_accum_probe(vp_tree T, vp_work W, int l
     if (W.trace_anode) W.trace_anode[(size_t)level * n + r] = id;
   }
   const bool ok = active && id < T.cap_actions;
+  // claim (anode, obs) in hash_b first: it is the longest dependent chain
+  const u64 key = ((u64)(u32)id << 32) | o;
+  const u32 word = warp_claim(slots(T.hash_b), T.hmask_b, key, (u32)r, ok);
+  if (active) W.slot_b[r] = (int)word;
   // warp-aggregated reward / visit accumulation, lane (= row) order inside a group
   s_rew[threadIdx.x] = rw;
   __syncwarp();
@@ -537,9 +544,6 @@ __global__ void __launch_bounds__(128) k_accum_probe(vp_tree T, vp_work W, int l
       W.plist[(size_t)level * n + pos] = id;
     }
   }
-  const u64 key = ((u64)(u32)id << 32) | o;
-  const u32 word = warp_claim(slots(T.hash_b), T.hmask_b, key, (u32)r, ok);
-  if (active) W.slot_b[r] = (int)word;
 }
 
 // ------------------------------------------------------------------ leaves
@@ -726,6 +730,10 @@ __global__ void k_root_argmax(vp_tree T, int* out) {
   if (lane == 0) out[0] = arg < A ? arg : 0;
 }
 
+__global__ void k_copy_counters(vp_tree T, int* out) {
+  if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x];
+}
+
 // ------------------------------------------------------------------ test hooks
 
 __global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
@@ -897,6 +905,19 @@ static StageCfg stage_cfg(int A) {
 }
 
 template <class Model, class PsiT, bool Exact>
+static int32_t set_stage_attr(const vp_tree& T) {
+  if constexpr (!Exact) {
+    const StageCfg sc = stage_cfg<PsiT>(T.action_count);
+    const size_t smem = (size_t)4 * sc.rows * sc.stride * sizeof(PsiT);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+      return VP_ERR_CUDA;
+  }
+  return VP_OK;
+}
+
+template <class Model, class PsiT, bool Exact>
 static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                           cudaStream_t st) {
   const int n = W.n;
@@ -910,21 +931,18 @@ static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W,
   if constexpr (!Exact) {
     sc = stage_cfg<PsiT>(T.action_count);
     smem = (size_t)4 * sc.rows * sc.stride * sizeof(PsiT);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return VP_ERR_CUDA;
-      configured = smem;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      if (int32_t rc = set_stage_attr<Model, PsiT, Exact>(T)) return rc;
     }
   }
   for (int l = S.depth0; l < S.d_max; ++l) {
-    const u64 lkey = fold(S.search_key, (u64)l);
     const u32 stamp = S.stamp_base + (u32)l + 1u;
     {
       Launch L_(KK_LEVEL_SAMPLE, st);
-      if constexpr (Exact) k_level_sample_exact<Model><<<grid, 128, 0, st>>>(T, M, W, S, l, lkey, stamp);
-      else k_level_sample<Model, PsiT><<<grid, 128, smem, st>>>(T, M, W, S, l, lkey, stamp, sc);
+      if constexpr (Exact) k_level_sample_exact<Model><<<grid, 128, 0, st>>>(T, M, W, S, l, stamp);
+      else k_level_sample<Model, PsiT><<<grid, 128, smem, st>>>(T, M, W, S, l, stamp, sc);
     }
     { Launch L_(KK_ASSIGN_ACTIONS, st); k_assign<0><<<tiles, VP_SCAN_TILE, 0, st>>>(T, W, l, (u32)(2 * l + 1)); }
     { Launch L_(KK_ACCUM_PROBE, st); k_accum_probe<<<grid, 128, 0, st>>>(T, W, l, stamp); }
@@ -955,6 +973,132 @@ static int32_t run_backup(const vp_tree& T, const vp_work& W, int depth0, int dm
     { Launch L_(KK_BACKUP_Q, st); k_backup_q<PsiT><<<grid, 256, 0, st>>>(T, W, d - 1, gamma); }
     { Launch L_(KK_BACKUP_V, st); k_backup_v<PsiT, Exact><<<vgrid, 256, 0, st>>>(T, W, d - 1, d >= 2 ? recorded(d - 2) : -1); }
   }
+  return check_launch();
+}
+
+
+// Everything one fixed-iteration planning step does on the device, in stream
+// order: inputs H2D, fresh tree, per iteration {root draw, search, backup},
+// root argmax, counters, result D2H.
+template <class Model, class PsiT, bool Exact>
+static int32_t enqueue_plan(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
+                            cudaStream_t st) {
+  typedef typename Model::State State;
+  if (P.keys_host &&
+      cudaMemcpyAsync(P.keys_dev, P.keys_host, 16 * (size_t)P.iterations, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return VP_ERR_CUDA;
+  if (P.particles_host && cudaMemcpyAsync(P.particles_dev, P.particles_host, (size_t)P.m * sizeof(State),
+                                          cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return VP_ERR_CUDA;
+  if (P.cumw_host &&
+      cudaMemcpyAsync(P.cumw_dev, P.cumw_host, 8 * (size_t)P.m, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return VP_ERR_CUDA;
+  if (cudaMemsetAsync(T.hash_a, 0xff, (T.hmask_a + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
+  if (cudaMemsetAsync(T.hash_b, 0xff, (T.hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
+  { Launch L_(KK_TREE_INIT, st); k_tree_init<PsiT, Exact><<<1, 256, 0, st>>>(T); }
+  const u64* keys = reinterpret_cast<const u64*>(P.keys_dev);
+  int d = 1;
+  for (int it = 0; it < P.iterations; ++it) {
+    {
+      Launch L_(KK_DRAW, st);
+      k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(W, reinterpret_cast<const State*>(P.particles_dev),
+                                                         P.cumw_dev, P.m, 0ull, keys + 2 * it);
+    }
+    vp_search_args S;
+    memset(&S, 0, sizeof(S));
+    S.search_key_dev = P.keys_dev + 2 * it + 1;
+    S.depth0 = 0;
+    S.d_max = d;
+    S.stamp_base = (u32)it * (u32)(W.max_levels + 3);
+    S.iteration = it;
+    int32_t rc = run_search<Model, PsiT, Exact>(T, M, W, S, st);
+    if (rc) return rc;
+    rc = run_backup<PsiT, Exact>(T, W, 0, d, P.gamma, S.stamp_base, st);
+    if (rc) return rc;
+    d = std::min(d + 1, P.d_max_cap);
+  }
+  { Launch L_(KK_ARGMAX, st); k_root_argmax<PsiT><<<1, 32, 0, st>>>(T, P.out_dev); }
+  { Launch L_(KK_ARGMAX, st); k_copy_counters<<<1, 32, 0, st>>>(T, P.out_dev); }
+  if (P.out_host &&
+      cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return VP_ERR_CUDA;
+  return check_launch();
+}
+
+struct GraphEntry {
+  std::vector<unsigned char> key;
+  cudaGraphExec_t exec;
+  long long launches;
+  unsigned long long used;
+};
+static std::vector<GraphEntry> g_graphs;
+static unsigned long long g_graph_clock = 0;
+static cudaStream_t g_capture_stream = nullptr;
+
+template <class T>
+static void append_pod(std::vector<unsigned char>& v, const T& x) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&x);
+  v.insert(v.end(), p, p + sizeof(T));
+}
+
+template <class Model, class PsiT, bool Exact>
+static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
+                        cudaStream_t st) {
+  int32_t rc = set_stage_attr<Model, PsiT, Exact>(T);
+  if (rc) return rc;
+  if (!P.use_graph || g_prof_on) return enqueue_plan<Model, PsiT, Exact>(T, M, W, P, st);
+  std::vector<unsigned char> key;
+  append_pod(key, T);
+  append_pod(key, M);
+  append_pod(key, W);
+  append_pod(key, P);
+  const int budget = stage_budget_bytes();
+  append_pod(key, budget);
+  GraphEntry* hit = nullptr;
+  for (auto& e : g_graphs)
+    if (e.key == key) hit = &e;
+  if (!hit) {
+    if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return VP_ERR_CUDA;
+    // order the capture stream after the caller's pending work (e.g. init_prefs upload)
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(g_capture_stream, ev, 0);
+    cudaEventDestroy(ev);
+    cudaStreamSynchronize(g_capture_stream);
+    const long long l0 = g_launches;
+    if (cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return VP_ERR_CUDA;
+    rc = enqueue_plan<Model, PsiT, Exact>(T, M, W, P, g_capture_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(g_capture_stream, &graph);
+    const long long launches = g_launches - l0;
+    g_launches = l0;
+    if (rc || ce != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      g_last_cuda = ce;
+      return rc ? rc : VP_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      g_last_cuda = ie;
+      return VP_ERR_CUDA;
+    }
+    if (g_graphs.size() >= 16) {  // evict the least recently used graph
+      size_t lru = 0;
+      for (size_t i = 1; i < g_graphs.size(); ++i)
+        if (g_graphs[i].used < g_graphs[lru].used) lru = i;
+      cudaGraphExecDestroy(g_graphs[lru].exec);
+      g_graphs.erase(g_graphs.begin() + lru);
+    }
+    g_graphs.push_back(GraphEntry{key, exec, launches, 0});
+    hit = &g_graphs.back();
+  }
+  hit->used = ++g_graph_clock;
+  if (cudaGraphLaunch(hit->exec, st) != cudaSuccess) return check_launch();
+  g_launches += hit->launches;
   return check_launch();
 }
 
@@ -1021,7 +1165,10 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, eta),
                        (int32_t)offsetof(vp_work, trace_belief),
                        (int32_t)offsetof(vp_search_args, start_beliefs),
-                       (int32_t)sizeof(Slot)};
+                       (int32_t)sizeof(Slot),
+                       (int32_t)sizeof(vp_plan_args),
+                       (int32_t)offsetof(vp_plan_args, out_dev),
+                       (int32_t)offsetof(vp_tree, init_cdf)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];
@@ -1070,7 +1217,7 @@ int32_t vp_draw_root_states(const vp_model* m, const vp_work* w, const void* par
     if (!state_size_ok<Model>(*m)) return VP_ERR_INVALID;
     Launch L_(KK_DRAW, st);
     k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(
-        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key);
+        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key, nullptr);
     return check_launch();
   });
 }
@@ -1089,6 +1236,27 @@ int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const v
     if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
     return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
       return run_search<Model, decltype(z), decltype(ex)::value>(T, M, W, S, st);
+    });
+  });
+}
+
+int32_t vp_plan(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_plan_args* p, void* stream) {
+  if (!t || !m || !w || !p) return VP_ERR_INVALID;
+  if (p->iterations < 1 || p->d_max_cap < 1 || p->m < 1 || !p->keys_dev || !p->particles_dev || !p->cumw_dev ||
+      !p->out_dev)
+    return VP_ERR_INVALID;
+  if (std::min(p->iterations, p->d_max_cap) > w->max_levels) return VP_ERR_INVALID;
+  if (m->action_count != t->action_count) return VP_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_tree T = *t;
+  const vp_model M = *m;
+  const vp_work W = *w;
+  const vp_plan_args P = *p;
+  return dispatch_model(M.kind, [&](auto mdl) -> int32_t {
+    typedef decltype(mdl) Model;
+    if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
+    return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
+      return run_plan<Model, decltype(z), decltype(ex)::value>(T, M, W, P, st);
     });
   });
 }

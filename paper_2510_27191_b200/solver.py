@@ -106,6 +106,8 @@ class Planner:
         self.work: Workspace | None = None
         self._cap_cache = {}
         self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
+        self.use_graph = True
+        self._bufs = {}
 
     def _capacity(self, n: int, config, A: int):
         """Worst-case node counts for the whole plan, bounded by a memory budget."""
@@ -124,7 +126,7 @@ class Planner:
         budget = int(free * self.mem_fraction) // (per_belief + 48 + 64)
         return min(need, max(budget, 1 + n * levels)), levels
 
-    def prepare(self, model, config, trace: bool = False):
+    def prepare(self, model, config, trace: bool = False, device_init: bool = True):
         dm = device_model(model)
         A = model.spec.action_count
         n = config.n_parallel
@@ -142,29 +144,111 @@ class Planner:
                 t = self.tree = DeviceTree(A, init, eta=config.eta, precision=self.precision, exact=self.exact,
                                            cap_beliefs=cap, cap_actions=cap)
             else:
-                t.reset(init, config.eta)
+                t.reset(init, config.eta, device_init=device_init)
         w = self.work
         if w is None or not w.fits(n, levels, dm.state_bytes, trace):
             w = self.work = Workspace(n, levels, dm.state_bytes, trace)
         return dm, t, w
 
-    def upload_belief(self, dm, belief):
-        """Pack the particle StateBatch and copy it (and the weight CDF) to HBM."""
+    def _buf(self, name: str, nbytes: int, pinned: bool):
+        """Persistent (pinned host or device) byte buffers; stable pointers let
+        the captured CUDA graph of a planning step be replayed."""
         torch = _torch()
+        t = self._bufs.get(name)
+        if t is None or t.numel() < nbytes:
+            size = max(nbytes, 64)
+            t = torch.empty(size, dtype=torch.uint8, pin_memory=True) if pinned else \
+                torch.empty(size, dtype=torch.uint8, device="cuda")
+            self._bufs[name] = t
+        return t
+
+    def stage_belief(self, dm, belief):
+        """Pack the particle StateBatch and its weight CDF into pinned buffers."""
         weights = np.asarray(belief.weights, dtype=np.float64)
         rec = dm.pack(belief.states)
-        particles = torch.from_numpy(rec.view(np.uint8).reshape(-1)).pin_memory().cuda(non_blocking=True)
-        # sequential fp64 cumsum exactly as belief.py:42
-        cumw = torch.from_numpy(np.cumsum(weights)).pin_memory().cuda(non_blocking=True)
-        return particles, cumw, len(weights)
+        m = len(weights)
+        hp = self._buf("particles_host", rec.nbytes, True)
+        hp.numpy()[: rec.nbytes] = rec.view(np.uint8).reshape(-1)
+        hc = self._buf("cumw_host", 8 * m, True)
+        hc.numpy()[: 8 * m].view(np.float64)[:] = np.cumsum(weights)  # sequential fp64 (belief.py:42)
+        self._buf("particles_dev", rec.nbytes, False)
+        self._buf("cumw_dev", 8 * m, False)
+        return m
+
+    def upload_belief(self, dm, belief):
+        """Copy the belief to HBM now (for callers that keep it resident)."""
+        m = self.stage_belief(dm, belief)
+        nb = m * dm.state_bytes
+        pd, cd = self._bufs["particles_dev"], self._bufs["cumw_dev"]
+        pd[:nb].copy_(self._bufs["particles_host"][:nb], non_blocking=True)
+        cd[: 8 * m].copy_(self._bufs["cumw_host"][: 8 * m], non_blocking=True)
+        return pd, cd, m
 
     def plan(self, belief, model, config, rng, *, keep_tree: bool = False, inject_actions=None,
              trace: bool = False) -> PlanOutcome:
         _validate_config(config)
-        dm, tree, work = self.prepare(model, config, trace)
+        fixed = config.iterations is not None and inject_actions is None and not trace
+        dm, tree, work = self.prepare(model, config, trace, device_init=not fixed)
+        if fixed and not self.fits_fixed(tree, config):
+            tree.reset(tree.init_prefs, config.eta)  # device reset for the iterative path
+            fixed = False
+        if fixed:
+            m = self.stage_belief(dm, belief)
+            return self.run_fixed(dm, tree, work, m, model.spec, config, key_of(rng), from_host=True,
+                                  keep_tree=keep_tree)
         particles, cumw, m = self.upload_belief(dm, belief)
         return self.run(dm, tree, work, particles, cumw, m, model.spec, config, key_of(rng),
                         keep_tree=keep_tree, inject_actions=inject_actions, trace=trace)
+
+    @staticmethod
+    def fits_fixed(tree, config) -> bool:
+        """Whether the arena holds the worst case of a whole fixed-iteration plan."""
+        need = 1 + config.n_parallel * sum(min(i + 1, config.d_max_cap) for i in range(config.iterations))
+        return need <= tree.cap_beliefs and need <= tree.cap_actions
+
+    def run_fixed(self, dm, tree, work, m: int, spec, config, key: int, *, from_host: bool = True,
+                  keep_tree: bool = False) -> PlanOutcome:
+        """A fixed-iteration planning step as ONE vp_plan call (CUDA graph replay).
+
+        ``from_host``: copy the staged pinned belief inside the step (the e2e
+        path); otherwise the particles already resident in HBM are used.
+        """
+        torch = _torch()
+        iters = config.iterations
+        keys = np.empty(2 * iters, dtype=np.uint64)
+        for i in range(iters):
+            it_key = fold(key, i)
+            keys[2 * i] = fold(it_key, SITE_DRAW)
+            keys[2 * i + 1] = fold(it_key, SITE_SEARCH)
+        kh = self._buf("keys_host", 16 * iters, True)
+        kh.numpy()[: 16 * iters].view(np.uint64)[:] = keys
+        kd = self._buf("keys_dev", 16 * iters, False)
+        oh = self._buf("out_host", 16, True)
+        od = self._buf("out_dev", 16, False)
+        if not self.fits_fixed(tree, config):
+            raise _lib.CapacityError("tree arena smaller than the plan's worst case; use Planner.run")
+        a = _lib.VpPlanArgs()
+        a.iterations, a.d_max_cap, a.m, a.use_graph = iters, config.d_max_cap, m, int(self.use_graph)
+        a.gamma = float(spec.discount)
+        a.particles_host = self._bufs["particles_host"].data_ptr() if from_host else None
+        a.particles_dev = self._bufs["particles_dev"].data_ptr()
+        a.cumw_host = self._bufs["cumw_host"].data_ptr() if from_host else None
+        a.cumw_dev = self._bufs["cumw_dev"].data_ptr()
+        a.keys_host, a.keys_dev = kh.data_ptr(), kd.data_ptr()
+        a.out_host, a.out_dev = oh.data_ptr(), od.data_ptr()
+        stream = torch.cuda.current_stream()
+        _lib.call("vp_plan", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(a),
+                  stream.cuda_stream)
+        stream.synchronize()
+        tree._stamp_cursor = iters * (work.max_levels + 3)
+        chosen, nb, na, overflow = (int(v) for v in oh.numpy()[:16].view(np.int32))
+        if overflow:
+            raise _lib.CapacityError("device tree overflowed its arena during plan()")
+        held = tree if keep_tree else TreeHandle(tree)
+        if keep_tree:
+            self.tree = None
+        d_final = min(iters, config.d_max_cap)
+        return PlanOutcome(chosen, iters, d_final, {"belief_rows": nb, "action_rows": na}, held, None)
 
     def run(self, dm, tree, work, particles, cumw, m: int, spec, config, key: int, *, keep_tree: bool = False,
             inject_actions=None, trace: bool = False) -> PlanOutcome:

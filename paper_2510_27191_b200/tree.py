@@ -139,8 +139,11 @@ class DeviceTree:
         self.eta = float(eta)
         self.struct.eta = self.eta
 
-    def reset(self, init_prefs=None, eta: float | None = None):
-        """Fresh tree (tree.py:103-132): root row, no actions, init PSI row."""
+    def reset(self, init_prefs=None, eta: float | None = None, device_init: bool = True):
+        """Fresh tree (tree.py:103-132): root row, no actions, init PSI row.
+
+        ``device_init=False`` leaves the device-side reset to a following
+        ``vp_plan`` call (which starts every planning step with it)."""
         torch = _torch()
         if eta is not None:
             self.set_eta(eta)
@@ -148,12 +151,14 @@ class DeviceTree:
         base = np.zeros(A) if init_prefs is None else np.asarray(init_prefs, dtype=np.float64)
         if base.shape != (A,) or not np.all(np.isfinite(base)):
             raise ValueError("init_prefs must be a finite vector of length |A|")
+        if getattr(self, "init_prefs", None) is None or not np.array_equal(self.init_prefs, base):
+            self._init_prefs.copy_(torch.from_numpy(base))
         self.init_prefs = base
-        self._init_prefs.copy_(torch.from_numpy(base))
         self.generation += 1
         self._stamp_cursor = 0
         self.last_search = None
-        _lib.call("vp_tree_init", C.byref(self.struct), _stream())
+        if device_init:
+            _lib.call("vp_tree_init", C.byref(self.struct), _stream())
 
     def counts(self):
         """(n_beliefs, n_actions, overflow) -- synchronises the stream."""
