@@ -152,15 +152,17 @@ typedef struct vp_search_args {
 } vp_search_args;
 
 /* A whole fixed-iteration planning step (solver.py:79-113) enqueued by one
- * call; with use_graph it is captured once into a CUDA graph and replayed
- * (re-captured whenever a pointer / size / model parameter changes).  Host
- * buffers must be pinned; the caller synchronises the stream and then reads
+ * call.  mode 2 (default): one persistent cooperative kernel with grid
+ * barriers between phases; mode 1: one launch per phase, captured once into
+ * a CUDA graph and replayed (re-captured when a pointer / size / model
+ * parameter changes); mode 0: one launch per phase.  Host buffers must be
+ * pinned; the caller synchronises the stream and then reads
  * out_host = {chosen action, n_beliefs, n_actions, overflow}. */
 typedef struct vp_plan_args {
   int32_t iterations;          /* fixed-iteration budget (>= 1)             */
   int32_t d_max_cap;
   int32_t m;                   /* particles                                 */
-  int32_t use_graph;
+  int32_t mode;                /* 0 kernels, 1 CUDA graph, 2 persistent     */
   double gamma;
   const void* particles_host;  /* [m * state_bytes] pinned, or NULL         */
   void* particles_dev;
@@ -184,8 +186,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n);
 /* ---- measurement -------------------------------------------------------- */
 /* Kernel kinds, in order: draw, level_sample, assign_actions, accum_probe,
  * assign_beliefs, leaf, backup_leaves, backup_q, backup_v, parent_lists,
- * argmax, tree_init, rehash. */
-#define VP_KERNEL_KINDS 13
+ * argmax, tree_init, rehash, plan (persistent kernel). */
+#define VP_KERNEL_KINDS 14
 /* on != 0: clear and start recording a CUDA-event pair around every launch. */
 int32_t vp_profile_enable(int32_t on);
 /* Sum recorded durations (ms) and launch counts per kind; returns #kinds. */

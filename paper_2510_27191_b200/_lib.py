@@ -80,7 +80,7 @@ class VpSearchArgs(C.Structure):
 
 class VpPlanArgs(C.Structure):
     _fields_ = [
-        ("iterations", C.c_int32), ("d_max_cap", C.c_int32), ("m", C.c_int32), ("use_graph", C.c_int32),
+        ("iterations", C.c_int32), ("d_max_cap", C.c_int32), ("m", C.c_int32), ("mode", C.c_int32),
         ("gamma", C.c_double),
         ("particles_host", C.c_void_p), ("particles_dev", C.c_void_p),
         ("cumw_host", C.c_void_p), ("cumw_dev", C.c_void_p),
@@ -126,7 +126,7 @@ _SIGNATURES = [
 EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)
 
 KERNEL_KINDS = ("draw", "level_sample", "assign_actions", "accum_probe", "assign_beliefs", "leaf",
-                "backup_leaves", "backup_q", "backup_v", "parent_lists", "argmax", "tree_init", "rehash")
+                "backup_leaves", "backup_q", "backup_v", "parent_lists", "argmax", "tree_init", "rehash", "plan")
 
 
 def profile_enable(on: bool):

@@ -1,257 +1,40 @@
 // vp_kernels.cu -- B200 (sm_100a) kernels of the PORPP planning step and the
 // C ABI declared in include/vpb200.h.
 //
-// One search level (search.py:106-118) is four launches over the n rows:
-//   K1 level_sample   : frontier belief -> softmax draw -> G(s,a) -> claim (b,a)
-//   K2 assign_actions : first-occurrence scan -> new action ids (tree.py:180-218)
-//   K3 accum_probe    : reward/visit accumulation, claim (anode, o)
-//   K4 assign_beliefs : first-occurrence scan -> new belief rows (tree.py:220-256)
-// The backup (backup.py:75-114) is one pass over the leaf list and two
-// launches per level over the per-level distinct lists recorded by search:
-//   Q / PSI scatter over the level's action nodes, LSE over its beliefs.
-// Nothing here is a dense contraction: every kernel is HBM / latency bound.
-//
-// PSI rows are created lazily: a new belief only gets a "fresh" flag (its row
-// equals the initial row); the sampler draws fresh beliefs from one shared
-// initial CDF, and the backup materialises a row the first time it updates it.
+// Two execution paths share the phase functions of vp_phases.cuh:
+//  * vp_plan: ONE persistent cooperative kernel per planning step
+//    (solver.py:79-113): tree reset, and per iteration the root draw, the
+//    d_max search levels and the d_max backup levels, separated by grid
+//    barriers.  Rows waiting for a node id published by the preceding
+//    numbering phase spin on the hash slot instead of taking a barrier, so a
+//    search level costs two grid barriers.
+//  * the API kernels (vp_search / vp_backup / hooks): one launch per phase.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
-#include <cstddef>
 #include <cstring>
-#include <cfloat>
 #include <type_traits>
-#include <algorithm>
 #include <vector>
 
 #include "vp_common.cuh"
 #include "vp_models.cuh"
+#include "vp_phases.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace vp {
 
 static thread_local cudaError_t g_last_cuda = cudaSuccess;
 
-constexpr float kLog2e = 1.4426950408889634f;
-
-__device__ __forceinline__ Slot* slots(void* p) { return reinterpret_cast<Slot*>(p); }
-
-// ------------------------------------------------------------------ exp helpers (fast mode)
-// The fast sampler and the fast LSE evaluate exp(eta * psi - shift) as
-// exp2(fma(eta*log2e, psi, -shift*log2e)); float uses ex2.approx, double exp2.
-__device__ __forceinline__ float fexp2(float x) { return exp2f(x); }
-__device__ __forceinline__ double fexp2(double x) { return exp2(x); }
-__device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-__device__ __forceinline__ double ffma(double a, double b, double c) { return __fma_rn(a, b, c); }
-
-// ------------------------------------------------------------------ LSE
-
-// Fast LSE: warp per row, max then sum of exp (backup.py:34-41 formula).
-template <class PsiT>
-__device__ double warp_lse_fast(const PsiT* row, int A, double eta) {
-  typedef PsiT CT;
-  const int lane = lane_id();
-  const CT e = (CT)eta;
-  CT m = -(CT)INFINITY;
-  for (int a = lane; a < A; a += 32) {
-    const CT z = e * row[a];
-    m = z > m ? z : m;
-  }
-  m = warp_max(m);
-  const CT e2 = (CT)(eta * 1.4426950408889634), m2 = m * (CT)1.4426950408889634;
-  CT s = 0;
-  for (int a = lane; a < A; a += 32) s += fexp2(ffma(e2, row[a], -m2));
-  s = warp_sum(s);
-  return (double)m / eta + log((double)s) / eta;
-}
-
-// numpy-order LSE for the fp64 parity mode: m/eta + log(pairwise sum)/eta.
-__device__ double lse_exact(const double* row, int A, double eta) {
-  double m = -INFINITY;
-  for (int a = 0; a < A; ++a) m = fmax(m, eta * row[a]);
-  auto ex = [&](int a) -> double { return exp(eta * row[a] - m); };
-  const double s = pairwise_sum(ex, 0, A);
-  return m / eta + log(s) / eta;
-}
-
-// ------------------------------------------------------------------ categorical draws
-
-// numpy-order inverse CDF draw (search.py:46-54 then 77-79, 83).
-__device__ int sample_exact(const double* row, int A, double eta, double u) {
-  double m = -INFINITY;
-  for (int a = 0; a < A; ++a) m = fmax(m, eta * row[a]);
-  auto ex = [&](int a) -> double { return exp(eta * row[a] - m); };
-  const double s = pairwise_sum(ex, 0, A);
-  double cum = 0.0;
-  for (int a = 0; a < A; ++a) {
-    const double p = ex(a) / s;
-    cum = a ? cum + p : p;
-    if (cum > u) return a;
-  }
-  return A - 1;
-}
-
-// Fast draw: the probabilities are exp(eta (psi - LSE)), normalised by the
-// row's cached LSE, accumulated left to right until the running sum exceeds u
-// (clamp |A|-1, search.py:83).  The scalar and the vectorised (staged shared
-// memory) versions perform the identical floating-point sequence.
-template <class CT>
-__device__ __forceinline__ int scan_cdf_scalar(const CT* row, int A, CT e2, CT sh2, CT u) {
-  CT cum = 0;
-  for (int a = 0; a < A; ++a) {
-    cum += fexp2(ffma(e2, row[a], -sh2));
-    if (cum > u) return a;
-  }
-  return A - 1;
-}
-template <class CT>
-struct Vec16;
-template <>
-struct Vec16<float> {
-  typedef float4 T;
-  static constexpr int N = 4;
-  static __device__ __forceinline__ void get(const T& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-};
-template <>
-struct Vec16<double> {
-  typedef double2 T;
-  static constexpr int N = 2;
-  static __device__ __forceinline__ void get(const T& v, double* o) { o[0] = v.x; o[1] = v.y; }
-};
-template <class CT>
-__device__ __forceinline__ int scan_cdf_vec(const CT* row, int A, CT e2, CT sh2, CT u) {
-  typedef Vec16<CT> V;
-  CT cum = 0;
-  const typename V::T* rv = reinterpret_cast<const typename V::T*>(row);
-  for (int a0 = 0; a0 < A; a0 += V::N) {
-    CT x[V::N];
-    V::get(rv[a0 / V::N], x);
-#pragma unroll
-    for (int j = 0; j < V::N; ++j) {
-      if (a0 + j < A) {
-        cum += fexp2(ffma(e2, x[j], -sh2));
-        if (cum > u) return a0 + j;
-      }
-    }
-  }
-  return A - 1;
-}
-// First index whose (initial-row) CDF value exceeds u.
-template <class CT>
-__device__ __forceinline__ int search_cdf(const CT* cdf, int A, CT u) {
-  int lo = 0, hi = A;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cdf[mid] > u) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo < A ? lo : A - 1;
-}
-
-// ------------------------------------------------------------------ TMA bulk staging
-
-__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-
-// ------------------------------------------------------------------ warp helpers
-
-// Warp-aggregated probe/claim: lanes with equal keys elect their lowest lane
-// (= smallest row, rows are contiguous per warp) to touch the table once.
-__device__ __forceinline__ u32 warp_claim(Slot* tab, u64 mask, u64 key, u32 row, bool active) {
-  const u32 grp = __match_any_sync(FULL, active ? key : kEmptyKey);
-  const int leader = __ffs(grp) - 1;
-  u32 word = 0;
-  if (active && lane_id() == leader) {
-    bool existing;
-    u32 id;
-    const u32 s = probe_claim(tab, mask, key, row, existing, id);
-    word = s | (existing ? kExistBit : 0u);
-  }
-  return __shfl_sync(FULL, word, leader);
-}
-
-// Dedup into a per-level list via per-node stamps (one stamp per level).
-__device__ __forceinline__ void warp_list_once(u32* stamp, int node, u32 value, bool active, int* count,
-                                               int* list) {
-  const u32 grp = __match_any_sync(FULL, active ? (u32)node : 0xffffffffu);
-  const int leader = __ffs(grp) - 1;
-  if (active && lane_id() == leader) {
-    if (atomicExch(&stamp[node], value) != value) {
-      const int pos = atomicAdd(count, 1);
-      list[pos] = node;
-    }
-  }
-}
-
-// Write the initial PSI row into belief b if it is still lazily fresh.
-template <class PsiT>
-__device__ __forceinline__ void warp_materialise(const vp_tree& T, int b) {
-  if (!(T.b_flags[b] & 1)) return;
-  PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
-  for (int a = lane_id(); a < T.action_count; a += 32) row[a] = (PsiT)T.init_prefs[a];
-  __syncwarp();
-  if (lane_id() == 0) T.b_flags[b] = 0;
-}
-
-// ------------------------------------------------------------------ tree init / rehash
+// ================================================================== standalone kernels (API path)
 
 template <class PsiT, bool Exact>
 __global__ void k_tree_init(vp_tree T) {
-  PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-  const int A = T.action_count;
-  for (int a = threadIdx.x; a < A; a += blockDim.x) psi[a] = (PsiT)T.init_prefs[a];
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v;
-    if constexpr (Exact) {
-      v = 0.0;
-      if (threadIdx.x == 0) v = lse_exact(reinterpret_cast<const double*>(psi), A, T.eta);
-    } else {
-      v = warp_lse_fast<PsiT>(psi, A, T.eta);
-    }
-    if (threadIdx.x == 0) {
-      T.init_lse[0] = v;
-      T.b_lse[0] = v;
-      // CDF of the initial row with the sampler's exact arithmetic
-      PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
-      const PsiT e2 = (PsiT)(T.eta * 1.4426950408889634), sh2 = (PsiT)(T.eta * v * 1.4426950408889634);
-      PsiT cum = 0;
-      for (int a = 0; a < A; ++a) {
-        cum += fexp2(ffma(e2, psi[a], -sh2));
-        cdf[a] = cum;
-      }
-      T.b_parent_action[0] = -1;
-      T.b_parent_obs[0] = 0xffffffffu;
-      T.b_depth[0] = 0;
-      T.b_value[0] = 0.0;
-      T.b_weight[0] = 0.0;
-      T.b_stamp[0] = 0;
-      T.b_flags[0] = 0;
-      T.counters[0] = 1;
-      T.counters[1] = 0;
-      T.counters[2] = 0;
-    }
-  }
+  block_tree_init<PsiT, Exact>(T);
 }
 
 __global__ void k_rehash(vp_tree T) {
@@ -270,529 +53,184 @@ __global__ void k_rehash(vp_tree T) {
   }
 }
 
-// ------------------------------------------------------------------ root draw
-
 template <class Model>
 __global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key,
                        const u64* key_dev) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= W.n) return;
-  const double u = uniform1(key_dev ? *key_dev : key, (u64)r);
-  int lo = 0, hi = m;  // first index with cum > u  (searchsorted side=right)
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cumw[mid] > u) hi = mid;
-    else lo = mid + 1;
-  }
-  const int idx = lo < m - 1 ? lo : m - 1;
-  reinterpret_cast<typename Model::State*>(W.states)[r] = particles[idx];
+  phase_draw<Model>(W, particles, cumw, m, key_dev ? *key_dev : key, this_span());
 }
 
-// ------------------------------------------------------------------ K1 level_sample
-
-struct StageCfg {
-  int rows;     // G: PSI rows staged per warp per batch
-  int stride;   // staged row stride in PsiT elements (odd multiple of 16 bytes)
-};
-
-// Frontier belief of row r at `level` (hash_b slot written by K3 of level-1).
-__device__ __forceinline__ int frontier_of(const vp_tree& T, const vp_work& W, const vp_search_args& S, int level,
-                                           int r) {
-  if (level == S.depth0) return S.start_beliefs ? S.start_beliefs[r] : 0;
-  const u32 sl = (u32)W.slot_b[r] & ~kExistBit;
-  const int b = (int)slots(T.hash_b)[sl].id;
-  if (W.trace_belief) W.trace_belief[(size_t)(level - 1) * W.n + r] = b;
-  return b;
+__device__ __forceinline__ LevelArgs level_args(const vp_search_args& S, int level, u32 stamp) {
+  LevelArgs L;
+  L.level = level;
+  L.depth0 = S.depth0;
+  L.lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);  // search.py:107
+  L.stamp = stamp;
+  L.inject = S.inject_actions;
+  L.start = S.start_beliefs;
+  return L;
 }
 
-// Model step + claim of (b, a) in hash_a; shared tail of both K1 variants.
-template <class Model>
-__device__ __forceinline__ void step_and_claim(const vp_tree& T, const vp_model& M, const vp_work& W, int level,
-                                               u64 lkey, int r, bool active, int b, int a) {
-  const int n = W.n;
-  u64 key = 0;
-  if (active) {
-    typename Model::State st = reinterpret_cast<typename Model::State*>(W.states)[r];
-    u32 o;
-    double rw;
-    Model::step(M, st, a, fold(lkey, 1), (u64)r, o, rw);  // level_rng.derive(1) (search.py:113-115)
-    reinterpret_cast<typename Model::State*>(W.states)[r] = st;
-    W.obs[r] = o;
-    W.reward[r] = rw;
-    W.action[r] = a;
-    if (W.trace_action) {
-      W.trace_action[(size_t)level * n + r] = a;
-      W.trace_obs[(size_t)level * n + r] = o;
-    }
-    key = ((u64)(u32)b << 32) | (u32)a;
-  }
-  const u32 word = warp_claim(slots(T.hash_a), T.hmask_a, key, (u32)r, active);
-  if (active) W.slot_a[r] = (int)word;
-}
-
-// Fast mode (fp32 or fp64 PSI).  Rows of the warp whose belief is fresh draw
-// from the shared initial CDF; the distinct non-fresh beliefs' PSI rows are
-// staged into shared memory with TMA bulk copies (one cp.async.bulk per row,
-// completion on a per-warp mbarrier), then every lane scans its own row.
-template <class Model, class PsiT>
-__global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S, int level,
-                                                      u32 stamp, StageCfg sc) {
-  const u64 lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);  // search.py:107
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) u64 s_bar[4];
-  const int n = W.n;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = r < n;
-  const int A = T.action_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level] = T.counters[1];
-  u64* bar = &s_bar[warp];
-  if (lane == 0) {
-    mbar_init(bar, 1);
+template <class PsiT>
+__device__ __forceinline__ Stage<PsiT> make_stage(unsigned char* smem, u64* bars, StageCfg cfg) {
+  const int warp = threadIdx.x >> 5;
+  Stage<PsiT> sg;
+  sg.buf = reinterpret_cast<PsiT*>(smem) + (size_t)warp * cfg.rows * cfg.stride;
+  sg.bar = &bars[warp];
+  sg.phase = 0;
+  sg.cfg = cfg;
+  if (lane_id() == 0) {
+    mbar_init(sg.bar, 1);
     fence_mbar_init();
   }
   __syncwarp();
-
-  const int b = active ? frontier_of(T, W, S, level, r) : 0;
-  warp_list_once(T.b_stamp, b, stamp, active, &W.fcount[level], W.flist + (size_t)level * n);
-  const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;  // level_rng.derive(0) (search.py:110)
-
-  int a = 0;
-  if (S.inject_actions) {
-    a = active ? S.inject_actions[(size_t)level * n + r] : 0;
-  } else {
-    const bool fresh = active && (T.b_flags[b] & 1);
-    const bool need = active && !fresh;
-    if (fresh) a = search_cdf(reinterpret_cast<const PsiT*>(T.init_cdf), A, (PsiT)u);
-    const u32 grp = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
-    const int my_leader = __ffs(grp) - 1;
-    const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
-    const int K = __popc(leaders);
-    const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-    const double lse = need ? T.b_lse[b] : 0.0;
-    const PsiT e2 = (PsiT)(T.eta * 1.4426950408889634), sh2 = (PsiT)(T.eta * lse * 1.4426950408889634);
-    PsiT* stage = reinterpret_cast<PsiT*>(smem_raw) + (size_t)warp * sc.rows * sc.stride;
-    const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
-    const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
-    u32 phase = 0;
-    u32 pending = leaders;
-    for (int s0 = 0; s0 < K; s0 += sc.rows) {
-      const int cnt = min(sc.rows, K - s0);
-      fence_async_smem();
-      if (lane == 0) mbar_expect_tx(bar, row_bytes * (u32)cnt);
-      __syncwarp();
-      // the j-th pending leader copies its belief's row into stage slot j
-      const bool copier = need && lane == my_leader && my_slot >= s0 && my_slot < s0 + cnt;
-      if (copier) bulk_g2s(stage + (size_t)(my_slot - s0) * sc.stride, psi + (size_t)b * T.psi_stride, row_bytes,
-                           bar);
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      if (need && my_slot >= s0 && my_slot < s0 + cnt)
-        a = scan_cdf_vec<PsiT>(stage + (size_t)(my_slot - s0) * sc.stride, A, e2, sh2, (PsiT)u);
-      __syncwarp();
-    }
-    (void)pending;
-  }
-  step_and_claim<Model>(T, M, W, level, lkey, r, active, b, a);
+  return sg;
 }
 
-// fp64 parity mode: thread per row, numpy operation order, no staging.
+template <class Model, class PsiT>
+__global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S, int level,
+                                                      u32 stamp, StageCfg sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) u64 s_bar[4];
+  Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, sc);
+  phase_sample_fast<Model, PsiT>(T, M, W, level_args(S, level, stamp), sg, this_span());
+}
+
 template <class Model>
 __global__ void __launch_bounds__(128) k_level_sample_exact(vp_tree T, vp_model M, vp_work W, vp_search_args S,
                                                             int level, u32 stamp) {
-  const u64 lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);
-  const int n = W.n;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = r < n;
-  const int A = T.action_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level] = T.counters[1];
-  const int b = active ? frontier_of(T, W, S, level, r) : 0;
-  warp_list_once(T.b_stamp, b, stamp, active, &W.fcount[level], W.flist + (size_t)level * n);
-  const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;
-  int a = 0;
-  if (active) {
-    if (S.inject_actions) {
-      a = S.inject_actions[(size_t)level * n + r];
-    } else {
-      const double* row = (T.b_flags[b] & 1) ? T.init_prefs
-                                             : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
-      a = sample_exact(row, A, T.eta, u);
-    }
-  }
-  step_and_claim<Model>(T, M, W, level, lkey, r, active, b, a);
+  phase_sample_exact<Model>(T, M, W, level_args(S, level, stamp), this_span());
 }
 
-// ------------------------------------------------------------------ K2/K4 first-occurrence scans
-
-// Number the rows that won their key this level, in row order (one row per
-// thread, one tile per block, tiles chained by decoupled look-back), and
-// write the new nodes' columns.  WhichTable: 0 = actions, 1 = beliefs.
 template <int WhichTable>
 __global__ void __launch_bounds__(VP_SCAN_TILE) k_assign(vp_tree T, vp_work W, int level, u32 epoch) {
-  __shared__ u32 s_tile;
-  __shared__ u32 s_warp[VP_SCAN_TILE / 32];
-  __shared__ u32 s_excl;
-  constexpr int NW = VP_SCAN_TILE / 32;
-  const int n = W.n;
-  Slot* tab = slots(WhichTable ? T.hash_b : T.hash_a);
-  const int* slot_of = WhichTable ? W.slot_b : W.slot_a;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&W.scan_ticket[0], 1u);
-  __syncthreads();
-  const int tile = (int)s_tile;
-  const int r = tile * VP_SCAN_TILE + threadIdx.x;
-  u32 sl = 0;
-  bool win = false;
-  if (r < n) {
-    const u32 w = (u32)slot_of[r];
-    sl = w & ~kExistBit;
-    if (!(w & kExistBit)) win = ld_volatile_u32(&tab[sl].id) == (kPending | (u32)r);
-  }
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const u32 ballot = __ballot_sync(FULL, win);
-  const u32 below = __popc(ballot & ((1u << lane) - 1u));
-  if (lane == 0) s_warp[warp] = __popc(ballot);
-  __syncthreads();
-  if (warp == 0) {
-    const u32 v = lane < NW ? s_warp[lane] : 0;
-    const u32 vi = warp_inclusive_scan(v);
-    if (lane < NW) s_warp[lane] = vi - v;
-    const u32 agg = __shfl_sync(FULL, vi, NW - 1);
-    const u32 excl = tile_lookback_warp(reinterpret_cast<u64*>(W.scan_status), tile, agg, epoch);
-    if (lane == 0) {
-      s_excl = excl;
-      const int ntiles = (n + VP_SCAN_TILE - 1) / VP_SCAN_TILE;
-      if (tile == ntiles - 1) {
-        const int base = W.level_base[2 * level + WhichTable];
-        T.counters[WhichTable ? 0 : 1] = base + (int)(excl + agg);
-        W.scan_ticket[0] = 0;
-      }
-    }
-  }
-  __syncthreads();
-  if (!win) return;
-  const int id = W.level_base[2 * level + WhichTable] + (int)(s_excl + s_warp[warp] + below);
-  Slot& s = tab[sl];
-  s.id = (u32)id;
-  const int cap = WhichTable ? T.cap_beliefs : T.cap_actions;
-  if (id >= cap) {
-    T.counters[2] = 1;  // overflow: the host fails the plan loudly
-    return;
-  }
-  const u64 key = s.key;
-  if (WhichTable == 0) {
-    T.a_parent_belief[id] = (int)(key >> 32);
-    T.a_action[id] = (int)(u32)key;
-    T.a_reward[id] = 0.0;
-    T.a_visits[id] = 0;
-    T.a_num[id] = 0.0;
-    T.a_den[id] = 0.0;
-    T.a_stamp[id] = 0;
-  } else {
-    const int pa = (int)(key >> 32);
-    T.b_parent_action[id] = pa;
-    T.b_parent_obs[id] = (u32)key;
-    T.b_depth[id] = T.b_depth[T.a_parent_belief[pa]] + 1;
-    T.b_lse[id] = T.init_lse[0];
-    T.b_value[id] = 0.0;
-    T.b_weight[id] = 0.0;
-    T.b_stamp[id] = 0;
-    T.b_flags[id] = 1;  // PSI row lazily equal to the initial row (tree.py:253)
-  }
+  phase_assign<WhichTable>(T, W, level, epoch, W.scan_ticket);
 }
-
-// ------------------------------------------------------------------ K3 accum_probe
 
 __global__ void __launch_bounds__(128) k_accum_probe(vp_tree T, vp_work W, int level, u32 stamp) {
-  __shared__ double s_rew[128];
-  const int n = W.n;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = r < n;
-  if (blockIdx.x == 0 && threadIdx.x == 0) W.level_base[2 * level + 1] = T.counters[0];
-  int id = 0;
-  double rw = 0.0;
-  u32 o = 0;
-  if (active) {
-    const u32 sl = (u32)W.slot_a[r] & ~kExistBit;
-    id = (int)slots(T.hash_a)[sl].id;
-    rw = W.reward[r];
-    o = W.obs[r];
-    if (W.trace_anode) W.trace_anode[(size_t)level * n + r] = id;
-  }
-  const bool ok = active && id < T.cap_actions;
-  // claim (anode, obs) in hash_b first: it is the longest dependent chain
-  const u64 key = ((u64)(u32)id << 32) | o;
-  const u32 word = warp_claim(slots(T.hash_b), T.hmask_b, key, (u32)r, ok);
-  if (active) W.slot_b[r] = (int)word;
-  // warp-aggregated reward / visit accumulation, lane (= row) order inside a group
-  s_rew[threadIdx.x] = rw;
-  __syncwarp();
-  const u32 grp = __match_any_sync(FULL, ok ? (u32)id : 0xffffffffu);
-  const int leader = __ffs(grp) - 1;
-  if (ok && lane_id() == leader) {
-    double sum = 0.0;
-    u32 g = grp;
-    const int wbase = threadIdx.x & ~31;
-    while (g) {
-      const int l2 = __ffs(g) - 1;
-      g &= g - 1;
-      sum += s_rew[wbase + l2];
-    }
-    atomicAdd(&T.a_reward[id], sum);
-    atomicAdd(&T.a_visits[id], __popc(grp));
-    if (atomicExch(&T.a_stamp[id], stamp) != stamp) {
-      const int pos = atomicAdd(&W.pcount[level], 1);
-      W.plist[(size_t)level * n + pos] = id;
-    }
-  }
+  phase_accum(T, W, level, stamp, this_span());
 }
-
-// ------------------------------------------------------------------ leaves
 
 template <class Model>
 __global__ void __launch_bounds__(128) k_leaf(vp_tree T, vp_model M, vp_work W, vp_search_args S, int dmax,
                                               u32 stamp) {
-  __shared__ double s_h[128];
-  const int n = W.n;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = r < n;
-  int b = 0;
-  double h = 0.0;
-  if (active) {
-    b = frontier_of(T, W, S, dmax, r);
-    h = Model::heuristic(M, reinterpret_cast<const typename Model::State*>(W.states)[r]);
-    W.leaf_belief[r] = b;
-    W.leaf_value[r] = h;
-  }
-  const bool ok = active && b < T.cap_beliefs;
-  warp_list_once(T.b_stamp, b, stamp, ok, &W.fcount[dmax], W.flist + (size_t)dmax * n);
-  s_h[threadIdx.x] = h;
-  __syncwarp();
-  const u32 grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
-  const int leader = __ffs(grp) - 1;
-  if (ok && lane_id() == leader) {
-    double sum = 0.0;
-    u32 g = grp;
-    const int wbase = threadIdx.x & ~31;
-    while (g) {
-      const int l2 = __ffs(g) - 1;
-      g &= g - 1;
-      sum += s_h[wbase + l2];
-    }
-    atomicAdd(&T.b_weight[b], (double)__popc(grp));
-    atomicAdd(&T.b_value[b], sum);
-  }
+  phase_leaf<Model>(T, M, W, level_args(S, dmax, stamp), this_span());
 }
 
-// ------------------------------------------------------------------ backup
-
-// Leaves: V = mean heuristic, N = batch count (backup.py:44-51, 82-87), then
-// feed the parent action's visit-weighted child mean (backup.py:64-68).
-// Warps with spare work materialise the fresh PSI rows of level `mat`
-// (the parents the next launch updates).
 template <class PsiT>
 __global__ void k_backup_leaves(vp_tree T, vp_work W, int dmax, int mat) {
-  const int cnt = W.fcount[dmax];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int b = W.flist[(size_t)dmax * W.n + i];
-    const double w = T.b_weight[b];
-    const double v = T.b_value[b] / w;
-    T.b_value[b] = 0.0;
-    T.b_weight[b] = 0.0;
-    const int pa = T.b_parent_action[b];
-    if (pa >= 0) {
-      atomicAdd(&T.a_num[pa], v * w);
-      atomicAdd(&T.a_den[pa], w);
-    }
-  }
-  if (mat >= 0) {
-    const int mc = W.fcount[mat];
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
-  }
+  phase_backup_leaves<PsiT>(T, W, dmax, mat, this_span());
 }
 
 template <class PsiT>
 __global__ void k_materialise(vp_tree T, vp_work W, int lvl) {
-  const int mc = W.fcount[lvl];
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)lvl * W.n + i]);
+  phase_materialise<PsiT>(T, W, lvl, this_span());
 }
 
-// Level d: actions of level d-1 -> Q -> PSI[b, a] += Q - LSE_pre(b)
-// (backup.py:96-108); N(b) += lifetime visits (backup.py:110-114).
 template <class PsiT>
 __global__ void k_backup_q(vp_tree T, vp_work W, int lvl, double gamma) {
-  const int cnt = W.pcount[lvl];
-  PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int a = W.plist[(size_t)lvl * W.n + i];
-    const double vis = (double)T.a_visits[a];
-    const double q = T.a_reward[a] / vis + (gamma * T.a_num[a]) / T.a_den[a];
-    T.a_num[a] = 0.0;
-    T.a_den[a] = 0.0;
-    const int b = T.a_parent_belief[a];
-    PsiT* cell = psi + (size_t)b * T.psi_stride + T.a_action[a];
-    *cell = (PsiT)((double)*cell + (q - T.b_lse[b]));
-    atomicAdd(&T.b_weight[b], vis);
-  }
+  phase_backup_q<PsiT>(T, W, lvl, gamma, this_span());
 }
 
-// Level d: beliefs of level d-1 -> V = LSE_post (backup.py:109), cached as
-// the next LSE_pre, then their own parent action's child mean (level d-1);
-// spare warps materialise the fresh rows of level `mat` = d-2.
 template <class PsiT, bool Exact>
 __global__ void k_backup_v(vp_tree T, vp_work W, int lvl, int mat) {
-  const int cnt = W.fcount[lvl];
-  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
-  const int A = T.action_count;
-  const int lane = lane_id();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  if constexpr (Exact) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-      const int b = W.flist[(size_t)lvl * W.n + i];
-      const double v = lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta);
-      T.b_lse[b] = v;
-      const double w = T.b_weight[b];
-      T.b_weight[b] = 0.0;
-      const int pa = T.b_parent_action[b];
-      if (pa >= 0) {
-        atomicAdd(&T.a_num[pa], v * w);
-        atomicAdd(&T.a_den[pa], w);
-      }
-    }
-  } else {
-    for (int i = gw; i < cnt; i += nw) {
-      const int b = W.flist[(size_t)lvl * W.n + i];
-      const double v = warp_lse_fast<PsiT>(psi + (size_t)b * T.psi_stride, A, T.eta);
-      if (lane == 0) {
-        T.b_lse[b] = v;
-        const double w = T.b_weight[b];
-        T.b_weight[b] = 0.0;
-        const int pa = T.b_parent_action[b];
-        if (pa >= 0) {
-          atomicAdd(&T.a_num[pa], v * w);
-          atomicAdd(&T.a_den[pa], w);
-        }
-      }
-    }
-  }
-  if (mat >= 0) {
-    const int mc = W.fcount[mat];
-    for (int i = gw; i < mc; i += nw) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
-  }
+  phase_backup_v<PsiT, Exact>(T, W, lvl, mat, this_span());
 }
 
-// Levels at or above the search start depth have no recorded lists: derive
-// them from the valued children (backup.py:90-95): P_{d-1} = distinct parent
-// actions of F_d, F_{d-1} = their distinct parent beliefs.
 __global__ void k_parent_lists(vp_tree T, vp_work W, int d, u32 stamp) {
-  const int cnt = W.fcount[d];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int b = W.flist[(size_t)d * W.n + i];
-    const int pa = T.b_parent_action[b];
-    if (pa < 0) continue;
-    if (atomicExch(&T.a_stamp[pa], stamp) != stamp) {
-      const int pos = atomicAdd(&W.pcount[d - 1], 1);
-      W.plist[(size_t)(d - 1) * W.n + pos] = pa;
-      const int pb = T.a_parent_belief[pa];
-      if (atomicExch(&T.b_stamp[pb], stamp) != stamp) {
-        const int q = atomicAdd(&W.fcount[d - 1], 1);
-        W.flist[(size_t)(d - 1) * W.n + q] = pb;
-      }
-    }
-  }
+  phase_parent_lists(T, W, d, stamp, this_span());
 }
 
 template <class PsiT>
 __global__ void k_root_argmax(vp_tree T, int* out) {
-  const PsiT* row = reinterpret_cast<const PsiT*>(T.psi);
-  const int A = T.action_count;
-  const int lane = lane_id();
-  PsiT best = -(PsiT)INFINITY;
-  int arg = A;
-  for (int a = lane; a < A; a += 32) {
-    const PsiT v = row[a];
-    if (v > best) {
-      best = v;
-      arg = a;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const PsiT vb = __shfl_xor_sync(FULL, best, o);
-    const int ab = __shfl_xor_sync(FULL, arg, o);
-    if (vb > best || (vb == best && ab < arg)) {
-      best = vb;
-      arg = ab;
-    }
-  }
-  if (lane == 0) out[0] = arg < A ? arg : 0;
+  warp_root_argmax<PsiT>(T, out);
 }
 
 __global__ void k_copy_counters(vp_tree T, int* out) {
   if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x];
 }
 
-// ------------------------------------------------------------------ test hooks
+// ================================================================== persistent planning kernel
 
-__global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const u64 r = (u64)rows[i];
-  if (k <= 0) out[i] = uniform1(key, r);
-  else
-    for (int j = 1; j <= k; ++j) out[i * k + (j - 1)] = uniform_j(key, r, (u64)j);
-}
-__global__ void k_rng_normal(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const u64 r = (u64)rows[i];
-  if (k <= 0) out[i] = normal_j(key, r, 0);
-  else
-    for (int j = 1; j <= k; ++j) out[i * k + (j - 1)] = normal_j(key, r, (u64)j);
-}
-template <class Model>
-__global__ void k_model_step(vp_model M, typename Model::State* st, const int32_t* act, u64 key,
-                             const int64_t* rows, int n, u32* obs, double* rew) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  typename Model::State s = st[i];
-  u32 o;
-  double r;
-  Model::step(M, s, act[i], key, (u64)rows[i], o, r);
-  st[i] = s;
-  obs[i] = o;
-  rew[i] = r;
-}
-template <class Model>
-__global__ void k_model_heur(vp_model M, const typename Model::State* st, int n, double* out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  out[i] = Model::heuristic(M, st[i]);
-}
-template <class PsiT, bool Exact>
-__global__ void k_lse_rows(const PsiT* rows, int count, int width, double eta, double* out) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= count) return;
-  if constexpr (Exact) {
-    if (lane_id() == 0) out[gw] = lse_exact(reinterpret_cast<const double*>(rows) + (size_t)gw * width, width, eta);
-  } else {
-    const double v = warp_lse_fast<PsiT>(rows + (size_t)gw * width, width, eta);
-    if (lane_id() == 0) out[gw] = v;
+struct PlanParams {
+  vp_tree T;
+  vp_model M;
+  vp_work W;
+  int iterations, d_max_cap, m;
+  double gamma;
+  const void* particles;
+  const double* cumw;
+  const u64* keys;  // [2 * iterations]: (draw key, search key) per iteration
+  int* out;         // [4]
+  StageCfg sc;
+};
+
+// One whole fixed-iteration planning step.  Barrier pattern per iteration
+// with d = d_max:  draw | A(0) | B(0) C(0) | D(0) A(1) | ... | D(d-1) leaf |
+// backup leaves | (Q | V |) x d, where B/D number new nodes, C/A(next)/leaf
+// spin on the ids they publish, and Q/V are the backup's action and belief
+// halves of each level.
+template <class Model, class PsiT, bool Exact>
+__global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) u64 s_bar[kStageWarps];
+  cg::grid_group grid = cg::this_grid();
+  const vp_tree& T = P.T;
+  const vp_work& W = P.W;
+  const Span sp = this_span();
+  const int L = W.max_levels;
+  Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, P.sc);
+  typedef typename Model::State State;
+
+  if (blockIdx.x == 0) block_tree_init<PsiT, Exact>(T);
+  int d = 1;
+  for (int it = 0; it < P.iterations; ++it) {
+    const u32 stamp_base = (u32)it * (u32)(L + 3);
+    const u64 skey = P.keys[2 * it + 1];
+    if (sp.gtid <= d) W.fcount[sp.gtid] = 0;
+    if (sp.gtid < d) W.pcount[sp.gtid] = 0;
+    phase_draw<Model>(W, reinterpret_cast<const State*>(P.particles), P.cumw, P.m, P.keys[2 * it], sp);
+    grid.sync();
+    for (int l = 0; l < d; ++l) {
+      LevelArgs la;
+      la.level = l;
+      la.depth0 = 0;
+      la.lkey = fold(skey, (u64)l);
+      la.stamp = stamp_base + (u32)l + 1u;
+      la.inject = nullptr;
+      la.start = nullptr;
+      const u32 epoch = 1u + 2u * ((u32)it * (u32)(L + 1) + (u32)l);
+      if constexpr (Exact) phase_sample_exact<Model>(T, P.M, W, la, sp);
+      else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, sp);
+      grid.sync();
+      phase_assign<0>(T, W, l, epoch, nullptr);
+      phase_accum(T, W, l, la.stamp, sp);
+      grid.sync();
+      phase_assign<1>(T, W, l, epoch + 1u, nullptr);
+    }
+    {
+      LevelArgs la;
+      la.level = d;
+      la.depth0 = 0;
+      la.lkey = 0;
+      la.stamp = stamp_base + (u32)d + 1u;
+      la.inject = nullptr;
+      la.start = nullptr;
+      phase_leaf<Model>(T, P.M, W, la, sp);
+    }
+    grid.sync();
+    phase_backup_leaves<PsiT>(T, W, d, d - 1, sp);
+    grid.sync();
+    for (int lv = d - 1; lv >= 0; --lv) {
+      phase_backup_q<PsiT>(T, W, lv, P.gamma, sp);
+      grid.sync();
+      phase_backup_v<PsiT, Exact>(T, W, lv, lv - 1, sp);
+      grid.sync();
+    }
+    d = d + 1 < P.d_max_cap ? d + 1 : P.d_max_cap;
   }
-}
-template <class PsiT, bool Exact>
-__global__ void k_sample_rows(const PsiT* rows, int width, double eta, const double* lse, const int32_t* group,
-                              const double* u, int n, int32_t* out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int g = group[i];
-  if constexpr (Exact) {
-    out[i] = sample_exact(reinterpret_cast<const double*>(rows) + (size_t)g * width, width, eta, u[i]);
-  } else {
-    const PsiT e2 = (PsiT)(eta * 1.4426950408889634), sh2 = (PsiT)(eta * lse[g] * 1.4426950408889634);
-    out[i] = scan_cdf_scalar<PsiT>(rows + (size_t)g * width, width, e2, sh2, (PsiT)u[i]);
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    warp_root_argmax<PsiT>(T, P.out);
+    if (threadIdx.x < 3) P.out[1 + threadIdx.x] = T.counters[threadIdx.x];
   }
 }
 
@@ -812,7 +250,7 @@ static int32_t check_launch() {
 // ---- per-launch accounting: launch counter + optional CUDA-event timing by kernel kind
 enum KernelKind {
   KK_DRAW = 0, KK_LEVEL_SAMPLE, KK_ASSIGN_ACTIONS, KK_ACCUM_PROBE, KK_ASSIGN_BELIEFS, KK_LEAF,
-  KK_BACKUP_LEAVES, KK_BACKUP_Q, KK_BACKUP_V, KK_PARENT_LISTS, KK_ARGMAX, KK_TREE_INIT, KK_REHASH, KK_COUNT
+  KK_BACKUP_LEAVES, KK_BACKUP_Q, KK_BACKUP_V, KK_PARENT_LISTS, KK_ARGMAX, KK_TREE_INIT, KK_REHASH, KK_PLAN, KK_COUNT
 };
 struct ProfRec {
   int kind;
@@ -882,37 +320,37 @@ static bool state_size_ok(const vp_model& M) {
   return M.state_bytes == (int)sizeof(typename Model::State);
 }
 
-static int stage_budget_bytes() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("VP_STAGE_KB");
-    v = (e ? atoi(e) : 200) * 1024;
-    if (v < 16 * 1024) v = 16 * 1024;
-    if (v > 220 * 1024) v = 220 * 1024;
-  }
-  return v;
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
+// Staged-row geometry: rows padded to an odd number of 16-B chunks so the
+// LDS.128 scans of 8 lanes in different rows hit different bank groups.
 template <class PsiT>
-static StageCfg stage_cfg(int A) {
+static StageCfg stage_cfg(int A, int warps, int budget_bytes) {
   int chunks = (int)(((size_t)A * sizeof(PsiT) + 15) / 16);
-  if ((chunks & 1) == 0) ++chunks;  // odd number of 16-B chunks: conflict-free LDS.128 across rows
+  if ((chunks & 1) == 0) ++chunks;
   StageCfg c;
   c.stride = chunks * 16 / (int)sizeof(PsiT);
-  const int per_warp = stage_budget_bytes() / 4;
-  c.rows = std::max(1, std::min(32, per_warp / (chunks * 16)));
+  c.rows = std::max(1, std::min(32, budget_bytes / warps / (chunks * 16)));
   return c;
+}
+template <class PsiT>
+static size_t stage_bytes(const StageCfg& c, int warps) {
+  return (size_t)warps * c.rows * c.stride * sizeof(PsiT);
 }
 
 template <class Model, class PsiT, bool Exact>
-static int32_t set_stage_attr(const vp_tree& T) {
+static int32_t set_sample_attr(size_t smem) {
   if constexpr (!Exact) {
-    const StageCfg sc = stage_cfg<PsiT>(T.action_count);
-    const size_t smem = (size_t)4 * sc.rows * sc.stride * sizeof(PsiT);
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-      return VP_ERR_CUDA;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      if (cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return VP_ERR_CUDA;
+      configured = smem;
+    }
   }
   return VP_OK;
 }
@@ -926,16 +364,13 @@ static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W,
   if (cudaMemsetAsync(W.fcount, 0, sizeof(int32_t) * (W.max_levels + 1), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(W.pcount, 0, sizeof(int32_t) * W.max_levels, st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * tiles, st) != cudaSuccess) return VP_ERR_CUDA;
+  if (cudaMemsetAsync(W.scan_ticket, 0, sizeof(uint32_t), st) != cudaSuccess) return VP_ERR_CUDA;
   StageCfg sc{0, 0};
   size_t smem = 0;
   if constexpr (!Exact) {
-    sc = stage_cfg<PsiT>(T.action_count);
-    smem = (size_t)4 * sc.rows * sc.stride * sizeof(PsiT);
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs == cudaStreamCaptureStatusNone) {
-      if (int32_t rc = set_stage_attr<Model, PsiT, Exact>(T)) return rc;
-    }
+    sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
+    smem = stage_bytes<PsiT>(sc, 4);
+    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   for (int l = S.depth0; l < S.d_max; ++l) {
     const u32 stamp = S.stamp_base + (u32)l + 1u;
@@ -976,13 +411,11 @@ static int32_t run_backup(const vp_tree& T, const vp_work& W, int depth0, int dm
   return check_launch();
 }
 
+// ---- whole planning step
 
-// Everything one fixed-iteration planning step does on the device, in stream
-// order: inputs H2D, fresh tree, per iteration {root draw, search, backup},
-// root argmax, counters, result D2H.
 template <class Model, class PsiT, bool Exact>
-static int32_t enqueue_plan(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
-                            cudaStream_t st) {
+static int32_t enqueue_inputs(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
+                              cudaStream_t st) {
   typedef typename Model::State State;
   if (P.keys_host &&
       cudaMemcpyAsync(P.keys_dev, P.keys_host, 16 * (size_t)P.iterations, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -995,10 +428,20 @@ static int32_t enqueue_plan(const vp_tree& T, const vp_model& M, const vp_work& 
     return VP_ERR_CUDA;
   if (cudaMemsetAsync(T.hash_a, 0xff, (T.hmask_a + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(T.hash_b, 0xff, (T.hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
+  return VP_OK;
+}
+
+// Multi-kernel version of a planning step (one launch per phase).
+template <class Model, class PsiT, bool Exact>
+static int32_t enqueue_plan_kernels(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
+                                    cudaStream_t st) {
+  typedef typename Model::State State;
+  if (int32_t rc = enqueue_inputs<Model, PsiT, Exact>(T, M, W, P, st)) return rc;
   { Launch L_(KK_TREE_INIT, st); k_tree_init<PsiT, Exact><<<1, 256, 0, st>>>(T); }
   const u64* keys = reinterpret_cast<const u64*>(P.keys_dev);
   int d = 1;
   for (int it = 0; it < P.iterations; ++it) {
+    // the API kernels read the keys from device memory via search_key_dev
     {
       Launch L_(KK_DRAW, st);
       k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(W, reinterpret_cast<const State*>(P.particles_dev),
@@ -1007,7 +450,6 @@ static int32_t enqueue_plan(const vp_tree& T, const vp_model& M, const vp_work& 
     vp_search_args S;
     memset(&S, 0, sizeof(S));
     S.search_key_dev = P.keys_dev + 2 * it + 1;
-    S.depth0 = 0;
     S.d_max = d;
     S.stamp_base = (u32)it * (u32)(W.max_levels + 3);
     S.iteration = it;
@@ -1019,6 +461,57 @@ static int32_t enqueue_plan(const vp_tree& T, const vp_model& M, const vp_work& 
   }
   { Launch L_(KK_ARGMAX, st); k_root_argmax<PsiT><<<1, 32, 0, st>>>(T, P.out_dev); }
   { Launch L_(KK_ARGMAX, st); k_copy_counters<<<1, 32, 0, st>>>(T, P.out_dev); }
+  if (P.out_host &&
+      cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return VP_ERR_CUDA;
+  return check_launch();
+}
+
+static int g_num_sms = 0;
+
+// Persistent version: inputs, tree reset, ONE cooperative kernel, result.
+template <class Model, class PsiT, bool Exact>
+static int32_t enqueue_plan_persistent(const vp_tree& T, const vp_model& M, const vp_work& W,
+                                       const vp_plan_args& P, cudaStream_t st) {
+  if (int32_t rc = enqueue_inputs<Model, PsiT, Exact>(T, M, W, P, st)) return rc;
+  const int tiles = blocks_for(W.n, VP_SCAN_TILE);
+  if (cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * tiles, st) != cudaSuccess) return VP_ERR_CUDA;
+  PlanParams pp;
+  pp.T = T;
+  pp.M = M;
+  pp.W = W;
+  pp.iterations = P.iterations;
+  pp.d_max_cap = P.d_max_cap;
+  pp.m = P.m;
+  pp.gamma = P.gamma;
+  pp.particles = P.particles_dev;
+  pp.cumw = P.cumw_dev;
+  pp.keys = reinterpret_cast<const u64*>(P.keys_dev);
+  pp.out = P.out_dev;
+  pp.sc = Exact ? StageCfg{1, 4} : stage_cfg<PsiT>(T.action_count, kStageWarps, env_int("VP_PLAN_STAGE_KB", 96) * 1024);
+  const size_t smem = Exact ? 16 : stage_bytes<PsiT>(pp.sc, kStageWarps);
+  auto kern = k_plan<Model, PsiT, Exact>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return check_launch();
+    configured = smem;
+  }
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageWarps * 32, smem) != cudaSuccess ||
+      per_sm < 1)
+    return check_launch();
+  per_sm = std::min(per_sm, env_int("VP_PLAN_BLOCKS_PER_SM", 4));
+  const int need = blocks_for(W.n, kStageWarps * 32);
+  const int grid = std::max(1, std::min(g_num_sms * per_sm, std::max(need, g_num_sms)));
+  void* args[] = {&pp};
+  {
+    Launch L_(KK_PLAN, st);
+    if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kStageWarps * 32), args, smem, st) !=
+        cudaSuccess)
+      return check_launch();
+  }
   if (P.out_host &&
       cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return VP_ERR_CUDA;
@@ -1041,18 +534,23 @@ static void append_pod(std::vector<unsigned char>& v, const T& x) {
   v.insert(v.end(), p, p + sizeof(T));
 }
 
+// mode 0: multi-kernel direct; 1: multi-kernel captured into a CUDA graph
+// (replayed while pointers / sizes / model are unchanged); 2: persistent.
 template <class Model, class PsiT, bool Exact>
 static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
                         cudaStream_t st) {
-  int32_t rc = set_stage_attr<Model, PsiT, Exact>(T);
-  if (rc) return rc;
-  if (!P.use_graph || g_prof_on) return enqueue_plan<Model, PsiT, Exact>(T, M, W, P, st);
+  if (P.mode == 2) return enqueue_plan_persistent<Model, PsiT, Exact>(T, M, W, P, st);
+  if constexpr (!Exact) {
+    const StageCfg sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
+    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(stage_bytes<PsiT>(sc, 4))) return rc;
+  }
+  if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);
   std::vector<unsigned char> key;
   append_pod(key, T);
   append_pod(key, M);
   append_pod(key, W);
   append_pod(key, P);
-  const int budget = stage_budget_bytes();
+  const int budget = env_int("VP_STAGE_KB", 200);
   append_pod(key, budget);
   GraphEntry* hit = nullptr;
   for (auto& e : g_graphs)
@@ -1060,7 +558,6 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   if (!hit) {
     if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
       return VP_ERR_CUDA;
-    // order the capture stream after the caller's pending work (e.g. init_prefs upload)
     cudaEvent_t ev;
     cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     cudaEventRecord(ev, st);
@@ -1069,7 +566,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
     cudaStreamSynchronize(g_capture_stream);
     const long long l0 = g_launches;
     if (cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return VP_ERR_CUDA;
-    rc = enqueue_plan<Model, PsiT, Exact>(T, M, W, P, g_capture_stream);
+    int32_t rc = enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, g_capture_stream);
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(g_capture_stream, &graph);
     const long long launches = g_launches - l0;
@@ -1086,7 +583,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
       g_last_cuda = ie;
       return VP_ERR_CUDA;
     }
-    if (g_graphs.size() >= 16) {  // evict the least recently used graph
+    if (g_graphs.size() >= 16) {
       size_t lru = 0;
       for (size_t i = 1; i < g_graphs.size(); ++i)
         if (g_graphs[i].used < g_graphs[lru].used) lru = i;
@@ -1100,6 +597,68 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   if (cudaGraphLaunch(hit->exec, st) != cudaSuccess) return check_launch();
   g_launches += hit->launches;
   return check_launch();
+}
+
+// ---- test-hook kernels
+
+__global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 r = (u64)rows[i];
+  if (k <= 0) out[i] = uniform1(key, r);
+  else
+    for (int j = 1; j <= k; ++j) out[i * k + (j - 1)] = uniform_j(key, r, (u64)j);
+}
+__global__ void k_rng_normal(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 r = (u64)rows[i];
+  if (k <= 0) out[i] = normal_j(key, r, 0);
+  else
+    for (int j = 1; j <= k; ++j) out[i * k + (j - 1)] = normal_j(key, r, (u64)j);
+}
+template <class Model>
+__global__ void k_model_step(vp_model M, typename Model::State* st, const int32_t* act, u64 key,
+                             const int64_t* rows, int n, u32* obs, double* rew) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  typename Model::State s = st[i];
+  u32 o;
+  double r;
+  Model::step(M, s, act[i], key, (u64)rows[i], o, r);
+  st[i] = s;
+  obs[i] = o;
+  rew[i] = r;
+}
+template <class Model>
+__global__ void k_model_heur(vp_model M, const typename Model::State* st, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = Model::heuristic(M, st[i]);
+}
+template <class PsiT, bool Exact>
+__global__ void k_lse_rows(const PsiT* rows, int count, int width, double eta, double* out) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= count) return;
+  if constexpr (Exact) {
+    if (lane_id() == 0) out[gw] = lse_exact(reinterpret_cast<const double*>(rows) + (size_t)gw * width, width, eta);
+  } else {
+    const double v = warp_lse_fast<PsiT>(rows + (size_t)gw * width, width, eta);
+    if (lane_id() == 0) out[gw] = v;
+  }
+}
+template <class PsiT, bool Exact>
+__global__ void k_sample_rows(const PsiT* rows, int width, double eta, const double* lse, const int32_t* group,
+                              const double* u, int n, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int g = group[i];
+  if constexpr (Exact) {
+    out[i] = sample_exact(reinterpret_cast<const double*>(rows) + (size_t)g * width, width, eta, u[i]);
+  } else {
+    const PsiT e2 = (PsiT)(eta * kLog2eD), sh2 = (PsiT)(eta * lse[g] * kLog2eD);
+    out[i] = scan_cdf_scalar<PsiT>(rows + (size_t)g * width, width, e2, sh2, (PsiT)u[i]);
+  }
 }
 
 }  // namespace vp

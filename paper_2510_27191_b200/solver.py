@@ -106,7 +106,7 @@ class Planner:
         self.work: Workspace | None = None
         self._cap_cache = {}
         self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
-        self.use_graph = True
+        self.mode = 2  # vp_plan: 2 persistent kernel, 1 CUDA graph of per-phase kernels, 0 direct
         self._bufs = {}
 
     def _capacity(self, n: int, config, A: int):
@@ -228,7 +228,7 @@ class Planner:
         if not self.fits_fixed(tree, config):
             raise _lib.CapacityError("tree arena smaller than the plan's worst case; use Planner.run")
         a = _lib.VpPlanArgs()
-        a.iterations, a.d_max_cap, a.m, a.use_graph = iters, config.d_max_cap, m, int(self.use_graph)
+        a.iterations, a.d_max_cap, a.m, a.mode = iters, config.d_max_cap, m, int(self.mode)
         a.gamma = float(spec.discount)
         a.particles_host = self._bufs["particles_host"].data_ptr() if from_host else None
         a.particles_dev = self._bufs["particles_dev"].data_ptr()

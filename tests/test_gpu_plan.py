@@ -217,3 +217,46 @@ def test_fast_sampler_draws_follow_softmax_of_tree(kind, n_par, precision):
         total += n_par
         belief_ids = tr["next_beliefs"]
     assert mism <= max(3, 1e-3 * total)
+
+
+@pytest.mark.parametrize("name", ["plan_mars7_8_c1", "plan_tiger", "plan_lightdark"])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_vp_plan_modes_reproduce_reference(name, mode):
+    """The persistent kernel (mode 2), the CUDA-graph replay (1) and direct
+    per-phase launches (0) all reproduce the reference tree in fp64 parity
+    mode; the second run of each planner replays with new keys/particles."""
+    case = manifest()["plans"][name]
+    g = load(name)
+    planner = vp.Planner("fp64", exact=True)
+    planner.mode = mode
+    for run in case["runs"]:
+        s = run["seed"]
+        om, belief, cfg, rng = plan_inputs(case, s)
+        out = planner.plan(belief, om, cfg, rng, keep_tree=True)
+        assert out.tree_stats == run["tree_stats"]
+        assert out.chosen_action == run["chosen_action"]
+        t = out.tree.tables()
+        for k in INT_COLUMNS:
+            np.testing.assert_array_equal(t[k], g[f"s{s}_{k}"].astype(np.int64), err_msg=k)
+        np.testing.assert_allclose(t["prefs"].sum(axis=1), g[f"s{s}_prefs_row_sum"], rtol=1e-9, atol=1e-8)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_fp32_modes_agree(mode):
+    """fp32 fast path: the three vp_plan modes give the same tree structure
+    (identical draws; only fp64 atomic summation order may differ)."""
+    om = oracle.MarsModel(11, 11, layout_seed=5)
+    belief = oracle.ParticleBelief.from_model(om, 4000, oracle.RowRng.from_seed(5).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=8192, iterations=6)
+    rng = oracle.RowRng.from_seed(5).derive(1, 0)
+    base = vp.Planner("fp32")
+    base.mode = 0
+    want = base.plan(belief, om, cfg, rng, keep_tree=True)
+    p = vp.Planner("fp32")
+    p.mode = mode
+    got = p.plan(belief, om, cfg, rng, keep_tree=True)
+    assert got.tree_stats == want.tree_stats
+    a, b = got.tree.tables(), want.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    assert scale_close(a["prefs"], b["prefs"], 1e-5)
