@@ -222,28 +222,65 @@ __device__ __forceinline__ u32 tile_lookback_warp(u64* status, int tile, u32 agg
 // numpy pairwise_sum for float64 (8 accumulators, 128-element blocks,
 // recursive halving rounded to a multiple of 8), over f(lo..lo+n).
 template <class F>
-__device__ double pairwise_sum(const F& f, int lo, int n) {
+__device__ __forceinline__ double pairwise_leaf(const F& f, int lo, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r += f(lo + i);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] += f(lo + i + j);
-    }
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += f(lo + i);
-    return res;
+    for (int j = 0; j < 8; ++j) r[j] += f(lo + i + j);
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return pairwise_sum(f, lo, n2) + pairwise_sum(f, lo + n2, n - n2);
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += f(lo + i);
+  return res;
+}
+
+// The recursion of numpy's pairwise_sum, evaluated with an explicit stack
+// (post-order: left half, right half, add) so the frame size is static.
+template <class F>
+__device__ double pairwise_sum(const F& f, int lo, int n) {
+  if (n <= 128) return pairwise_leaf(f, lo, n);
+  int s_lo[24], s_n[24], s_state[24];
+  double s_left[24];
+  int sp = 0;
+  s_lo[0] = lo;
+  s_n[0] = n;
+  s_state[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    const int cl = s_lo[sp], cn = s_n[sp];
+    if (cn <= 128) {
+      ret = pairwise_leaf(f, cl, cn);
+      --sp;
+      continue;
+    }
+    int n2 = cn / 2;
+    n2 -= n2 % 8;
+    if (s_state[sp] == 0) {
+      s_state[sp] = 1;
+      ++sp;
+      s_lo[sp] = cl;
+      s_n[sp] = n2;
+      s_state[sp] = 0;
+    } else if (s_state[sp] == 1) {
+      s_left[sp] = ret;
+      s_state[sp] = 2;
+      ++sp;
+      s_lo[sp] = cl + n2;
+      s_n[sp] = cn - n2;
+      s_state[sp] = 0;
+    } else {
+      ret = s_left[sp] + ret;
+      --sp;
+    }
+  }
+  return ret;
 }
 
 }  // namespace vp
