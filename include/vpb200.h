@@ -172,6 +172,9 @@ typedef struct vp_plan_args {
   uint64_t* keys_dev;
   int32_t* out_host;           /* [4] pinned                                */
   int32_t* out_dev;            /* [4]                                       */
+  uint64_t* timeline_dev;      /* mode 2 diagnostics: globaltimer stamp per  */
+  int32_t timeline_cap;        /* phase boundary (NULL / 0 = off)           */
+  int32_t pad0;
 } vp_plan_args;
 
 /* ---- library ---------------------------------------------------------- */

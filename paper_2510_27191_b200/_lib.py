@@ -86,6 +86,7 @@ class VpPlanArgs(C.Structure):
         ("cumw_host", C.c_void_p), ("cumw_dev", C.c_void_p),
         ("keys_host", C.c_void_p), ("keys_dev", C.c_void_p),
         ("out_host", C.c_void_p), ("out_dev", C.c_void_p),
+        ("timeline_dev", C.c_void_p), ("timeline_cap", C.c_int32), ("pad0", C.c_int32),
     ]
 
 

@@ -162,7 +162,15 @@ struct PlanParams {
   const u64* keys;  // [2 * iterations]: (draw key, search key) per iteration
   int* out;         // [4]
   StageCfg sc;
+  u64* timeline;    // optional: globaltimer at each phase boundary (block 0)
+  int timeline_cap;
 };
+
+__device__ __forceinline__ u64 global_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // One whole fixed-iteration planning step.  Barrier pattern per iteration
 // with d = d_max:  draw | A(0) | B(0) C(0) | D(0) A(1) | ... | D(d-1) leaf |
@@ -181,6 +189,11 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
   Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, P.sc);
   typedef typename Model::State State;
 
+  int tl = 0;
+  auto mark = [&]() {
+    if (P.timeline && blockIdx.x == 0 && threadIdx.x == 0 && tl < P.timeline_cap) P.timeline[tl++] = global_ns();
+  };
+  mark();
   if (blockIdx.x == 0) block_tree_init<PsiT, Exact>(T);
   int d = 1;
   for (int it = 0; it < P.iterations; ++it) {
@@ -190,6 +203,7 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
     if (sp.gtid < d) W.pcount[sp.gtid] = 0;
     phase_draw<Model>(W, reinterpret_cast<const State*>(P.particles), P.cumw, P.m, P.keys[2 * it], sp);
     grid.sync();
+    mark();
     for (int l = 0; l < d; ++l) {
       LevelArgs la;
       la.level = l;
@@ -202,9 +216,11 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
       if constexpr (Exact) phase_sample_exact<Model>(T, P.M, W, la, sp);
       else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, sp);
       grid.sync();
+      mark();
       phase_assign<0>(T, W, l, epoch, nullptr);
       phase_accum(T, W, l, la.stamp, sp);
       grid.sync();
+      mark();
       phase_assign<1>(T, W, l, epoch + 1u, nullptr);
     }
     {
@@ -218,13 +234,17 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
       phase_leaf<Model>(T, P.M, W, la, sp);
     }
     grid.sync();
+    mark();
     phase_backup_leaves<PsiT>(T, W, d, d - 1, sp);
     grid.sync();
+    mark();
     for (int lv = d - 1; lv >= 0; --lv) {
       phase_backup_q<PsiT>(T, W, lv, P.gamma, sp);
       grid.sync();
+      mark();
       phase_backup_v<PsiT, Exact>(T, W, lv, lv - 1, sp);
       grid.sync();
+      mark();
     }
     d = d + 1 < P.d_max_cap ? d + 1 : P.d_max_cap;
   }
@@ -488,6 +508,8 @@ static int32_t enqueue_plan_persistent(const vp_tree& T, const vp_model& M, cons
   pp.cumw = P.cumw_dev;
   pp.keys = reinterpret_cast<const u64*>(P.keys_dev);
   pp.out = P.out_dev;
+  pp.timeline = reinterpret_cast<u64*>(P.timeline_dev);
+  pp.timeline_cap = P.timeline_cap;
   pp.sc = Exact ? StageCfg{1, 4} : stage_cfg<PsiT>(T.action_count, kStageWarps, env_int("VP_PLAN_STAGE_KB", 96) * 1024);
   const size_t smem = Exact ? 16 : stage_bytes<PsiT>(pp.sc, kStageWarps);
   auto kern = k_plan<Model, PsiT, Exact>;
