@@ -29,12 +29,16 @@ struct Span {
   int gtid, gthreads;  // thread index / count
   int gwarp, gwarps;   // warp index / count
 };
+// Warps are numbered block-fastest (warp w of block b is global warp
+// w * gridDim + b) so that consecutive 32-row chunks land on different SMs
+// even when a phase has far fewer chunks than the grid has warps; lanes stay
+// contiguous, so thread-granular loops remain coalesced.
 __device__ __forceinline__ Span this_span() {
   Span s;
-  s.gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  s.gthreads = gridDim.x * blockDim.x;
-  s.gwarp = s.gtid >> 5;
-  s.gwarps = s.gthreads >> 5;
+  s.gwarp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  s.gwarps = (blockDim.x >> 5) * gridDim.x;
+  s.gtid = s.gwarp * 32 + (threadIdx.x & 31);
+  s.gthreads = s.gwarps * 32;
   return s;
 }
 
@@ -49,19 +53,42 @@ constexpr double kLog2eD = 1.4426950408889634;
 // ------------------------------------------------------------------ LSE
 
 // Fast LSE: warp per row, max then sum of exp (backup.py:34-41 formula).
+// The whole row is loaded into registers first (one memory round trip),
+// then reduced twice from registers.
 template <class PsiT>
 __device__ double warp_lse_fast(const PsiT* row, int A, double eta) {
   const int lane = lane_id();
+  constexpr int R = 16;  // register-resident elements per lane (|A| <= 512)
   const PsiT e = (PsiT)eta;
   PsiT m = -(PsiT)INFINITY;
-  for (int a = lane; a < A; a += 32) {
-    const PsiT z = e * row[a];
-    m = z > m ? z : m;
-  }
-  m = warp_max(m);
-  const PsiT e2 = (PsiT)(eta * kLog2eD), m2 = m * (PsiT)kLog2eD;
+  const PsiT e2 = (PsiT)(eta * kLog2eD);
   PsiT s = 0;
-  for (int a = lane; a < A; a += 32) s += fexp2(ffma(e2, row[a], -m2));
+  if (A <= 32 * R) {
+    PsiT v[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int a = lane + 32 * k;
+      v[k] = a < A ? row[a] : -(PsiT)INFINITY;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const PsiT z = e * v[k];
+      m = z > m ? z : m;
+    }
+    m = warp_max(m);
+    const PsiT m2 = m * (PsiT)kLog2eD;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (lane + 32 * k < A) s += fexp2(ffma(e2, v[k], -m2));
+  } else {
+    for (int a = lane; a < A; a += 32) {
+      const PsiT z = e * row[a];
+      m = z > m ? z : m;
+    }
+    m = warp_max(m);
+    const PsiT m2 = m * (PsiT)kLog2eD;
+    for (int a = lane; a < A; a += 32) s += fexp2(ffma(e2, row[a], -m2));
+  }
   s = warp_sum(s);
   return (double)m / eta + log((double)s) / eta;
 }
