@@ -525,8 +525,7 @@ static int32_t enqueue_plan_persistent(const vp_tree& T, const vp_model& M, cons
       per_sm < 1)
     return check_launch();
   per_sm = std::min(per_sm, env_int("VP_PLAN_BLOCKS_PER_SM", 4));
-  const int need = blocks_for(W.n, kStageWarps * 32);
-  const int grid = std::max(1, std::min(g_num_sms * per_sm, std::max(need, g_num_sms)));
+  const int grid = std::max(1, g_num_sms * per_sm);
   void* args[] = {&pp};
   {
     Launch L_(KK_PLAN, st);
