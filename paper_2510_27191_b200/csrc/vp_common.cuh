@@ -72,6 +72,28 @@ __device__ __forceinline__ u64 slot_hash(u64 key) { return mix64(key ^ 0x5851F42
 
 __device__ __forceinline__ u64 ld_volatile_u64(const u64* p) { return *(volatile const u64*)p; }
 __device__ __forceinline__ u32 ld_volatile_u32(const u32* p) { return *(volatile const u32*)p; }
+// gpu-scope relaxed loads read L2 without invalidating L1 (an acquire would
+// emit CCTL.IVALL and throw away every warp's L1 lines on the SM).
+__device__ __forceinline__ u32 ld_relaxed_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u32 ld_relaxed_u8(const uint8_t* p) {
+  unsigned short v;
+  asm volatile("ld.relaxed.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return (u32)v;
+}
 __device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
   u32 v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -91,25 +113,17 @@ __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
 
 // Find or claim `key`.  Returns the slot index; sets `existing` when the key
 // already carried a final id from an earlier phase.  New keys record the
-// minimum claiming row (first occurrence) via atomicMin on the id word.
+// minimum claiming row (first occurrence) via atomicMin on the id word; the
+// returned old id tells hits (< kPending) from claims, so a probe costs two
+// L2 atomics (CAS on the key, min on the id) and no plain loads.
 __device__ __forceinline__ u32 probe_claim(Slot* tab, u64 mask, u64 key, u32 row, bool& existing, u32& id) {
   u64 h = slot_hash(key) & mask;
   while (true) {
-    u64 k = ld_volatile_u64(&tab[h].key);
-    if (k == kEmptyKey) {
-      const u64 prev = atomicCAS(&tab[h].key, kEmptyKey, key);
-      k = (prev == kEmptyKey) ? key : prev;
-    }
-    if (k == key) {
-      const u32 v = ld_volatile_u32(&tab[h].id);
-      if (v < kPending) {
-        existing = true;
-        id = v;
-      } else {
-        existing = false;
-        id = kEmptyId;
-        atomicMin(&tab[h].id, kPending | row);
-      }
+    const u64 prev = atomicCAS(&tab[h].key, kEmptyKey, key);
+    if (prev == kEmptyKey || prev == key) {
+      const u32 old = atomicMin(&tab[h].id, kPending | row);
+      existing = old < kPending;
+      id = existing ? old : kEmptyId;
       return (u32)h;
     }
     h = (h + 1) & mask;
@@ -199,7 +213,7 @@ __device__ __forceinline__ u32 tile_lookback_warp(u64* status, int tile, u32 agg
   int base = tile - 1;
   while (true) {
     const int j = base - lane;
-    const u64 s = j >= 0 ? ld_acquire_u64(&status[j]) : pack_status(epoch, kFlagInc, 0);
+    const u64 s = j >= 0 ? ld_relaxed_u64(&status[j]) : pack_status(epoch, kFlagInc, 0);
     const bool valid = (u32)(s >> 32) == epoch;
     const u32 inc = __ballot_sync(0xffffffffu, valid && ((s >> 30) & 3) == kFlagInc);
     const u32 bad = __ballot_sync(0xffffffffu, !valid);

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) u64 s_bar[4];
   Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, sc);
-  phase_sample_fast<Model, PsiT>(T, M, W, level_args(S, level, stamp), sg, this_span());
+  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)4 * sc.rows * sc.stride;
+  phase_sample_fast<Model, PsiT>(T, M, W, level_args(S, level, stamp), sg, init_cdf, this_span());
 }
 
 template <class Model>
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
   const Span sp = this_span();
   const int L = W.max_levels;
   Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, P.sc);
+  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)kStageWarps * P.sc.rows * P.sc.stride;
   typedef typename Model::State State;
 
   int tl = 0;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
       la.start = nullptr;
       const u32 epoch = 1u + 2u * ((u32)it * (u32)(L + 1) + (u32)l);
       if constexpr (Exact) phase_sample_exact<Model>(T, P.M, W, la, sp);
-      else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, sp);
+      else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, init_cdf, sp);
       grid.sync();
       mark();
       phase_assign<0>(T, W, l, epoch, nullptr);
@@ -356,9 +358,10 @@ static StageCfg stage_cfg(int A, int warps, int budget_bytes) {
   c.rows = std::max(1, std::min(32, budget_bytes / warps / (chunks * 16)));
   return c;
 }
+// staged rows of every warp + the block's copy of the initial-row CDF
 template <class PsiT>
-static size_t stage_bytes(const StageCfg& c, int warps) {
-  return (size_t)warps * c.rows * c.stride * sizeof(PsiT);
+static size_t stage_bytes(const StageCfg& c, int warps, int A) {
+  return ((size_t)warps * c.rows * c.stride + (size_t)A) * sizeof(PsiT);
 }
 
 template <class Model, class PsiT, bool Exact>
@@ -389,7 +392,7 @@ static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W,
   size_t smem = 0;
   if constexpr (!Exact) {
     sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
-    smem = stage_bytes<PsiT>(sc, 4);
+    smem = stage_bytes<PsiT>(sc, 4, T.action_count);
     if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   for (int l = S.depth0; l < S.d_max; ++l) {
@@ -511,7 +514,7 @@ static int32_t enqueue_plan_persistent(const vp_tree& T, const vp_model& M, cons
   pp.timeline = reinterpret_cast<u64*>(P.timeline_dev);
   pp.timeline_cap = P.timeline_cap;
   pp.sc = Exact ? StageCfg{1, 4} : stage_cfg<PsiT>(T.action_count, kStageWarps, env_int("VP_PLAN_STAGE_KB", 96) * 1024);
-  const size_t smem = Exact ? 16 : stage_bytes<PsiT>(pp.sc, kStageWarps);
+  const size_t smem = Exact ? 16 : stage_bytes<PsiT>(pp.sc, kStageWarps, T.action_count);
   auto kern = k_plan<Model, PsiT, Exact>;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -563,7 +566,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   if (P.mode == 2) return enqueue_plan_persistent<Model, PsiT, Exact>(T, M, W, P, st);
   if constexpr (!Exact) {
     const StageCfg sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
-    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(stage_bytes<PsiT>(sc, 4))) return rc;
+    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(stage_bytes<PsiT>(sc, 4, T.action_count))) return rc;
   }
   if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);
   std::vector<unsigned char> key;

@@ -249,10 +249,13 @@ __device__ __forceinline__ bool warp_list_once(u32* stamp, int node, u32 value, 
 }
 
 // Id of a slot once its first-occurrence row has numbered it (spin while pending).
+// Relaxed spin: the id's publisher stores it with st.release after the node's
+// columns, and readers only touch those columns through addresses that
+// depend on the id (or with relaxed gpu-scope loads).
 __device__ __forceinline__ int wait_final(const Slot* tab, u32 slot_word) {
   const u32* p = &tab[slot_word & ~kExistBit].id;
-  u32 v = ld_acquire_u32(p);
-  while (v >= kPending) v = ld_acquire_u32(p);
+  u32 v = ld_relaxed_u32(p);
+  while (v >= kPending) v = ld_relaxed_u32(p);
   return (int)v;
 }
 
@@ -267,14 +270,27 @@ __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
   return s;
 }
 
-// Write the initial PSI row into belief b if it is still lazily fresh.
+// Write the initial PSI row into every still-fresh belief of list[0..cnt)
+// (lazy rows, tree.py:253).  Warps take 32 items at a time: one round trip
+// for the 32 flags, then coalesced row stores for the fresh ones.
 template <class PsiT>
-__device__ __forceinline__ void warp_materialise(const vp_tree& T, int b) {
-  if (!(T.b_flags[b] & 1)) return;
-  PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
-  for (int a = lane_id(); a < T.action_count; a += 32) row[a] = (PsiT)T.init_prefs[a];
-  __syncwarp();
-  if (lane_id() == 0) T.b_flags[b] = 0;
+__device__ void materialise_list(const vp_tree& T, const int* list, int cnt, const Span& sp) {
+  const int lane = lane_id();
+  const int A = T.action_count;
+  for (int base = sp.gwarp * 32; base < cnt; base += sp.gwarps * 32) {
+    const int i = base + lane;
+    const int b = i < cnt ? list[i] : 0;
+    const bool fresh = i < cnt && (T.b_flags[b] & 1);
+    u32 m = __ballot_sync(FULL, fresh);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int bb = __shfl_sync(FULL, b, src);
+      PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)bb * T.psi_stride;
+      for (int a = lane; a < A; a += 32) row[a] = (PsiT)T.init_prefs[a];
+    }
+    if (fresh) T.b_flags[b] = 0;
+  }
 }
 
 // ------------------------------------------------------------------ tree init (one block)
@@ -385,8 +401,11 @@ __device__ __forceinline__ void step_and_claim(const vp_tree& T, const vp_model&
 // scans its own row.
 template <class Model, class PsiT>
 __device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_work& W, const LevelArgs& L,
-                                  Stage<PsiT>& sg, const Span& sp) {
+                                  Stage<PsiT>& sg, PsiT* init_cdf, const Span& sp) {
   const int n = W.n, A = T.action_count, lane = lane_id();
+  // the shared initial-row CDF (fresh beliefs) lives in shared memory
+  for (int a = threadIdx.x; a < A; a += blockDim.x) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
+  __syncthreads();
   if (sp.gtid == 0) W.level_base[2 * L.level] = T.counters[1];
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
@@ -401,15 +420,15 @@ __device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_
     if (L.inject) {
       a = active ? L.inject[(size_t)L.level * n + r] : 0;
     } else {
-      const bool fresh = active && (T.b_flags[b] & 1);
+      const bool fresh = active && (ld_relaxed_u8(&T.b_flags[b]) & 1);
       const bool need = active && !fresh;
-      if (fresh) a = search_cdf(reinterpret_cast<const PsiT*>(T.init_cdf), A, (PsiT)u);
+      if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
       const u32 grp = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
       const int my_leader = __ffs(grp) - 1;
       const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
       const int K = __popc(leaders);
       const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-      const PsiT sh2 = need ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
+      const PsiT sh2 = need ? (PsiT)(T.eta * ld_relaxed_f64(&T.b_lse[b]) * kLog2eD) : (PsiT)0;
       for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
         const int cnt = min(sg.cfg.rows, K - s0);
         fence_async_smem();
@@ -446,8 +465,9 @@ __device__ void phase_sample_exact(const vp_tree& T, const vp_model& M, const vp
       if (L.inject) {
         a = L.inject[(size_t)L.level * n + r];
       } else {
-        const double* row = (T.b_flags[b] & 1) ? T.init_prefs
-                                               : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
+        const double* row = (ld_relaxed_u8(&T.b_flags[b]) & 1)
+                                ? T.init_prefs
+                                : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
         a = sample_exact(row, A, T.eta, u);
       }
     }
@@ -631,16 +651,12 @@ __device__ void phase_backup_leaves(const vp_tree& T, const vp_work& W, int dmax
       atomicAdd(&T.a_den[pa], w);
     }
   }
-  if (mat >= 0) {
-    const int mc = W.fcount[mat];
-    for (int i = sp.gwarp; i < mc; i += sp.gwarps) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
-  }
+  if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);
 }
 
 template <class PsiT>
 __device__ void phase_materialise(const vp_tree& T, const vp_work& W, int lvl, const Span& sp) {
-  const int mc = W.fcount[lvl];
-  for (int i = sp.gwarp; i < mc; i += sp.gwarps) warp_materialise<PsiT>(T, W.flist[(size_t)lvl * W.n + i]);
+  materialise_list<PsiT>(T, W.flist + (size_t)lvl * W.n, W.fcount[lvl], sp);
 }
 
 // Actions of level lvl: Q = R/visits + gamma num/den; PSI[b, a] += Q - LSE_pre(b)
@@ -692,10 +708,7 @@ __device__ void phase_backup_v(const vp_tree& T, const vp_work& W, int lvl, int 
       if (lane_id() == 0) finish(b, v);
     }
   }
-  if (mat >= 0) {
-    const int mc = W.fcount[mat];
-    for (int i = sp.gwarp; i < mc; i += sp.gwarps) warp_materialise<PsiT>(T, W.flist[(size_t)mat * W.n + i]);
-  }
+  if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);
 }
 
 // Levels at or above the search start depth have no recorded lists: derive
