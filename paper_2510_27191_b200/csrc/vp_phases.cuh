@@ -53,44 +53,85 @@ constexpr double kLog2eD = 1.4426950408889634;
 // ------------------------------------------------------------------ LSE
 
 // Fast LSE: warp per row, max then sum of exp (backup.py:34-41 formula).
-// The whole row is loaded into registers first (one memory round trip),
-// then reduced twice from registers.
+// Rows of up to 32*R elements are loaded into registers first (one memory
+// round trip); NR rows are processed together so their load latencies and
+// shuffle-reduction chains overlap.
+__device__ __forceinline__ double lse_log(float s) { return (double)logf(s); }
+__device__ __forceinline__ double lse_log(double s) { return log(s); }
+
+template <class PsiT, int NR>
+__device__ __forceinline__ void warp_lse_fast_n(const PsiT* const* rows, int A, double eta, double* out) {
+  const int lane = lane_id();
+  constexpr int R = 16;  // register-resident elements per lane and row (|A| <= 512)
+  const PsiT e = (PsiT)eta;
+  const PsiT e2 = (PsiT)(eta * kLog2eD);
+  PsiT m[NR], s[NR];
+  if (A <= 32 * R) {
+    PsiT v[NR][R];
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int a = lane + 32 * k;
+        v[q][k] = (rows[q] && a < A) ? rows[q][a] : -(PsiT)INFINITY;
+      }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      PsiT mm = -(PsiT)INFINITY;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const PsiT z = e * v[q][k];
+        mm = z > mm ? z : mm;
+      }
+      m[q] = mm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const PsiT w = __shfl_xor_sync(FULL, m[q], o);
+        m[q] = w > m[q] ? w : m[q];
+      }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const PsiT m2 = m[q] * (PsiT)kLog2eD;
+      PsiT acc = 0;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (lane + 32 * k < A) acc += fexp2(ffma(e2, v[q][k], -m2));
+      s[q] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      PsiT mm = -(PsiT)INFINITY;
+      if (rows[q])
+        for (int a = lane; a < A; a += 32) {
+          const PsiT z = e * rows[q][a];
+          mm = z > mm ? z : mm;
+        }
+      m[q] = warp_max(mm);
+      const PsiT m2 = m[q] * (PsiT)kLog2eD;
+      PsiT acc = 0;
+      if (rows[q])
+        for (int a = lane; a < A; a += 32) acc += fexp2(ffma(e2, rows[q][a], -m2));
+      s[q] = acc;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < NR; ++q) s[q] += __shfl_xor_sync(FULL, s[q], o);
+#pragma unroll
+  for (int q = 0; q < NR; ++q) out[q] = (double)m[q] / eta + lse_log(s[q]) / eta;
+}
+
 template <class PsiT>
 __device__ double warp_lse_fast(const PsiT* row, int A, double eta) {
-  const int lane = lane_id();
-  constexpr int R = 16;  // register-resident elements per lane (|A| <= 512)
-  const PsiT e = (PsiT)eta;
-  PsiT m = -(PsiT)INFINITY;
-  const PsiT e2 = (PsiT)(eta * kLog2eD);
-  PsiT s = 0;
-  if (A <= 32 * R) {
-    PsiT v[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int a = lane + 32 * k;
-      v[k] = a < A ? row[a] : -(PsiT)INFINITY;
-    }
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const PsiT z = e * v[k];
-      m = z > m ? z : m;
-    }
-    m = warp_max(m);
-    const PsiT m2 = m * (PsiT)kLog2eD;
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if (lane + 32 * k < A) s += fexp2(ffma(e2, v[k], -m2));
-  } else {
-    for (int a = lane; a < A; a += 32) {
-      const PsiT z = e * row[a];
-      m = z > m ? z : m;
-    }
-    m = warp_max(m);
-    const PsiT m2 = m * (PsiT)kLog2eD;
-    for (int a = lane; a < A; a += 32) s += fexp2(ffma(e2, row[a], -m2));
-  }
-  s = warp_sum(s);
-  return (double)m / eta + log((double)s) / eta;
+  const PsiT* rows[1] = {row};
+  double out[1];
+  warp_lse_fast_n<PsiT, 1>(rows, A, eta, out);
+  return out[0];
 }
 
 // numpy-order LSE for the fp64 parity mode: m/eta + log(pairwise sum)/eta.
@@ -702,10 +743,20 @@ __device__ void phase_backup_v(const vp_tree& T, const vp_work& W, int lvl, int 
       finish(b, lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta));
     }
   } else {
-    for (int i = sp.gwarp; i < cnt; i += sp.gwarps) {
-      const int b = W.flist[(size_t)lvl * W.n + i];
-      const double v = warp_lse_fast<PsiT>(psi + (size_t)b * T.psi_stride, A, T.eta);
-      if (lane_id() == 0) finish(b, v);
+    constexpr int NR = 2;  // rows per warp iteration
+    for (int i0 = sp.gwarp * NR; i0 < cnt; i0 += sp.gwarps * NR) {
+      int bs[NR];
+      const PsiT* rows[NR];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        bs[q] = i0 + q < cnt ? W.flist[(size_t)lvl * W.n + i0 + q] : -1;
+        rows[q] = bs[q] >= 0 ? psi + (size_t)bs[q] * T.psi_stride : nullptr;
+      }
+      double v[NR];
+      warp_lse_fast_n<PsiT, NR>(rows, A, T.eta, v);
+#pragma unroll
+      for (int q = 0; q < NR; ++q)
+        if (lane_id() == q && bs[q] >= 0) finish(bs[q], v[q]);
     }
   }
   if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);

@@ -106,7 +106,7 @@ class Planner:
         self.work: Workspace | None = None
         self._cap_cache = {}
         self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
-        self.mode = 2  # vp_plan: 2 persistent kernel, 1 CUDA graph of per-phase kernels, 0 direct
+        self.mode = 1  # vp_plan: 1 CUDA graph of per-phase kernels (default), 2 persistent kernel, 0 direct
         self._bufs = {}
 
     def _capacity(self, n: int, config, A: int):
