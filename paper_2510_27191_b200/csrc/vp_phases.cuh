@@ -312,25 +312,17 @@ __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
 }
 
 // Write the initial PSI row into every still-fresh belief of list[0..cnt)
-// (lazy rows, tree.py:253).  Warps take 32 items at a time: one round trip
-// for the 32 flags, then coalesced row stores for the fresh ones.
+// (lazy rows, tree.py:253); one warp per belief.
 template <class PsiT>
 __device__ void materialise_list(const vp_tree& T, const int* list, int cnt, const Span& sp) {
   const int lane = lane_id();
   const int A = T.action_count;
-  for (int base = sp.gwarp * 32; base < cnt; base += sp.gwarps * 32) {
-    const int i = base + lane;
-    const int b = i < cnt ? list[i] : 0;
-    const bool fresh = i < cnt && (T.b_flags[b] & 1);
-    u32 m = __ballot_sync(FULL, fresh);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int bb = __shfl_sync(FULL, b, src);
-      PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)bb * T.psi_stride;
-      for (int a = lane; a < A; a += 32) row[a] = (PsiT)T.init_prefs[a];
-    }
-    if (fresh) T.b_flags[b] = 0;
+  for (int i = sp.gwarp; i < cnt; i += sp.gwarps) {
+    const int b = list[i];
+    if (!(T.b_flags[b] & 1)) continue;
+    PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
+    for (int a = lane; a < A; a += 32) row[a] = (PsiT)T.init_prefs[a];
+    if (lane == 0) T.b_flags[b] = 0;
   }
 }
 
@@ -743,7 +735,7 @@ __device__ void phase_backup_v(const vp_tree& T, const vp_work& W, int lvl, int 
       finish(b, lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta));
     }
   } else {
-    constexpr int NR = 2;  // rows per warp iteration
+    constexpr int NR = 1;  // rows per warp iteration (enough warps to hide latency)
     for (int i0 = sp.gwarp * NR; i0 < cnt; i0 += sp.gwarps * NR) {
       int bs[NR];
       const PsiT* rows[NR];
