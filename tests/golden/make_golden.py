@@ -150,6 +150,13 @@ def gen_episodes():
         recs.append({"seed": s, "return": rec.discounted_return, "steps": rec.steps,
                      "reason": rec.terminal_reason, "degenerate": rec.degenerate_updates})
     out["episode_mars4_3"] = recs
+    # a larger sample for the statistical closed-loop check (fp32 device planner)
+    cfg = ref.SolverConfig(n_parallel=256, iterations=5, particles=1000)
+    recs = []
+    for s in range(100, 130):
+        rec = ref.run_episode(MarsModel(n=5, m=4, layout_seed=7), cfg, seed=s)
+        recs.append({"seed": s, "return": rec.discounted_return, "steps": rec.steps})
+    out["episode_mars5_4_campaign"] = recs
     return out
 
 
