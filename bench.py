@@ -43,6 +43,18 @@ sys.path.insert(0, REPO)
 
 WORKLOAD = {"problem": "mars", "n": 11, "m": 11, "n_parallel": 16384, "iterations": 10, "eta": 2.0,
             "particles": 10_000}
+# BASELINE.json configs: c2 is the headline workload;
+# the others are measured on request (--config) for the scaling evidence.
+CONFIGS = {
+    "c1": {"problem": "mars", "n": 7, "m": 8, "n_parallel": 1024, "iterations": 8,
+           "name": "RockSample(7,8)=MarsModel(7,8)"},
+    "c2": {"problem": "mars", "n": 11, "m": 11, "n_parallel": 16384, "iterations": 10,
+           "name": "RockSample(11,11)=MarsModel(11,11)"},
+    "c3": {"problem": "mars", "n": 15, "m": 15, "n_parallel": 65536, "iterations": 10,
+           "name": "RockSample(15,15)=MarsModel(15,15)"},
+    "c4": {"problem": "lightdark", "n_parallel": 16384, "iterations": 20, "name": "LightDark(64x64 bins)"},
+    "c5": {"problem": "synthetic", "n_parallel": 65536, "iterations": 20, "name": "Synthetic(|A|=16,|O|=8)"},
+}
 METRIC = "belief-tree simulations/sec per planning step"
 UNIT = "simulations/s"
 
@@ -53,12 +65,27 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n-parallel", type=int, default=WORKLOAD["n_parallel"])
-    ap.add_argument("--iterations", type=int, default=WORKLOAD["iterations"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n-parallel", type=int, default=None)
+    ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    c = CONFIGS[a.config]
+    a.n_parallel = a.n_parallel or c["n_parallel"]
+    a.iterations = a.iterations or c["iterations"]
+    return a
+
+
+def make_model(lib, args, seed):
+    """The config's problem model from `lib` (the product package or the oracle)."""
+    c = CONFIGS[args.config]
+    if c["problem"] == "mars":
+        return lib.MarsModel(n=c["n"], m=c["m"], layout_seed=seed)
+    if c["problem"] == "lightdark":
+        return lib.LightDarkModel()
+    return lib.SyntheticModel(n_actions=16, n_obs=8, seed=seed)
 
 
 def dist_env():
@@ -68,10 +95,10 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(args, world):
-    return {"workload": f"RockSample(11,11)=MarsModel(11,11) plan(), n_parallel={args.n_parallel}, "
-                        f"iterations={args.iterations}",
-            "problem": "MarsModel(n=11, m=11)", "actions": 256, "n_parallel": args.n_parallel,
+def workload_config(args, world, actions=None):
+    c = CONFIGS[args.config]
+    return {"workload": f"{c['name']} plan(), n_parallel={args.n_parallel}, iterations={args.iterations}",
+            "config_id": args.config, "problem": c["name"], "actions": actions, "n_parallel": args.n_parallel,
             "iterations": args.iterations, "eta": WORKLOAD["eta"], "particles": WORKLOAD["particles"],
             "simulations_per_step": args.n_parallel * args.iterations,
             "episode_steps_per_step": args.n_parallel * sum(range(1, args.iterations + 1)),
@@ -156,7 +183,8 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     seed = 1000 + rank
-    model = vp.MarsModel(n=WORKLOAD["n"], m=WORKLOAD["m"], layout_seed=seed)
+    model = make_model(vp, args, seed)
+    A = model.spec.action_count
     belief = vp.ParticleBelief.from_model(model, WORKLOAD["particles"], vp.RowRng.from_seed(seed).derive(3))
     cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=args.n_parallel, iterations=args.iterations)
     planner = vp.Planner(args.precision)
@@ -209,55 +237,68 @@ def run_b200(args):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e = sims / (e2e_ms / 1e3)
-    h2d = belief.states.x.shape[0] * dm.state_bytes + 8 * len(belief.weights)
+    h2d = len(belief.states) * dm.state_bytes + 8 * len(belief.weights)
 
-    # profiled pass of the same steps: per-kernel-kind device time and the dominant kernel
+    # profiled pass of the same steps: per-kernel-kind device time (CUDA events around every
+    # launch on the planner's stream) and the traffic counters the kernels keep
     _lib.profile_enable(True)
     prof_steps = min(args.steps, 3)
+    planner.work.stats.zero_()
     for t in range(prof_steps):
         step(args.warmup + t)
     torch.cuda.synchronize()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
+    st = planner.work.stats.cpu().numpy().astype(np.float64)
     kinds = {k: v for k, v in prof.items() if v[1]}
     total_ms = sum(v[0] for v in kinds.values())
     top = max(kinds, key=lambda k: kinds[k][0])
-    # algorithmic bytes of level_sample for one step, from the recorded per-level lists
-    step(args.warmup)
-    fc, pc = level_counts(planner.work, args.iterations)
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    ls_ms, ls_n = kinds.get("level_sample", (0.0, 0))
-    roof = None
-    if ls_n:
-        # bytes of the last iteration's levels (the only ones whose lists survive) scaled per launch
-        per_launch = bytes_level_sample(args.n_parallel, 256, dm.state_bytes, fc, pc,
-                                        4 if args.precision == "fp32" else 8)
-        avg_bytes = float(np.mean(per_launch))
-        avg_ms = ls_ms / ls_n
-        ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        roof = {"kernel": "k_level_sample", "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
-                "bytes_per_launch": avg_bytes, "avg_launch_us": round(avg_ms * 1e3, 2),
-                "share_of_step": round(ls_ms / total_ms, 3) if total_ms else None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+    psi_b = 4 if args.precision == "fp32" else 8
+    S = dm.state_bytes
+
+    def roof(kind, kname, total_bytes, formula):
+        ms, cnt = kinds.get(kind, (0.0, 0))
+        if not cnt:
+            return None
+        per_launch = total_bytes / cnt
+        avg_ms = ms / cnt
+        ach = per_launch / (avg_ms / 1e3) / 1e9
+        return {"kernel": kname, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "bytes_per_launch": round(per_launch),
+                "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
+                "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+
+    U, P, staged, rows = st[0], st[1], st[2], st[4]
+    roof_sample = roof("level_sample", "k_level_sample",
+                       rows * (24 + 2 * S) + U * 96 + staged * (psi_b * A + 32) + 64 * P,
+                       "n(24+2S) + 96 U_l + (4|A|+32) staged_l + 64 P_l per level (SURVEY 8d B_search)")
+    roof_backup = roof("backup_v", "k_backup_v", U * (psi_b * A + 64),
+                       "(4|A|+64) U_l per level (SURVEY 8d B_backup; PSI row read once per belief)")
+    dominant = {"level_sample": roof_sample, "backup_v": roof_backup}.get(top) or roof_sample
     kernel_table = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
                     for k, v in kinds.items()}
+    traffic = {"distinct_beliefs_per_step": st[0] / prof_steps, "distinct_actions_per_step": st[1] / prof_steps,
+               "psi_rows_staged_per_step": st[2] / prof_steps, "new_actions_per_step": st[5] / prof_steps,
+               "new_beliefs_per_step": st[6] / prof_steps}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
             "data": "synthetic (MARS belief sampled from the model; no dataset)",
-            "config": workload_config(args, world),
+            "config": workload_config(args, world, A),
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
                     "ms_per_step": round(e2e_ms / args.steps, 4)},
-            "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
-            "kernels": kernel_table, "dominant_kernel": top,
+            "gpu_launches": int(launches), "clocks": clk, "roofline": dominant,
+            "roofline_other": {"k_level_sample": roof_sample, "k_backup_v": roof_backup},
+            "kernels": kernel_table, "dominant_kernel": top, "level_traffic": traffic,
             "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1),
             "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
+        line["speedup_vs_cpu_1core"] = round(line["e2e"]["value"] / line["cpu_baseline"]["value"], 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -268,11 +309,11 @@ def run_b200(args):
 # ---------------------------------------------------------------- CPU (oracle port of the reference)
 
 
-def _cpu_plan(seed, n_parallel, iterations):
+def _cpu_plan(seed, n_parallel, iterations, config="c2"):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     import oracle
 
-    model = oracle.MarsModel(n=WORKLOAD["n"], m=WORKLOAD["m"], layout_seed=seed)
+    model = make_model(oracle, argparse.Namespace(config=config), seed)
     belief = oracle.ParticleBelief.from_model(model, WORKLOAD["particles"], oracle.RowRng.from_seed(seed).derive(3))
     cfg = oracle.SolverConfig(eta=WORKLOAD["eta"], n_parallel=n_parallel, iterations=iterations)
     t0 = time.perf_counter()
@@ -285,7 +326,7 @@ def cpu_baseline(args) -> dict:
     times = []
     t_start = time.perf_counter()
     while not times or (time.perf_counter() - t_start < args.cpu_budget_s and len(times) < 3):
-        dt, _ = _cpu_plan(1000 + len(times), args.n_parallel, args.iterations)
+        dt, _ = _cpu_plan(1000 + len(times), args.n_parallel, args.iterations, args.config)
         times.append(dt)
     sims = args.n_parallel * args.iterations
     return {"value": round(sims * len(times) / sum(times), 1), "unit": UNIT, "cores": 1, "kind": "port",
@@ -311,10 +352,12 @@ def run_reference(args):
     os.environ["OMP_NUM_THREADS"] = "1"  # inherited by the spawned workers
     with ctx.Pool(cores) as pool:
         for w in range(args.warmup):
-            pool.starmap(_cpu_plan, [(2000 + w * cores + c, args.n_parallel, args.iterations) for c in range(cores)])
+            pool.starmap(_cpu_plan, [(2000 + w * cores + c, args.n_parallel, args.iterations, args.config)
+                                     for c in range(cores)])
         t0 = time.perf_counter()
         for s in range(args.steps):
-            pool.starmap(_cpu_plan, [(3000 + s * cores + c, args.n_parallel, args.iterations) for c in range(cores)])
+            pool.starmap(_cpu_plan, [(3000 + s * cores + c, args.n_parallel, args.iterations, args.config)
+                                     for c in range(cores)])
         dt = time.perf_counter() - t0
     sims = args.n_parallel * args.iterations * cores * args.steps
     value = sims / dt

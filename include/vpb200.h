@@ -130,6 +130,10 @@ typedef struct vp_work {
   uint32_t* scan_ticket;      /* [2]                                        */
   int32_t* leaf_belief;       /* [n] frontier belief per row after search   */
   double* leaf_value;         /* [n] heuristic per row after search         */
+  unsigned long long* stats;  /* [8] or NULL: traffic counters summed over a plan:
+                                 0 distinct beliefs/level, 1 distinct actions/level,
+                                 2 PSI rows staged by the sampler, 3 sample launches,
+                                 4 rows sampled, 5 new actions, 6 new beliefs */
   /* optional per-level traces (level-major, n each); NULL = off */
   int32_t* trace_action;
   uint32_t* trace_obs;

@@ -65,6 +65,7 @@ class VpWork(C.Structure):
         ("action", C.c_void_p), ("flist", C.c_void_p), ("fcount", C.c_void_p), ("plist", C.c_void_p),
         ("pcount", C.c_void_p), ("level_base", C.c_void_p), ("scan_status", C.c_void_p),
         ("scan_ticket", C.c_void_p), ("leaf_belief", C.c_void_p), ("leaf_value", C.c_void_p),
+        ("stats", C.c_void_p),
         ("trace_action", C.c_void_p), ("trace_obs", C.c_void_p), ("trace_anode", C.c_void_p),
         ("trace_belief", C.c_void_p),
     ]

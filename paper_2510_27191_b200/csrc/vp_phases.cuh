@@ -436,6 +436,10 @@ template <class Model, class PsiT>
 __device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_work& W, const LevelArgs& L,
                                   Stage<PsiT>& sg, PsiT* init_cdf, const Span& sp) {
   const int n = W.n, A = T.action_count, lane = lane_id();
+  if (W.stats && sp.gtid == 0) {
+    atomicAdd(&W.stats[3], 1ull);
+    atomicAdd(&W.stats[4], (unsigned long long)n);
+  }
   // the shared initial-row CDF (fresh beliefs) lives in shared memory
   for (int a = threadIdx.x; a < A; a += blockDim.x) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
   __syncthreads();
@@ -460,6 +464,7 @@ __device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_
       const int my_leader = __ffs(grp) - 1;
       const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
       const int K = __popc(leaders);
+      if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
       const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
       const PsiT sh2 = need ? (PsiT)(T.eta * ld_relaxed_f64(&T.b_lse[b]) * kLog2eD) : (PsiT)0;
       for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
@@ -562,6 +567,12 @@ __device__ void phase_assign(const vp_tree& T, const vp_work& W, int level, u32 
       if (lane == 0) {
         s_excl = excl;
         if (tile == ntiles - 1) {
+          if (W.stats) {
+            // lists of this level are complete by now: F_l after sample, P_l after accum
+            atomicAdd(&W.stats[WhichTable ? 1 : 0],
+                      (unsigned long long)(WhichTable ? W.pcount[level] : W.fcount[level]));
+            atomicAdd(&W.stats[WhichTable ? 6 : 5], (unsigned long long)(excl + agg));
+          }
           T.counters[WhichTable ? 0 : 1] = base + (int)(excl + agg);
           if (ticket) *ticket = 0;  // every block has taken its ticket by now
         }

@@ -57,10 +57,11 @@ class Workspace:
         self.scan_ticket = torch.zeros(2, **i32)
         self.leaf_belief = torch.empty(n, **i32)
         self.leaf_value = torch.empty(n, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(8, dtype=torch.int64, device=dev)
         s = _lib.VpWork()
         s.n, s.max_levels = n, L
         for name in ("states", "slot_a", "slot_b", "obs", "reward", "action", "flist", "fcount", "plist",
-                     "pcount", "level_base", "scan_status", "scan_ticket", "leaf_belief", "leaf_value"):
+                     "pcount", "level_base", "scan_status", "scan_ticket", "leaf_belief", "leaf_value", "stats"):
             setattr(s, name, getattr(self, name).data_ptr())
         if trace:
             self.trace_action = torch.empty(L * n, **i32)
