@@ -667,7 +667,7 @@ __global__ void k_lse_rows(const PsiT* rows, int count, int width, double eta, d
   if constexpr (Exact) {
     if (lane_id() == 0) out[gw] = lse_exact(reinterpret_cast<const double*>(rows) + (size_t)gw * width, width, eta);
   } else {
-    const double v = warp_lse_fast<PsiT>(rows + (size_t)gw * width, width, eta);
+    const double v = row_lse_fast<PsiT>(rows + (size_t)gw * width, width, eta);
     if (lane_id() == 0) out[gw] = v;
   }
 }

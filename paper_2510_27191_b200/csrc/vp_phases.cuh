@@ -15,6 +15,8 @@
 //   backup_*    backup.py:75-114       leaf means, Q + PSI scatter, LSE per level
 #pragma once
 
+#include <type_traits>
+
 #include "vp_common.cuh"
 #include "vp_models.cuh"
 
@@ -52,86 +54,89 @@ constexpr double kLog2eD = 1.4426950408889634;
 
 // ------------------------------------------------------------------ LSE
 
-// Fast LSE: warp per row, max then sum of exp (backup.py:34-41 formula).
-// Rows of up to 32*R elements are loaded into registers first (one memory
-// round trip); NR rows are processed together so their load latencies and
-// shuffle-reduction chains overlap.
+// Fast LSE (backup.py:34-41 formula: max, then sum of exp), evaluated by a
+// group of lanes per row with the row held in registers.
 __device__ __forceinline__ double lse_log(float s) { return (double)logf(s); }
 __device__ __forceinline__ double lse_log(double s) { return log(s); }
 
-template <class PsiT, int NR>
-__device__ __forceinline__ void warp_lse_fast_n(const PsiT* const* rows, int A, double eta, double* out) {
-  const int lane = lane_id();
-  constexpr int R = 16;  // register-resident elements per lane and row (|A| <= 512)
-  const PsiT e = (PsiT)eta;
-  const PsiT e2 = (PsiT)(eta * kLog2eD);
-  PsiT m[NR], s[NR];
-  if (A <= 32 * R) {
-    PsiT v[NR][R];
-#pragma unroll
-    for (int q = 0; q < NR; ++q)
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int a = lane + 32 * k;
-        v[q][k] = (rows[q] && a < A) ? rows[q][a] : -(PsiT)INFINITY;
-      }
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      PsiT mm = -(PsiT)INFINITY;
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const PsiT z = e * v[q][k];
-        mm = z > mm ? z : mm;
-      }
-      m[q] = mm;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        const PsiT w = __shfl_xor_sync(FULL, m[q], o);
-        m[q] = w > m[q] ? w : m[q];
-      }
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const PsiT m2 = m[q] * (PsiT)kLog2eD;
-      PsiT acc = 0;
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-        if (lane + 32 * k < A) acc += fexp2(ffma(e2, v[q][k], -m2));
-      s[q] = acc;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      PsiT mm = -(PsiT)INFINITY;
-      if (rows[q])
-        for (int a = lane; a < A; a += 32) {
-          const PsiT z = e * rows[q][a];
-          mm = z > mm ? z : mm;
-        }
-      m[q] = warp_max(mm);
-      const PsiT m2 = m[q] * (PsiT)kLog2eD;
-      PsiT acc = 0;
-      if (rows[q])
-        for (int a = lane; a < A; a += 32) acc += fexp2(ffma(e2, rows[q][a], -m2));
-      s[q] = acc;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int q = 0; q < NR; ++q) s[q] += __shfl_xor_sync(FULL, s[q], o);
-#pragma unroll
-  for (int q = 0; q < NR; ++q) out[q] = (double)m[q] / eta + lse_log(s[q]) / eta;
+// Sub-warp LSE: a group of G lanes (G a power of two) per row, so short rows
+// (|A| <= 16 G) keep every lane busy and take one memory round trip.  All
+// 32 lanes must call it (rows may be null for idle groups).
+__host__ __device__ constexpr int lse_group_size(int A) {
+  return A <= 16 ? 1 : A <= 32 ? 2 : A <= 64 ? 4 : A <= 128 ? 8 : A <= 256 ? 16 : 32;
 }
 
+template <class PsiT, int G>
+__device__ __forceinline__ double lse_group(const PsiT* row, int A, double eta) {
+  const int gl = lane_id() & (G - 1);
+  constexpr int R = 16;
+  const PsiT e = (PsiT)eta;
+  const PsiT e2 = (PsiT)(eta * kLog2eD);
+  PsiT m = -(PsiT)INFINITY, s = 0;
+  if (A <= G * R) {
+    PsiT v[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int a = gl + G * k;
+      v[k] = (row && a < A) ? row[a] : -(PsiT)INFINITY;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const PsiT z = e * v[k];
+      m = z > m ? z : m;
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const PsiT w = __shfl_xor_sync(FULL, m, o, G);
+      m = w > m ? w : m;
+    }
+    const PsiT m2 = m * (PsiT)kLog2eD;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (row && gl + G * k < A) s += fexp2(ffma(e2, v[k], -m2));
+  } else {
+    if (row)
+      for (int a = gl; a < A; a += G) {
+        const PsiT z = e * row[a];
+        m = z > m ? z : m;
+      }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const PsiT w = __shfl_xor_sync(FULL, m, o, G);
+      m = w > m ? w : m;
+    }
+    const PsiT m2 = m * (PsiT)kLog2eD;
+    if (row)
+      for (int a = gl; a < A; a += G) s += fexp2(ffma(e2, row[a], -m2));
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
+  return (double)m / eta + lse_log(s) / eta;
+}
+
+// Runtime dispatch of the group size; f is called as f(std::integral_constant<int, G>()).
+template <class F>
+__device__ __forceinline__ void with_group(int A, const F& f) {
+  switch (lse_group_size(A)) {
+    case 1: f(std::integral_constant<int, 1>()); break;
+    case 2: f(std::integral_constant<int, 2>()); break;
+    case 4: f(std::integral_constant<int, 4>()); break;
+    case 8: f(std::integral_constant<int, 8>()); break;
+    case 16: f(std::integral_constant<int, 16>()); break;
+    default: f(std::integral_constant<int, 32>()); break;
+  }
+}
+
+// The fast LSE of one row as the tree caches it (group size from |A|); called by a full warp.
 template <class PsiT>
-__device__ double warp_lse_fast(const PsiT* row, int A, double eta) {
-  const PsiT* rows[1] = {row};
-  double out[1];
-  warp_lse_fast_n<PsiT, 1>(rows, A, eta, out);
-  return out[0];
+__device__ double row_lse_fast(const PsiT* row, int A, double eta) {
+  double out = 0.0;
+  with_group(A, [&](auto g) {
+    constexpr int G = decltype(g)::value;
+    const double v = lse_group<PsiT, G>(lane_id() < G ? row : nullptr, A, eta);
+    out = __shfl_sync(FULL, v, 0);
+  });
+  return out;
 }
 
 // numpy-order LSE for the fp64 parity mode: m/eta + log(pairwise sum)/eta.
@@ -312,18 +317,24 @@ __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
 }
 
 // Write the initial PSI row into every still-fresh belief of list[0..cnt)
-// (lazy rows, tree.py:253); one warp per belief.
+// (lazy rows, tree.py:253); a group of G lanes per belief.
 template <class PsiT>
 __device__ void materialise_list(const vp_tree& T, const int* list, int cnt, const Span& sp) {
-  const int lane = lane_id();
   const int A = T.action_count;
-  for (int i = sp.gwarp; i < cnt; i += sp.gwarps) {
-    const int b = list[i];
-    if (!(T.b_flags[b] & 1)) continue;
-    PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
-    for (int a = lane; a < A; a += 32) row[a] = (PsiT)T.init_prefs[a];
-    if (lane == 0) T.b_flags[b] = 0;
-  }
+  with_group(A, [&](auto g) {
+    constexpr int G = decltype(g)::value;
+    constexpr int RPW = 32 / G;
+    const int gl = lane_id() & (G - 1), grp = lane_id() / G;
+    for (int i0 = sp.gwarp * RPW; i0 < cnt; i0 += sp.gwarps * RPW) {
+      const int i = i0 + grp;
+      if (i >= cnt) continue;
+      const int b = list[i];
+      if (!(T.b_flags[b] & 1)) continue;
+      PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
+      for (int a = gl; a < A; a += G) row[a] = (PsiT)T.init_prefs[a];
+      if (gl == 0) T.b_flags[b] = 0;
+    }
+  });
 }
 
 // ------------------------------------------------------------------ tree init (one block)
@@ -340,7 +351,7 @@ __device__ void block_tree_init(const vp_tree& T) {
       v = 0.0;
       if (threadIdx.x == 0) v = lse_exact(reinterpret_cast<const double*>(psi), A, T.eta);
     } else {
-      v = warp_lse_fast<PsiT>(psi, A, T.eta);
+      v = row_lse_fast<PsiT>(psi, A, T.eta);
     }
     if (threadIdx.x == 0) {
       T.init_lse[0] = v;
@@ -746,21 +757,17 @@ __device__ void phase_backup_v(const vp_tree& T, const vp_work& W, int lvl, int 
       finish(b, lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta));
     }
   } else {
-    constexpr int NR = 1;  // rows per warp iteration (enough warps to hide latency)
-    for (int i0 = sp.gwarp * NR; i0 < cnt; i0 += sp.gwarps * NR) {
-      int bs[NR];
-      const PsiT* rows[NR];
-#pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        bs[q] = i0 + q < cnt ? W.flist[(size_t)lvl * W.n + i0 + q] : -1;
-        rows[q] = bs[q] >= 0 ? psi + (size_t)bs[q] * T.psi_stride : nullptr;
+    with_group(A, [&](auto g) {
+      constexpr int G = decltype(g)::value;
+      constexpr int RPW = 32 / G;  // rows per warp
+      const int gl = lane_id() & (G - 1), grp = lane_id() / G;
+      for (int i0 = sp.gwarp * RPW; i0 < cnt; i0 += sp.gwarps * RPW) {
+        const int i = i0 + grp;
+        const int b = i < cnt ? W.flist[(size_t)lvl * W.n + i] : -1;
+        const double v = lse_group<PsiT, G>(b >= 0 ? psi + (size_t)b * T.psi_stride : nullptr, A, T.eta);
+        if (gl == 0 && b >= 0) finish(b, v);
       }
-      double v[NR];
-      warp_lse_fast_n<PsiT, NR>(rows, A, T.eta, v);
-#pragma unroll
-      for (int q = 0; q < NR; ++q)
-        if (lane_id() == q && bs[q] >= 0) finish(bs[q], v[q]);
-    }
+    });
   }
   if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);
 }
