@@ -183,6 +183,14 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) u64 s_bar[kStageWarps];
   cg::grid_group grid = cg::this_grid();
+  // grid barrier + gpu-scope fence: the fence also invalidates this SM's L1
+  // (CCTL.IVALL), so plain loads after the barrier never hit lines cached
+  // before another SM rewrote them (e.g. a lazily materialised PSI row that
+  // shares a 128-B line with a row read earlier).
+  auto barrier = [&]() {
+    grid.sync();
+    __threadfence();
+  };
   const vp_tree& T = P.T;
   const vp_work& W = P.W;
   const Span sp = this_span();
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
     if (sp.gtid <= d) W.fcount[sp.gtid] = 0;
     if (sp.gtid < d) W.pcount[sp.gtid] = 0;
     phase_draw<Model>(W, reinterpret_cast<const State*>(P.particles), P.cumw, P.m, P.keys[2 * it], sp);
-    grid.sync();
+    barrier();
     mark();
     for (int l = 0; l < d; ++l) {
       LevelArgs la;
@@ -217,11 +225,11 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
       const u32 epoch = 1u + 2u * ((u32)it * (u32)(L + 1) + (u32)l);
       if constexpr (Exact) phase_sample_exact<Model>(T, P.M, W, la, sp);
       else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, init_cdf, sp);
-      grid.sync();
+      barrier();
       mark();
       phase_assign<0>(T, W, l, epoch, nullptr);
       phase_accum(T, W, l, la.stamp, sp);
-      grid.sync();
+      barrier();
       mark();
       phase_assign<1>(T, W, l, epoch + 1u, nullptr);
     }
@@ -235,17 +243,17 @@ __global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
       la.start = nullptr;
       phase_leaf<Model>(T, P.M, W, la, sp);
     }
-    grid.sync();
+    barrier();
     mark();
     phase_backup_leaves<PsiT>(T, W, d, d - 1, sp);
-    grid.sync();
+    barrier();
     mark();
     for (int lv = d - 1; lv >= 0; --lv) {
       phase_backup_q<PsiT>(T, W, lv, P.gamma, sp);
-      grid.sync();
+      barrier();
       mark();
       phase_backup_v<PsiT, Exact>(T, W, lv, lv - 1, sp);
-      grid.sync();
+      barrier();
       mark();
     }
     d = d + 1 < P.d_max_cap ? d + 1 : P.d_max_cap;
