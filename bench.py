@@ -149,22 +149,28 @@ class ClockSampler:
 # ---------------------------------------------------------------- algorithmic bytes
 
 
-def level_counts(work, d_max):
-    """Per-level U_l (distinct beliefs), P_l (distinct actions) from the device lists."""
-    fc = work.fcount.cpu().numpy()[: d_max + 1].astype(np.int64)
-    pc = work.pcount.cpu().numpy()[:d_max].astype(np.int64)
-    return fc, pc
+def algorithmic_bytes(st, n, S, A, psi_b, passes):
+    """Compulsory HBM bytes of the search and backup kernels summed over `passes`
+    passes, from the device traffic counters (adapted to the
+    fused design: states and frontier ids stay in registers across levels).
 
-
-def bytes_level_sample(n, A, S, fc, pc, psi_bytes=4):
-    """K1 per launch (level l): frontier slot + hash slot (4 + 32/distinct), state in/out
-    (2S), obs/reward/action/slot writes (20), PSI row + LSE + stamp per distinct belief,
-    one probed sector per distinct (b, a)."""
-    out = []
-    for lvl in range(len(pc)):
-        u, p = fc[lvl], pc[lvl]
-        out.append(n * (4 + 2 * S + 20) + u * (psi_bytes * A + 32 + 32 + 32) + 32 * p)
-    return out
+    U   interior beliefs visited (rows sampled from), Unf those whose PSI row is not
+        lazily initial (read by the sampler), P distinct action nodes visited,
+        L distinct leaves, NA / NB new action / belief rows.
+    """
+    U, P, L, NA, NB, Unf = st[0], st[1], st[7], st[5], st[6], st[8]
+    children = (U - passes) + L  # distinct (a, o) probes: every visited non-root belief
+    search = (n * passes * max(S, 32)          # root-state gather (one sector per row)
+              + psi_b * A * Unf                # PSI row per distinct non-fresh belief per level
+              + psi_b * A * (U - Unf)          # lazily initial rows written once (interior now)
+              + 32 * (P + children)            # one hash sector per distinct probe
+              + 16 * P                         # reward / visit / row reductions
+              + 52 * NA + 56 * NB              # new node columns
+              + 8 * L)                         # leaf heuristic sums
+    backup = (12 * children                    # child (parent, V, N) reads
+              + 96 * P                         # action stats + Q scratch + sector-granular PSI scatter
+              + (psi_b * A + 8) * U)           # one PSI row read + V/N write per belief
+    return search, backup
 
 
 # ---------------------------------------------------------------- b200 arm
@@ -244,11 +250,13 @@ def run_b200(args):
     _lib.profile_enable(True)
     prof_steps = min(args.steps, 3)
     planner.work.stats.zero_()
+    planner.work.enable_stats(True)
     for t in range(prof_steps):
         step(args.warmup + t)
     torch.cuda.synchronize()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
+    planner.work.enable_stats(False)
     st = planner.work.stats.cpu().numpy().astype(np.float64)
     kinds = {k: v for k, v in prof.items() if v[1]}
     total_ms = sum(v[0] for v in kinds.values())
@@ -258,6 +266,8 @@ def run_b200(args):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     psi_b = 4 if args.precision == "fp32" else 8
     S = dm.state_bytes
+    passes = prof_steps * args.iterations
+    b_search, b_backup = algorithmic_bytes(st, args.n_parallel, S, A, psi_b, passes)
 
     def roof(kind, kname, total_bytes, formula):
         ms, cnt = kinds.get(kind, (0.0, 0))
@@ -271,18 +281,16 @@ def run_b200(args):
                 "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
                 "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
 
-    U, P, staged, rows = st[0], st[1], st[2], st[4]
-    roof_sample = roof("level_sample", "k_level_sample",
-                       rows * (24 + 2 * S) + U * 96 + staged * (psi_b * A + 32) + 64 * P,
-                       "n(24+2S) + 96 U_l + (4|A|+32) staged_l + 64 P_l per level (SURVEY 8d B_search)")
-    roof_backup = roof("backup_v", "k_backup_v", U * (psi_b * A + 64),
-                       "(4|A|+64) U_l per level (SURVEY 8d B_backup; PSI row read once per belief)")
-    dominant = {"level_sample": roof_sample, "backup_v": roof_backup}.get(top) or roof_sample
+    roof_search = roof("search", "k_search", b_search,
+                       "n max(S,32) + psi_b|A| U + 48 P + 32 children + 52 NA + 56 NB + 8 L per pass (bench.algorithmic_bytes)")
+    roof_backup = roof("backup", "k_backup", b_backup,
+                       "12 children + 96 P + (psi_b|A| + 8) U per pass (bench.algorithmic_bytes)")
+    dominant = {"search": roof_search, "backup": roof_backup}.get(top) or roof_search
     kernel_table = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
                     for k, v in kinds.items()}
-    traffic = {"distinct_beliefs_per_step": st[0] / prof_steps, "distinct_actions_per_step": st[1] / prof_steps,
-               "psi_rows_staged_per_step": st[2] / prof_steps, "new_actions_per_step": st[5] / prof_steps,
-               "new_beliefs_per_step": st[6] / prof_steps}
+    names = ["interior_beliefs", "actions_visited", "psi_rows_staged", "search_launches", "row_levels",
+             "new_actions", "new_beliefs", "leaves", "psi_rows_read"]
+    traffic = {nm: st[i] / prof_steps for i, nm in enumerate(names)}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
@@ -292,8 +300,8 @@ def run_b200(args):
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
                     "ms_per_step": round(e2e_ms / args.steps, 4)},
             "gpu_launches": int(launches), "clocks": clk, "roofline": dominant,
-            "roofline_other": {"k_level_sample": roof_sample, "k_backup_v": roof_backup},
-            "kernels": kernel_table, "dominant_kernel": top, "level_traffic": traffic,
+            "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},
+            "kernels": kernel_table, "dominant_kernel": top, "traffic_per_step": traffic,
             "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1),
             "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
     if rank == 0 and not args.no_cpu_baseline:

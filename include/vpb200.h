@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 1
+#define VPB200_ABI_VERSION 2
 
 enum vp_status {
   VP_OK = 0,
@@ -75,7 +75,14 @@ typedef struct vp_model {
 } vp_model;
 
 /* Structure-of-arrays belief tree in HBM (tree.py:100-132 columns plus the
- * device-only hash indexes and backup scratch). */
+ * device-only hash indexes and backup scratch).
+ *
+ * Node ids are handed out by the device in completion order (one atomic per
+ * warp), not in the reference's first-occurrence order; every node records
+ * its creation key (pass << 32 | level << 24 | first row), and sorting by it
+ * reproduces the reference numbering exactly (tree.py:10-12, 180-256).  The
+ * host applies that permutation when it exports tables / traces, so the hot
+ * path needs no ordering scan. */
 typedef struct vp_tree {
   int32_t cap_beliefs, cap_actions;
   int32_t action_count;
@@ -87,87 +94,89 @@ typedef struct vp_tree {
   int32_t* b_parent_action;   /* -1 for the root                            */
   uint32_t* b_parent_obs;     /* 0xFFFFFFFF for the root                    */
   int32_t* b_depth;
-  void* psi;                  /* [cap_beliefs * |A|] float or double        */
+  void* psi;                  /* [cap_beliefs * psi_stride] float or double */
   double* b_lse;              /* cached (1/eta) log sum exp(eta PSI[b])      */
-  double* b_value;            /* backup scratch V                           */
-  double* b_weight;           /* backup scratch N                           */
-  uint32_t* b_stamp;          /* per-(iteration, level) visit stamp         */
-  uint8_t* b_flags;           /* bit 0: PSI row still equals init (lazy)    */
+  double* b_value;            /* leaf heuristic sum (search) / V (backup)    */
+  double* b_weight;           /* backup N: lifetime visits of valued actions */
+  int32_t* b_rows;            /* rows that reached b in the current pass     */
+  int32_t* b_done;            /* rows of b whose action completed (backup)   */
+  uint32_t* b_flags;          /* bit0: PSI row lazily == init; bit1: row not written */
+  uint64_t* b_ckey;           /* creation key (canonical order)              */
   /* action table A */
   int32_t* a_parent_belief;
   int32_t* a_action;
   double* a_reward;
   int32_t* a_visits;
-  double* a_num;              /* backup scratch sum V*N                      */
-  double* a_den;              /* backup scratch sum N                        */
-  uint32_t* a_stamp;
-  /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pad} */
+  double* a_num;              /* backup: sum V*N over valued children        */
+  double* a_den;              /* backup: sum N                               */
+  int32_t* a_rows;            /* rows through the action in the current pass */
+  int32_t* a_done;            /* rows of its children delivered (backup)     */
+  uint64_t* a_ckey;           /* creation key (canonical order)              */
+  /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */
   void* hash_b;               /* (action row << 32 | obs) -> belief row     */
-  int32_t* counters;          /* [0] n_beliefs [1] n_actions [2] overflow    */
+  int32_t* counters;          /* [0] n_beliefs [1] n_actions [2] overflow [3] 0 */
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
   double eta;
 } vp_tree;
 
-/* Per-plan row workspace (n = n_parallel rows) and per-level lists. */
+/* Per-search row workspace (n = n_parallel rows, n < 2^24). */
 typedef struct vp_work {
   int32_t n;
-  int32_t max_levels;         /* capacity of the level lists (>= d_max)     */
-  void* states;               /* [n * state_bytes]                          */
-  int32_t* slot_a;            /* per row hash slot (bit 31: pre-existing)   */
-  int32_t* slot_b;
-  uint32_t* obs;
-  double* reward;
-  int32_t* action;
-  int32_t* flist;             /* [(max_levels+1) * n] distinct beliefs/level */
-  int32_t* fcount;            /* [max_levels+1]                             */
-  int32_t* plist;             /* [max_levels * n] distinct action nodes/level*/
-  int32_t* pcount;            /* [max_levels]                               */
-  int32_t* level_base;        /* [2*(max_levels+1)] node counts per level    */
-  uint64_t* scan_status;      /* [ceil(n / VP_SCAN_TILE)] look-back words   */
-  uint32_t* scan_ticket;      /* [2]                                        */
+  int32_t max_levels;         /* deepest d_max this workspace serves (<= 255) */
+  void* states;               /* [n * state_bytes] start states (API search) */
+  int32_t* leaves;            /* [n] distinct leaf beliefs of the last search */
+  int32_t* leaf_count;        /* [1]                                        */
   int32_t* leaf_belief;       /* [n] frontier belief per row after search   */
   double* leaf_value;         /* [n] heuristic per row after search         */
-  unsigned long long* stats;  /* [8] or NULL: traffic counters summed over a plan:
-                                 0 distinct beliefs/level, 1 distinct actions/level,
-                                 2 PSI rows staged by the sampler, 3 sample launches,
-                                 4 rows sampled, 5 new actions, 6 new beliefs */
-  /* optional per-level traces (level-major, n each); NULL = off */
+  unsigned long long* stats;  /* [16] or NULL: traffic counters summed over calls:
+                                 0 interior beliefs backed up, 1 actions backed up,
+                                 2 PSI rows staged by the sampler, 3 search launches,
+                                 4 row-levels sampled, 5 new actions, 6 new beliefs,
+                                 7 leaves, 8 interior beliefs whose PSI row was not
+                                 lazily initial (rows the sampler must read) */
+  /* optional per-level traces (level-major, n each; device ids); NULL = off */
   int32_t* trace_action;
   uint32_t* trace_obs;
   int32_t* trace_anode;
   int32_t* trace_belief;
 } vp_work;
 
-#define VP_SCAN_TILE 128
-
-/* One search call (search.py:86-119). */
+/* One search call (search.py:86-119).  With `particles` set, every row first
+ * draws its start state from the particle belief (belief.py:37-44, fused);
+ * otherwise start states are read from work->states. */
 typedef struct vp_search_args {
   uint64_t search_key;        /* it_rng.derive(1).key (solver.py:102)       */
   int32_t depth0;             /* batch.depth                                */
   int32_t d_max;
-  uint32_t stamp_base;        /* unique per (plan, iteration)               */
-  int32_t iteration;
+  uint32_t pass;              /* search pass number (>= 1, increasing)      */
+  int32_t pad0;
   const int32_t* inject_actions; /* [d_max * n] level-major, or NULL       */
   const int32_t* start_beliefs;  /* [n] frontier at depth0, NULL = root     */
   const uint64_t* search_key_dev; /* device copy of search_key, or NULL     */
+  const void* particles;      /* [m * state_bytes] or NULL                  */
+  const double* cum_weights;  /* [m] cumsum of the particle weights         */
+  const uint64_t* draw_key_dev; /* device copy of draw_key, or NULL         */
+  uint64_t draw_key;          /* it_rng.derive(0).key (solver.py:98)        */
+  int32_t m;                  /* particles                                  */
+  int32_t pad1;
 } vp_search_args;
 
 /* A whole fixed-iteration planning step (solver.py:79-113) enqueued by one
- * call.  mode 2 (default): one persistent cooperative kernel with grid
- * barriers between phases; mode 1: one launch per phase, captured once into
- * a CUDA graph and replayed (re-captured when a pointer / size / model
- * parameter changes); mode 0: one launch per phase.  Host buffers must be
- * pinned; the caller synchronises the stream and then reads
- * out_host = {chosen action, n_beliefs, n_actions, overflow}. */
+ * call: per iteration one search kernel (root draw fused) and one backup
+ * kernel.  mode 1 (default): captured once into a CUDA graph and replayed
+ * (re-captured when a pointer / size / model parameter changes); mode 0:
+ * direct launches.  Host buffers must be pinned; the caller synchronises the
+ * stream and then reads out_host = {chosen action, n_beliefs, n_actions,
+ * overflow}. */
 typedef struct vp_plan_args {
   int32_t iterations;          /* fixed-iteration budget (>= 1)             */
   int32_t d_max_cap;
   int32_t m;                   /* particles                                 */
-  int32_t mode;                /* 0 kernels, 1 CUDA graph, 2 persistent     */
-  double gamma;
+  int32_t mode;                /* 0 kernels, 1 CUDA graph                   */
+  double gamma;                /* passes are numbered 1..iterations (fresh tree) */
   const void* particles_host;  /* [m * state_bytes] pinned, or NULL         */
   void* particles_dev;
   const double* cumw_host;     /* [m] cumsum(weights) pinned, or NULL       */
@@ -176,9 +185,6 @@ typedef struct vp_plan_args {
   uint64_t* keys_dev;
   int32_t* out_host;           /* [4] pinned                                */
   int32_t* out_dev;            /* [4]                                       */
-  uint64_t* timeline_dev;      /* mode 2 diagnostics: globaltimer stamp per  */
-  int32_t timeline_cap;        /* phase boundary (NULL / 0 = off)           */
-  int32_t pad0;
 } vp_plan_args;
 
 /* ---- library ---------------------------------------------------------- */
@@ -191,10 +197,8 @@ int32_t vp_last_cuda_error(void);
 int32_t vp_abi_layout(int32_t* out, int32_t n);
 
 /* ---- measurement -------------------------------------------------------- */
-/* Kernel kinds, in order: draw, level_sample, assign_actions, accum_probe,
- * assign_beliefs, leaf, backup_leaves, backup_q, backup_v, parent_lists,
- * argmax, tree_init, rehash, plan (persistent kernel). */
-#define VP_KERNEL_KINDS 14
+/* Kernel kinds, in order: draw, search, backup, tree_init, rehash, argmax, hooks. */
+#define VP_KERNEL_KINDS 7
 /* on != 0: clear and start recording a CUDA-event pair around every launch. */
 int32_t vp_profile_enable(int32_t on);
 /* Sum recorded durations (ms) and launch counts per kind; returns #kinds. */
@@ -211,18 +215,21 @@ int32_t vp_tree_rehash(const vp_tree* tree, void* stream);
 int32_t vp_tree_counts(const vp_tree* tree, int32_t* host_out, void* stream);
 
 /* ---- planning step pieces ---------------------------------------------- */
-/* Root-state draw (belief.py:37-44): u = uniform(draw_key, row); binary
- * search (side=right) in cum_weights[m]; gather packed particle records. */
+/* Root-state draw (belief.py:37-44) into work->states: u = uniform(draw_key,
+ * row); binary search (side=right) in cum_weights[m]; gather the particle. */
 int32_t vp_draw_root_states(const vp_model* model, const vp_work* work,
                             const void* particles, const double* cum_weights,
                             int32_t m, uint64_t draw_key, void* stream);
-/* All levels of one search call (search.py:106-118) + leaf heuristic
- * accumulation (search.py:119, backup.py:44-51). */
+/* All levels of one search call (search.py:86-119) in ONE kernel: per row and
+ * level the softmax draw, G(s,a), the (b,a) and (a,o) hash claims, reward /
+ * visit accumulation; then the leaf heuristic (search.py:119) and the
+ * distinct-leaf list for the backup. */
 int32_t vp_search(const vp_tree* tree, const vp_model* model, const vp_work* work,
                   const vp_search_args* args, void* stream);
-/* Level-synchronous backup d = d_max..depth0+1 (backup.py:75-114). */
-int32_t vp_backup(const vp_tree* tree, const vp_work* work, int32_t depth0,
-                  int32_t d_max, double gamma, uint32_t stamp_base, void* stream);
+/* Backup of the last search (backup.py:75-114) in ONE kernel: leaf means,
+ * then a bottom-up completion wave -- the last child to deliver completes its
+ * action (Q, PSI scatter), the last action completes its belief (LSE). */
+int32_t vp_backup(const vp_tree* tree, const vp_work* work, uint32_t pass, double gamma, void* stream);
 int32_t vp_plan(const vp_tree* tree, const vp_model* model, const vp_work* work,
                 const vp_plan_args* args, void* stream);
 /* argmax of PSI[0] with lowest-id ties (solver.py:112) into out_dev[0]. */

@@ -17,8 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libvpb200.so")
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
 VP_PSI_F32, VP_PSI_F64 = 0, 1
-VP_SCAN_TILE = 128
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
     C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
@@ -50,9 +49,10 @@ class VpTree(C.Structure):
         ("hmask_a", C.c_uint64), ("hmask_b", C.c_uint64),
         ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_depth", C.c_void_p),
         ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p), ("b_weight", C.c_void_p),
-        ("b_stamp", C.c_void_p), ("b_flags", C.c_void_p),
+        ("b_rows", C.c_void_p), ("b_done", C.c_void_p), ("b_flags", C.c_void_p), ("b_ckey", C.c_void_p),
         ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),
-        ("a_visits", C.c_void_p), ("a_num", C.c_void_p), ("a_den", C.c_void_p), ("a_stamp", C.c_void_p),
+        ("a_visits", C.c_void_p), ("a_num", C.c_void_p), ("a_den", C.c_void_p), ("a_rows", C.c_void_p),
+        ("a_done", C.c_void_p), ("a_ckey", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p), ("eta", C.c_double),
     ]
@@ -61,11 +61,8 @@ class VpTree(C.Structure):
 class VpWork(C.Structure):
     _fields_ = [
         ("n", C.c_int32), ("max_levels", C.c_int32), ("states", C.c_void_p),
-        ("slot_a", C.c_void_p), ("slot_b", C.c_void_p), ("obs", C.c_void_p), ("reward", C.c_void_p),
-        ("action", C.c_void_p), ("flist", C.c_void_p), ("fcount", C.c_void_p), ("plist", C.c_void_p),
-        ("pcount", C.c_void_p), ("level_base", C.c_void_p), ("scan_status", C.c_void_p),
-        ("scan_ticket", C.c_void_p), ("leaf_belief", C.c_void_p), ("leaf_value", C.c_void_p),
-        ("stats", C.c_void_p),
+        ("leaves", C.c_void_p), ("leaf_count", C.c_void_p), ("leaf_belief", C.c_void_p),
+        ("leaf_value", C.c_void_p), ("stats", C.c_void_p),
         ("trace_action", C.c_void_p), ("trace_obs", C.c_void_p), ("trace_anode", C.c_void_p),
         ("trace_belief", C.c_void_p),
     ]
@@ -74,8 +71,10 @@ class VpWork(C.Structure):
 class VpSearchArgs(C.Structure):
     _fields_ = [
         ("search_key", C.c_uint64), ("depth0", C.c_int32), ("d_max", C.c_int32),
-        ("stamp_base", C.c_uint32), ("iteration", C.c_int32),
+        ("pass_", C.c_uint32), ("pad0", C.c_int32),
         ("inject_actions", C.c_void_p), ("start_beliefs", C.c_void_p), ("search_key_dev", C.c_void_p),
+        ("particles", C.c_void_p), ("cum_weights", C.c_void_p), ("draw_key_dev", C.c_void_p),
+        ("draw_key", C.c_uint64), ("m", C.c_int32), ("pad1", C.c_int32),
     ]
 
 
@@ -87,7 +86,6 @@ class VpPlanArgs(C.Structure):
         ("cumw_host", C.c_void_p), ("cumw_dev", C.c_void_p),
         ("keys_host", C.c_void_p), ("keys_dev", C.c_void_p),
         ("out_host", C.c_void_p), ("out_dev", C.c_void_p),
-        ("timeline_dev", C.c_void_p), ("timeline_cap", C.c_int32), ("pad0", C.c_int32),
     ]
 
 
@@ -109,8 +107,7 @@ _SIGNATURES = [
      [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpSearchArgs), C.c_void_p]),
     ("vp_plan", C.c_int32,
      [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpPlanArgs), C.c_void_p]),
-    ("vp_backup", C.c_int32,
-     [C.POINTER(VpTree), C.POINTER(VpWork), C.c_int32, C.c_int32, C.c_double, C.c_uint32, C.c_void_p]),
+    ("vp_backup", C.c_int32, [C.POINTER(VpTree), C.POINTER(VpWork), C.c_uint32, C.c_double, C.c_void_p]),
     ("vp_root_argmax", C.c_int32, [C.POINTER(VpTree), C.c_void_p, C.c_void_p]),
     ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_rng_normal", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
@@ -127,8 +124,7 @@ _SIGNATURES = [
 
 EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)
 
-KERNEL_KINDS = ("draw", "level_sample", "assign_actions", "accum_probe", "assign_beliefs", "leaf",
-                "backup_leaves", "backup_q", "backup_v", "parent_lists", "argmax", "tree_init", "rehash", "plan")
+KERNEL_KINDS = ("draw", "search", "backup", "tree_init", "rehash", "argmax", "hooks")
 
 
 def profile_enable(on: bool):
@@ -188,11 +184,11 @@ def layout_mismatches() -> list:
     mine = [C.sizeof(VpModel), C.sizeof(VpTree), C.sizeof(VpWork), C.sizeof(VpSearchArgs),
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
-            VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset]
+            VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf"]
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

@@ -1,12 +1,13 @@
 """Device PORPP backup (API mirror of /root/reference/pkg/src/vecpomdp/backup.py).
 
-``backup(tree, leaves, d_max, eta, gamma)`` runs Alg. 3 level-synchronously on
-the device (csrc/vp_kernels.cu k_backup_*): leaf means and counts, then for
-d = d_max..1 the action Q values and PSI scatter over the distinct action
-nodes of level d-1 followed by the LSE of their parent beliefs.  The visited
-sets come from the per-level lists the device search recorded (the
-reference's valued(d) equals the beliefs visited at search level d, SURVEY.md
-section 0 finding 2), so no depth scan is needed.
+``backup(tree, leaves, d_max, eta, gamma)`` runs Alg. 3 on the device in ONE
+kernel (csrc/vp_phases.cuh backup_warp): leaf means and counts, then a
+bottom-up completion wave -- an action's Q and PSI scatter happen when its
+last valued child delivers, a belief's LSE when its last visited action
+completes.  That is the reference's level order restricted to each subtree:
+every node is updated after all of its valued children, exactly once, and
+the valued sets are the nodes the search visited (SURVEY.md section 0
+finding 2), so no depth scan is needed.
 """
 
 from __future__ import annotations
@@ -26,10 +27,10 @@ def _torch():
     return torch
 
 
-def run_backup(tree, work, depth0: int, d_max: int, gamma: float, stamp_base: int):
+def run_backup(tree, work, pass_: int, gamma: float):
     stream = _torch().cuda.current_stream().cuda_stream
-    _lib.call("vp_backup", C.byref(tree.struct), C.byref(work.struct), depth0, d_max, float(gamma), stamp_base,
-              stream)
+    _lib.call("vp_backup", C.byref(tree.struct), C.byref(work.struct), pass_, float(gamma), stream)
+    tree._scratch_dirty = False
 
 
 def backup(tree, leaves, d_max: int, eta: float, gamma: float) -> None:
@@ -43,7 +44,7 @@ def backup(tree, leaves, d_max: int, eta: float, gamma: float) -> None:
     if d_max != leaves.d_max:
         raise ValueError("d_max must match the search that produced the leaves")
     tree.set_eta(eta)
-    run_backup(tree, leaves.work, leaves.depth0, d_max, gamma, leaves.stamp_base)
+    run_backup(tree, leaves.work, leaves.pass_, gamma)
     tree.last_search = None
 
 

@@ -2,9 +2,8 @@
 //
 //  * counter-hash RNG, bit-identical to the reference RowRng
 //    (/root/reference/pkg/src/vecpomdp/rng.py:26-89);
-//  * open-addressing hash index with deterministic first-occurrence ids
+//  * open-addressing hash index claimed with one 128-bit CAS per probe
 //    (replaces tree.py:44-68 sorted-cache matching);
-//  * decoupled look-back tile scan used to number new nodes in batch order;
 //  * numpy-order pairwise summation (for the fp64 parity mode).
 #pragma once
 
@@ -58,25 +57,31 @@ __device__ __forceinline__ double normal_j(u64 key, u64 row, u64 j) {
 
 // ---------------------------------------------------------------- hashing
 
+// 16-byte slot of an open-addressing index.  Empty slots are all-ones (one
+// memset).  A claim is ONE 128-bit CAS {empty, unpublished} -> {key,
+// unpublished}: the winner numbers the node and publishes {id, pass} with a
+// 64-bit store; a loser gets the whole slot back from the failed CAS, so a
+// hit on a published node costs one L2 round trip.
 struct __align__(16) Slot {
   u64 key;
-  u32 id;   // final node id, or kPending|min_row while being claimed this level
-  u32 pad;
+  u32 id;    // node id, kUnpublished while the winner is still numbering it
+  u32 pass;  // search pass that created the node (0 after a rehash)
 };
 constexpr u64 kEmptyKey = ~0ull;
-constexpr u32 kEmptyId = 0xffffffffu;
-constexpr u32 kPending = 0x80000000u;
-constexpr u32 kExistBit = 0x80000000u;  // in per-row slot words
+constexpr u32 kUnpublished = 0xffffffffu;
 
 __device__ __forceinline__ u64 slot_hash(u64 key) { return mix64(key ^ 0x5851F42D4C957F2Dull); }
 
-__device__ __forceinline__ u64 ld_volatile_u64(const u64* p) { return *(volatile const u64*)p; }
 __device__ __forceinline__ u32 ld_volatile_u32(const u32* p) { return *(volatile const u32*)p; }
-// gpu-scope relaxed loads read L2 without invalidating L1 (an acquire would
-// emit CCTL.IVALL and throw away every warp's L1 lines on the SM).
+// gpu-scope relaxed loads read L2 (never a stale L1 line written by another SM)
 __device__ __forceinline__ u32 ld_relaxed_u32(const u32* p) {
   u32 v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
@@ -89,19 +94,6 @@ __device__ __forceinline__ double ld_relaxed_f64(const double* p) {
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ u32 ld_relaxed_u8(const uint8_t* p) {
-  unsigned short v;
-  asm volatile("ld.relaxed.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
-  return (u32)v;
-}
-__device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
-  u32 v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(u32* p, u32 v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -110,33 +102,76 @@ __device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
 __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// fire-and-forget reductions (REDG): nothing waits for them inside a kernel
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_min(uint64_t* p, u64 v) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// acq_rel add: releases this thread's earlier writes (REDs included) and
+// acquires everything released by earlier adders of the same counter.
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 
-// Find or claim `key`.  Returns the slot index; sets `existing` when the key
-// already carried a final id from an earlier phase.  New keys record the
-// minimum claiming row (first occurrence) via atomicMin on the id word; the
-// returned old id tells hits (< kPending) from claims, so a probe costs two
-// L2 atomics (CAS on the key, min on the id) and no plain loads.
-__device__ __forceinline__ u32 probe_claim(Slot* tab, u64 mask, u64 key, u32 row, bool& existing, u32& id) {
+__device__ __forceinline__ void cas128(void* p, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64& old_lo,
+                                       u64& old_hi) {
+  asm volatile(
+      "{\n .reg .b128 c, n, d;\n mov.b128 c, {%2, %3};\n mov.b128 n, {%4, %5};\n"
+      " atom.relaxed.gpu.global.cas.b128 d, [%6], c, n;\n mov.b128 {%0, %1}, d;\n}\n"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(p)
+      : "memory");
+}
+
+// Result of a claim: the slot, whether this thread created the key, and --
+// for a hit -- the published {id, pass} word (id == kUnpublished: the
+// creator has not numbered it yet; spin with wait_published).
+struct Claim {
+  u32 slot;
+  bool won;
+  u64 word;  // id | pass << 32
+};
+
+__device__ __forceinline__ Claim claim_key(Slot* tab, u64 mask, u64 key) {
   u64 h = slot_hash(key) & mask;
   while (true) {
-    const u64 prev = atomicCAS(&tab[h].key, kEmptyKey, key);
-    if (prev == kEmptyKey || prev == key) {
-      const u32 old = atomicMin(&tab[h].id, kPending | row);
-      existing = old < kPending;
-      id = existing ? old : kEmptyId;
-      return (u32)h;
-    }
+    u64 old_key, old_word;
+    cas128(&tab[h], kEmptyKey, ~0ull, key, ~0ull, old_key, old_word);
+    if (old_key == kEmptyKey) return Claim{(u32)h, true, ~0ull};
+    if (old_key == key) return Claim{(u32)h, false, old_word};
     h = (h + 1) & mask;
   }
 }
 
-// Plain insert of a known (key, id) pair; used by rehash.
+// Publication needs no release: everything other rows touch inside the
+// search kernel is either an accumulator (zero before the pass, updated with
+// L2 reductions) or derived from the slot word itself (the creating pass);
+// the columns the creator writes are read only by later kernels.
+__device__ __forceinline__ void publish(Slot* tab, u32 slot, u32 id, u32 pass) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(&tab[slot].id), "l"(((u64)pass << 32) | id) : "memory");
+}
+
+__device__ __forceinline__ u64 wait_published(const Slot* tab, u32 slot, u64 word) {
+  const u64* p = reinterpret_cast<const u64*>(&tab[slot].id);
+  while ((u32)word == kUnpublished) word = ld_relaxed_u64(p);
+  return word;
+}
+
+// Plain insert of a known (key, id) pair; used by rehash (pass 0 = "old").
 __device__ __forceinline__ void put_final(Slot* tab, u64 mask, u64 key, u32 id) {
   u64 h = slot_hash(key) & mask;
   while (true) {
     const u64 prev = atomicCAS(&tab[h].key, kEmptyKey, key);
     if (prev == kEmptyKey || prev == key) {
       tab[h].id = id;
+      tab[h].pass = 0;
       return;
     }
     h = (h + 1) & mask;
@@ -171,64 +206,6 @@ __device__ __forceinline__ T warp_inclusive_scan(T v) {
     if (lane >= o) v += w;
   }
   return v;
-}
-
-// ---------------------------------------------------------------- tile scan
-
-// Decoupled look-back: returns the exclusive prefix of `agg` over tiles in
-// ticket order.  Status word: epoch(32) | flag(2) | value(30).
-constexpr u64 kFlagAgg = 1, kFlagInc = 2;
-__device__ __forceinline__ u64 pack_status(u32 epoch, u64 flag, u32 v) {
-  return ((u64)epoch << 32) | (flag << 30) | (u64)(v & 0x3fffffffu);
-}
-
-__device__ __forceinline__ u32 tile_lookback(u64* status, int tile, u32 agg, u32 epoch) {
-  // called by one thread
-  if (tile == 0) {
-    st_release_u64(&status[0], pack_status(epoch, kFlagInc, agg));
-    return 0;
-  }
-  st_release_u64(&status[tile], pack_status(epoch, kFlagAgg, agg));
-  u32 excl = 0;
-  int j = tile - 1;
-  while (true) {
-    const u64 s = ld_acquire_u64(&status[j]);
-    if ((u32)(s >> 32) != epoch) continue;  // predecessor not published yet
-    excl += (u32)(s & 0x3fffffffu);
-    if (((s >> 30) & 3) == kFlagInc) break;
-    --j;
-  }
-  st_release_u64(&status[tile], pack_status(epoch, kFlagInc, excl + agg));
-  return excl;
-}
-
-// Warp-parallel variant (called by all 32 lanes of one warp): each round
-// inspects 32 predecessors at once, so a tile waits ~tiles/32 L2 round trips
-// instead of one per predecessor.
-__device__ __forceinline__ u32 tile_lookback_warp(u64* status, int tile, u32 agg, u32 epoch) {
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, tile == 0 ? kFlagInc : kFlagAgg, agg));
-  if (tile == 0) return 0;
-  u32 excl = 0;
-  int base = tile - 1;
-  while (true) {
-    const int j = base - lane;
-    const u64 s = j >= 0 ? ld_relaxed_u64(&status[j]) : pack_status(epoch, kFlagInc, 0);
-    const bool valid = (u32)(s >> 32) == epoch;
-    const u32 inc = __ballot_sync(0xffffffffu, valid && ((s >> 30) & 3) == kFlagInc);
-    const u32 bad = __ballot_sync(0xffffffffu, !valid);
-    const int limit = inc ? __ffs(inc) - 1 : 31;
-    const u32 upto = limit == 31 ? 0xffffffffu : ((2u << limit) - 1u);
-    if (bad & upto) continue;  // a needed predecessor has not published yet
-    u32 v = lane <= limit ? (u32)(s & 0x3fffffffu) : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (inc) break;
-    base -= 32;
-  }
-  if (lane == 0) st_release_u64(&status[tile], pack_status(epoch, kFlagInc, excl + agg));
-  return excl;
 }
 
 // ---------------------------------------------------------------- numpy-order sums

@@ -1,16 +1,10 @@
 // vp_kernels.cu -- B200 (sm_100a) kernels of the PORPP planning step and the
 // C ABI declared in include/vpb200.h.
 //
-// Two execution paths share the phase functions of vp_phases.cuh:
-//  * vp_plan: ONE persistent cooperative kernel per planning step
-//    (solver.py:79-113): tree reset, and per iteration the root draw, the
-//    d_max search levels and the d_max backup levels, separated by grid
-//    barriers.  Rows waiting for a node id published by the preceding
-//    numbering phase spin on the hash slot instead of taking a barrier, so a
-//    search level costs two grid barriers.
-//  * the API kernels (vp_search / vp_backup / hooks): one launch per phase.
-#include <cooperative_groups.h>
-
+// A planning pass (root draw + search + backup, solver.py:96-111) is two
+// kernel launches with no grid barrier (vp_phases.cuh); a fixed-iteration
+// planning step (vp_plan) is tree reset + 2 x iterations launches + the root
+// argmax, captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <cfloat>
 #include <cstddef>
@@ -24,17 +18,48 @@
 #include "vp_models.cuh"
 #include "vp_phases.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace vp {
 
 static thread_local cudaError_t g_last_cuda = cudaSuccess;
 
-// ================================================================== standalone kernels (API path)
+// ================================================================== kernels
 
 template <class PsiT, bool Exact>
 __global__ void k_tree_init(vp_tree T) {
   block_tree_init<PsiT, Exact>(T);
+}
+
+// Tree reset, part 1: every row the previous tree used gets zero accumulators
+// and an unset creation key, so node creation needs no initialising stores
+// that other rows would have to wait for (rows beyond the previous counts are
+// in that state since allocation).  Part 2 (k_tree_init) rewrites the root.
+__global__ void k_clear(vp_tree T) {
+  const int nb = min(T.counters[0], T.cap_beliefs), na = min(T.counters[1], T.cap_actions);
+  const int total = max(nb, na);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (i < nb) {
+      T.b_value[i] = 0.0;
+      T.b_weight[i] = 0.0;
+      T.b_rows[i] = 0;
+      T.b_done[i] = 0;
+      T.b_ckey[i] = ~0ull;
+    }
+    if (i < na) {
+      T.a_reward[i] = 0.0;
+      T.a_visits[i] = 0;
+      T.a_num[i] = 0.0;
+      T.a_den[i] = 0.0;
+      T.a_rows[i] = 0;
+      T.a_done[i] = 0;
+      T.a_ckey[i] = ~0ull;
+    }
+  }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms && cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) g_num_sms = 148;
+  return g_num_sms;
 }
 
 __global__ void k_rehash(vp_tree T) {
@@ -53,21 +78,11 @@ __global__ void k_rehash(vp_tree T) {
   }
 }
 
+// Root-state draw into work.states (hook / iterative path; vp_plan fuses it into k_search).
 template <class Model>
-__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key,
-                       const u64* key_dev) {
-  phase_draw<Model>(W, particles, cumw, m, key_dev ? *key_dev : key, this_span());
-}
-
-__device__ __forceinline__ LevelArgs level_args(const vp_search_args& S, int level, u32 stamp) {
-  LevelArgs L;
-  L.level = level;
-  L.depth0 = S.depth0;
-  L.lkey = fold(S.search_key_dev ? *S.search_key_dev : S.search_key, (u64)level);  // search.py:107
-  L.stamp = stamp;
-  L.inject = S.inject_actions;
-  L.start = S.start_beliefs;
-  return L;
+__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < W.n) reinterpret_cast<typename Model::State*>(W.states)[r] = draw_state(particles, cumw, m, key, r);
 }
 
 template <class PsiT>
@@ -86,59 +101,36 @@ __device__ __forceinline__ Stage<PsiT> make_stage(unsigned char* smem, u64* bars
   return sg;
 }
 
-template <class Model, class PsiT>
-__global__ void __launch_bounds__(128) k_level_sample(vp_tree T, vp_model M, vp_work W, vp_search_args S, int level,
-                                                      u32 stamp, StageCfg sc) {
+// One search call: every warp carries 32 rows through all levels.
+template <class Model, class PsiT, bool Exact>
+__global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_model M, vp_work W, vp_search_args S,
+                                                              StageCfg sc) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) u64 s_bar[4];
+  __shared__ __align__(8) u64 s_bar[kSearchWarps];
+  const int A = T.action_count;
   Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, sc);
-  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)4 * sc.rows * sc.stride;
-  phase_sample_fast<Model, PsiT>(T, M, W, level_args(S, level, stamp), sg, init_cdf, this_span());
-}
-
-template <class Model>
-__global__ void __launch_bounds__(128) k_level_sample_exact(vp_tree T, vp_model M, vp_work W, vp_search_args S,
-                                                            int level, u32 stamp) {
-  phase_sample_exact<Model>(T, M, W, level_args(S, level, stamp), this_span());
-}
-
-template <int WhichTable>
-__global__ void __launch_bounds__(VP_SCAN_TILE) k_assign(vp_tree T, vp_work W, int level, u32 epoch) {
-  phase_assign<WhichTable>(T, W, level, epoch, W.scan_ticket);
-}
-
-__global__ void __launch_bounds__(128) k_accum_probe(vp_tree T, vp_work W, int level, u32 stamp) {
-  phase_accum(T, W, level, stamp, this_span());
-}
-
-template <class Model>
-__global__ void __launch_bounds__(128) k_leaf(vp_tree T, vp_model M, vp_work W, vp_search_args S, int dmax,
-                                              u32 stamp) {
-  phase_leaf<Model>(T, M, W, level_args(S, dmax, stamp), this_span());
-}
-
-template <class PsiT>
-__global__ void k_backup_leaves(vp_tree T, vp_work W, int dmax, int mat) {
-  phase_backup_leaves<PsiT>(T, W, dmax, mat, this_span());
-}
-
-template <class PsiT>
-__global__ void k_materialise(vp_tree T, vp_work W, int lvl) {
-  phase_materialise<PsiT>(T, W, lvl, this_span());
-}
-
-template <class PsiT>
-__global__ void k_backup_q(vp_tree T, vp_work W, int lvl, double gamma) {
-  phase_backup_q<PsiT>(T, W, lvl, gamma, this_span());
+  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)kSearchWarps * sc.rows * sc.stride;
+  PsiT* init_row = init_cdf + A;
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
+    init_row[a] = (PsiT)T.init_prefs[a];
+  }
+  // the leaf counter of the NEXT pass is reset here: its previous user (the
+  // backup of the pass before this one) has finished
+  if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;
+  __syncthreads();
+  const int wi = blockIdx.x * kSearchWarps + (threadIdx.x >> 5);
+  if (wi * 32 >= W.n) return;
+  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi);
 }
 
 template <class PsiT, bool Exact>
-__global__ void k_backup_v(vp_tree T, vp_work W, int lvl, int mat) {
-  phase_backup_v<PsiT, Exact>(T, W, lvl, mat, this_span());
-}
-
-__global__ void k_parent_lists(vp_tree T, vp_work W, int d, u32 stamp) {
-  phase_parent_lists(T, W, d, stamp, this_span());
+__global__ void __launch_bounds__(kBackupWarps * 32) k_backup(vp_tree T, vp_work W, u32 pass, double gamma) {
+  __shared__ double s_v[kBackupWarps][32];
+  const int warp = threadIdx.x >> 5;
+  const int wi = blockIdx.x * kBackupWarps + warp;
+  if (wi * 32 >= W.leaf_count[pass & 1u]) return;
+  backup_warp<PsiT, Exact>(T, W, pass, gamma, wi, s_v[warp]);
 }
 
 template <class PsiT>
@@ -148,120 +140,6 @@ __global__ void k_root_argmax(vp_tree T, int* out) {
 
 __global__ void k_copy_counters(vp_tree T, int* out) {
   if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x];
-}
-
-// ================================================================== persistent planning kernel
-
-struct PlanParams {
-  vp_tree T;
-  vp_model M;
-  vp_work W;
-  int iterations, d_max_cap, m;
-  double gamma;
-  const void* particles;
-  const double* cumw;
-  const u64* keys;  // [2 * iterations]: (draw key, search key) per iteration
-  int* out;         // [4]
-  StageCfg sc;
-  u64* timeline;    // optional: globaltimer at each phase boundary (block 0)
-  int timeline_cap;
-};
-
-__device__ __forceinline__ u64 global_ns() {
-  u64 t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// One whole fixed-iteration planning step.  Barrier pattern per iteration
-// with d = d_max:  draw | A(0) | B(0) C(0) | D(0) A(1) | ... | D(d-1) leaf |
-// backup leaves | (Q | V |) x d, where B/D number new nodes, C/A(next)/leaf
-// spin on the ids they publish, and Q/V are the backup's action and belief
-// halves of each level.
-template <class Model, class PsiT, bool Exact>
-__global__ void __launch_bounds__(kStageWarps * 32) k_plan(PlanParams P) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) u64 s_bar[kStageWarps];
-  cg::grid_group grid = cg::this_grid();
-  // grid barrier + gpu-scope fence: the fence also invalidates this SM's L1
-  // (CCTL.IVALL), so plain loads after the barrier never hit lines cached
-  // before another SM rewrote them (e.g. a lazily materialised PSI row that
-  // shares a 128-B line with a row read earlier).
-  auto barrier = [&]() {
-    grid.sync();
-    __threadfence();
-  };
-  const vp_tree& T = P.T;
-  const vp_work& W = P.W;
-  const Span sp = this_span();
-  const int L = W.max_levels;
-  Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, P.sc);
-  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)kStageWarps * P.sc.rows * P.sc.stride;
-  typedef typename Model::State State;
-
-  int tl = 0;
-  auto mark = [&]() {
-    if (P.timeline && blockIdx.x == 0 && threadIdx.x == 0 && tl < P.timeline_cap) P.timeline[tl++] = global_ns();
-  };
-  mark();
-  if (blockIdx.x == 0) block_tree_init<PsiT, Exact>(T);
-  int d = 1;
-  for (int it = 0; it < P.iterations; ++it) {
-    const u32 stamp_base = (u32)it * (u32)(L + 3);
-    const u64 skey = P.keys[2 * it + 1];
-    if (sp.gtid <= d) W.fcount[sp.gtid] = 0;
-    if (sp.gtid < d) W.pcount[sp.gtid] = 0;
-    phase_draw<Model>(W, reinterpret_cast<const State*>(P.particles), P.cumw, P.m, P.keys[2 * it], sp);
-    barrier();
-    mark();
-    for (int l = 0; l < d; ++l) {
-      LevelArgs la;
-      la.level = l;
-      la.depth0 = 0;
-      la.lkey = fold(skey, (u64)l);
-      la.stamp = stamp_base + (u32)l + 1u;
-      la.inject = nullptr;
-      la.start = nullptr;
-      const u32 epoch = 1u + 2u * ((u32)it * (u32)(L + 1) + (u32)l);
-      if constexpr (Exact) phase_sample_exact<Model>(T, P.M, W, la, sp);
-      else phase_sample_fast<Model, PsiT>(T, P.M, W, la, sg, init_cdf, sp);
-      barrier();
-      mark();
-      phase_assign<0>(T, W, l, epoch, nullptr);
-      phase_accum(T, W, l, la.stamp, sp);
-      barrier();
-      mark();
-      phase_assign<1>(T, W, l, epoch + 1u, nullptr);
-    }
-    {
-      LevelArgs la;
-      la.level = d;
-      la.depth0 = 0;
-      la.lkey = 0;
-      la.stamp = stamp_base + (u32)d + 1u;
-      la.inject = nullptr;
-      la.start = nullptr;
-      phase_leaf<Model>(T, P.M, W, la, sp);
-    }
-    barrier();
-    mark();
-    phase_backup_leaves<PsiT>(T, W, d, d - 1, sp);
-    barrier();
-    mark();
-    for (int lv = d - 1; lv >= 0; --lv) {
-      phase_backup_q<PsiT>(T, W, lv, P.gamma, sp);
-      barrier();
-      mark();
-      phase_backup_v<PsiT, Exact>(T, W, lv, lv - 1, sp);
-      barrier();
-      mark();
-    }
-    d = d + 1 < P.d_max_cap ? d + 1 : P.d_max_cap;
-  }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    warp_root_argmax<PsiT>(T, P.out);
-    if (threadIdx.x < 3) P.out[1 + threadIdx.x] = T.counters[threadIdx.x];
-  }
 }
 
 // ================================================================== host side
@@ -278,10 +156,8 @@ static int32_t check_launch() {
 }
 
 // ---- per-launch accounting: launch counter + optional CUDA-event timing by kernel kind
-enum KernelKind {
-  KK_DRAW = 0, KK_LEVEL_SAMPLE, KK_ASSIGN_ACTIONS, KK_ACCUM_PROBE, KK_ASSIGN_BELIEFS, KK_LEAF,
-  KK_BACKUP_LEAVES, KK_BACKUP_Q, KK_BACKUP_V, KK_PARENT_LISTS, KK_ARGMAX, KK_TREE_INIT, KK_REHASH, KK_PLAN, KK_COUNT
-};
+enum KernelKind { KK_DRAW = 0, KK_SEARCH, KK_BACKUP, KK_TREE_INIT, KK_REHASH, KK_ARGMAX, KK_HOOK, KK_COUNT };
+static_assert(KK_COUNT == VP_KERNEL_KINDS, "kernel kinds out of sync with vpb200.h");
 struct ProfRec {
   int kind;
   cudaEvent_t a, b;
@@ -358,95 +234,65 @@ static int env_int(const char* name, int dflt) {
 // Staged-row geometry: rows padded to an odd number of 16-B chunks so the
 // LDS.128 scans of 8 lanes in different rows hit different bank groups.
 template <class PsiT>
-static StageCfg stage_cfg(int A, int warps, int budget_bytes) {
+static StageCfg stage_cfg(int A, int per_warp_bytes) {
   int chunks = (int)(((size_t)A * sizeof(PsiT) + 15) / 16);
   if ((chunks & 1) == 0) ++chunks;
   StageCfg c;
   c.stride = chunks * 16 / (int)sizeof(PsiT);
-  c.rows = std::max(1, std::min(32, budget_bytes / warps / (chunks * 16)));
+  c.rows = std::max(1, std::min(32, per_warp_bytes / (chunks * 16)));
   return c;
 }
-// staged rows of every warp + the block's copy of the initial-row CDF
-template <class PsiT>
-static size_t stage_bytes(const StageCfg& c, int warps, int A) {
-  return ((size_t)warps * c.rows * c.stride + (size_t)A) * sizeof(PsiT);
+
+// Search launch geometry: staged rows of every warp + the block's copies of
+// the initial row and its CDF.
+template <class PsiT, bool Exact>
+static int32_t search_geometry(int A, StageCfg& sc, size_t& smem) {
+  sc = Exact ? StageCfg{0, 4} : stage_cfg<PsiT>(A, env_int("VP_STAGE_KB", 32) * 1024);
+  smem = ((size_t)kSearchWarps * sc.rows * sc.stride + 2 * (size_t)A) * sizeof(PsiT);
+  return VP_OK;
 }
 
 template <class Model, class PsiT, bool Exact>
-static int32_t set_sample_attr(size_t smem) {
-  if constexpr (!Exact) {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(k_level_sample<Model, PsiT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return VP_ERR_CUDA;
-      configured = smem;
-    }
+static int32_t set_search_attr(size_t smem) {
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    if (cudaFuncSetAttribute(k_search<Model, PsiT, Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return check_launch() ? VP_ERR_CUDA : VP_ERR_CUDA;
+    configured = smem;
   }
   return VP_OK;
 }
 
 template <class Model, class PsiT, bool Exact>
-static int32_t run_search(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
-                          cudaStream_t st) {
-  const int n = W.n;
-  const int grid = blocks_for(n, 128);
-  const int tiles = blocks_for(n, VP_SCAN_TILE);
-  if (cudaMemsetAsync(W.fcount, 0, sizeof(int32_t) * (W.max_levels + 1), st) != cudaSuccess) return VP_ERR_CUDA;
-  if (cudaMemsetAsync(W.pcount, 0, sizeof(int32_t) * W.max_levels, st) != cudaSuccess) return VP_ERR_CUDA;
-  if (cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * tiles, st) != cudaSuccess) return VP_ERR_CUDA;
-  if (cudaMemsetAsync(W.scan_ticket, 0, sizeof(uint32_t), st) != cudaSuccess) return VP_ERR_CUDA;
-  StageCfg sc{0, 0};
-  size_t smem = 0;
-  if constexpr (!Exact) {
-    sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
-    smem = stage_bytes<PsiT>(sc, 4, T.action_count);
-    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(smem)) return rc;
+static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
+                             cudaStream_t st) {
+  StageCfg sc;
+  size_t smem;
+  search_geometry<PsiT, Exact>(T.action_count, sc, smem);
+  if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
+  const int grid = blocks_for(blocks_for(W.n, 32), kSearchWarps);
+  {
+    Launch L_(KK_SEARCH, st);
+    k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc);
   }
-  for (int l = S.depth0; l < S.d_max; ++l) {
-    const u32 stamp = S.stamp_base + (u32)l + 1u;
-    {
-      Launch L_(KK_LEVEL_SAMPLE, st);
-      if constexpr (Exact) k_level_sample_exact<Model><<<grid, 128, 0, st>>>(T, M, W, S, l, stamp);
-      else k_level_sample<Model, PsiT><<<grid, 128, smem, st>>>(T, M, W, S, l, stamp, sc);
-    }
-    { Launch L_(KK_ASSIGN_ACTIONS, st); k_assign<0><<<tiles, VP_SCAN_TILE, 0, st>>>(T, W, l, (u32)(2 * l + 1)); }
-    { Launch L_(KK_ACCUM_PROBE, st); k_accum_probe<<<grid, 128, 0, st>>>(T, W, l, stamp); }
-    { Launch L_(KK_ASSIGN_BELIEFS, st); k_assign<1><<<tiles, VP_SCAN_TILE, 0, st>>>(T, W, l, (u32)(2 * l + 2)); }
-  }
-  { Launch L_(KK_LEAF, st); k_leaf<Model><<<grid, 128, 0, st>>>(T, M, W, S, S.d_max, S.stamp_base + (u32)S.d_max + 1u); }
   return check_launch();
 }
 
 template <class PsiT, bool Exact>
-static int32_t run_backup(const vp_tree& T, const vp_work& W, int depth0, int dmax, double gamma, u32 stamp_base,
-                          cudaStream_t st) {
-  const int n = W.n;
-  const int grid = blocks_for(n, 256);
-  const int wgrid = std::min(blocks_for((long long)n * 32, 256), 148 * 32);
-  const int vgrid = Exact ? std::max(grid, wgrid) : wgrid;
-  if (dmax < 1) return VP_OK;
-  // lists of level L exist (recorded by search) for depth0 <= L <= dmax
-  auto recorded = [&](int L) { return L >= depth0 && L >= 0 ? L : -1; };
-  { Launch L_(KK_BACKUP_LEAVES, st); k_backup_leaves<PsiT><<<wgrid, 256, 0, st>>>(T, W, dmax, recorded(dmax - 1)); }
-  for (int d = dmax; d >= 1; --d) {
-    if (d <= depth0) {
-      if (cudaMemsetAsync(W.pcount + (d - 1), 0, sizeof(int32_t), st) != cudaSuccess) return VP_ERR_CUDA;
-      if (cudaMemsetAsync(W.fcount + (d - 1), 0, sizeof(int32_t), st) != cudaSuccess) return VP_ERR_CUDA;
-      { Launch L_(KK_PARENT_LISTS, st); k_parent_lists<<<grid, 256, 0, st>>>(T, W, d, stamp_base + 0x40000000u + (u32)d); }
-      { Launch L_(KK_PARENT_LISTS, st); k_materialise<PsiT><<<wgrid, 256, 0, st>>>(T, W, d - 1); }
-    }
-    { Launch L_(KK_BACKUP_Q, st); k_backup_q<PsiT><<<grid, 256, 0, st>>>(T, W, d - 1, gamma); }
-    { Launch L_(KK_BACKUP_V, st); k_backup_v<PsiT, Exact><<<vgrid, 256, 0, st>>>(T, W, d - 1, d >= 2 ? recorded(d - 2) : -1); }
+static int32_t launch_backup(const vp_tree& T, const vp_work& W, u32 pass, double gamma, cudaStream_t st) {
+  const int grid = blocks_for(blocks_for(W.n, 32), kBackupWarps);
+  {
+    Launch L_(KK_BACKUP, st);
+    k_backup<PsiT, Exact><<<grid, kBackupWarps * 32, 0, st>>>(T, W, pass, gamma);
   }
   return check_launch();
 }
 
 // ---- whole planning step
 
-template <class Model, class PsiT, bool Exact>
-static int32_t enqueue_inputs(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
-                              cudaStream_t st) {
+template <class Model>
+static int32_t enqueue_inputs(const vp_tree& T, const vp_work& W, const vp_plan_args& P, cudaStream_t st) {
   typedef typename Model::State State;
   if (P.keys_host &&
       cudaMemcpyAsync(P.keys_dev, P.keys_host, 16 * (size_t)P.iterations, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -459,91 +305,41 @@ static int32_t enqueue_inputs(const vp_tree& T, const vp_model& M, const vp_work
     return VP_ERR_CUDA;
   if (cudaMemsetAsync(T.hash_a, 0xff, (T.hmask_a + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(T.hash_b, 0xff, (T.hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
+  if (cudaMemsetAsync(W.leaf_count, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return VP_ERR_CUDA;
   return VP_OK;
 }
 
-// Multi-kernel version of a planning step (one launch per phase).
+template <class PsiT, bool Exact>
+static int32_t enqueue_tree_reset(const vp_tree& T, cudaStream_t st) {
+  { Launch L_(KK_TREE_INIT, st); k_clear<<<num_sms() * 4, 256, 0, st>>>(T); }
+  { Launch L_(KK_TREE_INIT, st); k_tree_init<PsiT, Exact><<<1, 256, 0, st>>>(T); }
+  return check_launch();
+}
+
+// The launches of one fixed-iteration planning step.
 template <class Model, class PsiT, bool Exact>
 static int32_t enqueue_plan_kernels(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
                                     cudaStream_t st) {
-  typedef typename Model::State State;
-  if (int32_t rc = enqueue_inputs<Model, PsiT, Exact>(T, M, W, P, st)) return rc;
-  { Launch L_(KK_TREE_INIT, st); k_tree_init<PsiT, Exact><<<1, 256, 0, st>>>(T); }
-  const u64* keys = reinterpret_cast<const u64*>(P.keys_dev);
+  if (int32_t rc = enqueue_inputs<Model>(T, W, P, st)) return rc;
+  if (int32_t rc = enqueue_tree_reset<PsiT, Exact>(T, st)) return rc;
   int d = 1;
   for (int it = 0; it < P.iterations; ++it) {
-    // the API kernels read the keys from device memory via search_key_dev
-    {
-      Launch L_(KK_DRAW, st);
-      k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(W, reinterpret_cast<const State*>(P.particles_dev),
-                                                         P.cumw_dev, P.m, 0ull, keys + 2 * it);
-    }
     vp_search_args S;
     memset(&S, 0, sizeof(S));
-    S.search_key_dev = P.keys_dev + 2 * it + 1;
+    S.depth0 = 0;
     S.d_max = d;
-    S.stamp_base = (u32)it * (u32)(W.max_levels + 3);
-    S.iteration = it;
-    int32_t rc = run_search<Model, PsiT, Exact>(T, M, W, S, st);
-    if (rc) return rc;
-    rc = run_backup<PsiT, Exact>(T, W, 0, d, P.gamma, S.stamp_base, st);
-    if (rc) return rc;
+    S.pass = (u32)it + 1u;  // the tree is fresh: passes restart at 1
+    S.search_key_dev = P.keys_dev + 2 * it + 1;
+    S.particles = P.particles_dev;
+    S.cum_weights = P.cumw_dev;
+    S.draw_key_dev = P.keys_dev + 2 * it;
+    S.m = P.m;
+    if (int32_t rc = launch_search<Model, PsiT, Exact>(T, M, W, S, st)) return rc;
+    if (int32_t rc = launch_backup<PsiT, Exact>(T, W, S.pass, P.gamma, st)) return rc;
     d = std::min(d + 1, P.d_max_cap);
   }
   { Launch L_(KK_ARGMAX, st); k_root_argmax<PsiT><<<1, 32, 0, st>>>(T, P.out_dev); }
   { Launch L_(KK_ARGMAX, st); k_copy_counters<<<1, 32, 0, st>>>(T, P.out_dev); }
-  if (P.out_host &&
-      cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
-    return VP_ERR_CUDA;
-  return check_launch();
-}
-
-static int g_num_sms = 0;
-
-// Persistent version: inputs, tree reset, ONE cooperative kernel, result.
-template <class Model, class PsiT, bool Exact>
-static int32_t enqueue_plan_persistent(const vp_tree& T, const vp_model& M, const vp_work& W,
-                                       const vp_plan_args& P, cudaStream_t st) {
-  if (int32_t rc = enqueue_inputs<Model, PsiT, Exact>(T, M, W, P, st)) return rc;
-  const int tiles = blocks_for(W.n, VP_SCAN_TILE);
-  if (cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * tiles, st) != cudaSuccess) return VP_ERR_CUDA;
-  PlanParams pp;
-  pp.T = T;
-  pp.M = M;
-  pp.W = W;
-  pp.iterations = P.iterations;
-  pp.d_max_cap = P.d_max_cap;
-  pp.m = P.m;
-  pp.gamma = P.gamma;
-  pp.particles = P.particles_dev;
-  pp.cumw = P.cumw_dev;
-  pp.keys = reinterpret_cast<const u64*>(P.keys_dev);
-  pp.out = P.out_dev;
-  pp.timeline = reinterpret_cast<u64*>(P.timeline_dev);
-  pp.timeline_cap = P.timeline_cap;
-  pp.sc = Exact ? StageCfg{1, 4} : stage_cfg<PsiT>(T.action_count, kStageWarps, env_int("VP_PLAN_STAGE_KB", 96) * 1024);
-  const size_t smem = Exact ? 16 : stage_bytes<PsiT>(pp.sc, kStageWarps, T.action_count);
-  auto kern = k_plan<Model, PsiT, Exact>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return check_launch();
-    configured = smem;
-  }
-  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageWarps * 32, smem) != cudaSuccess ||
-      per_sm < 1)
-    return check_launch();
-  per_sm = std::min(per_sm, env_int("VP_PLAN_BLOCKS_PER_SM", 4));
-  const int grid = std::max(1, g_num_sms * per_sm);
-  void* args[] = {&pp};
-  {
-    Launch L_(KK_PLAN, st);
-    if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kStageWarps * 32), args, smem, st) !=
-        cudaSuccess)
-      return check_launch();
-  }
   if (P.out_host &&
       cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return VP_ERR_CUDA;
@@ -566,15 +362,16 @@ static void append_pod(std::vector<unsigned char>& v, const T& x) {
   v.insert(v.end(), p, p + sizeof(T));
 }
 
-// mode 0: multi-kernel direct; 1: multi-kernel captured into a CUDA graph
-// (replayed while pointers / sizes / model are unchanged); 2: persistent.
+// mode 0: direct launches; 1: captured into a CUDA graph (replayed while
+// pointers / sizes / model are unchanged).
 template <class Model, class PsiT, bool Exact>
 static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_plan_args& P,
                         cudaStream_t st) {
-  if (P.mode == 2) return enqueue_plan_persistent<Model, PsiT, Exact>(T, M, W, P, st);
-  if constexpr (!Exact) {
-    const StageCfg sc = stage_cfg<PsiT>(T.action_count, 4, env_int("VP_STAGE_KB", 200) * 1024);
-    if (int32_t rc = set_sample_attr<Model, PsiT, Exact>(stage_bytes<PsiT>(sc, 4, T.action_count))) return rc;
+  {
+    StageCfg sc;
+    size_t smem;
+    search_geometry<PsiT, Exact>(T.action_count, sc, smem);
+    if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);
   std::vector<unsigned char> key;
@@ -582,7 +379,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   append_pod(key, M);
   append_pod(key, W);
   append_pod(key, P);
-  const int budget = env_int("VP_STAGE_KB", 200);
+  const int budget = env_int("VP_STAGE_KB", 32);
   append_pod(key, budget);
   GraphEntry* hit = nullptr;
   for (auto& e : g_graphs)
@@ -759,7 +556,9 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)sizeof(Slot),
                        (int32_t)sizeof(vp_plan_args),
                        (int32_t)offsetof(vp_plan_args, out_dev),
-                       (int32_t)offsetof(vp_tree, init_cdf)};
+                       (int32_t)offsetof(vp_tree, init_cdf),
+                       (int32_t)offsetof(vp_tree, a_ckey),
+                       (int32_t)offsetof(vp_search_args, m)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];
@@ -773,10 +572,7 @@ int32_t vp_tree_init(const vp_tree* t, void* stream) {
   if (cudaMemsetAsync(t->hash_b, 0xff, (t->hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
   const vp_tree T = *t;
   return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
-    typedef decltype(z) PsiT;
-    Launch L_(KK_TREE_INIT, st);
-    k_tree_init<PsiT, decltype(ex)::value><<<1, 256, 0, st>>>(T);
-    return check_launch();
+    return enqueue_tree_reset<decltype(z), decltype(ex)::value>(T, st);
   });
 }
 
@@ -785,7 +581,7 @@ int32_t vp_tree_rehash(const vp_tree* t, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(t->hash_a, 0xff, (t->hmask_a + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(t->hash_b, 0xff, (t->hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
-  { Launch L_(KK_REHASH, st); k_rehash<<<148 * 8, 256, 0, st>>>(*t); }
+  { Launch L_(KK_REHASH, st); k_rehash<<<num_sms() * 8, 256, 0, st>>>(*t); }
   return check_launch();
 }
 
@@ -798,9 +594,11 @@ int32_t vp_tree_counts(const vp_tree* t, int32_t* host_out, void* stream) {
   return VP_OK;
 }
 
+static bool work_ok(const vp_work& W) { return W.n >= 1 && W.n < (1 << 24) && W.max_levels >= 1 && W.max_levels <= 255; }
+
 int32_t vp_draw_root_states(const vp_model* m, const vp_work* w, const void* particles, const double* cumw,
                             int32_t count, uint64_t key, void* stream) {
-  if (!m || !w || !particles || !cumw || count < 1 || w->n < 1) return VP_ERR_INVALID;
+  if (!m || !w || !particles || !cumw || count < 1 || !work_ok(*w)) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   const vp_work W = *w;
   return dispatch_model(m->kind, [&](auto mdl) -> int32_t {
@@ -808,14 +606,15 @@ int32_t vp_draw_root_states(const vp_model* m, const vp_work* w, const void* par
     if (!state_size_ok<Model>(*m)) return VP_ERR_INVALID;
     Launch L_(KK_DRAW, st);
     k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(
-        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key, nullptr);
+        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key);
     return check_launch();
   });
 }
 
 int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_search_args* a, void* stream) {
-  if (!t || !m || !w || !a) return VP_ERR_INVALID;
-  if (a->depth0 < 0 || a->d_max < a->depth0 || a->d_max > w->max_levels) return VP_ERR_INVALID;
+  if (!t || !m || !w || !a || !work_ok(*w)) return VP_ERR_INVALID;
+  if (a->depth0 < 0 || a->d_max < a->depth0 || a->d_max > w->max_levels || a->pass < 1) return VP_ERR_INVALID;
+  if (a->particles && (!a->cum_weights || a->m < 1)) return VP_ERR_INVALID;
   if (m->action_count != t->action_count) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   const vp_tree T = *t;
@@ -826,15 +625,15 @@ int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const v
     typedef decltype(mdl) Model;
     if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
     return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
-      return run_search<Model, decltype(z), decltype(ex)::value>(T, M, W, S, st);
+      return launch_search<Model, decltype(z), decltype(ex)::value>(T, M, W, S, st);
     });
   });
 }
 
 int32_t vp_plan(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_plan_args* p, void* stream) {
-  if (!t || !m || !w || !p) return VP_ERR_INVALID;
+  if (!t || !m || !w || !p || !work_ok(*w)) return VP_ERR_INVALID;
   if (p->iterations < 1 || p->d_max_cap < 1 || p->m < 1 || !p->keys_dev || !p->particles_dev || !p->cumw_dev ||
-      !p->out_dev)
+      !p->out_dev || (p->mode != 0 && p->mode != 1))
     return VP_ERR_INVALID;
   if (std::min(p->iterations, p->d_max_cap) > w->max_levels) return VP_ERR_INVALID;
   if (m->action_count != t->action_count) return VP_ERR_INVALID;
@@ -852,14 +651,13 @@ int32_t vp_plan(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_
   });
 }
 
-int32_t vp_backup(const vp_tree* t, const vp_work* w, int32_t depth0, int32_t d_max, double gamma,
-                  uint32_t stamp_base, void* stream) {
-  if (!t || !w || depth0 < 0 || d_max < depth0 || d_max > w->max_levels) return VP_ERR_INVALID;
+int32_t vp_backup(const vp_tree* t, const vp_work* w, uint32_t pass, double gamma, void* stream) {
+  if (!t || !w || !work_ok(*w) || pass < 1) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   const vp_tree T = *t;
   const vp_work W = *w;
   return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
-    return run_backup<decltype(z), decltype(ex)::value>(T, W, depth0, d_max, gamma, stamp_base, st);
+    return launch_backup<decltype(z), decltype(ex)::value>(T, W, pass, gamma, st);
   });
 }
 

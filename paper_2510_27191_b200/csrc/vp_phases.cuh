@@ -1,18 +1,25 @@
-// vp_phases.cuh -- the phases of one PORPP planning step as __device__
-// functions over a grid-stride index space.  They run either as individual
-// kernels (the API path: vp_search / vp_backup, one launch per phase) or back
-// to back inside the persistent planning kernel (vp_plan), separated by grid
-// barriers.  Every phase is bound by HBM latency / bandwidth; nothing here is
-// a dense contraction.
+// vp_phases.cuh -- device code of one PORPP planning pass (sm_100a).
 //
-// Phase map (reference: /root/reference/pkg/src/vecpomdp):
-//   draw        belief.py:37-44        root states for the n rows
-//   sample      search.py:107-115      frontier -> softmax draw -> G(s,a) -> claim (b,a)
-//   assign<0>   tree.py:180-218        number new action rows in first-occurrence order
-//   accum       tree.py:216-217,236    reward/visit sums, claim (anode, obs)
-//   assign<1>   tree.py:220-256        number new belief rows in first-occurrence order
-//   leaf        search.py:119, backup.py:44-51
-//   backup_*    backup.py:75-114       leaf means, Q + PSI scatter, LSE per level
+// A pass is TWO kernels and no grid barrier:
+//
+//   search  (search.py:86-119)  each warp carries its 32 rows through every
+//           level: softmax draw from the belief's PSI row (TMA-staged into
+//           shared memory), G(s,a) in registers, the (b,a) and (a,o) hash
+//           claims (one 128-bit CAS each), reward / visit / row-count
+//           reductions -- then the leaf heuristic.  Ids come from one atomic
+//           per warp, so a row never waits for rows of other warps except for
+//           the few cycles between a creator's CAS and its publish.
+//   backup  (backup.py:75-114)  a bottom-up completion wave: every distinct
+//           leaf delivers (V, N) to its parent action; the delivery that
+//           brings an action's delivered-row count to its row count completes
+//           the action (Q, PSI scatter), and the action completion that does
+//           the same for its belief completes the belief (LSE over the row,
+//           computed by the warp) and delivers it upward.
+//
+// Node ids are therefore assigned in completion order.  Each node stores the
+// key (pass, level, first row) under which the reference would have created
+// it; the host sorts by it when exporting, which reproduces the reference's
+// first-occurrence numbering (tree.py:10-12) exactly.
 #pragma once
 
 #include <type_traits>
@@ -22,51 +29,52 @@
 
 namespace vp {
 
-constexpr int kStageWarps = 8;  // warps per block of the persistent kernel
+constexpr int kSearchWarps = 2;   // warps per search block
+constexpr int kBackupWarps = 8;   // warps per backup block
 
 __device__ __forceinline__ Slot* slots(void* p) { return reinterpret_cast<Slot*>(p); }
 
-// Grid-stride execution context.
-struct Span {
-  int gtid, gthreads;  // thread index / count
-  int gwarp, gwarps;   // warp index / count
-};
-// Warps are numbered block-fastest (warp w of block b is global warp
-// w * gridDim + b) so that consecutive 32-row chunks land on different SMs
-// even when a phase has far fewer chunks than the grid has warps; lanes stay
-// contiguous, so thread-granular loops remain coalesced.
-__device__ __forceinline__ Span this_span() {
-  Span s;
-  s.gwarp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  s.gwarps = (blockDim.x >> 5) * gridDim.x;
-  s.gtid = s.gwarp * 32 + (threadIdx.x & 31);
-  s.gthreads = s.gwarps * 32;
-  return s;
+// Canonical creation key: the reference creates node ids pass by pass, level
+// by level, in first-occurrence row order (tree.py:180-256).
+__device__ __forceinline__ u64 creation_key(u32 pass, int level, int row) {
+  return ((u64)pass << 32) | ((u64)(u32)level << 24) | (u64)(u32)row;
 }
 
 // ------------------------------------------------------------------ exp helpers (fast mode)
 // exp(eta * psi - shift) is evaluated as exp2(fma(eta*log2e, psi, -shift*log2e)).
-__device__ __forceinline__ float fexp2(float x) { return exp2f(x); }
+// fp32: one MUFU.EX2 (flush-to-zero: probabilities below 2^-126 are zero mass)
+__device__ __forceinline__ float fexp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ double fexp2(double x) { return exp2(x); }
 __device__ __forceinline__ float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double ffma(double a, double b, double c) { return __fma_rn(a, b, c); }
 constexpr double kLog2eD = 1.4426950408889634;
 
+// Loads of PSI: plain (search: rows are stable for the whole kernel) or L2
+// (backup: rows are rewritten by other SMs inside the kernel).
+template <bool L2, class T>
+__device__ __forceinline__ T ldp(const T* p) {
+  if constexpr (L2) return __ldcg(p);
+  else return *p;
+}
+
 // ------------------------------------------------------------------ LSE
 
-// Fast LSE (backup.py:34-41 formula: max, then sum of exp), evaluated by a
-// group of lanes per row with the row held in registers.
 __device__ __forceinline__ double lse_log(float s) { return (double)logf(s); }
 __device__ __forceinline__ double lse_log(double s) { return log(s); }
 
-// Sub-warp LSE: a group of G lanes (G a power of two) per row, so short rows
-// (|A| <= 16 G) keep every lane busy and take one memory round trip.  All
-// 32 lanes must call it (rows may be null for idle groups).
+// Fast LSE (backup.py:34-41 formula: max, then sum of exp) by a group of G
+// lanes per row with the row held in registers, so short rows (|A| <= 16 G)
+// keep every lane busy and take one memory round trip.  All 32 lanes must
+// call it (rows may be null for idle groups).
 __host__ __device__ constexpr int lse_group_size(int A) {
   return A <= 16 ? 1 : A <= 32 ? 2 : A <= 64 ? 4 : A <= 128 ? 8 : A <= 256 ? 16 : 32;
 }
 
-template <class PsiT, int G>
+template <class PsiT, int G, bool L2 = false>
 __device__ __forceinline__ double lse_group(const PsiT* row, int A, double eta) {
   const int gl = lane_id() & (G - 1);
   constexpr int R = 16;
@@ -78,7 +86,7 @@ __device__ __forceinline__ double lse_group(const PsiT* row, int A, double eta) 
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int a = gl + G * k;
-      v[k] = (row && a < A) ? row[a] : -(PsiT)INFINITY;
+      v[k] = (row && a < A) ? ldp<L2>(row + a) : -(PsiT)INFINITY;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -97,7 +105,7 @@ __device__ __forceinline__ double lse_group(const PsiT* row, int A, double eta) 
   } else {
     if (row)
       for (int a = gl; a < A; a += G) {
-        const PsiT z = e * row[a];
+        const PsiT z = e * ldp<L2>(row + a);
         m = z > m ? z : m;
       }
 #pragma unroll
@@ -107,7 +115,7 @@ __device__ __forceinline__ double lse_group(const PsiT* row, int A, double eta) 
     }
     const PsiT m2 = m * (PsiT)kLog2eD;
     if (row)
-      for (int a = gl; a < A; a += G) s += fexp2(ffma(e2, row[a], -m2));
+      for (int a = gl; a < A; a += G) s += fexp2(ffma(e2, ldp<L2>(row + a), -m2));
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
@@ -140,10 +148,11 @@ __device__ double row_lse_fast(const PsiT* row, int A, double eta) {
 }
 
 // numpy-order LSE for the fp64 parity mode: m/eta + log(pairwise sum)/eta.
+template <bool L2 = false>
 __device__ double lse_exact(const double* row, int A, double eta) {
   double m = -INFINITY;
-  for (int a = 0; a < A; ++a) m = fmax(m, eta * row[a]);
-  auto ex = [&](int a) -> double { return exp(eta * row[a] - m); };
+  for (int a = 0; a < A; ++a) m = fmax(m, eta * ldp<L2>(row + a));
+  auto ex = [&](int a) -> double { return exp(eta * ldp<L2>(row + a) - m); };
   const double s = pairwise_sum(ex, 0, A);
   return m / eta + log(s) / eta;
 }
@@ -174,38 +183,6 @@ __device__ __forceinline__ int scan_cdf_scalar(const CT* row, int A, CT e2, CT s
   for (int a = 0; a < A; ++a) {
     cum += fexp2(ffma(e2, row[a], -sh2));
     if (cum > u) return a;
-  }
-  return A - 1;
-}
-template <class CT>
-struct Vec16;
-template <>
-struct Vec16<float> {
-  typedef float4 T;
-  static constexpr int N = 4;
-  static __device__ __forceinline__ void get(const T& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-};
-template <>
-struct Vec16<double> {
-  typedef double2 T;
-  static constexpr int N = 2;
-  static __device__ __forceinline__ void get(const T& v, double* o) { o[0] = v.x; o[1] = v.y; }
-};
-template <class CT>
-__device__ __forceinline__ int scan_cdf_vec(const CT* row, int A, CT e2, CT sh2, CT u) {
-  typedef Vec16<CT> V;
-  CT cum = 0;
-  const typename V::T* rv = reinterpret_cast<const typename V::T*>(row);
-  for (int a0 = 0; a0 < A; a0 += V::N) {
-    CT x[V::N];
-    V::get(rv[a0 / V::N], x);
-#pragma unroll
-    for (int j = 0; j < V::N; ++j) {
-      if (a0 + j < A) {
-        cum += fexp2(ffma(e2, x[j], -sh2));
-        if (cum > u) return a0 + j;
-      }
-    }
   }
   return A - 1;
 }
@@ -248,11 +225,11 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 struct StageCfg {
-  int rows;    // G: PSI rows staged per warp per batch
+  int rows;    // PSI rows staged per warp per batch
   int stride;  // staged row stride in PsiT elements (odd multiple of 16 bytes)
 };
 
-// Per-warp staging state carried across phases of the persistent kernel.
+// Per-warp staging state (buffer, mbarrier, phase parity).
 template <class PsiT>
 struct Stage {
   PsiT* buf;
@@ -262,48 +239,6 @@ struct Stage {
 };
 
 // ------------------------------------------------------------------ warp helpers
-
-// Lanes with equal keys elect their lowest lane (= smallest row) to probe or
-// claim the slot once; the slot word is broadcast back.
-__device__ __forceinline__ u32 warp_claim(Slot* tab, u64 mask, u64 key, u32 row, bool active) {
-  const u32 grp = __match_any_sync(FULL, active ? key : kEmptyKey);
-  const int leader = __ffs(grp) - 1;
-  u32 word = 0;
-  if (active && lane_id() == leader) {
-    bool existing;
-    u32 id;
-    const u32 s = probe_claim(tab, mask, key, row, existing, id);
-    word = s | (existing ? kExistBit : 0u);
-  }
-  return __shfl_sync(FULL, word, leader);
-}
-
-// Append `node` to a per-level list once per level (stamp dedup).  Returns
-// true on the lane that appended it.
-__device__ __forceinline__ bool warp_list_once(u32* stamp, int node, u32 value, bool active, int* count, int* list) {
-  const u32 grp = __match_any_sync(FULL, active ? (u32)node : 0xffffffffu);
-  const int leader = __ffs(grp) - 1;
-  bool added = false;
-  if (active && lane_id() == leader) {
-    if (atomicExch(&stamp[node], value) != value) {
-      const int pos = atomicAdd(count, 1);
-      list[pos] = node;
-      added = true;
-    }
-  }
-  return added;
-}
-
-// Id of a slot once its first-occurrence row has numbered it (spin while pending).
-// Relaxed spin: the id's publisher stores it with st.release after the node's
-// columns, and readers only touch those columns through addresses that
-// depend on the id (or with relaxed gpu-scope loads).
-__device__ __forceinline__ int wait_final(const Slot* tab, u32 slot_word) {
-  const u32* p = &tab[slot_word & ~kExistBit].id;
-  u32 v = ld_relaxed_u32(p);
-  while (v >= kPending) v = ld_relaxed_u32(p);
-  return (int)v;
-}
 
 // Sum of v over the lanes in `grp`, in lane (= row) order, delivered to all lanes.
 __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
@@ -315,26 +250,36 @@ __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
   }
   return s;
 }
+// Same, short-circuited when every active key of the warp is distinct.
+__device__ __forceinline__ double group_sum(double v, u32 grp, bool active) {
+  if (__all_sync(FULL, !active || __popc(grp) == 1)) return v;
+  return group_sum_ordered(v, grp);
+}
 
-// Write the initial PSI row into every still-fresh belief of list[0..cnt)
-// (lazy rows, tree.py:253); a group of G lanes per belief.
+// Write the initial PSI row (tree.py:253) into the rows named by the lanes
+// set in `mask` (lazy rows become real the first time they are interior).
 template <class PsiT>
-__device__ void materialise_list(const vp_tree& T, const int* list, int cnt, const Span& sp) {
+__device__ __forceinline__ void materialise_rows(const vp_tree& T, const PsiT* init_row, u32 mask, int b) {
   const int A = T.action_count;
-  with_group(A, [&](auto g) {
-    constexpr int G = decltype(g)::value;
-    constexpr int RPW = 32 / G;
-    const int gl = lane_id() & (G - 1), grp = lane_id() / G;
-    for (int i0 = sp.gwarp * RPW; i0 < cnt; i0 += sp.gwarps * RPW) {
-      const int i = i0 + grp;
-      if (i >= cnt) continue;
-      const int b = list[i];
-      if (!(T.b_flags[b] & 1)) continue;
-      PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)b * T.psi_stride;
-      for (int a = gl; a < A; a += G) row[a] = (PsiT)T.init_prefs[a];
-      if (gl == 0) T.b_flags[b] = 0;
-    }
-  });
+  PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
+  while (mask) {
+    const int j = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int bj = __shfl_sync(FULL, b, j);
+    PsiT* row = psi + (size_t)bj * T.psi_stride;
+    for (int a = lane_id(); a < A; a += 32) row[a] = init_row[a];
+  }
+}
+
+// Numbered-node allocation for the winners of a warp: one atomic per warp.
+__device__ __forceinline__ int warp_alloc(int* counter, bool won) {
+  const u32 winners = __ballot_sync(FULL, won);
+  if (!winners) return 0;
+  const int first = __ffs(winners) - 1;
+  int base = 0;
+  if (lane_id() == first) base = atomicAdd(counter, __popc(winners));
+  base = __shfl_sync(FULL, base, first);
+  return base + __popc(winners & ((1u << lane_id()) - 1u));
 }
 
 // ------------------------------------------------------------------ tree init (one block)
@@ -369,115 +314,139 @@ __device__ void block_tree_init(const vp_tree& T) {
       T.b_depth[0] = 0;
       T.b_value[0] = 0.0;
       T.b_weight[0] = 0.0;
-      T.b_stamp[0] = 0;
-      T.b_flags[0] = 0;
+      T.b_rows[0] = 0;
+      T.b_done[0] = 0;
+      T.b_flags[0] = 0;  // the root row is written (above), not lazy
+      T.b_ckey[0] = 0;
       T.counters[0] = 1;
       T.counters[1] = 0;
       T.counters[2] = 0;
+      T.counters[3] = 0;
     }
   }
   __syncthreads();
 }
 
-// ------------------------------------------------------------------ draw
+// ------------------------------------------------------------------ root-state draw
 
-template <class Model>
-__device__ void phase_draw(const vp_work& W, const typename Model::State* particles, const double* cumw, int m,
-                           u64 key, const Span& sp) {
-  for (int r = sp.gtid; r < W.n; r += sp.gthreads) {
-    const double u = uniform1(key, (u64)r);
-    int lo = 0, hi = m;  // first index with cum > u  (searchsorted side=right)
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (cumw[mid] > u) hi = mid;
-      else lo = mid + 1;
-    }
-    const int idx = lo < m - 1 ? lo : m - 1;
-    reinterpret_cast<typename Model::State*>(W.states)[r] = particles[idx];
+// belief.py:37-44: u = uniform(draw_key, row); first index with cum > u
+// (searchsorted side=right), clamped to m - 1.
+template <class State>
+__device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r) {
+  const double u = uniform1(key, (u64)r);
+  int lo = 0, hi = m;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cumw[mid] > u) hi = mid;
+    else lo = mid + 1;
+  }
+  return particles[lo < m - 1 ? lo : m - 1];
+}
+
+// ------------------------------------------------------------------ search
+
+// Rows arriving at belief c (one reduction per distinct belief of the warp).
+// At the leaf level the first arrival also appends c to the leaf list.
+__device__ __forceinline__ void arrive(const vp_tree& T, const vp_work& W, int* leaf_count, int c, u32 grp,
+                                       bool lead, bool leaf_level) {
+  if (!lead) return;
+  const int cnt = __popc(grp);
+  if (leaf_level) {
+    if (atomicAdd(&T.b_rows[c], cnt) == 0) W.leaves[atomicAdd(leaf_count, 1)] = c;
+  } else {
+    red_add(&T.b_rows[c], cnt);
   }
 }
 
-// ------------------------------------------------------------------ sample (K1)
-
-struct LevelArgs {
-  int level;
-  int depth0;
-  u64 lkey;       // search_rng.derive(level).key (search.py:107)
-  u32 stamp;
-  const int32_t* inject;  // [*, n] level-major, or null
-  const int32_t* start;   // [n] frontier at depth0, or null (root)
-};
-
-__device__ __forceinline__ int frontier_of(const vp_tree& T, const vp_work& W, const LevelArgs& L, int r) {
-  if (L.level == L.depth0) return L.start ? L.start[r] : 0;
-  const int b = wait_final(slots(T.hash_b), (u32)W.slot_b[r]);
-  if (W.trace_belief) W.trace_belief[(size_t)(L.level - 1) * W.n + r] = b;
-  return b;
-}
-
-template <class Model>
-__device__ __forceinline__ void step_and_claim(const vp_tree& T, const vp_model& M, const vp_work& W,
-                                               const LevelArgs& L, int r, bool active, int b, int a) {
-  u64 key = 0;
-  if (active) {
-    typename Model::State st = reinterpret_cast<typename Model::State*>(W.states)[r];
-    u32 o;
-    double rw;
-    Model::step(M, st, a, fold(L.lkey, 1), (u64)r, o, rw);  // level_rng.derive(1) (search.py:113-115)
-    reinterpret_cast<typename Model::State*>(W.states)[r] = st;
-    W.obs[r] = o;
-    W.reward[r] = rw;
-    W.action[r] = a;
-    if (W.trace_action) {
-      W.trace_action[(size_t)L.level * W.n + r] = a;
-      W.trace_obs[(size_t)L.level * W.n + r] = o;
-    }
-    key = ((u64)(u32)b << 32) | (u32)a;
-  }
-  const u32 word = warp_claim(slots(T.hash_a), T.hmask_a, key, (u32)r, active);
-  if (active) W.slot_a[r] = (int)word;
-}
-
-// Fast mode: warps take 32-row chunks.  Rows whose belief is fresh draw from
-// the shared initial CDF; the chunk's distinct non-fresh beliefs have their
-// PSI rows TMA bulk-copied into the warp's shared-memory stage (one
-// cp.async.bulk per row, completion on the warp's mbarrier) and every lane
-// scans its own row.
-template <class Model, class PsiT>
-__device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_work& W, const LevelArgs& L,
-                                  Stage<PsiT>& sg, PsiT* init_cdf, const Span& sp) {
+// The search kernel body for one warp = 32 consecutive rows.
+template <class Model, class PsiT, bool Exact>
+__device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
+                            Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index) {
+  typedef typename Model::State State;
   const int n = W.n, A = T.action_count, lane = lane_id();
-  if (W.stats && sp.gtid == 0) {
-    atomicAdd(&W.stats[3], 1ull);
-    atomicAdd(&W.stats[4], (unsigned long long)n);
-  }
-  // the shared initial-row CDF (fresh beliefs) lives in shared memory
-  for (int a = threadIdx.x; a < A; a += blockDim.x) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
-  __syncthreads();
-  if (sp.gtid == 0) W.level_base[2 * L.level] = T.counters[1];
+  const int r = warp_index * 32 + lane;
+  const bool active = r < n;
+  const int d = S.d_max, depth0 = S.depth0;
+  const u32 pass = S.pass;
+  const u64 skey = S.search_key_dev ? *S.search_key_dev : S.search_key;
+  Slot* ha = slots(T.hash_a);
+  Slot* hb = slots(T.hash_b);
+  int* leaf_count = W.leaf_count + (pass & 1u);
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
   const PsiT e2 = (PsiT)(T.eta * kLog2eD);
-  for (int c = sp.gwarp; c * 32 < n; c += sp.gwarps) {
-    const int r = c * 32 + lane;
-    const bool active = r < n;
-    const int b = active ? frontier_of(T, W, L, r) : 0;
-    warp_list_once(T.b_stamp, b, L.stamp, active, &W.fcount[L.level], W.flist + (size_t)L.level * n);
-    const double u = active ? uniform1(fold(L.lkey, 0), (u64)r) : 0.0;  // level_rng.derive(0) (search.py:110)
-    int a = 0;
-    if (L.inject) {
-      a = active ? L.inject[(size_t)L.level * n + r] : 0;
+
+  State st{};
+  if (active) {
+    if (S.particles) {
+      const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
+      st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, r);
     } else {
-      const bool fresh = active && (ld_relaxed_u8(&T.b_flags[b]) & 1);
-      const bool need = active && !fresh;
+      st = reinterpret_cast<const State*>(W.states)[r];
+    }
+  }
+  int b = active ? (S.start_beliefs ? S.start_beliefs[r] : 0) : 0;
+  bool ok = active;
+  u32 fl = ok ? T.b_flags[b] : 0u;  // flags of nodes older than this pass are stable here
+  u32 grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
+  bool lead = ok && lane == __ffs(grp) - 1;
+  arrive(T, W, leaf_count, b, grp, lead, depth0 == d);
+
+  // An interior frontier (depth0 > 0): the rows also count toward every
+  // ancestor, so the completion wave of the backup reaches the root
+  // (backup.py:90-95 derives those levels from the valued children).
+  if (depth0 > 0 && S.start_beliefs) {
+    int cur = b;
+    for (int k = depth0; k > 0; --k) {
+      const int x = ok ? T.b_parent_action[cur] : -1;
+      const u32 g = __match_any_sync(FULL, (u32)x);
+      const bool ld = ok && lane == __ffs(g) - 1;
+      const int p = ok ? T.a_parent_belief[x] : 0;
+      bool mat = false;
+      if (ld) {
+        red_add(&T.a_rows[x], __popc(g));
+        red_add(&T.b_rows[p], __popc(g));
+        if (T.b_flags[p] & 2u) mat = atomicAnd(&T.b_flags[p], ~2u) & 2u;
+      }
+      materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), p);
+      cur = p;
+    }
+  }
+
+  bool made_interior = false;  // this lane created b at the previous level and it is interior now
+  for (int l = depth0; l < d; ++l) {
+    const u64 lkey = fold(skey, (u64)l);  // search.py:107
+    // ---- lazy rows: b is interior at this level; write its PSI row once
+    {
+      bool mat = made_interior;
+      if (lead && !made_interior && (fl & 2u)) mat = atomicAnd(&T.b_flags[b], ~2u) & 2u;
+      materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), b);
+    }
+    // ---- softmax draw (search.py:108-112)
+    const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;  // level_rng.derive(0)
+    int a = 0;
+    if (S.inject_actions) {
+      a = active ? S.inject_actions[(size_t)l * n + r] : 0;
+    } else if constexpr (Exact) {
+      if (ok) {
+        const double* row = (fl & 1u) ? T.init_prefs : reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride;
+        a = sample_exact(row, A, T.eta, u);
+      }
+    } else {
+      const bool fresh = ok && (fl & 1u);
+      const bool need = ok && !fresh;
       if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
-      const u32 grp = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
-      const int my_leader = __ffs(grp) - 1;
+      // distinct non-fresh beliefs of the warp: one TMA bulk copy of each PSI
+      // row into the warp's stage; the warp turns every staged row into its
+      // CDF (32 columns per step, shuffle scan) and each lane binary-searches
+      // its row with u scaled by the row total (p = e / sum e, search.py:51-54)
+      const u32 g = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
+      const int my_leader = __ffs(g) - 1;
       const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
       const int K = __popc(leaders);
       if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
       const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-      const PsiT sh2 = need ? (PsiT)(T.eta * ld_relaxed_f64(&T.b_lse[b]) * kLog2eD) : (PsiT)0;
+      const PsiT sh2 = need ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
       for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
         const int cnt = min(sg.cfg.rows, K - s0);
         fence_async_smem();
@@ -489,305 +458,289 @@ __device__ void phase_sample_fast(const vp_tree& T, const vp_model& M, const vp_
                    sg.bar);
         mbar_wait(sg.bar, sg.phase);
         sg.phase ^= 1u;
-        if (mine) a = scan_cdf_vec<PsiT>(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, A, e2, sh2, (PsiT)u);
+        PsiT my_total = 0;
+        for (int k = 0; k < cnt; ++k) {
+          const int src = (int)__fns(leaders, 0, s0 + k + 1);
+          const PsiT shk = __shfl_sync(FULL, sh2, src);
+          PsiT* row = sg.buf + (size_t)k * sg.cfg.stride;
+          PsiT carry = 0;
+          for (int a0 = 0; a0 < A; a0 += 32) {
+            const int c = a0 + lane;
+            PsiT v = c < A ? fexp2(ffma(e2, row[c], -shk)) : (PsiT)0;
+            v = warp_inclusive_scan(v) + carry;
+            if (c < A) row[c] = v;
+            carry = __shfl_sync(FULL, v, 31);
+          }
+          if (lane == k) my_total = carry;
+        }
+        __syncwarp();
+        const PsiT total = __shfl_sync(FULL, my_total, mine ? my_slot - s0 : 0);
+        if (mine) a = search_cdf(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, A, (PsiT)(u * (double)total));
         __syncwarp();
       }
     }
-    step_and_claim<Model>(T, M, W, L, r, active, b, a);
-  }
-}
-
-// fp64 parity mode: numpy operation order, no staging.
-template <class Model>
-__device__ void phase_sample_exact(const vp_tree& T, const vp_model& M, const vp_work& W, const LevelArgs& L,
-                                   const Span& sp) {
-  const int n = W.n, A = T.action_count, lane = lane_id();
-  if (sp.gtid == 0) W.level_base[2 * L.level] = T.counters[1];
-  for (int c = sp.gwarp; c * 32 < n; c += sp.gwarps) {
-    const int r = c * 32 + lane;
-    const bool active = r < n;
-    const int b = active ? frontier_of(T, W, L, r) : 0;
-    warp_list_once(T.b_stamp, b, L.stamp, active, &W.fcount[L.level], W.flist + (size_t)L.level * n);
-    int a = 0;
-    if (active) {
-      const double u = uniform1(fold(L.lkey, 0), (u64)r);
-      if (L.inject) {
-        a = L.inject[(size_t)L.level * n + r];
-      } else {
-        const double* row = (ld_relaxed_u8(&T.b_flags[b]) & 1)
-                                ? T.init_prefs
-                                : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
-        a = sample_exact(row, A, T.eta, u);
-      }
-    }
-    step_and_claim<Model>(T, M, W, L, r, active, b, a);
-  }
-}
-
-// ------------------------------------------------------------------ assign (K2 / K4)
-
-// Number the rows that won their key this level in row order: tiles of
-// blockDim.x rows (one per thread), chained by a warp-parallel decoupled
-// look-back; write the new nodes' columns and publish the id (release) so
-// rows spinning in the next phase can proceed.  Block-collective.
-// WhichTable: 0 = actions, 1 = beliefs.
-// `ticket` != null (one tile per block, standalone launch): tiles are taken in
-// block start order from an atomic ticket, which makes the look-back
-// deadlock-free for any grid size; null (persistent kernel, all blocks
-// resident): block b owns tiles b, b + grid, ...
-template <int WhichTable>
-__device__ void phase_assign(const vp_tree& T, const vp_work& W, int level, u32 epoch, u32* ticket) {
-  __shared__ u32 s_warp[32];
-  __shared__ u32 s_excl;
-  __shared__ int s_tile;
-  const int n = W.n;
-  const int NW = blockDim.x >> 5;
-  const int tile_rows = blockDim.x;
-  const int ntiles = (n + tile_rows - 1) / tile_rows;
-  Slot* tab = slots(WhichTable ? T.hash_b : T.hash_a);
-  const int* slot_of = WhichTable ? W.slot_b : W.slot_a;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const int base = W.level_base[2 * level + WhichTable];
-  const int cap = WhichTable ? T.cap_beliefs : T.cap_actions;
-  int first = blockIdx.x;
-  if (ticket) {
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    first = s_tile;
-  }
-  const int step = ticket ? ntiles : gridDim.x;
-  for (int tile = first; tile < ntiles; tile += step) {
-    const int r = tile * tile_rows + threadIdx.x;
-    u32 sl = 0;
-    bool win = false;
-    if (r < n) {
-      const u32 w = (u32)slot_of[r];
-      sl = w & ~kExistBit;
-      if (!(w & kExistBit)) win = ld_volatile_u32(&tab[sl].id) == (kPending | (u32)r);
-    }
-    const u32 ballot = __ballot_sync(FULL, win);
-    const u32 below = __popc(ballot & ((1u << lane) - 1u));
-    if (lane == 0) s_warp[warp] = __popc(ballot);
-    __syncthreads();
-    if (warp == 0) {
-      const u32 v = lane < NW ? s_warp[lane] : 0;
-      const u32 vi = warp_inclusive_scan(v);
-      if (lane < NW) s_warp[lane] = vi - v;
-      const u32 agg = __shfl_sync(FULL, vi, NW - 1);
-      const u32 excl = tile_lookback_warp(reinterpret_cast<u64*>(W.scan_status), tile, agg, epoch);
-      if (lane == 0) {
-        s_excl = excl;
-        if (tile == ntiles - 1) {
-          if (W.stats) {
-            // lists of this level are complete by now: F_l after sample, P_l after accum
-            atomicAdd(&W.stats[WhichTable ? 1 : 0],
-                      (unsigned long long)(WhichTable ? W.pcount[level] : W.fcount[level]));
-            atomicAdd(&W.stats[WhichTable ? 6 : 5], (unsigned long long)(excl + agg));
-          }
-          T.counters[WhichTable ? 0 : 1] = base + (int)(excl + agg);
-          if (ticket) *ticket = 0;  // every block has taken its ticket by now
-        }
-      }
-    }
-    __syncthreads();
-    if (win) {
-      const int id = base + (int)(s_excl + s_warp[warp] + below);
-      Slot& s = tab[sl];
-      if (id < cap) {
-        const u64 key = s.key;
-        if (WhichTable == 0) {
-          T.a_parent_belief[id] = (int)(key >> 32);
-          T.a_action[id] = (int)(u32)key;
-          T.a_reward[id] = 0.0;
-          T.a_visits[id] = 0;
-          T.a_num[id] = 0.0;
-          T.a_den[id] = 0.0;
-          T.a_stamp[id] = 0;
-        } else {
-          const int pa = (int)(key >> 32);
-          T.b_parent_action[id] = pa;
-          T.b_parent_obs[id] = (u32)key;
-          T.b_depth[id] = T.b_depth[T.a_parent_belief[pa]] + 1;
-          T.b_lse[id] = T.init_lse[0];
-          T.b_value[id] = 0.0;
-          T.b_weight[id] = 0.0;
-          T.b_stamp[id] = 0;
-          T.b_flags[id] = 1;  // PSI row lazily equal to the initial row (tree.py:253)
-        }
-      } else {
-        T.counters[2] = 1;  // overflow: the host fails the plan loudly
-      }
-      st_release_u32(&s.id, (u32)id);
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------ accum (K3)
-
-__device__ void phase_accum(const vp_tree& T, const vp_work& W, int level, u32 stamp, const Span& sp) {
-  const int n = W.n, lane = lane_id();
-  if (sp.gtid == 0) W.level_base[2 * level + 1] = T.counters[0];
-  for (int c = sp.gwarp; c * 32 < n; c += sp.gwarps) {
-    const int r = c * 32 + lane;
-    const bool active = r < n;
-    int id = 0;
-    double rw = 0.0;
+    // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
-    if (active) {
-      id = wait_final(slots(T.hash_a), (u32)W.slot_a[r]);
-      rw = W.reward[r];
-      o = W.obs[r];
-      if (W.trace_anode) W.trace_anode[(size_t)level * n + r] = id;
-    }
-    const bool ok = active && id < T.cap_actions;
-    // claim (anode, obs) in hash_b first: it is the longest dependent chain
-    const u32 word = warp_claim(slots(T.hash_b), T.hmask_b, ((u64)(u32)id << 32) | o, (u32)r, ok);
-    if (active) W.slot_b[r] = (int)word;
-    // warp-aggregated reward / visit accumulation (lane = row order inside a group)
-    const u32 grp = __match_any_sync(FULL, ok ? (u32)id : 0xffffffffu);
-    const double sum = group_sum_ordered(rw, grp);
-    if (ok && lane == __ffs(grp) - 1) {
-      atomicAdd(&T.a_reward[id], sum);
-      atomicAdd(&T.a_visits[id], __popc(grp));
-      if (atomicExch(&T.a_stamp[id], stamp) != stamp) {
-        const int pos = atomicAdd(&W.pcount[level], 1);
-        W.plist[(size_t)level * n + pos] = id;
+    double rw = 0.0;
+    if (ok) Model::step(M, st, a, fold(lkey, 1), (u64)r, o, rw);  // level_rng.derive(1)
+
+    // ---- action node (b, a): append_actions (tree.py:180-218)
+    int x = 0;
+    {
+      const u64 key = ((u64)(u32)b << 32) | (u32)a;
+      grp = __match_any_sync(FULL, ok ? key : kEmptyKey);
+      const int leader = __ffs(grp) - 1;
+      lead = ok && lane == leader;
+      Claim cl{0, false, 0};
+      if (lead) cl = claim_key(ha, T.hmask_a, key);
+      const int id = warp_alloc(&T.counters[1], cl.won);
+      if (cl.won) {
+        x = id;
+        if (x < T.cap_actions) {
+          // accumulators are zero (cleared at tree reset); the key is a min-reduction
+          T.a_parent_belief[x] = b;
+          T.a_action[x] = a;
+          red_min(&T.a_ckey[x], creation_key(pass, l, r));
+        } else {
+          T.counters[2] = 1;  // overflow: the host fails the plan loudly
+        }
+        publish(ha, cl.slot, (u32)x, pass);
+      }
+      __syncwarp();  // every creator of the warp has published before any lane spins
+      if (lead && !cl.won) {
+        const u64 w = wait_published(ha, cl.slot, cl.word);
+        x = (int)(u32)w;
+        if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, r));
+      }
+      x = __shfl_sync(FULL, x, leader);
+      if (W.stats) {
+        const u32 wn = __ballot_sync(FULL, cl.won);
+        if (lane == 0 && wn) atomicAdd(&W.stats[5], (unsigned long long)__popc(wn));
       }
     }
+    ok = ok && x < T.cap_actions;
+    // rewards and visits (tree.py:216-217); rows through x for the backup
+    {
+      const double sum = group_sum(rw, grp, ok);
+      if (lead && ok) {
+        const int cnt = __popc(grp);
+        red_add(&T.a_reward[x], sum);
+        red_add(&T.a_visits[x], cnt);
+        red_add(&T.a_rows[x], cnt);
+      }
+    }
+
+    // ---- belief node (x, o): append_beliefs (tree.py:220-256)
+    int c = 0;
+    bool c_new = false;
+    const bool interior_next = l + 1 < d;
+    {
+      const u64 key = ((u64)(u32)x << 32) | o;
+      grp = __match_any_sync(FULL, ok ? key : kEmptyKey);
+      const int leader = __ffs(grp) - 1;
+      lead = ok && lane == leader;
+      Claim cl{0, false, 0};
+      if (lead) cl = claim_key(hb, T.hmask_b, key);
+      const int id = warp_alloc(&T.counters[0], cl.won);
+      u32 cpass = 0;
+      if (cl.won) {
+        c = id;
+        cpass = pass;
+        if (c < T.cap_beliefs) {
+          T.b_parent_action[c] = x;
+          T.b_parent_obs[c] = o;
+          T.b_depth[c] = l + 1;
+          T.b_lse[c] = T.init_lse[0];
+          // fresh (PSI == init); an interior node's row is written by its creator next level
+          T.b_flags[c] = interior_next ? 1u : 3u;
+          red_min(&T.b_ckey[c], creation_key(pass, l, r));
+        } else {
+          T.counters[2] = 1;
+        }
+        publish(hb, cl.slot, (u32)c, pass);
+      }
+      __syncwarp();
+      if (lead && !cl.won) {
+        const u64 w = wait_published(hb, cl.slot, cl.word);
+        c = (int)(u32)w;
+        cpass = (u32)(w >> 32);
+        if (cpass == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, l, r));
+      }
+      c = __shfl_sync(FULL, c, leader);
+      c_new = __shfl_sync(FULL, cpass, leader) == pass;
+      made_interior = cl.won && interior_next && c < T.cap_beliefs;
+      if (W.stats) {
+        const u32 wn = __ballot_sync(FULL, cl.won);
+        if (lane == 0 && wn) atomicAdd(&W.stats[6], (unsigned long long)__popc(wn));
+      }
+    }
+    ok = ok && c < T.cap_beliefs;
+    arrive(T, W, leaf_count, c, grp, lead && ok, !interior_next);
+    if (active && W.trace_action) {
+      const size_t t = (size_t)l * n + r;
+      W.trace_action[t] = a;
+      W.trace_obs[t] = o;
+      W.trace_anode[t] = x;
+      W.trace_belief[t] = c;
+    }
+    b = c;
+    fl = c_new ? (interior_next ? 1u : 3u) : (ok ? T.b_flags[c] : 0u);
   }
-}
 
-// ------------------------------------------------------------------ leaves
-
-template <class Model>
-__device__ void phase_leaf(const vp_tree& T, const vp_model& M, const vp_work& W, const LevelArgs& L,
-                           const Span& sp) {
-  const int n = W.n, lane = lane_id();
-  for (int c = sp.gwarp; c * 32 < n; c += sp.gwarps) {
-    const int r = c * 32 + lane;
-    const bool active = r < n;
-    int b = 0;
-    double h = 0.0;
-    if (active) {
-      b = frontier_of(T, W, L, r);
-      h = Model::heuristic(M, reinterpret_cast<const typename Model::State*>(W.states)[r]);
-      W.leaf_belief[r] = b;
-      W.leaf_value[r] = h;
-    }
-    const bool ok = active && b < T.cap_beliefs;
-    warp_list_once(T.b_stamp, b, L.stamp, ok, &W.fcount[L.level], W.flist + (size_t)L.level * n);
-    const u32 grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
-    const double sum = group_sum_ordered(h, grp);
-    if (ok && lane == __ffs(grp) - 1) {
-      atomicAdd(&T.b_weight[b], (double)__popc(grp));
-      atomicAdd(&T.b_value[b], sum);
-    }
+  // ---- leaves: heuristic value (search.py:119), summed per leaf (backup.py:44-51)
+  double h = 0.0;
+  if (active) {
+    h = ok ? Model::heuristic(M, st) : 0.0;
+    W.leaf_belief[r] = b;
+    W.leaf_value[r] = h;
+  }
+  grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
+  const double sum = group_sum(h, grp, ok);
+  if (ok && lane == __ffs(grp) - 1) red_add(&T.b_value[b], sum);
+  if (W.stats && threadIdx.x == 0 && blockIdx.x == 0) {
+    atomicAdd(&W.stats[3], 1ull);
+    atomicAdd(&W.stats[4], (unsigned long long)n * (unsigned long long)(d - depth0));
   }
 }
 
 // ------------------------------------------------------------------ backup
 
-// Leaves: V = mean heuristic, N = batch count (backup.py:44-51, 82-87), fed
-// to the parent action's child mean (backup.py:64-68); warps also
-// materialise the fresh PSI rows of level `mat` (the parents updated next).
-template <class PsiT>
-__device__ void phase_backup_leaves(const vp_tree& T, const vp_work& W, int dmax, int mat, const Span& sp) {
-  const int cnt = W.fcount[dmax];
-  for (int i = sp.gtid; i < cnt; i += sp.gthreads) {
-    const int b = W.flist[(size_t)dmax * W.n + i];
-    const double w = T.b_weight[b];
-    const double v = T.b_value[b] / w;
-    T.b_value[b] = 0.0;
-    T.b_weight[b] = 0.0;
-    const int pa = T.b_parent_action[b];
-    if (pa >= 0) {
-      atomicAdd(&T.a_num[pa], v * w);
-      atomicAdd(&T.a_den[pa], w);
-    }
-  }
-  if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);
-}
-
-template <class PsiT>
-__device__ void phase_materialise(const vp_tree& T, const vp_work& W, int lvl, const Span& sp) {
-  materialise_list<PsiT>(T, W.flist + (size_t)lvl * W.n, W.fcount[lvl], sp);
-}
-
-// Actions of level lvl: Q = R/visits + gamma num/den; PSI[b, a] += Q - LSE_pre(b)
-// (backup.py:96-108); N(b) += lifetime visits (backup.py:110-114).
-template <class PsiT>
-__device__ void phase_backup_q(const vp_tree& T, const vp_work& W, int lvl, double gamma, const Span& sp) {
-  const int cnt = W.pcount[lvl];
-  PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-  for (int i = sp.gtid; i < cnt; i += sp.gthreads) {
-    const int a = W.plist[(size_t)lvl * W.n + i];
-    const double vis = (double)T.a_visits[a];
-    const double q = T.a_reward[a] / vis + (gamma * T.a_num[a]) / T.a_den[a];
-    T.a_num[a] = 0.0;
-    T.a_den[a] = 0.0;
-    const int b = T.a_parent_belief[a];
-    PsiT* cell = psi + (size_t)b * T.psi_stride + T.a_action[a];
-    *cell = (PsiT)((double)*cell + (q - T.b_lse[b]));
-    atomicAdd(&T.b_weight[b], vis);
-  }
-}
-
-// Beliefs of level lvl: V = LSE_post (backup.py:109), cached as the next
-// LSE_pre, then their parent action's child mean; warps also materialise
-// the fresh rows of level `mat`.
+// LSE of the rows held by the lanes in `rmask` (lane j's row is ready[j]);
+// results land in out[j].  Rows are read from L2: their cells were written by
+// other SMs inside this kernel.
 template <class PsiT, bool Exact>
-__device__ void phase_backup_v(const vp_tree& T, const vp_work& W, int lvl, int mat, const Span& sp) {
-  const int cnt = W.fcount[lvl];
-  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+__device__ __forceinline__ void lse_ready(const vp_tree& T, int ready, u32 rmask, double* out) {
   const int A = T.action_count;
-  auto finish = [&](int b, double v) {
-    T.b_lse[b] = v;
-    const double w = T.b_weight[b];
-    T.b_weight[b] = 0.0;
-    const int pa = T.b_parent_action[b];
-    if (pa >= 0) {
-      atomicAdd(&T.a_num[pa], v * w);
-      atomicAdd(&T.a_den[pa], w);
-    }
-  };
+  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   if constexpr (Exact) {
-    for (int i = sp.gtid; i < cnt; i += sp.gthreads) {
-      const int b = W.flist[(size_t)lvl * W.n + i];
-      finish(b, lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride, A, T.eta));
-    }
+    if (ready >= 0) out[lane_id()] = lse_exact<true>(reinterpret_cast<const double*>(psi) + (size_t)ready * T.psi_stride,
+                                                      A, T.eta);
   } else {
     with_group(A, [&](auto g) {
       constexpr int G = decltype(g)::value;
-      constexpr int RPW = 32 / G;  // rows per warp
-      const int gl = lane_id() & (G - 1), grp = lane_id() / G;
-      for (int i0 = sp.gwarp * RPW; i0 < cnt; i0 += sp.gwarps * RPW) {
-        const int i = i0 + grp;
-        const int b = i < cnt ? W.flist[(size_t)lvl * W.n + i] : -1;
-        const double v = lse_group<PsiT, G>(b >= 0 ? psi + (size_t)b * T.psi_stride : nullptr, A, T.eta);
-        if (gl == 0 && b >= 0) finish(b, v);
+      constexpr int RPW = 32 / G;  // rows per warp per round
+      const int gl = lane_id() & (G - 1), gi = lane_id() / G;
+      const int k = __popc(rmask);
+      for (int p0 = 0; p0 < k; p0 += RPW) {
+        const int idx = p0 + gi;
+        const int owner = idx < k ? (int)__fns(rmask, 0, idx + 1) : -1;
+        const int bb = __shfl_sync(FULL, ready, owner < 0 ? 0 : owner);
+        const double v = lse_group<PsiT, G, true>(owner >= 0 ? psi + (size_t)bb * T.psi_stride : nullptr, A, T.eta);
+        if (owner >= 0 && gl == 0) out[owner] = v;
       }
     });
   }
-  if (mat >= 0) materialise_list<PsiT>(T, W.flist + (size_t)mat * W.n, W.fcount[mat], sp);
+  __syncwarp();
 }
 
-// Levels at or above the search start depth have no recorded lists: derive
-// them from the valued children (backup.py:90-95).
-__device__ void phase_parent_lists(const vp_tree& T, const vp_work& W, int d, u32 stamp, const Span& sp) {
-  const int cnt = W.fcount[d];
-  for (int i = sp.gtid; i < cnt; i += sp.gthreads) {
-    const int b = W.flist[(size_t)d * W.n + i];
-    const int pa = T.b_parent_action[b];
-    if (pa < 0) continue;
-    if (atomicExch(&T.a_stamp[pa], stamp) != stamp) {
-      const int pos = atomicAdd(&W.pcount[d - 1], 1);
-      W.plist[(size_t)(d - 1) * W.n + pos] = pa;
-      const int pb = T.a_parent_belief[pa];
-      if (atomicExch(&T.b_stamp[pb], stamp) != stamp) {
-        const int q = atomicAdd(&W.fcount[d - 1], 1);
-        W.flist[(size_t)(d - 1) * W.n + q] = pb;
+// One warp = up to 32 distinct leaves; each lane climbs while it is the last
+// arrival of the node above it.
+template <class PsiT, bool Exact>
+__device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double gamma, int warp_index,
+                            double* s_v) {
+  const int lane = lane_id();
+  const int cnt = W.leaf_count[pass & 1u];
+  const int i = warp_index * 32 + lane;
+  PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
+  int c = -1, rows = 0;
+  double V = 0.0, N = 0.0;
+  if (i < cnt) {
+    // leaf: V = mean heuristic, N = batch count (backup.py:44-51, 82-87)
+    c = W.leaves[i];
+    rows = T.b_rows[c];
+    N = (double)rows;
+    V = T.b_value[c] / N;
+    T.b_value[c] = 0.0;
+    T.b_rows[c] = 0;
+  }
+  bool live = c >= 0;
+  unsigned long long n_act = 0, n_bel = 0, n_psi = 0;
+  while (__any_sync(FULL, live)) {
+    int ready = -1;
+    if (live) {
+      live = false;
+      const int x = T.b_parent_action[c];
+      if (x >= 0) {
+        // child mean of the action (backup.py:64-68)
+        red_add(&T.a_num[x], V * N);
+        red_add(&T.a_den[x], N);
+        const int tot = T.a_rows[x];
+        if (atom_add_acq_rel(&T.a_done[x], rows) + rows == tot) {
+          // last child: Q (backup.py:96-104) and PSI[b, a] += Q - LSE_pre(b) (:106-108)
+          ++n_act;
+          const double num = ld_relaxed_f64(&T.a_num[x]), den = ld_relaxed_f64(&T.a_den[x]);
+          T.a_num[x] = 0.0;
+          T.a_den[x] = 0.0;
+          T.a_done[x] = 0;
+          T.a_rows[x] = 0;
+          const int vis = T.a_visits[x];
+          const double q = T.a_reward[x] / (double)vis + (gamma * num) / den;
+          const int pb = T.a_parent_belief[x];
+          const double lse_pre = T.b_lse[pb];
+          PsiT* cell = psi + (size_t)pb * T.psi_stride + T.a_action[x];
+          const double old_v = (double)__ldcg(cell);
+          const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
+          *cell = new_v;
+          if constexpr (!Exact) {
+            // a lazily-initial row (LSE_pre is its exact LSE): LSE_post follows from the
+            // changed cells, sum_a exp(eta (psi_a - LSE_pre)) = 1 + sum_changed (new - old)
+            if (T.b_flags[pb] & 1u)
+              red_add(&T.b_value[pb], exp(T.eta * ((double)new_v - lse_pre)) - exp(T.eta * (old_v - lse_pre)));
+          }
+          // N(b) = lifetime visits of the valued actions (backup.py:110-114)
+          red_add(&T.b_weight[pb], (double)vis);
+          const int btot = T.b_rows[pb];
+          if (atom_add_acq_rel(&T.b_done[pb], tot) + tot == btot) ready = pb;
+        }
       }
+    }
+    if (__any_sync(FULL, ready >= 0)) {
+      // last action of a belief: V = LSE_post (backup.py:109), cached as the next LSE_pre.
+      // Lazily-initial rows use the incremental sum; other rows (and tiny / overflowing
+      // incremental sums) are read in full by the warp.
+      bool full = Exact && ready >= 0;
+      if constexpr (!Exact) {
+        if (ready >= 0) {
+          full = true;
+          if (T.b_flags[ready] & 1u) {
+            const double sum = 1.0 + ld_relaxed_f64(&T.b_value[ready]);
+            if (sum > 1e-9 && sum < 1e300) {
+              V = T.b_lse[ready] + log(sum) / T.eta;
+              full = false;
+            }
+          }
+        }
+      }
+      const u32 fmask = __ballot_sync(FULL, full);
+      if (fmask) lse_ready<PsiT, Exact>(T, full ? ready : -1, fmask, s_v);
+      if (ready >= 0) {
+        ++n_bel;
+        if (full) {
+          V = s_v[lane];
+          ++n_psi;
+        }
+        T.b_lse[ready] = V;
+        T.b_flags[ready] = 0u;
+        N = ld_relaxed_f64(&T.b_weight[ready]);
+        rows = T.b_rows[ready];
+        T.b_weight[ready] = 0.0;
+        T.b_value[ready] = 0.0;
+        T.b_rows[ready] = 0;
+        T.b_done[ready] = 0;
+        c = ready;
+        live = true;
+      }
+    }
+  }
+  if (W.stats) {
+    n_act = warp_sum(n_act);
+    n_bel = warp_sum(n_bel);
+    n_psi = warp_sum(n_psi);
+    if (lane == 0) {
+      if (n_bel) atomicAdd(&W.stats[0], n_bel);
+      if (n_psi) atomicAdd(&W.stats[8], n_psi);
+      if (n_act) atomicAdd(&W.stats[1], n_act);
+      if (i < cnt) atomicAdd(&W.stats[7], (unsigned long long)min(32, cnt - warp_index * 32));
     }
   }
 }

@@ -1,10 +1,10 @@
 """Device forward search (API mirror of /root/reference/pkg/src/vecpomdp/search.py).
 
 ``search(tree, model, batch, d_max, eta, rng)`` descends every row of the
-batch ``d_max - batch.depth`` levels in one ``vp_search`` call: per level the
-rows draw actions from the softmax of their belief's PSI row, step the device
-generative model and extend the tree through the two hash indexes, all
-without a host round trip (csrc/vp_kernels.cu, K1..K4).
+batch ``d_max - batch.depth`` levels in ONE kernel launch (``vp_search``):
+per level the rows draw actions from the softmax of their belief's PSI row,
+step the device generative model and extend the tree through the two hash
+indexes, without a grid barrier or a host round trip (csrc/vp_phases.cuh).
 """
 
 from __future__ import annotations
@@ -31,37 +31,30 @@ def _torch():
 
 
 class Workspace:
-    """Per-row scratch and per-level distinct lists for n simulation rows."""
+    """Per-row scratch of n simulation rows: start states, leaf list and traces."""
 
-    def __init__(self, n: int, max_levels: int, state_bytes: int, trace: bool = False):
+    def __init__(self, n: int, max_levels: int, state_bytes: int, trace: bool = False, stats: bool = False):
         if n < 1:
             raise ValueError("n_parallel must be >= 1")
+        if n >= 1 << 24:
+            raise ValueError("n_parallel must be < 2**24")
         torch = _torch()
         dev = "cuda"
         L = max(1, int(max_levels))
+        if L > 255:
+            raise ValueError("d_max must be <= 255")
         self.n, self.max_levels, self.state_bytes, self.trace = n, L, state_bytes, trace
         i32 = dict(dtype=torch.int32, device=dev)
         self.states = torch.empty(n * state_bytes + 16, dtype=torch.uint8, device=dev)
-        self.slot_a = torch.empty(n, **i32)
-        self.slot_b = torch.empty(n, **i32)
-        self.obs = torch.empty(n, **i32)
-        self.reward = torch.empty(n, dtype=torch.float64, device=dev)
-        self.action = torch.empty(n, **i32)
-        self.flist = torch.empty((L + 1) * n, **i32)
-        self.fcount = torch.zeros(L + 1, **i32)
-        self.plist = torch.empty(L * n, **i32)
-        self.pcount = torch.zeros(L, **i32)
-        self.level_base = torch.zeros(2 * (L + 1), **i32)
-        tiles = (n + _lib.VP_SCAN_TILE - 1) // _lib.VP_SCAN_TILE
-        self.scan_status = torch.zeros(tiles, dtype=torch.int64, device=dev)
-        self.scan_ticket = torch.zeros(2, **i32)
+        self.leaves = torch.empty(n, **i32)
+        self.leaf_count = torch.zeros(2, **i32)
         self.leaf_belief = torch.empty(n, **i32)
         self.leaf_value = torch.empty(n, dtype=torch.float64, device=dev)
-        self.stats = torch.zeros(8, dtype=torch.int64, device=dev)
+        self.stats = torch.zeros(16, dtype=torch.int64, device=dev)
+        self.last_pass = 0
         s = _lib.VpWork()
         s.n, s.max_levels = n, L
-        for name in ("states", "slot_a", "slot_b", "obs", "reward", "action", "flist", "fcount", "plist",
-                     "pcount", "level_base", "scan_status", "scan_ticket", "leaf_belief", "leaf_value", "stats"):
+        for name in ("states", "leaves", "leaf_count", "leaf_belief", "leaf_value"):
             setattr(s, name, getattr(self, name).data_ptr())
         if trace:
             self.trace_action = torch.empty(L * n, **i32)
@@ -71,22 +64,27 @@ class Workspace:
             for name in ("trace_action", "trace_obs", "trace_anode", "trace_belief"):
                 setattr(s, name, getattr(self, name).data_ptr())
         self.struct = s
+        self.enable_stats(stats)
+
+    def enable_stats(self, on: bool):
+        """Traffic counters (vp_work.stats) -- off on the timed path."""
+        self.struct.stats = self.stats.data_ptr() if on else None
 
     def fits(self, n: int, levels: int, state_bytes: int, trace: bool) -> bool:
         return (self.n == n and self.max_levels >= levels and self.state_bytes == state_bytes
                 and (self.trace or not trace))
 
-    def traces(self, depth0: int, d_max: int) -> list:
-        """Per-level host copies of the traced columns (like oracle.search(trace=))."""
+    def traces(self, tree, depth0: int, d_max: int) -> list:
+        """Per-level host copies of the traced columns (like oracle.search(trace=)),
+        node ids in reference numbering."""
         n = self.n
         out = []
-        cols = {k: getattr(self, "trace_" + k).cpu().numpy() for k in ("action", "obs", "anode", "belief")}
         for lvl in range(depth0, d_max):
             sl = slice(lvl * n, (lvl + 1) * n)
-            out.append({"actions": cols["action"][sl].astype(np.int64),
-                        "observations": cols["obs"][sl].view(np.uint32).astype(np.int64),
-                        "action_nodes": cols["anode"][sl].astype(np.int64),
-                        "next_beliefs": cols["belief"][sl].astype(np.int64)})
+            out.append({"actions": self.trace_action[sl].cpu().numpy().astype(np.int64),
+                        "observations": self.trace_obs[sl].cpu().numpy().view(np.uint32).astype(np.int64),
+                        "action_nodes": tree.to_reference_actions(self.trace_anode[sl]).cpu().numpy(),
+                        "next_beliefs": tree.to_reference_beliefs(self.trace_belief[sl]).cpu().numpy()})
         return out
 
 
@@ -105,32 +103,39 @@ class SearchBatch:
 
 
 class LeafResult:
-    """Device frontier after a search (search.py:40-43); host arrays on demand."""
+    """Device frontier after a search (search.py:40-43); host arrays on demand
+    (belief ids in reference numbering)."""
 
-    def __init__(self, tree, work: Workspace, depth0: int, d_max: int, stamp_base: int, generation: int):
+    def __init__(self, tree, work: Workspace, depth0: int, d_max: int, pass_: int, generation: int):
         self.tree, self.work = tree, work
-        self.depth0, self.d_max, self.stamp_base, self.generation = depth0, d_max, stamp_base, generation
+        self.depth0, self.d_max, self.pass_, self.generation = depth0, d_max, pass_, generation
 
     @property
     def leaf_belief_indices(self) -> np.ndarray:
-        return self.work.leaf_belief.cpu().numpy().astype(np.int64)
+        return self.tree.to_reference_beliefs(self.work.leaf_belief.to(_torch().int64)).cpu().numpy()
 
     @property
     def heuristic_values(self) -> np.ndarray:
         return self.work.leaf_value.cpu().numpy().copy()
 
 
-def run_search(tree, dm, work: Workspace, search_key: int, depth0: int, d_max: int, stamp_base: int,
-               iteration: int = 0, inject=None, start=None):
-    """Launch one device search (no host synchronisation)."""
+def run_search(tree, dm, work: Workspace, search_key: int, depth0: int, d_max: int, pass_: int, inject=None,
+               start=None, particles=None, cumw=None, m: int = 0, draw_key: int = 0):
+    """Launch one device search (no host synchronisation).  With ``particles``
+    the rows draw their start states from the belief inside the kernel."""
     args = _lib.VpSearchArgs()
     args.search_key = search_key
-    args.depth0, args.d_max = depth0, d_max
-    args.stamp_base, args.iteration = stamp_base, iteration
+    args.depth0, args.d_max, args.pass_ = depth0, d_max, pass_
     args.inject_actions = inject.data_ptr() if inject is not None else None
     args.start_beliefs = start.data_ptr() if start is not None else None
+    if particles is not None:
+        args.particles, args.cum_weights, args.m, args.draw_key = particles.data_ptr(), cumw.data_ptr(), m, draw_key
+    if pass_ != work.last_pass + 1:
+        work.leaf_count.zero_()  # the leaf-list parity chain restarts (fresh tree or another tree)
+    work.last_pass = pass_
     stream = _torch().cuda.current_stream().cuda_stream
     _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args), stream)
+    tree._scratch_dirty = True
 
 
 def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inject_actions=None,
@@ -152,6 +157,7 @@ def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inje
     if n and (bi.min() < 0 or bi.max() >= tree.counts()[0]):
         raise ValueError("invalid belief index in batch")
     tree.set_eta(eta)
+    tree.clear_pass_scratch()
     levels = max(d_max, 1)
     work = getattr(tree, "_api_work", None)
     if work is None or not work.fits(n, levels, dm.state_bytes, trace):
@@ -162,15 +168,15 @@ def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inje
     tree.ensure_capacity(nb + grow, na + grow)
     rec = dm.pack(batch.states)
     work.states[: rec.nbytes].copy_(torch.from_numpy(rec.view(np.uint8).reshape(-1)))
-    start = torch.from_numpy(bi.astype(np.int32)).cuda()
+    start = tree.to_device_beliefs(bi).to(torch.int32)
     inject = None
     if inject_actions is not None:
         arr = np.zeros((levels, n), dtype=np.int32)
         arr[: d_max] = np.asarray(inject_actions, dtype=np.int32).reshape(d_max, n)
         inject = torch.from_numpy(arr.reshape(-1)).cuda()
-    stamp = tree.next_stamp_base(levels)
-    run_search(tree, dm, work, key_of(rng), batch.depth, d_max, stamp, 0, inject, start)
-    leaves = LeafResult(tree, work, batch.depth, d_max, stamp, tree.generation)
+    pass_ = tree.next_pass()
+    run_search(tree, dm, work, key_of(rng), batch.depth, d_max, pass_, inject, start)
+    leaves = LeafResult(tree, work, batch.depth, d_max, pass_, tree.generation)
     tree.last_search = leaves
     return leaves
 

@@ -106,7 +106,7 @@ class Planner:
         self.work: Workspace | None = None
         self._cap_cache = {}
         self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
-        self.mode = 1  # vp_plan: 1 CUDA graph of per-phase kernels (default), 2 persistent kernel, 0 direct
+        self.mode = 1  # vp_plan: 1 CUDA graph of the step's launches (default), 0 direct launches
         self._bufs = {}
 
     def _capacity(self, n: int, config, A: int):
@@ -240,7 +240,9 @@ class Planner:
         _lib.call("vp_plan", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(a),
                   stream.cuda_stream)
         stream.synchronize()
-        tree._stamp_cursor = iters * (work.max_levels + 3)
+        tree.pass_cursor = iters  # vp_plan numbers its passes 1..iterations on the fresh tree
+        work.last_pass = iters
+        tree._canon_cache = None
         chosen, nb, na, overflow = (int(v) for v in oh.numpy()[:16].view(np.int32))
         if overflow:
             raise _lib.CapacityError("device tree overflowed its arena during plan()")
@@ -266,18 +268,17 @@ class Planner:
                 nb, na, _ = tree.counts()
                 ub_b, ub_a = nb, na
                 tree.ensure_capacity(nb + n * d_max, na + n * d_max)
-            _lib.call("vp_draw_root_states", C.byref(dm.desc), C.byref(work.struct), particles.data_ptr(),
-                      cumw.data_ptr(), m, fold(it_key, SITE_DRAW), stream)
             inject = None
             if inject_actions is not None:
                 arr = np.asarray(inject_actions[done], dtype=np.int32).reshape(d_max, n)
                 inject = torch.from_numpy(arr.reshape(-1)).cuda()
-            stamp = tree.next_stamp_base(work.max_levels)
-            run_search(tree, dm, work, fold(it_key, SITE_SEARCH), 0, d_max, stamp, done, inject)
-            run_backup(tree, work, 0, d_max, spec.discount, stamp)
+            pass_ = tree.next_pass()
+            run_search(tree, dm, work, fold(it_key, SITE_SEARCH), 0, d_max, pass_, inject,
+                       particles=particles, cumw=cumw, m=m, draw_key=fold(it_key, SITE_DRAW))
+            run_backup(tree, work, pass_, spec.discount)
             if trace:
-                traces.append({"levels": work.traces(0, d_max),
-                               "leaf_beliefs": work.leaf_belief.cpu().numpy().astype(np.int64),
+                traces.append({"levels": work.traces(tree, 0, d_max),
+                               "leaf_beliefs": tree.to_reference_beliefs(work.leaf_belief).cpu().numpy(),
                                "heuristic_values": work.leaf_value.cpu().numpy().copy()})
             ub_b += n * d_max
             ub_a += n * d_max

@@ -3,19 +3,22 @@
 
 Layout (all device tensors, row-indexed):
 
-    B   b_parent_action i32 | b_parent_obs u32 | b_depth i32
+    B   b_parent_action i32 | b_parent_obs u32 | b_depth i32 | b_ckey i64
     PSI psi [cap_beliefs, stride] fp32 (fast) or fp64 (parity), row-major,
-        rows padded to 16 B; b_flags bit 0 = row still lazily equal to init
-        b_lse f64 (cached LSE of the row) | b_value, b_weight f64 (backup scratch)
-    A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32
-        a_num, a_den f64 (backup scratch)
+        rows padded to 16 B; b_flags bit 0 = row still lazily equal to init,
+        bit 1 = row not yet written
+        b_lse f64 (cached LSE of the row) | b_value, b_weight f64, b_rows, b_done i32 (pass scratch)
+    A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32 | a_ckey i64
+        a_num, a_den f64, a_rows, a_done i32 (pass scratch)
     two open-addressing hash indexes of 16-byte slots, load factor <= 1/2:
         (belief << 32 | action) -> action row, (action row << 32 | obs) -> belief row
 
-Row 0 is the root (parent fields -1).  New rows are numbered in
-first-occurrence order of each batch (tree.py:10-12) by the device scans.
-Host-facing accessors download on demand and mirror the reference
-properties and ``serialize()`` text format (tree.py:298-320).
+Row 0 is the root (parent fields -1).  The device numbers new rows in the
+order warps create them; each row carries its creation key (pass, level,
+first row), and sorting by it gives the reference's first-occurrence ids
+(tree.py:10-12).  Every host-facing accessor (``tables``, ``serialize``,
+traces, search frontiers) speaks reference ids; the permutation is computed
+on the device (one sort per table) when something is exported.
 """
 
 from __future__ import annotations
@@ -66,7 +69,9 @@ class DeviceTree:
         self.exact = bool(exact)
         self.eta = float(eta)
         self.generation = 0
-        self._stamp_cursor = 0
+        self.pass_cursor = 0       # last search pass run on this tree (creation keys use it)
+        self._canon_cache = None
+        self._scratch_dirty = False  # a search ran without its backup
         self.last_search = None
         self._psi_dtype = torch.float32 if precision == "fp32" else torch.float64
         self._counters = torch.zeros(4, dtype=torch.int32, device="cuda")
@@ -88,8 +93,11 @@ class DeviceTree:
         dev = "cuda"
         A = self.action_count
 
-        def col(old, shape, dtype, keep):
-            new = torch.empty(shape, dtype=dtype, device=dev)
+        def col(old, shape, dtype, keep, fill=None):
+            # accumulators start at zero and creation keys unset (-1 = ~0): node creation
+            # on the device relies on rows beyond the counts being in that state
+            new = torch.empty(shape, dtype=dtype, device=dev) if fill is None else \
+                torch.full(shape if isinstance(shape, tuple) else (shape,), fill, dtype=dtype, device=dev)
             if old is not None and keep:
                 new[:keep] = old[:keep]
             return new
@@ -100,17 +108,21 @@ class DeviceTree:
         self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
         self.psi = col(g("psi"), (cap_b, self.psi_stride), self._psi_dtype, keep_b)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
-        self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b)
-        self.b_weight = col(g("b_weight"), cap_b, torch.float64, keep_b)
-        self.b_stamp = col(g("b_stamp"), cap_b, torch.int32, keep_b)
-        self.b_flags = col(g("b_flags"), cap_b, torch.uint8, keep_b)
+        self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b, 0)
+        self.b_weight = col(g("b_weight"), cap_b, torch.float64, keep_b, 0)
+        self.b_rows = col(g("b_rows"), cap_b, torch.int32, keep_b, 0)
+        self.b_done = col(g("b_done"), cap_b, torch.int32, keep_b, 0)
+        self.b_flags = col(g("b_flags"), cap_b, torch.int32, keep_b)
+        self.b_ckey = col(g("b_ckey"), cap_b, torch.int64, keep_b, -1)
         self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
         self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
-        self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a)
-        self.a_visits = col(g("a_visits"), cap_a, torch.int32, keep_a)
-        self.a_num = col(g("a_num"), cap_a, torch.float64, keep_a)
-        self.a_den = col(g("a_den"), cap_a, torch.float64, keep_a)
-        self.a_stamp = col(g("a_stamp"), cap_a, torch.int32, keep_a)
+        self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a, 0)
+        self.a_visits = col(g("a_visits"), cap_a, torch.int32, keep_a, 0)
+        self.a_num = col(g("a_num"), cap_a, torch.float64, keep_a, 0)
+        self.a_den = col(g("a_den"), cap_a, torch.float64, keep_a, 0)
+        self.a_rows = col(g("a_rows"), cap_a, torch.int32, keep_a, 0)
+        self.a_done = col(g("a_done"), cap_a, torch.int32, keep_a, 0)
+        self.a_ckey = col(g("a_ckey"), cap_a, torch.int64, keep_a, -1)
         ha = _pow2_at_least(2 * cap_a)
         hb = _pow2_at_least(2 * cap_b)
         self.hash_a = torch.empty((ha, 2), dtype=torch.int64, device=dev)
@@ -123,8 +135,8 @@ class DeviceTree:
         s.hmask_a, s.hmask_b = ha - 1, hb - 1
         s.psi_stride = self.psi_stride
         for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_weight",
-                     "b_stamp", "b_flags", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_num", "a_den",
-                     "a_stamp", "hash_a", "hash_b"):
+                     "b_rows", "b_done", "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits",
+                     "a_num", "a_den", "a_rows", "a_done", "a_ckey", "hash_a", "hash_b"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
@@ -155,7 +167,9 @@ class DeviceTree:
             self._init_prefs.copy_(torch.from_numpy(base))
         self.init_prefs = base
         self.generation += 1
-        self._stamp_cursor = 0
+        self.pass_cursor = 0
+        self._canon_cache = None
+        self._scratch_dirty = False
         self.last_search = None
         if device_init:
             _lib.call("vp_tree_init", C.byref(self.struct), _stream())
@@ -180,10 +194,61 @@ class DeviceTree:
         _lib.call("vp_tree_rehash", C.byref(self.struct), _stream())
         return True
 
-    def next_stamp_base(self, levels: int) -> int:
-        base = self._stamp_cursor
-        self._stamp_cursor += levels + 3
-        return base
+    def next_pass(self) -> int:
+        """Pass number of the next search on this tree (ckey order, leaf-list parity)."""
+        self.pass_cursor += 1
+        self._canon_cache = None
+        return self.pass_cursor
+
+    def clear_pass_scratch(self):
+        """Zero the per-pass counters after a search that was never backed up."""
+        if not self._scratch_dirty:
+            return
+        nb, na, _ = self.counts()
+        for t in (self.b_rows, self.b_done, self.b_value, self.b_weight):
+            t[:nb].zero_()
+        for t in (self.a_rows, self.a_done, self.a_num, self.a_den):
+            t[:na].zero_()
+        self._scratch_dirty = False
+
+    def canonical(self):
+        """(b_order, b_rank, a_order, a_rank) device tensors: ``order[k]`` is the
+        device row of reference id k, ``rank[row]`` its reference id."""
+        nb, na, _ = self.counts()
+        key = (self.generation, self.pass_cursor, nb, na)
+        if self._canon_cache is not None and self._canon_cache[0] == key:
+            return self._canon_cache[1]
+        torch = _torch()
+        out = []
+        for ck, cnt in ((self.b_ckey, nb), (self.a_ckey, na)):
+            order = torch.argsort(ck[:cnt], stable=True).to(torch.int64)
+            rank = torch.empty_like(order)
+            rank[order] = torch.arange(cnt, device=order.device, dtype=torch.int64)
+            out += [order, rank]
+        self._canon_cache = (key, tuple(out))
+        return self._canon_cache[1]
+
+    def to_reference_beliefs(self, rows):
+        """Device belief rows -> reference belief ids (numpy or torch input)."""
+        torch = _torch()
+        _, brank, _, _ = self.canonical()
+        t = torch.as_tensor(np.asarray(rows, dtype=np.int64) if not torch.is_tensor(rows) else rows,
+                            device="cuda").to(torch.int64)
+        return brank[t]
+
+    def to_reference_actions(self, rows):
+        torch = _torch()
+        _, _, _, arank = self.canonical()
+        t = torch.as_tensor(np.asarray(rows, dtype=np.int64) if not torch.is_tensor(rows) else rows,
+                            device="cuda").to(torch.int64)
+        return arank[t]
+
+    def to_device_beliefs(self, ids):
+        """Reference belief ids -> device rows."""
+        torch = _torch()
+        border, _, _, _ = self.canonical()
+        t = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda")
+        return border[t]
 
     # ------------------------------------------------------------------ reference-style accessors
     @property
@@ -195,24 +260,30 @@ class DeviceTree:
         return self.counts()[1]
 
     def tables(self) -> dict:
-        """All columns as host numpy arrays (int64 / float64 like the reference)."""
+        """All columns as host numpy arrays (int64 / float64 like the reference),
+        rows in reference (first-occurrence) order."""
+        torch = _torch()
         nb, na, _ = self.counts()
-        obs = self.b_parent_obs[:nb].cpu().numpy().view(np.uint32).astype(np.int64)
+        border, brank, aorder, arank = self.canonical()
+        pa = self.b_parent_action[:nb].to(torch.int64)[border]
+        pa = torch.where(pa >= 0, arank[pa.clamp(min=0)], pa)
+        obs = self.b_parent_obs[:nb][border].cpu().numpy().view(np.uint32).astype(np.int64)
         if nb:
             obs[0] = ROOT_SENTINEL
-        fresh = (self.b_flags[:nb] & 1).bool()[:, None]
+        fresh = (self.b_flags[:nb][border] & 1).bool()[:, None]
         init = self._init_prefs.to(self._psi_dtype)[None, :]
         # lazily initialised rows read as the initial row (tree.py:253)
-        prefs = _torch().where(fresh, init, self.psi[:nb, : self.action_count]).cpu().numpy().astype(np.float64)
+        prefs = torch.where(fresh, init, self.psi[:nb, : self.action_count][border]).cpu().numpy().astype(np.float64)
+        apb = brank[self.a_parent_belief[:na].to(torch.int64)[aorder]] if na else torch.zeros(0, dtype=torch.int64)
         return {
-            "parent_action": self.b_parent_action[:nb].cpu().numpy().astype(np.int64),
+            "parent_action": pa.cpu().numpy(),
             "parent_obs": obs,
-            "depth": self.b_depth[:nb].cpu().numpy().astype(np.int64),
+            "depth": self.b_depth[:nb][border].cpu().numpy().astype(np.int64),
             "prefs": prefs,
-            "action_parent_belief": self.a_parent_belief[:na].cpu().numpy().astype(np.int64),
-            "action_id": self.a_action[:na].cpu().numpy().astype(np.int64),
-            "action_reward_sum": self.a_reward[:na].cpu().numpy().copy(),
-            "action_visits": self.a_visits[:na].cpu().numpy().astype(np.int64),
+            "action_parent_belief": apb.cpu().numpy().astype(np.int64),
+            "action_id": self.a_action[:na][aorder].cpu().numpy().astype(np.int64),
+            "action_reward_sum": self.a_reward[:na][aorder].cpu().numpy().copy(),
+            "action_visits": self.a_visits[:na][aorder].cpu().numpy().astype(np.int64),
         }
 
     parent_action = property(lambda s: s.tables()["parent_action"])
