@@ -96,10 +96,9 @@ typedef struct vp_tree {
   int32_t* b_depth;
   void* psi;                  /* [cap_beliefs * psi_stride] float or double */
   double* b_lse;              /* cached (1/eta) log sum exp(eta PSI[b])      */
-  double* b_value;            /* leaf heuristic sum (search) / V (backup)    */
-  double* b_weight;           /* backup N: lifetime visits of valued actions */
+  double* b_value;            /* leaf heuristic sum of the current pass      */
   int32_t* b_rows;            /* rows that reached b in the current pass     */
-  int32_t* b_done;            /* rows of b whose action completed (backup)   */
+  void* b_acc;                /* backup accumulator, 16 B {f64 sum; u32 rows done; u32 N} */
   uint32_t* b_flags;          /* bit0: PSI row lazily == init; bit1: row not written */
   uint64_t* b_ckey;           /* creation key (canonical order)              */
   /* action table A */
@@ -107,10 +106,8 @@ typedef struct vp_tree {
   int32_t* a_action;
   double* a_reward;
   int32_t* a_visits;
-  double* a_num;              /* backup: sum V*N over valued children        */
-  double* a_den;              /* backup: sum N                               */
   int32_t* a_rows;            /* rows through the action in the current pass */
-  int32_t* a_done;            /* rows of its children delivered (backup)     */
+  void* a_acc;                /* backup accumulator, 16 B {f64 sum V*N; u32 rows done; u32 sum N} */
   uint64_t* a_ckey;           /* creation key (canonical order)              */
   /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */

@@ -48,11 +48,10 @@ class VpTree(C.Structure):
         ("psi_dtype", C.c_int32), ("exact", C.c_int32), ("psi_stride", C.c_int32),
         ("hmask_a", C.c_uint64), ("hmask_b", C.c_uint64),
         ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_depth", C.c_void_p),
-        ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p), ("b_weight", C.c_void_p),
-        ("b_rows", C.c_void_p), ("b_done", C.c_void_p), ("b_flags", C.c_void_p), ("b_ckey", C.c_void_p),
+        ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p),
+        ("b_rows", C.c_void_p), ("b_acc", C.c_void_p), ("b_flags", C.c_void_p), ("b_ckey", C.c_void_p),
         ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),
-        ("a_visits", C.c_void_p), ("a_num", C.c_void_p), ("a_den", C.c_void_p), ("a_rows", C.c_void_p),
-        ("a_done", C.c_void_p), ("a_ckey", C.c_void_p),
+        ("a_visits", C.c_void_p), ("a_rows", C.c_void_p), ("a_acc", C.c_void_p), ("a_ckey", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p), ("eta", C.c_double),
     ]

@@ -39,18 +39,15 @@ __global__ void k_clear(vp_tree T) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i < nb) {
       T.b_value[i] = 0.0;
-      T.b_weight[i] = 0.0;
       T.b_rows[i] = 0;
-      T.b_done[i] = 0;
+      reinterpret_cast<Acc*>(T.b_acc)[i] = Acc{0.0, 0u, 0u};
       T.b_ckey[i] = ~0ull;
     }
     if (i < na) {
       T.a_reward[i] = 0.0;
       T.a_visits[i] = 0;
-      T.a_num[i] = 0.0;
-      T.a_den[i] = 0.0;
       T.a_rows[i] = 0;
-      T.a_done[i] = 0;
+      reinterpret_cast<Acc*>(T.a_acc)[i] = Acc{0.0, 0u, 0u};
       T.a_ckey[i] = ~0ull;
     }
   }
@@ -109,11 +106,12 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
   __shared__ __align__(8) u64 s_bar[kSearchWarps];
   const int A = T.action_count;
   Stage<PsiT> sg = make_stage<PsiT>(smem_raw, s_bar, sc);
-  PsiT* init_cdf = reinterpret_cast<PsiT*>(smem_raw) + (size_t)kSearchWarps * sc.rows * sc.stride;
-  PsiT* init_row = init_cdf + A;
-  for (int a = threadIdx.x; a < A; a += blockDim.x) {
-    init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
-    init_row[a] = (PsiT)T.init_prefs[a];
+  // [stage rows | initial row (16-B padded) | initial CDF]
+  PsiT* init_row = reinterpret_cast<PsiT*>(smem_raw) + (size_t)kSearchWarps * sc.rows * sc.stride;
+  PsiT* init_cdf = init_row + T.psi_stride;
+  for (int a = threadIdx.x; a < T.psi_stride; a += blockDim.x) {
+    init_row[a] = a < A ? (PsiT)T.init_prefs[a] : (PsiT)0;
+    if (a < A) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
   }
   // the leaf counter of the NEXT pass is reset here: its previous user (the
   // backup of the pass before this one) has finished
@@ -248,7 +246,8 @@ static StageCfg stage_cfg(int A, int per_warp_bytes) {
 template <class PsiT, bool Exact>
 static int32_t search_geometry(int A, StageCfg& sc, size_t& smem) {
   sc = Exact ? StageCfg{0, 4} : stage_cfg<PsiT>(A, env_int("VP_STAGE_KB", 32) * 1024);
-  smem = ((size_t)kSearchWarps * sc.rows * sc.stride + 2 * (size_t)A) * sizeof(PsiT);
+  const size_t padded = ((size_t)A * sizeof(PsiT) + 15) / 16 * 16 / sizeof(PsiT);
+  smem = ((size_t)kSearchWarps * sc.rows * sc.stride + padded + (size_t)A) * sizeof(PsiT);
   return VP_OK;
 }
 

@@ -40,6 +40,38 @@ __device__ __forceinline__ u64 creation_key(u32 pass, int level, int row) {
   return ((u64)pass << 32) | ((u64)(u32)level << 24) | (u64)(u32)row;
 }
 
+// Backup accumulator of a node: sum (V*N for an action, the incremental
+// exp-sum for a belief), rows delivered so far, and an integer count (sum N
+// for an action, lifetime visits of the valued actions for a belief).
+struct __align__(16) Acc {
+  double sum;
+  u32 rows;
+  u32 cnt;
+};
+
+// Deliver (dsum, drows, dcnt) to a node whose deliveries total `target` rows.
+// A delivery carrying all of them is the node's only one: it completes the
+// node with no atomic (the usual case below the top levels).  Otherwise the
+// sums go out as L2 reductions (contention-friendly) and an acq_rel add on
+// the row count elects the completing delivery, which then reads the totals.
+// Returns true on the completing delivery, with the totals in `out`.
+__device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 drows, u32 dcnt, u32 target,
+                                            Acc& out) {
+  if (drows == target) {
+    out = Acc{dsum, drows, dcnt};
+    return true;
+  }
+  Acc* p = reinterpret_cast<Acc*>(base) + i;
+  red_add(&p->sum, dsum);
+  red_add(reinterpret_cast<int*>(&p->cnt), (int)dcnt);
+  if ((u32)atom_add_acq_rel(reinterpret_cast<int*>(&p->rows), (int)drows) + drows != target) return false;
+  out.sum = ld_relaxed_f64(&p->sum);
+  out.cnt = ld_relaxed_u32(&p->cnt);
+  out.rows = target;
+  *p = Acc{0.0, 0u, 0u};
+  return true;
+}
+
 // ------------------------------------------------------------------ exp helpers (fast mode)
 // exp(eta * psi - shift) is evaluated as exp2(fma(eta*log2e, psi, -shift*log2e)).
 // fp32: one MUFU.EX2 (flush-to-zero: probabilities below 2^-126 are zero mass)
@@ -197,6 +229,65 @@ __device__ __forceinline__ int search_cdf(const CT* cdf, int A, CT u) {
   return lo < A ? lo : A - 1;
 }
 
+// A staged PSI row (shared memory) becomes its unnormalised CDF, in place:
+// lane j owns the contiguous columns [j C, j C + C), C = ceil(A / 32), keeps a
+// running sum over them, and one warp scan adds the preceding lanes' totals.
+// Returns the row total (the softmax normaliser) on every lane.
+template <class PsiT>
+struct VecOf;
+template <>
+struct VecOf<float> {
+  typedef float4 T;
+  static constexpr int N = 4;
+};
+template <>
+struct VecOf<double> {
+  typedef double2 T;
+  static constexpr int N = 2;
+};
+template <class PsiT>
+__device__ __forceinline__ PsiT row_cdf_inplace(PsiT* row, int A, PsiT e2, PsiT sh2) {
+  typedef VecOf<PsiT> V;
+  const int C = (A + 31) >> 5;
+  const int lo = lane_id() * C, hi = min(A, lo + C);
+  PsiT loc = 0;
+  const bool vec = (C % V::N) == 0;  // chunks start 16-B aligned: vector LDS/STS
+  if (vec) {
+    for (int c = lo; c < hi; c += V::N) {
+      typename V::T v = *reinterpret_cast<typename V::T*>(row + c);
+      PsiT* x = reinterpret_cast<PsiT*>(&v);
+#pragma unroll
+      for (int j = 0; j < V::N; ++j) {
+        loc += (c + j < hi) ? fexp2(ffma(e2, x[j], -sh2)) : (PsiT)0;
+        x[j] = loc;
+      }
+      *reinterpret_cast<typename V::T*>(row + c) = v;
+    }
+  } else {
+    for (int c = lo; c < hi; ++c) {
+      loc += fexp2(ffma(e2, row[c], -sh2));
+      row[c] = loc;
+    }
+  }
+  const PsiT incl = warp_inclusive_scan(loc);
+  const PsiT excl = __shfl_up_sync(FULL, incl, 1);
+  if (lane_id() > 0) {
+    if (vec) {
+      for (int c = lo; c < hi; c += V::N) {
+        typename V::T v = *reinterpret_cast<typename V::T*>(row + c);
+        PsiT* x = reinterpret_cast<PsiT*>(&v);
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) x[j] += excl;
+        *reinterpret_cast<typename V::T*>(row + c) = v;
+      }
+    } else {
+      for (int c = lo; c < hi; ++c) row[c] += excl;
+    }
+  }
+  __syncwarp();
+  return __shfl_sync(FULL, incl, 31);
+}
+
 // ------------------------------------------------------------------ TMA bulk staging
 
 __device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -240,13 +331,18 @@ struct Stage {
 
 // ------------------------------------------------------------------ warp helpers
 
-// Sum of v over the lanes in `grp`, in lane (= row) order, delivered to all lanes.
+// Sum of v over the lanes in `grp`, in lane (= row) order, delivered to all
+// lanes; as many shuffle rounds as the largest group has members.
 __device__ __forceinline__ double group_sum_ordered(double v, u32 grp) {
+  const int rounds = (int)__reduce_max_sync(FULL, (unsigned)__popc(grp));
+  u32 m = grp;
   double s = 0.0;
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    const double x = __shfl_sync(FULL, v, j);
-    if ((grp >> j) & 1u) s += x;
+  for (int t = 0; t < rounds; ++t) {
+    const double x = __shfl_sync(FULL, v, m ? __ffs(m) - 1 : lane_id());
+    if (m) {
+      s += x;
+      m &= m - 1u;
+    }
   }
   return s;
 }
@@ -267,7 +363,11 @@ __device__ __forceinline__ void materialise_rows(const vp_tree& T, const PsiT* i
     mask &= mask - 1;
     const int bj = __shfl_sync(FULL, b, j);
     PsiT* row = psi + (size_t)bj * T.psi_stride;
-    for (int a = lane_id(); a < A; a += 32) row[a] = init_row[a];
+    // rows and the shared initial row are 16-B aligned and padded: 16-B stores
+    typedef typename VecOf<PsiT>::T VT;
+    const int nv = (A + VecOf<PsiT>::N - 1) / VecOf<PsiT>::N;
+    for (int v = lane_id(); v < nv; v += 32)
+      reinterpret_cast<VT*>(row)[v] = reinterpret_cast<const VT*>(init_row)[v];
   }
 }
 
@@ -313,9 +413,8 @@ __device__ void block_tree_init(const vp_tree& T) {
       T.b_parent_obs[0] = 0xffffffffu;
       T.b_depth[0] = 0;
       T.b_value[0] = 0.0;
-      T.b_weight[0] = 0.0;
       T.b_rows[0] = 0;
-      T.b_done[0] = 0;
+      reinterpret_cast<Acc*>(T.b_acc)[0] = Acc{0.0, 0u, 0u};
       T.b_flags[0] = 0;  // the root row is written (above), not lazy
       T.b_ckey[0] = 0;
       T.counters[0] = 1;
@@ -334,28 +433,42 @@ __device__ void block_tree_init(const vp_tree& T) {
 template <class State>
 __device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r) {
   const double u = uniform1(key, (u64)r);
-  int lo = 0, hi = m;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cumw[mid] > u) hi = mid;
-    else lo = mid + 1;
+  // weights are uniform after every SIR update (belief.py:101): the first
+  // guess floor(u m) is usually the answer, confirmed with two loads
+  int idx = min((int)(u * (double)m), m - 1);
+  const double hi_v = cumw[idx], lo_v = idx ? cumw[idx - 1] : -1.0;
+  if (!(hi_v > u && lo_v <= u)) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cumw[mid] > u) hi = mid;
+      else lo = mid + 1;
+    }
+    idx = lo < m - 1 ? lo : m - 1;
   }
-  return particles[lo < m - 1 ? lo : m - 1];
+  return particles[idx];
 }
 
 // ------------------------------------------------------------------ search
 
 // Rows arriving at belief c (one reduction per distinct belief of the warp).
-// At the leaf level the first arrival also appends c to the leaf list.
+// At the leaf level the first arrival also appends c to the leaf list (one
+// list atomic per warp).  Called by all lanes.
 __device__ __forceinline__ void arrive(const vp_tree& T, const vp_work& W, int* leaf_count, int c, u32 grp,
                                        bool lead, bool leaf_level) {
-  if (!lead) return;
   const int cnt = __popc(grp);
-  if (leaf_level) {
-    if (atomicAdd(&T.b_rows[c], cnt) == 0) W.leaves[atomicAdd(leaf_count, 1)] = c;
-  } else {
-    red_add(&T.b_rows[c], cnt);
+  if (!leaf_level) {
+    if (lead) red_add(&T.b_rows[c], cnt);
+    return;
   }
+  const bool first = lead && atomicAdd(&T.b_rows[c], cnt) == 0;
+  const u32 fm = __ballot_sync(FULL, first);
+  if (!fm) return;
+  const int src = __ffs(fm) - 1;
+  int base = 0;
+  if (lane_id() == src) base = atomicAdd(leaf_count, __popc(fm));
+  base = __shfl_sync(FULL, base, src);
+  if (first) W.leaves[base + __popc(fm & ((1u << lane_id()) - 1u))] = c;
 }
 
 // The search kernel body for one warp = 32 consecutive rows.
@@ -459,19 +572,13 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         mbar_wait(sg.bar, sg.phase);
         sg.phase ^= 1u;
         PsiT my_total = 0;
+        u32 rem = leaders;
+        for (int k = 0; k < s0; ++k) rem &= rem - 1u;
         for (int k = 0; k < cnt; ++k) {
-          const int src = (int)__fns(leaders, 0, s0 + k + 1);
-          const PsiT shk = __shfl_sync(FULL, sh2, src);
-          PsiT* row = sg.buf + (size_t)k * sg.cfg.stride;
-          PsiT carry = 0;
-          for (int a0 = 0; a0 < A; a0 += 32) {
-            const int c = a0 + lane;
-            PsiT v = c < A ? fexp2(ffma(e2, row[c], -shk)) : (PsiT)0;
-            v = warp_inclusive_scan(v) + carry;
-            if (c < A) row[c] = v;
-            carry = __shfl_sync(FULL, v, 31);
-          }
-          if (lane == k) my_total = carry;
+          const int src = __ffs(rem) - 1;
+          rem &= rem - 1u;
+          const PsiT tot = row_cdf_inplace(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
+          if (lane == k) my_total = tot;
         }
         __syncwarp();
         const PsiT total = __shfl_sync(FULL, my_total, mine ? my_slot - s0 : 0);
@@ -642,14 +749,16 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   const int cnt = W.leaf_count[pass & 1u];
   const int i = warp_index * 32 + lane;
   PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
+  const double eta = T.eta;
   int c = -1, rows = 0;
-  double V = 0.0, N = 0.0;
+  double V = 0.0;
+  u32 N = 0;
   if (i < cnt) {
     // leaf: V = mean heuristic, N = batch count (backup.py:44-51, 82-87)
     c = W.leaves[i];
     rows = T.b_rows[c];
-    N = (double)rows;
-    V = T.b_value[c] / N;
+    N = (u32)rows;
+    V = T.b_value[c] / (double)rows;
     T.b_value[c] = 0.0;
     T.b_rows[c] = 0;
   }
@@ -657,40 +766,42 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0;
   while (__any_sync(FULL, live)) {
     int ready = -1;
+    double lse_pre = 0.0, bsum = 0.0;
+    u32 bcnt = 0, btot = 0;
+    bool fresh = false;
     if (live) {
       live = false;
       const int x = T.b_parent_action[c];
       if (x >= 0) {
-        // child mean of the action (backup.py:64-68)
-        red_add(&T.a_num[x], V * N);
-        red_add(&T.a_den[x], N);
-        const int tot = T.a_rows[x];
-        if (atom_add_acq_rel(&T.a_done[x], rows) + rows == tot) {
+        // the completing delivery needs these; load them before the CAS round trip
+        const int tot = T.a_rows[x], vis = T.a_visits[x], pb = T.a_parent_belief[x], act = T.a_action[x];
+        const double rew = T.a_reward[x];
+        // child mean of the action (backup.py:64-68): sum V*N, sum N
+        Acc aa;
+        if (acc_deliver(T.a_acc, x, V * (double)N, (u32)rows, N, (u32)tot, aa)) {
           // last child: Q (backup.py:96-104) and PSI[b, a] += Q - LSE_pre(b) (:106-108)
           ++n_act;
-          const double num = ld_relaxed_f64(&T.a_num[x]), den = ld_relaxed_f64(&T.a_den[x]);
-          T.a_num[x] = 0.0;
-          T.a_den[x] = 0.0;
-          T.a_done[x] = 0;
           T.a_rows[x] = 0;
-          const int vis = T.a_visits[x];
-          const double q = T.a_reward[x] / (double)vis + (gamma * num) / den;
-          const int pb = T.a_parent_belief[x];
-          const double lse_pre = T.b_lse[pb];
-          PsiT* cell = psi + (size_t)pb * T.psi_stride + T.a_action[x];
+          lse_pre = T.b_lse[pb];
+          btot = (u32)T.b_rows[pb];
+          fresh = !Exact && (T.b_flags[pb] & 1u);
+          const double q = rew / (double)vis + (gamma * aa.sum) / (double)aa.cnt;
+          PsiT* cell = psi + (size_t)pb * T.psi_stride + act;
           const double old_v = (double)__ldcg(cell);
           const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
           *cell = new_v;
-          if constexpr (!Exact) {
-            // a lazily-initial row (LSE_pre is its exact LSE): LSE_post follows from the
-            // changed cells, sum_a exp(eta (psi_a - LSE_pre)) = 1 + sum_changed (new - old)
-            if (T.b_flags[pb] & 1u)
-              red_add(&T.b_value[pb], exp(T.eta * ((double)new_v - lse_pre)) - exp(T.eta * (old_v - lse_pre)));
-          }
+          // a lazily-initial row (LSE_pre is its exact LSE): LSE_post follows from the
+          // changed cells, sum_a exp(eta (psi_a - LSE_pre)) = 1 + sum_changed (new - old)
+          double term = 0.0;
+          if (fresh) term = exp(eta * ((double)new_v - lse_pre)) - exp(eta * (old_v - lse_pre));
+          else __threadfence();  // the full-row LSE of pb reads this cell from another SM
           // N(b) = lifetime visits of the valued actions (backup.py:110-114)
-          red_add(&T.b_weight[pb], (double)vis);
-          const int btot = T.b_rows[pb];
-          if (atom_add_acq_rel(&T.b_done[pb], tot) + tot == btot) ready = pb;
+          Acc ba;
+          if (acc_deliver(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba)) {
+            ready = pb;
+            bsum = ba.sum;
+            bcnt = ba.cnt;
+          }
         }
       }
     }
@@ -698,21 +809,19 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
       // last action of a belief: V = LSE_post (backup.py:109), cached as the next LSE_pre.
       // Lazily-initial rows use the incremental sum; other rows (and tiny / overflowing
       // incremental sums) are read in full by the warp.
-      bool full = Exact && ready >= 0;
-      if constexpr (!Exact) {
-        if (ready >= 0) {
-          full = true;
-          if (T.b_flags[ready] & 1u) {
-            const double sum = 1.0 + ld_relaxed_f64(&T.b_value[ready]);
-            if (sum > 1e-9 && sum < 1e300) {
-              V = T.b_lse[ready] + log(sum) / T.eta;
-              full = false;
-            }
-          }
+      bool full = ready >= 0;
+      if (fresh) {
+        const double sum = 1.0 + bsum;
+        if (sum > 1e-9 && sum < 1e300) {
+          V = lse_pre + log(sum) / eta;
+          full = false;
         }
       }
       const u32 fmask = __ballot_sync(FULL, full);
-      if (fmask) lse_ready<PsiT, Exact>(T, full ? ready : -1, fmask, s_v);
+      if (fmask) {
+        __threadfence();
+        lse_ready<PsiT, Exact>(T, full ? ready : -1, fmask, s_v);
+      }
       if (ready >= 0) {
         ++n_bel;
         if (full) {
@@ -721,12 +830,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         }
         T.b_lse[ready] = V;
         T.b_flags[ready] = 0u;
-        N = ld_relaxed_f64(&T.b_weight[ready]);
-        rows = T.b_rows[ready];
-        T.b_weight[ready] = 0.0;
-        T.b_value[ready] = 0.0;
         T.b_rows[ready] = 0;
-        T.b_done[ready] = 0;
+        N = bcnt;
+        rows = (int)btot;
         c = ready;
         live = true;
       }

@@ -7,9 +7,9 @@ Layout (all device tensors, row-indexed):
     PSI psi [cap_beliefs, stride] fp32 (fast) or fp64 (parity), row-major,
         rows padded to 16 B; b_flags bit 0 = row still lazily equal to init,
         bit 1 = row not yet written
-        b_lse f64 (cached LSE of the row) | b_value, b_weight f64, b_rows, b_done i32 (pass scratch)
+        b_lse f64 (cached LSE of the row) | b_value f64, b_rows i32, b_acc 16 B (pass scratch)
     A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32 | a_ckey i64
-        a_num, a_den f64, a_rows, a_done i32 (pass scratch)
+        a_rows i32, a_acc 16 B (pass scratch)
     two open-addressing hash indexes of 16-byte slots, load factor <= 1/2:
         (belief << 32 | action) -> action row, (action row << 32 | obs) -> belief row
 
@@ -109,19 +109,16 @@ class DeviceTree:
         self.psi = col(g("psi"), (cap_b, self.psi_stride), self._psi_dtype, keep_b)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
         self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b, 0)
-        self.b_weight = col(g("b_weight"), cap_b, torch.float64, keep_b, 0)
         self.b_rows = col(g("b_rows"), cap_b, torch.int32, keep_b, 0)
-        self.b_done = col(g("b_done"), cap_b, torch.int32, keep_b, 0)
+        self.b_acc = col(g("b_acc"), (cap_b, 2), torch.int64, keep_b, 0)
         self.b_flags = col(g("b_flags"), cap_b, torch.int32, keep_b)
         self.b_ckey = col(g("b_ckey"), cap_b, torch.int64, keep_b, -1)
         self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
         self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
         self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a, 0)
         self.a_visits = col(g("a_visits"), cap_a, torch.int32, keep_a, 0)
-        self.a_num = col(g("a_num"), cap_a, torch.float64, keep_a, 0)
-        self.a_den = col(g("a_den"), cap_a, torch.float64, keep_a, 0)
         self.a_rows = col(g("a_rows"), cap_a, torch.int32, keep_a, 0)
-        self.a_done = col(g("a_done"), cap_a, torch.int32, keep_a, 0)
+        self.a_acc = col(g("a_acc"), (cap_a, 2), torch.int64, keep_a, 0)
         self.a_ckey = col(g("a_ckey"), cap_a, torch.int64, keep_a, -1)
         ha = _pow2_at_least(2 * cap_a)
         hb = _pow2_at_least(2 * cap_b)
@@ -134,9 +131,9 @@ class DeviceTree:
         s.exact = int(self.exact)
         s.hmask_a, s.hmask_b = ha - 1, hb - 1
         s.psi_stride = self.psi_stride
-        for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_weight",
-                     "b_rows", "b_done", "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits",
-                     "a_num", "a_den", "a_rows", "a_done", "a_ckey", "hash_a", "hash_b"):
+        for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
+                     "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_rows", "a_acc",
+                     "a_ckey", "hash_a", "hash_b"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
@@ -205,9 +202,9 @@ class DeviceTree:
         if not self._scratch_dirty:
             return
         nb, na, _ = self.counts()
-        for t in (self.b_rows, self.b_done, self.b_value, self.b_weight):
+        for t in (self.b_rows, self.b_value, self.b_acc):
             t[:nb].zero_()
-        for t in (self.a_rows, self.a_done, self.a_num, self.a_den):
+        for t in (self.a_rows, self.a_acc):
             t[:na].zero_()
         self._scratch_dirty = False
 
