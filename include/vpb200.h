@@ -57,6 +57,8 @@ typedef struct vp_model {
   int32_t mars_n, mars_m, mars_ops, mars_pad;
   double mars_half_eff;
   const int8_t* mars_rock_at; /* [n*n], index x*n + y, -1 = no rock      */
+  const double* mars_acc;     /* [(n+1)^2] check accuracy at |dx|*(n+1)+|dy|, host numpy (mars.py:136-140) */
+  const double* mars_gpow;    /* [2n+2] gamma**k, host numpy (mars.py:232-240) */
   int16_t mars_rock_x[64];
   int16_t mars_rock_y[64];
   /* TABULAR */

@@ -29,7 +29,8 @@ class VpModel(C.Structure):
         ("kind", C.c_int32), ("action_count", C.c_int32), ("obs_arity", C.c_int32),
         ("state_bytes", C.c_int32), ("discount", C.c_double),
         ("mars_n", C.c_int32), ("mars_m", C.c_int32), ("mars_ops", C.c_int32), ("mars_pad", C.c_int32),
-        ("mars_half_eff", C.c_double), ("mars_rock_at", C.c_void_p),
+        ("mars_half_eff", C.c_double), ("mars_rock_at", C.c_void_p), ("mars_acc", C.c_void_p),
+        ("mars_gpow", C.c_void_p),
         ("mars_rock_x", C.c_int16 * 64), ("mars_rock_y", C.c_int16 * 64),
         ("tab_states", C.c_int32), ("tab_obs", C.c_int32),
         ("tab_cum_t", C.c_void_p), ("tab_cum_z", C.c_void_p), ("tab_reward", C.c_void_p),
@@ -183,11 +184,12 @@ def layout_mismatches() -> list:
     mine = [C.sizeof(VpModel), C.sizeof(VpTree), C.sizeof(VpWork), C.sizeof(VpSearchArgs),
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
-            VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset]
+            VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
+            VpModel.mars_gpow.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m"]
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

@@ -557,7 +557,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_plan_args, out_dev),
                        (int32_t)offsetof(vp_tree, init_cdf),
                        (int32_t)offsetof(vp_tree, a_ckey),
-                       (int32_t)offsetof(vp_search_args, m)};
+                       (int32_t)offsetof(vp_search_args, m),
+                       (int32_t)offsetof(vp_model, mars_gpow)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];

@@ -69,10 +69,8 @@ struct MarsModel {
       reading[k] = 2;  // NULL
       if (!gone[k] && op[k] >= 5) {
         const int rk = op[k] - 5;
-        const double ddx = (double)(x[k] - M.mars_rock_x[rk]);
-        const double ddy = (double)(y[k] - M.mars_rock_y[rk]);
-        const double d = sqrt(ddx * ddx + ddy * ddy);
-        const double acc = 0.5 * (1.0 + exp2(-d / M.mars_half_eff));
+        const int adx = abs(x[k] - M.mars_rock_x[rk]), ady = abs(y[k] - M.mars_rock_y[rk]);
+        const double acc = M.mars_acc[adx * (n + 1) + ady];  // 0.5 (1 + 2^(-d / half_eff))
         const bool correct = u < acc;
         const bool truth = (rocks >> rk) & 1ull;
         reading[k] = (truth == correct) ? 0 : 1;
@@ -96,12 +94,11 @@ struct MarsModel {
     // mars.py:223-243
     if (s.term) return 0.0;
     const int n = M.mars_n;
-    const double g = M.discount;
     const int xs[2] = {s.x0, s.x1}, ys[2] = {s.y0, s.y1};
     const bool act[2] = {xs[0] < n, xs[1] < n};
     double h = 0.0;
-    h += act[0] ? 10.0 * pow(g, (double)(n - xs[0] - 1)) : 0.0;
-    h += act[1] ? 10.0 * pow(g, (double)(n - xs[1] - 1)) : 0.0;
+    h += act[0] ? 10.0 * M.mars_gpow[n - xs[0] - 1] : 0.0;
+    h += act[1] ? 10.0 * M.mars_gpow[n - xs[1] - 1] : 0.0;
     if (!(act[0] || act[1])) return h;
     auto term_i = [&](int i) -> double {
       int best = 0x3fffffff;
@@ -112,9 +109,9 @@ struct MarsModel {
         best = dd < best ? dd : best;
       }
       const double good = ((s.rocks >> i) & 1ull) ? 10.0 : 0.0;
-      return good * pow(g, (double)best);
+      return good * M.mars_gpow[best];
     };
-    h += pairwise_sum(term_i, 0, M.mars_m);
+    h += pairwise_leaf(term_i, 0, M.mars_m);  // numpy pairwise sum; m <= 64 < 128: one leaf block
     return h;
   }
 };

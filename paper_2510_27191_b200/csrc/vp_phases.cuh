@@ -395,20 +395,19 @@ __device__ void block_tree_init(const vp_tree& T) {
     if constexpr (Exact) {
       v = 0.0;
       if (threadIdx.x == 0) v = lse_exact(reinterpret_cast<const double*>(psi), A, T.eta);
+      v = __shfl_sync(FULL, v, 0);
     } else {
       v = row_lse_fast<PsiT>(psi, A, T.eta);
     }
+    // normalised CDF of the initial row with the fast sampler's arithmetic (warp-parallel)
+    PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
+    for (int a = threadIdx.x; a < A; a += 32) cdf[a] = psi[a];
+    __syncwarp();
+    const PsiT total = row_cdf_inplace(cdf, A, (PsiT)(T.eta * kLog2eD), (PsiT)(T.eta * v * kLog2eD));
+    for (int a = threadIdx.x; a < A; a += 32) cdf[a] = cdf[a] / total;
     if (threadIdx.x == 0) {
       T.init_lse[0] = v;
       T.b_lse[0] = v;
-      // CDF of the initial row with the fast sampler's exact arithmetic
-      PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
-      const PsiT e2 = (PsiT)(T.eta * kLog2eD), sh2 = (PsiT)(T.eta * v * kLog2eD);
-      PsiT cum = 0;
-      for (int a = 0; a < A; ++a) {
-        cum += fexp2(ffma(e2, psi[a], -sh2));
-        cdf[a] = cum;
-      }
       T.b_parent_action[0] = -1;
       T.b_parent_obs[0] = 0xffffffffu;
       T.b_depth[0] = 0;

@@ -126,13 +126,25 @@ def _rock_bits(rocks: np.ndarray) -> np.ndarray:
 
 
 def mars_pack(states) -> np.ndarray:
+    """MarsStates -> 16-B records, written as raw bytes (this runs on the host inside every
+    e2e planning step, so it avoids per-field structured assignment)."""
     x = np.asarray(states.x)
     y = np.asarray(states.y)
-    rec = np.zeros(len(x), dtype=MARS_DTYPE)
-    rec["x0"], rec["y0"], rec["x1"], rec["y1"] = x[:, 0], y[:, 0], x[:, 1], y[:, 1]
-    rec["term"] = np.asarray(states.terminal, dtype=bool)
-    rec["rocks"] = _rock_bits(states.rocks)
-    return rec
+    n = len(x)
+    out = np.zeros((n, 16), dtype=np.uint8)
+    xy = out[:, :4].reshape(n, 2, 2)
+    xy[:, :, 0] = x
+    xy[:, :, 1] = y
+    out[:, 4] = np.asarray(states.terminal, dtype=bool)
+    r = np.asarray(states.rocks, dtype=bool)
+    m = r.shape[1]
+    if m > 64:
+        raise ValueError("MARS device records hold at most 64 rocks")
+    if 0 < m <= 52:  # bit weights 2^k are exact in float64: one BLAS mat-vec
+        out[:, 8:].view(np.uint64)[:, 0] = (r.astype(np.float64) @ np.exp2(np.arange(m))).astype(np.uint64)
+    elif m:
+        out[:, 8:8 + (m + 7) // 8] = np.packbits(r, axis=1, bitorder="little")
+    return out.view(MARS_DTYPE).reshape(n)
 
 
 def mars_descriptor(model, unpack=None) -> DeviceModel:
@@ -146,6 +158,12 @@ def mars_descriptor(model, unpack=None) -> DeviceModel:
     d.mars_half_eff = float(model.half_efficiency_distance)
     rock_at = np.asarray(model.rock_at, dtype=np.int64).astype(np.int8).reshape(-1)  # [x, y] -> x*n + y
     d.mars_rock_at = dm.upload(rock_at)
+    # the generative model's only transcendental terms, tabulated with the reference's own numpy
+    # arithmetic (bit-exact by construction): sensor accuracy by |dx|, |dy| and gamma**k
+    dxy = np.arange(n + 1, dtype=np.int64)
+    dist = np.sqrt(dxy[:, None] ** 2.0 + dxy[None, :] ** 2.0)
+    d.mars_acc = dm.upload(np.ascontiguousarray(model.check_accuracy(dist.reshape(-1)), dtype=np.float64))
+    d.mars_gpow = dm.upload(model.spec.discount ** np.arange(2 * n + 2, dtype=np.float64))
     for i in range(m):
         d.mars_rock_x[i] = int(model.rock_x[i])
         d.mars_rock_y[i] = int(model.rock_y[i])
