@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
+                    help="N > 1: one planning step sharded over the GPUs (n_parallel rows per GPU, "
+                         "trajectories all-gathered over NCCL) or independent replicas")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     a.n_parallel = a.n_parallel or c["n_parallel"]
@@ -95,14 +98,15 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(args, world, actions=None):
+def workload_config(args, world, actions=None, sharded=False):
     c = CONFIGS[args.config]
     return {"workload": f"{c['name']} plan(), n_parallel={args.n_parallel}, iterations={args.iterations}",
             "config_id": args.config, "problem": c["name"], "actions": actions, "n_parallel": args.n_parallel,
             "iterations": args.iterations, "eta": WORKLOAD["eta"], "particles": WORKLOAD["particles"],
             "simulations_per_step": args.n_parallel * args.iterations,
             "episode_steps_per_step": args.n_parallel * sum(range(1, args.iterations + 1)),
-            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "parallelism": (f"sharded x{world}: {args.n_parallel} rows per GPU, one tree, NCCL all-gather of "
+                            f"trajectories per pass" if sharded else f"replicas x{world}") if world > 1 else "1 GPU",
             "l2": "per-step tree arena (~1 GB) > 126 MB L2; no flush needed"}
 
 
@@ -188,20 +192,32 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    seed = 1000 + rank
+    sharded = world > 1 and args.multi == "sharded"
+    # sharded: ONE planning step over world * n_parallel rows (same seed on every rank);
+    # replicas: every rank plans its own problem
+    seed = 1000 + (0 if sharded else rank)
     model = make_model(vp, args, seed)
     A = model.spec.action_count
     belief = vp.ParticleBelief.from_model(model, WORKLOAD["particles"], vp.RowRng.from_seed(seed).derive(3))
-    cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=args.n_parallel, iterations=args.iterations)
-    planner = vp.Planner(args.precision)
+    n_rows = args.n_parallel * (world if sharded else 1)
+    cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=n_rows, iterations=args.iterations)
+    planner = vp.ShardedPlanner(world, rank, group=dist.group.WORLD, precision=args.precision) if sharded \
+        else vp.Planner(args.precision)
     dm = vp.device_model(model)
     particles, cumw, m = planner.upload_belief(dm, belief)
     rngs = [vp.RowRng.from_seed(seed).derive(1, t) for t in range(args.warmup + args.steps)]
 
     def step(t):
+        if sharded:  # trajectories of this rank's rows, one NCCL all-gather per pass, replicated insert + backup
+            return planner.plan(belief, model, cfg, rngs[t], resident=(particles, cumw, m))
         # belief resident in HBM; one vp_plan call (CUDA graph replay) per planning step
         d, tree, work = planner.prepare(model, cfg, device_init=False)
         return planner.run_fixed(d, tree, work, m, model.spec, cfg, key_of(rngs[t]), from_host=False)
+
+    def plan_e2e(t):
+        if sharded:
+            return planner.plan(belief, model, cfg, rngs[t])
+        return vp.plan(belief, model, cfg, rngs[t], precision=args.precision)
 
     def barrier():
         torch.cuda.synchronize()
@@ -233,12 +249,12 @@ def run_b200(args):
 
     # e2e through the public API with host buffers (own warm-up: first call captures its graph)
     for t in range(args.warmup):
-        vp.plan(belief, model, cfg, rngs[t], precision=args.precision)
+        plan_e2e(t)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in range(args.steps):
-        out = vp.plan(belief, model, cfg, rngs[args.warmup + t], precision=args.precision)
+        out = plan_e2e(args.warmup + t)
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -296,7 +312,7 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
             "data": "synthetic (MARS belief sampled from the model; no dataset)",
-            "config": workload_config(args, world, A),
+            "config": workload_config(args, world, A, sharded),
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
                     "ms_per_step": round(e2e_ms / args.steps, 4)},
             "gpu_launches": int(launches), "clocks": clk, "roofline": dominant,

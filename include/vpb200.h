@@ -141,6 +141,7 @@ typedef struct vp_work {
   uint32_t* trace_obs;
   int32_t* trace_anode;
   int32_t* trace_belief;
+  double* trace_reward;       /* written in VP_SEARCH_TRAJECTORY mode        */
 } vp_work;
 
 /* One search call (search.py:86-119).  With `particles` set, every row first
@@ -160,8 +161,25 @@ typedef struct vp_search_args {
   const uint64_t* draw_key_dev; /* device copy of draw_key, or NULL         */
   uint64_t draw_key;          /* it_rng.derive(0).key (solver.py:98)        */
   int32_t m;                  /* particles                                  */
+  int32_t mode;               /* vp_search_mode                             */
+  int32_t row0;               /* global id of row 0 (RNG streams, creation keys); 0 unless sharded */
   int32_t pad1;
+  const uint32_t* inject_obs;    /* VP_SEARCH_INSERT: [d_max * n] observations */
+  const double* inject_reward;   /* VP_SEARCH_INSERT: [d_max * n] rewards      */
+  const double* inject_leaf;     /* VP_SEARCH_INSERT: [n] leaf heuristic values */
 } vp_search_args;
+
+/* Search modes.  Within a pass a row's trajectory depends only on the tree as
+ * it was when the pass started (PSI changes only in the backup; nodes created
+ * during the pass are lazily initial), so a pass splits into a trajectory
+ * phase that can be sharded over GPUs with no interaction and an insert phase
+ * that replays all trajectories into each replica of the tree. */
+enum vp_search_mode {
+  VP_SEARCH_FUSED = 0,       /* sample, step and insert (one GPU)                       */
+  VP_SEARCH_TRAJECTORY = 1,  /* sample and step rows row0..row0+n-1 against the tree
+                                read-only; write trace_action/obs/reward + leaf_value */
+  VP_SEARCH_INSERT = 2       /* insert the injected trajectories of all rows, no sampling */
+};
 
 /* A whole fixed-iteration planning step (solver.py:79-113) enqueued by one
  * call: per iteration one search kernel (root draw fused) and one backup

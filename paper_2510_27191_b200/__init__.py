@@ -17,13 +17,14 @@ from .envs import (LightDarkModel, MarsModel, SyntheticModel, TabularModel, Tabu
 from .rng import BoundRng, RowRng
 from .search import LeafResult, SearchBatch, sample_actions, search, softmax_rows
 from .solver import Planner, PlanOutcome, RunRecord, SolverConfig, get_planner, plan, run_episode
+from .shard import ShardedPlanner, shard_rows
 from .tree import DeviceTree, init_tree
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BoundRng", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "ParticleBelief", "PlanOutcome",
-    "Planner", "ProblemModel", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
+    "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",
     "sir_update", "softmax_rows", "systematic_resample", "tiger_model",

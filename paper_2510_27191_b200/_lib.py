@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libvpb200.so")
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
 VP_PSI_F32, VP_PSI_F64 = 0, 1
+VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
 ABI_VERSION = 2
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
@@ -64,7 +65,7 @@ class VpWork(C.Structure):
         ("leaves", C.c_void_p), ("leaf_count", C.c_void_p), ("leaf_belief", C.c_void_p),
         ("leaf_value", C.c_void_p), ("stats", C.c_void_p),
         ("trace_action", C.c_void_p), ("trace_obs", C.c_void_p), ("trace_anode", C.c_void_p),
-        ("trace_belief", C.c_void_p),
+        ("trace_belief", C.c_void_p), ("trace_reward", C.c_void_p),
     ]
 
 
@@ -74,7 +75,9 @@ class VpSearchArgs(C.Structure):
         ("pass_", C.c_uint32), ("pad0", C.c_int32),
         ("inject_actions", C.c_void_p), ("start_beliefs", C.c_void_p), ("search_key_dev", C.c_void_p),
         ("particles", C.c_void_p), ("cum_weights", C.c_void_p), ("draw_key_dev", C.c_void_p),
-        ("draw_key", C.c_uint64), ("m", C.c_int32), ("pad1", C.c_int32),
+        ("draw_key", C.c_uint64), ("m", C.c_int32), ("mode", C.c_int32), ("row0", C.c_int32),
+        ("pad1", C.c_int32), ("inject_obs", C.c_void_p), ("inject_reward", C.c_void_p),
+        ("inject_leaf", C.c_void_p),
     ]
 
 

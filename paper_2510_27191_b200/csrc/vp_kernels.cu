@@ -615,6 +615,12 @@ int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const v
   if (!t || !m || !w || !a || !work_ok(*w)) return VP_ERR_INVALID;
   if (a->depth0 < 0 || a->d_max < a->depth0 || a->d_max > w->max_levels || a->pass < 1) return VP_ERR_INVALID;
   if (a->particles && (!a->cum_weights || a->m < 1)) return VP_ERR_INVALID;
+  if (a->mode < VP_SEARCH_FUSED || a->mode > VP_SEARCH_INSERT || a->row0 < 0) return VP_ERR_INVALID;
+  if (a->mode == VP_SEARCH_TRAJECTORY &&
+      (a->depth0 != 0 || a->start_beliefs || !w->trace_action || !w->trace_obs || !w->trace_reward))
+    return VP_ERR_INVALID;
+  if (a->mode == VP_SEARCH_INSERT && (!a->inject_actions || !a->inject_obs || !a->inject_reward || !a->inject_leaf))
+    return VP_ERR_INVALID;
   if (m->action_count != t->action_count) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   const vp_tree T = *t;

@@ -450,6 +450,67 @@ __device__ __forceinline__ State draw_state(const State* particles, const double
 
 // ------------------------------------------------------------------ search
 
+// Softmax draw of one action per lane (search.py:46-83) from the PSI row of
+// belief b (or the initial row when flags bit 0 says it is lazily initial).
+// Called by all 32 lanes; lanes with ok == false return 0.
+template <class PsiT, bool Exact>
+__device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, Stage<PsiT>& sg, const PsiT* init_cdf,
+                                           int b, u32 fl, bool ok, double u) {
+  const int A = T.action_count, lane = lane_id();
+  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+  const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
+  const PsiT e2 = (PsiT)(T.eta * kLog2eD);
+  int a = 0;
+  if constexpr (Exact) {
+    if (ok) {
+      const double* row = (fl & 1u) ? T.init_prefs : reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride;
+      a = sample_exact(row, A, T.eta, u);
+    }
+  } else {
+    const bool fresh = ok && (fl & 1u);
+    const bool need = ok && !fresh;
+    if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
+    // distinct non-fresh beliefs of the warp: one TMA bulk copy of each PSI
+    // row into the warp's stage; the warp turns every staged row into its
+    // CDF (32 columns per step, shuffle scan) and each lane binary-searches
+    // its row with u scaled by the row total (p = e / sum e, search.py:51-54)
+    const u32 g = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
+    const int my_leader = __ffs(g) - 1;
+    const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
+    const int K = __popc(leaders);
+    if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
+    const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
+    const PsiT sh2 = need ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
+    for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
+      const int cnt = min(sg.cfg.rows, K - s0);
+      fence_async_smem();
+      if (lane == 0) mbar_expect_tx(sg.bar, row_bytes * (u32)cnt);
+      __syncwarp();
+      const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
+      if (mine && lane == my_leader)
+        bulk_g2s(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, psi + (size_t)b * T.psi_stride, row_bytes,
+                 sg.bar);
+      mbar_wait(sg.bar, sg.phase);
+      sg.phase ^= 1u;
+      PsiT my_total = 0;
+      u32 rem = leaders;
+      for (int k = 0; k < s0; ++k) rem &= rem - 1u;
+      for (int k = 0; k < cnt; ++k) {
+        const int src = __ffs(rem) - 1;
+        rem &= rem - 1u;
+        const PsiT tot = row_cdf_inplace(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
+        if (lane == k) my_total = tot;
+      }
+      __syncwarp();
+      const PsiT total = __shfl_sync(FULL, my_total, mine ? my_slot - s0 : 0);
+      if (mine) a = search_cdf(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, A, (PsiT)(u * (double)total));
+      __syncwarp();
+    }
+  }
+  return a;
+}
+
+
 // Rows arriving at belief c (one reduction per distinct belief of the warp).
 // At the leaf level the first arrival also appends c to the leaf list (one
 // list atomic per warp).  Called by all lanes.
@@ -470,32 +531,88 @@ __device__ __forceinline__ void arrive(const vp_tree& T, const vp_work& W, int* 
   if (first) W.leaves[base + __popc(fm & ((1u << lane_id()) - 1u))] = c;
 }
 
+// Read-only probe of a hash index (no inserts run concurrently): node id or -1.
+__device__ __forceinline__ int find_key(const Slot* tab, u64 mask, u64 key) {
+  u64 h = slot_hash(key) & mask;
+  while (true) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(tab + h));
+    if (v.x == key) return (int)(u32)v.y;
+    if (v.x == kEmptyKey) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+// VP_SEARCH_TRAJECTORY: the rows' actions, observations, rewards and leaf
+// values against the tree as it stands (no node is created).  A row whose path
+// leaves the existing tree draws from the initial row from then on -- exactly
+// what the fused search does, since nodes created during a pass are lazily
+// initial -- so the trajectory is that of the fused search.
+template <class Model, class PsiT, bool Exact>
+__device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
+                                Stage<PsiT>& sg, const PsiT* init_cdf, typename Model::State& st, int r, int rg,
+                                u64 skey) {
+  const int n = W.n;
+  const bool active = r < n;
+  const Slot* ha = slots(T.hash_a);
+  const Slot* hb = slots(T.hash_b);
+  int b = 0;
+  bool known = active;  // the row's belief existed when the pass started
+  u32 fl = known ? T.b_flags[0] : 1u;
+  for (int l = 0; l < S.d_max; ++l) {
+    const u64 lkey = fold(skey, (u64)l);
+    const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
+    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u);
+    u32 o = 0;
+    double rw = 0.0;
+    if (active) {
+      Model::step(M, st, a, fold(lkey, 1), (u64)rg, o, rw);
+      const size_t t = (size_t)l * n + r;
+      W.trace_action[t] = a;
+      W.trace_obs[t] = o;
+      W.trace_reward[t] = rw;
+    }
+    if (known) {
+      const int x = find_key(ha, T.hmask_a, ((u64)(u32)b << 32) | (u32)a);
+      const int c = x < 0 ? -1 : find_key(hb, T.hmask_b, ((u64)(u32)x << 32) | o);
+      known = c >= 0;
+      if (known) {
+        b = c;
+        fl = T.b_flags[c];
+      }
+    }
+  }
+  if (active) W.leaf_value[r] = Model::heuristic(M, st);
+}
+
 // The search kernel body for one warp = 32 consecutive rows.
 template <class Model, class PsiT, bool Exact>
 __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                             Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index) {
   typedef typename Model::State State;
-  const int n = W.n, A = T.action_count, lane = lane_id();
+  const int n = W.n, lane = lane_id();
   const int r = warp_index * 32 + lane;
+  const int rg = S.row0 + r;  // global row id: RNG streams and creation keys
   const bool active = r < n;
+  const bool insert = S.mode == VP_SEARCH_INSERT;
   const int d = S.d_max, depth0 = S.depth0;
   const u32 pass = S.pass;
   const u64 skey = S.search_key_dev ? *S.search_key_dev : S.search_key;
   Slot* ha = slots(T.hash_a);
   Slot* hb = slots(T.hash_b);
   int* leaf_count = W.leaf_count + (pass & 1u);
-  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
-  const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
-  const PsiT e2 = (PsiT)(T.eta * kLog2eD);
 
   State st{};
-  if (active) {
+  if (active && !insert) {
     if (S.particles) {
       const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
-      st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, r);
+      st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, rg);
     } else {
       st = reinterpret_cast<const State*>(W.states)[r];
     }
+  }
+  if (S.mode == VP_SEARCH_TRAJECTORY) {
+    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, st, r, rg, skey);
+    return;
   }
   int b = active ? (S.start_beliefs ? S.start_beliefs[r] : 0) : 0;
   bool ok = active;
@@ -535,60 +652,21 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), b);
     }
     // ---- softmax draw (search.py:108-112)
-    const double u = active ? uniform1(fold(lkey, 0), (u64)r) : 0.0;  // level_rng.derive(0)
+    const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
     int a = 0;
-    if (S.inject_actions) {
-      a = active ? S.inject_actions[(size_t)l * n + r] : 0;
-    } else if constexpr (Exact) {
-      if (ok) {
-        const double* row = (fl & 1u) ? T.init_prefs : reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride;
-        a = sample_exact(row, A, T.eta, u);
-      }
-    } else {
-      const bool fresh = ok && (fl & 1u);
-      const bool need = ok && !fresh;
-      if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
-      // distinct non-fresh beliefs of the warp: one TMA bulk copy of each PSI
-      // row into the warp's stage; the warp turns every staged row into its
-      // CDF (32 columns per step, shuffle scan) and each lane binary-searches
-      // its row with u scaled by the row total (p = e / sum e, search.py:51-54)
-      const u32 g = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
-      const int my_leader = __ffs(g) - 1;
-      const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
-      const int K = __popc(leaders);
-      if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
-      const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-      const PsiT sh2 = need ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
-      for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
-        const int cnt = min(sg.cfg.rows, K - s0);
-        fence_async_smem();
-        if (lane == 0) mbar_expect_tx(sg.bar, row_bytes * (u32)cnt);
-        __syncwarp();
-        const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
-        if (mine && lane == my_leader)
-          bulk_g2s(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, psi + (size_t)b * T.psi_stride, row_bytes,
-                   sg.bar);
-        mbar_wait(sg.bar, sg.phase);
-        sg.phase ^= 1u;
-        PsiT my_total = 0;
-        u32 rem = leaders;
-        for (int k = 0; k < s0; ++k) rem &= rem - 1u;
-        for (int k = 0; k < cnt; ++k) {
-          const int src = __ffs(rem) - 1;
-          rem &= rem - 1u;
-          const PsiT tot = row_cdf_inplace(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
-          if (lane == k) my_total = tot;
-        }
-        __syncwarp();
-        const PsiT total = __shfl_sync(FULL, my_total, mine ? my_slot - s0 : 0);
-        if (mine) a = search_cdf(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, A, (PsiT)(u * (double)total));
-        __syncwarp();
-      }
-    }
+    if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
+    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u);
     // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
     double rw = 0.0;
-    if (ok) Model::step(M, st, a, fold(lkey, 1), (u64)r, o, rw);  // level_rng.derive(1)
+    if (insert) {
+      if (active) {
+        o = S.inject_obs[(size_t)l * n + r];
+        rw = S.inject_reward[(size_t)l * n + r];
+      }
+    } else if (ok) {
+      Model::step(M, st, a, fold(lkey, 1), (u64)rg, o, rw);  // level_rng.derive(1)
+    }
 
     // ---- action node (b, a): append_actions (tree.py:180-218)
     int x = 0;
@@ -606,7 +684,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
           // accumulators are zero (cleared at tree reset); the key is a min-reduction
           T.a_parent_belief[x] = b;
           T.a_action[x] = a;
-          red_min(&T.a_ckey[x], creation_key(pass, l, r));
+          red_min(&T.a_ckey[x], creation_key(pass, l, rg));
         } else {
           T.counters[2] = 1;  // overflow: the host fails the plan loudly
         }
@@ -616,7 +694,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (lead && !cl.won) {
         const u64 w = wait_published(ha, cl.slot, cl.word);
         x = (int)(u32)w;
-        if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, r));
+        if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, rg));
       }
       x = __shfl_sync(FULL, x, leader);
       if (W.stats) {
@@ -659,7 +737,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
           T.b_lse[c] = T.init_lse[0];
           // fresh (PSI == init); an interior node's row is written by its creator next level
           T.b_flags[c] = interior_next ? 1u : 3u;
-          red_min(&T.b_ckey[c], creation_key(pass, l, r));
+          red_min(&T.b_ckey[c], creation_key(pass, l, rg));
         } else {
           T.counters[2] = 1;
         }
@@ -670,7 +748,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         const u64 w = wait_published(hb, cl.slot, cl.word);
         c = (int)(u32)w;
         cpass = (u32)(w >> 32);
-        if (cpass == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, l, r));
+        if (cpass == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, l, rg));
       }
       c = __shfl_sync(FULL, c, leader);
       c_new = __shfl_sync(FULL, cpass, leader) == pass;
@@ -696,7 +774,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   // ---- leaves: heuristic value (search.py:119), summed per leaf (backup.py:44-51)
   double h = 0.0;
   if (active) {
-    h = ok ? Model::heuristic(M, st) : 0.0;
+    h = !ok ? 0.0 : insert ? S.inject_leaf[r] : Model::heuristic(M, st);
     W.leaf_belief[r] = b;
     W.leaf_value[r] = h;
   }

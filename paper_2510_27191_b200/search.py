@@ -61,7 +61,8 @@ class Workspace:
             self.trace_obs = torch.empty(L * n, **i32)
             self.trace_anode = torch.empty(L * n, **i32)
             self.trace_belief = torch.empty(L * n, **i32)
-            for name in ("trace_action", "trace_obs", "trace_anode", "trace_belief"):
+            self.trace_reward = torch.empty(L * n, dtype=torch.float64, device=dev)
+            for name in ("trace_action", "trace_obs", "trace_anode", "trace_belief", "trace_reward"):
                 setattr(s, name, getattr(self, name).data_ptr())
         self.struct = s
         self.enable_stats(stats)
