@@ -67,6 +67,7 @@ typedef struct vp_model {
   const double* tab_cum_z;     /* [A*S*O] cumsum over o                   */
   const double* tab_reward;    /* [S*A]                                   */
   const uint8_t* tab_terminal; /* [S]                                     */
+  const double* tab_log_z;     /* [A*S*O] log Z (SIR likelihood)          */
   /* SYNTHETIC */
   int32_t syn_branching, syn_term_per_mille;
   double syn_obs_accuracy;
@@ -251,6 +252,19 @@ int32_t vp_plan(const vp_tree* tree, const vp_model* model, const vp_work* work,
                 const vp_plan_args* args, void* stream);
 /* argmax of PSI[0] with lowest-id ties (solver.py:112) into out_dev[0]. */
 int32_t vp_root_argmax(const vp_tree* tree, int32_t* out_dev, void* stream);
+
+/* ---- SIR belief update between planning steps (belief.py:47-102) ---------- */
+/* Propagate the m particles through G(s, action) with the counter RNG `key`
+ * (rng.derive(retry), rows 0..m-1), reweight by log P(observation | s'), and
+ * normalise: cum_out = cumsum of the new weights in numpy order with
+ * cum_out[m-1] = 1 (belief.py:50-53).  finite_out[0] = 1 if any weight is
+ * non-zero (otherwise the caller retries with the next key, belief.py:86-97). */
+int32_t vp_sir_weigh(const vp_model* model, const void* states, const double* weights, int32_t m, int32_t action,
+                     uint32_t observation, uint64_t key, void* states_out, double* logw_scratch, double* cum_out,
+                     int32_t* finite_out, void* stream);
+/* Systematic resampling (belief.py:47-53): out[j] = prop[first i with cum[i] > (j + u0) / m]. */
+int32_t vp_sir_resample(const vp_model* model, const void* prop, const double* cum, int32_t m, double u0,
+                        void* states_out, void* stream);
 
 /* ---- test hooks (parity of individual kernels) ------------------------- */
 int32_t vp_rng_uniform(uint64_t key, const int64_t* rows, int64_t n, int32_t k,

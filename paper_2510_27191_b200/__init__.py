@@ -10,7 +10,7 @@ point raises.
 
 from . import _lib
 from .backup import backup, log_sum_exp_rows
-from .belief import ParticleBelief, SirUpdate, sir_update, systematic_resample
+from .belief import DeviceBelief, ParticleBelief, SirUpdate, sir_update, systematic_resample
 from .core import ProblemModel, ProblemSpec, StepResult
 from .envs import (LightDarkModel, MarsModel, SyntheticModel, TabularModel, TabularPOMDP, device_model,
                    problem_from_config, tiger_model)
@@ -23,7 +23,7 @@ from .tree import DeviceTree, init_tree
 __version__ = "0.1.0"
 
 __all__ = [
-    "BoundRng", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "ParticleBelief", "PlanOutcome",
+    "BoundRng", "DeviceBelief", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "ParticleBelief", "PlanOutcome",
     "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",

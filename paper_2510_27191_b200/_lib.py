@@ -35,7 +35,7 @@ class VpModel(C.Structure):
         ("mars_rock_x", C.c_int16 * 64), ("mars_rock_y", C.c_int16 * 64),
         ("tab_states", C.c_int32), ("tab_obs", C.c_int32),
         ("tab_cum_t", C.c_void_p), ("tab_cum_z", C.c_void_p), ("tab_reward", C.c_void_p),
-        ("tab_terminal", C.c_void_p),
+        ("tab_terminal", C.c_void_p), ("tab_log_z", C.c_void_p),
         ("syn_branching", C.c_int32), ("syn_term_per_mille", C.c_int32),
         ("syn_obs_accuracy", C.c_double), ("syn_salt", C.c_uint64),
         ("ld_step", C.c_double), ("ld_light_x", C.c_double), ("ld_goal_radius", C.c_double),
@@ -112,6 +112,11 @@ _SIGNATURES = [
      [C.POINTER(VpTree), C.POINTER(VpModel), C.POINTER(VpWork), C.POINTER(VpPlanArgs), C.c_void_p]),
     ("vp_backup", C.c_int32, [C.POINTER(VpTree), C.POINTER(VpWork), C.c_uint32, C.c_double, C.c_void_p]),
     ("vp_root_argmax", C.c_int32, [C.POINTER(VpTree), C.c_void_p, C.c_void_p]),
+    ("vp_sir_weigh", C.c_int32,
+     [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_uint32, C.c_uint64, C.c_void_p,
+      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("vp_sir_resample", C.c_int32,
+     [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
     ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_rng_normal", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_model_step", C.c_int32,

@@ -427,6 +427,75 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   return check_launch();
 }
 
+// ---- SIR belief update (belief.py:47-102)
+
+template <class Model>
+__global__ void k_sir_propagate(vp_model M, const typename Model::State* in, const double* w, int m, int a, u32 obs,
+                                u64 key, typename Model::State* out, double* logw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  typename Model::State st = in[i];
+  u32 o;
+  double r;
+  Model::step(M, st, a, key, (u64)i, o, r);  // step_batch(states, actions, rng.derive(retry).bind(rows))
+  out[i] = st;
+  logw[i] = log(w[i]) + Model::obs_loglik(M, st, a, obs);  // log(weights) + log_lik (belief.py:88-90)
+}
+
+// One block: max over finite log-weights, shifted = exp(lw - max), its numpy
+// pairwise sum, then the sequential cumsum of shifted / sum with cum[-1] = 1
+// (belief.py:91-93, 50-52) -- the serial parts by one thread, in numpy order.
+__global__ void k_sir_normalise(const double* logw, int m, double* cum, int* finite) {
+  __shared__ double s_max[32];
+  double mx = -INFINITY;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double v = logw[i];
+    if (v > -INFINITY) mx = fmax(mx, v);
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0) s_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? s_max[threadIdx.x] : -INFINITY;
+    v = warp_max(v);
+    if (threadIdx.x == 0) s_max[0] = v;
+  }
+  __syncthreads();
+  mx = s_max[0];
+  if (mx == -INFINITY) {
+    if (threadIdx.x == 0) finite[0] = 0;
+    return;
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) cum[i] = exp(logw[i] - mx);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double total = pairwise_sum([&](int i) -> double { return cum[i]; }, 0, m);
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double wi = cum[i] / total;
+      acc = i ? acc + wi : wi;
+      cum[i] = acc;
+    }
+    cum[m - 1] = 1.0;
+    finite[0] = 1;
+  }
+}
+
+template <class Model>
+__global__ void k_sir_resample(const typename Model::State* prop, const double* cum, int m, double u0,
+                               typename Model::State* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const double pos = ((double)j + u0) / (double)m;
+  int lo = 0, hi = m;  // searchsorted(cum, pos, side="right")
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cum[mid] > pos) hi = mid;
+    else lo = mid + 1;
+  }
+  out[j] = prop[lo < m ? lo : m - 1];
+}
+
 // ---- test-hook kernels
 
 __global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
@@ -674,6 +743,44 @@ int32_t vp_root_argmax(const vp_tree* t, int32_t* out_dev, void* stream) {
   return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto) -> int32_t {
     Launch L_(KK_ARGMAX, st);
     k_root_argmax<decltype(z)><<<1, 32, 0, st>>>(T, out_dev);
+    return check_launch();
+  });
+}
+
+int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weights, int32_t m, int32_t action,
+                     uint32_t observation, uint64_t key, void* states_out, double* logw, double* cum, int32_t* finite,
+                     void* stream) {
+  if (!mdl || !states || !weights || m < 1 || !states_out || !logw || !cum || !finite) return VP_ERR_INVALID;
+  if (action < 0 || action >= mdl->action_count || observation > (uint32_t)mdl->obs_arity) return VP_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_model M = *mdl;
+  return dispatch_model(M.kind, [&](auto md) -> int32_t {
+    typedef decltype(md) Model;
+    typedef typename Model::State State;
+    if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
+    {
+      Launch L_(KK_HOOK, st);
+      k_sir_propagate<Model><<<blocks_for(m, 256), 256, 0, st>>>(M, reinterpret_cast<const State*>(states), weights,
+                                                                   m, action, observation, key,
+                                                                   reinterpret_cast<State*>(states_out), logw);
+    }
+    { Launch L_(KK_HOOK, st); k_sir_normalise<<<1, 1024, 0, st>>>(logw, m, cum, finite); }
+    return check_launch();
+  });
+}
+
+int32_t vp_sir_resample(const vp_model* mdl, const void* prop, const double* cum, int32_t m, double u0,
+                        void* states_out, void* stream) {
+  if (!mdl || !prop || !cum || m < 1 || !states_out || !(u0 >= 0.0 && u0 < 1.0)) return VP_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_model M = *mdl;
+  return dispatch_model(M.kind, [&](auto md) -> int32_t {
+    typedef decltype(md) Model;
+    typedef typename Model::State State;
+    if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
+    Launch L_(KK_HOOK, st);
+    k_sir_resample<Model><<<blocks_for(m, 256), 256, 0, st>>>(reinterpret_cast<const State*>(prop), cum, m, u0,
+                                                              reinterpret_cast<State*>(states_out));
     return check_launch();
   });
 }

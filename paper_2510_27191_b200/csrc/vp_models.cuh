@@ -90,6 +90,32 @@ struct MarsModel {
     s.term = term ? 1u : 0u;
   }
 
+  // log P(obs | s', a) for the SIR reweighting (mars.py:182-221)
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int a, u32 obs) {
+    if (obs == (u32)M.obs_arity) return s.term ? 0.0 : -INFINITY;
+    if (s.term) return -INFINITY;
+    const int n = M.mars_n, P = M.mars_ops;
+    const int ops[2] = {a / P, a % P};
+    const int want[2] = {(int)obs / 3, (int)obs % 3};  // GOOD 0, BAD 1, NULL 2
+    const int xs[2] = {s.x0, s.x1}, ys[2] = {s.y0, s.y1};
+    double logp = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double p;
+      if (ops[k] >= 5) {
+        const int rk = ops[k] - 5;
+        const double acc = M.mars_acc[abs(xs[k] - M.mars_rock_x[rk]) * (n + 1) + abs(ys[k] - M.mars_rock_y[rk])];
+        const bool good = (s.rocks >> rk) & 1ull;
+        p = want[k] == 0 ? (good ? acc : 1.0 - acc) : want[k] == 1 ? (good ? 1.0 - acc : acc) : 0.0;
+        if (xs[k] == n) p = want[k] == 2 ? 1.0 : 0.0;
+      } else {
+        p = want[k] == 2 ? 1.0 : 0.0;
+      }
+      logp += log(p);
+    }
+    return logp;
+  }
+
   static __device__ __forceinline__ double heuristic(const vp_model& M, const State& s) {
     // mars.py:223-243
     if (s.term) return 0.0;
@@ -149,6 +175,12 @@ struct TabularModel {
     s.term = term ? 1 : 0;
   }
   static __device__ __forceinline__ double heuristic(const vp_model&, const State&) { return 0.0; }
+  // log Z[a, s', o] (tabular.py observation model)
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int a, u32 obs) {
+    if (obs == (u32)M.obs_arity) return s.term ? 0.0 : -INFINITY;
+    if (s.term) return -INFINITY;
+    return M.tab_log_z[((size_t)a * M.tab_states + s.idx) * M.tab_obs + obs];
+  }
 };
 
 // ------------------------------------------------------------------ SYNTHETIC
@@ -190,6 +222,19 @@ struct SyntheticModel {
   static __device__ __forceinline__ double heuristic(const vp_model&, const State& s) {
     if (s.term) return 0.0;
     return 0.5 * unit53(mix64(s.word + kSynHeur));
+  }
+  // P(o) = acc [o == true] + (1 - acc) P(floor(u |O|) == o), u = k 2^-53 (oracle SyntheticModel)
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int, u32 obs) {
+    const int no = M.obs_arity;
+    if (obs == (u32)no) return s.term ? 0.0 : -INFINITY;
+    if (s.term) return -INFINITY;
+    const int true_obs = (int)((s.word >> 17) % (u64)no);
+    const double two53 = 9007199254740992.0;
+    const double lo = ceil((double)obs / (double)no * two53);
+    const double hi = (int)obs < no - 1 ? ceil((double)(obs + 1) / (double)no * two53) : two53;
+    const double p_noise = (hi - lo) * kInv53;
+    const double acc = M.syn_obs_accuracy;
+    return log(acc * (double)((int)obs == true_obs) + (1.0 - acc) * p_noise);
   }
 };
 
@@ -236,6 +281,20 @@ struct LightDarkModel {
   static __device__ __forceinline__ double heuristic(const vp_model&, const State& s) {
     if (s.term) return 0.0;
     return -(fabs(s.x) + fabs(s.y));
+  }
+  // Bin mass of the per-axis Gaussian, border bins absorbing the tails (oracle LightDarkModel)
+  static __device__ __forceinline__ double bin_mass(const vp_model& M, double center, double sigma, int b) {
+    const int half = M.ld_bins / 2;
+    const double den = sigma * 1.4142135623730951;
+    const double chi = b == M.ld_bins - 1 ? 1.0 : 0.5 * (1.0 + erf(((b + 1 - half) * M.ld_bin_width - center) / den));
+    const double clo = b == 0 ? 0.0 : 0.5 * (1.0 + erf(((b - half) * M.ld_bin_width - center) / den));
+    return chi - clo;
+  }
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int, u32 obs) {
+    if (obs == (u32)M.obs_arity) return s.term ? 0.0 : -INFINITY;
+    if (s.term) return -INFINITY;
+    const double sigma = M.ld_sigma0 + M.ld_sigma_slope * fabs(s.x - M.ld_light_x);
+    return log(bin_mass(M, s.x, sigma, (int)obs / M.ld_bins) * bin_mass(M, s.y, sigma, (int)obs % M.ld_bins));
   }
 };
 

@@ -193,6 +193,8 @@ def tabular_descriptor(model, unpack=None) -> DeviceModel:
     d.tab_cum_z = dm.upload(np.cumsum(z, axis=2).reshape(-1))
     d.tab_reward = dm.upload(np.asarray(p.rewards, dtype=np.float64).reshape(-1))
     d.tab_terminal = dm.upload(np.asarray(p.terminal_states, dtype=np.uint8))
+    with np.errstate(divide="ignore"):
+        d.tab_log_z = dm.upload(np.log(z).reshape(-1))  # SIR likelihood (tabular.py observation model)
     return dm
 
 

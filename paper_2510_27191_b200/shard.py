@@ -100,6 +100,7 @@ class ShardedPlanner(Planner):
         self.world, self.rank, self.group = int(world), int(rank), group
         self.distributed = group is not None or (world > 1 and self._dist_ready())
         self._traj_work = None
+        self.phase_ms = None  # set to {} to accumulate per-phase device time (CUDA events)
 
     @staticmethod
     def _dist_ready() -> bool:
@@ -133,10 +134,19 @@ class ShardedPlanner(Planner):
         key = key_of(rng)
         stream = torch.cuda.current_stream().cuda_stream
         d_max = 1
+        ev = []
+
+        def mark(name):
+            if self.phase_ms is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append((name, e))
+
         for it in range(config.iterations):
             it_key = fold(key, it)
             pass_ = tree.next_pass()
             # 1. trajectories of this process's shard(s), read-only on the replica
+            mark("start")
             blocks = []
             for s in self._shards():
                 row0, cnt = shard_rows(n, self.world, s)
@@ -151,12 +161,14 @@ class ShardedPlanner(Planner):
                 o = tw.trace_obs[: d_max * cnt].view(d_max, cnt)
                 r = tw.trace_reward[: d_max * cnt].view(d_max, cnt)
                 blocks.append(pack_trajectories(a, o, r, tw.leaf_value[:cnt], torch))
+            mark("trajectory")
             # 2. exchange
             if self.distributed:
                 full = all_gather_blocks(blocks[0], self.world, self.group, torch)
             else:
                 full = gather_blocks(blocks, torch)
             actions, obs, rewards, leaf = unpack_trajectories(full, d_max, torch)
+            mark("exchange")
             # 3. insert every trajectory into the replica, then back up
             args = _lib.VpSearchArgs()
             args.depth0, args.d_max, args.pass_ = 0, d_max, pass_
@@ -169,11 +181,16 @@ class ShardedPlanner(Planner):
             _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
                       stream)
             tree._scratch_dirty = True
+            mark("insert")
             run_backup(tree, work, pass_, model.spec.discount)
+            mark("backup")
             d_max = min(d_max + 1, config.d_max_cap)
         _lib.call("vp_root_argmax", C.byref(tree.struct), self._out.data_ptr(), stream)
         _lib.call("vp_tree_counts", C.byref(tree.struct), tree._host_counts, stream)
         chosen = int(self._out.item())
+        for (_, e0), (name, e1) in zip(ev, ev[1:]):
+            if name != "start":
+                self.phase_ms[name] = self.phase_ms.get(name, 0.0) + e0.elapsed_time(e1)
         nb, na, overflow = (int(v) for v in tree._host_counts)
         if overflow:
             raise _lib.CapacityError("device tree overflowed its arena during plan()")

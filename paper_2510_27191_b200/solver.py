@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .backup import run_backup
-from .belief import ParticleBelief, sir_update
+from .belief import DeviceBelief, ParticleBelief, sir_update
 from .envs._device import device_model
 from .rng import RowRng, fold, key_of
 from .search import Workspace, run_search
@@ -176,7 +176,15 @@ class Planner:
         return m
 
     def upload_belief(self, dm, belief):
-        """Copy the belief to HBM now (for callers that keep it resident)."""
+        """Copy the belief to HBM now (for callers that keep it resident).  A
+        DeviceBelief is copied device to device into the planner's persistent
+        buffers (stable pointers keep the captured CUDA graph valid)."""
+        if isinstance(belief, DeviceBelief):
+            m, nb = belief.m, belief.records.numel()
+            pd, cd = self._buf("particles_dev", nb, False), self._buf("cumw_dev", 8 * m, False)
+            pd[:nb].copy_(belief.records)
+            cd[: 8 * m].view(_torch().float64).copy_(belief.cumw_dev)
+            return pd, cd, m
         m = self.stage_belief(dm, belief)
         nb = m * dm.state_bytes
         pd, cd = self._bufs["particles_dev"], self._bufs["cumw_dev"]
@@ -193,6 +201,10 @@ class Planner:
             tree.reset(tree.init_prefs, config.eta)  # device reset for the iterative path
             fixed = False
         if fixed:
+            if isinstance(belief, DeviceBelief):
+                _, _, m = self.upload_belief(dm, belief)
+                return self.run_fixed(dm, tree, work, m, model.spec, config, key_of(rng), from_host=False,
+                                      keep_tree=keep_tree)
             m = self.stage_belief(dm, belief)
             return self.run_fixed(dm, tree, work, m, model.spec, config, key_of(rng), from_host=True,
                                   keep_tree=keep_tree)
@@ -341,15 +353,33 @@ class RunRecord:
     degenerate_updates: int
 
 
+def _identity_hooks(model) -> bool:
+    """The model keeps the base ProblemModel's reconcile_belief / refresh_executed
+    (core.py:119-136), so beliefs never need the host between steps."""
+    return all(getattr(type(model), name).__qualname__ == f"ProblemModel.{name}"
+               for name in ("reconcile_belief", "refresh_executed"))
+
+
 def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str = "fp32",
-                exact: bool = False) -> RunRecord:
-    """Plan / execute / filter loop (solver.py:130-194) around the device plan."""
+                exact: bool = False, device_belief: bool | None = None) -> RunRecord:
+    """Plan / execute / filter loop (solver.py:130-194) around the device plan.
+
+    ``device_belief`` (default: fast mode with identity belief hooks) keeps the
+    particles in HBM and runs the SIR update on the device (belief.py:47-102);
+    otherwise the update runs through the model's host step_batch, as the
+    reference does (the fp64 parity mode reproduces the reference's episodes)."""
     spec = model.spec
     root = RowRng.from_seed(seed)
     env_rng = root.derive(NS_ENV)
     env_state = model.sample_initial_states(1, env_rng.derive(0))
     belief = ParticleBelief.from_model(model, config.particles, root.derive(NS_INIT_BELIEF))
     belief = ParticleBelief(model.reconcile_belief(belief.states, env_state), belief.weights)
+    if device_belief is None:
+        device_belief = not exact and _identity_hooks(model)
+    if device_belief:
+        if not _identity_hooks(model):
+            raise ValueError("device-resident beliefs need the identity reconcile_belief / refresh_executed hooks")
+        belief = DeviceBelief.from_host(belief, model)
     total, counters, times, degenerate, t, reason = 0.0, {}, [], 0, 0, "truncated"
     while t < spec.max_steps:
         t0 = time.perf_counter()
@@ -369,5 +399,8 @@ def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str 
                          max_retries=config.max_sir_retries)
         degenerate += int(upd.degenerate)
         env_state = model.refresh_executed(env_state)
-        belief = ParticleBelief(model.reconcile_belief(upd.belief.states, env_state), upd.belief.weights)
+        if device_belief:
+            belief = upd.belief
+        else:
+            belief = ParticleBelief(model.reconcile_belief(upd.belief.states, env_state), upd.belief.weights)
     return RunRecord(run_index, seed, total, t, reason, times, counters, degenerate)

@@ -1,0 +1,44 @@
+"""Per-phase device time of the sharded planning step, run as virtual ranks on one GPU.
+
+    python scripts/shard_phases.py [--world 8] [--rows-per-gpu 16384] [--iterations 10] [--config c2]
+
+On G GPUs the trajectory phase runs concurrently (each GPU its own block of rows), so
+the projected per-GPU step time is trajectory / G + exchange + insert + backup, with
+the exchange an NCCL all-gather of (2 d + 1) x 8 B per row (measured here as the
+in-process concatenation only).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2510_27191_b200 as vp  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--world", type=int, default=8)
+ap.add_argument("--rows-per-gpu", type=int, default=16384)
+ap.add_argument("--iterations", type=int, default=10)
+ap.add_argument("--steps", type=int, default=3)
+a = ap.parse_args()
+model = vp.MarsModel(11, 11, layout_seed=1000)
+belief = vp.ParticleBelief.from_model(model, 10_000, vp.RowRng.from_seed(1000).derive(3))
+out = {}
+for world in sorted({1, a.world}):
+    cfg = vp.SolverConfig(n_parallel=a.rows_per_gpu * a.world, iterations=a.iterations)
+    p = vp.ShardedPlanner(world=world, precision="fp32")
+    p.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, 0))
+    p.phase_ms = {}
+    for t in range(a.steps):
+        p.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, t + 1))
+    torch.cuda.synchronize()
+    out[world] = {k: v / a.steps for k, v in p.phase_ms.items()}
+ph = out[a.world]
+proj = ph["trajectory"] / a.world + ph["insert"] + ph["backup"]
+res = {"rows_total": a.rows_per_gpu * a.world, "world": a.world, "ms_per_step_by_phase": out,
+       "projected_ms_per_step_per_gpu_excl_nccl": proj,
+       "bytes_all_gathered_per_step": sum((2 * min(i + 1, 90) + 1) * 8 * a.rows_per_gpu * a.world
+                                          for i in range(a.iterations))}
+print(json.dumps(res))
