@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--episodes", type=int, default=3, help="closed-loop episodes reported beside the step metric")
     ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
                     help="N > 1: one planning step sharded over the GPUs (n_parallel rows per GPU, "
                          "trajectories all-gathered over NCCL) or independent replicas")
@@ -320,6 +321,8 @@ def run_b200(args):
             "kernels": kernel_table, "dominant_kernel": top, "traffic_per_step": traffic,
             "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1),
             "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
+    if rank == 0 and world == 1 and args.episodes > 0:
+        line["closed_loop"] = closed_loop(args, vp, model)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
         line["speedup_vs_cpu_1core"] = round(line["e2e"]["value"] / line["cpu_baseline"]["value"], 1)
@@ -328,6 +331,26 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def closed_loop(args, vp, model) -> dict:
+    """Closed-loop episodes (solver.py:130-194) with the belief resident in HBM: plan ->
+    execute -> device SIR per step.  Reports the planning throughput inside the loop and
+    the episode returns (BASELINE configs[1]: RockSample(11,11) closed-loop episodes)."""
+    cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=args.n_parallel, iterations=args.iterations,
+                          particles=WORKLOAD["particles"])
+    vp.run_episode(model, cfg, seed=999, precision=args.precision)  # warm-up (graph capture)
+    t0 = time.perf_counter()
+    recs = [vp.run_episode(model, cfg, seed=s, precision=args.precision) for s in range(args.episodes)]
+    wall = time.perf_counter() - t0
+    steps = sum(r.steps for r in recs)
+    plan_s = sum(sum(r.plan_wall_times) for r in recs)
+    returns = [r.discounted_return for r in recs]
+    return {"episodes": len(recs), "env_steps": steps, "belief": "device-resident (DeviceBelief, device SIR)",
+            "plan_wall_ms_per_step": round(1e3 * plan_s / steps, 4),
+            "simulations_per_s_in_loop": round(steps * args.n_parallel * args.iterations / plan_s, 1),
+            "env_steps_per_s": round(steps / wall, 1), "mean_discounted_return": round(float(np.mean(returns)), 3),
+            "returns": [round(x, 3) for x in returns]}
 
 
 # ---------------------------------------------------------------- CPU (oracle port of the reference)
