@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 2
+#define VPB200_ABI_VERSION 3
 
 enum vp_status {
   VP_OK = 0,

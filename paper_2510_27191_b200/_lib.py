@@ -18,7 +18,7 @@ VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
     C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
