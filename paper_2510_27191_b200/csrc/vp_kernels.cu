@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
     init_row[a] = a < A ? (PsiT)T.init_prefs[a] : (PsiT)0;
     if (a < A) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
   }
+  fence_async_smem();  // the initial row is the source of TMA bulk stores (lazy rows)
   // the leaf counter of the NEXT pass is reset here: its previous user (the
   // backup of the pass before this one) has finished
   if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;

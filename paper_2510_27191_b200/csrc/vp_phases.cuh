@@ -353,22 +353,28 @@ __device__ __forceinline__ double group_sum(double v, u32 grp, bool active) {
 }
 
 // Write the initial PSI row (tree.py:253) into the rows named by the lanes
-// set in `mask` (lazy rows become real the first time they are interior).
+// set in `mask` (lazy rows become real the first time they are interior):
+// each such lane issues ONE TMA bulk store of the block's shared copy of the
+// initial row; the copy engine moves the bytes, the warp moves on.  Rows are
+// only read after this kernel (or as staged rows of non-lazy beliefs), and
+// bulk_store_drain() at the end of the warp's work completes the stores.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_drain() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <class PsiT>
 __device__ __forceinline__ void materialise_rows(const vp_tree& T, const PsiT* init_row, u32 mask, int b) {
-  const int A = T.action_count;
+  if (!((mask >> lane_id()) & 1u)) return;
   PsiT* psi = reinterpret_cast<PsiT*>(T.psi);
-  while (mask) {
-    const int j = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int bj = __shfl_sync(FULL, b, j);
-    PsiT* row = psi + (size_t)bj * T.psi_stride;
-    // rows and the shared initial row are 16-B aligned and padded: 16-B stores
-    typedef typename VecOf<PsiT>::T VT;
-    const int nv = (A + VecOf<PsiT>::N - 1) / VecOf<PsiT>::N;
-    for (int v = lane_id(); v < nv; v += 32)
-      reinterpret_cast<VT*>(row)[v] = reinterpret_cast<const VT*>(init_row)[v];
-  }
+  const u32 bytes = (u32)(((size_t)T.action_count * sizeof(PsiT) + 15) & ~(size_t)15);
+  bulk_s2g(psi + (size_t)b * T.psi_stride, init_row, bytes);
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 // Numbered-node allocation for the winners of a warp: one atomic per warp.
@@ -781,6 +787,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
   const double sum = group_sum(h, grp, ok);
   if (ok && lane == __ffs(grp) - 1) red_add(&T.b_value[b], sum);
+  bulk_store_drain();
   if (W.stats && threadIdx.x == 0 && blockIdx.x == 0) {
     atomicAdd(&W.stats[3], 1ull);
     atomicAdd(&W.stats[4], (unsigned long long)n * (unsigned long long)(d - depth0));
