@@ -119,6 +119,9 @@ typedef struct vp_tree {
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
+  void* cdf_cache;            /* [cap_beliefs * psi_stride] normalised softmax CDF of a row, built
+                                 once per pass by the first warp that samples it */
+  uint32_t* cdf_pass;         /* [cap_beliefs] pass whose PSI the cached CDF reflects (0 = none) */
   double eta;
 } vp_tree;
 

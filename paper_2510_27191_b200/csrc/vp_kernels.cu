@@ -42,6 +42,7 @@ __global__ void k_clear(vp_tree T) {
       T.b_rows[i] = 0;
       reinterpret_cast<Acc*>(T.b_acc)[i] = Acc{0.0, 0u, 0u};
       T.b_ckey[i] = ~0ull;
+      T.cdf_pass[i] = 0u;  // cached CDFs of the previous tree's rows
     }
     if (i < na) {
       T.a_reward[i] = 0.0;
@@ -628,7 +629,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, init_cdf),
                        (int32_t)offsetof(vp_tree, a_ckey),
                        (int32_t)offsetof(vp_search_args, m),
-                       (int32_t)offsetof(vp_model, mars_gpow)};
+                       (int32_t)offsetof(vp_model, mars_gpow),
+                       (int32_t)offsetof(vp_tree, cdf_pass)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];

@@ -245,7 +245,7 @@ struct VecOf<double> {
   typedef double2 T;
   static constexpr int N = 2;
 };
-template <class PsiT>
+template <class PsiT, bool Normalise = false>
 __device__ __forceinline__ PsiT row_cdf_inplace(PsiT* row, int A, PsiT e2, PsiT sh2) {
   typedef VecOf<PsiT> V;
   const int C = (A + 31) >> 5;
@@ -270,22 +270,25 @@ __device__ __forceinline__ PsiT row_cdf_inplace(PsiT* row, int A, PsiT e2, PsiT 
     }
   }
   const PsiT incl = warp_inclusive_scan(loc);
-  const PsiT excl = __shfl_up_sync(FULL, incl, 1);
-  if (lane_id() > 0) {
+  const PsiT up = __shfl_up_sync(FULL, incl, 1);  // all 32 lanes take part in the shuffle
+  const PsiT excl = lane_id() ? up : (PsiT)0;
+  const PsiT total = __shfl_sync(FULL, incl, 31);
+  if (Normalise || lane_id() > 0) {
+    const PsiT scale = Normalise ? (PsiT)1 / total : (PsiT)1;
     if (vec) {
       for (int c = lo; c < hi; c += V::N) {
         typename V::T v = *reinterpret_cast<typename V::T*>(row + c);
         PsiT* x = reinterpret_cast<PsiT*>(&v);
 #pragma unroll
-        for (int j = 0; j < V::N; ++j) x[j] += excl;
+        for (int j = 0; j < V::N; ++j) x[j] = Normalise ? (x[j] + excl) * scale : x[j] + excl;
         *reinterpret_cast<typename V::T*>(row + c) = v;
       }
     } else {
-      for (int c = lo; c < hi; ++c) row[c] += excl;
+      for (int c = lo; c < hi; ++c) row[c] = Normalise ? (row[c] + excl) * scale : row[c] + excl;
     }
   }
   __syncwarp();
-  return __shfl_sync(FULL, incl, 31);
+  return total;
 }
 
 // ------------------------------------------------------------------ TMA bulk staging
@@ -459,11 +462,21 @@ __device__ __forceinline__ State draw_state(const State* particles, const double
 // Softmax draw of one action per lane (search.py:46-83) from the PSI row of
 // belief b (or the initial row when flags bit 0 says it is lazily initial).
 // Called by all 32 lanes; lanes with ok == false return 0.
+// Stamp a CDF this lane bulk-stored into the cache (after the store completed).
+__device__ __forceinline__ void publish_pending_cdf(const vp_tree& T, int& pend, u32 pass) {
+  if (pend < 0) return;
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(T.cdf_pass + pend), "r"(pass) : "memory");
+  pend = -1;
+}
+
 template <class PsiT, bool Exact>
 __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, Stage<PsiT>& sg, const PsiT* init_cdf,
-                                           int b, u32 fl, bool ok, double u) {
+                                           int b, u32 fl, bool ok, double u, u32 pass, int& pend) {
   const int A = T.action_count, lane = lane_id();
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+  PsiT* cache = reinterpret_cast<PsiT*>(T.cdf_cache);
   const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
   const PsiT e2 = (PsiT)(T.eta * kLog2eD);
   int a = 0;
@@ -473,43 +486,71 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
       a = sample_exact(row, A, T.eta, u);
     }
   } else {
+    // CDFs this lane built at the previous level: the bulk stores have long
+    // completed; make them visible and stamp them with the pass
+    if (pend >= 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(T.cdf_pass + pend), "r"(pass) : "memory");
+      pend = -1;
+    }
     const bool fresh = ok && (fl & 1u);
     const bool need = ok && !fresh;
     if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
-    // distinct non-fresh beliefs of the warp: one TMA bulk copy of each PSI
-    // row into the warp's stage; the warp turns every staged row into its
-    // CDF (32 columns per step, shuffle scan) and each lane binary-searches
-    // its row with u scaled by the row total (p = e / sum e, search.py:51-54)
+    // Distinct non-fresh beliefs of the warp: one TMA bulk copy of each row into the
+    // warp's stage -- the row's normalised CDF if some warp already built it this pass
+    // (the PSI row is read-only during a pass), else its PSI row, which the warp turns
+    // into the CDF in place (lane j owns a contiguous ceil(|A|/32)-column chunk, one
+    // shuffle scan, p = e / sum e, search.py:51-54) and publishes for the other warps.
+    // Every lane then binary-searches its row.
     const u32 g = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
     const int my_leader = __ffs(g) - 1;
-    const u32 leaders = __ballot_sync(FULL, need && lane == my_leader);
+    const bool lead = need && lane == my_leader;
+    const u32 leaders = __ballot_sync(FULL, lead);
     const int K = __popc(leaders);
     if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
     const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-    const PsiT sh2 = need ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
+    bool cached = false;
+    if (lead) {
+      u32 stamp;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(stamp) : "l"(T.cdf_pass + b) : "memory");
+      cached = stamp == pass;
+    }
+    const u32 cmask = __ballot_sync(FULL, cached);
+    if (cmask) asm volatile("fence.proxy.async.global;" ::: "memory");
+    const PsiT sh2 = lead && !cached ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
     for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
       const int cnt = min(sg.cfg.rows, K - s0);
       fence_async_smem();
       if (lane == 0) mbar_expect_tx(sg.bar, row_bytes * (u32)cnt);
       __syncwarp();
       const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
+      PsiT* srow = sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride;
       if (mine && lane == my_leader)
-        bulk_g2s(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, psi + (size_t)b * T.psi_stride, row_bytes,
-                 sg.bar);
+        bulk_g2s(srow, (cached ? cache : psi) + (size_t)b * T.psi_stride, row_bytes, sg.bar);
       mbar_wait(sg.bar, sg.phase);
       sg.phase ^= 1u;
-      PsiT my_total = 0;
       u32 rem = leaders;
       for (int k = 0; k < s0; ++k) rem &= rem - 1u;
+      bool built = false;
       for (int k = 0; k < cnt; ++k) {
         const int src = __ffs(rem) - 1;
         rem &= rem - 1u;
-        const PsiT tot = row_cdf_inplace(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
-        if (lane == k) my_total = tot;
+        if (!((cmask >> src) & 1u)) {
+          row_cdf_inplace<PsiT, true>(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
+          built |= lane == src;
+        }
+      }
+      if (built) {  // publish the normalised CDF: one bulk store from the stage
+        fence_async_smem();
+        bulk_s2g(cache + (size_t)b * T.psi_stride, srow, row_bytes);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        pend = b;
       }
       __syncwarp();
-      const PsiT total = __shfl_sync(FULL, my_total, mine ? my_slot - s0 : 0);
-      if (mine) a = search_cdf(sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride, A, (PsiT)(u * (double)total));
+      if (mine) a = search_cdf(srow, A, (PsiT)u);
+      // the stage is refilled next: the bulk stores must have read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
     }
   }
@@ -561,13 +602,13 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
   const bool active = r < n;
   const Slot* ha = slots(T.hash_a);
   const Slot* hb = slots(T.hash_b);
-  int b = 0;
+  int b = 0, pend = -1;
   bool known = active;  // the row's belief existed when the pass started
   u32 fl = known ? T.b_flags[0] : 1u;
   for (int l = 0; l < S.d_max; ++l) {
     const u64 lkey = fold(skey, (u64)l);
     const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
-    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u);
+    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u, S.pass, pend);
     u32 o = 0;
     double rw = 0.0;
     if (active) {
@@ -588,6 +629,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     }
   }
   if (active) W.leaf_value[r] = Model::heuristic(M, st);
+  publish_pending_cdf(T, pend, S.pass);
 }
 
 // The search kernel body for one warp = 32 consecutive rows.
@@ -649,6 +691,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   }
 
   bool made_interior = false;  // this lane created b at the previous level and it is interior now
+  int pend = -1;               // belief whose CDF this lane published, stamp pending
   for (int l = depth0; l < d; ++l) {
     const u64 lkey = fold(skey, (u64)l);  // search.py:107
     // ---- lazy rows: b is interior at this level; write its PSI row once
@@ -661,7 +704,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
     int a = 0;
     if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
-    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u);
+    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u, pass, pend);
     // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
     double rw = 0.0;
@@ -788,6 +831,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   const double sum = group_sum(h, grp, ok);
   if (ok && lane == __ffs(grp) - 1) red_add(&T.b_value[b], sum);
   bulk_store_drain();
+  publish_pending_cdf(T, pend, pass);
   if (W.stats && threadIdx.x == 0 && blockIdx.x == 0) {
     atomicAdd(&W.stats[3], 1ull);
     atomicAdd(&W.stats[4], (unsigned long long)n * (unsigned long long)(d - depth0));
