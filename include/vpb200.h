@@ -119,9 +119,13 @@ typedef struct vp_tree {
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
-  void* cdf_cache;            /* [cap_beliefs * psi_stride] normalised softmax CDF of a row, built
-                                 once per pass by the first warp that samples it */
-  uint32_t* cdf_pass;         /* [cap_beliefs] pass whose PSI the cached CDF reflects (0 = none) */
+  void* cdf_cache;            /* [cdf_slots * psi_stride] normalised softmax CDFs of non-lazy rows,
+                                 direct-mapped by belief id, built once per pass by the first
+                                 warp that samples the row */
+  uint64_t* cdf_tag;          /* [cdf_slots] pass << 32 | belief of the slot's CDF (bit 31 of the
+                                 low word: being written); cleared at tree reset */
+  int32_t cdf_slots;          /* power of two                                */
+  int32_t pad_cdf;
   double eta;
 } vp_tree;
 

@@ -56,7 +56,8 @@ class VpTree(C.Structure):
         ("a_visits", C.c_void_p), ("a_rows", C.c_void_p), ("a_acc", C.c_void_p), ("a_ckey", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p),
-        ("cdf_cache", C.c_void_p), ("cdf_pass", C.c_void_p), ("eta", C.c_double),
+        ("cdf_cache", C.c_void_p), ("cdf_tag", C.c_void_p), ("cdf_slots", C.c_int32), ("pad_cdf", C.c_int32),
+        ("eta", C.c_double),
     ]
 
 
@@ -194,11 +195,11 @@ def layout_mismatches() -> list:
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
-            VpModel.mars_gpow.offset, VpTree.cdf_pass.offset]
+            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_pass"]
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

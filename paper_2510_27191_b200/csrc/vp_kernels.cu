@@ -35,15 +35,15 @@ __global__ void k_tree_init(vp_tree T) {
 // in that state since allocation).  Part 2 (k_tree_init) rewrites the root.
 __global__ void k_clear(vp_tree T) {
   const int nb = min(T.counters[0], T.cap_beliefs), na = min(T.counters[1], T.cap_actions);
-  const int total = max(nb, na);
+  const int total = max(max(nb, na), T.cdf_slots);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i < nb) {
       T.b_value[i] = 0.0;
       T.b_rows[i] = 0;
       reinterpret_cast<Acc*>(T.b_acc)[i] = Acc{0.0, 0u, 0u};
       T.b_ckey[i] = ~0ull;
-      T.cdf_pass[i] = 0u;  // cached CDFs of the previous tree's rows
     }
+    if (i < T.cdf_slots) T.cdf_tag[i] = 0;  // cached CDFs of the previous tree
     if (i < na) {
       T.a_reward[i] = 0.0;
       T.a_visits[i] = 0;
@@ -630,7 +630,7 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, a_ckey),
                        (int32_t)offsetof(vp_search_args, m),
                        (int32_t)offsetof(vp_model, mars_gpow),
-                       (int32_t)offsetof(vp_tree, cdf_pass)};
+                       (int32_t)offsetof(vp_tree, cdf_tag)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];

@@ -462,18 +462,23 @@ __device__ __forceinline__ State draw_state(const State* particles, const double
 // Softmax draw of one action per lane (search.py:46-83) from the PSI row of
 // belief b (or the initial row when flags bit 0 says it is lazily initial).
 // Called by all 32 lanes; lanes with ok == false return 0.
-// Stamp a CDF this lane bulk-stored into the cache (after the store completed).
-__device__ __forceinline__ void publish_pending_cdf(const vp_tree& T, int& pend, u32 pass) {
+// CDF cache tags: pass << 32 | belief; kCdfBuilding marks a slot being written.
+constexpr u64 kCdfBuilding = 0x80000000ull;
+__device__ __forceinline__ u64 cdf_tag(u32 pass, int b) { return ((u64)pass << 32) | (u32)b; }
+
+// Publish the CDF this lane bulk-stored into cache slot `pend` for belief
+// `pend_b`: once the store has completed, release the slot's tag.
+__device__ __forceinline__ void publish_pending_cdf(const vp_tree& T, int& pend, int pend_b, u32 pass) {
   if (pend < 0) return;
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(T.cdf_pass + pend), "r"(pass) : "memory");
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(T.cdf_tag + pend), "l"(cdf_tag(pass, pend_b)) : "memory");
   pend = -1;
 }
 
 template <class PsiT, bool Exact>
 __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, Stage<PsiT>& sg, const PsiT* init_cdf,
-                                           int b, u32 fl, bool ok, double u, u32 pass, int& pend) {
+                                           int b, u32 fl, bool ok, double u, u32 pass, int& pend, int& pend_b) {
   const int A = T.action_count, lane = lane_id();
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   PsiT* cache = reinterpret_cast<PsiT*>(T.cdf_cache);
@@ -488,12 +493,7 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
   } else {
     // CDFs this lane built at the previous level: the bulk stores have long
     // completed; make them visible and stamp them with the pass
-    if (pend >= 0) {
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(T.cdf_pass + pend), "r"(pass) : "memory");
-      pend = -1;
-    }
+    publish_pending_cdf(T, pend, pend_b, pass);
     const bool fresh = ok && (fl & 1u);
     const bool need = ok && !fresh;
     if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
@@ -510,11 +510,18 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
     const int K = __popc(leaders);
     if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
     const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-    bool cached = false;
+    // direct-mapped cache slot of b: a hit when it holds b's CDF of this pass; otherwise the
+    // builder claims the slot (one writer per slot and pass) unless it holds this pass's CDF
+    // of another row
+    bool cached = false, claim = false;
+    const int cslot = b & (T.cdf_slots - 1);
     if (lead) {
-      u32 stamp;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(stamp) : "l"(T.cdf_pass + b) : "memory");
-      cached = stamp == pass;
+      u64 tag;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(tag) : "l"(T.cdf_tag + cslot) : "memory");
+      cached = tag == cdf_tag(pass, b);
+      if (!cached && (u32)(tag >> 32) != pass)
+        claim = atomicCAS(reinterpret_cast<unsigned long long*>(T.cdf_tag + cslot), tag,
+                          cdf_tag(pass, b) | kCdfBuilding) == tag;
     }
     const u32 cmask = __ballot_sync(FULL, cached);
     if (cmask) asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -527,25 +534,24 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
       const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
       PsiT* srow = sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride;
       if (mine && lane == my_leader)
-        bulk_g2s(srow, (cached ? cache : psi) + (size_t)b * T.psi_stride, row_bytes, sg.bar);
+        bulk_g2s(srow, cached ? cache + (size_t)cslot * T.psi_stride : psi + (size_t)b * T.psi_stride, row_bytes,
+                 sg.bar);
       mbar_wait(sg.bar, sg.phase);
       sg.phase ^= 1u;
       u32 rem = leaders;
       for (int k = 0; k < s0; ++k) rem &= rem - 1u;
-      bool built = false;
       for (int k = 0; k < cnt; ++k) {
         const int src = __ffs(rem) - 1;
         rem &= rem - 1u;
-        if (!((cmask >> src) & 1u)) {
+        if (!((cmask >> src) & 1u))
           row_cdf_inplace<PsiT, true>(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
-          built |= lane == src;
-        }
       }
-      if (built) {  // publish the normalised CDF: one bulk store from the stage
+      if (claim && mine) {  // publish the normalised CDF: one bulk store from the stage
         fence_async_smem();
-        bulk_s2g(cache + (size_t)b * T.psi_stride, srow, row_bytes);
+        bulk_s2g(cache + (size_t)cslot * T.psi_stride, srow, row_bytes);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        pend = b;
+        pend = cslot;
+        pend_b = b;
       }
       __syncwarp();
       if (mine) a = search_cdf(srow, A, (PsiT)u);
@@ -602,13 +608,13 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
   const bool active = r < n;
   const Slot* ha = slots(T.hash_a);
   const Slot* hb = slots(T.hash_b);
-  int b = 0, pend = -1;
+  int b = 0, pend = -1, pend_b = 0;
   bool known = active;  // the row's belief existed when the pass started
   u32 fl = known ? T.b_flags[0] : 1u;
   for (int l = 0; l < S.d_max; ++l) {
     const u64 lkey = fold(skey, (u64)l);
     const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
-    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u, S.pass, pend);
+    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u, S.pass, pend, pend_b);
     u32 o = 0;
     double rw = 0.0;
     if (active) {
@@ -629,7 +635,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     }
   }
   if (active) W.leaf_value[r] = Model::heuristic(M, st);
-  publish_pending_cdf(T, pend, S.pass);
+  publish_pending_cdf(T, pend, pend_b, S.pass);
 }
 
 // The search kernel body for one warp = 32 consecutive rows.
@@ -691,7 +697,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   }
 
   bool made_interior = false;  // this lane created b at the previous level and it is interior now
-  int pend = -1;               // belief whose CDF this lane published, stamp pending
+  int pend = -1, pend_b = 0;   // CDF cache slot (and belief) this lane wrote, tag pending
   for (int l = depth0; l < d; ++l) {
     const u64 lkey = fold(skey, (u64)l);  // search.py:107
     // ---- lazy rows: b is interior at this level; write its PSI row once
@@ -704,7 +710,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
     int a = 0;
     if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
-    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u, pass, pend);
+    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u, pass, pend, pend_b);
     // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
     double rw = 0.0;
@@ -831,7 +837,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   const double sum = group_sum(h, grp, ok);
   if (ok && lane == __ffs(grp) - 1) red_add(&T.b_value[b], sum);
   bulk_store_drain();
-  publish_pending_cdf(T, pend, pass);
+  publish_pending_cdf(T, pend, pend_b, pass);
   if (W.stats && threadIdx.x == 0 && blockIdx.x == 0) {
     atomicAdd(&W.stats[3], 1ull);
     atomicAdd(&W.stats[4], (unsigned long long)n * (unsigned long long)(d - depth0));

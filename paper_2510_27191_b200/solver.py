@@ -120,11 +120,16 @@ class Planner:
             total = sum(min(i + 1, cap_levels) for i in range(16))
             levels = cap_levels
         need = 1 + n * total
+        return min(need, max(self.node_budget(A), 1 + n * levels)), levels
+
+    def node_budget(self, A: int, fraction: float | None = None) -> int:
+        """Nodes (belief + action pairs) that fit in mem_fraction of the free HBM: a PSI row and
+        the B columns per belief, the A columns per action, and a 2x-oversized 16-B hash slot each."""
+        torch = _torch()
         elem = 4 if self.precision == "fp32" else 8
-        per_belief = A * elem + 8 * 3 + 4 * 4 + 64  # PSI row + columns + hash slots
+        per_pair = (A + 4) * elem + 60 + 48 + 2 * 2 * 16
         free, _ = torch.cuda.mem_get_info()
-        budget = int(free * self.mem_fraction) // (per_belief + 48 + 64)
-        return min(need, max(budget, 1 + n * levels)), levels
+        return int(free * (self.mem_fraction if fraction is None else fraction)) // per_pair
 
     def prepare(self, model, config, trace: bool = False, device_init: bool = True):
         dm = device_model(model)
@@ -272,6 +277,7 @@ class Planner:
         stream = torch.cuda.current_stream().cuda_stream
         ub_b, ub_a = 1, 0
         d_max, done, last = 1, 0, 0
+        stopped = None
         traces = [] if trace else None
         t0 = time.perf_counter()
         while True:
@@ -279,7 +285,18 @@ class Planner:
             if ub_b + n * d_max > tree.cap_beliefs or ub_a + n * d_max > tree.cap_actions:
                 nb, na, _ = tree.counts()
                 ub_b, ub_a = nb, na
-                tree.ensure_capacity(nb + n * d_max, na + n * d_max)
+                need_b, need_a = nb + n * d_max, na + n * d_max
+                if done and (need_b > tree.cap_beliefs or need_a > tree.cap_actions):
+                    # growth allocates the doubled arena beside the old one: stop deepening when
+                    # it would not fit in HBM (a memory-bounded budget; the reference would
+                    # exhaust host memory the same way, only later)
+                    grown = max(tree.cap_beliefs, tree.cap_actions, 16)
+                    while grown < max(need_b, need_a):
+                        grown *= 2
+                    if grown > self.node_budget(tree.action_count, fraction=0.85):
+                        stopped = "memory"
+                        break
+                tree.ensure_capacity(need_b, need_a)
             inject = None
             if inject_actions is not None:
                 arr = np.asarray(inject_actions[done], dtype=np.int32).reshape(d_max, n)
@@ -313,7 +330,10 @@ class Planner:
         held = tree if keep_tree else TreeHandle(tree)
         if keep_tree:
             self.tree = None  # hand the storage to the caller
-        return PlanOutcome(chosen, done, last, {"belief_rows": nb, "action_rows": na}, held, traces)
+        stats = {"belief_rows": nb, "action_rows": na}
+        if stopped:
+            stats["stopped"] = stopped
+        return PlanOutcome(chosen, done, last, stats, held, traces)
 
 
 _PLANNERS: dict = {}

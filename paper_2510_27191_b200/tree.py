@@ -55,6 +55,8 @@ def _stream():
 class DeviceTree:
     """B / A / PSI tables of one planning step on the current CUDA device."""
 
+    CDF_SLOTS = 1 << 16  # direct-mapped CDF cache rows (csrc draw_action)
+
     def __init__(self, action_count: int, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32",
                  exact: bool = False, cap_beliefs: int = 4096, cap_actions: int = 4096):
         if action_count < 1:
@@ -113,8 +115,10 @@ class DeviceTree:
         self.b_acc = col(g("b_acc"), (cap_b, 2), torch.int64, keep_b, 0)
         self.b_flags = col(g("b_flags"), cap_b, torch.int32, keep_b)
         self.b_ckey = col(g("b_ckey"), cap_b, torch.int64, keep_b, -1)
-        self.cdf_cache = col(g("cdf_cache"), (cap_b, self.psi_stride), self._psi_dtype, 0)
-        self.cdf_pass = col(g("cdf_pass"), cap_b, torch.int32, 0, 0)  # 0: no cached CDF
+        slots = min(_pow2_at_least(cap_b), self.CDF_SLOTS)
+        if getattr(self, "cdf_tag", None) is None or self.cdf_tag.numel() != slots:
+            self.cdf_cache = torch.empty((slots, self.psi_stride), dtype=self._psi_dtype, device=dev)
+            self.cdf_tag = torch.zeros(slots, dtype=torch.int64, device=dev)  # pass 0: empty
         self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
         self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
         self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a, 0)
@@ -135,8 +139,9 @@ class DeviceTree:
         s.psi_stride = self.psi_stride
         for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
                      "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_rows", "a_acc",
-                     "a_ckey", "hash_a", "hash_b", "cdf_cache", "cdf_pass"):
+                     "a_ckey", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
             setattr(s, name, getattr(self, name).data_ptr())
+        s.cdf_slots = self.cdf_tag.numel()
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
         s.init_lse = self._init_lse.data_ptr()

@@ -1,0 +1,54 @@
+"""Campaign harness host logic (bench.py:93-146 mirror): summary statistics and the
+JSON-lines layout, on synthetic run records (no GPU)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from paper_2510_27191_b200.campaign import CampaignConfig, build_model, config_from_args, build_parser, \
+    format_summary, summarize
+
+
+def _records(returns):
+    return [{"type": "run", "run_index": i, "seed": i, "discounted_return": r, "steps": 10 + i,
+             "terminal_reason": "terminal" if i % 2 else "truncated", "plan_wall_times": [0.01, 0.03],
+             "counters": {"rock_samples": float(i)}, "degenerate_updates": 0} for i, r in enumerate(returns)]
+
+
+def test_summary_matches_reference_formulas():
+    rets = [10.0, 12.5, 7.25, 30.0, -3.0]
+    s = summarize(_records(rets))
+    arr = np.asarray(rets)
+    assert s["n"] == 5 and s["terminal_runs"] == 2
+    m = s["metrics"]["discounted_return"]
+    assert m["mean"] == pytest.approx(arr.mean())
+    assert m["std"] == pytest.approx(arr.std(ddof=1))
+    assert m["ci95"] == pytest.approx(1.96 * arr.std(ddof=1) / np.sqrt(5))
+    assert s["metrics"]["plan_seconds"]["mean"] == pytest.approx(0.02)
+    assert "rock_samples" in s["metrics"]
+    assert "terminal runs: 2/5" in format_summary(s)
+    with pytest.raises(ValueError):
+        summarize([])
+
+
+def test_single_run_has_zero_ci():
+    s = summarize(_records([4.0]))
+    assert s["metrics"]["discounted_return"] == {"mean": 4.0, "std": 0.0, "ci95": 0.0}
+
+
+def test_config_header_and_cli_defaults():
+    args = build_parser().parse_args(["--problem", "mars", "--runs", "3", "--planning-time", "0.05"])
+    cfg = config_from_args(args)
+    assert cfg.solver.n_parallel == 60_000 and cfg.solver.planning_seconds == 0.05  # bench.py:26-31 defaults
+    head = cfg.to_dict()
+    assert head["type"] == "config" and head["problem_params"] == {"n": 20, "m": 20}
+    json.dumps(head)
+    with pytest.raises(ValueError):
+        CampaignConfig(problem="mars", runs=0)
+    # MARS draws a fresh layout per run unless pinned (bench.py:64-72)
+    from paper_2510_27191_b200 import MarsModel
+
+    assert np.array_equal(build_model("mars", {"n": 6, "m": 4}, 7).rock_at, MarsModel(6, 4, layout_seed=7).rock_at)
+    assert np.array_equal(build_model("mars", {"n": 6, "m": 4, "layout_seed": 1}, 7).rock_at,
+                          MarsModel(6, 4, layout_seed=1).rock_at)

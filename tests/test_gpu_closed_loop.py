@@ -8,6 +8,8 @@
   the 99 % level, and the means' 95 % CIs overlap).
 """
 
+import json
+
 import numpy as np
 import pytest
 
@@ -54,3 +56,17 @@ def test_time_budget_mode_runs_at_least_one_iteration():
     assert out.iterations_run >= 2
     assert out.final_d_max == min(out.iterations_run, 6)
     assert 0 <= out.chosen_action < model.spec.action_count
+
+
+def test_campaign_jsonl_on_device(tmp_path):
+    """paper_2510_27191_b200.campaign: config header, one record per run, summary (bench.py:128-146)."""
+    from paper_2510_27191_b200.campaign import CampaignConfig, run_campaign
+
+    out = tmp_path / "c.jsonl"
+    cfg = CampaignConfig(problem="tiger", solver=vp.SolverConfig(n_parallel=1024, iterations=4, particles=500),
+                         runs=3, out_path=str(out))
+    records, summary = run_campaign(cfg)
+    lines = [json.loads(x) for x in out.read_text().splitlines()]
+    assert [x["type"] for x in lines] == ["config", "run", "run", "run", "summary"]
+    assert [r["run_index"] for r in records] == [0, 1, 2]
+    assert summary["n"] == 3 and "discounted_return" in summary["metrics"]
