@@ -96,6 +96,8 @@ typedef struct vp_tree {
   /* belief table B + PSI */
   int32_t* b_parent_action;   /* -1 for the root                            */
   uint32_t* b_parent_obs;     /* 0xFFFFFFFF for the root                    */
+  int32_t* b_parent_belief;   /* = a_parent_belief[b_parent_action] (backup climbs without chasing) */
+  int32_t* b_parent_act;      /* = a_action[b_parent_action]                  */
   int32_t* b_depth;
   void* psi;                  /* [cap_beliefs * psi_stride] float or double */
   double* b_lse;              /* cached (1/eta) log sum exp(eta PSI[b])      */

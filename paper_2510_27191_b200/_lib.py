@@ -49,7 +49,8 @@ class VpTree(C.Structure):
         ("cap_beliefs", C.c_int32), ("cap_actions", C.c_int32), ("action_count", C.c_int32),
         ("psi_dtype", C.c_int32), ("exact", C.c_int32), ("psi_stride", C.c_int32),
         ("hmask_a", C.c_uint64), ("hmask_b", C.c_uint64),
-        ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_depth", C.c_void_p),
+        ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_parent_belief", C.c_void_p),
+        ("b_parent_act", C.c_void_p), ("b_depth", C.c_void_p),
         ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p),
         ("b_rows", C.c_void_p), ("b_acc", C.c_void_p), ("b_flags", C.c_void_p), ("b_ckey", C.c_void_p),
         ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),

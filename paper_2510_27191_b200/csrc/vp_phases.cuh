@@ -419,6 +419,8 @@ __device__ void block_tree_init(const vp_tree& T) {
       T.b_lse[0] = v;
       T.b_parent_action[0] = -1;
       T.b_parent_obs[0] = 0xffffffffu;
+      T.b_parent_belief[0] = -1;
+      T.b_parent_act[0] = -1;
       T.b_depth[0] = 0;
       T.b_value[0] = 0.0;
       T.b_rows[0] = 0;
@@ -788,6 +790,8 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         if (c < T.cap_beliefs) {
           T.b_parent_action[c] = x;
           T.b_parent_obs[c] = o;
+          T.b_parent_belief[c] = b;
+          T.b_parent_act[c] = a;
           T.b_depth[c] = l + 1;
           T.b_lse[c] = T.init_lse[0];
           // fresh (PSI == init); an interior node's row is written by its creator next level
@@ -897,31 +901,43 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
     T.b_rows[c] = 0;
   }
   bool live = c >= 0;
+  // the climb's pointers: parent action x, parent belief pb and the action label of c
+  int x = -1, pb = -1, act = 0;
+  if (live) {
+    x = T.b_parent_action[c];
+    pb = T.b_parent_belief[c];
+    act = T.b_parent_act[c];
+  }
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0;
   while (__any_sync(FULL, live)) {
-    int ready = -1;
+    int ready = -1, nx = -1, npb = -1, nact = 0;
     double lse_pre = 0.0, bsum = 0.0;
     u32 bcnt = 0, btot = 0;
     bool fresh = false;
     if (live) {
       live = false;
-      const int x = T.b_parent_action[c];
       if (x >= 0) {
-        // the completing delivery needs these; load them before the CAS round trip
-        const int tot = T.a_rows[x], vis = T.a_visits[x], pb = T.a_parent_belief[x], act = T.a_action[x];
+        // ONE round trip for everything a completing delivery needs -- the action's
+        // statistics, the parent belief's LSE / rows / flags, the PSI cell -- and the next
+        // level's pointers.  All of it is stable until this lane completes the nodes.
+        const int tot = T.a_rows[x], vis = T.a_visits[x];
         const double rew = T.a_reward[x];
+        lse_pre = T.b_lse[pb];
+        btot = (u32)T.b_rows[pb];
+        const u32 pflags = T.b_flags[pb];
+        PsiT* cell = psi + (size_t)pb * T.psi_stride + act;
+        const double old_v = (double)__ldcg(cell);
+        nx = T.b_parent_action[pb];
+        npb = T.b_parent_belief[pb];
+        nact = T.b_parent_act[pb];
         // child mean of the action (backup.py:64-68): sum V*N, sum N
         Acc aa;
         if (acc_deliver(T.a_acc, x, V * (double)N, (u32)rows, N, (u32)tot, aa)) {
           // last child: Q (backup.py:96-104) and PSI[b, a] += Q - LSE_pre(b) (:106-108)
           ++n_act;
           T.a_rows[x] = 0;
-          lse_pre = T.b_lse[pb];
-          btot = (u32)T.b_rows[pb];
-          fresh = !Exact && (T.b_flags[pb] & 1u);
+          fresh = !Exact && (pflags & 1u);
           const double q = rew / (double)vis + (gamma * aa.sum) / (double)aa.cnt;
-          PsiT* cell = psi + (size_t)pb * T.psi_stride + act;
-          const double old_v = (double)__ldcg(cell);
           const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
           *cell = new_v;
           // a lazily-initial row (LSE_pre is its exact LSE): LSE_post follows from the
@@ -968,6 +984,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         N = bcnt;
         rows = (int)btot;
         c = ready;
+        x = nx;
+        pb = npb;
+        act = nact;
         live = true;
       }
     }

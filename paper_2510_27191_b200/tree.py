@@ -107,6 +107,8 @@ class DeviceTree:
         g = lambda name: getattr(self, name, None)  # noqa: E731
         self.b_parent_action = col(g("b_parent_action"), cap_b, torch.int32, keep_b)
         self.b_parent_obs = col(g("b_parent_obs"), cap_b, torch.int32, keep_b)
+        self.b_parent_belief = col(g("b_parent_belief"), cap_b, torch.int32, keep_b)
+        self.b_parent_act = col(g("b_parent_act"), cap_b, torch.int32, keep_b)
         self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
         self.psi = col(g("psi"), (cap_b, self.psi_stride), self._psi_dtype, keep_b)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
@@ -137,7 +139,7 @@ class DeviceTree:
         s.exact = int(self.exact)
         s.hmask_a, s.hmask_b = ha - 1, hb - 1
         s.psi_stride = self.psi_stride
-        for name in ("b_parent_action", "b_parent_obs", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
+        for name in ("b_parent_action", "b_parent_obs", "b_parent_belief", "b_parent_act", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
                      "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_rows", "a_acc",
                      "a_ckey", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
             setattr(s, name, getattr(self, name).data_ptr())

@@ -31,6 +31,8 @@ ap.add_argument("--n", type=int, default=11)
 ap.add_argument("--m", type=int, default=11)
 ap.add_argument("--n-parallel", type=int, default=16_384)
 ap.add_argument("--out", default=None)
+ap.add_argument("--cpu-runs", type=int, default=0,
+                help="also run the CPU reference algorithm (oracle/ port) at its smallest budget")
 a = ap.parse_args()
 rows = []
 for b in [float(x) for x in a.budgets.split(",")]:
@@ -54,6 +56,26 @@ res = {"problem": f"MARS({a.n},{a.m})", "n_parallel": a.n_parallel, "eta": 2.0, 
        "time_to_near_optimal_s": near["planning_seconds"],
        "definition": "smallest planning_seconds whose mean return lies within the 95% CI of the best mean (SURVEY 8d)",
        "runs_per_budget": a.runs}
+if a.cpu_runs:
+    # the reference always completes its first iteration (solver.py:106-110), so on the CPU the
+    # smallest achievable planning step is one iteration of n_parallel rows
+    import oracle  # CPU baseline only
+
+    t0 = time.perf_counter()
+    recs = []
+    for i in range(a.cpu_runs):
+        model = oracle.MarsModel(n=a.n, m=a.m, layout_seed=i)
+        recs.append(oracle.run_episode(model, oracle.SolverConfig(n_parallel=a.n_parallel, planning_seconds=1e-6),
+                                       seed=i))
+    rets = [r.discounted_return for r in recs]
+    import numpy as np
+
+    res["cpu_reference_min_budget"] = {
+        "runs": a.cpu_runs, "mean_return": round(float(np.mean(rets)), 3),
+        "ci95": round(float(1.96 * np.std(rets, ddof=1) / np.sqrt(len(rets))), 3) if len(rets) > 1 else 0.0,
+        "mean_plan_seconds": round(float(np.mean([np.mean(r.plan_wall_times) for r in recs])), 4),
+        "cores": 1, "kind": "port (oracle/, numpy restatement of vecpomdp.plan)",
+        "wall_s": round(time.perf_counter() - t0, 1)}
 print(json.dumps(res))
 if a.out:
     json.dump(res, open(a.out, "w"), indent=1)
