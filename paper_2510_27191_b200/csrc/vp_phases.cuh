@@ -50,11 +50,18 @@ struct __align__(16) Acc {
 };
 
 // Deliver (dsum, drows, dcnt) to a node whose deliveries total `target` rows.
-// A delivery carrying all of them is the node's only one: it completes the
-// node with no atomic (the usual case below the top levels).  Otherwise the
-// sums go out as L2 reductions (contention-friendly) and an acq_rel add on
-// the row count elects the completing delivery, which then reads the totals.
 // Returns true on the completing delivery, with the totals in `out`.
+//  * A delivery carrying all of the node's rows is its only one: no atomic.
+//  * A node with few rows (target <= kCasRows) sees few, rarely concurrent
+//    deliveries: ONE optimistic 128-bit CAS on {sum, rows, cnt} (guess: still
+//    zero), retried from the returned value; the completing CAS returns the
+//    totals -- no fence, no reload.
+//  * Busy nodes (the top of the tree) take many concurrent deliveries: L2
+//    reductions of the sums, then an acq_rel add on the row count elects the
+//    completing delivery, which reads the totals.
+// The path depends only on `target`, so all deliveries to a node agree on it.
+constexpr u32 kCasRows = 16;
+
 __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 drows, u32 dcnt, u32 target,
                                             Acc& out) {
   if (drows == target) {
@@ -62,6 +69,24 @@ __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 
     return true;
   }
   Acc* p = reinterpret_cast<Acc*>(base) + i;
+  if (target <= kCasRows) {
+    u64 lo = 0, hi = 0;
+    while (true) {
+      const double s = __longlong_as_double((long long)lo) + dsum;
+      const u32 r = (u32)hi + drows, c = (u32)(hi >> 32) + dcnt;
+      const u64 nlo = (u64)__double_as_longlong(s), nhi = (u64)r | ((u64)c << 32);
+      u64 olo, ohi;
+      cas128(p, lo, hi, nlo, nhi, olo, ohi);
+      if (olo == lo && ohi == hi) {
+        if (r != target) return false;
+        out = Acc{s, r, c};
+        *p = Acc{0.0, 0u, 0u};
+        return true;
+      }
+      lo = olo;
+      hi = ohi;
+    }
+  }
   red_add(&p->sum, dsum);
   red_add(reinterpret_cast<int*>(&p->cnt), (int)dcnt);
   if ((u32)atom_add_acq_rel(reinterpret_cast<int*>(&p->rows), (int)drows) + drows != target) return false;
