@@ -286,6 +286,11 @@ def run_b200(args):
     passes = prof_steps * args.iterations
     b_search, b_backup = algorithmic_bytes(st, args.n_parallel, S, A, psi_b, passes)
 
+    # measured DRAM bytes per launch of the same workload (ncu launch list, scripts/ncu_capture.sh +
+    # scripts/launch_traffic.py), committed under profiles/
+    tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
+    measured = json.load(open(tpath))["kernels"] if os.path.exists(tpath) and world == 1 else {}
+
     def roof(kind, kname, total_bytes, formula):
         ms, cnt = kinds.get(kind, (0.0, 0))
         if not cnt:
@@ -293,8 +298,12 @@ def run_b200(args):
         per_launch = total_bytes / cnt
         avg_ms = ms / cnt
         ach = per_launch / (avg_ms / 1e3) / 1e9
+        traffic = measured.get(kname, {}).get("dram_bytes_per_launch")
         return {"kernel": kname, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "bytes_per_launch": round(per_launch),
+                "frac": round(ach / peak, 4), "traffic": round(traffic) if traffic else None,
+                "traffic_source": f"profiles/traffic_{args.config}.json (ncu dram__bytes_read+write, "
+                                  f"avg per launch)" if traffic else None,
+                "bytes_per_launch": round(per_launch),
                 "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
                 "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
 
@@ -411,7 +420,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, 1), "impl": "reference",
+            "config": dict(workload_config(args, 1), parallelism=f"{cores} host processes (one planning step each)"),
+            "impl": "reference",
             "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"each step: {cores} concurrent full planning steps (one per core) of "
                                        f"the workload, oracle/ numpy port of vecpomdp.plan"},

@@ -1,9 +1,9 @@
 # usage: bash scripts/ncu_capture.sh <tag> [skip] [extra profile_step args]
-# launch list of one planning step + full captures of k_search and k_backup
-# (launch index `skip` = pass skip+1 of the first profiled step, default pass 8)
+# 1. launch list of one planning step with per-launch duration and DRAM bytes (roofline traffic)
+# 2. full captures of k_search and k_backup (launch index `skip` = pass skip+1, default pass 8)
 set -x
 TAG=$1; S=${2:-7}; shift; shift
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 2000 --csv \
     --log-file gpurun_out/launches_${TAG}.csv python scripts/profile_step.py --steps 1 "$@" > /dev/null 2>&1
 echo launches_rc=$?
 for K in k_search k_backup; do
