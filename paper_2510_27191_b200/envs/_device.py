@@ -256,7 +256,9 @@ def device_model(model) -> DeviceModel:
     if hasattr(model, "device_descriptor"):
         dm = model.device_descriptor()
     else:
-        build = _BY_NAME.get(type(model).__name__)
+        # the model's class or its nearest known base (subclasses of the reference's models,
+        # e.g. with another reference policy, keep their device layout)
+        build = next((_BY_NAME[c.__name__] for c in type(model).__mro__ if c.__name__ in _BY_NAME), None)
         if build is None:
             raise TypeError(f"no device model for {type(model).__name__}; supported: {sorted(_BY_NAME)}")
         dm = build(model)
