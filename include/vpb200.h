@@ -40,7 +40,8 @@ enum vp_model_kind {
   VP_MODEL_MARS = 1,      /* envs/mars.py:44-257 (RockSample family) */
   VP_MODEL_TABULAR = 2,   /* envs/tabular.py:79-145 (Tiger et al.) */
   VP_MODEL_SYNTHETIC = 3, /* NEW: integer-hash scaling model (BASELINE config 5) */
-  VP_MODEL_LIGHTDARK = 4  /* NEW: continuous-observation Light-Dark (config 4) */
+  VP_MODEL_LIGHTDARK = 4, /* NEW: continuous-observation Light-Dark (config 4) */
+  VP_MODEL_NAVIGATION = 5 /* envs/navigation.py (13x13 grid, gates, 8-bit sensor) */
 };
 
 enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
@@ -75,6 +76,13 @@ typedef struct vp_model {
   /* LIGHTDARK */
   double ld_step, ld_light_x, ld_goal_radius, ld_sigma0, ld_sigma_slope, ld_bin_width;
   int32_t ld_bins, ld_pad;
+  /* NAVIGATION (navigation.py:62-251); tables in row-major cell order */
+  int32_t nav_h, nav_w, nav_unknown, nav_pad;
+  const int8_t* nav_kind;     /* [h*w] 0 free, 1 wall, 2 gate, 3 unknown    */
+  const int16_t* nav_aux;     /* [h*w] gate / unknown-cell index            */
+  const uint8_t* nav_goal;    /* [h*w]                                       */
+  const double* nav_heur;     /* [h*w] value heuristic per cell, host numpy (navigation.py:241-251) */
+  double nav_acc, nav_log_acc, nav_log_miss; /* sensor accuracy, log(acc), log(1 - acc) (host numpy) */
 } vp_model;
 
 /* Structure-of-arrays belief tree in HBM (tree.py:100-132 columns plus the

@@ -42,6 +42,8 @@ from .envs import (
     SyntheticStates,
     LightDarkModel,
     LightDarkStates,
+    NavigationModel,
+    NavStates,
 )
 
 __all__ = [
@@ -52,5 +54,5 @@ __all__ = [
     "SolverConfig", "PlanOutcome", "plan", "run_episode",
     "ProblemSpec", "MarsModel", "MarsStates", "TabularPOMDP", "TabularModel",
     "TabularStates", "tiger_model", "SyntheticModel", "SyntheticStates",
-    "LightDarkModel", "LightDarkStates",
+    "LightDarkModel", "LightDarkStates", "NavigationModel", "NavStates",
 ]

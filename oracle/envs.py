@@ -611,3 +611,167 @@ class LightDarkModel(ProblemModel):
         with np.errstate(divide="ignore"):
             out[live] = np.log(p[live])
         return out
+
+
+# --------------------------------------------------------------------------- Navigation
+
+
+NAV_DEFAULT_MAP = "\n".join([
+    ".............",
+    "?????????????",
+    "?????????????",
+    "?????????????",
+    "?????????????",
+    "???.?????.???",
+    "###|#####|###",
+    "???.?????.???",
+    "?????????????",
+    "?????????????",
+    "??????.??????",
+    "??????.??????",
+    "......G......",
+])
+NAV_FREE, NAV_WALL, NAV_GATE, NAV_UNKNOWN = 0, 1, 2, 3
+# neighbour / move order N, NE, E, SE, S, SW, W, NW; action 8 stays (navigation.py:42-47)
+NAV_DR = np.array([-1, -1, 0, 1, 1, 1, 0, -1], dtype=np.int64)
+NAV_DC = np.array([0, 1, 1, 1, 0, -1, -1, -1], dtype=np.int64)
+NAV_STAY = 8
+
+
+@dataclass
+class NavStates:
+    pos: np.ndarray        # flat cell, row * width + col
+    occ: np.ndarray        # (n, n_unknown) occupancy of the unknown cells
+    open_gate: np.ndarray  # which of the two gates is open
+    terminal: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.pos)
+
+    def take(self, idx) -> "NavStates":
+        i = np.asarray(idx, dtype=np.int64)
+        return NavStates(self.pos[i], self.occ[i], self.open_gate[i], self.terminal[i])
+
+
+class NavigationModel(ProblemModel):
+    """Grid navigation through a partially known obstacle field (navigation.py:1-251):
+    hidden occupancy of the '?' cells and of which gate is open, an 8-bit noisy
+    neighbour-occupancy reading per step, goal at the bottom."""
+
+    def __init__(self, map_text: str = NAV_DEFAULT_MAP, p_obstacle: float = 0.25, sensor_accuracy: float = 0.9,
+                 discount: float = 0.983, max_steps: int = 60):
+        lines = [ln for ln in map_text.splitlines() if ln.strip()]
+        self.height, self.width = len(lines), len(lines[0])
+        if any(len(ln) != self.width for ln in lines):
+            raise ValueError("map rows must have equal length")
+        code = {"#": NAV_WALL, "|": NAV_GATE, "?": NAV_UNKNOWN, ".": NAV_FREE, "G": NAV_FREE}
+        grid = np.array([[code.get(ch, -1) for ch in ln] for ln in lines], dtype=np.int64)
+        if (grid < 0).any():
+            raise ValueError("unknown map character")
+        self.kind = grid.astype(np.int8)
+        self.goal = np.array([[ch == "G" for ch in ln] for ln in lines])
+        # per-cell index among the gates / among the unknown cells, in row-major order
+        self.aux = np.full(grid.shape, -1, dtype=np.int64)
+        for k in (NAV_GATE, NAV_UNKNOWN):
+            cells = np.flatnonzero(grid.reshape(-1) == k)
+            self.aux.reshape(-1)[cells] = np.arange(len(cells))
+        self.n_gates = int((grid == NAV_GATE).sum())
+        self.n_unknown = int((grid == NAV_UNKNOWN).sum())
+        if self.n_gates != 2:
+            raise ValueError("map must contain exactly two gates")
+        self.start_cells = np.flatnonzero((grid[0] == NAV_FREE) & ~self.goal[0]).astype(np.int64)
+        if not len(self.start_cells):
+            raise ValueError("top border has no free start cells")
+        self.p_obstacle, self.sensor_accuracy = p_obstacle, sensor_accuracy
+        self.spec = ProblemSpec("navigation", 9, 256, discount, max_steps)
+        self.goal_dist = self._goal_distances()
+
+    def _goal_distances(self) -> np.ndarray:
+        """8-connected BFS distance to the goal with walls blocking and gates / unknown
+        cells optimistic (navigation.py:127-144)."""
+        dist = np.full(self.kind.shape, np.inf)
+        ring = [tuple(x) for x in np.argwhere(self.goal)]
+        for r, c in ring:
+            dist[r, c] = 0.0
+        while ring:
+            nxt = []
+            for r, c in ring:
+                for dr, dc in zip(NAV_DR, NAV_DC):
+                    rr, cc = r + dr, c + dc
+                    if 0 <= rr < self.height and 0 <= cc < self.width and self.kind[rr, cc] != NAV_WALL \
+                            and dist[rr, cc] == np.inf:
+                        dist[rr, cc] = dist[r, c] + 1
+                        nxt.append((rr, cc))
+            ring = nxt
+        return dist
+
+    def blocked(self, s: NavStates, r, c) -> np.ndarray:
+        """Occupancy of target cells per row; off-map counts as occupied (navigation.py:146-162)."""
+        off = (r < 0) | (r >= self.height) | (c < 0) | (c >= self.width)
+        rr, cc = np.clip(r, 0, self.height - 1), np.clip(c, 0, self.width - 1)
+        kind, aux = self.kind[rr, cc], self.aux[rr, cc]
+        out = off | (kind == NAV_WALL) | (~off & (kind == NAV_GATE) & (aux != s.open_gate))
+        unk = np.flatnonzero(~off & (kind == NAV_UNKNOWN))
+        out[unk] |= s.occ[unk, aux[unk]]
+        return out
+
+    def neighbour_bits(self, s: NavStates) -> np.ndarray:
+        r, c = s.pos // self.width, s.pos % self.width
+        return np.stack([self.blocked(s, r + NAV_DR[i], c + NAV_DC[i]) for i in range(8)], axis=1)
+
+    def sample_initial_states(self, n: int, rng: RowRng) -> NavStates:
+        if n < 1:
+            raise ValueError("n must be >= 1")
+        rows = np.arange(n, dtype=np.int64)
+        pos = self.start_cells[(rng.derive(0).uniform(rows) * len(self.start_cells)).astype(np.int64)]
+        occ = rng.derive(1).uniform(rows, self.n_unknown) < self.p_obstacle
+        gate = (rng.derive(2).uniform(rows) < 0.5).astype(np.int64)
+        return NavStates(pos, occ, gate, np.zeros(n, dtype=bool))
+
+    def step_batch(self, s: NavStates, actions, rng) -> StepResult:
+        """navigation.py:172-213."""
+        check_step_inputs(self.spec, s, actions)
+        a = np.asarray(actions, dtype=np.int64)
+        r, c = s.pos // self.width, s.pos % self.width
+        move = a != NAV_STAY
+        k = np.minimum(a, 7)
+        tr = np.where(move, r + NAV_DR[k], r)
+        tc = np.where(move, c + NAV_DC[k], c)
+        hit = move & self.blocked(s, tr, tc)
+        nr, nc = np.where(hit, r, tr), np.where(hit, c, tc)
+        goal = self.goal[nr, nc] & move & ~hit
+        rew = np.where(goal, 20.0, np.where(hit, -1.1, np.where(move, -0.1, -0.3)))
+        term = s.terminal | goal
+        nxt = NavStates(nr * self.width + nc, s.occ.copy(), s.open_gate.copy(), term)
+        flips = rng.derive(0).uniform(8) >= self.sensor_accuracy
+        obs = ((self.neighbour_bits(nxt) ^ flips) @ (1 << np.arange(8, dtype=np.int64))).astype(np.int64)
+        obs[term] = self.spec.terminal_obs
+        nxt.pos[s.terminal] = s.pos[s.terminal]
+        rew = np.where(s.terminal, 0.0, rew)
+        return StepResult(nxt, obs, rew)
+
+    def observation_log_likelihood(self, nxt: NavStates, action: int, observation: int) -> np.ndarray:
+        """matches * log(acc) + misses * log(1 - acc) over the 8 bits (navigation.py:215-239)."""
+        if not 0 <= observation <= self.spec.terminal_obs:
+            raise ValueError("invalid observation code")
+        out = np.full(len(nxt), -np.inf)
+        if observation == self.spec.terminal_obs:
+            out[nxt.terminal] = 0.0
+            return out
+        want = ((observation >> np.arange(8)) & 1).astype(bool)
+        live = ~nxt.terminal
+        hits = (self.neighbour_bits(nxt) == want).sum(axis=1)[live]
+        miss = 8 - hits
+        with np.errstate(divide="ignore", invalid="ignore"):
+            out[live] = hits * np.log(self.sensor_accuracy) + np.where(
+                miss > 0, miss * np.log(1.0 - self.sensor_accuracy), 0.0)
+        return out
+
+    def value_heuristic(self, s: NavStates) -> np.ndarray:
+        """Discounted goal bonus minus step costs at the optimistic distance (navigation.py:241-251)."""
+        g = self.spec.discount
+        d = np.maximum(self.goal_dist[s.pos // self.width, s.pos % self.width] - 1.0, 0.0)
+        decay = g ** d
+        h = 20.0 * decay - 0.1 * (1.0 - decay) / (1.0 - g)
+        h[s.terminal] = 0.0
+        return h

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvpb200.so")
 
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
-VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK = 1, 2, 3, 4
+VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK, VP_MODEL_NAVIGATION = 1, 2, 3, 4, 5
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
 ABI_VERSION = 3
@@ -41,6 +41,9 @@ class VpModel(C.Structure):
         ("ld_step", C.c_double), ("ld_light_x", C.c_double), ("ld_goal_radius", C.c_double),
         ("ld_sigma0", C.c_double), ("ld_sigma_slope", C.c_double), ("ld_bin_width", C.c_double),
         ("ld_bins", C.c_int32), ("ld_pad", C.c_int32),
+        ("nav_h", C.c_int32), ("nav_w", C.c_int32), ("nav_unknown", C.c_int32), ("nav_pad", C.c_int32),
+        ("nav_kind", C.c_void_p), ("nav_aux", C.c_void_p), ("nav_goal", C.c_void_p), ("nav_heur", C.c_void_p),
+        ("nav_acc", C.c_double), ("nav_log_acc", C.c_double), ("nav_log_miss", C.c_double),
     ]
 
 
@@ -196,11 +199,11 @@ def layout_mismatches() -> list:
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
-            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset]
+            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset, VpModel.nav_log_miss.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag"]
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag", "vp_model.nav_log_miss"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

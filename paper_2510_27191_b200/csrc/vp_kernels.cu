@@ -204,6 +204,7 @@ static int32_t dispatch_model(int kind, F&& f) {
     case VP_MODEL_TABULAR: return f(TabularModel());
     case VP_MODEL_SYNTHETIC: return f(SyntheticModel());
     case VP_MODEL_LIGHTDARK: return f(LightDarkModel());
+    case VP_MODEL_NAVIGATION: return f(NavigationModel());
     default: return VP_ERR_MODEL;
   }
 }
@@ -630,7 +631,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, a_ckey),
                        (int32_t)offsetof(vp_search_args, m),
                        (int32_t)offsetof(vp_model, mars_gpow),
-                       (int32_t)offsetof(vp_tree, cdf_tag)};
+                       (int32_t)offsetof(vp_tree, cdf_tag),
+                       (int32_t)offsetof(vp_model, nav_log_miss)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];

@@ -5,6 +5,7 @@
 //   TABULAR   /root/reference/pkg/src/vecpomdp/envs/tabular.py:106-130
 //   SYNTHETIC oracle/envs.py SyntheticModel   (new; integer hash dynamics)
 //   LIGHTDARK oracle/envs.py LightDarkModel   (new; continuous observations)
+//   NAVIGATION /root/reference/pkg/src/vecpomdp/envs/navigation.py:146-251
 // The per-row model stream is `mkey` = level_rng.derive(1) (search.py:113-115)
 // and the logical row id is the global simulation index.
 #pragma once
@@ -295,6 +296,87 @@ struct LightDarkModel {
     if (s.term) return -INFINITY;
     const double sigma = M.ld_sigma0 + M.ld_sigma_slope * fabs(s.x - M.ld_light_x);
     return log(bin_mass(M, s.x, sigma, (int)obs / M.ld_bins) * bin_mass(M, s.y, sigma, (int)obs % M.ld_bins));
+  }
+};
+
+// ------------------------------------------------------------------ NAVIGATION
+// 24-byte record: occupancy bits of the unknown cells (<= 128), flat cell,
+// open gate, terminal flag.
+struct __align__(8) NavState {
+  u64 occ0, occ1;
+  int32_t pos;
+  uint8_t gate, term;
+  uint16_t pad;
+};
+
+struct NavigationModel {
+  typedef NavState State;
+  // neighbour / move order N, NE, E, SE, S, SW, W, NW; action 8 stays (navigation.py:42-47)
+  static __device__ __forceinline__ int dr(int i) { return (i == 0 || i == 1 || i == 7) ? -1 : (i >= 3 && i <= 5) ? 1 : 0; }
+  static __device__ __forceinline__ int dc(int i) { return (i >= 1 && i <= 3) ? 1 : (i >= 5 && i <= 7) ? -1 : 0; }
+
+  // off-map, wall, closed gate or occupied unknown cell (navigation.py:146-162)
+  static __device__ __forceinline__ bool blocked(const vp_model& M, const State& s, int r, int c) {
+    if (r < 0 || r >= M.nav_h || c < 0 || c >= M.nav_w) return true;
+    const int cell = r * M.nav_w + c;
+    const int kind = M.nav_kind[cell];
+    if (kind == 1) return true;
+    if (kind == 2) return M.nav_aux[cell] != (int)s.gate;
+    if (kind == 3) {
+      const int u = M.nav_aux[cell];
+      return ((u < 64 ? s.occ0 >> u : s.occ1 >> (u - 64)) & 1ull) != 0;
+    }
+    return false;
+  }
+
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row, u32& obs,
+                                              double& rew) {
+    // navigation.py:172-213
+    const int r = s.pos / M.nav_w, c = s.pos % M.nav_w;
+    const bool move = a != 8;
+    const int k = a < 7 ? a : 7;
+    const int tr = move ? r + dr(k) : r, tc = move ? c + dc(k) : c;
+    const bool hit = move && blocked(M, s, tr, tc);
+    const int nr = hit ? r : tr, nc = hit ? c : tc;
+    const bool goal = M.nav_goal[nr * M.nav_w + nc] && move && !hit;
+    const double rw = goal ? 20.0 : hit ? -1.1 : move ? -0.1 : -0.3;
+    const bool term = s.term || goal;
+    State nx = s;
+    nx.pos = nr * M.nav_w + nc;
+    // 8-bit noisy neighbour occupancy of the next cell: bit i flips when
+    // rng.derive(0).uniform(8)[i] >= accuracy
+    const u64 fk = fold(mkey, 0);
+    u32 o = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool bit = blocked(M, nx, nr + dr(i), nc + dc(i));
+      const bool flip = uniform_j(fk, row, (u64)(i + 1)) >= M.nav_acc;
+      o |= (u32)(bit != flip) << i;
+    }
+    obs = term ? (u32)M.obs_arity : o;
+    if (s.term) {
+      rew = 0.0;
+      return;  // absorbing: the state stays
+    }
+    rew = rw;
+    nx.term = term ? 1 : 0;
+    s = nx;
+  }
+
+  static __device__ __forceinline__ double heuristic(const vp_model& M, const State& s) {
+    return s.term ? 0.0 : M.nav_heur[s.pos];
+  }
+
+  // matches * log(acc) + misses * log(1 - acc) over the 8 bits (navigation.py:215-239)
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int, u32 obs) {
+    if (obs == (u32)M.obs_arity) return s.term ? 0.0 : -INFINITY;
+    if (s.term) return -INFINITY;
+    const int r = s.pos / M.nav_w, c = s.pos % M.nav_w;
+    int hits = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hits += blocked(M, s, r + dr(i), c + dc(i)) == (bool)((obs >> i) & 1u);
+    const int miss = 8 - hits;
+    return (double)hits * M.nav_log_acc + (miss > 0 ? (double)miss * M.nav_log_miss : 0.0);
   }
 };
 

@@ -31,6 +31,8 @@ MARS_DTYPE = np.dtype([("x0", "u1"), ("y0", "u1"), ("x1", "u1"), ("y1", "u1"), (
 TAB_DTYPE = np.dtype([("idx", "<i4"), ("term", "<i4")])
 SYN_DTYPE = np.dtype([("word", "<u8"), ("term", "<u4"), ("pad", "<u4")])
 LD_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("term", "<u4"), ("pad", "<u4")])
+NAV_DTYPE = np.dtype([("occ0", "<u8"), ("occ1", "<u8"), ("pos", "<i4"), ("gate", "u1"), ("term", "u1"),
+                      ("pad", "<u2")])
 
 
 def _torch():
@@ -238,11 +240,63 @@ def lightdark_descriptor(model, unpack=None) -> DeviceModel:
     return dm
 
 
+# ------------------------------------------------------------------ NAVIGATION
+
+
+def nav_pack(states) -> np.ndarray:
+    occ = np.asarray(states.occ, dtype=bool)
+    if occ.shape[1] > 128:
+        raise ValueError("Navigation device records hold at most 128 unknown cells")
+    bits = np.packbits(np.pad(occ, ((0, 0), (0, 128 - occ.shape[1]))), axis=1, bitorder="little")
+    rec = np.zeros(len(occ), dtype=NAV_DTYPE)
+    words = bits.view("<u8")
+    rec["occ0"], rec["occ1"] = words[:, 0], words[:, 1]
+    rec["pos"] = np.asarray(states.pos)
+    rec["gate"] = np.asarray(states.open_gate)
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    return rec
+
+
+def nav_unpacker(n_unknown: int, states_cls):
+    def unpack(rec):
+        words = np.stack([rec["occ0"], rec["occ1"]], axis=1).astype("<u8")
+        occ = np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, :n_unknown].astype(bool)
+        return states_cls(rec["pos"].astype(np.int64), occ, rec["gate"].astype(np.int64), rec["term"].astype(bool))
+    return unpack
+
+
+def navigation_descriptor(model, unpack=None) -> DeviceModel:
+    """vp_model for a NavigationModel (reference envs/navigation.py:62-121 attributes)."""
+    if model.n_unknown > 128:
+        raise ValueError("Navigation device records hold at most 128 unknown cells")
+    if unpack is None:  # a reference model object: rebuild records as the product's NavStates
+        from .navigation import NavStates
+
+        unpack = nav_unpacker(int(model.n_unknown), NavStates)
+    dm = DeviceModel(_lib.VP_MODEL_NAVIGATION, model.spec, NAV_DTYPE, nav_pack, unpack)
+    d = dm.desc
+    d.nav_h, d.nav_w, d.nav_unknown = int(model.height), int(model.width), int(model.n_unknown)
+    d.nav_kind = dm.upload(np.asarray(model.kind, dtype=np.int8).reshape(-1))
+    d.nav_aux = dm.upload(np.asarray(model.aux, dtype=np.int64).astype(np.int16).reshape(-1))
+    d.nav_goal = dm.upload(np.asarray(model.goal, dtype=np.uint8).reshape(-1))
+    # the heuristic and the sensor logs with the reference's own numpy arithmetic (bit-exact)
+    g = model.spec.discount
+    dist = np.asarray(model.goal_dist if hasattr(model, "goal_dist") else model._goal_dist)
+    decay = g ** np.maximum(dist - 1.0, 0.0)
+    d.nav_heur = dm.upload((20.0 * decay - 0.1 * (1.0 - decay) / (1.0 - g)).reshape(-1))
+    d.nav_acc = float(model.sensor_accuracy)
+    d.nav_log_acc = float(np.log(model.sensor_accuracy))
+    with np.errstate(divide="ignore"):
+        d.nav_log_miss = float(np.log(1.0 - model.sensor_accuracy))
+    return dm
+
+
 _BY_NAME = {
     "MarsModel": mars_descriptor,
     "TabularModel": tabular_descriptor,
     "SyntheticModel": synthetic_descriptor,
     "LightDarkModel": lightdark_descriptor,
+    "NavigationModel": navigation_descriptor,
 }
 _CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 

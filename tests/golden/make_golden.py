@@ -30,6 +30,7 @@ sys.path.insert(0, REPO)
 
 import vecpomdp as ref  # noqa: E402
 from vecpomdp.envs import MarsModel, tiger_model  # noqa: E402
+from vecpomdp.envs.navigation import NavigationModel  # noqa: E402
 
 import oracle  # noqa: E402  (only for the two NEW models the reference lacks)
 
@@ -107,6 +108,8 @@ def make_model(kind: str, seed: int):
         return oracle.SyntheticModel(n_actions=16, n_obs=8, seed=seed)
     if kind == "lightdark":
         return oracle.LightDarkModel()
+    if kind == "navigation":
+        return NavigationModel()
     raise ValueError(kind)
 
 
@@ -118,6 +121,7 @@ PLAN_CASES = [
     ("plan_tiger", "tiger", 256, 8, [0, 1], True),
     ("plan_synthetic", "synthetic", 256, 6, [0, 1], True),
     ("plan_lightdark", "lightdark", 128, 5, [0, 1], True),
+    ("plan_navigation", "navigation", 256, 6, [0, 1], True),
 ]
 
 
@@ -160,7 +164,31 @@ def gen_episodes():
     return out
 
 
+def gen_navigation_steps():
+    """Navigation model vectors (navigation.py:172-251): steps from random states / actions,
+    likelihoods of the realised observations, heuristics."""
+    model = NavigationModel()
+    n = 400
+    st = model.sample_initial_states(n, ref.RowRng.from_seed(21))
+    out = {"pos0": st.pos, "occ0": st.occ, "gate0": st.open_gate}
+    for t in range(8):
+        a = (ref.RowRng.from_seed(22 + t).uniform(np.arange(n)) * 9).astype(np.int64)
+        res = model.step_batch(st, a, ref.RowRng.from_seed(40 + t).bind(np.arange(n)))
+        out[f"a{t}"] = a
+        out[f"pos{t + 1}"] = res.next_states.pos
+        out[f"term{t + 1}"] = res.next_states.terminal
+        out[f"obs{t + 1}"] = res.observations
+        out[f"rew{t + 1}"] = res.rewards
+        o = int(res.observations[0])
+        out[f"ll{t + 1}"] = model.observation_log_likelihood(res.next_states, int(a[0]), o)
+        out[f"llobs{t + 1}"] = np.array([int(a[0]), o])
+        out[f"h{t + 1}"] = model.value_heuristic(res.next_states)
+        st = res.next_states
+    np.savez_compressed(os.path.join(HERE, "nav_steps.npz"), **out)
+
+
 if __name__ == "__main__":
+    gen_navigation_steps()
     gen_rng()
     gen_formulas()
     manifest = {"plans": gen_plans(), "episodes": gen_episodes(),

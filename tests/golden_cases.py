@@ -39,6 +39,8 @@ def oracle_model(kind: str, seed: int):
         return oracle.SyntheticModel(n_actions=16, n_obs=8, seed=seed)
     if kind == "lightdark":
         return oracle.LightDarkModel()
+    if kind == "navigation":
+        return oracle.NavigationModel()
     raise ValueError(kind)
 
 

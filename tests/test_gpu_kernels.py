@@ -50,6 +50,12 @@ def _random_states(model, kind, n, rng):
         st = model.sample_initial_states(n, oracle.RowRng.from_seed(7))
         st.terminal = rng.random(n) < 0.05
         return st
+    if kind == "navigation":
+        st = model.sample_initial_states(n, oracle.RowRng.from_seed(7))
+        free = np.flatnonzero(model.kind.reshape(-1) != 1)  # anywhere off the walls, incl. next to the goal
+        st.pos = free[rng.integers(0, len(free), size=n)]
+        st.terminal = rng.random(n) < 0.05
+        return st
     st = model.sample_initial_states(n, oracle.RowRng.from_seed(7))
     st.x = st.x + rng.normal(size=n) * 4
     st.y = st.y + rng.normal(size=n) * 4
@@ -63,6 +69,7 @@ MODELS = [
     ("tiger", lambda: (oracle.tiger_model(), vp.tiger_model())),
     ("synthetic", lambda: (oracle.SyntheticModel(seed=3), vp.SyntheticModel(seed=3))),
     ("lightdark", lambda: (oracle.LightDarkModel(), vp.LightDarkModel())),
+    ("navigation", lambda: (oracle.NavigationModel(), vp.NavigationModel())),
 ]
 
 
@@ -80,7 +87,7 @@ def test_device_model_step_matches_oracle(kind, make):
     np.testing.assert_array_equal(got.observations, want.observations)
     np.testing.assert_array_equal(got.rewards, want.rewards)
     np.testing.assert_array_equal(got.next_states.terminal, want.next_states.terminal)
-    for f in ("x", "y", "rocks", "idx", "word"):
+    for f in ("x", "y", "rocks", "idx", "word", "pos", "occ", "open_gate"):
         if hasattr(want.next_states, f):
             np.testing.assert_array_equal(getattr(got.next_states, f), getattr(want.next_states, f), err_msg=f)
     h_want = om.value_heuristic(want.next_states)

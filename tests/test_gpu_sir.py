@@ -21,6 +21,7 @@ MODELS = {
     "tiger": lambda: (oracle.tiger_model(), vp.tiger_model()),
     "synthetic": lambda: (oracle.SyntheticModel(seed=4), vp.SyntheticModel(seed=4)),
     "lightdark": lambda: (oracle.LightDarkModel(), vp.LightDarkModel()),
+    "navigation": lambda: (oracle.NavigationModel(), vp.NavigationModel()),
 }
 
 
@@ -35,7 +36,7 @@ def _scenario(kind, seed, m=3000):
 
 
 def _states_equal(x, y):
-    for f in ("x", "y", "rocks", "terminal", "idx", "word"):
+    for f in ("x", "y", "rocks", "terminal", "idx", "word", "pos", "occ", "open_gate"):
         if hasattr(x, f):
             np.testing.assert_array_equal(np.asarray(getattr(x, f)), np.asarray(getattr(y, f)), err_msg=f)
 

@@ -97,3 +97,23 @@ def test_oracle_episode_matches_reference():
         got = oracle.run_episode(oracle.MarsModel(n=4, m=3, layout_seed=r["seed"]), cfg, seed=r["seed"])
         assert got.steps == r["steps"] and got.terminal_reason == r["reason"]
         assert got.discounted_return == r["return"]
+
+
+def test_navigation_model_vectors():
+    """oracle.NavigationModel vs the reference's navigation.py (steps, likelihoods, heuristic)."""
+    g = load("nav_steps")
+    m = oracle.NavigationModel()
+    st = m.sample_initial_states(400, oracle.RowRng.from_seed(21))
+    np.testing.assert_array_equal(st.pos, g["pos0"])
+    np.testing.assert_array_equal(st.occ, g["occ0"])
+    np.testing.assert_array_equal(st.open_gate, g["gate0"])
+    for t in range(8):
+        res = m.step_batch(st, g[f"a{t}"], oracle.RowRng.from_seed(40 + t).bind(np.arange(400)))
+        np.testing.assert_array_equal(res.next_states.pos, g[f"pos{t + 1}"])
+        np.testing.assert_array_equal(res.next_states.terminal, g[f"term{t + 1}"])
+        np.testing.assert_array_equal(res.observations, g[f"obs{t + 1}"])
+        np.testing.assert_array_equal(res.rewards, g[f"rew{t + 1}"])
+        a, o = (int(v) for v in g[f"llobs{t + 1}"])
+        np.testing.assert_array_equal(m.observation_log_likelihood(res.next_states, a, o), g[f"ll{t + 1}"])
+        np.testing.assert_array_equal(m.value_heuristic(res.next_states), g[f"h{t + 1}"])
+        st = res.next_states
