@@ -52,3 +52,43 @@ def test_config_header_and_cli_defaults():
     assert np.array_equal(build_model("mars", {"n": 6, "m": 4}, 7).rock_at, MarsModel(6, 4, layout_seed=7).rock_at)
     assert np.array_equal(build_model("mars", {"n": 6, "m": 4, "layout_seed": 1}, 7).rock_at,
                           MarsModel(6, 4, layout_seed=1).rock_at)
+
+
+def _campaign_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    import paper_2510_27191_b200.campaign as camp
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # stand-in episodes (no GPU): the record of run i depends only on i
+        camp.run_one = lambda cfg, i: _records([float(i) * 1.5 - 2.0])[0] | {"run_index": i, "seed": i}
+        cfg = CampaignConfig(problem="tiger", runs=7)
+        recs, summ = camp.run_campaign(cfg, rank, world)
+        q.put((rank, [r["run_index"] for r in recs], summ["metrics"]["discounted_return"]["mean"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_campaign_runs_split_over_ranks_gloo():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_campaign_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = sorted(q.get() for _ in range(2))
+    want_mean = np.mean([i * 1.5 - 2.0 for i in range(7)])
+    for rank, idx, mean in res:
+        assert idx == list(range(7)) and mean == pytest.approx(want_mean)
