@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 3
+#define VPB200_ABI_VERSION 4
 
 enum vp_status {
   VP_OK = 0,
@@ -41,7 +41,8 @@ enum vp_model_kind {
   VP_MODEL_TABULAR = 2,   /* envs/tabular.py:79-145 (Tiger et al.) */
   VP_MODEL_SYNTHETIC = 3, /* NEW: integer-hash scaling model (BASELINE config 5) */
   VP_MODEL_LIGHTDARK = 4, /* NEW: continuous-observation Light-Dark (config 4) */
-  VP_MODEL_NAVIGATION = 5 /* envs/navigation.py (13x13 grid, gates, 8-bit sensor) */
+  VP_MODEL_NAVIGATION = 5, /* envs/navigation.py (13x13 grid, gates, 8-bit sensor) */
+  VP_MODEL_CROWDNAV = 6    /* envs/crowdnav.py (robot through a reactive crowd) */
 };
 
 enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
@@ -83,6 +84,12 @@ typedef struct vp_model {
   const uint8_t* nav_goal;    /* [h*w]                                       */
   const double* nav_heur;     /* [h*w] value heuristic per cell, host numpy (navigation.py:241-251) */
   double nav_acc, nav_log_acc, nav_log_miss; /* sensor accuracy, log(acc), log(1 - acc) (host numpy) */
+  /* CROWDNAV (crowdnav.py:64-241); records hold <= 320 people, <= 8 tracked */
+  int32_t crowd_people, crowd_tracked;
+  double crowd_hall_w, crowd_hall_d, crowd_noise, crowd_react, crowd_r_nearby;
+  double crowd_v_curious, crowd_v_shy, crowd_v_back, crowd_collision;
+  const double* crowd_heur;   /* [crowd_heur_len] heuristic by remaining rows k, host numpy (crowdnav.py:203-210) */
+  int32_t crowd_heur_len, crowd_pad;
 } vp_model;
 
 /* Structure-of-arrays belief tree in HBM (tree.py:100-132 columns plus the

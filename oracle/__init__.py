@@ -44,6 +44,8 @@ from .envs import (
     LightDarkStates,
     NavigationModel,
     NavStates,
+    CrowdNavModel,
+    CrowdStates,
 )
 
 __all__ = [
@@ -54,5 +56,5 @@ __all__ = [
     "SolverConfig", "PlanOutcome", "plan", "run_episode",
     "ProblemSpec", "MarsModel", "MarsStates", "TabularPOMDP", "TabularModel",
     "TabularStates", "tiger_model", "SyntheticModel", "SyntheticStates",
-    "LightDarkModel", "LightDarkStates", "NavigationModel", "NavStates",
+    "LightDarkModel", "LightDarkStates", "NavigationModel", "NavStates", "CrowdNavModel", "CrowdStates",
 ]

@@ -775,3 +775,131 @@ class NavigationModel(ProblemModel):
         h = 20.0 * decay - 0.1 * (1.0 - decay) / (1.0 - g)
         h[s.terminal] = 0.0
         return h
+
+
+# --------------------------------------------------------------------------- CrowdNav
+
+CROWD_DIRS = np.array([(0.0, 1.0), (1.0, 0.0), (0.0, -1.0), (-1.0, 0.0), (0.0, 0.0)])  # N E S W YELL
+CROWD_YELL = 4
+
+
+@dataclass
+class CrowdStates:
+    robot: np.ndarray      # (n, 2) float64 metres
+    persons: np.ndarray    # (n, p, 2) float32 metres
+    curious: np.ndarray    # (n, p) hidden traits
+    tracked: np.ndarray    # (n, k) persons the sensor watches
+    prev_dist: np.ndarray  # (n, k) their distances at the previous step
+    last_code: np.ndarray  # (n,) observation emitted on entering the state
+    terminal: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.robot)
+
+    def take(self, idx) -> "CrowdStates":
+        i = np.asarray(idx, dtype=np.int64)
+        return CrowdStates(self.robot[i], self.persons[i], self.curious[i], self.tracked[i], self.prev_dist[i],
+                           self.last_code[i], self.terminal[i])
+
+
+class CrowdNavModel(ProblemModel):
+    """Robot crossing a hall among a reactive crowd (crowdnav.py:1-241): hidden curious / shy
+    traits, every person jitters, nearby people react; the observation is one bit per
+    tracked person telling whether it closed distance."""
+
+    def __init__(self, p_curious: float = 0.5, n_people: int = 300, n_tracked: int = 6, hall_width: float = 50.0,
+                 hall_depth: float = 40.0, motion_noise: float = 0.05, react_prob: float = 0.9,
+                 r_nearby: float = 4.0, v_curious: float = 0.3, v_shy: float = 0.8, v_back: float = 2.0,
+                 collision_radius: float = 0.5, discount: float = 0.97, max_steps: int = 200):
+        if not 0.0 <= p_curious <= 1.0:
+            raise ValueError("p_curious must be in [0, 1]")
+        self.p_curious, self.n_people, self.n_tracked = p_curious, n_people, n_tracked
+        self.hall = np.array([hall_width, hall_depth])
+        self.motion_noise, self.react_prob, self.r_nearby = motion_noise, react_prob, r_nearby
+        self.v_curious, self.v_shy, self.v_back = v_curious, v_shy, v_back
+        self.collision_radius = collision_radius
+        self.spec = ProblemSpec("crowdnav", 5, 2 ** n_tracked, discount, max_steps)
+
+    @staticmethod
+    def _dist(persons, robot) -> np.ndarray:
+        d = persons.astype(np.float64) - robot[:, None, :]
+        return np.sqrt((d ** 2).sum(axis=2))
+
+    def _track(self, robot, persons):
+        dist = self._dist(persons, robot)
+        tracked = np.argsort(dist, axis=1)[:, : self.n_tracked].astype(np.int64)
+        return tracked, np.take_along_axis(dist, tracked, axis=1)
+
+    def sample_initial_states(self, n: int, rng: RowRng) -> CrowdStates:
+        if n < 1:
+            raise ValueError("n must be >= 1")
+        rows = np.arange(n, dtype=np.int64)
+        robot = np.tile(np.array([self.hall[0] / 2.0, 0.0]), (n, 1))
+        u = rng.derive(0).uniform(rows, self.n_people * 2).reshape(n, self.n_people, 2)
+        persons = (u * self.hall).astype(np.float32)
+        curious = rng.derive(1).uniform(rows, self.n_people) < self.p_curious
+        tracked, prev = self._track(robot, persons)
+        return CrowdStates(robot, persons, curious, tracked, prev, np.zeros(n, dtype=np.int64), np.zeros(n, dtype=bool))
+
+    def step_batch(self, s: CrowdStates, actions, rng) -> StepResult:
+        """crowdnav.py:120-186."""
+        check_step_inputs(self.spec, s, actions)
+        a = np.asarray(actions, dtype=np.int64)
+        n, p = len(s), self.n_people
+        robot = s.robot + CROWD_DIRS[a]
+        entered = robot[:, 1] >= self.hall[1]
+        robot = np.stack([np.clip(robot[:, 0], 0.0, self.hall[0]), np.clip(robot[:, 1], 0.0, self.hall[1])], axis=1)
+        people = s.persons.astype(np.float64) + rng.derive(0).normal(p * 2).reshape(n, p, 2) * self.motion_noise
+        diff = robot[:, None, :] - people
+        dist = np.sqrt((diff ** 2).sum(axis=2))
+        react = (dist < self.r_nearby) & (dist > 1e-9) & (rng.derive(1).uniform(p) < self.react_prob)
+        unit = diff / np.maximum(dist, 1e-9)[:, :, None]
+        speed = np.where(s.curious, self.v_curious, -self.v_shy)
+        speed = np.where((a == CROWD_YELL)[:, None], -self.v_back, speed)
+        people = people + react[:, :, None] * speed[:, :, None] * unit
+        people[:, :, 0] = np.clip(people[:, :, 0], 0.0, self.hall[0])
+        people[:, :, 1] = np.clip(people[:, :, 1], 0.0, self.hall[1])
+        people = people.astype(np.float32)
+        new_dist = self._dist(people, robot)
+        bumped = (new_dist < self.collision_radius).any(axis=1)
+        rew = -1.0 - 25.0 * (a == CROWD_YELL) - 200.0 * bumped + 1000.0 * entered
+        tdist = np.take_along_axis(new_dist, s.tracked, axis=1)
+        code = ((tdist < s.prev_dist) @ (1 << np.arange(self.n_tracked, dtype=np.int64))).astype(np.int64)
+        term = s.terminal | entered
+        obs = np.where(term, self.spec.terminal_obs, code)
+        nxt = CrowdStates(robot, people, s.curious.copy(), s.tracked.copy(), tdist, code, term)
+        old = s.terminal
+        if old.any():
+            nxt.robot[old], nxt.persons[old] = s.robot[old], s.persons[old]
+            nxt.prev_dist[old], nxt.last_code[old] = s.prev_dist[old], s.last_code[old]
+            rew = np.where(old, 0.0, rew)
+        return StepResult(nxt, obs, rew)
+
+    def observation_log_likelihood(self, nxt: CrowdStates, action: int, observation: int) -> np.ndarray:
+        """Deterministic observation: 0 where the state emitted it, -inf elsewhere (crowdnav.py:188-201)."""
+        if not 0 <= observation <= self.spec.terminal_obs:
+            raise ValueError("invalid observation code")
+        out = np.full(len(nxt), -np.inf)
+        if observation == self.spec.terminal_obs:
+            out[nxt.terminal] = 0.0
+        else:
+            out[~nxt.terminal & (nxt.last_code == observation)] = 0.0
+        return out
+
+    def value_heuristic(self, s: CrowdStates) -> np.ndarray:
+        g = self.spec.discount
+        decay = g ** np.maximum(np.ceil(self.hall[1] - s.robot[:, 1]) - 1.0, 0.0)
+        h = 1000.0 * decay - (1.0 - decay) / (1.0 - g)
+        h[s.terminal] = 0.0
+        return h
+
+    def refresh_executed(self, executed: CrowdStates) -> CrowdStates:
+        tracked, prev = self._track(executed.robot, executed.persons)
+        return CrowdStates(executed.robot, executed.persons, executed.curious, tracked, prev, executed.last_code,
+                           executed.terminal)
+
+    def reconcile_belief(self, particles: CrowdStates, executed: CrowdStates) -> CrowdStates:
+        n = len(particles)
+        rep = lambda x: np.repeat(x, n, axis=0)  # noqa: E731
+        return CrowdStates(rep(executed.robot), rep(executed.persons), particles.curious, rep(executed.tracked),
+                           rep(executed.prev_dist), rep(executed.last_code), rep(executed.terminal))

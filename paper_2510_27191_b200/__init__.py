@@ -12,7 +12,7 @@ from . import _lib
 from .backup import backup, log_sum_exp_rows
 from .belief import DeviceBelief, ParticleBelief, SirUpdate, sir_update, systematic_resample
 from .core import ProblemModel, ProblemSpec, StepResult
-from .envs import (LightDarkModel, MarsModel, NavigationModel, SyntheticModel, TabularModel, TabularPOMDP,
+from .envs import (CrowdNavModel, CrowdStates, LightDarkModel, MarsModel, NavigationModel, SyntheticModel, TabularModel, TabularPOMDP,
                    device_model, problem_from_config, tiger_model)
 from .rng import BoundRng, RowRng
 from .search import LeafResult, SearchBatch, sample_actions, search, softmax_rows
@@ -23,7 +23,7 @@ from .tree import DeviceTree, init_tree
 __version__ = "0.1.0"
 
 __all__ = [
-    "BoundRng", "DeviceBelief", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "NavigationModel", "ParticleBelief", "PlanOutcome",
+    "BoundRng", "CrowdNavModel", "CrowdStates", "DeviceBelief", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "NavigationModel", "ParticleBelief", "PlanOutcome",
     "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",

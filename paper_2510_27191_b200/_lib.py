@@ -16,9 +16,11 @@ LIB_PATH = os.path.join(_HERE, "libvpb200.so")
 
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK, VP_MODEL_NAVIGATION = 1, 2, 3, 4, 5
+VP_MODEL_CROWDNAV = 6
+CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
     C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
@@ -44,6 +46,11 @@ class VpModel(C.Structure):
         ("nav_h", C.c_int32), ("nav_w", C.c_int32), ("nav_unknown", C.c_int32), ("nav_pad", C.c_int32),
         ("nav_kind", C.c_void_p), ("nav_aux", C.c_void_p), ("nav_goal", C.c_void_p), ("nav_heur", C.c_void_p),
         ("nav_acc", C.c_double), ("nav_log_acc", C.c_double), ("nav_log_miss", C.c_double),
+        ("crowd_people", C.c_int32), ("crowd_tracked", C.c_int32),
+        ("crowd_hall_w", C.c_double), ("crowd_hall_d", C.c_double), ("crowd_noise", C.c_double),
+        ("crowd_react", C.c_double), ("crowd_r_nearby", C.c_double), ("crowd_v_curious", C.c_double),
+        ("crowd_v_shy", C.c_double), ("crowd_v_back", C.c_double), ("crowd_collision", C.c_double),
+        ("crowd_heur", C.c_void_p), ("crowd_heur_len", C.c_int32), ("crowd_pad", C.c_int32),
     ]
 
 
@@ -199,11 +206,13 @@ def layout_mismatches() -> list:
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
-            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset, VpModel.nav_log_miss.offset]
+            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset, VpModel.nav_log_miss.offset,
+            VpModel.crowd_heur.offset, CROWD_STATE_BYTES]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag", "vp_model.nav_log_miss"]
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag", "vp_model.nav_log_miss",
+             "vp_model.crowd_heur", "sizeof(CrowdState)"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

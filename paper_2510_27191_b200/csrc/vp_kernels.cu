@@ -205,6 +205,7 @@ static int32_t dispatch_model(int kind, F&& f) {
     case VP_MODEL_SYNTHETIC: return f(SyntheticModel());
     case VP_MODEL_LIGHTDARK: return f(LightDarkModel());
     case VP_MODEL_NAVIGATION: return f(NavigationModel());
+    case VP_MODEL_CROWDNAV: return f(CrowdNavModel());
     default: return VP_ERR_MODEL;
   }
 }
@@ -222,8 +223,26 @@ static int32_t dispatch_psi(int dtype, int exact, F&& f) {
   return VP_ERR_INVALID;
 }
 
+// Per-thread stack for models whose records live in local memory: reserved
+// once, before any launch or graph capture needs it.
+static bool ensure_stack(size_t bytes) {
+  static size_t have = 0;
+  if (have >= bytes) return true;
+  size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) != cudaSuccess) return false;
+  if (cur < bytes && cudaDeviceSetLimit(cudaLimitStackSize, bytes) != cudaSuccess) return false;
+  have = bytes;
+  return true;
+}
+
 template <class Model>
 static bool state_size_ok(const vp_model& M) {
+  if constexpr (std::is_same<Model, CrowdNavModel>::value) {
+    if (M.crowd_people < 1 || M.crowd_people > kCrowdPeople || M.crowd_tracked < 0 ||
+        M.crowd_tracked > kCrowdTracked || M.crowd_heur_len < 1 || !M.crowd_heur)
+      return false;
+    if (!ensure_stack(3 * sizeof(CrowdState))) return false;
+  }
   return M.state_bytes == (int)sizeof(typename Model::State);
 }
 
@@ -632,7 +651,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_search_args, m),
                        (int32_t)offsetof(vp_model, mars_gpow),
                        (int32_t)offsetof(vp_tree, cdf_tag),
-                       (int32_t)offsetof(vp_model, nav_log_miss)};
+                       (int32_t)offsetof(vp_model, nav_log_miss), (int32_t)offsetof(vp_model, crowd_heur),
+                       (int32_t)sizeof(CrowdState)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];

@@ -380,4 +380,107 @@ struct NavigationModel {
   }
 };
 
+// ------------------------------------------------------------------ CROWDNAV
+// 2704-byte record (crowdnav.py:33-52): robot, tracked distances at the last
+// step, the emitted code, terminal flag, tracked person ids, curious bits and
+// float32 person positions (x, y interleaved).  A row's record is far larger
+// than a register file slice, so the planner keeps it in local memory (L1/L2)
+// and the step streams over the people once.
+constexpr int kCrowdPeople = 320;
+constexpr int kCrowdTracked = 8;
+
+struct __align__(8) CrowdState {
+  double rx, ry;
+  double prev[kCrowdTracked];
+  int32_t last_code;
+  uint32_t term;
+  uint16_t tracked[kCrowdTracked];
+  uint32_t curious[kCrowdPeople / 32];
+  float px[2 * kCrowdPeople];
+};
+
+struct CrowdNavModel {
+  typedef CrowdState State;
+
+  // j-th of the row's Box-Muller normals from precomputed row bases (rng.py:81-89)
+  static __device__ __forceinline__ double normal_at(u64 b1, u64 b2, u64 j) {
+    const u64 h1 = mix64(b1 + j * kMixB), h2 = mix64(b2 + j * kMixB);
+    const double u1 = ((double)(h1 >> 11) + 1.0) * kInv53;
+    const double u2 = (double)(h2 >> 11) * kInv53;
+    return sqrt(-2.0 * log(u1)) * cos(kTwoPi * u2);
+  }
+  static __device__ __forceinline__ double clamp(double v, double hi) { return fmin(fmax(v, 0.0), hi); }
+  static __device__ __forceinline__ double dist(float x, float y, double rx, double ry) {
+    const double dx = (double)x - rx, dy = (double)y - ry;
+    return sqrt(dx * dx + dy * dy);
+  }
+
+  // crowdnav.py:116-174, every operation in numpy's order and precision
+  // (float64 motion, float32 storage; no FMA contraction, see Makefile)
+  static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row, u32& obs,
+                                              double& rew) {
+    if (s.term) {  // absorbing: state, distances and code stay
+      obs = (u32)M.obs_arity;
+      rew = 0.0;
+      return;
+    }
+    const bool yell = a == 4;  // N E S W YELL
+    const double ddx = a == 1 ? 1.0 : a == 3 ? -1.0 : 0.0;
+    const double ddy = a == 0 ? 1.0 : a == 2 ? -1.0 : 0.0;
+    const double ry0 = s.ry + ddy;
+    const bool entered = ry0 >= M.crowd_hall_d;
+    const double rx = clamp(s.rx + ddx, M.crowd_hall_w), ry = clamp(ry0, M.crowd_hall_d);
+    const u64 nk = fold(mkey, 0), uk = fold(mkey, 1);
+    const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
+    const double rad = M.crowd_collision;
+    bool bumped = false;
+    for (int i = 0; i < M.crowd_people; ++i) {
+      double x = (double)s.px[2 * i] + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
+      double y = (double)s.px[2 * i + 1] + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
+      const double dx = rx - x, dy = ry - y;
+      const double d = sqrt(dx * dx + dy * dy);
+      const double u = unit53(mix64(bu + (u64)(i + 1) * kMixB));
+      if (d < M.crowd_r_nearby && d > 1e-9 && u < M.crowd_react) {
+        const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
+        const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
+        const double dn = fmax(d, 1e-9);
+        x = x + speed * (dx / dn);
+        y = y + speed * (dy / dn);
+      }
+      const float fx = __double2float_rn(clamp(x, M.crowd_hall_w));
+      const float fy = __double2float_rn(clamp(y, M.crowd_hall_d));
+      s.px[2 * i] = fx;
+      s.px[2 * i + 1] = fy;
+      bumped |= dist(fx, fy, rx, ry) < rad;
+    }
+    rew = -1.0 - 25.0 * (yell ? 1.0 : 0.0) - 200.0 * (bumped ? 1.0 : 0.0) + 1000.0 * (entered ? 1.0 : 0.0);
+    u32 code = 0;
+    for (int k = 0; k < M.crowd_tracked; ++k) {
+      const int t = s.tracked[k];
+      const double td = dist(s.px[2 * t], s.px[2 * t + 1], rx, ry);
+      code |= (u32)(td < s.prev[k]) << k;
+      s.prev[k] = td;
+    }
+    s.rx = rx;
+    s.ry = ry;
+    s.last_code = (int32_t)code;
+    s.term = entered ? 1u : 0u;
+    obs = entered ? (u32)M.obs_arity : code;
+  }
+
+  // table of 1000 g^k - (1 - g^k) / (1 - g), k = max(ceil(depth - y) - 1, 0) (crowdnav.py:191-197)
+  static __device__ __forceinline__ double heuristic(const vp_model& M, const State& s) {
+    if (s.term) return 0.0;
+    int k = (int)fmax(ceil(M.crowd_hall_d - s.ry) - 1.0, 0.0);
+    k = k < M.crowd_heur_len ? k : M.crowd_heur_len - 1;
+    return M.crowd_heur[k];
+  }
+
+  // deterministic observation: the code the state emitted (crowdnav.py:176-189)
+  static __device__ __forceinline__ double obs_loglik(const vp_model& M, const State& s, int, u32 obs) {
+    if (obs == (u32)M.obs_arity) return s.term ? 0.0 : -INFINITY;
+    return (!s.term && (u32)s.last_code == obs) ? 0.0 : -INFINITY;
+  }
+};
+
 }  // namespace vp

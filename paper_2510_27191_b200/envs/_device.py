@@ -9,6 +9,9 @@ A ``DeviceModel`` binds one ProblemModel instance to:
     TABULAR     8 B  {i32 state index; i32 terminal}
     SYNTHETIC  16 B  {u64 word; u32 terminal; u32 pad}
     LIGHTDARK  24 B  {f64 x; f64 y; u32 terminal; u32 pad}
+    NAVIGATION 24 B  {u64 occ[2]; i32 cell; u8 gate; u8 terminal; u16 pad}
+    CROWDNAV 2704 B  {f64 robot[2]; f64 prev[8]; i32 code; u32 terminal; u16 tracked[8];
+                      u32 curious bits[10]; f32 persons[320][2]}
 
 Models are recognised either by a ``device_descriptor()`` method or, for
 objects of the reference package (vecpomdp.envs.MarsModel / TabularModel),
@@ -33,6 +36,8 @@ SYN_DTYPE = np.dtype([("word", "<u8"), ("term", "<u4"), ("pad", "<u4")])
 LD_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("term", "<u4"), ("pad", "<u4")])
 NAV_DTYPE = np.dtype([("occ0", "<u8"), ("occ1", "<u8"), ("pos", "<i4"), ("gate", "u1"), ("term", "u1"),
                       ("pad", "<u2")])
+CROWD_DTYPE = np.dtype([("robot", "<f8", (2,)), ("prev", "<f8", (8,)), ("code", "<i4"), ("term", "<u4"),
+                        ("tracked", "<u2", (8,)), ("curious", "<u4", (10,)), ("persons", "<f4", (640,))])
 
 
 def _torch():
@@ -291,12 +296,72 @@ def navigation_descriptor(model, unpack=None) -> DeviceModel:
     return dm
 
 
+# ------------------------------------------------------------------ CROWDNAV
+
+
+def crowd_pack(states) -> np.ndarray:
+    persons = np.asarray(states.persons, dtype=np.float32)
+    n, p = persons.shape[:2]
+    k = np.asarray(states.tracked).shape[1]
+    if p > _lib.CROWD_MAX_PEOPLE or k > _lib.CROWD_MAX_TRACKED:
+        raise ValueError(f"CrowdNav device records hold at most {_lib.CROWD_MAX_PEOPLE} people and "
+                         f"{_lib.CROWD_MAX_TRACKED} tracked persons")
+    rec = np.zeros(n, dtype=CROWD_DTYPE)
+    rec["robot"] = np.asarray(states.robot, dtype=np.float64)
+    rec["prev"][:, :k] = np.asarray(states.prev_dist, dtype=np.float64)
+    rec["code"] = np.asarray(states.last_code)
+    rec["term"] = np.asarray(states.terminal, dtype=bool)
+    rec["tracked"][:, :k] = np.asarray(states.tracked)
+    cur = np.pad(np.asarray(states.curious, dtype=bool), ((0, 0), (0, _lib.CROWD_MAX_PEOPLE - p)))
+    rec["curious"] = np.packbits(cur, axis=1, bitorder="little").view("<u4")
+    rec["persons"][:, : 2 * p] = persons.reshape(n, 2 * p)
+    return rec
+
+
+def crowd_unpacker(n_people: int, n_tracked: int, states_cls):
+    def unpack(rec):
+        n = len(rec)
+        bits = np.ascontiguousarray(rec["curious"]).view(np.uint8)
+        curious = np.unpackbits(bits, axis=1, bitorder="little")[:, :n_people].astype(bool)
+        persons = np.ascontiguousarray(rec["persons"][:, : 2 * n_people]).reshape(n, n_people, 2)
+        return states_cls(np.array(rec["robot"]), persons, curious, rec["tracked"][:, :n_tracked].astype(np.int64),
+                          np.array(rec["prev"][:, :n_tracked]), rec["code"].astype(np.int64), rec["term"].astype(bool))
+    return unpack
+
+
+def crowdnav_descriptor(model, unpack=None) -> DeviceModel:
+    """vp_model for a CrowdNavModel (reference envs/crowdnav.py:54-91 attributes)."""
+    if model.n_people > _lib.CROWD_MAX_PEOPLE or model.n_tracked > _lib.CROWD_MAX_TRACKED:
+        raise ValueError(f"CrowdNav device records hold at most {_lib.CROWD_MAX_PEOPLE} people and "
+                         f"{_lib.CROWD_MAX_TRACKED} tracked persons")
+    if unpack is None:  # a reference model object: rebuild records as the product's CrowdStates
+        from .crowdnav import CrowdStates
+
+        unpack = crowd_unpacker(int(model.n_people), int(model.n_tracked), CrowdStates)
+    dm = DeviceModel(_lib.VP_MODEL_CROWDNAV, model.spec, CROWD_DTYPE, crowd_pack, unpack)
+    d = dm.desc
+    hall = np.asarray(model.hall, dtype=np.float64)
+    d.crowd_people, d.crowd_tracked = int(model.n_people), int(model.n_tracked)
+    d.crowd_hall_w, d.crowd_hall_d = float(hall[0]), float(hall[1])
+    d.crowd_noise, d.crowd_react, d.crowd_r_nearby = (float(model.motion_noise), float(model.react_prob),
+                                                      float(model.r_nearby))
+    d.crowd_v_curious, d.crowd_v_shy, d.crowd_v_back = float(model.v_curious), float(model.v_shy), float(model.v_back)
+    d.crowd_collision = float(model.collision_radius)
+    # heuristic per remaining-row count with the reference's own numpy arithmetic (bit-exact)
+    g = model.spec.discount
+    decay = g ** np.arange(int(np.ceil(hall[1])) + 1, dtype=np.float64)
+    heur = 1000.0 * decay - (1.0 - decay) / (1.0 - g)
+    d.crowd_heur, d.crowd_heur_len = dm.upload(heur), len(heur)
+    return dm
+
+
 _BY_NAME = {
     "MarsModel": mars_descriptor,
     "TabularModel": tabular_descriptor,
     "SyntheticModel": synthetic_descriptor,
     "LightDarkModel": lightdark_descriptor,
     "NavigationModel": navigation_descriptor,
+    "CrowdNavModel": crowdnav_descriptor,
 }
 _CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 

@@ -1,6 +1,7 @@
 """Generate golden vectors from the REAL reference (run in the build container).
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py            # everything
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py crowdnav   # only the CrowdNav cases
 
 Imports ``vecpomdp`` from /root/reference/pkg/src (read-only, never copied)
 and writes small ``.npz`` fixtures next to this script.  The GPU box has no
@@ -31,6 +32,7 @@ sys.path.insert(0, REPO)
 import vecpomdp as ref  # noqa: E402
 from vecpomdp.envs import MarsModel, tiger_model  # noqa: E402
 from vecpomdp.envs.navigation import NavigationModel  # noqa: E402
+from vecpomdp.envs.crowdnav import CrowdNavModel  # noqa: E402
 
 import oracle  # noqa: E402  (only for the two NEW models the reference lacks)
 
@@ -110,6 +112,8 @@ def make_model(kind: str, seed: int):
         return oracle.LightDarkModel()
     if kind == "navigation":
         return NavigationModel()
+    if kind.startswith("crowdnav"):
+        return CrowdNavModel(n_people=int(kind[8:] or 300))
     raise ValueError(kind)
 
 
@@ -123,16 +127,20 @@ PLAN_CASES = [
     ("plan_lightdark", "lightdark", 128, 5, [0, 1], True),
     ("plan_navigation", "navigation", 256, 6, [0, 1], True),
 ]
+CROWD_PLAN_CASES = [
+    ("plan_crowdnav40", "crowdnav40", 128, 5, [0, 1], True),
+    ("plan_crowdnav", "crowdnav", 64, 3, [0], True),
+]
 
 
-def gen_plans():
+def gen_plans(cases=PLAN_CASES + CROWD_PLAN_CASES, particles=2000):
     manifest = {}
-    for name, kind, n_par, iters, seeds, full in PLAN_CASES:
+    for name, kind, n_par, iters, seeds, full in cases:
         arrays = {}
         meta = []
         for s in seeds:
             model = make_model(kind, s)
-            belief = ref.ParticleBelief.from_model(model, 2000, ref.RowRng.from_seed(s).derive(3))
+            belief = ref.ParticleBelief.from_model(model, particles, ref.RowRng.from_seed(s).derive(3))
             cfg = ref.SolverConfig(n_parallel=n_par, iterations=iters, eta=2.0)
             out = ref.plan(belief, model, cfg, ref.RowRng.from_seed(s).derive(1, 0))
             for k, v in tree_arrays(out.tree, full).items():
@@ -140,7 +148,7 @@ def gen_plans():
             meta.append({"seed": s, "chosen_action": out.chosen_action, "iterations_run": out.iterations_run,
                          "final_d_max": out.final_d_max, "tree_stats": out.tree_stats})
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
-        manifest[name] = {"kind": kind, "n_parallel": n_par, "iterations": iters, "particles": 2000,
+        manifest[name] = {"kind": kind, "n_parallel": n_par, "iterations": iters, "particles": particles,
                           "eta": 2.0, "runs": meta}
     return manifest
 
@@ -187,11 +195,64 @@ def gen_navigation_steps():
     np.savez_compressed(os.path.join(HERE, "nav_steps.npz"), **out)
 
 
+def gen_crowd_episodes():
+    """Closed-loop CrowdNav episodes (reference run_episode with its refresh / reconcile hooks)."""
+    cfg = ref.SolverConfig(n_parallel=128, iterations=4, particles=300)
+    recs = []
+    for s in range(2):
+        rec = ref.run_episode(CrowdNavModel(n_people=40, hall_depth=8.0, max_steps=15), cfg, seed=s)
+        recs.append({"seed": s, "return": rec.discounted_return, "steps": rec.steps, "reason": rec.terminal_reason,
+                     "degenerate": rec.degenerate_updates, "counters": rec.counters})
+    return recs
+
+
+CROWD_FIELDS = ("robot", "persons", "curious", "tracked", "prev_dist", "last_code", "terminal")
+
+
+def gen_crowd_steps():
+    """CrowdNav vectors (crowdnav.py:98-224): 6 steps of 96 rows with 40 people (every
+    field after every step except the people, kept at the start and the end) and 3
+    steps of 8 rows at the default 300 people; likelihoods, heuristics, refresh."""
+    out = {}
+    for tag, people, n, steps in (("p40", 40, 96, 6), ("p300", 300, 8, 3)):
+        model = CrowdNavModel(n_people=people)
+        st = model.sample_initial_states(n, ref.RowRng.from_seed(31))
+        for f in CROWD_FIELDS:
+            out[f"{tag}_{f}0"] = getattr(st, f)
+        for t in range(steps):
+            a = (ref.RowRng.from_seed(32 + t).uniform(np.arange(n)) * 5).astype(np.int64)
+            a[: n // 4] = 0  # a quarter of the rows walk north
+            res = model.step_batch(st, a, ref.RowRng.from_seed(50 + t).bind(np.arange(n)))
+            out[f"{tag}_a{t}"] = a
+            for f in ("robot", "prev_dist", "last_code", "terminal"):
+                out[f"{tag}_{f}{t + 1}"] = getattr(res.next_states, f)
+            out[f"{tag}_obs{t + 1}"], out[f"{tag}_rew{t + 1}"] = res.observations, res.rewards
+            o = int(res.observations[1])
+            out[f"{tag}_ll{t + 1}"] = model.observation_log_likelihood(res.next_states, int(a[1]), o)
+            out[f"{tag}_llobs{t + 1}"] = np.array([int(a[1]), o])
+            out[f"{tag}_h{t + 1}"] = model.value_heuristic(res.next_states)
+            st = res.next_states
+        out[f"{tag}_persons_end"] = st.persons
+        ref_st = model.refresh_executed(st.take([2]))
+        out[f"{tag}_refresh_tracked"], out[f"{tag}_refresh_prev"] = ref_st.tracked, ref_st.prev_dist
+    np.savez_compressed(os.path.join(HERE, "crowd_steps.npz"), **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["crowdnav"]:
+        gen_crowd_steps()
+        with open(os.path.join(HERE, "manifest.json")) as f:
+            manifest = json.load(f)
+        manifest["plans"].update(gen_plans(CROWD_PLAN_CASES))
+        manifest["episodes"]["episode_crowdnav40"] = gen_crowd_episodes()
+        with open(os.path.join(HERE, "manifest.json"), "w") as f:
+            json.dump(manifest, f, indent=1, sort_keys=True)
+        sys.exit(0)
+    gen_crowd_steps()
     gen_navigation_steps()
     gen_rng()
     gen_formulas()
-    manifest = {"plans": gen_plans(), "episodes": gen_episodes(),
+    manifest = {"plans": gen_plans(), "episodes": dict(gen_episodes(), episode_crowdnav40=gen_crowd_episodes()),
                 "numpy": np.__version__, "reference": "/root/reference/pkg/src/vecpomdp @ 0.1.0"}
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump(manifest, f, indent=1, sort_keys=True)

@@ -41,7 +41,13 @@ def oracle_model(kind: str, seed: int):
         return oracle.LightDarkModel()
     if kind == "navigation":
         return oracle.NavigationModel()
+    if kind.startswith("crowdnav"):
+        return oracle.CrowdNavModel(n_people=int(kind[8:] or 300))
     raise ValueError(kind)
+
+
+CROWD_CASES = (("p40", 40, 96, 6), ("p300", 300, 8, 3))  # tag, people, rows, steps (make_golden.py)
+CROWD_FIELDS = ("robot", "persons", "curious", "tracked", "prev_dist", "last_code", "terminal")
 
 
 def plan_inputs(case: dict, seed: int, model=None):

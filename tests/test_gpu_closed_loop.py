@@ -30,6 +30,18 @@ def test_fp64_exact_episodes_equal_reference():
         assert abs(got.discounted_return - r["return"]) < 1e-9
 
 
+def test_fp64_exact_crowdnav_episodes_equal_reference():
+    """CrowdNav closed loop: device planner, device env step and host SIR behind the
+    model's refresh / reconcile hooks reproduce the reference's episodes."""
+    cfg = vp.SolverConfig(n_parallel=128, iterations=4, particles=300)
+    for r in manifest()["episodes"]["episode_crowdnav40"]:
+        model = vp.CrowdNavModel(n_people=40, hall_depth=8.0, max_steps=15)
+        got = vp.run_episode(model, cfg, seed=r["seed"], precision="fp64", exact=True)
+        assert (got.steps, got.terminal_reason, got.degenerate_updates) == (r["steps"], r["reason"], r["degenerate"])
+        assert abs(got.discounted_return - r["return"]) < 1e-9
+        assert got.counters == pytest.approx(r["counters"])
+
+
 def test_fp32_campaign_returns_match_reference():
     recs = manifest()["episodes"]["episode_mars5_4_campaign"]
     cfg = vp.SolverConfig(n_parallel=256, iterations=5, particles=1000)

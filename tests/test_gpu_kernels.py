@@ -56,6 +56,13 @@ def _random_states(model, kind, n, rng):
         st.pos = free[rng.integers(0, len(free), size=n)]
         st.terminal = rng.random(n) < 0.05
         return st
+    if kind == "crowdnav":
+        st = model.sample_initial_states(n, oracle.RowRng.from_seed(7))
+        # robots anywhere in the hall (some a step from the exit), so reactions, bumps and exits all occur
+        st.robot = rng.uniform(0.0, 1.0, size=(n, 2)) * model.hall
+        st.robot[: n // 8, 1] = model.hall[1] - rng.uniform(0.0, 1.5, size=n // 8)
+        st.terminal = rng.random(n) < 0.05
+        return st
     st = model.sample_initial_states(n, oracle.RowRng.from_seed(7))
     st.x = st.x + rng.normal(size=n) * 4
     st.y = st.y + rng.normal(size=n) * 4
@@ -70,14 +77,18 @@ MODELS = [
     ("synthetic", lambda: (oracle.SyntheticModel(seed=3), vp.SyntheticModel(seed=3))),
     ("lightdark", lambda: (oracle.LightDarkModel(), vp.LightDarkModel())),
     ("navigation", lambda: (oracle.NavigationModel(), vp.NavigationModel())),
+    ("crowdnav", lambda: (oracle.CrowdNavModel(), vp.CrowdNavModel())),
+    ("crowdnav", lambda: (oracle.CrowdNavModel(n_people=17, n_tracked=8, p_curious=0.3),
+                          vp.CrowdNavModel(n_people=17, n_tracked=8, p_curious=0.3))),
 ]
+CROWD_FIELDS = ("robot", "persons", "curious", "tracked", "prev_dist", "last_code")
 
 
 @pytest.mark.parametrize("kind,make", MODELS)
 def test_device_model_step_matches_oracle(kind, make):
     om, dm = make()
     rng = np.random.default_rng(11)
-    n = 4096
+    n = 1024 if kind == "crowdnav" else 4096
     st = _random_states(om, kind, n, rng)
     acts = rng.integers(0, om.spec.action_count, size=n)
     key = oracle.RowRng.from_seed(5).derive(2, 1)
@@ -87,12 +98,29 @@ def test_device_model_step_matches_oracle(kind, make):
     np.testing.assert_array_equal(got.observations, want.observations)
     np.testing.assert_array_equal(got.rewards, want.rewards)
     np.testing.assert_array_equal(got.next_states.terminal, want.next_states.terminal)
-    for f in ("x", "y", "rocks", "idx", "word", "pos", "occ", "open_gate"):
+    for f in ("x", "y", "rocks", "idx", "word", "pos", "occ", "open_gate") + CROWD_FIELDS:
         if hasattr(want.next_states, f):
             np.testing.assert_array_equal(getattr(got.next_states, f), getattr(want.next_states, f), err_msg=f)
     h_want = om.value_heuristic(want.next_states)
     h_got = dm.value_heuristic(want.next_states)
     np.testing.assert_allclose(h_got, h_want, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("tag,people,n,steps", [("p40", 40, 96, 6), ("p300", 300, 8, 3)])
+def test_device_crowdnav_steps_equal_reference_golden(tag, people, n, steps):
+    """The device CrowdNav step against vectors made by the REAL reference (crowdnav.py:116-197)."""
+    g = load("crowd_steps")
+    m = vp.CrowdNavModel(n_people=people)
+    st = m.sample_initial_states(n, vp.RowRng.from_seed(31))
+    for t in range(steps):
+        res = m.step_batch(st, g[f"{tag}_a{t}"], vp.RowRng.from_seed(50 + t).bind(np.arange(n)))
+        for f in ("robot", "prev_dist", "last_code", "terminal"):
+            np.testing.assert_array_equal(getattr(res.next_states, f), g[f"{tag}_{f}{t + 1}"], err_msg=f)
+        np.testing.assert_array_equal(res.observations, g[f"{tag}_obs{t + 1}"])
+        np.testing.assert_array_equal(res.rewards, g[f"{tag}_rew{t + 1}"])
+        np.testing.assert_array_equal(m.value_heuristic(res.next_states), g[f"{tag}_h{t + 1}"])
+        st = res.next_states
+    np.testing.assert_array_equal(st.persons, g[f"{tag}_persons_end"])
 
 
 def test_device_lse_matches_oracle():

@@ -67,7 +67,7 @@ def _oracle_traces(case, seed):
 
 
 @pytest.mark.parametrize("name", ["plan_mars4_3", "plan_mars7_8_small", "plan_tiger", "plan_synthetic",
-                                  "plan_lightdark", "plan_navigation"])
+                                  "plan_lightdark", "plan_navigation", "plan_crowdnav40"])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_injected_streams_structure_exact_values_close(name, precision):
     case = manifest()["plans"][name]
@@ -178,7 +178,8 @@ def test_tiger_decision_quality_vs_reference_solver():
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("kind,n_par", [("mars7_8", 2048), ("mars11_11", 4096), ("tiger", 1024),
-                                        ("synthetic", 2048), ("lightdark", 1024), ("navigation", 2048)])
+                                        ("synthetic", 2048), ("lightdark", 1024), ("navigation", 2048),
+                                        ("crowdnav", 512)])
 def test_fast_sampler_draws_follow_softmax_of_tree(kind, n_par, precision):
     """In-kernel fast draws (fresh rows via the shared initial CDF, other rows
     TMA-staged) equal the inverse CDF of softmax(eta * PSI) of the tree at the
@@ -187,7 +188,8 @@ def test_fast_sampler_draws_follow_softmax_of_tree(kind, n_par, precision):
     om = {"mars7_8": lambda: oracle.MarsModel(7, 8, layout_seed=seed),
           "mars11_11": lambda: oracle.MarsModel(11, 11, layout_seed=seed),
           "tiger": oracle.tiger_model, "synthetic": lambda: oracle.SyntheticModel(seed=seed),
-          "lightdark": oracle.LightDarkModel, "navigation": oracle.NavigationModel}[kind]()
+          "lightdark": oracle.LightDarkModel, "navigation": oracle.NavigationModel,
+          "crowdnav": lambda: oracle.CrowdNavModel(n_people=60)}[kind]()
     belief = oracle.ParticleBelief.from_model(om, 2000, oracle.RowRng.from_seed(seed).derive(3))
     rng = oracle.RowRng.from_seed(seed).derive(1, 0)
     k = 5

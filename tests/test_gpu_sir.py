@@ -22,6 +22,7 @@ MODELS = {
     "synthetic": lambda: (oracle.SyntheticModel(seed=4), vp.SyntheticModel(seed=4)),
     "lightdark": lambda: (oracle.LightDarkModel(), vp.LightDarkModel()),
     "navigation": lambda: (oracle.NavigationModel(), vp.NavigationModel()),
+    "crowdnav": lambda: (oracle.CrowdNavModel(n_people=50), vp.CrowdNavModel(n_people=50)),
 }
 
 
@@ -36,7 +37,8 @@ def _scenario(kind, seed, m=3000):
 
 
 def _states_equal(x, y):
-    for f in ("x", "y", "rocks", "terminal", "idx", "word", "pos", "occ", "open_gate"):
+    for f in ("x", "y", "rocks", "terminal", "idx", "word", "pos", "occ", "open_gate", "robot", "persons", "curious",
+              "tracked", "prev_dist", "last_code"):
         if hasattr(x, f):
             np.testing.assert_array_equal(np.asarray(getattr(x, f)), np.asarray(getattr(y, f)), err_msg=f)
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
-from golden_cases import INT_COLUMNS, load, manifest, plan_inputs, tree_columns
+from golden_cases import CROWD_CASES, CROWD_FIELDS, INT_COLUMNS, load, manifest, plan_inputs, tree_columns
 
 
 def test_rng_streams_match_reference():
@@ -99,6 +99,15 @@ def test_oracle_episode_matches_reference():
         assert got.discounted_return == r["return"]
 
 
+def test_oracle_crowdnav_episodes_match_reference():
+    """Closed loop with CrowdNav's refresh / reconcile hooks (crowdnav.py:199-224)."""
+    cfg = oracle.SolverConfig(n_parallel=128, iterations=4, particles=300)
+    for r in manifest()["episodes"]["episode_crowdnav40"]:
+        got = oracle.run_episode(oracle.CrowdNavModel(n_people=40, hall_depth=8.0, max_steps=15), cfg, seed=r["seed"])
+        assert (got.steps, got.terminal_reason, got.degenerate_updates) == (r["steps"], r["reason"], r["degenerate"])
+        assert got.discounted_return == r["return"]
+
+
 def test_navigation_model_vectors():
     """oracle.NavigationModel vs the reference's navigation.py (steps, likelihoods, heuristic)."""
     g = load("nav_steps")
@@ -117,3 +126,28 @@ def test_navigation_model_vectors():
         np.testing.assert_array_equal(m.observation_log_likelihood(res.next_states, a, o), g[f"ll{t + 1}"])
         np.testing.assert_array_equal(m.value_heuristic(res.next_states), g[f"h{t + 1}"])
         st = res.next_states
+
+
+@pytest.mark.parametrize("tag,people,n,steps", CROWD_CASES)
+def test_crowdnav_model_vectors(tag, people, n, steps):
+    """oracle.CrowdNavModel vs the reference's crowdnav.py (sampler, steps, likelihoods,
+    heuristic, tracking refresh)."""
+    g = load("crowd_steps")
+    m = oracle.CrowdNavModel(n_people=people)
+    st = m.sample_initial_states(n, oracle.RowRng.from_seed(31))
+    for f in CROWD_FIELDS:
+        np.testing.assert_array_equal(getattr(st, f), g[f"{tag}_{f}0"], err_msg=f)
+    for t in range(steps):
+        res = m.step_batch(st, g[f"{tag}_a{t}"], oracle.RowRng.from_seed(50 + t).bind(np.arange(n)))
+        for f in ("robot", "prev_dist", "last_code", "terminal"):
+            np.testing.assert_array_equal(getattr(res.next_states, f), g[f"{tag}_{f}{t + 1}"], err_msg=f)
+        np.testing.assert_array_equal(res.observations, g[f"{tag}_obs{t + 1}"])
+        np.testing.assert_array_equal(res.rewards, g[f"{tag}_rew{t + 1}"])
+        a, o = (int(v) for v in g[f"{tag}_llobs{t + 1}"])
+        np.testing.assert_array_equal(m.observation_log_likelihood(res.next_states, a, o), g[f"{tag}_ll{t + 1}"])
+        np.testing.assert_array_equal(m.value_heuristic(res.next_states), g[f"{tag}_h{t + 1}"])
+        st = res.next_states
+    np.testing.assert_array_equal(st.persons, g[f"{tag}_persons_end"])
+    r = m.refresh_executed(st.take([2]))
+    np.testing.assert_array_equal(r.tracked, g[f"{tag}_refresh_tracked"])
+    np.testing.assert_array_equal(r.prev_dist, g[f"{tag}_refresh_prev"])
