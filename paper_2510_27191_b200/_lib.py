@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvpb200.so")
+LIB_PATH = os.environ.get("VPB200_LIB") or os.path.join(_HERE, "libvpb200.so")  # override: experiments only
 
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK, VP_MODEL_NAVIGATION = 1, 2, 3, 4, 5

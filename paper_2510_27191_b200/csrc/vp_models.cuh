@@ -434,6 +434,7 @@ struct CrowdNavModel {
     const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
     const double rad = M.crowd_collision;
     bool bumped = false;
+#pragma unroll 2
     for (int i = 0; i < M.crowd_people; ++i) {
       double x = (double)s.px[2 * i] + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
       double y = (double)s.px[2 * i + 1] + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
