@@ -125,12 +125,12 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
 }
 
 template <class PsiT, bool Exact>
-__global__ void __launch_bounds__(kBackupWarps * 32) k_backup(vp_tree T, vp_work W, u32 pass, double gamma) {
+__global__ void __launch_bounds__(kBackupWarps * 32) k_backup(vp_tree T, vp_work W, u32 pass, double gamma, int rpw) {
   __shared__ double s_v[kBackupWarps][32];
   const int warp = threadIdx.x >> 5;
   const int wi = blockIdx.x * kBackupWarps + warp;
-  if (wi * 32 >= W.leaf_count[pass & 1u]) return;
-  backup_warp<PsiT, Exact>(T, W, pass, gamma, wi, s_v[warp]);
+  if (wi * rpw >= W.leaf_count[pass & 1u]) return;
+  backup_warp<PsiT, Exact>(T, W, pass, gamma, wi, s_v[warp], rpw);
 }
 
 template <class PsiT>
@@ -251,6 +251,20 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// Leaves per backup warp.  The climbs of a warp's leaves are independent chains of
+// dependent L2 round trips: when the pass is small, fewer leaves per warp (more
+// warps per SM) hide more latency; when it fills the GPU anyway, full warps issue
+// fewer instructions.  Sized for ~16 warps per SM of the 148, between 8 and 32
+// (measured: C2 16k rows: 8 -> -7 % step time; C3 64k rows flat; C5 64k rows but
+// deeper trees: 32, 16 costs +8 %).
+// VP_LEAVES_PER_WARP overrides (measurement only).
+static int leaves_per_warp(int n) {
+  static const int forced = env_int("VP_LEAVES_PER_WARP", 0);
+  if (forced > 0) return std::min(32, forced);
+  const int want = (n + 148 * 16 - 1) / (148 * 16);
+  return want <= 8 ? 8 : want <= 16 ? 16 : 32;
+}
+
 // Staged-row geometry: rows padded to an odd number of 16-B chunks so the
 // LDS.128 scans of 8 lanes in different rows hit different bank groups.
 template <class PsiT>
@@ -302,10 +316,11 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
 
 template <class PsiT, bool Exact>
 static int32_t launch_backup(const vp_tree& T, const vp_work& W, u32 pass, double gamma, cudaStream_t st) {
-  const int grid = blocks_for(blocks_for(W.n, 32), kBackupWarps);
+  const int rpw = leaves_per_warp(W.n);
+  const int grid = blocks_for(blocks_for(W.n, rpw), kBackupWarps);
   {
     Launch L_(KK_BACKUP, st);
-    k_backup<PsiT, Exact><<<grid, kBackupWarps * 32, 0, st>>>(T, W, pass, gamma);
+    k_backup<PsiT, Exact><<<grid, kBackupWarps * 32, 0, st>>>(T, W, pass, gamma, rpw);
   }
   return check_launch();
 }
