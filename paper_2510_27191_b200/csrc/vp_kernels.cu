@@ -114,14 +114,20 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
     init_row[a] = a < A ? (PsiT)T.init_prefs[a] : (PsiT)0;
     if (a < A) init_cdf[a] = reinterpret_cast<const PsiT*>(T.init_cdf)[a];
   }
+  typedef typename Model::State State;
+  State* shared_state = nullptr;  // cooperative models: one record per warp, after the initial CDF
+  if constexpr (coop_trait<Model>::value) {
+    const size_t off = ((size_t)(init_cdf + A - reinterpret_cast<PsiT*>(smem_raw)) * sizeof(PsiT) + 15) / 16 * 16;
+    shared_state = reinterpret_cast<State*>(smem_raw + off) + (threadIdx.x >> 5);
+  }
   fence_async_smem();  // the initial row is the source of TMA bulk stores (lazy rows)
   // the leaf counter of the NEXT pass is reset here: its previous user (the
   // backup of the pass before this one) has finished
   if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;
   __syncthreads();
   const int wi = blockIdx.x * kSearchWarps + (threadIdx.x >> 5);
-  if (wi * 32 >= W.n) return;
-  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi);
+  if (wi * rows_per_search_warp<Model>() >= W.n) return;
+  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state);
 }
 
 template <class PsiT, bool Exact>
@@ -278,12 +284,13 @@ static StageCfg stage_cfg(int A, int per_warp_bytes) {
 }
 
 // Search launch geometry: staged rows of every warp + the block's copies of
-// the initial row and its CDF.
-template <class PsiT, bool Exact>
+// the initial row and its CDF (+ one record per warp for cooperative models).
+template <class Model, class PsiT, bool Exact>
 static int32_t search_geometry(int A, StageCfg& sc, size_t& smem) {
   sc = Exact ? StageCfg{0, 4} : stage_cfg<PsiT>(A, env_int("VP_STAGE_KB", 32) * 1024);
   const size_t padded = ((size_t)A * sizeof(PsiT) + 15) / 16 * 16 / sizeof(PsiT);
   smem = ((size_t)kSearchWarps * sc.rows * sc.stride + padded + (size_t)A) * sizeof(PsiT);
+  if (coop_trait<Model>::value) smem = (smem + 15) / 16 * 16 + kSearchWarps * sizeof(typename Model::State);
   return VP_OK;
 }
 
@@ -304,9 +311,9 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
                              cudaStream_t st) {
   StageCfg sc;
   size_t smem;
-  search_geometry<PsiT, Exact>(T.action_count, sc, smem);
+  search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
   if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
-  const int grid = blocks_for(blocks_for(W.n, 32), kSearchWarps);
+  const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>()), kSearchWarps);
   {
     Launch L_(KK_SEARCH, st);
     k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc);
@@ -406,7 +413,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   {
     StageCfg sc;
     size_t smem;
-    search_geometry<PsiT, Exact>(T.action_count, sc, smem);
+    search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
     if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);

@@ -401,6 +401,9 @@ struct __align__(8) CrowdState {
 
 struct CrowdNavModel {
   typedef CrowdState State;
+  // the planner steps a row with the whole warp (people split over the lanes),
+  // record in shared memory; step() below is the one-lane form (SIR, hooks)
+  static constexpr bool kCoop = true;
 
   // j-th of the row's Box-Muller normals from precomputed row bases (rng.py:81-89)
   static __device__ __forceinline__ double normal_at(u64 b1, u64 b2, u64 j) {
@@ -466,6 +469,70 @@ struct CrowdNavModel {
     s.ry = ry;
     s.last_code = (int32_t)code;
     s.term = entered ? 1u : 0u;
+    obs = entered ? (u32)M.obs_arity : code;
+  }
+
+  // step() with the 32 lanes of a warp on ONE row whose record s is in shared
+  // memory: lane j moves people j, j + 32, ...; the arithmetic of every person
+  // is step()'s, so the result is bit-identical.  a, row, live are warp-uniform.
+  static __device__ __forceinline__ void step_warp(const vp_model& M, State& s, int a, u64 mkey, u64 row, bool live,
+                                                   u32& obs, double& rew) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    obs = 0;
+    rew = 0.0;
+    if (!live) return;
+    if (s.term) {
+      obs = (u32)M.obs_arity;
+      return;
+    }
+    const bool yell = a == 4;
+    const double ddx = a == 1 ? 1.0 : a == 3 ? -1.0 : 0.0;
+    const double ddy = a == 0 ? 1.0 : a == 2 ? -1.0 : 0.0;
+    const double ry0 = s.ry + ddy;
+    const bool entered = ry0 >= M.crowd_hall_d;
+    const double rx = clamp(s.rx + ddx, M.crowd_hall_w), ry = clamp(ry0, M.crowd_hall_d);
+    const u64 nk = fold(mkey, 0), uk = fold(mkey, 1);
+    const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
+    bool bumped = false;
+    for (int i = lane; i < M.crowd_people; i += 32) {
+      const float2 p = reinterpret_cast<const float2*>(s.px)[i];
+      double x = (double)p.x + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
+      double y = (double)p.y + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
+      const double dx = rx - x, dy = ry - y;
+      const double d = sqrt(dx * dx + dy * dy);
+      if (d < M.crowd_r_nearby && d > 1e-9 && unit53(mix64(bu + (u64)(i + 1) * kMixB)) < M.crowd_react) {
+        const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
+        const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
+        const double dn = fmax(d, 1e-9);
+        x = x + speed * (dx / dn);
+        y = y + speed * (dy / dn);
+      }
+      const float fx = __double2float_rn(clamp(x, M.crowd_hall_w));
+      const float fy = __double2float_rn(clamp(y, M.crowd_hall_d));
+      reinterpret_cast<float2*>(s.px)[i] = make_float2(fx, fy);
+      bumped |= dist(fx, fy, rx, ry) < M.crowd_collision;
+    }
+    bumped = __any_sync(full, bumped);
+    __syncwarp();  // every person written before the tracked ones are read
+    double td = 0.0;
+    bool closer = false;
+    if (lane < M.crowd_tracked) {
+      const int t = s.tracked[lane];
+      td = dist(s.px[2 * t], s.px[2 * t + 1], rx, ry);
+      closer = td < s.prev[lane];
+    }
+    const u32 code = __ballot_sync(full, closer);
+    __syncwarp();
+    if (lane < M.crowd_tracked) s.prev[lane] = td;
+    if (lane == 0) {
+      s.rx = rx;
+      s.ry = ry;
+      s.last_code = (int32_t)code;
+      s.term = entered ? 1u : 0u;
+    }
+    __syncwarp();
+    rew = -1.0 - 25.0 * (yell ? 1.0 : 0.0) - 200.0 * (bumped ? 1.0 : 0.0) + 1000.0 * (entered ? 1.0 : 0.0);
     obs = entered ? (u32)M.obs_arity : code;
   }
 

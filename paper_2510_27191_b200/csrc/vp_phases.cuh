@@ -465,8 +465,7 @@ __device__ void block_tree_init(const vp_tree& T) {
 
 // belief.py:37-44: u = uniform(draw_key, row); first index with cum > u
 // (searchsorted side=right), clamped to m - 1.
-template <class State>
-__device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r) {
+__device__ __forceinline__ int draw_index(const double* cumw, int m, u64 key, int r) {
   const double u = uniform1(key, (u64)r);
   // weights are uniform after every SIR update (belief.py:101): the first
   // guess floor(u m) is usually the answer, confirmed with two loads
@@ -481,7 +480,52 @@ __device__ __forceinline__ State draw_state(const State* particles, const double
     }
     idx = lo < m - 1 ? lo : m - 1;
   }
-  return particles[idx];
+  return idx;
+}
+
+template <class State>
+__device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r) {
+  return particles[draw_index(cumw, m, key, r)];
+}
+
+// ------------------------------------------------------------------ cooperative models
+// A model whose record is too large for one lane (CrowdNav) declares kCoop: the
+// search then carries ONE row per warp, keeps its record in shared memory and
+// calls Model::step_warp with all 32 lanes, which split the work inside the row.
+template <class M, class = void>
+struct coop_trait : std::false_type {};
+template <class M>
+struct coop_trait<M, std::void_t<decltype(M::kCoop)>> : std::integral_constant<bool, M::kCoop> {};
+template <class Model>
+constexpr int rows_per_search_warp() { return coop_trait<Model>::value ? 1 : 32; }
+
+struct NoState {};
+template <class State>
+__device__ __forceinline__ State& state_slot(State* shared, NoState&) { return *shared; }
+template <class State>
+__device__ __forceinline__ State& state_slot(State*, State& local) { return local; }
+
+// whole-warp copy of one record (8-byte words; records are 8-byte aligned)
+template <class State>
+__device__ __forceinline__ void warp_copy_state(State& dst, const State& src) {
+  static_assert(sizeof(State) % 8 == 0, "records are whole 8-byte words");
+  u64* d = reinterpret_cast<u64*>(&dst);
+  const u64* q = reinterpret_cast<const u64*>(&src);
+  for (int i = lane_id(); i < (int)(sizeof(State) / 8); i += 32) d[i] = q[i];
+  __syncwarp();
+}
+
+// one generative step of every live row of the warp (search.py:113-115)
+template <class Model>
+__device__ __forceinline__ void model_step(const vp_model& M, typename Model::State& st, int a, u64 key, int rg,
+                                           bool live, u32& o, double& rw) {
+  if constexpr (coop_trait<Model>::value) {
+    // the row is lane 0's; every lane takes part
+    Model::step_warp(M, st, __shfl_sync(FULL, a, 0), key, (u64)__shfl_sync(FULL, rg, 0),
+                     __shfl_sync(FULL, (int)live, 0) != 0, o, rw);
+  } else if (live) {
+    Model::step(M, st, a, key, (u64)rg, o, rw);
+  }
 }
 
 // ------------------------------------------------------------------ search
@@ -630,9 +674,8 @@ __device__ __forceinline__ int find_key(const Slot* tab, u64 mask, u64 key) {
 template <class Model, class PsiT, bool Exact>
 __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                                 Stage<PsiT>& sg, const PsiT* init_cdf, typename Model::State& st, int r, int rg,
-                                u64 skey) {
+                                bool active, u64 skey) {
   const int n = W.n;
-  const bool active = r < n;
   const Slot* ha = slots(T.hash_a);
   const Slot* hb = slots(T.hash_b);
   int b = 0, pend = -1, pend_b = 0;
@@ -644,8 +687,8 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u, S.pass, pend, pend_b);
     u32 o = 0;
     double rw = 0.0;
+    model_step<Model>(M, st, a, fold(lkey, 1), rg, active, o, rw);
     if (active) {
-      Model::step(M, st, a, fold(lkey, 1), (u64)rg, o, rw);
       const size_t t = (size_t)l * n + r;
       W.trace_action[t] = a;
       W.trace_obs[t] = o;
@@ -668,13 +711,16 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
 // The search kernel body for one warp = 32 consecutive rows.
 template <class Model, class PsiT, bool Exact>
 __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
-                            Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index) {
+                            Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index,
+                            typename Model::State* shared_state) {
   typedef typename Model::State State;
+  constexpr bool kCoop = coop_trait<Model>::value;
+  constexpr int kRows = rows_per_search_warp<Model>();
   const int n = W.n, lane = lane_id();
   // 32 rows per warp: rows of a warp at the same belief share one draw (match_any
   // groups), which pays more than the latency hiding of more, emptier warps
-  // (16 rows per warp: +27 % search time at C2)
-  const int r = warp_index * 32 + lane;
+  // (16 rows per warp: +27 % search time at C2).  Cooperative models: one row.
+  const int r = lane < kRows ? warp_index * kRows + lane : n;
   const int rg = S.row0 + r;  // global row id: RNG streams and creation keys
   const bool active = r < n;
   const bool insert = S.mode == VP_SEARCH_INSERT;
@@ -685,8 +731,21 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   Slot* hb = slots(T.hash_b);
   int* leaf_count = W.leaf_count + (pass & 1u);
 
-  State st{};
-  if (active && !insert) {
+  typename std::conditional<kCoop, NoState, State>::type own{};
+  State& st = state_slot<State>(shared_state, own);
+  if constexpr (kCoop) {
+    if (!insert) {  // lane 0 picks the record, the warp copies it into shared memory
+      const State* src = nullptr;
+      if (active) {
+        const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
+        src = S.particles ? reinterpret_cast<const State*>(S.particles) +
+                                draw_index(S.cum_weights, S.m, dkey, rg)
+                          : reinterpret_cast<const State*>(W.states) + r;
+      }
+      src = reinterpret_cast<const State*>(__shfl_sync(FULL, (unsigned long long)src, 0));
+      if (src) warp_copy_state(st, *src);
+    }
+  } else if (active && !insert) {
     if (S.particles) {
       const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
       st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, rg);
@@ -695,7 +754,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     }
   }
   if (S.mode == VP_SEARCH_TRAJECTORY) {
-    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, st, r, rg, skey);
+    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, st, r, rg, active, skey);
     return;
   }
   int b = active ? (S.start_beliefs ? S.start_beliefs[r] : 0) : 0;
@@ -749,8 +808,8 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         o = S.inject_obs[(size_t)l * n + r];
         rw = S.inject_reward[(size_t)l * n + r];
       }
-    } else if (ok) {
-      Model::step(M, st, a, fold(lkey, 1), (u64)rg, o, rw);  // level_rng.derive(1)
+    } else {
+      model_step<Model>(M, st, a, fold(lkey, 1), rg, ok, o, rw);  // level_rng.derive(1)
     }
 
     // ---- action node (b, a): append_actions (tree.py:180-218)
