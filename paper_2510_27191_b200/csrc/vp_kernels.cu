@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
   if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;
   __syncthreads();
   const int wi = blockIdx.x * kSearchWarps + (threadIdx.x >> 5);
-  if (wi * rows_per_search_warp<Model>() >= W.n) return;
+  if (wi * rows_per_search_warp<Model>(S.mode) >= W.n) return;
   search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state);
 }
 
@@ -313,7 +313,7 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
   size_t smem;
   search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
   if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
-  const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>()), kSearchWarps);
+  const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>(S.mode)), kSearchWarps);
   {
     Launch L_(KK_SEARCH, st);
     k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc);

@@ -495,23 +495,34 @@ struct CrowdNavModel {
     const u64 nk = fold(mkey, 0), uk = fold(mkey, 1);
     const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
     bool bumped = false;
+    // squared-distance gates: sqrt is correctly rounded and monotone, so d < r can only
+    // hold when s < r^2 (1 + 1e-12); outside the gate the reference's comparisons are
+    // false and no sqrt is taken
+    const double near2 = M.crowd_r_nearby * M.crowd_r_nearby * (1.0 + 1e-12);
+    const double bump2 = M.crowd_collision * M.crowd_collision * (1.0 + 1e-12);
     for (int i = lane; i < M.crowd_people; i += 32) {
       const float2 p = reinterpret_cast<const float2*>(s.px)[i];
       double x = (double)p.x + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
       double y = (double)p.y + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
       const double dx = rx - x, dy = ry - y;
-      const double d = sqrt(dx * dx + dy * dy);
-      if (d < M.crowd_r_nearby && d > 1e-9 && unit53(mix64(bu + (u64)(i + 1) * kMixB)) < M.crowd_react) {
-        const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
-        const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
-        const double dn = fmax(d, 1e-9);
-        x = x + speed * (dx / dn);
-        y = y + speed * (dy / dn);
+      const double s2 = dx * dx + dy * dy;
+      if (s2 < near2) {
+        const double d = sqrt(s2);
+        // the react draw only matters when both distance tests pass (pure function of row, i)
+        if (d < M.crowd_r_nearby && d > 1e-9 && unit53(mix64(bu + (u64)(i + 1) * kMixB)) < M.crowd_react) {
+          const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
+          const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
+          const double dn = fmax(d, 1e-9);
+          x = x + speed * (dx / dn);
+          y = y + speed * (dy / dn);
+        }
       }
       const float fx = __double2float_rn(clamp(x, M.crowd_hall_w));
       const float fy = __double2float_rn(clamp(y, M.crowd_hall_d));
       reinterpret_cast<float2*>(s.px)[i] = make_float2(fx, fy);
-      bumped |= dist(fx, fy, rx, ry) < M.crowd_collision;
+      const double ex = (double)fx - rx, ey = (double)fy - ry;
+      const double e2 = ex * ex + ey * ey;
+      bumped |= e2 < bump2 && sqrt(e2) < M.crowd_collision;
     }
     bumped = __any_sync(full, bumped);
     __syncwarp();  // every person written before the tracked ones are read

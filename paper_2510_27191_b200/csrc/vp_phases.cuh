@@ -496,8 +496,11 @@ template <class M, class = void>
 struct coop_trait : std::false_type {};
 template <class M>
 struct coop_trait<M, std::void_t<decltype(M::kCoop)>> : std::integral_constant<bool, M::kCoop> {};
+// (insert replays recorded trajectories without stepping the model: full warps)
 template <class Model>
-constexpr int rows_per_search_warp() { return coop_trait<Model>::value ? 1 : 32; }
+__host__ __device__ constexpr int rows_per_search_warp(int mode) {
+  return coop_trait<Model>::value && mode != VP_SEARCH_INSERT ? 1 : 32;
+}
 
 struct NoState {};
 template <class State>
@@ -715,7 +718,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
                             typename Model::State* shared_state) {
   typedef typename Model::State State;
   constexpr bool kCoop = coop_trait<Model>::value;
-  constexpr int kRows = rows_per_search_warp<Model>();
+  const int kRows = rows_per_search_warp<Model>(S.mode);
   const int n = W.n, lane = lane_id();
   // 32 rows per warp: rows of a warp at the same belief share one draw (match_any
   // groups), which pays more than the latency hiding of more, emptier warps

@@ -16,11 +16,11 @@ ap.add_argument("--m", type=int, default=11)
 ap.add_argument("--n-parallel", type=int, default=16384)
 ap.add_argument("--iterations", type=int, default=10)
 ap.add_argument("--precision", default="fp32")
-ap.add_argument("--problem", default="mars", choices=["mars", "synthetic", "lightdark"])
+ap.add_argument("--problem", default="mars", choices=["mars", "synthetic", "lightdark", "crowdnav"])
 a = ap.parse_args()
 model = {"mars": lambda: vp.MarsModel(a.n, a.m, layout_seed=1000),
          "synthetic": lambda: vp.SyntheticModel(n_actions=16, n_obs=8, seed=1000),
-         "lightdark": vp.LightDarkModel}[a.problem]()
+         "lightdark": vp.LightDarkModel, "crowdnav": vp.CrowdNavModel}[a.problem]()
 belief = vp.ParticleBelief.from_model(model, 10_000, vp.RowRng.from_seed(1000).derive(3))
 cfg = vp.SolverConfig(n_parallel=a.n_parallel, iterations=a.iterations)
 for t in range(a.steps):
