@@ -51,12 +51,14 @@ def _torch():
 class DeviceModel:
     """Descriptor + packer for one model instance."""
 
-    def __init__(self, kind: int, spec, state_dtype: np.dtype, pack, unpack=None):
+    def __init__(self, kind: int, spec, state_dtype: np.dtype, pack, unpack=None, pack_into=None):
         self.kind = kind
         self.spec = spec
         self.state_dtype = state_dtype
         self._pack = pack
+        self._pack_into = pack_into
         self._unpack = unpack
+        self.init_prefs_cache = {}  # eta -> initial PSI row (solver.initial_prefs)
         self.desc = _lib.VpModel()
         self.desc.kind = kind
         self.desc.action_count = spec.action_count
@@ -77,6 +79,15 @@ class DeviceModel:
 
     def pack(self, states) -> np.ndarray:
         return self._pack(states)
+
+    def pack_into(self, states, dst: np.ndarray) -> int:
+        """Pack ``states`` straight into the byte buffer ``dst`` (e.g. pinned host memory);
+        returns the bytes written."""
+        if self._pack_into is not None:
+            return self._pack_into(states, dst)
+        rec = self._pack(states)
+        dst[: rec.nbytes] = rec.view(np.uint8).reshape(-1)
+        return rec.nbytes
 
     def unpack(self, records: np.ndarray):
         if self._unpack is None:
@@ -132,26 +143,41 @@ def _rock_bits(rocks: np.ndarray) -> np.ndarray:
         np.zeros(len(r), dtype=np.uint64)
 
 
-def mars_pack(states) -> np.ndarray:
-    """MarsStates -> 16-B records, written as raw bytes (this runs on the host inside every
-    e2e planning step, so it avoids per-field structured assignment)."""
+def mars_pack_into(states, dst: np.ndarray) -> int:
+    """MarsStates -> 16-B records written into the byte buffer ``dst`` as two little-endian
+    words {x0 | y0 << 8 | x1 << 16 | y1 << 24 | terminal << 32, rock bits}.  This runs on the
+    host inside every e2e planning step, so it uses whole-vector integer ops on contiguous
+    columns (no strided byte stores, no per-row bit packing)."""
     x = np.asarray(states.x)
     y = np.asarray(states.y)
     n = len(x)
-    out = np.zeros((n, 16), dtype=np.uint8)
-    xy = out[:, :4].reshape(n, 2, 2)
-    xy[:, :, 0] = x
-    xy[:, :, 1] = y
-    out[:, 4] = np.asarray(states.terminal, dtype=bool)
+    out = dst[: 16 * n].view(np.uint64).reshape(n, 2)
+    t = np.left_shift(y, 8, dtype=np.int64)
+    t |= x
+    w0 = t[:, 1] << 16
+    w0 |= t[:, 0]
+    w0 |= np.asarray(states.terminal).astype(np.int64) << 32
+    out[:, 0] = w0
     r = np.asarray(states.rocks, dtype=bool)
     m = r.shape[1]
     if m > 64:
         raise ValueError("MARS device records hold at most 64 rocks")
-    if 0 < m <= 52:  # bit weights 2^k are exact in float64: one BLAS mat-vec
-        out[:, 8:].view(np.uint64)[:, 0] = (r.astype(np.float64) @ np.exp2(np.arange(m))).astype(np.uint64)
-    elif m:
-        out[:, 8:8 + (m + 7) // 8] = np.packbits(r, axis=1, bitorder="little")
-    return out.view(MARS_DTYPE).reshape(n)
+    if m == 0:
+        out[:, 1] = 0
+    elif m <= 24:  # sums of distinct 2^k < 2^24 are exact in float32: one mat-vec
+        out[:, 1] = r.astype(np.float32) @ np.exp2(np.arange(m, dtype=np.float32))
+    elif m <= 52:
+        out[:, 1] = r.astype(np.float64) @ np.exp2(np.arange(m))
+    else:
+        out[:, 1] = np.packbits(np.pad(r, ((0, 0), (0, 64 - m))), axis=1, bitorder="little").view("<u8")[:, 0]
+    return 16 * n
+
+
+def mars_pack(states) -> np.ndarray:
+    n = len(np.asarray(states.x))
+    out = np.empty(16 * n, dtype=np.uint8)
+    mars_pack_into(states, out)
+    return out.view(MARS_DTYPE)
 
 
 def mars_descriptor(model, unpack=None) -> DeviceModel:
@@ -159,7 +185,7 @@ def mars_descriptor(model, unpack=None) -> DeviceModel:
     n, m = int(model.n), int(model.m)
     if n > 254 or m > 64:
         raise ValueError("MARS device model supports n <= 254 and m <= 64")
-    dm = DeviceModel(_lib.VP_MODEL_MARS, model.spec, MARS_DTYPE, mars_pack, unpack)
+    dm = DeviceModel(_lib.VP_MODEL_MARS, model.spec, MARS_DTYPE, mars_pack, unpack, mars_pack_into)
     d = dm.desc
     d.mars_n, d.mars_m, d.mars_ops = n, m, int(model.per_agent_ops)
     d.mars_half_eff = float(model.half_efficiency_distance)

@@ -139,7 +139,9 @@ class Planner:
         if ck not in self._cap_cache:
             self._cap_cache[ck] = self._capacity(n, config, A)
         cap, levels = self._cap_cache[ck]
-        init = initial_prefs(model, config.eta)
+        init = dm.init_prefs_cache.get(config.eta, False)
+        if init is False:  # the model's reference policy is fixed: once per (model, eta)
+            init = dm.init_prefs_cache[config.eta] = initial_prefs(model, config.eta)
         t = self.tree
         if t is None or t.action_count != A or t.precision != self.precision or t.exact != self.exact:
             t = self.tree = DeviceTree(A, init, eta=config.eta, precision=self.precision, exact=self.exact,
@@ -170,13 +172,14 @@ class Planner:
     def stage_belief(self, dm, belief):
         """Pack the particle StateBatch and its weight CDF into pinned buffers."""
         weights = np.asarray(belief.weights, dtype=np.float64)
-        rec = dm.pack(belief.states)
         m = len(weights)
-        hp = self._buf("particles_host", rec.nbytes, True)
-        hp.numpy()[: rec.nbytes] = rec.view(np.uint8).reshape(-1)
+        nbytes = m * dm.state_bytes
+        hp = self._buf("particles_host", nbytes, True)
+        if dm.pack_into(belief.states, hp.numpy()) != nbytes:
+            raise ValueError("belief states and weights differ in length")
         hc = self._buf("cumw_host", 8 * m, True)
-        hc.numpy()[: 8 * m].view(np.float64)[:] = np.cumsum(weights)  # sequential fp64 (belief.py:42)
-        self._buf("particles_dev", rec.nbytes, False)
+        np.cumsum(weights, out=hc.numpy()[: 8 * m].view(np.float64))  # sequential fp64 (belief.py:42)
+        self._buf("particles_dev", nbytes, False)
         self._buf("cumw_dev", 8 * m, False)
         return m
 
