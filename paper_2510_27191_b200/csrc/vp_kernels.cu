@@ -488,9 +488,17 @@ __global__ void k_sir_propagate(vp_model M, const typename Model::State* in, con
 
 // One block: max over finite log-weights, shifted = exp(lw - max), its numpy
 // pairwise sum, then the sequential cumsum of shifted / sum with cum[-1] = 1
-// (belief.py:91-93, 50-52) -- the serial parts by one thread, in numpy order.
+// (belief.py:91-93, 50-52).  The two serial sums run on one thread in numpy
+// order; everything else is block-parallel.  Up to kSirSmem particles the
+// values live in shared memory, so the serial chains wait on shared-memory
+// loads (fetched 8 ahead), not on L2 round trips.
+constexpr int kSirSmem = 16384;
+
 __global__ void k_sir_normalise(const double* logw, int m, double* cum, int* finite) {
+  extern __shared__ double s_w[];
   __shared__ double s_max[32];
+  __shared__ double s_total;
+  double* w = m <= kSirSmem ? s_w : cum;
   double mx = -INFINITY;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     const double v = logw[i];
@@ -510,19 +518,36 @@ __global__ void k_sir_normalise(const double* logw, int m, double* cum, int* fin
     if (threadIdx.x == 0) finite[0] = 0;
     return;
   }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) cum[i] = exp(logw[i] - mx);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] = exp(logw[i] - mx);
+  __syncthreads();
+  if (threadIdx.x == 0) s_total = pairwise_sum([&](int i) -> double { return w[i]; }, 0, m);
+  __syncthreads();
+  const double total = s_total;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] = w[i] / total;  // numpy's vectorised divide
   __syncthreads();
   if (threadIdx.x == 0) {
-    const double total = pairwise_sum([&](int i) -> double { return cum[i]; }, 0, m);
     double acc = 0.0;
-    for (int i = 0; i < m; ++i) {
-      const double wi = cum[i] / total;
-      acc = i ? acc + wi : wi;
-      cum[i] = acc;
+    int i = 0;
+    for (; i + 8 <= m; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = w[i + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        acc = (i + k) ? acc + v[k] : v[k];
+        w[i + k] = acc;
+      }
     }
-    cum[m - 1] = 1.0;
+    for (; i < m; ++i) {
+      acc = i ? acc + w[i] : w[i];
+      w[i] = acc;
+    }
     finite[0] = 1;
   }
+  __syncthreads();
+  if (w != cum)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) cum[i] = w[i];
+  if (threadIdx.x == 0) cum[m - 1] = 1.0;
 }
 
 template <class Model>
@@ -811,7 +836,18 @@ int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weig
                                                                    m, action, observation, key,
                                                                    reinterpret_cast<State*>(states_out), logw);
     }
-    { Launch L_(KK_HOOK, st); k_sir_normalise<<<1, 1024, 0, st>>>(logw, m, cum, finite); }
+    {
+      const size_t smem = m <= kSirSmem ? (size_t)m * sizeof(double) : 0;
+      static bool attr = false;
+      if (!attr) {
+        if (cudaFuncSetAttribute(k_sir_normalise, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSirSmem * (int)sizeof(double)) != cudaSuccess)
+          return VP_ERR_CUDA;
+        attr = true;
+      }
+      Launch L_(KK_HOOK, st);
+      k_sir_normalise<<<1, 1024, smem, st>>>(logw, m, cum, finite);
+    }
     return check_launch();
   });
 }
