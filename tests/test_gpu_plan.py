@@ -108,6 +108,24 @@ def test_c1_fp32_invariants_and_conservation():
         assert 0.6 * nb_ref < out.tree_stats["belief_rows"] < 1.6 * nb_ref
 
 
+@pytest.mark.parametrize("n_par", [30000, 40000])
+def test_fp64_exact_large_batches_equal_oracle(n_par):
+    """Large passes take the backup's 16- and 32-leaves-per-warp launch shapes (sized from
+    the row count; small tests run 8): whole trees still equal the oracle's."""
+    om = oracle.MarsModel(7, 8, layout_seed=5)
+    belief = oracle.ParticleBelief.from_model(om, 2000, oracle.RowRng.from_seed(5).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=n_par, iterations=3, eta=2.0)
+    rng = oracle.RowRng.from_seed(5).derive(1, 0)
+    ref = oracle.plan(belief, om, cfg, rng)
+    out = vp.plan(belief, om, cfg, rng, precision="fp64", exact=True, keep_tree=True)
+    assert out.tree_stats == ref.tree_stats and out.chosen_action == ref.chosen_action
+    got, want = out.tree.tables(), ref.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    np.testing.assert_allclose(got["action_reward_sum"], want["action_reward_sum"], rtol=1e-12, atol=1e-9)
+    assert scale_close(got["prefs"], want["prefs"], 1e-9)
+
+
 def test_capacity_growth_matches_preallocated():
     case = manifest()["plans"]["plan_mars4_3"]
     s = case["runs"][0]["seed"]
