@@ -17,7 +17,8 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["plan_mars7_8_c1", "plan_tiger", "plan_lightdark", "plan_synthetic"])
+@pytest.mark.parametrize("name", ["plan_mars7_8_c1", "plan_tiger", "plan_lightdark", "plan_synthetic", "plan_navigation",
+                                  "plan_crowdnav40"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_fp64_plan_equals_reference_tree(name, world):
     case = manifest()["plans"][name]
