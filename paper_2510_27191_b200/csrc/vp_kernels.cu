@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "vp_common.cuh"
@@ -56,7 +58,10 @@ __global__ void k_clear(vp_tree T) {
 
 static int g_num_sms = 0;
 static int num_sms() {
-  if (!g_num_sms && cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) g_num_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_num_sms && cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    g_num_sms = 148;
   return g_num_sms;
 }
 
@@ -229,10 +234,32 @@ static int32_t dispatch_psi(int dtype, int exact, F&& f) {
   return VP_ERR_INVALID;
 }
 
-// Per-thread stack for models whose records live in local memory: reserved
-// once, before any launch or graph capture needs it.
+// One-time per-device settings (kernel shared-memory opt-in, stack limit) are
+// applied on first use on EACH device and remembered per (device, what).
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+static size_t& device_setting(const void* what) {
+  static std::map<std::pair<int, const void*>, size_t> done;
+  return done[{current_device(), what}];
+}
+static bool ensure_smem_optin(const void* kernel, size_t bytes) {
+  size_t& have = device_setting(kernel);
+  if (bytes <= 48 * 1024 || bytes <= have) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return false;
+  have = bytes;
+  return true;
+}
+
+// Per-thread stack for models whose records live in local memory (the one-lane
+// CrowdNav step of the SIR / hook kernels): reserved before any launch or graph
+// capture needs it.
 static bool ensure_stack(size_t bytes) {
-  static size_t have = 0;
+  static const char tag = 0;
+  size_t& have = device_setting(&tag);
   if (have >= bytes) return true;
   size_t cur = 0;
   if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) != cudaSuccess) return false;
@@ -296,14 +323,7 @@ static int32_t search_geometry(int A, StageCfg& sc, size_t& smem) {
 
 template <class Model, class PsiT, bool Exact>
 static int32_t set_search_attr(size_t smem) {
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    if (cudaFuncSetAttribute(k_search<Model, PsiT, Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return check_launch() ? VP_ERR_CUDA : VP_ERR_CUDA;
-    configured = smem;
-  }
-  return VP_OK;
+  return ensure_smem_optin((const void*)k_search<Model, PsiT, Exact>, smem) ? VP_OK : VP_ERR_CUDA;
 }
 
 template <class Model, class PsiT, bool Exact>
@@ -838,13 +858,7 @@ int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weig
     }
     {
       const size_t smem = m <= kSirSmem ? (size_t)m * sizeof(double) : 0;
-      static bool attr = false;
-      if (!attr) {
-        if (cudaFuncSetAttribute(k_sir_normalise, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSirSmem * (int)sizeof(double)) != cudaSuccess)
-          return VP_ERR_CUDA;
-        attr = true;
-      }
+      if (!ensure_smem_optin((const void*)k_sir_normalise, kSirSmem * sizeof(double))) return VP_ERR_CUDA;
       Launch L_(KK_HOOK, st);
       k_sir_normalise<<<1, 1024, smem, st>>>(logw, m, cum, finite);
     }
