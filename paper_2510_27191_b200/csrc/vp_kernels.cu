@@ -107,7 +107,7 @@ __device__ __forceinline__ Stage<PsiT> make_stage(unsigned char* smem, u64* bars
 // One search call: every warp carries 32 rows through all levels.
 template <class Model, class PsiT, bool Exact>
 __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_model M, vp_work W, vp_search_args S,
-                                                              StageCfg sc) {
+                                                              StageCfg sc, int rows) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) u64 s_bar[kSearchWarps];
   const int A = T.action_count;
@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
   if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;
   __syncthreads();
   const int wi = blockIdx.x * kSearchWarps + (threadIdx.x >> 5);
-  if (wi * rows_per_search_warp<Model>(S.mode) >= W.n) return;
-  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state);
+  if (wi * rows_per_search_warp<Model>(S.mode, rows) >= W.n) return;
+  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state, rows);
 }
 
 template <class PsiT, bool Exact>
@@ -291,6 +291,12 @@ static int env_int(const char* name, int dflt) {
 // (measured: C2 16k rows: 8 -> -7 % step time; C3 64k rows flat; C5 64k rows but
 // deeper trees: 32, 16 costs +8 %).
 // VP_LEAVES_PER_WARP overrides (measurement only).
+// Rows per search warp (32; VP_ROWS_PER_WARP overrides, measurement only).
+static int search_rows_per_warp(int) {
+  static const int forced = env_int("VP_ROWS_PER_WARP", 0);
+  return forced > 0 ? std::min(32, forced) : 32;
+}
+
 static int leaves_per_warp(int n) {
   static const int forced = env_int("VP_LEAVES_PER_WARP", 0);
   if (forced > 0) return std::min(32, forced);
@@ -333,10 +339,11 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
   size_t smem;
   search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
   if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
-  const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>(S.mode)), kSearchWarps);
+  const int rows = search_rows_per_warp(W.n);
+  const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>(S.mode, rows)), kSearchWarps);
   {
     Launch L_(KK_SEARCH, st);
-    k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc);
+    k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc, rows);
   }
   return check_launch();
 }

@@ -498,8 +498,8 @@ template <class M>
 struct coop_trait<M, std::void_t<decltype(M::kCoop)>> : std::integral_constant<bool, M::kCoop> {};
 // (insert replays recorded trajectories without stepping the model: full warps)
 template <class Model>
-__host__ __device__ constexpr int rows_per_search_warp(int mode) {
-  return coop_trait<Model>::value && mode != VP_SEARCH_INSERT ? 1 : 32;
+__host__ __device__ constexpr int rows_per_search_warp(int mode, int rows = 32) {
+  return coop_trait<Model>::value && mode != VP_SEARCH_INSERT ? 1 : rows;
 }
 
 struct NoState {};
@@ -715,10 +715,10 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
 template <class Model, class PsiT, bool Exact>
 __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                             Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index,
-                            typename Model::State* shared_state) {
+                            typename Model::State* shared_state, int rows) {
   typedef typename Model::State State;
   constexpr bool kCoop = coop_trait<Model>::value;
-  const int kRows = rows_per_search_warp<Model>(S.mode);
+  const int kRows = rows_per_search_warp<Model>(S.mode, rows);
   const int n = W.n, lane = lane_id();
   // 32 rows per warp: rows of a warp at the same belief share one draw (match_any
   // groups), which pays more than the latency hiding of more, emptier warps
