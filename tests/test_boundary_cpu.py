@@ -98,6 +98,51 @@ def test_state_packing_roundtrip():
     assert _device.TAB_DTYPE.itemsize == 8 and _device.SYN_DTYPE.itemsize == 16 and _device.LD_DTYPE.itemsize == 24
 
 
+@pytest.mark.parametrize("n,m", [(4, 3), (11, 11), (20, 30), (20, 60)])
+def test_mars_word_packing_equals_field_layout(n, m):
+    """mars_pack_into writes {x0,y0,x1,y1,terminal,rock bits} as two 64-bit words; every field
+    must land where MARS_DTYPE (and the kernel's MarsState) says, for every rock-count path."""
+    model = oracle.MarsModel(n, m, layout_seed=1)
+    st = model.sample_initial_states(300, oracle.RowRng.from_seed(3))
+    g = np.random.default_rng(0)
+    st.x = g.integers(0, n + 1, size=(300, 2))
+    st.y = g.integers(0, n, size=(300, 2))
+    st.terminal = g.random(300) < 0.3
+    rec = _device.mars_pack(st)
+    assert rec.dtype == _device.MARS_DTYPE
+    for i, f in enumerate(("x0", "x1")):
+        np.testing.assert_array_equal(rec[f], st.x[:, i])
+    for i, f in enumerate(("y0", "y1")):
+        np.testing.assert_array_equal(rec[f], st.y[:, i])
+    np.testing.assert_array_equal(rec["term"], st.terminal)
+    want = (st.rocks.astype(np.uint64) << np.arange(m, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
+    np.testing.assert_array_equal(rec["rocks"], want)
+    buf = np.full(16 * 300 + 40, 0xAB, dtype=np.uint8)  # dirty pinned-buffer stand-in
+    assert _device.mars_pack_into(st, buf) == 16 * 300
+    np.testing.assert_array_equal(buf[: 16 * 300], rec.view(np.uint8))
+    assert (buf[16 * 300:] == 0xAB).all()
+
+
+@pytest.mark.parametrize("people,tracked", [(300, 6), (17, 8), (320, 1)])
+def test_crowdnav_record_roundtrip(people, tracked):
+    model = oracle.CrowdNavModel(n_people=people, n_tracked=tracked, p_curious=0.4)
+    st = model.sample_initial_states(40, oracle.RowRng.from_seed(2))
+    st.terminal[3] = True
+    st.last_code[:] = np.arange(40) % (2 ** tracked)
+    rec = _device.crowd_pack(st)
+    assert rec.dtype.itemsize == _lib.CROWD_STATE_BYTES
+    back = _device.crowd_unpacker(people, tracked, oracle.CrowdStates)(rec)
+    for f in ("robot", "persons", "curious", "tracked", "prev_dist", "last_code", "terminal"):
+        np.testing.assert_array_equal(getattr(back, f), getattr(st, f), err_msg=f)
+
+
+def test_crowdnav_capacity_is_checked():
+    with pytest.raises(ValueError):
+        _device.crowdnav_descriptor(oracle.CrowdNavModel(n_people=321))
+    with pytest.raises(ValueError):
+        _device.crowdnav_descriptor(oracle.CrowdNavModel(n_people=30, n_tracked=9))
+
+
 def test_solver_config_contract():
     with pytest.raises(ValueError):
         vp.SolverConfig(iterations=None)
