@@ -316,11 +316,26 @@ static StageCfg stage_cfg(int A, int per_warp_bytes) {
   return c;
 }
 
+// Per-warp TMA stage budget.  Stage shared memory bounds the resident search
+// warps; a pass wants all of its warps resident at once (one wave), so the
+// budget shrinks as the warps per SM grow: 100 KB / warps-per-SM, 4-32 KB
+// (measured: C2 512 warps -> 25 KB, 16-32 KB flat; C3 2048 warps -> 7 KB,
+// 4-8 KB 11 % faster than 32 KB; C5's 64-B rows never fill it).
+// VP_STAGE_KB overrides (measurement only).
+static int stage_budget_bytes(int n, int rows_per_warp) {
+  static const int forced = env_int("VP_STAGE_KB", 0);
+  if (forced > 0) return forced * 1024;
+  const int warps = (n + rows_per_warp - 1) / rows_per_warp;
+  const int per_sm = std::max(1, (warps + num_sms() - 1) / num_sms());
+  return std::min(32, std::max(4, 100 / per_sm)) * 1024;
+}
+
 // Search launch geometry: staged rows of every warp + the block's copies of
 // the initial row and its CDF (+ one record per warp for cooperative models).
 template <class Model, class PsiT, bool Exact>
-static int32_t search_geometry(int A, StageCfg& sc, size_t& smem) {
-  sc = Exact ? StageCfg{0, 4} : stage_cfg<PsiT>(A, env_int("VP_STAGE_KB", 32) * 1024);
+static int32_t search_geometry(int A, int n, int mode, StageCfg& sc, size_t& smem) {
+  const int rows = rows_per_search_warp<Model>(mode, search_rows_per_warp(n));
+  sc = Exact ? StageCfg{0, 4} : stage_cfg<PsiT>(A, stage_budget_bytes(n, rows));
   const size_t padded = ((size_t)A * sizeof(PsiT) + 15) / 16 * 16 / sizeof(PsiT);
   smem = ((size_t)kSearchWarps * sc.rows * sc.stride + padded + (size_t)A) * sizeof(PsiT);
   if (coop_trait<Model>::value) smem = (smem + 15) / 16 * 16 + kSearchWarps * sizeof(typename Model::State);
@@ -337,7 +352,7 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
                              cudaStream_t st) {
   StageCfg sc;
   size_t smem;
-  search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
+  search_geometry<Model, PsiT, Exact>(T.action_count, W.n, S.mode, sc, smem);
   if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
   const int rows = search_rows_per_warp(W.n);
   const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>(S.mode, rows)), kSearchWarps);
@@ -440,7 +455,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   {
     StageCfg sc;
     size_t smem;
-    search_geometry<Model, PsiT, Exact>(T.action_count, sc, smem);
+    search_geometry<Model, PsiT, Exact>(T.action_count, W.n, VP_SEARCH_FUSED, sc, smem);
     if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);
@@ -449,7 +464,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   append_pod(key, M);
   append_pod(key, W);
   append_pod(key, P);
-  const int budget = env_int("VP_STAGE_KB", 32);
+  const int budget = stage_budget_bytes(W.n, 32);
   append_pod(key, budget);
   GraphEntry* hit = nullptr;
   for (auto& e : g_graphs)
