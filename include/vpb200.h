@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 4
+#define VPB200_ABI_VERSION 5
 
 enum vp_status {
   VP_OK = 0,
@@ -46,6 +46,9 @@ enum vp_model_kind {
 };
 
 enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
+
+#define VP_COUNTERS 64
+#define VP_COUNTER_ACTIONS 32
 
 /* Device descriptor of a ProblemModel (core.py:84-142).  Passed by value to
  * every kernel; constant tables live in device memory. */
@@ -132,7 +135,8 @@ typedef struct vp_tree {
   /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */
   void* hash_b;               /* (action row << 32 | obs) -> belief row     */
-  int32_t* counters;          /* [0] n_beliefs [1] n_actions [2] overflow [3] 0 */
+  int32_t* counters;          /* [VP_COUNTERS]: [0] n_beliefs, [2] overflow, [VP_COUNTER_ACTIONS] n_actions
+                               (the two id counters on separate 128-B lines: every warp allocates from both) */
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
@@ -253,7 +257,7 @@ int64_t vp_launch_count(void);
 int32_t vp_tree_init(const vp_tree* tree, void* stream);
 /* Rebuild both hash indexes from the node columns (after capacity growth). */
 int32_t vp_tree_rehash(const vp_tree* tree, void* stream);
-/* Copy the 3 counters (n_beliefs, n_actions, overflow) to host memory. */
+/* Copy (n_beliefs, n_actions, overflow) to host memory (3 x int32). */
 int32_t vp_tree_counts(const vp_tree* tree, int32_t* host_out, void* stream);
 
 /* ---- planning step pieces ---------------------------------------------- */

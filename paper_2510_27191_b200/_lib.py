@@ -20,7 +20,8 @@ VP_MODEL_CROWDNAV = 6
 CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 4
+ABI_VERSION = 5
+VP_COUNTERS, VP_COUNTER_ACTIONS = 64, 32  # include/vpb200.h
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
     C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),

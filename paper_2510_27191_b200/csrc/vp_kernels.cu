@@ -36,7 +36,7 @@ __global__ void k_tree_init(vp_tree T) {
 // that other rows would have to wait for (rows beyond the previous counts are
 // in that state since allocation).  Part 2 (k_tree_init) rewrites the root.
 __global__ void k_clear(vp_tree T) {
-  const int nb = min(T.counters[0], T.cap_beliefs), na = min(T.counters[1], T.cap_actions);
+  const int nb = min(T.counters[0], T.cap_beliefs), na = min(T.counters[VP_COUNTER_ACTIONS], T.cap_actions);
   const int total = max(max(nb, na), T.cdf_slots);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i < nb) {
@@ -66,7 +66,7 @@ static int num_sms() {
 }
 
 __global__ void k_rehash(vp_tree T) {
-  const int na = T.counters[1], nb = T.counters[0];
+  const int na = T.counters[VP_COUNTER_ACTIONS], nb = T.counters[0];
   const int total = na + nb;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i < na) {
@@ -150,7 +150,7 @@ __global__ void k_root_argmax(vp_tree T, int* out) {
 }
 
 __global__ void k_copy_counters(vp_tree T, int* out) {
-  if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x];
+  if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x == 1 ? VP_COUNTER_ACTIONS : threadIdx.x];
 }
 
 // ================================================================== host side
@@ -771,8 +771,11 @@ int32_t vp_tree_rehash(const vp_tree* t, void* stream) {
 int32_t vp_tree_counts(const vp_tree* t, int32_t* host_out, void* stream) {
   if (!t || !host_out) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMemcpyAsync(host_out, t->counters, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
-    return VP_ERR_CUDA;
+  const int idx[3] = {0, VP_COUNTER_ACTIONS, 2};
+  for (int k = 0; k < 3; ++k)
+    if (cudaMemcpyAsync(host_out + k, t->counters + idx[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+        cudaSuccess)
+      return VP_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return VP_ERR_CUDA;
   return VP_OK;
 }

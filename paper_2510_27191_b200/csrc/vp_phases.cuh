@@ -453,7 +453,7 @@ __device__ void block_tree_init(const vp_tree& T) {
       T.b_flags[0] = 0;  // the root row is written (above), not lazy
       T.b_ckey[0] = 0;
       T.counters[0] = 1;
-      T.counters[1] = 0;
+      T.counters[VP_COUNTER_ACTIONS] = 0;
       T.counters[2] = 0;
       T.counters[3] = 0;
     }
@@ -824,7 +824,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       lead = ok && lane == leader;
       Claim cl{0, false, 0};
       if (lead) cl = claim_key(ha, T.hmask_a, key);
-      const int id = warp_alloc(&T.counters[1], cl.won);
+      const int id = warp_alloc(&T.counters[VP_COUNTER_ACTIONS], cl.won);
       if (cl.won) {
         x = id;
         if (x < T.cap_actions) {

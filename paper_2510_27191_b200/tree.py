@@ -76,7 +76,7 @@ class DeviceTree:
         self._scratch_dirty = False  # a search ran without its backup
         self.last_search = None
         self._psi_dtype = torch.float32 if precision == "fp32" else torch.float64
-        self._counters = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self._counters = torch.zeros(_lib.VP_COUNTERS, dtype=torch.int32, device="cuda")
         self._init_lse = torch.zeros(1, dtype=torch.float64, device="cuda")
         self._init_prefs = torch.zeros(action_count, dtype=torch.float64, device="cuda")
         # PSI rows padded to 16 bytes so they can be TMA bulk-copied (csrc K1)
