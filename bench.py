@@ -234,9 +234,16 @@ def run_b200(args):
     from paper_2510_27191_b200.rng import key_of
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # VP_DIST_BACKEND=gloo check on one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # VP_DIST_BACKEND=gloo: several ranks on ONE GPU (NCCL refuses a shared device) -- a
+        # functional check of the multi-rank path only, never a measurement
+        backend = os.environ.get("VP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     sharded = world > 1 and args.multi == "sharded"
     # sharded: ONE planning step over world * n_parallel rows (same seed on every rank);
     # replicas: every rank plans its own problem
