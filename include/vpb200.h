@@ -293,6 +293,11 @@ int32_t vp_sir_weigh(const vp_model* model, const void* states, const double* we
 /* Systematic resampling (belief.py:47-53): out[j] = prop[first i with cum[i] > (j + u0) / m]. */
 int32_t vp_sir_resample(const vp_model* model, const void* prop, const double* cum, int32_t m, double u0,
                         void* states_out, void* stream);
+/* Belief reconciliation with the executed state (ProblemModel.reconcile_belief, core.py:119-136;
+ * crowdnav.py:213-224): every particle record takes `source`'s bytes except [keep_lo, keep_hi)
+ * (the hidden component, kept per particle).  Sizes and offsets are multiples of 8. */
+int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, const void* source, int32_t keep_lo,
+                            int32_t keep_hi, void* stream);
 
 /* ---- test hooks (parity of individual kernels) ------------------------- */
 int32_t vp_rng_uniform(uint64_t key, const int64_t* rows, int64_t n, int32_t k,

@@ -907,6 +907,28 @@ int32_t vp_sir_resample(const vp_model* mdl, const void* prop, const double* cum
   });
 }
 
+__global__ void k_broadcast_record(u64* rec, long long words_total, int words, const u64* src, int keep_lo,
+                                   int keep_hi) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words_total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(i % words);
+    if (w < keep_lo || w >= keep_hi) rec[i] = src[w];
+  }
+}
+
+int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, const void* source, int32_t keep_lo,
+                            int32_t keep_hi, void* stream) {
+  if (!records || !source || m < 1 || record_bytes < 8 || record_bytes % 8 || keep_lo % 8 || keep_hi % 8 ||
+      keep_lo < 0 || keep_hi < keep_lo || keep_hi > record_bytes)
+    return VP_ERR_INVALID;
+  const long long total = (long long)m * (record_bytes / 8);
+  Launch L_(KK_HOOK, (cudaStream_t)stream);
+  k_broadcast_record<<<(int)std::min<long long>((total + 255) / 256, 148LL * 16), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<u64*>(records), total, record_bytes / 8, reinterpret_cast<const u64*>(source), keep_lo / 8,
+      keep_hi / 8);
+  return check_launch();
+}
+
 int32_t vp_rng_uniform(uint64_t key, const int64_t* rows, int64_t n, int32_t k, double* out, void* stream) {
   if (n < 0 || (n && (!rows || !out))) return VP_ERR_INVALID;
   if (!n) return VP_OK;

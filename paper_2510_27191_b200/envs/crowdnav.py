@@ -10,11 +10,12 @@ bit per tracked person (the 6 nearest at the last executed step) telling
 whether it closed distance, |O| = 64 + terminal.
 
 The generative step, the leaf heuristic and the likelihood run on the device
-(csrc/vp_models.cuh, CrowdNavModel) on 2704-byte records kept in local memory.
-The host keeps the initial-state sampler and the two belief hooks that re-anchor
-the observable part of every particle on the executed state
-(crowdnav.py:199-224); these hooks are why closed-loop CrowdNav uses the host
-SIR update rather than the device-resident belief.
+(csrc/vp_models.cuh, CrowdNavModel) on 2704-byte records: the planner steps a
+row with a whole warp, the record in shared memory (``step_warp``).  The host
+keeps the initial-state sampler and the tracking refresh of the one executed
+state; re-anchoring every particle's observable part on it (crowdnav.py:213-224)
+is a device broadcast (``reconcile_device``), so the closed loop keeps the
+belief resident in HBM with the device SIR update.
 """
 
 from __future__ import annotations
@@ -107,6 +108,23 @@ class CrowdNavModel(ProblemModel):
 
         return CrowdStates(rep(executed.robot), rep(executed.persons), particles.curious, rep(executed.tracked),
                            rep(executed.prev_dist), rep(executed.last_code), rep(executed.terminal))
+
+    def reconcile_device(self, belief, executed: CrowdStates):
+        """reconcile_belief on a device-resident belief: every particle record takes the
+        executed state's observable fields and keeps its own curious bits (one broadcast
+        kernel, vp_broadcast_record); weights are unchanged."""
+        import torch
+
+        from .. import _lib
+        from ._device import CROWD_DTYPE
+
+        dm = self.device_descriptor()
+        src = torch.from_numpy(dm.pack(executed.take([0])).view(np.uint8).reshape(-1).copy()).cuda()
+        lo = CROWD_DTYPE.fields["curious"][1]
+        hi = lo + CROWD_DTYPE.fields["curious"][0].itemsize
+        _lib.call("vp_broadcast_record", belief.records.data_ptr(), belief.m, dm.state_bytes, src.data_ptr(), lo, hi,
+                  torch.cuda.current_stream().cuda_stream)
+        return belief
 
     # -- device pieces
     def step_batch(self, states, actions, rng):

@@ -397,11 +397,15 @@ def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str 
     env_state = model.sample_initial_states(1, env_rng.derive(0))
     belief = ParticleBelief.from_model(model, config.particles, root.derive(NS_INIT_BELIEF))
     belief = ParticleBelief(model.reconcile_belief(belief.states, env_state), belief.weights)
+    # a model with its own belief hooks can keep the belief resident when it reconciles on the
+    # device (reconcile_device); refresh_executed runs on the single executed state
+    device_hooks = hasattr(model, "reconcile_device")
     if device_belief is None:
-        device_belief = not exact and _identity_hooks(model)
+        device_belief = not exact and (_identity_hooks(model) or device_hooks)
     if device_belief:
-        if not _identity_hooks(model):
-            raise ValueError("device-resident beliefs need the identity reconcile_belief / refresh_executed hooks")
+        if not (_identity_hooks(model) or device_hooks):
+            raise ValueError("device-resident beliefs need identity reconcile_belief / refresh_executed hooks "
+                             "or a model.reconcile_device")
         belief = DeviceBelief.from_host(belief, model)
     total, counters, times, degenerate, t, reason = 0.0, {}, [], 0, 0, "truncated"
     while t < spec.max_steps:
@@ -423,7 +427,7 @@ def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str 
         degenerate += int(upd.degenerate)
         env_state = model.refresh_executed(env_state)
         if device_belief:
-            belief = upd.belief
+            belief = model.reconcile_device(upd.belief, env_state) if device_hooks else upd.belief
         else:
             belief = ParticleBelief(model.reconcile_belief(upd.belief.states, env_state), upd.belief.weights)
     return RunRecord(run_index, seed, total, t, reason, times, counters, degenerate)

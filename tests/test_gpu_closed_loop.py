@@ -42,6 +42,19 @@ def test_fp64_exact_crowdnav_episodes_equal_reference():
         assert got.counters == pytest.approx(r["counters"])
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_crowdnav_device_belief_equals_host_belief(seed):
+    """Device-resident CrowdNav loop (device SIR + reconcile_device broadcast) equals the host
+    belief loop (host SIR + numpy reconcile_belief) step for step."""
+    model = vp.CrowdNavModel(n_people=40, hall_depth=8.0, max_steps=12)
+    cfg = vp.SolverConfig(n_parallel=256, iterations=4, particles=300)
+    a = vp.run_episode(model, cfg, seed=seed, precision="fp64", device_belief=True)
+    b = vp.run_episode(model, cfg, seed=seed, precision="fp64", device_belief=False)
+    assert (a.steps, a.terminal_reason, a.degenerate_updates) == (b.steps, b.terminal_reason, b.degenerate_updates)
+    assert a.discounted_return == pytest.approx(b.discounted_return, abs=1e-12)
+    assert a.counters == pytest.approx(b.counters)
+
+
 def test_fp32_campaign_returns_match_reference():
     recs = manifest()["episodes"]["episode_mars5_4_campaign"]
     cfg = vp.SolverConfig(n_parallel=256, iterations=5, particles=1000)
