@@ -528,6 +528,29 @@ __global__ void k_sir_propagate(vp_model M, const typename Model::State* in, con
   logw[i] = log(w[i]) + Model::obs_loglik(M, st, a, obs);  // log(weights) + log_lik (belief.py:88-90)
 }
 
+// Cooperative models (CrowdNav): one warp per particle, the record staged in
+// shared memory and stepped by Model::step_warp (bit-identical to step()).
+constexpr int kCoopSirWarps = 4;
+
+template <class Model>
+__global__ void __launch_bounds__(kCoopSirWarps * 32) k_sir_propagate_coop(vp_model M, const typename Model::State* in,
+                                                                            const double* w, int m, int a, u32 obs,
+                                                                            u64 key, typename Model::State* out,
+                                                                            double* logw) {
+  typedef typename Model::State State;
+  __shared__ State s_state[kCoopSirWarps];
+  const int warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * kCoopSirWarps + warp;
+  if (i >= m) return;
+  State& st = s_state[warp];
+  warp_copy_state(st, in[i]);
+  u32 o;
+  double r;
+  Model::step_warp(M, st, a, key, (u64)i, true, o, r);
+  warp_copy_state(out[i], st);
+  if (lane_id() == 0) logw[i] = log(w[i]) + Model::obs_loglik(M, st, a, obs);
+}
+
 // One block: max over finite log-weights, shifted = exp(lw - max), its numpy
 // pairwise sum, then the sequential cumsum of shifted / sum with cum[-1] = 1
 // (belief.py:91-93, 50-52).  The two serial sums run on one thread in numpy
@@ -877,9 +900,14 @@ int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weig
     if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
     {
       Launch L_(KK_HOOK, st);
-      k_sir_propagate<Model><<<blocks_for(m, 256), 256, 0, st>>>(M, reinterpret_cast<const State*>(states), weights,
-                                                                   m, action, observation, key,
-                                                                   reinterpret_cast<State*>(states_out), logw);
+      if constexpr (coop_trait<Model>::value)
+        k_sir_propagate_coop<Model><<<blocks_for(m, kCoopSirWarps), kCoopSirWarps * 32, 0, st>>>(
+            M, reinterpret_cast<const State*>(states), weights, m, action, observation, key,
+            reinterpret_cast<State*>(states_out), logw);
+      else
+        k_sir_propagate<Model><<<blocks_for(m, 256), 256, 0, st>>>(M, reinterpret_cast<const State*>(states), weights,
+                                                                     m, action, observation, key,
+                                                                     reinterpret_cast<State*>(states_out), logw);
     }
     {
       const size_t smem = m <= kSirSmem ? (size_t)m * sizeof(double) : 0;

@@ -401,8 +401,9 @@ struct __align__(8) CrowdState {
 
 struct CrowdNavModel {
   typedef CrowdState State;
-  // the planner steps a row with the whole warp (people split over the lanes),
-  // record in shared memory; step() below is the one-lane form (SIR, hooks)
+  // the planner and the SIR propagation step a row with the whole warp (people
+  // split over the lanes), record in shared memory; step() below is the one-lane
+  // form (vp_model_step: the environment step and the per-row parity hook)
   static constexpr bool kCoop = true;
 
   // j-th of the row's Box-Muller normals from precomputed row bases (rng.py:81-89)
