@@ -293,6 +293,14 @@ int32_t vp_sir_weigh(const vp_model* model, const void* states, const double* we
 /* Systematic resampling (belief.py:47-53): out[j] = prop[first i with cum[i] > (j + u0) / m]. */
 int32_t vp_sir_resample(const vp_model* model, const void* prop, const double* cum, int32_t m, double u0,
                         void* states_out, void* stream);
+/* Host-level tree mutation on device ids (tree.py:180-218 append_actions: claim (belief, action),
+ * reward / visit accumulation; tree.py:220-256 append_beliefs: claim (action node, observation),
+ * new rows lazily == init_prefs).  `pass` (> 0, fresh per call) orders the new nodes after every
+ * existing one in the canonical export; out[i] = the edge's device id (-1: capacity exceeded). */
+int32_t vp_tree_append_actions(const vp_tree* tree, const int32_t* beliefs, const int32_t* actions,
+                               const double* rewards, int32_t n, uint32_t pass, int32_t* out, void* stream);
+int32_t vp_tree_append_beliefs(const vp_tree* tree, const int32_t* action_nodes, const uint32_t* observations,
+                               int32_t n, uint32_t pass, int32_t* out, void* stream);
 /* Belief reconciliation with the executed state (ProblemModel.reconcile_belief, core.py:119-136;
  * crowdnav.py:213-224): every particle record takes `source`'s bytes except [keep_lo, keep_hi)
  * (the hidden component, kept per particle).  Sizes and offsets are multiples of 8. */

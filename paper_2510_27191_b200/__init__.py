@@ -9,7 +9,7 @@ point raises.
 """
 
 from . import _lib
-from .backup import backup, log_sum_exp_rows
+from .backup import LevelValues, action_q_values, aggregate_leaves, backup, log_sum_exp_rows
 from .belief import DeviceBelief, ParticleBelief, SirUpdate, sir_update, systematic_resample
 from .core import ProblemModel, ProblemSpec, StepResult
 from .envs import (CrowdNavModel, CrowdStates, LightDarkModel, MarsModel, NavigationModel, SyntheticModel, TabularModel, TabularPOMDP,
@@ -18,7 +18,7 @@ from .rng import BoundRng, RowRng
 from .search import LeafResult, SearchBatch, sample_actions, search, softmax_rows
 from .solver import Planner, PlanOutcome, RunRecord, SolverConfig, get_planner, plan, run_episode
 from .shard import ShardedPlanner, shard_rows
-from .tree import DeviceTree, init_tree
+from .tree import DeviceTree, init_tree, match_or_append_pairs
 
 __version__ = "0.1.0"
 
@@ -27,5 +27,6 @@ __all__ = [
     "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",
-    "sir_update", "softmax_rows", "systematic_resample", "tiger_model",
+    "sir_update", "softmax_rows", "systematic_resample", "tiger_model", "LevelValues", "aggregate_leaves",
+    "action_q_values", "match_or_append_pairs",
 ]

@@ -131,6 +131,10 @@ _SIGNATURES = [
       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("vp_sir_resample", C.c_int32,
      [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
+    ("vp_tree_append_actions", C.c_int32,
+     [C.POINTER(VpTree), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    ("vp_tree_append_beliefs", C.c_int32,
+     [C.POINTER(VpTree), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p]),
     ("vp_broadcast_record", C.c_int32,
      [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),

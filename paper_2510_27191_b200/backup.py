@@ -63,3 +63,58 @@ def log_sum_exp_rows(pref_rows, eta: float, *, precision: str = "fp64", exact: b
               rows.shape[1], float(eta), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
     res = out.cpu().numpy()
     return res if np.ndim(pref_rows) > 1 else res[0]
+
+
+class LevelValues:
+    """Per-belief values of one level (backup.py:25-31): distinct beliefs, their values and
+    visit weights (device tensors; host arrays through the properties)."""
+
+    def __init__(self, belief_indices, values, visit_weights):
+        self._b, self._v, self._w = belief_indices, values, visit_weights
+
+    @property
+    def belief_indices(self) -> np.ndarray:
+        return self._b.cpu().numpy()
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._v.cpu().numpy()
+
+    @property
+    def visit_weights(self) -> np.ndarray:
+        return self._w.cpu().numpy()
+
+
+def aggregate_leaves(leaves) -> LevelValues:
+    """backup.py:44-51 on the device: per distinct leaf belief, N = rows that ended there and
+    V = their mean heuristic value (sums by device reductions: equal to numpy's bincount up to
+    the order of floating-point additions)."""
+    torch = _torch()
+    ids = torch.as_tensor(np.asarray(leaves.leaf_belief_indices, dtype=np.int64), device="cuda")
+    h = torch.as_tensor(np.asarray(leaves.heuristic_values, dtype=np.float64), device="cuda")
+    if ids.shape != h.shape:
+        raise ValueError("leaf ids and heuristic values differ in length")
+    distinct, grp = torch.unique(ids, sorted=True, return_inverse=True)
+    n = torch.zeros(len(distinct), dtype=torch.float64, device="cuda").index_add_(0, grp, torch.ones_like(h))
+    total = torch.zeros(len(distinct), dtype=torch.float64, device="cuda").index_add_(0, grp, h)
+    return LevelValues(distinct, total / n, n)
+
+
+def action_q_values(tree, action_rows, child: LevelValues, gamma: float) -> np.ndarray:
+    """backup.py:54-72 on the device tree: Q(a) = reward_sum / visits + gamma * sum(V N) / sum(N)
+    over a's valued children (reference ids in; ValueError for an action without valued child)."""
+    torch = _torch()
+    t = tree.tables()  # reference-ordered columns (parent_action of the children, action stats)
+    acts = torch.as_tensor(np.asarray(action_rows, dtype=np.int64), device="cuda")
+    kids = torch.as_tensor(np.asarray(child.belief_indices, dtype=np.int64), device="cuda")
+    v = torch.as_tensor(np.asarray(child.values, dtype=np.float64), device="cuda")
+    w = torch.as_tensor(np.asarray(child.visit_weights, dtype=np.float64), device="cuda")
+    par = torch.as_tensor(t["parent_action"], device="cuda")[kids]
+    na = len(t["action_id"])
+    num = torch.zeros(na, dtype=torch.float64, device="cuda").index_add_(0, par, v * w)
+    den = torch.zeros(na, dtype=torch.float64, device="cuda").index_add_(0, par, w)
+    if bool((den[acts] <= 0).any()):
+        raise ValueError("action node without valued children")
+    reward = torch.as_tensor(t["action_reward_sum"], device="cuda")[acts]
+    visits = torch.as_tensor(t["action_visits"], device="cuda").to(torch.float64)[acts]
+    return (reward / visits + gamma * num[acts] / den[acts]).cpu().numpy()

@@ -935,6 +935,89 @@ int32_t vp_sir_resample(const vp_model* mdl, const void* prop, const double* cum
   });
 }
 
+// Host-level tree mutation (tree.py:180-256 append_actions / append_beliefs):
+// one thread per edge, the search's claim / numbering / creation-key protocol,
+// so new nodes take reference ids n + rank in first-occurrence order at export.
+__global__ void k_append_actions(vp_tree T, const int32_t* beliefs, const int32_t* actions, const double* rewards,
+                                 int n, u32 pass, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Slot* ha = slots(T.hash_a);
+  const int b = beliefs[i], a = actions[i];
+  const Claim cl = claim_key(ha, T.hmask_a, ((u64)(u32)b << 32) | (u32)a);
+  int x;
+  if (cl.won) {
+    x = atomicAdd(&T.counters[VP_COUNTER_ACTIONS], 1);
+    if (x < T.cap_actions) {
+      T.a_parent_belief[x] = b;
+      T.a_action[x] = a;
+      red_min(&T.a_ckey[x], creation_key(pass, 0, i));
+    } else {
+      T.counters[2] = 1;
+    }
+    publish(ha, cl.slot, (u32)x, pass);
+  } else {
+    const u64 w = wait_published(ha, cl.slot, cl.word);
+    x = (int)(u32)w;
+    if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, 0, i));
+  }
+  if (x < T.cap_actions) {
+    red_add(&T.a_reward[x], rewards[i]);  // np.add.at(reward, idx, r) (tree.py:216-217)
+    red_add(&T.a_visits[x], 1);
+  }
+  out[i] = x < T.cap_actions ? x : -1;
+}
+
+__global__ void k_append_beliefs(vp_tree T, const int32_t* anodes, const uint32_t* obs, int n, u32 pass, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Slot* hb = slots(T.hash_b);
+  const int x = anodes[i];
+  const u32 o = obs[i];
+  const Claim cl = claim_key(hb, T.hmask_b, ((u64)(u32)x << 32) | o);
+  int c;
+  if (cl.won) {
+    c = atomicAdd(&T.counters[0], 1);
+    if (c < T.cap_beliefs) {
+      const int pb = T.a_parent_belief[x];
+      T.b_parent_action[c] = x;
+      T.b_parent_obs[c] = o;
+      T.b_parent_belief[c] = pb;
+      T.b_parent_act[c] = T.a_action[x];
+      T.b_depth[c] = T.b_depth[pb] + 1;  // tree.py:253
+      T.b_lse[c] = T.init_lse[0];
+      T.b_flags[c] = 3u;  // PSI row == init_prefs, not materialised (tree.py:253)
+      red_min(&T.b_ckey[c], creation_key(pass, 0, i));
+    } else {
+      T.counters[2] = 1;
+    }
+    publish(hb, cl.slot, (u32)c, pass);
+  } else {
+    const u64 w = wait_published(hb, cl.slot, cl.word);
+    c = (int)(u32)w;
+    if ((u32)(w >> 32) == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, 0, i));
+  }
+  out[i] = c < T.cap_beliefs ? c : -1;
+}
+
+int32_t vp_tree_append_actions(const vp_tree* t, const int32_t* beliefs, const int32_t* actions, const double* rewards,
+                               int32_t n, uint32_t pass, int32_t* out, void* stream) {
+  if (!t || n < 0 || (n && (!beliefs || !actions || !rewards || !out)) || pass == 0) return VP_ERR_INVALID;
+  if (!n) return VP_OK;
+  Launch L_(KK_HOOK, (cudaStream_t)stream);
+  k_append_actions<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*t, beliefs, actions, rewards, n, pass, out);
+  return check_launch();
+}
+
+int32_t vp_tree_append_beliefs(const vp_tree* t, const int32_t* action_nodes, const uint32_t* observations, int32_t n,
+                               uint32_t pass, int32_t* out, void* stream) {
+  if (!t || n < 0 || (n && (!action_nodes || !observations || !out)) || pass == 0) return VP_ERR_INVALID;
+  if (!n) return VP_OK;
+  Launch L_(KK_HOOK, (cudaStream_t)stream);
+  k_append_beliefs<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*t, action_nodes, observations, n, pass, out);
+  return check_launch();
+}
+
 __global__ void k_broadcast_record(u64* rec, long long words_total, int words, const u64* src, int keep_lo,
                                    int keep_hi) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words_total;

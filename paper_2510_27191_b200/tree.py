@@ -256,6 +256,130 @@ class DeviceTree:
         t = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda")
         return border[t]
 
+    # ------------------------------------------------------------------ host-level mutation (tree.py:180-265)
+    def _append(self, fn: str, ids_dev, labels, extra, n: int):
+        torch = _torch()
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        args = [C.byref(self.struct), ids_dev.data_ptr(), labels.data_ptr()]
+        if extra is not None:
+            args.append(extra.data_ptr())
+        _lib.call(fn, *args, n, self.next_pass(), out.data_ptr(), _stream())
+        return out
+
+    def append_actions(self, belief_indices, actions, rewards) -> np.ndarray:
+        """tree.py:180-218 on the device: resolve (belief, action) edges -- new nodes numbered
+        n_actions + rank in first-occurrence order -- and add each row's reward and one visit.
+        Reference ids in and out."""
+        torch = _torch()
+        b = np.asarray(belief_indices, dtype=np.int64)
+        a = np.asarray(actions, dtype=np.int64)
+        r = np.asarray(rewards, dtype=np.float64)
+        if not (len(b) == len(a) == len(r)):
+            raise ValueError("append_actions: batch lengths differ")
+        nb, na, _ = self.counts()
+        if len(b) and (b.min() < 0 or b.max() >= nb):
+            raise ValueError("append_actions: invalid belief index")
+        if len(a) and (a.min() < 0 or a.max() >= self.action_count):
+            raise ValueError("append_actions: actions must be in [0, |A|)")
+        if not len(b):
+            return np.zeros(0, dtype=np.int64)
+        self.ensure_capacity(nb, na + len(b))
+        dev_b = self.to_device_beliefs(b).to(torch.int32)
+        out = self._append("vp_tree_append_actions", dev_b, torch.from_numpy(a.astype(np.int32)).cuda(),
+                           torch.from_numpy(r).cuda(), len(b))
+        if self.counts()[2]:
+            raise _lib.CapacityError("action table overflow")
+        return self.to_reference_actions(out.to(torch.int64)).cpu().numpy()
+
+    def append_beliefs(self, action_node_indices, observations) -> np.ndarray:
+        """tree.py:220-256 on the device: resolve (action node, observation) edges; new beliefs
+        get depth = parent depth + 1 and the initial PSI row (lazily).  Reference ids in and out."""
+        torch = _torch()
+        x = np.asarray(action_node_indices, dtype=np.int64)
+        o = np.asarray(observations, dtype=np.int64)
+        if len(x) != len(o):
+            raise ValueError("append_beliefs: batch lengths differ")
+        nb, na, _ = self.counts()
+        if len(x) and (x.min() < 0 or x.max() >= na):
+            raise ValueError("append_beliefs: invalid action-node index")
+        if len(o) and (o.min() < 0 or o.max() >= 1 << 32):
+            raise ValueError("pair entries must be in [0, 2**32)")
+        if not len(x):
+            return np.zeros(0, dtype=np.int64)
+        self.ensure_capacity(nb + len(x), na)
+        _, _, aorder, _ = self.canonical()
+        dev_x = aorder[torch.from_numpy(x).cuda()].to(torch.int32)
+        out = self._append("vp_tree_append_beliefs", dev_x, torch.from_numpy(o.astype(np.uint32).view(np.int32)).cuda(),
+                           None, len(x))
+        if self.counts()[2]:
+            raise _lib.CapacityError("belief table overflow")
+        return self.to_reference_beliefs(out.to(torch.int64)).cpu().numpy()
+
+    def nodes_at_depth(self, d: int):
+        """Beliefs at depth d with their parent action and grandparent belief (tree.py:258-265),
+        reference ids."""
+        if d < 1:
+            raise ValueError("nodes_at_depth requires d >= 1")
+        t = self.tables()
+        bel = np.flatnonzero(t["depth"] == d)
+        par = t["parent_action"][bel]
+        grand = t["action_parent_belief"][par] if len(par) else par
+        return bel, par, grand
+
+    @classmethod
+    def deserialize(cls, text: str, *, eta: float = 2.0, precision: str = "fp32") -> "DeviceTree":
+        """Inverse of ``serialize`` (tree.py:322-368): the B / A / P rows become device columns
+        (reference ids = device ids), the hash indexes are rebuilt on the device."""
+        torch = _torch()
+        b_rows, a_rows, p_rows = [], [], []
+        for line in text.splitlines():
+            if not line.strip():
+                continue
+            parts = line.split("\t")
+            if parts[0] == "B":
+                b_rows.append([int(v) for v in parts[1:5]])
+            elif parts[0] == "A":
+                a_rows.append((int(parts[1]), int(parts[2]), int(parts[3]), float(parts[4]), int(parts[5])))
+            elif parts[0] == "P":
+                p_rows.append((int(parts[1]), [float(v) for v in parts[3:]]))
+            else:
+                raise ValueError(f"unknown row tag {parts[0]!r}")
+        if not b_rows or b_rows[0][0] != 0:
+            raise ValueError("serialized tree must start with belief row 0")
+        A = len(p_rows[0][1])
+        nb, na = len(b_rows), len(a_rows)
+        tree = cls(A, eta=eta, precision=precision, cap_beliefs=max(16, nb), cap_actions=max(16, na))
+        prefs = np.zeros((nb, A))
+        for row, vals in p_rows:
+            prefs[row] = vals
+        pa = np.array([r[1] for r in b_rows], dtype=np.int64)
+        apb = np.array([r[1] for r in a_rows], dtype=np.int64)
+        act = np.array([r[2] for r in a_rows], dtype=np.int64)
+        dev = lambda v, dt: torch.as_tensor(np.asarray(v), device="cuda").to(dt)  # noqa: E731
+        tree.b_parent_action[:nb] = dev(np.where(pa >= 0, pa, -1), torch.int32)
+        tree.b_parent_obs[:nb] = dev(np.array([r[2] for r in b_rows], dtype=np.int64).astype(np.uint32).view(np.int32),
+                                     torch.int32)
+        tree.b_depth[:nb] = dev([r[3] for r in b_rows], torch.int32)
+        tree.b_parent_belief[:nb] = dev(np.where(pa >= 0, apb[np.maximum(pa, 0)] if na else -1, -1), torch.int32)
+        tree.b_parent_act[:nb] = dev(np.where(pa >= 0, act[np.maximum(pa, 0)] if na else 0, 0), torch.int32)
+        tree.psi[:nb, :A] = dev(prefs, tree._psi_dtype)
+        tree.b_lse[:nb] = dev(np.max(eta * prefs, axis=1) / eta
+                              + np.log(np.exp(eta * prefs - np.max(eta * prefs, axis=1)[:, None]).sum(axis=1)) / eta,
+                              torch.float64)
+        tree.b_flags[:nb] = 0  # every row is written
+        tree.b_ckey[:nb] = torch.arange(nb, device="cuda", dtype=torch.int64)  # canonical order = ids
+        if na:
+            tree.a_parent_belief[:na] = dev(apb, torch.int32)
+            tree.a_action[:na] = dev(act, torch.int32)
+            tree.a_reward[:na] = dev([r[3] for r in a_rows], torch.float64)
+            tree.a_visits[:na] = dev([r[4] for r in a_rows], torch.int32)
+            tree.a_ckey[:na] = torch.arange(na, device="cuda", dtype=torch.int64)
+        tree._counters[0], tree._counters[_lib.VP_COUNTER_ACTIONS], tree._counters[2] = nb, na, 0
+        _lib.call("vp_tree_rehash", C.byref(tree.struct), _stream())
+        tree.pass_cursor = 1
+        tree._canon_cache = None
+        return tree
+
     # ------------------------------------------------------------------ reference-style accessors
     @property
     def n_beliefs(self) -> int:
@@ -356,6 +480,40 @@ class TreeHandle:
             raise RuntimeError("this plan's device tree was recycled by a later plan() call; "
                                "pass keep_tree=True to keep it")
         return getattr(tree, name)
+
+
+def match_or_append_pairs(existing_keys, query_keys):
+    """tree.py:71-87 on the device: resolve (k, 2) integer pairs against a table whose row
+    index is the pair's position, appending unseen ones -- new rows k, k+1, ... in
+    first-occurrence order of the batch.  Returns (row per query, number of new rows)."""
+    torch = _torch()
+    ex = np.asarray(existing_keys, dtype=np.int64).reshape(-1, 2)
+    q = np.asarray(query_keys, dtype=np.int64).reshape(-1, 2)
+    for arr in (ex, q):
+        if arr.size and (arr.min() < 0 or arr.max() >= 1 << 32):
+            raise ValueError("pair entries must be in [0, 2**32)")
+    enc = lambda a: (torch.as_tensor(a[:, 0], device="cuda") << 32) | torch.as_tensor(a[:, 1], device="cuda")  # noqa: E731
+    k = len(ex)
+    if not len(q):
+        return np.zeros(0, dtype=np.int64), 0
+    qk = enc(q)
+    uq, inv = torch.unique(qk, sorted=True, return_inverse=True)
+    row = torch.full((len(uq),), -1, dtype=torch.int64, device="cuda")
+    if k:
+        ek = enc(ex)
+        es, eo = torch.sort(ek, stable=True)
+        pos = torch.searchsorted(es, uq).clamp(max=k - 1)
+        hit = es[pos] == uq
+        row = torch.where(hit, eo[pos], row)
+    miss = row < 0
+    first = torch.full((len(uq),), len(q), dtype=torch.int64, device="cuda")
+    first.scatter_reduce_(0, inv, torch.arange(len(q), device="cuda"), reduce="amin")
+    order = torch.argsort(torch.where(miss, first, torch.full_like(first, len(q) + 1)), stable=True)
+    n_new = int(miss.sum())
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(len(uq), device="cuda")
+    row = torch.where(miss, k + rank, row)
+    return row[inv].cpu().numpy(), n_new
 
 
 def init_tree(spec, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32", exact: bool = False,

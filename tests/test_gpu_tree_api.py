@@ -1,0 +1,105 @@
+"""The reference's tree / backup utility surface on the device:
+match_or_append_pairs, BeliefTree.append_actions / append_beliefs / nodes_at_depth /
+serialize / deserialize, aggregate_leaves, action_q_values -- against the reference's golden
+vectors and the oracle restatement, on identical inputs."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2510_27191_b200 as vp
+from golden_cases import load
+
+pytestmark = pytest.mark.gpu
+
+
+def test_match_or_append_pairs_equals_reference_golden():
+    g = load("formulas")
+    rows, n_new = vp.match_or_append_pairs(g["moa_existing"], g["moa_query"])
+    np.testing.assert_array_equal(rows, g["moa_rows"])
+    assert n_new == int(g["moa_new"][0])
+    rows, n_new = vp.match_or_append_pairs(np.zeros((0, 2), dtype=np.int64), [[5, 1], [2, 2], [5, 1], [0, 9]])
+    np.testing.assert_array_equal(rows, [0, 1, 0, 2])
+    assert n_new == 3
+    with pytest.raises(ValueError):
+        vp.match_or_append_pairs([[0, 0]], [[-1, 0]])
+
+
+def _grow_both(A, steps, seed):
+    """The same random append sequence on the oracle tree and the device tree."""
+    ot = oracle.ColumnarTree(A)
+    dt = vp.DeviceTree(A, precision="fp64", cap_beliefs=16, cap_actions=16)
+    g = np.random.default_rng(seed)
+    for _ in range(steps):
+        nb = ot.n_beliefs
+        k = int(g.integers(1, 300))
+        b = g.integers(0, nb, size=k)
+        a = g.integers(0, A, size=k)
+        r = g.integers(-5, 6, size=k).astype(np.float64)
+        xo = ot.append_actions(b, a, r)
+        xd = dt.append_actions(b, a, r)
+        np.testing.assert_array_equal(xd, xo)
+        o = g.integers(0, 4, size=k)
+        co = ot.append_beliefs(xo, o)
+        cd = dt.append_beliefs(xd, o)
+        np.testing.assert_array_equal(cd, co)
+    return ot, dt
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_appends_equal_oracle_tables(seed):
+    ot, dt = _grow_both(A=7, steps=6, seed=seed)
+    want, got = ot.tables(), dt.tables()
+    for k in ("parent_action", "parent_obs", "depth", "action_parent_belief", "action_id", "action_visits"):
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    np.testing.assert_array_equal(got["action_reward_sum"], want["action_reward_sum"])  # integer rewards: exact
+    np.testing.assert_array_equal(got["prefs"], want["prefs"])
+    dt.validate()
+    for d in (1, 2, 3):
+        for x, y in zip(dt.nodes_at_depth(d), ot.nodes_at_depth(d)):
+            np.testing.assert_array_equal(x, y)
+    with pytest.raises(ValueError):
+        dt.nodes_at_depth(0)
+    with pytest.raises(ValueError):
+        dt.append_actions([0, 1], [0], [0.0, 0.0])
+    with pytest.raises(ValueError):
+        dt.append_beliefs([dt.n_actions], [0])
+
+
+def test_serialize_deserialize_round_trip():
+    model = oracle.MarsModel(4, 3, layout_seed=0)
+    belief = oracle.ParticleBelief.from_model(model, 500, oracle.RowRng.from_seed(0).derive(3))
+    out = vp.plan(belief, model, oracle.SolverConfig(n_parallel=256, iterations=5), oracle.RowRng.from_seed(0),
+                  precision="fp64", keep_tree=True)
+    text = out.tree.serialize()
+    back = vp.DeviceTree.deserialize(text, precision="fp64")
+    assert back.serialize() == text
+    back.validate()
+    # the rebuilt hash indexes resolve the existing edges to their ids and append past them
+    t = back.tables()
+    np.testing.assert_array_equal(back.append_actions(t["action_parent_belief"][:50], t["action_id"][:50],
+                                                      np.zeros(50)), np.arange(50))
+    assert back.append_beliefs([0], [7]) == [t["depth"].shape[0]]
+
+
+def test_aggregate_leaves_and_q_values_equal_oracle():
+    ot, dt = _grow_both(A=5, steps=4, seed=3)
+
+    class Leaves:
+        pass
+
+    g = np.random.default_rng(9)
+    deep = np.flatnonzero(ot.depth == ot.depth.max())
+    leaves = Leaves()
+    leaves.leaf_belief_indices = g.choice(deep, size=2000)
+    leaves.heuristic_values = g.normal(size=2000)
+    lo, ld = oracle.aggregate_leaves(leaves), vp.aggregate_leaves(leaves)
+    np.testing.assert_array_equal(ld.belief_indices, lo.belief_indices)
+    np.testing.assert_array_equal(ld.visit_weights, lo.visit_weights)
+    np.testing.assert_allclose(ld.values, lo.values, rtol=1e-13, atol=1e-15)
+    acts = np.unique(ot.parent_action[lo.belief_indices])
+    qo = oracle.action_q_values(ot, acts, lo, 0.95)
+    qd = vp.action_q_values(dt, acts, ld, 0.95)
+    np.testing.assert_allclose(qd, qo, rtol=1e-13, atol=1e-13)
+    with pytest.raises(ValueError):
+        vp.action_q_values(dt, [0], ld, 0.95)  # the root's first action has no valued child here
