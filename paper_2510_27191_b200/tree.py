@@ -389,6 +389,16 @@ class DeviceTree:
     def n_actions(self) -> int:
         return self.counts()[1]
 
+    # the reference's column properties (tree.py:136-166), host arrays in reference order
+    parent_action = property(lambda s: s.tables()["parent_action"])
+    parent_obs = property(lambda s: s.tables()["parent_obs"])
+    depth = property(lambda s: s.tables()["depth"])
+    prefs = property(lambda s: s.tables()["prefs"])
+    action_parent_belief = property(lambda s: s.tables()["action_parent_belief"])
+    action_id = property(lambda s: s.tables()["action_id"])
+    action_reward_sum = property(lambda s: s.tables()["action_reward_sum"])
+    action_visits = property(lambda s: s.tables()["action_visits"])
+
     def tables(self) -> dict:
         """All columns as host numpy arrays (int64 / float64 like the reference),
         rows in reference (first-occurrence) order."""

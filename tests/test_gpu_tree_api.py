@@ -55,6 +55,8 @@ def test_appends_equal_oracle_tables(seed):
     np.testing.assert_array_equal(got["action_reward_sum"], want["action_reward_sum"])  # integer rewards: exact
     np.testing.assert_array_equal(got["prefs"], want["prefs"])
     dt.validate()
+    for k in ("parent_action", "depth", "prefs", "action_id", "action_visits"):  # column properties
+        np.testing.assert_array_equal(getattr(dt, k), getattr(ot, k), err_msg=k)
     for d in (1, 2, 3):
         for x, y in zip(dt.nodes_at_depth(d), ot.nodes_at_depth(d)):
             np.testing.assert_array_equal(x, y)
