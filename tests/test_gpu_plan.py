@@ -126,6 +126,26 @@ def test_fp64_exact_large_batches_equal_oracle(n_par):
     assert scale_close(got["prefs"], want["prefs"], 1e-9)
 
 
+@pytest.mark.parametrize("kind,n_par,iters", [("mars15_15", 65536, 10), ("synthetic", 65536, 20)])
+def test_full_size_invariants(kind, n_par, iters):
+    """BASELINE C3 / C5 at full size, fp32: properties that hold at any size -- every row adds
+    one visit per level (visit conservation), the tree validates, PSI is finite, the
+    chosen action is the root's first argmax, and depth-l beliefs never outnumber the rows."""
+    om = oracle.MarsModel(15, 15, layout_seed=3) if kind.startswith("mars") else oracle.SyntheticModel(n_actions=16,
+                                                                                                       n_obs=8, seed=3)
+    belief = oracle.ParticleBelief.from_model(om, 10_000, oracle.RowRng.from_seed(3).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=n_par, iterations=iters)
+    out = vp.plan(belief, om, cfg, oracle.RowRng.from_seed(3).derive(1, 0), keep_tree=True)
+    t = out.tree.tables()
+    assert t["action_visits"].sum() == n_par * sum(min(i + 1, cfg.d_max_cap) for i in range(iters))
+    assert np.isfinite(t["prefs"]).all()
+    assert out.chosen_action == int(np.argmax(t["prefs"][0]))
+    depth_counts = np.bincount(t["depth"])
+    assert depth_counts[0] == 1 and (depth_counts[1:] <= n_par * iters).all()
+    assert out.tree_stats == {"belief_rows": len(t["depth"]), "action_rows": len(t["action_id"])}
+    out.tree.validate()
+
+
 def test_capacity_growth_matches_preallocated():
     case = manifest()["plans"]["plan_mars4_3"]
     s = case["runs"][0]["seed"]
