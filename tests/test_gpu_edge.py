@@ -1,6 +1,7 @@
 """Edge cases of the planning step against the oracle (fp64 parity mode, tree structure bit-exact):
 row counts that do not fill warps, a saturated depth cap, other eta, |A| large enough that a
-warp stages its PSI rows in several batches, and a non-uniform reference policy (init rows)."""
+warp stages its PSI rows in several batches, a non-uniform reference policy (init rows),
+|A| = 1 or |O| = 1, heavy termination, and non-uniform or one-particle beliefs."""
 
 import numpy as np
 import pytest
@@ -77,3 +78,30 @@ def test_non_uniform_reference_policy():
     np.testing.assert_allclose(t["prefs"][-1], np.log([0.6, 0.25, 0.15]) / 2.0, rtol=1e-12)  # a lazy row
     fast = vp.plan(belief, om, cfg, rng, precision="fp32", keep_tree=True)
     fast.tree.validate()
+
+
+@pytest.mark.parametrize("n_actions,n_obs", [(1, 3), (2, 1)])
+def test_single_action_or_observation(n_actions, n_obs):
+    """|A| = 1 (one-entry softmax rows and CDFs) and |O| = 1 (every action has one child)."""
+    om = oracle.SyntheticModel(n_actions=n_actions, n_obs=n_obs, seed=2)
+    belief = oracle.ParticleBelief.from_model(om, 200, oracle.RowRng.from_seed(2).derive(3))
+    _compare(om, belief, oracle.SolverConfig(n_parallel=300, iterations=5), oracle.RowRng.from_seed(2))
+
+
+def test_heavy_termination():
+    """Half the transitions terminate: rows go absorbing mid-trajectory (terminal observation,
+    zero reward) at every level."""
+    om = oracle.SyntheticModel(term_per_mille=500, seed=4)
+    belief = oracle.ParticleBelief.from_model(om, 500, oracle.RowRng.from_seed(4).derive(3))
+    _compare(om, belief, oracle.SolverConfig(n_parallel=512, iterations=6), oracle.RowRng.from_seed(4))
+
+
+@pytest.mark.parametrize("m", [1, 7])
+def test_non_uniform_and_tiny_particle_sets(m):
+    """Root draws through the weight CDF: non-uniform weights (the binary-search path, not the
+    uniform guess) and a one-particle belief."""
+    om = oracle.MarsModel(5, 4, layout_seed=6)
+    base = oracle.ParticleBelief.from_model(om, m, oracle.RowRng.from_seed(6).derive(3))
+    w = np.arange(1, m + 1, dtype=np.float64)
+    belief = oracle.ParticleBelief(base.states, w / w.sum())
+    _compare(om, belief, oracle.SolverConfig(n_parallel=256, iterations=5), oracle.RowRng.from_seed(6))
