@@ -311,7 +311,10 @@ def run_b200(args):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e = sims / (e2e_ms / 1e3)
-    h2d = len(belief.states) * dm.state_bytes + 8 * len(belief.weights)
+    # bytes actually copied per e2e step: the particle records, plus the weight CDF unless the
+    # weights are exactly uniform (then the planner uses its cached device CDF)
+    w = np.asarray(belief.weights, dtype=np.float64)
+    h2d = len(belief.states) * dm.state_bytes + (0 if not (w != 1.0 / len(w)).any() else 8 * len(w))
 
     # profiled pass of the same steps: per-kernel-kind device time (CUDA events around every
     # launch on the planner's stream) and the traffic counters the kernels keep

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .backup import run_backup
-from .belief import DeviceBelief, ParticleBelief, sir_update
+from .belief import DeviceBelief, ParticleBelief, sir_update, uniform_cum
 from .envs._device import device_model
 from .rng import RowRng, fold, key_of
 from .search import Workspace, run_search
@@ -104,6 +104,7 @@ class Planner:
         self.precision, self.exact, self.mem_fraction = precision, exact, mem_fraction
         self.tree: DeviceTree | None = None
         self.work: Workspace | None = None
+        self.uniform_weights = False  # the last staged belief had weights of exactly 1/m
         self._cap_cache = {}
         self._out = _torch().zeros(1, dtype=_torch().int32, device="cuda")
         self.mode = 1  # vp_plan: 1 CUDA graph of the step's launches (default), 0 direct launches
@@ -177,8 +178,12 @@ class Planner:
         hp = self._buf("particles_host", nbytes, True)
         if dm.pack_into(belief.states, hp.numpy()) != nbytes:
             raise ValueError("belief states and weights differ in length")
-        hc = self._buf("cumw_host", 8 * m, True)
-        np.cumsum(weights, out=hc.numpy()[: 8 * m].view(np.float64))  # sequential fp64 (belief.py:42)
+        # weights of exactly 1/m (every SIR update leaves them so, belief.py:101): their
+        # sequential cumsum is the cached device array uniform_cum(m), bit for bit
+        self.uniform_weights = bool(m) and not (weights != 1.0 / m).any()
+        if not self.uniform_weights:
+            hc = self._buf("cumw_host", 8 * m, True)
+            np.cumsum(weights, out=hc.numpy()[: 8 * m].view(np.float64))  # sequential fp64 (belief.py:42)
         self._buf("particles_dev", nbytes, False)
         self._buf("cumw_dev", 8 * m, False)
         return m
@@ -197,7 +202,10 @@ class Planner:
         nb = m * dm.state_bytes
         pd, cd = self._bufs["particles_dev"], self._bufs["cumw_dev"]
         pd[:nb].copy_(self._bufs["particles_host"][:nb], non_blocking=True)
-        cd[: 8 * m].copy_(self._bufs["cumw_host"][: 8 * m], non_blocking=True)
+        if self.uniform_weights:
+            cd[: 8 * m].view(_torch().float64).copy_(uniform_cum(m))
+        else:
+            cd[: 8 * m].copy_(self._bufs["cumw_host"][: 8 * m], non_blocking=True)
         return pd, cd, m
 
     def plan(self, belief, model, config, rng, *, keep_tree: bool = False, inject_actions=None,
@@ -252,8 +260,11 @@ class Planner:
         a.gamma = float(spec.discount)
         a.particles_host = self._bufs["particles_host"].data_ptr() if from_host else None
         a.particles_dev = self._bufs["particles_dev"].data_ptr()
-        a.cumw_host = self._bufs["cumw_host"].data_ptr() if from_host else None
-        a.cumw_dev = self._bufs["cumw_dev"].data_ptr()
+        if from_host and self.uniform_weights:  # no weight bytes to copy: the cached uniform CDF
+            a.cumw_host, a.cumw_dev = None, uniform_cum(m).data_ptr()
+        else:
+            a.cumw_host = self._bufs["cumw_host"].data_ptr() if from_host else None
+            a.cumw_dev = self._bufs["cumw_dev"].data_ptr()
         a.keys_host, a.keys_dev = kh.data_ptr(), kd.data_ptr()
         a.out_host, a.out_dev = oh.data_ptr(), od.data_ptr()
         stream = torch.cuda.current_stream()
