@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 5
+#define VPB200_ABI_VERSION 6
 
 enum vp_status {
   VP_OK = 0,
@@ -134,7 +134,7 @@ typedef struct vp_tree {
   uint64_t* a_ckey;           /* creation key (canonical order)              */
   /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */
-  void* hash_b;               /* (action row << 32 | obs) -> belief row     */
+  void* hash_b;               /* belief key (see bkey_mode) -> belief row    */
   int32_t* counters;          /* [VP_COUNTERS]: [0] n_beliefs, [2] overflow, [VP_COUNTER_ACTIONS] n_actions
                                (the two id counters on separate 128-B lines: every warp allocates from both) */
   const double* init_prefs;   /* [|A|] initial PSI row                      */
@@ -146,7 +146,9 @@ typedef struct vp_tree {
   uint64_t* cdf_tag;          /* [cdf_slots] pass << 32 | belief of the slot's CDF (bit 31 of the
                                  low word: being written); cleared at tree reset */
   int32_t cdf_slots;          /* power of two                                */
-  int32_t pad_cdf;
+  int32_t bkey_mode;          /* belief-index key: 0 = (action row << 32 | obs); 1 = (belief << 32 |
+                                 action << 20 | obs), needs |A| <= 4096 and obs < 2^20 -- both
+                                 claims of a level can then be issued together */
   double eta;
 } vp_tree;
 

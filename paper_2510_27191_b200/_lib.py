@@ -20,7 +20,7 @@ VP_MODEL_CROWDNAV = 6
 CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 5
+ABI_VERSION = 6
 VP_COUNTERS, VP_COUNTER_ACTIONS = 64, 32  # include/vpb200.h
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
@@ -68,7 +68,7 @@ class VpTree(C.Structure):
         ("a_visits", C.c_void_p), ("a_rows", C.c_void_p), ("a_acc", C.c_void_p), ("a_ckey", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p),
-        ("cdf_cache", C.c_void_p), ("cdf_tag", C.c_void_p), ("cdf_slots", C.c_int32), ("pad_cdf", C.c_int32),
+        ("cdf_cache", C.c_void_p), ("cdf_tag", C.c_void_p), ("cdf_slots", C.c_int32), ("bkey_mode", C.c_int32),
         ("eta", C.c_double),
     ]
 

@@ -75,7 +75,7 @@ __global__ void k_rehash(vp_tree T) {
     } else {
       const int b = i - na;
       if (b == 0) continue;
-      const u64 key = ((u64)(u32)T.b_parent_action[b] << 32) | T.b_parent_obs[b];
+      const u64 key = belief_key(T, T.b_parent_belief[b], T.b_parent_act[b], T.b_parent_action[b], T.b_parent_obs[b]);
       put_final(slots(T.hash_b), T.hmask_b, key, (u32)b);
     }
   }
@@ -974,7 +974,7 @@ __global__ void k_append_beliefs(vp_tree T, const int32_t* anodes, const uint32_
   Slot* hb = slots(T.hash_b);
   const int x = anodes[i];
   const u32 o = obs[i];
-  const Claim cl = claim_key(hb, T.hmask_b, ((u64)(u32)x << 32) | o);
+  const Claim cl = claim_key(hb, T.hmask_b, belief_key(T, T.a_parent_belief[x], T.a_action[x], x, o));
   int c;
   if (cl.won) {
     c = atomicAdd(&T.counters[0], 1);

@@ -40,6 +40,33 @@ __device__ __forceinline__ u64 creation_key(u32 pass, int level, int row) {
   return ((u64)pass << 32) | ((u64)(u32)level << 24) | (u64)(u32)row;
 }
 
+// Key of belief node (parent belief b, action a -> action row x, observation o)
+// in the belief index: mode 1 does not need x, so a level can issue its action
+// and belief claims together (vp_tree.bkey_mode).
+__device__ __forceinline__ u64 belief_key(const vp_tree& T, int b, int a, int x, u32 o) {
+  return T.bkey_mode ? (((u64)(u32)b << 32) | ((u64)(u32)a << 20) | (u64)o) : (((u64)(u32)x << 32) | (u64)o);
+}
+
+// Two-phase claim: the first CAS of a probe sequence (predicated, no branch, so a
+// warp can have several claims in flight), then the rest of the probe loop.
+struct ClaimTry {
+  u64 h, old_key, old_word;
+};
+__device__ __forceinline__ ClaimTry claim_try(Slot* tab, u64 mask, u64 key, bool go) {
+  ClaimTry t{slot_hash(key) & mask, kEmptyKey, ~0ull};
+  if (go) cas128(&tab[t.h], kEmptyKey, ~0ull, key, ~0ull, t.old_key, t.old_word);
+  return t;
+}
+__device__ __forceinline__ Claim claim_finish(Slot* tab, u64 mask, u64 key, ClaimTry t) {
+  u64 h = t.h, old_key = t.old_key, old_word = t.old_word;
+  while (true) {
+    if (old_key == kEmptyKey) return Claim{(u32)h, true, ~0ull};
+    if (old_key == key) return Claim{(u32)h, false, old_word};
+    h = (h + 1) & mask;
+    cas128(&tab[h], kEmptyKey, ~0ull, key, ~0ull, old_key, old_word);
+  }
+}
+
 // Backup accumulator of a node: sum (V*N for an action, the incremental
 // exp-sum for a belief), rows delivered so far, and an integer count (sum N
 // for an action, lifetime visits of the valued actions for a belief).
@@ -416,6 +443,20 @@ __device__ __forceinline__ int warp_alloc(int* counter, bool won) {
   return base + __popc(winners & ((1u << lane_id()) - 1u));
 }
 
+// Two tables' allocations of a warp with both atomics in flight together.
+__device__ __forceinline__ void warp_alloc2(int* ca, bool wa, int* cb, bool wb, int& ida, int& idb) {
+  const u32 ma = __ballot_sync(FULL, wa), mb = __ballot_sync(FULL, wb);
+  const int fa = ma ? __ffs(ma) - 1 : 0, fb = mb ? __ffs(mb) - 1 : 0;
+  int ba = 0, bb = 0;
+  if (ma && lane_id() == fa) ba = atomicAdd(ca, __popc(ma));
+  if (mb && lane_id() == fb) bb = atomicAdd(cb, __popc(mb));
+  ba = __shfl_sync(FULL, ba, fa);
+  bb = __shfl_sync(FULL, bb, fb);
+  const u32 below = (1u << lane_id()) - 1u;
+  ida = ba + __popc(ma & below);
+  idb = bb + __popc(mb & below);
+}
+
 // ------------------------------------------------------------------ tree init (one block)
 
 template <class PsiT, bool Exact>
@@ -699,7 +740,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     }
     if (known) {
       const int x = find_key(ha, T.hmask_a, ((u64)(u32)b << 32) | (u32)a);
-      const int c = x < 0 ? -1 : find_key(hb, T.hmask_b, ((u64)(u32)x << 32) | o);
+      const int c = x < 0 ? -1 : find_key(hb, T.hmask_b, belief_key(T, b, a, x, o));
       known = c >= 0;
       if (known) {
         b = c;
@@ -815,67 +856,79 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       model_step<Model>(M, st, a, fold(lkey, 1), rg, ok, o, rw);  // level_rng.derive(1)
     }
 
-    // ---- action node (b, a): append_actions (tree.py:180-218)
-    int x = 0;
+    // ---- action node (b, a) and belief node: append_actions / append_beliefs (tree.py:180-256)
+    // With (belief, action, obs) belief keys (bkey_mode 1) the belief claim does not wait for
+    // the action's row: the first CAS of both claims and both id atomics go out together.
+    const bool early = T.bkey_mode != 0;
+    const bool interior_next = l + 1 < d;
+    const u64 key_a = ((u64)(u32)b << 32) | (u32)a;
+    const u32 grp_a = __match_any_sync(FULL, ok ? key_a : kEmptyKey);
+    const int leader_a = __ffs(grp_a) - 1;
+    const bool lead_a = ok && lane == leader_a;
+    u64 key_b = early ? belief_key(T, b, a, 0, o) : 0ull;
+    u32 grp_b = early ? __match_any_sync(FULL, ok ? key_b : kEmptyKey) : 0u;
+    int leader_b = early ? __ffs(grp_b) - 1 : 0;
+    bool lead_b = early && ok && lane == leader_b;
+    Claim cl_a{0, false, 0}, cl_b{0, false, 0};
     {
-      const u64 key = ((u64)(u32)b << 32) | (u32)a;
-      grp = __match_any_sync(FULL, ok ? key : kEmptyKey);
-      const int leader = __ffs(grp) - 1;
-      lead = ok && lane == leader;
-      Claim cl{0, false, 0};
-      if (lead) cl = claim_key(ha, T.hmask_a, key);
-      const int id = warp_alloc(&T.counters[VP_COUNTER_ACTIONS], cl.won);
-      if (cl.won) {
-        x = id;
-        if (x < T.cap_actions) {
-          // accumulators are zero (cleared at tree reset); the key is a min-reduction
-          T.a_parent_belief[x] = b;
-          T.a_action[x] = a;
-          red_min(&T.a_ckey[x], creation_key(pass, l, rg));
-        } else {
-          T.counters[2] = 1;  // overflow: the host fails the plan loudly
-        }
-        publish(ha, cl.slot, (u32)x, pass);
+      ClaimTry ta = claim_try(ha, T.hmask_a, key_a, lead_a);
+      ClaimTry tb = claim_try(hb, T.hmask_b, key_b, lead_b);  // in flight together with ta
+      if (lead_a) cl_a = claim_finish(ha, T.hmask_a, key_a, ta);
+      if (lead_b) cl_b = claim_finish(hb, T.hmask_b, key_b, tb);
+    }
+    int id_a = 0, id_b = 0;
+    warp_alloc2(&T.counters[VP_COUNTER_ACTIONS], cl_a.won, &T.counters[0], early && cl_b.won, id_a, id_b);
+    int x = 0;
+    if (cl_a.won) {
+      x = id_a;
+      if (x < T.cap_actions) {
+        // accumulators are zero (cleared at tree reset); the key is a min-reduction
+        T.a_parent_belief[x] = b;
+        T.a_action[x] = a;
+        red_min(&T.a_ckey[x], creation_key(pass, l, rg));
+      } else {
+        T.counters[2] = 1;  // overflow: the host fails the plan loudly
       }
-      __syncwarp();  // every creator of the warp has published before any lane spins
-      if (lead && !cl.won) {
-        const u64 w = wait_published(ha, cl.slot, cl.word);
-        x = (int)(u32)w;
-        if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, rg));
-      }
-      x = __shfl_sync(FULL, x, leader);
-      if (W.stats) {
-        const u32 wn = __ballot_sync(FULL, cl.won);
-        if (lane == 0 && wn) atomicAdd(&W.stats[5], (unsigned long long)__popc(wn));
-      }
+      publish(ha, cl_a.slot, (u32)x, pass);
+    }
+    __syncwarp();  // every creator of the warp has published before any lane spins
+    if (lead_a && !cl_a.won) {
+      const u64 w = wait_published(ha, cl_a.slot, cl_a.word);
+      x = (int)(u32)w;
+      if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, rg));
+    }
+    x = __shfl_sync(FULL, x, leader_a);
+    if (W.stats) {
+      const u32 wn = __ballot_sync(FULL, cl_a.won);
+      if (lane == 0 && wn) atomicAdd(&W.stats[5], (unsigned long long)__popc(wn));
     }
     ok = ok && x < T.cap_actions;
     // rewards and visits (tree.py:216-217); rows through x for the backup
     {
-      const double sum = group_sum(rw, grp, ok);
-      if (lead && ok) {
-        const int cnt = __popc(grp);
+      const double sum = group_sum(rw, grp_a, ok);
+      if (lead_a && ok) {
+        const int cnt = __popc(grp_a);
         red_add(&T.a_reward[x], sum);
         red_add(&T.a_visits[x], cnt);
         red_add(&T.a_rows[x], cnt);
       }
     }
-
-    // ---- belief node (x, o): append_beliefs (tree.py:220-256)
+    if (!early) {  // (action row, obs) keys: the belief claim needs x
+      key_b = belief_key(T, b, a, x, o);
+      grp_b = __match_any_sync(FULL, ok ? key_b : kEmptyKey);
+      leader_b = __ffs(grp_b) - 1;
+      lead_b = ok && lane == leader_b;
+      if (lead_b) cl_b = claim_key(hb, T.hmask_b, key_b);
+      id_b = warp_alloc(&T.counters[0], cl_b.won);
+    }
+    grp = grp_b;
+    lead = lead_b;
     int c = 0;
     bool c_new = false;
-    const bool interior_next = l + 1 < d;
     {
-      const u64 key = ((u64)(u32)x << 32) | o;
-      grp = __match_any_sync(FULL, ok ? key : kEmptyKey);
-      const int leader = __ffs(grp) - 1;
-      lead = ok && lane == leader;
-      Claim cl{0, false, 0};
-      if (lead) cl = claim_key(hb, T.hmask_b, key);
-      const int id = warp_alloc(&T.counters[0], cl.won);
       u32 cpass = 0;
-      if (cl.won) {
-        c = id;
+      if (cl_b.won) {
+        c = id_b;
         cpass = pass;
         if (c < T.cap_beliefs) {
           T.b_parent_action[c] = x;
@@ -890,20 +943,20 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         } else {
           T.counters[2] = 1;
         }
-        publish(hb, cl.slot, (u32)c, pass);
+        publish(hb, cl_b.slot, (u32)c, pass);
       }
       __syncwarp();
-      if (lead && !cl.won) {
-        const u64 w = wait_published(hb, cl.slot, cl.word);
+      if (lead_b && !cl_b.won) {
+        const u64 w = wait_published(hb, cl_b.slot, cl_b.word);
         c = (int)(u32)w;
         cpass = (u32)(w >> 32);
         if (cpass == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, l, rg));
       }
-      c = __shfl_sync(FULL, c, leader);
-      c_new = __shfl_sync(FULL, cpass, leader) == pass;
-      made_interior = cl.won && interior_next && c < T.cap_beliefs;
+      c = __shfl_sync(FULL, c, leader_b);
+      c_new = __shfl_sync(FULL, cpass, leader_b) == pass;
+      made_interior = cl_b.won && interior_next && c < T.cap_beliefs;
       if (W.stats) {
-        const u32 wn = __ballot_sync(FULL, cl.won);
+        const u32 wn = __ballot_sync(FULL, cl_b.won);
         if (lane == 0 && wn) atomicAdd(&W.stats[6], (unsigned long long)__popc(wn));
       }
     }

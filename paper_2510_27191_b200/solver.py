@@ -13,6 +13,7 @@ budget mode (the reference checks perf_counter after every iteration).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -153,6 +154,9 @@ class Planner:
                                            cap_beliefs=cap, cap_actions=cap)
             else:
                 t.reset(init, config.eta, device_init=device_init)
+        # (belief, action, obs) belief keys when the action and observation codes fit
+        mode = 1 if A <= 4096 and model.spec.observation_arity + 1 <= (1 << 20) else 0
+        t.set_belief_key_mode(min(mode, int(os.environ.get("VP_BKEY_MODE", "1"))))  # env: measurement only
         w = self.work
         if w is None or not w.fits(n, levels, dm.state_bytes, trace):
             w = self.work = Workspace(n, levels, dm.state_bytes, trace)

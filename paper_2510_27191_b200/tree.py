@@ -144,12 +144,22 @@ class DeviceTree:
                      "a_ckey", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.cdf_slots = self.cdf_tag.numel()
+        s.bkey_mode = getattr(self, "bkey_mode", 0)
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
         s.init_lse = self._init_lse.data_ptr()
         s.init_cdf = self._init_cdf.data_ptr()
         s.eta = self.eta
         self.struct = s
+
+    def set_belief_key_mode(self, mode: int):
+        """0: belief index keyed by (action row, obs) -- any |A|, any obs < 2^32; 1: keyed by
+        (belief, action, obs) so the search issues a level's two claims together (needs
+        |A| <= 4096 and obs codes < 2^20).  Only on an empty index (right after reset)."""
+        if mode not in (0, 1):
+            raise ValueError("belief key mode must be 0 or 1")
+        self.bkey_mode = mode
+        self.struct.bkey_mode = mode
 
     def set_eta(self, eta: float):
         if eta <= 0:
