@@ -58,6 +58,25 @@ def test_fp64_exact_plan_equals_reference_tree(name):
         out.tree.validate()
 
 
+@pytest.mark.parametrize("name", ["plan_mars7_8_small", "plan_navigation"])
+def test_general_belief_key_plan_equals_reference_tree(name, monkeypatch):
+    """The (action row, obs) belief key -- the fallback for |A| > 4096 or observation codes >= 2^20 --
+    still reproduces the reference's trees (the planner defaults to (belief, action, obs) keys)."""
+    monkeypatch.setenv("VP_BKEY_MODE", "0")
+    case = manifest()["plans"][name]
+    g = load(name)
+    run = case["runs"][0]
+    s = run["seed"]
+    om, belief, cfg, rng = plan_inputs(case, s)
+    planner = vp.Planner("fp64", exact=True)
+    out = planner.plan(belief, om, cfg, rng, keep_tree=True)
+    assert planner.tree is None or out.tree.struct.bkey_mode == 0
+    t = out.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(t[k], g[f"s{s}_{k}"].astype(np.int64), err_msg=k)
+    assert out.chosen_action == run["chosen_action"]
+
+
 def _oracle_traces(case, seed):
     om, belief, cfg, rng = plan_inputs(case, seed)
     traces = []
