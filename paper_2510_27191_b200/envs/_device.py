@@ -325,14 +325,33 @@ def navigation_descriptor(model, unpack=None) -> DeviceModel:
 # ------------------------------------------------------------------ CROWDNAV
 
 
+def crowd_pack_into(states, dst: np.ndarray) -> int:
+    """CrowdStates -> 2704-B records written straight into the byte buffer ``dst`` (pinned host
+    memory on the e2e path: one pass over the 2.7 KB records, no temporary copy)."""
+    n = len(np.asarray(states.robot))
+    rec = dst[: n * CROWD_DTYPE.itemsize].view(CROWD_DTYPE)
+    _crowd_fill(states, rec)
+    return n * CROWD_DTYPE.itemsize
+
+
 def crowd_pack(states) -> np.ndarray:
+    rec = np.zeros(len(np.asarray(states.robot)), dtype=CROWD_DTYPE)
+    _crowd_fill(states, rec)
+    return rec
+
+
+def _crowd_fill(states, rec) -> None:
     persons = np.asarray(states.persons, dtype=np.float32)
     n, p = persons.shape[:2]
     k = np.asarray(states.tracked).shape[1]
     if p > _lib.CROWD_MAX_PEOPLE or k > _lib.CROWD_MAX_TRACKED:
         raise ValueError(f"CrowdNav device records hold at most {_lib.CROWD_MAX_PEOPLE} people and "
                          f"{_lib.CROWD_MAX_TRACKED} tracked persons")
-    rec = np.zeros(n, dtype=CROWD_DTYPE)
+    if k < _lib.CROWD_MAX_TRACKED:
+        rec["prev"][:, k:] = 0.0
+        rec["tracked"][:, k:] = 0
+    if p < _lib.CROWD_MAX_PEOPLE:
+        rec["persons"][:, 2 * p:] = 0.0
     rec["robot"] = np.asarray(states.robot, dtype=np.float64)
     rec["prev"][:, :k] = np.asarray(states.prev_dist, dtype=np.float64)
     rec["code"] = np.asarray(states.last_code)
@@ -341,7 +360,6 @@ def crowd_pack(states) -> np.ndarray:
     cur = np.pad(np.asarray(states.curious, dtype=bool), ((0, 0), (0, _lib.CROWD_MAX_PEOPLE - p)))
     rec["curious"] = np.packbits(cur, axis=1, bitorder="little").view("<u4")
     rec["persons"][:, : 2 * p] = persons.reshape(n, 2 * p)
-    return rec
 
 
 def crowd_unpacker(n_people: int, n_tracked: int, states_cls):
@@ -364,7 +382,7 @@ def crowdnav_descriptor(model, unpack=None) -> DeviceModel:
         from .crowdnav import CrowdStates
 
         unpack = crowd_unpacker(int(model.n_people), int(model.n_tracked), CrowdStates)
-    dm = DeviceModel(_lib.VP_MODEL_CROWDNAV, model.spec, CROWD_DTYPE, crowd_pack, unpack)
+    dm = DeviceModel(_lib.VP_MODEL_CROWDNAV, model.spec, CROWD_DTYPE, crowd_pack, unpack, crowd_pack_into)
     d = dm.desc
     hall = np.asarray(model.hall, dtype=np.float64)
     d.crowd_people, d.crowd_tracked = int(model.n_people), int(model.n_tracked)
