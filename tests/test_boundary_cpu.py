@@ -123,6 +123,33 @@ def test_mars_word_packing_equals_field_layout(n, m):
     assert (buf[16 * 300:] == 0xAB).all()
 
 
+def test_small_record_packers_match_their_layouts():
+    """Navigation / Synthetic / Light-Dark / Tabular records: every field where the dtype (and the
+    kernel's struct) puts it, Navigation through its unpacker round trip."""
+    g = np.random.default_rng(4)
+    nav = oracle.NavigationModel()
+    st = nav.sample_initial_states(64, oracle.RowRng.from_seed(2))
+    st.terminal = g.random(64) < 0.3
+    rec = _device.nav_pack(st)
+    assert rec.dtype.itemsize == 24
+    back = _device.nav_unpacker(nav.n_unknown, oracle.NavStates)(rec)
+    for f in ("pos", "occ", "open_gate", "terminal"):
+        np.testing.assert_array_equal(getattr(back, f), getattr(st, f), err_msg=f)
+    sy = oracle.SyntheticModel(seed=1).sample_initial_states(50, oracle.RowRng.from_seed(3))
+    sy.terminal = g.random(50) < 0.5
+    r = _device.syn_pack(sy)
+    np.testing.assert_array_equal(r["word"], sy.word)
+    np.testing.assert_array_equal(r["term"].astype(bool), sy.terminal)
+    ld = oracle.LightDarkModel().sample_initial_states(50, oracle.RowRng.from_seed(3))
+    r = _device.ld_pack(ld)
+    np.testing.assert_array_equal(r["x"], ld.x)
+    np.testing.assert_array_equal(r["y"], ld.y)
+    tb = oracle.TabularStates(g.integers(0, 3, size=40), g.random(40) < 0.5)
+    r = _device.tab_pack(tb)
+    np.testing.assert_array_equal(r["idx"], tb.idx)
+    np.testing.assert_array_equal(r["term"].astype(bool), tb.terminal)
+
+
 @pytest.mark.parametrize("people,tracked", [(300, 6), (17, 8), (320, 1)])
 def test_crowdnav_record_roundtrip(people, tracked):
     model = oracle.CrowdNavModel(n_people=people, n_tracked=tracked, p_curious=0.4)
