@@ -257,6 +257,9 @@ int64_t vp_launch_count(void);
 /* ---- tree store (tree.py:100-132, 370-378) ----------------------------- */
 /* Fresh tree: root row, init PSI row + LSE, empty hash indexes. */
 int32_t vp_tree_init(const vp_tree* tree, void* stream);
+/* tree->eta changed on a live tree (search.py:86 / backup.py:75 take eta per call): recompute the
+ * initial row's LSE and CDF and every live row's cached LSE. */
+int32_t vp_tree_set_eta(const vp_tree* tree, void* stream);
 /* Rebuild both hash indexes from the node columns (after capacity growth). */
 int32_t vp_tree_rehash(const vp_tree* tree, void* stream);
 /* Copy (n_beliefs, n_actions, overflow) to host memory (3 x int32). */
@@ -286,12 +289,14 @@ int32_t vp_root_argmax(const vp_tree* tree, int32_t* out_dev, void* stream);
 /* ---- SIR belief update between planning steps (belief.py:47-102) ---------- */
 /* Propagate the m particles through G(s, action) with the counter RNG `key`
  * (rng.derive(retry), rows 0..m-1), reweight by log P(observation | s'), and
- * normalise: cum_out = cumsum of the new weights in numpy order with
- * cum_out[m-1] = 1 (belief.py:50-53).  finite_out[0] = 1 if any weight is
- * non-zero (otherwise the caller retries with the next key, belief.py:86-97). */
+ * normalise: cum_out = cumsum of the new weights with cum_out[m-1] = 1
+ * (belief.py:50-53) -- in numpy's serial order when `exact` (bit-identical
+ * resampling), else by one block-wide parallel scan.  finite_out[0] = 1 if any
+ * weight is non-zero (otherwise the caller retries with the next key,
+ * belief.py:86-97). */
 int32_t vp_sir_weigh(const vp_model* model, const void* states, const double* weights, int32_t m, int32_t action,
                      uint32_t observation, uint64_t key, void* states_out, double* logw_scratch, double* cum_out,
-                     int32_t* finite_out, void* stream);
+                     int32_t* finite_out, int32_t exact, void* stream);
 /* Systematic resampling (belief.py:47-53): out[j] = prop[first i with cum[i] > (j + u0) / m]. */
 int32_t vp_sir_resample(const vp_model* model, const void* prop, const double* cum, int32_t m, double u0,
                         void* states_out, void* stream);

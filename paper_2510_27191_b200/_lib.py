@@ -117,6 +117,7 @@ _SIGNATURES = [
     ("vp_launch_count", C.c_int64, []),
     ("vp_tree_init", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_rehash", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
+    ("vp_tree_set_eta", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_counts", C.c_int32, [C.POINTER(VpTree), p_i32, C.c_void_p]),
     ("vp_draw_root_states", C.c_int32,
      [C.POINTER(VpModel), C.POINTER(VpWork), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]),
@@ -128,7 +129,7 @@ _SIGNATURES = [
     ("vp_root_argmax", C.c_int32, [C.POINTER(VpTree), C.c_void_p, C.c_void_p]),
     ("vp_sir_weigh", C.c_int32,
      [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_uint32, C.c_uint64, C.c_void_p,
-      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     ("vp_sir_resample", C.c_int32,
      [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
     ("vp_tree_append_actions", C.c_int32,

@@ -12,7 +12,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <atomic>
 #include <map>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -53,6 +55,51 @@ __global__ void k_clear(vp_tree T) {
       reinterpret_cast<Acc*>(T.a_acc)[i] = Acc{0.0, 0u, 0u};
       T.a_ckey[i] = ~0ull;
     }
+  }
+}
+
+// eta changed on a live tree (the search / backup hooks take eta per call, search.py:86,
+// backup.py:75): the initial row's LSE and CDF (one warp) and then every live row's cached
+// LSE -- the initial LSE for lazily initial rows, the row's own LSE otherwise.
+template <class PsiT, bool Exact>
+__global__ void k_eta_init_row(vp_tree T) {
+  if (threadIdx.x >= 32) return;
+  const int A = T.action_count;
+  PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
+  double v;
+  if constexpr (Exact) {
+    v = 0.0;
+    if (threadIdx.x == 0) v = lse_exact(T.init_prefs, A, T.eta);
+    v = __shfl_sync(FULL, v, 0);
+  } else {
+    for (int a = threadIdx.x; a < A; a += 32) cdf[a] = (PsiT)T.init_prefs[a];
+    __syncwarp();
+    v = row_lse_fast<PsiT>(cdf, A, T.eta);
+  }
+  for (int a = threadIdx.x; a < A; a += 32) cdf[a] = (PsiT)T.init_prefs[a];
+  __syncwarp();
+  const PsiT total = row_cdf_inplace(cdf, A, (PsiT)(T.eta * kLog2eD), (PsiT)(T.eta * v * kLog2eD));
+  for (int a = threadIdx.x; a < A; a += 32) cdf[a] = cdf[a] / total;
+  if (threadIdx.x == 0) T.init_lse[0] = v;
+}
+
+template <class PsiT, bool Exact>
+__global__ void k_eta_rows(vp_tree T) {
+  const int nb = min(T.counters[0], T.cap_beliefs);
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+  for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+    double v;
+    if (T.b_flags[b] & 1u) {
+      v = T.init_lse[0];
+    } else if constexpr (Exact) {
+      v = 0.0;
+      if (lane_id() == 0) v = lse_exact(reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride,
+                                        T.action_count, T.eta);
+    } else {
+      v = row_lse_fast<PsiT>(psi + (size_t)b * T.psi_stride, T.action_count, T.eta);
+    }
+    if (lane_id() == 0) T.b_lse[b] = v;
   }
 }
 
@@ -177,7 +224,7 @@ static std::vector<ProfRec> g_prof_recs;
 static std::vector<cudaEvent_t> g_prof_pool;
 static size_t g_prof_used = 0;
 static bool g_prof_on = false;
-static long long g_launches = 0;
+static std::atomic<long long> g_launches{0};
 
 static cudaEvent_t prof_event() {
   if (g_prof_used == g_prof_pool.size()) {
@@ -437,9 +484,12 @@ struct GraphEntry {
   long long launches;
   unsigned long long used;
 };
+// Graph cache and capture streams are shared by every caller thread (ctypes releases the GIL):
+// guarded by one mutex; one capture stream per device, and the device is part of the key.
 static std::vector<GraphEntry> g_graphs;
 static unsigned long long g_graph_clock = 0;
-static cudaStream_t g_capture_stream = nullptr;
+static std::map<int, cudaStream_t> g_capture_streams;
+static std::mutex g_graph_mu;
 
 template <class T>
 static void append_pod(std::vector<unsigned char>& v, const T& x) {
@@ -459,7 +509,10 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
     if (int32_t rc = set_search_attr<Model, PsiT, Exact>(smem)) return rc;
   }
   if (P.mode == 0 || g_prof_on) return enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, st);
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(g_graph_mu);
   std::vector<unsigned char> key;
+  append_pod(key, dev);
   append_pod(key, T);
   append_pod(key, M);
   append_pod(key, W);
@@ -470,6 +523,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
   for (auto& e : g_graphs)
     if (e.key == key) hit = &e;
   if (!hit) {
+    cudaStream_t& g_capture_stream = g_capture_streams[dev];
     if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
       return VP_ERR_CUDA;
     cudaEvent_t ev;
@@ -478,7 +532,7 @@ static int32_t run_plan(const vp_tree& T, const vp_model& M, const vp_work& W, c
     cudaStreamWaitEvent(g_capture_stream, ev, 0);
     cudaEventDestroy(ev);
     cudaStreamSynchronize(g_capture_stream);
-    const long long l0 = g_launches;
+    const long long l0 = g_launches.load();
     if (cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return VP_ERR_CUDA;
     int32_t rc = enqueue_plan_kernels<Model, PsiT, Exact>(T, M, W, P, g_capture_stream);
     cudaGraph_t graph = nullptr;
@@ -610,9 +664,60 @@ __global__ void k_sir_normalise(const double* logw, int m, double* cum, int* fin
     finite[0] = 1;
   }
   __syncthreads();
-  if (w != cum)
-    for (int i = threadIdx.x; i < m; i += blockDim.x) cum[i] = w[i];
-  if (threadIdx.x == 0) cum[m - 1] = 1.0;
+  if (w != cum) {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) cum[i] = i == m - 1 ? 1.0 : w[i];
+  } else if (threadIdx.x == 0) {
+    cum[m - 1] = 1.0;
+  }
+}
+
+// Fast-mode normaliser (fp32 closed loops): the same max / exp / divide, but the sum and the
+// cumsum are one block-wide scan -- thread t owns the contiguous chunk [t C, t C + C) -- instead
+// of numpy's serial order, so the CDF differs from numpy's by a few ulps and a resampled index
+// can move only where (j + u0) / m falls within those ulps of a CDF edge.
+__global__ void __launch_bounds__(1024) k_sir_normalise_fast(const double* logw, int m, double* cum, int* finite) {
+  __shared__ double s_red[32];
+  const int t = threadIdx.x, nt = blockDim.x, lane = lane_id(), warp = t >> 5;
+  double mx = -INFINITY;
+  for (int i = t; i < m; i += nt) {
+    const double v = logw[i];
+    if (v > -INFINITY) mx = fmax(mx, v);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) s_red[warp] = mx;
+  __syncthreads();
+  mx = s_red[lane < (nt >> 5) ? lane : 0];
+  mx = warp_max(mx);
+  __syncthreads();
+  if (mx == -INFINITY) {
+    if (t == 0) finite[0] = 0;
+    return;
+  }
+  const int C = (m + nt - 1) / nt;
+  const int lo = min(m, t * C), hi = min(m, lo + C);
+  double loc = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const double e = exp(logw[i] - mx);
+    cum[i] = e;
+    loc += e;
+  }
+  // block exclusive scan of the chunk sums
+  const double incl = warp_inclusive_scan(loc);
+  if (lane == 31) s_red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const double v = lane < (nt >> 5) ? s_red[lane] : 0.0;
+    s_red[lane] = warp_inclusive_scan(v);
+  }
+  __syncthreads();
+  const double total = s_red[(nt >> 5) - 1];
+  double run = incl - loc + (warp ? s_red[warp - 1] : 0.0);
+  const double inv = 1.0 / total;
+  for (int i = lo; i < hi; ++i) {
+    run += cum[i];
+    cum[i] = i == m - 1 ? 1.0 : run * inv;
+  }
+  if (t == 0) finite[0] = 1;
 }
 
 template <class Model>
@@ -742,7 +847,7 @@ int32_t vp_profile_read(double* ms_by_kind, int64_t* launches_by_kind, int32_t n
   return KK_COUNT;
 }
 
-int64_t vp_launch_count(void) { return g_launches; }
+int64_t vp_launch_count(void) { return g_launches.load(); }
 
 int32_t vp_abi_layout(int32_t* out, int32_t n) {
   // sizes and a few field offsets so the host binding can verify its mirror
@@ -779,6 +884,19 @@ int32_t vp_tree_init(const vp_tree* t, void* stream) {
   const vp_tree T = *t;
   return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
     return enqueue_tree_reset<decltype(z), decltype(ex)::value>(T, st);
+  });
+}
+
+int32_t vp_tree_set_eta(const vp_tree* t, void* stream) {
+  if (!t || !(t->eta > 0.0) || t->action_count < 1) return VP_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_tree T = *t;
+  return dispatch_psi(T.psi_dtype, T.exact, [&](auto z, auto ex) -> int32_t {
+    typedef decltype(z) PsiT;
+    constexpr bool E = decltype(ex)::value;
+    { Launch L_(KK_TREE_INIT, st); k_eta_init_row<PsiT, E><<<1, 32, 0, st>>>(T); }
+    { Launch L_(KK_TREE_INIT, st); k_eta_rows<PsiT, E><<<num_sms() * 8, 256, 0, st>>>(T); }
+    return check_launch();
   });
 }
 
@@ -889,7 +1007,7 @@ int32_t vp_root_argmax(const vp_tree* t, int32_t* out_dev, void* stream) {
 
 int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weights, int32_t m, int32_t action,
                      uint32_t observation, uint64_t key, void* states_out, double* logw, double* cum, int32_t* finite,
-                     void* stream) {
+                     int32_t exact, void* stream) {
   if (!mdl || !states || !weights || m < 1 || !states_out || !logw || !cum || !finite) return VP_ERR_INVALID;
   if (action < 0 || action >= mdl->action_count || observation > (uint32_t)mdl->obs_arity) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
@@ -909,11 +1027,14 @@ int32_t vp_sir_weigh(const vp_model* mdl, const void* states, const double* weig
                                                                      m, action, observation, key,
                                                                      reinterpret_cast<State*>(states_out), logw);
     }
-    {
+    if (exact) {
       const size_t smem = m <= kSirSmem ? (size_t)m * sizeof(double) : 0;
       if (!ensure_smem_optin((const void*)k_sir_normalise, kSirSmem * sizeof(double))) return VP_ERR_CUDA;
       Launch L_(KK_HOOK, st);
       k_sir_normalise<<<1, 1024, smem, st>>>(logw, m, cum, finite);
+    } else {
+      Launch L_(KK_HOOK, st);
+      k_sir_normalise_fast<<<1, 1024, 0, st>>>(logw, m, cum, finite);
     }
     return check_launch();
   });

@@ -312,6 +312,10 @@ class Planner:
                     while grown < max(need_b, need_a):
                         grown *= 2
                     if grown > self.node_budget(tree.action_count, fraction=0.85):
+                        if config.iterations is not None:  # the reference always runs `iterations`
+                            raise _lib.CapacityError(
+                                f"a {config.iterations}-iteration plan does not fit in HBM after "
+                                f"{done} iterations ({nb} beliefs, {na} actions)")
                         stopped = "memory"
                         break
                 tree.ensure_capacity(need_b, need_a)
@@ -437,8 +441,9 @@ def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str 
         if bool(env_state.terminal[0]):
             reason = "terminal"
             break
+        # fp32 fast mode also takes the parallel-scan SIR normaliser; fp64 keeps numpy's order
         upd = sir_update(belief, model, a, int(res.observations[0]), root.derive(NS_SIR, t),
-                         max_retries=config.max_sir_retries)
+                         max_retries=config.max_sir_retries, exact=precision != "fp32")
         degenerate += int(upd.degenerate)
         env_state = model.refresh_executed(env_state)
         if device_belief:

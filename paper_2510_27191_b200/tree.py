@@ -161,11 +161,17 @@ class DeviceTree:
         self.bkey_mode = mode
         self.struct.bkey_mode = mode
 
-    def set_eta(self, eta: float):
+    def set_eta(self, eta: float, *, refresh: bool = True):
+        """Change eta.  On a live tree the cached per-row LSEs and the initial row's LSE / CDF
+        depend on eta, so ``refresh`` recomputes them on the device (the reference tree is
+        eta-free: search / backup take eta per call, search.py:86, backup.py:75)."""
         if eta <= 0:
             raise ValueError("eta must be positive")
+        changed = float(eta) != self.eta
         self.eta = float(eta)
         self.struct.eta = self.eta
+        if changed and refresh:
+            _lib.call("vp_tree_set_eta", C.byref(self.struct), _stream())
 
     def reset(self, init_prefs=None, eta: float | None = None, device_init: bool = True):
         """Fresh tree (tree.py:103-132): root row, no actions, init PSI row.
@@ -174,7 +180,7 @@ class DeviceTree:
         ``vp_plan`` call (which starts every planning step with it)."""
         torch = _torch()
         if eta is not None:
-            self.set_eta(eta)
+            self.set_eta(eta, refresh=False)  # the reset below recomputes everything
         A = self.action_count
         base = np.zeros(A) if init_prefs is None else np.asarray(init_prefs, dtype=np.float64)
         if base.shape != (A,) or not np.all(np.isfinite(base)):
@@ -436,14 +442,6 @@ class DeviceTree:
             "action_visits": self.a_visits[:na][aorder].cpu().numpy().astype(np.int64),
         }
 
-    parent_action = property(lambda s: s.tables()["parent_action"])
-    parent_obs = property(lambda s: s.tables()["parent_obs"])
-    depth = property(lambda s: s.tables()["depth"])
-    prefs = property(lambda s: s.tables()["prefs"])
-    action_parent_belief = property(lambda s: s.tables()["action_parent_belief"])
-    action_id = property(lambda s: s.tables()["action_id"])
-    action_reward_sum = property(lambda s: s.tables()["action_reward_sum"])
-    action_visits = property(lambda s: s.tables()["action_visits"])
 
     def root_prefs(self) -> np.ndarray:
         return self.psi[0, : self.action_count].cpu().numpy().astype(np.float64)

@@ -2,6 +2,7 @@
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py            # everything
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py crowdnav   # only the CrowdNav cases
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py large      # only the C2 / C3 digests
 
 Imports ``vecpomdp`` from /root/reference/pkg/src (read-only, never copied)
 and writes small ``.npz`` fixtures next to this script.  The GPU box has no
@@ -13,6 +14,8 @@ Cases (see SURVEY.md section 4 "parity ladder" and Appendix C):
                  aggregate_leaves / action_q_values examples
 * plan_*      -- full ``plan()`` trees on MARS, Tiger and (reference solver
                  driving the oracle's new models) Synthetic and Light-Dark
+* large_*     -- digests of full-size C2 / C3 ``plan()`` trees (MARS(11,11) 16384 x 10,
+                 MARS(15,15) 65536 x 10)
 * episode_*   -- closed-loop ``run_episode`` records
 """
 
@@ -238,7 +241,65 @@ def gen_crowd_steps():
     np.savez_compressed(os.path.join(HERE, "crowd_steps.npz"), **out)
 
 
+# Full-size BASELINE configs: the trees are too large to commit,
+# so each run stores SHA-256 digests of every integer column in reference order (and of the
+# reward sums, which are exact integers for MARS), the per-depth belief counts, the root PSI row
+# the PSI row sums of the first LARGE_HEAD rows, and per-depth totals of the row sums and of |PSI|.
+# (name, (n, m), n_parallel, iterations, [(seed, plan step t)])  -- plan key RowRng(seed).derive(1, t)
+LARGE_CASES = [
+    ("large_c2", (11, 11), 16384, 10, [(1000, 5), (1000, 24)]),
+    ("large_c3", (15, 15), 65536, 10, [(1000, 0)]),
+]
+LARGE_PARTICLES = 10_000
+LARGE_HEAD = 1 << 15
+
+
+def column_digests(tree) -> dict:
+    import hashlib
+
+    cols = {"parent_action": tree.parent_action, "parent_obs": tree.parent_obs, "depth": tree.depth,
+            "action_parent_belief": tree.action_parent_belief, "action_id": tree.action_id,
+            "action_visits": tree.action_visits}
+    out = {k: hashlib.sha256(np.ascontiguousarray(v, dtype="<i8").tobytes()).hexdigest() for k, v in cols.items()}
+    out["action_reward_sum"] = hashlib.sha256(
+        np.ascontiguousarray(tree.action_reward_sum, dtype="<f8").tobytes()).hexdigest()
+    return out
+
+
+def gen_large(cases=LARGE_CASES):
+    manifest = {}
+    for name, (n, m), n_par, iters, runs in cases:
+        arrays, meta = {}, []
+        for seed, t in runs:
+            model = MarsModel(n=n, m=m, layout_seed=seed)
+            belief = ref.ParticleBelief.from_model(model, LARGE_PARTICLES, ref.RowRng.from_seed(seed).derive(3))
+            cfg = ref.SolverConfig(n_parallel=n_par, iterations=iters, eta=2.0)
+            out = ref.plan(belief, model, cfg, ref.RowRng.from_seed(seed).derive(1, t))
+            tree = out.tree
+            tag = f"s{seed}_t{t}"
+            arrays[f"{tag}_prefs_root"] = tree.prefs[0].copy()
+            rs = tree.prefs.sum(axis=1)
+            arrays[f"{tag}_prefs_row_sum_head"] = rs[:LARGE_HEAD].copy()
+            arrays[f"{tag}_prefs_row_sum_by_depth"] = np.bincount(tree.depth, weights=rs)
+            arrays[f"{tag}_prefs_abs_sum_by_depth"] = np.bincount(tree.depth, weights=np.abs(tree.prefs).sum(axis=1))
+            arrays[f"{tag}_depth_counts"] = np.bincount(tree.depth).astype(np.int64)
+            meta.append({"seed": seed, "t": t, "chosen_action": out.chosen_action, "tree_stats": out.tree_stats,
+                         "iterations_run": out.iterations_run, "digests": column_digests(tree)})
+            print(name, tag, out.tree_stats, out.chosen_action, flush=True)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+        manifest[name] = {"mars": [n, m], "n_parallel": n_par, "iterations": iters, "particles": LARGE_PARTICLES,
+                          "eta": 2.0, "runs": meta}
+    return manifest
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["large"]:
+        with open(os.path.join(HERE, "manifest.json")) as f:
+            manifest = json.load(f)
+        manifest["large_plans"] = gen_large()
+        with open(os.path.join(HERE, "manifest.json"), "w") as f:
+            json.dump(manifest, f, indent=1, sort_keys=True)
+        sys.exit(0)
     if sys.argv[1:] == ["crowdnav"]:
         gen_crowd_steps()
         with open(os.path.join(HERE, "manifest.json")) as f:
@@ -252,7 +313,7 @@ if __name__ == "__main__":
     gen_navigation_steps()
     gen_rng()
     gen_formulas()
-    manifest = {"plans": gen_plans(), "episodes": dict(gen_episodes(), episode_crowdnav40=gen_crowd_episodes()),
+    manifest = {"plans": gen_plans(), "large_plans": gen_large(), "episodes": dict(gen_episodes(), episode_crowdnav40=gen_crowd_episodes()),
                 "numpy": np.__version__, "reference": "/root/reference/pkg/src/vecpomdp @ 0.1.0"}
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump(manifest, f, indent=1, sort_keys=True)

@@ -65,7 +65,7 @@ def _campaign_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         # stand-in episodes (no GPU): the record of run i depends only on i
-        camp.run_one = lambda cfg, i: _records([float(i) * 1.5 - 2.0])[0] | {"run_index": i, "seed": i}
+        camp.play = lambda cfg, i: _records([float(i) * 1.5 - 2.0])[0] | {"run_index": i, "seed": i}
         cfg = CampaignConfig(problem="tiger", runs=7)
         recs, summ = camp.run_campaign(cfg, rank, world)
         q.put((rank, [r["run_index"] for r in recs], summ["metrics"]["discounted_return"]["mean"]))

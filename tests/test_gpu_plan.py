@@ -319,3 +319,38 @@ def test_fp32_modes_agree(mode):
     for k in INT_COLUMNS:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
     assert scale_close(a["prefs"], b["prefs"], 1e-5)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_search_backup_api_after_eta_change(precision):
+    """The reference tree is eta-free: search / backup take eta per call (search.py:86,
+    backup.py:75).  A device tree grown at eta = 2 and then searched and backed up at eta = 1
+    must use LSEs / CDFs of eta = 1 everywhere (cached row LSEs and the initial row's CDF are
+    recomputed on the eta change)."""
+    om = oracle.MarsModel(4, 3, layout_seed=1)
+    belief = oracle.ParticleBelief.from_model(om, 500, oracle.RowRng.from_seed(1).derive(3))
+    rng = oracle.RowRng.from_seed(1).derive(1, 0)
+    cfg = oracle.SolverConfig(n_parallel=64, iterations=3, eta=2.0)
+    traces = []
+    ref = oracle.plan(belief, om, cfg, rng, traces=traces)
+    inject = [np.stack([lv["actions"] for lv in it["levels"]]) for it in traces]
+    exact = precision == "fp64"
+    dev = vp.plan(belief, om, cfg, rng, precision=precision, exact=exact, keep_tree=True,
+                  inject_actions=inject).tree
+    tree_o = ref.tree
+    n = 64
+    states = belief.sample_states(n, rng.derive(11))
+    start = np.zeros(n, dtype=np.int64)
+    # oracle draws at eta = 1, injected into the device search for fp32 (fp64 exact draws itself)
+    tr_o = []
+    leaves_o = oracle.search(tree_o, om, oracle.SearchBatch(start, states, depth=0), 3, 1.0, rng.derive(12),
+                             trace=tr_o)
+    kw = {} if exact else {"inject_actions": np.stack([lv["actions"] for lv in tr_o])}
+    leaves_d = vp.search(dev, om, vp.SearchBatch(start, states, depth=0), 3, 1.0, vp.RowRng(rng.derive(12).key), **kw)
+    np.testing.assert_array_equal(leaves_d.leaf_belief_indices, leaves_o.leaf_belief_indices)
+    oracle.backup(tree_o, leaves_o, 3, 1.0, om.spec.discount)
+    vp.backup(dev, leaves_d, 3, 1.0, om.spec.discount)
+    want, got = tree_o.tables(), dev.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    assert scale_close(got["prefs"], want["prefs"], 1e-10 if exact else 1e-5)

@@ -55,7 +55,7 @@ def test_log_weights_match_oracle(kind, seed):
     cum = torch.empty(m, dtype=torch.float64, device="cuda")
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("vp_sir_weigh", C.byref(dbel.dm.desc), dbel.records.data_ptr(), dbel.weights_dev.data_ptr(), m, a, o,
-              key_of(key), prop.data_ptr(), logw.data_ptr(), cum.data_ptr(), flag.data_ptr(),
+              key_of(key), prop.data_ptr(), logw.data_ptr(), cum.data_ptr(), flag.data_ptr(), 1,
               torch.cuda.current_stream().cuda_stream)
     res = om.step_batch(belief.states, np.full(m, a), key.bind(np.arange(m)))
     with np.errstate(divide="ignore"):
@@ -79,6 +79,21 @@ def test_device_sir_equals_oracle_sir(kind, seed):
     assert (got.retries, got.degenerate) == (want.retries, want.degenerate)
     _states_equal(got.belief.states, want.belief.states)
     np.testing.assert_array_equal(got.belief.weights, want.belief.weights)
+
+
+@pytest.mark.parametrize("kind", sorted(MODELS))
+@pytest.mark.parametrize("seed", [0, 1])
+def test_fast_sir_normaliser_matches_exact(kind, seed):
+    """The fast mode's parallel-scan weight CDF (exact=False) resamples the same particles as
+    numpy's serial order except where (j + u0) / m lies within a few ulps of a CDF edge."""
+    om, pm, belief, a, o = _scenario(kind, seed)
+    rng = oracle.RowRng.from_seed(seed).derive(2, 1)
+    want = vp.sir_update(vp.DeviceBelief.from_host(belief, pm), pm, a, o, rng, max_retries=3, exact=True)
+    got = vp.sir_update(vp.DeviceBelief.from_host(belief, pm), pm, a, o, rng, max_retries=3, exact=False)
+    assert (got.retries, got.degenerate) == (want.retries, want.degenerate)
+    rw, rg = want.belief.records.cpu().numpy(), got.belief.records.cpu().numpy()
+    differ = np.any(rw.reshape(len(rw), -1) != rg.reshape(len(rg), -1), axis=1)
+    assert differ.sum() <= 2, differ.sum()
 
 
 def test_device_sir_degenerate_observation():
