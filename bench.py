@@ -9,12 +9,16 @@ eta = 2.0, a 10 000-particle belief.  A "step" is one whole planning step.
 
 * ``value``  -- simulations/s with the belief already resident in HBM: each
   step is tree reset + 10 x (root draw, search, backup) + root argmax, timed
-  with CUDA events on the planner's stream; the per-step tree arena (~1 GB)
-  exceeds the 126 MB L2, so no explicit flush is needed.
+  with CUDA events on the planner's stream around each step; L2 is flushed
+  (256 MB write) between steps, outside the events.
 * ``e2e``    -- the same metric through the public ``plan()`` call with the
   particle StateBatch on the host (pack + pinned H2D + D2H of the action).
 * ``roofline`` -- the dominant kernel's algorithmic bytes per launch over its
-  CUDA-event duration (profiled pass of the same steps) vs MEASURED_PEAKS.
+  CUDA-event duration (profiled pass of the same steps) vs MEASURED_PEAKS, and
+  beside it a latency floor: dependent L2 round trips per level x the L2 load /
+  atomic latency measured on this GPU (vp_probe_latency).
+* ``secondary`` -- (N = 1) the same measurements for C3 (RockSample(15,15),
+  65 536 x 10), C5 (Synthetic, 65 536 x 20) and the headline in fp64.
 * ``cpu_baseline`` -- the CPU oracle (numpy port of the reference) timed on
   this host, one core, on one planning step of the same workload.
 * ``--impl reference`` -- the reference algorithm on the host CPU (the oracle
@@ -70,6 +74,8 @@ def parse():
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false",
+                    help="skip the secondary workloads (C3, C5, fp64 C2) measured beside the headline at N = 1")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--episodes", type=int, default=3, help="closed-loop episodes reported beside the step metric")
     ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
@@ -99,16 +105,17 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(args, world, actions=None, sharded=False):
+def workload_config(args, actions):
+    """The workload, identical in the b200 and reference arms (how it is executed goes to the line's
+    top-level "execution" key)."""
     c = CONFIGS[args.config]
     return {"workload": f"{c['name']} plan(), n_parallel={args.n_parallel}, iterations={args.iterations}",
             "config_id": args.config, "problem": c["name"], "actions": actions, "n_parallel": args.n_parallel,
             "iterations": args.iterations, "eta": WORKLOAD["eta"], "particles": WORKLOAD["particles"],
             "simulations_per_step": args.n_parallel * args.iterations,
             "episode_steps_per_step": args.n_parallel * sum(range(1, args.iterations + 1)),
-            "parallelism": (f"sharded x{world}: {args.n_parallel} rows per GPU, one tree, NCCL all-gather of "
-                            f"trajectories per pass" if sharded else f"replicas x{world}") if world > 1 else "1 GPU",
-            "l2": "per-step tree arena (~1 GB) > 126 MB L2; no flush needed"}
+            "parallelism": "one plan() per step",
+            "l2": "flushed between timed steps (256 MB write, outside the per-step CUDA events)"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -199,39 +206,65 @@ class ClockSampler:
 
 
 def algorithmic_bytes(st, n, S, A, psi_b, passes):
-    """Compulsory HBM bytes of the search and backup kernels summed over `passes`
-    passes, from the device traffic counters (adapted to the
-    fused design: states and frontier ids stay in registers across levels).
+    """Compulsory HBM bytes of the search and backup kernels summed over `passes` passes, from
+    the device traffic counters (adapted to the fused design: states and
+    frontier ids stay in registers across levels; node fields at element granularity, hash
+    probes at 32-B sector granularity; lazily initial PSI rows are neither written nor read).
 
-    U   interior beliefs visited (rows sampled from), Unf those whose PSI row is not
-        lazily initial (read by the sampler), P distinct action nodes visited,
-        L distinct leaves, NA / NB new action / belief rows.
+    U   interior beliefs backed up (= distinct beliefs sampled from), Unf those whose PSI row was
+        not the initial row (the only rows the sampler and the backup must read), P distinct
+        action nodes visited, L distinct leaves, NA / NB new action / belief nodes.
     """
     U, P, L, NA, NB, Unf = st[0], st[1], st[7], st[5], st[6], st[8]
     children = (U - passes) + L  # distinct (a, o) probes: every visited non-root belief
-    search = (n * passes * max(S, 32)          # root-state gather (one sector per row)
-              + psi_b * A * Unf                # PSI row per distinct non-fresh belief per level
-              + psi_b * A * (U - Unf)          # lazily initial rows written once (interior now)
-              + 32 * (P + children)            # one hash sector per distinct probe
-              + 16 * P                         # reward / visit / row reductions
-              + 52 * NA + 56 * NB              # new node columns
-              + 8 * L)                         # leaf heuristic sums
-    backup = (12 * children                    # child (parent, V, N) reads
-              + 96 * P                         # action stats + Q scratch + sector-granular PSI scatter
-              + (psi_b * A + 8) * U)           # one PSI row read + V/N write per belief
+    search = (n * passes * S                   # root-state gather
+              + psi_b * A * Unf                # PSI row per distinct non-initial belief sampled
+              + 32 * (P + children)            # one hash sector per distinct probe (claims)
+              + 16 * P                         # reward / visit / row reductions per action
+              + 16 * NA + 40 * NB              # new node columns
+              + 12 * L)                        # leaf heuristic sums + leaf list
+    backup = (24 * L                           # leaf (rows, value) read + reset
+              + (52 + 2 * psi_b) * P           # action stats, accumulator r/w, PSI cell r/w
+              + 76 * U                         # belief LSE / rows / flags / parents, accumulator r/w
+              + psi_b * A * Unf)               # full-row LSE of non-initial rows
     return search, backup
+
+
+# dependent global round trips on a warp's critical path per level (DESIGN.md section 4):
+# search = PSI-row / CDF-tag fetch + child flags (loads), (b,a)+(a,o) claim CAS + id allocation
+# (atomics); backup = node fetch (load) + delivery to the parent (atomic)
+ROUND_TRIPS = {"search": {"load": 2, "atomic": 2}, "backup": {"load": 1, "atomic": 1}}
+
+
+def probe_latency(vp_lib, torch) -> dict:
+    """Unloaded L2 load and L2 atomic round-trip latency on this GPU (vp_probe_latency: one thread
+    chasing a random cycle of 128-B lines in a 64 MB, L2-resident buffer)."""
+    lines = 1 << 19
+    perm = torch.randperm(lines, device="cuda", dtype=torch.int64)
+    nxt = torch.zeros(lines * 16, dtype=torch.int64, device="cuda")
+    nxt[perm * 16] = torch.roll(perm, -1) * 16
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    res = {}
+    for name, atomic in (("l2_load", 0), ("l2_atomic", 1)):
+        vals = []
+        for rep in range(3):
+            vp_lib.call("vp_probe_latency", nxt.data_ptr(), 20000, atomic, int(perm[0].item()) * 16, out.data_ptr(),
+                        stream)
+            torch.cuda.synchronize()
+            vals.append(out[:2].cpu().numpy().copy())
+        best = min(vals, key=lambda v: v[0])
+        res[name] = {"ns": round(float(best[0]), 1), "cycles": round(float(best[1]), 1)}
+    del nxt, perm
+    return res
 
 
 # ---------------------------------------------------------------- b200 arm
 
 
-def run_b200(args):
+def _dist_setup(args):
     import torch
     import torch.distributed as dist
-
-    import paper_2510_27191_b200 as vp
-    from paper_2510_27191_b200 import _lib
-    from paper_2510_27191_b200.rng import key_of
 
     rank, world, local = dist_env()
     local = local % max(1, torch.cuda.device_count())  # VP_DIST_BACKEND=gloo check on one GPU
@@ -244,6 +277,19 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    return rank, world, local
+
+
+def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None) -> dict:
+    """One workload: device-timed planning steps (belief resident), the same through the public
+    plan() with host buffers (e2e), and a profiled pass (per-kernel times + traffic counters)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_27191_b200 as vp
+    from paper_2510_27191_b200 import _lib
+    from paper_2510_27191_b200.rng import key_of
+
     sharded = world > 1 and args.multi == "sharded"
     # sharded: ONE planning step over world * n_parallel rows (same seed on every rank);
     # replicas: every rank plans its own problem
@@ -283,19 +329,33 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # L2 flush between timed steps (outside the timed events): a 256 MB write, twice the L2
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def timed(fn, t0, count):
+        """Per-step CUDA events on the planner's stream with an L2 flush between steps; returns
+        (sum of step times in ms, outputs)."""
+        evs, outs = [], []
+        for t in range(count):
+            flush_buf.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            outs.append(fn(t0 + t))
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs), outs
+
     for t in range(args.warmup):
         step(t)
     barrier()
-    clocks = ClockSampler(local)
+    sampler = ClockSampler(local) if clocks else None
     launches0 = _lib.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    outs = [step(args.warmup + t) for t in range(args.steps)]
-    ev1.record()
+    elapsed, outs = timed(step, args.warmup, args.steps)
     barrier()
-    launches = _lib.launch_count() - launches0
-    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0  # the library's own launches (flushes are torch's)
+    elapsed_ms = max_over_ranks(elapsed)
+    clk = sampler.stop() if sampler else None
     sims = args.n_parallel * args.iterations * args.steps * world
     value = sims / (elapsed_ms / 1e3)
 
@@ -303,18 +363,22 @@ def run_b200(args):
     for t in range(args.warmup):
         plan_e2e(t)
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for t in range(args.steps):
-        out = plan_e2e(args.warmup + t)
-    e1.record()
+    e2e_elapsed, _ = timed(plan_e2e, args.warmup, args.steps)
     barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_ms = max_over_ranks(e2e_elapsed)
     e2e = sims / (e2e_ms / 1e3)
     # bytes actually copied per e2e step: the particle records, plus the weight CDF unless the
     # weights are exactly uniform (then the planner uses its cached device CDF)
     w = np.asarray(belief.weights, dtype=np.float64)
     h2d = len(belief.states) * dm.state_bytes + (0 if not (w != 1.0 / len(w)).any() else 8 * len(w))
+
+    res = {"value": round(value, 1), "ms_per_step": round(elapsed_ms / args.steps, 4),
+           "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
+                   "ms_per_step": round(e2e_ms / args.steps, 4)},
+           "gpu_launches": int(launches), "clocks": clk, "actions": A,
+           "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
+    if not profile:
+        return res
 
     # profiled pass of the same steps: per-kernel-kind device time (CUDA events around every
     # launch on the planner's stream) and the traffic counters the kernels keep
@@ -339,11 +403,16 @@ def run_b200(args):
     S = dm.state_bytes
     passes = prof_steps * args.iterations
     b_search, b_backup = algorithmic_bytes(st, args.n_parallel, S, A, psi_b, passes)
+    levels_per_pass = st[4] / max(1.0, args.n_parallel * passes)
 
     # measured DRAM bytes per launch of the same workload (ncu launch list, scripts/ncu_capture.sh +
     # scripts/launch_traffic.py), committed under profiles/
     tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
-    measured = json.load(open(tpath))["kernels"] if os.path.exists(tpath) and world == 1 else {}
+    measured = {}
+    if os.path.exists(tpath) and world == 1:
+        tj = json.load(open(tpath))
+        if tj.get("precision", "fp32") == args.precision and tj.get("n_parallel", args.n_parallel) == args.n_parallel:
+            measured = tj["kernels"]
 
     def roof(kind, kname, total_bytes, formula):
         ms, cnt = kinds.get(kind, (0.0, 0))
@@ -353,37 +422,86 @@ def run_b200(args):
         avg_ms = ms / cnt
         ach = per_launch / (avg_ms / 1e3) / 1e9
         traffic = measured.get(kname, {}).get("dram_bytes_per_launch")
-        return {"kernel": kname, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": round(traffic) if traffic else None,
-                "traffic_source": f"profiles/traffic_{args.config}.json (ncu dram__bytes_read+write, "
-                                  f"avg per launch)" if traffic else None,
-                "bytes_per_launch": round(per_launch),
-                "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
-                "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+        out = {"kernel": kname, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+               "frac": round(ach / peak, 4), "traffic": round(traffic) if traffic else None,
+               "traffic_source": f"profiles/traffic_{args.config}.json (ncu dram__bytes_read+write, "
+                                 f"avg per launch)" if traffic else None,
+               "bytes_per_launch": round(per_launch),
+               "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
+               "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+        if latency:
+            rt = ROUND_TRIPS[kind]
+            lvl_ns = rt["load"] * latency["l2_load"]["ns"] + rt["atomic"] * latency["l2_atomic"]["ns"]
+            floor_us = levels_per_pass * lvl_ns / 1e3
+            out["latency"] = {"bound": "l2_round_trips", "levels_per_launch": round(levels_per_pass, 2),
+                              "round_trips_per_level": rt, "ns_per_level": round(lvl_ns, 1),
+                              "floor_us": round(floor_us, 2), "frac": round(floor_us / (avg_ms * 1e3), 4),
+                              "latency_source": "vp_probe_latency (unloaded, this GPU)"}
+        return out
 
     roof_search = roof("search", "k_search", b_search,
-                       "n max(S,32) + psi_b|A| U + 48 P + 32 children + 52 NA + 56 NB + 8 L per pass (bench.algorithmic_bytes)")
+                       "n S + psi_b|A| Unf + 48 P + 32 children + 16 NA + 40 NB + 12 L per pass (bench.algorithmic_bytes)")
     roof_backup = roof("backup", "k_backup", b_backup,
-                       "12 children + 96 P + (psi_b|A| + 8) U per pass (bench.algorithmic_bytes)")
-    dominant = {"search": roof_search, "backup": roof_backup}.get(top) or roof_search
-    kernel_table = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
-                    for k, v in kinds.items()}
+                       "24 L + (52 + 2 psi_b) P + 76 U + psi_b|A| Unf per pass (bench.algorithmic_bytes)")
     names = ["interior_beliefs", "actions_visited", "psi_rows_staged", "search_launches", "row_levels",
              "new_actions", "new_beliefs", "leaves", "psi_rows_read"]
-    traffic = {nm: st[i] / prof_steps for i, nm in enumerate(names)}
+    res.update({
+        "roofline": {"search": roof_search, "backup": roof_backup}.get(top) or roof_search,
+        "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},
+        "kernels": {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
+                    for k, v in kinds.items()},
+        "dominant_kernel": top,
+        "traffic_per_step": {nm: st[i] / prof_steps for i, nm in enumerate(names)},
+        "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1)})
+    res["_model"] = model
+    return res
 
-    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+
+# secondary workloads measured beside the headline at N = 1 (BASELINE configs[2] and [4] and the
+# reference precision of the headline)
+SECONDARY = [("c3", "fp32"), ("c5", "fp32"), ("c2", "fp64")]
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_27191_b200 as vp
+    from paper_2510_27191_b200 import _lib
+
+    rank, world, local = _dist_setup(args)
+    sharded = world > 1 and args.multi == "sharded"
+    latency = probe_latency(_lib, torch) if world == 1 else None
+    main = measure(args, rank, world, local, latency=latency)
+    model = main.pop("_model")
+    line = {"metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
             "data": "synthetic (MARS belief sampled from the model; no dataset)",
-            "config": workload_config(args, world, A, sharded),
-            "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
-                    "ms_per_step": round(e2e_ms / args.steps, 4)},
-            "gpu_launches": int(launches), "clocks": clk, "roofline": dominant,
-            "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},
-            "kernels": kernel_table, "dominant_kernel": top, "traffic_per_step": traffic,
-            "episode_steps_per_s": round(value * sum(range(1, args.iterations + 1)) / args.iterations, 1),
-            "tree_stats": outs[-1].tree_stats, "chosen_action": outs[-1].chosen_action}
+            "config": workload_config(args, main["actions"]),
+            "execution": (f"sharded x{world}: {args.n_parallel} rows per GPU, one tree, NCCL all-gather of "
+                          f"trajectories per pass" if sharded else f"replicas x{world}") if world > 1 else "1 GPU",
+            **{k: main[k] for k in ("e2e", "gpu_launches", "clocks", "roofline", "roofline_other", "kernels",
+                                    "dominant_kernel", "traffic_per_step", "episode_steps_per_s", "tree_stats",
+                                    "chosen_action")}}
+    if latency:
+        line["latency_probe"] = latency
+    if rank == 0 and world == 1 and args.secondary:
+        sec = {}
+        for cid, prec in SECONDARY:
+            if cid == args.config and prec == args.precision:
+                continue
+            a2 = argparse.Namespace(**vars(args))
+            a2.config, a2.precision = cid, prec
+            a2.n_parallel, a2.iterations = CONFIGS[cid]["n_parallel"], CONFIGS[cid]["iterations"]
+            r = measure(a2, rank, world, local, clocks=False, latency=latency)
+            r.pop("_model")
+            sec[f"{cid}_{prec}"] = {"config": workload_config(a2, r["actions"]), "value": r["value"],
+                                    "ms_per_step": r["ms_per_step"], "e2e": r["e2e"], "dtype": prec,
+                                    "roofline_other": r["roofline_other"], "kernels": r["kernels"],
+                                    "tree_stats": r["tree_stats"], "traffic_per_step": r["traffic_per_step"]}
+            torch.cuda.empty_cache()
+        line["secondary"] = sec
     if rank == 0 and world == 1 and args.episodes > 0:
         line["closed_loop"] = closed_loop(args, vp, model)
     if rank == 0 and not args.no_cpu_baseline:
@@ -436,8 +554,10 @@ CPU_SAMPLE_ROWS = 16384  # larger workloads are timed on a bounded sample of the
 
 def cpu_baseline(args) -> dict:
     """One core, whole planning steps of the same problem and iteration budget until the time
-    budget is used; workloads above CPU_SAMPLE_ROWS rows per iteration run on that many rows (the
-    numpy reference's cost per simulation is flat in the row count)."""
+    budget is used.  Workloads above CPU_SAMPLE_ROWS rows per iteration run on that many rows to
+    bound the time; the value is then the sample's rate, not a measurement at the full row count
+    (the reference's per-simulation cost changes with the row count), and the
+    sample string says so."""
     rows = min(args.n_parallel, CPU_SAMPLE_ROWS)
     times = []
     t_start = time.perf_counter()
@@ -451,6 +571,12 @@ def cpu_baseline(args) -> dict:
                  f"{args.n_parallel} rows per iteration, 1 core"
     return {"value": round(sims * len(times) / sum(times), 1), "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{sample} ({sum(times):.1f} s; oracle/ numpy port of vecpomdp.plan)"}
+
+
+def _actions(args) -> int:
+    import oracle
+
+    return make_model(oracle, args, 1000).spec.action_count
 
 
 def run_reference(args):
@@ -483,7 +609,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(workload_config(args, 1), parallelism=f"{cores} host processes (one planning step each)"),
+            "config": workload_config(args, _actions(args)),
+            "execution": f"{cores} host processes, each one whole planning step of the workload per step",
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"each step: {cores} concurrent full planning steps (one per core) of "

@@ -314,6 +314,12 @@ int32_t vp_tree_append_beliefs(const vp_tree* tree, const int32_t* action_nodes,
 int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, const void* source, int32_t keep_lo,
                             int32_t keep_hi, void* stream);
 
+/* Latency probe: one thread follows `hops` dependent pointers next[p] (element indices) from
+ * `start` with gpu-scope loads (atomic = 0: L2 round trips) or atom.add 0 (atomic = 1); out[0] =
+ * ns per hop, out[1] = SM cycles per hop, out[2] = the final index. */
+int32_t vp_probe_latency(const uint64_t* next, int32_t hops, int32_t atomic, uint64_t start, double* out,
+                         void* stream);
+
 /* ---- test hooks (parity of individual kernels) ------------------------- */
 int32_t vp_rng_uniform(uint64_t key, const int64_t* rows, int64_t n, int32_t k,
                        double* out, void* stream);

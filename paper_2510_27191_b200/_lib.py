@@ -118,6 +118,7 @@ _SIGNATURES = [
     ("vp_tree_init", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_rehash", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_set_eta", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
+    ("vp_probe_latency", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
     ("vp_tree_counts", C.c_int32, [C.POINTER(VpTree), p_i32, C.c_void_p]),
     ("vp_draw_root_states", C.c_int32,
      [C.POINTER(VpModel), C.POINTER(VpWork), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]),

@@ -735,6 +735,26 @@ __global__ void k_sir_resample(const typename Model::State* prop, const double* 
   out[j] = prop[lo < m ? lo : m - 1];
 }
 
+// ---- latency probe (bench.py's latency roofline): one thread chases a random cycle of 128-B lines
+// with dependent gpu-scope loads (L2: never an L1 hit) or dependent atomics (atom.add 0 returns
+// the next pointer), timed with %globaltimer (ns) and clock64 (SM cycles).
+__global__ void k_probe_chase(const u64* next, int hops, int atomic, u64 start, double* out) {
+  u64 p = start;
+  long long c0 = clock64();
+  u64 t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = 0; i < hops; ++i) {
+    if (atomic) p = atomicAdd(const_cast<unsigned long long*>(next + p), 0ull);
+    else p = ld_relaxed_u64(next + p);
+  }
+  u64 t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  const long long c1 = clock64();
+  out[0] = (double)(t1 - t0) / hops;
+  out[1] = (double)(c1 - c0) / hops;
+  out[2] = (double)p;  // keeps the chain live
+}
+
 // ---- test-hook kernels
 
 __global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
@@ -1158,6 +1178,13 @@ int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, cons
   k_broadcast_record<<<(int)std::min<long long>((total + 255) / 256, 148LL * 16), 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<u64*>(records), total, record_bytes / 8, reinterpret_cast<const u64*>(source), keep_lo / 8,
       keep_hi / 8);
+  return check_launch();
+}
+
+int32_t vp_probe_latency(const uint64_t* next, int32_t hops, int32_t atomic, uint64_t start, double* out,
+                         void* stream) {
+  if (!next || hops < 1 || !out) return VP_ERR_INVALID;
+  k_probe_chase<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<const u64*>(next), hops, atomic, start, out);
   return check_launch();
 }
 
