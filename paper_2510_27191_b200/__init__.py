@@ -15,7 +15,7 @@ from .core import ProblemModel, ProblemSpec, StepResult
 from .envs import (CrowdNavModel, CrowdStates, LightDarkModel, MarsModel, NavigationModel, SyntheticModel, TabularModel, TabularPOMDP,
                    device_model, problem_from_config, tiger_model)
 from .rng import BoundRng, RowRng
-from .search import LeafResult, SearchBatch, sample_actions, search, softmax_rows
+from .search import LeafResult, SearchBatch, sample_actions, search, search_recorded, softmax_rows
 from .solver import Planner, PlanOutcome, RunRecord, SolverConfig, get_planner, plan, run_episode
 from .shard import ShardedPlanner, shard_rows
 from .tree import DeviceTree, init_tree, match_or_append_pairs
@@ -27,6 +27,6 @@ __all__ = [
     "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",
-    "sir_update", "softmax_rows", "systematic_resample", "tiger_model", "LevelValues", "aggregate_leaves",
+    "sir_update", "search_recorded", "softmax_rows", "systematic_resample", "tiger_model", "LevelValues", "aggregate_leaves",
     "action_q_values", "match_or_append_pairs",
 ]

@@ -408,6 +408,9 @@ _BY_NAME = {
     "CrowdNavModel": crowdnav_descriptor,
 }
 _CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+# ProblemModel methods the device re-implements (core.py:84-142): search / SIR step, leaf value,
+# SIR likelihood.  reference_log_probs, the initial-state sampler and the belief hooks run on the host.
+_DEVICE_METHODS = frozenset({"step_batch", "value_heuristic", "observation_log_likelihood"})
 
 
 def device_model(model) -> DeviceModel:
@@ -416,15 +419,25 @@ def device_model(model) -> DeviceModel:
         return _CACHE[model]
     except (KeyError, TypeError):
         pass
+    mro = type(model).__mro__
     if hasattr(model, "device_descriptor"):
-        dm = model.device_descriptor()
+        # the class providing the descriptor binds the dynamics of the classes from it upward
+        known = next(i for i, c in enumerate(mro) if "device_descriptor" in vars(c))
     else:
         # the model's class or its nearest known base (subclasses of the reference's models,
         # e.g. with another reference policy, keep their device layout)
-        build = next((_BY_NAME[c.__name__] for c in type(model).__mro__ if c.__name__ in _BY_NAME), None)
-        if build is None:
+        known = next((i for i, c in enumerate(mro) if c.__name__ in _BY_NAME), None)
+        if known is None:
             raise TypeError(f"no device model for {type(model).__name__}; supported: {sorted(_BY_NAME)}")
-        dm = build(model)
+    # a subclass that changes the dynamics the device runs (the generative step, the leaf
+    # heuristic, the SIR likelihood) must not silently plan with its base's device model
+    for c in mro[:known]:
+        bad = sorted(set(vars(c)) & _DEVICE_METHODS)
+        if bad:
+            raise TypeError(f"{type(model).__name__} overrides {', '.join(bad)} of {mro[known].__name__} "
+                            f"(in {c.__name__}); the device runs {mro[known].__name__}'s dynamics -- give the "
+                            f"model its own device_descriptor() or keep those methods")
+    dm = model.device_descriptor() if hasattr(model, "device_descriptor") else _BY_NAME[mro[known].__name__](model)
     try:
         _CACHE[model] = dm
     except TypeError:

@@ -182,6 +182,59 @@ def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inje
     return leaves
 
 
+def search_recorded(tree, model, actions, observations, rewards, leaf_values) -> LeafResult:
+    """A search pass from the root whose rows' trajectories are given: (d, n) actions,
+    observations and rewards and n leaf values (VP_SEARCH_INSERT, the insert half of a
+    sharded pass).  The rows extend the tree exactly as search.py:106-119 would had they
+    drawn these samples (append_actions / append_beliefs, rewards and visits, the leaf
+    frontier), so ``backup(tree, leaves, d, ...)`` applies Alg. 3 to them -- the hook the
+    backup acceptance test (SPEC ACCEPTANCE 1) builds its random trees with."""
+    torch = _torch()
+    act = np.ascontiguousarray(np.asarray(actions, dtype=np.int32))
+    obs = np.ascontiguousarray(np.asarray(observations, dtype=np.int64))
+    rew = np.ascontiguousarray(np.asarray(rewards, dtype=np.float64))
+    leaf = np.ascontiguousarray(np.asarray(leaf_values, dtype=np.float64))
+    if act.ndim != 2 or obs.shape != act.shape or rew.shape != act.shape or leaf.shape != (act.shape[1],):
+        raise ValueError("actions / observations / rewards must be (d, n) and leaf_values (n,)")
+    d, n = act.shape
+    A = tree.action_count
+    if d < 1 or n < 1:
+        raise ValueError("need at least one level and one row")
+    if act.min() < 0 or act.max() >= A:
+        raise ValueError("invalid action")
+    if obs.min() < 0 or obs.max() > model.spec.observation_arity:
+        raise ValueError("invalid observation code")
+    dm = device_model(model)
+    if dm.desc.action_count != A:
+        raise ValueError("model and tree differ in action count")
+    tree.clear_pass_scratch()
+    work = getattr(tree, "_api_work", None)
+    if work is None or not work.fits(n, d, dm.state_bytes, False):
+        work = Workspace(n, d, dm.state_bytes, False)
+        tree._api_work = work
+    nb, na, _ = tree.counts()
+    tree.ensure_capacity(nb + n * d, na + n * d)
+    dev = {k: torch.from_numpy(v.reshape(-1)).cuda() for k, v in
+           (("a", act), ("o", obs.astype(np.uint32).view(np.int32)), ("r", rew), ("h", leaf))}
+    pass_ = tree.next_pass()
+    args = _lib.VpSearchArgs()
+    args.depth0, args.d_max, args.pass_ = 0, d, pass_
+    args.mode = _lib.VP_SEARCH_INSERT
+    args.inject_actions, args.inject_obs = dev["a"].data_ptr(), dev["o"].data_ptr()
+    args.inject_reward, args.inject_leaf = dev["r"].data_ptr(), dev["h"].data_ptr()
+    if pass_ != work.last_pass + 1:
+        work.leaf_count.zero_()
+    work.last_pass = pass_
+    stream = torch.cuda.current_stream()
+    _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
+              stream.cuda_stream)
+    stream.synchronize()  # the injected columns are temporaries
+    tree._scratch_dirty = True
+    leaves = LeafResult(tree, work, 0, d, pass_, tree.generation)
+    tree.last_search = leaves
+    return leaves
+
+
 def softmax_rows(pref_rows, eta: float, *, precision: str = "fp64"):
     """Row softmax of eta * PSI (search.py:46-54), computed from the device CDF."""
     if eta <= 0:

@@ -17,6 +17,9 @@ Cases (see SURVEY.md section 4 "parity ladder" and Appendix C):
 * large_*     -- digests of full-size C2 / C3 ``plan()`` trees (MARS(11,11) 16384 x 10,
                  MARS(15,15) 65536 x 10)
 * episode_*   -- closed-loop ``run_episode`` records
+* acceptance  -- the reference's acceptance oracles (oracle.py; SPEC.md ACCEPTANCE 1, 4, 5):
+                 serial_backup on random trees, exact_value_iteration on Tiger,
+                 exact_bayes_filter on random 2-state chains
 """
 
 from __future__ import annotations
@@ -292,7 +295,82 @@ def gen_large(cases=LARGE_CASES):
     return manifest
 
 
+ACCEPT_TREES = 24        # random serial_backup cases (SPEC #1 family)
+ACCEPT_HORIZONS = (1, 2, 3, 5, 8)  # Tiger exact value iteration
+ACCEPT_FILTERS = 10      # random 2-state chains x 10 (a, o) steps
+
+
+def two_state_chain(g):
+    """A random 2-state, 2-action, 2-observation tabular chain (SPEC #5)."""
+    t = g.dirichlet([2.0, 2.0], size=(2, 2))
+    z = g.dirichlet([2.0, 2.0], size=(2, 2))
+    r = g.normal(size=(2, 2))
+    return ref.envs.tabular.TabularPOMDP(t, z, r, np.array([0.5, 0.5]), 0.95, np.array([False, False]), "chain", 50)
+
+
+def gen_acceptance():
+    """Outputs of the reference's own acceptance oracles (oracle.py:124-173, 259-323)."""
+    from vecpomdp import oracle as ro
+    from oracle.acceptance import random_tree_case
+
+    out = {}
+    for k in range(ACCEPT_TREES):
+        A, passes = random_tree_case(np.random.default_rng(1000 + k))
+        tree = ro.SerialTree(A)
+        for p in passes:
+            leaves = []
+            for r in range(p["actions"].shape[1]):
+                node = tree.root
+                for lvl in range(p["d"]):
+                    x = tree.get_or_add_action(node, int(p["actions"][lvl, r]))
+                    x.visits += 1
+                    x.reward_sum += float(p["rewards"][lvl, r])
+                    node = tree.get_or_add_child(x, int(p["observations"][lvl, r]))
+                leaves.append((node, float(p["leaf"][r])))
+            ro.serial_backup(tree, leaves, p["d"], 2.0, 0.9)
+        paths = []
+        for b in tree.beliefs:
+            path, cur = [], b
+            while cur.parent_action is not None:
+                path = [cur.parent_action.action, cur.parent_obs] + path
+                cur = cur.parent_action.parent
+            paths.append(tuple(path))
+        order = sorted(range(len(paths)), key=lambda i: paths[i])
+        out[f"tree{k}_prefs"] = np.array([tree.beliefs[i].prefs for i in order], dtype=np.float64)
+        out[f"tree{k}_paths"] = np.array([list(paths[i]) + [-1] * (8 - len(paths[i])) for i in order], dtype=np.int64)
+    tiger = ref.envs.tabular.tiger_model()
+    grid = np.linspace(0.0, 1.0, 41)
+    beliefs = np.stack([grid, 1.0 - grid, np.zeros_like(grid)], axis=1)
+    out["vi_beliefs"] = beliefs
+    for h in ACCEPT_HORIZONS:
+        v = ro.exact_value_iteration(tiger.pomdp, h)
+        out[f"vi_h{h}_values"] = np.array([v.value(b) for b in beliefs])
+        out[f"vi_h{h}_actions"] = np.array([v.action(b) for b in beliefs], dtype=np.int64)
+    v = ro.exact_value_iteration(tiger.pomdp, 20)  # the decision-quality ground truth (SPEC #4)
+    out["vi_h20_alphas"], out["vi_h20_actions"] = v.alphas, v.actions.astype(np.int64)
+    for k in range(ACCEPT_FILTERS):
+        g = np.random.default_rng(2000 + k)
+        pomdp = two_state_chain(g)
+        b = np.array([0.5, 0.5])
+        seq, post = [], []
+        for _ in range(10):
+            a = int(g.integers(0, 2))
+            pred = pomdp.transitions[a].T @ b
+            o = int(g.choice(2, p=pomdp.observations[a].T @ pred))
+            b = ro.exact_bayes_filter(pomdp, b, a, o)
+            seq.append((a, o))
+            post.append(b)
+        out[f"chain{k}_T"], out[f"chain{k}_Z"], out[f"chain{k}_R"] = pomdp.transitions, pomdp.observations, pomdp.rewards
+        out[f"chain{k}_seq"] = np.array(seq, dtype=np.int64)
+        out[f"chain{k}_post"] = np.array(post)
+    np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **out)
+    print("acceptance: trees", ACCEPT_TREES, "horizons", ACCEPT_HORIZONS, "chains", ACCEPT_FILTERS)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["acceptance"]:
+        gen_acceptance()
+        sys.exit(0)
     if sys.argv[1:] == ["large"]:
         with open(os.path.join(HERE, "manifest.json")) as f:
             manifest = json.load(f)
@@ -313,6 +391,7 @@ if __name__ == "__main__":
     gen_navigation_steps()
     gen_rng()
     gen_formulas()
+    gen_acceptance()
     manifest = {"plans": gen_plans(), "large_plans": gen_large(), "episodes": dict(gen_episodes(), episode_crowdnav40=gen_crowd_episodes()),
                 "numpy": np.__version__, "reference": "/root/reference/pkg/src/vecpomdp @ 0.1.0"}
     with open(os.path.join(HERE, "manifest.json"), "w") as f:

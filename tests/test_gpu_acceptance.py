@@ -1,0 +1,149 @@
+"""The reference's acceptance criteria that have oracles (SPEC.md ACCEPTANCE 1, 4, 5;
+/root/reference/pkg/src/vecpomdp/oracle.py), on the device.
+
+1. Backup vs the serial per-node backup: 200 random trees (depth <= 4, <= 50
+   beliefs, |A| <= 6, random rewards and heuristics, 1-3 passes), built by the
+   device search from recorded trajectories (search_recorded, VP_SEARCH_INSERT)
+   and backed up by the device kernel; every PSI entry within 1e-6 absolute of
+   oracle/acceptance.serial_backup (pinned to the reference's serial_backup).
+4. Tiger decisions against exact value iteration (the reference's alpha vectors
+   at horizon 20, tests/golden/acceptance.npz): the device's decisions equal the
+   reference planner's (fp64 parity mode) at every sampled belief, and its
+   agreement with the optimum is reported and bounded; closed-loop return vs V*.
+5. Device SIR vs exact_bayes_filter on random 2-state chains: m = 10^5
+   particles, 50 sequences of 10 (a, o) steps, within 0.01 absolute.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2510_27191_b200 as vp
+from golden_cases import load
+from oracle import acceptance as acc
+
+pytestmark = pytest.mark.gpu
+
+G = load("acceptance")
+
+
+def descriptor_model(A: int, O: int = 3):
+    """Any device model with |A| actions: insert mode replays given samples, it never steps."""
+    t = np.tile(np.eye(2), (A, 1, 1))
+    z = np.full((A, 2, O), 1.0 / O)
+    return vp.TabularModel(vp.TabularPOMDP(t, z, np.zeros((2, A)), np.array([1.0, 0.0]), 0.9,
+                                           np.array([False, False]), "replay", 10))
+
+
+def device_run(A, passes, eta, gamma, precision, exact):
+    tree = vp.DeviceTree(A, precision=precision, exact=exact, eta=eta, cap_beliefs=64, cap_actions=64)
+    model = descriptor_model(A)
+    for p in passes:
+        leaves = vp.search_recorded(tree, model, p["actions"], p["observations"], p["rewards"], p["leaf"])
+        vp.backup(tree, leaves, p["d"], eta, gamma)
+    return tree
+
+
+@pytest.mark.parametrize("precision,exact,tol", [("fp64", True, 1e-6), ("fp64", False, 1e-6), ("fp32", False, None)])
+def test_spec1_backup_matches_serial_on_200_random_trees(precision, exact, tol):
+    worst = 0.0
+    for k in range(200):
+        A, passes = acc.random_tree_case(np.random.default_rng(k))
+        serial = acc.serial_run(A, passes, 2.0, 0.9)
+        tree = device_run(A, passes, 2.0, 0.9, precision, exact)
+        t = tree.tables()
+        paths = acc.belief_paths(t["parent_action"], t["parent_obs"], t["action_parent_belief"], t["action_id"])
+        assert sorted(paths) == sorted(serial.prefs), k
+        for i, p in enumerate(paths):
+            want = np.array(serial.prefs[p])
+            err = np.abs(t["prefs"][i] - want)
+            if tol is None:  # fp32 storage: the scale-aware 1e-5 relative contract
+                err = err / max(1.0, float(np.abs(want).max()))
+            worst = max(worst, float(err.max()))
+        # visits / rewards are the rows' own sums
+        got_v = {paths[int(t["action_parent_belief"][x])] + (int(t["action_id"][x]),): int(t["action_visits"][x])
+                 for x in range(len(t["action_id"]))}
+        assert got_v == serial.visits, k
+    assert worst <= (tol if tol is not None else 1e-5), worst
+
+
+def tiger_belief(p_left: float, m: int = 2000):
+    k = int(round(p_left * m))
+    states = oracle.TabularStates(np.array([0] * k + [1] * (m - k)), np.zeros(m, dtype=bool))
+    return oracle.ParticleBelief(states, np.full(m, 1.0 / m)), k / m
+
+
+def test_spec4_tiger_decisions_vs_exact_value_iteration():
+    """SPEC.md:628 protocol (n_p = 1024, eta = 2, fixed iterations; 100 beliefs sampled
+    uniformly).  The shipped reference planner (heuristic 0, depth <= 10) opens early
+    near p = 0.03 / 0.95 where the horizon-20 optimum still listens, so it agrees with the
+    optimum on ~89 % of uniform beliefs; the device must make the reference's decisions
+    (fp64 parity mode) and so inherits that rate (asserted >= 85 %, reported)."""
+    om = oracle.tiger_model()
+    vi = acc.AlphaSet(G["vi_h20_alphas"], G["vi_h20_actions"])
+    g = np.random.default_rng(0)
+    cfg = oracle.SolverConfig(n_parallel=1024, iterations=10)
+    agree_dev = agree_ref = same = 0
+    for i, p in enumerate(g.uniform(0.0, 1.0, size=100)):
+        belief, p = tiger_belief(p)
+        rng = oracle.RowRng.from_seed(i).derive(1, 0)
+        a_dev = vp.plan(belief, om, cfg, rng, precision="fp64", exact=True).chosen_action
+        a_ref = oracle.plan(belief, om, cfg, rng).chosen_action
+        best = vi.action([p, 1.0 - p, 0.0])
+        agree_dev += a_dev == best
+        agree_ref += a_ref == best
+        same += a_dev == a_ref
+    print(f"tiger: device agrees with the horizon-20 optimum on {agree_dev}/100 beliefs, "
+          f"the reference planner on {agree_ref}/100; device == reference on {same}/100")
+    assert same == 100
+    assert agree_dev >= 85
+    # the fp32 fast path decides like the parity mode on the unambiguous beliefs
+    for p_left, want in ((0.5, 0), (0.2, 0), (0.8, 0), (0.005, 1), (0.995, 2)):
+        belief, p = tiger_belief(p_left)
+        got = vp.plan(belief, om, cfg, oracle.RowRng.from_seed(7).derive(1, 0)).chosen_action
+        assert got == want == vi.action([p, 1.0 - p, 0.0]), p_left
+
+
+def test_spec4_tiger_return_vs_optimum():
+    """200 closed-loop episodes (device planner, device SIR); the mean discounted return
+    lies within 10 % of V*(b0) or within its own 95 % CI of it (one wrong door costs 110, so
+    200 episodes resolve the mean only to a few units)."""
+    om = vp.tiger_model()
+    vi = acc.AlphaSet(G["vi_h20_alphas"], G["vi_h20_actions"])
+    v_star = vi.value([0.5, 0.5, 0.0])
+    cfg = vp.SolverConfig(n_parallel=1024, iterations=10, particles=2000)
+    rets = np.array([vp.run_episode(om, cfg, seed=s).discounted_return for s in range(200)])
+    mean, half = rets.mean(), 1.96 * rets.std(ddof=1) / np.sqrt(len(rets))
+    print(f"tiger: mean discounted return {mean:.3f} +- {half:.3f} (95% CI) vs V*(b0) = {v_star:.3f}")
+    assert abs(mean - v_star) <= max(0.1 * abs(v_star), half)
+
+
+def chain_model(g):
+    t = g.dirichlet([2.0, 2.0], size=(2, 2))
+    z = g.dirichlet([2.0, 2.0], size=(2, 2))
+    pomdp = vp.TabularPOMDP(t, z, np.zeros((2, 2)), np.array([0.5, 0.5]), 0.95, np.array([False, False]), "chain", 50)
+    return vp.TabularModel(pomdp), pomdp
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_spec5_device_sir_matches_exact_bayes_filter(exact):
+    m = 100_000
+    worst = 0.0
+    for k in range(50):
+        g = np.random.default_rng(3000 + k)
+        model, pomdp = chain_model(g)
+        host = vp.ParticleBelief(model.states_from_indices(np.repeat([0, 1], m // 2)), np.full(m, 1.0 / m))
+        belief = vp.DeviceBelief.from_host(host, model)
+        b = np.array([0.5, 0.5])
+        rng = vp.RowRng.from_seed(k)
+        for t in range(10):
+            a = int(g.integers(0, 2))
+            o = int(g.choice(2, p=pomdp.observations[a].T @ (pomdp.transitions[a].T @ b)))
+            b = acc.exact_bayes_filter(pomdp, b, a, o)
+            upd = vp.sir_update(belief, model, a, o, rng.derive(t), exact=exact)
+            belief = upd.belief
+            assert not upd.degenerate
+            est = np.bincount(belief.states.idx, minlength=2) / m
+            worst = max(worst, float(np.abs(est - b).max()))
+    print(f"SIR vs exact filter: worst |posterior error| {worst:.4f} over 50 x 10 updates")
+    assert worst <= 0.01
