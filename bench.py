@@ -209,24 +209,30 @@ def algorithmic_bytes(st, n, S, A, psi_b, passes):
     """Compulsory HBM bytes of the search and backup kernels summed over `passes` passes, from
     the device traffic counters (adapted to the fused design: states and
     frontier ids stay in registers across levels; node fields at element granularity, hash
-    probes at 32-B sector granularity; lazily initial PSI rows are neither written nor read).
+    probes at 32-B sector granularity; fast-mode PSI: a belief is its overlay record -- one
+    record + its cached LSE per distinct belief visited -- and only beliefs with more than 4
+    action children own a dense row, read once per pass when sampled).
 
-    U   interior beliefs backed up (= distinct beliefs sampled from), Unf those whose PSI row was
-        not the initial row (the only rows the sampler and the backup must read), P distinct
-        action nodes visited, L distinct leaves, NA / NB new action / belief nodes.
+    U   interior beliefs backed up (= distinct beliefs sampled from), P distinct action nodes
+        visited, L distinct leaves, NA / NB new action / belief nodes, D distinct dense rows
+        sampled (CDFs built), M dense rows materialised, F full-row LSE reads (fallback).
     """
-    U, P, L, NA, NB, Unf = st[0], st[1], st[7], st[5], st[6], st[8]
+    U, P, L, NA, NB = st[0], st[1], st[7], st[5], st[6]
+    D, M, F = st[11], st[10], st[8]
+    rec = 8 * psi_b + 8  # overlay record: 32 B (fp32) / 48 B (fp64)
     children = (U - passes) + L  # distinct (a, o) probes: every visited non-root belief
     search = (n * passes * S                   # root-state gather
-              + psi_b * A * Unf                # PSI row per distinct non-initial belief sampled
+              + (rec + 8) * (U + L)            # record + cached LSE of every distinct belief reached
+              + psi_b * A * D                  # dense PSI row per distinct dense belief sampled
               + 32 * (P + children)            # one hash sector per distinct probe (claims)
               + 16 * P                         # reward / visit / row reductions per action
-              + 16 * NA + 40 * NB              # new node columns
+              + 24 * NA + 40 * NB              # new node columns (+ child count, overlay slot)
+              + psi_b * A * M                  # dense rows materialised
               + 12 * L)                        # leaf heuristic sums + leaf list
     backup = (24 * L                           # leaf (rows, value) read + reset
-              + (52 + 2 * psi_b) * P           # action stats, accumulator r/w, PSI cell r/w
-              + 76 * U                         # belief LSE / rows / flags / parents, accumulator r/w
-              + psi_b * A * Unf)               # full-row LSE of non-initial rows
+              + (56 + rec + 2 * psi_b) * P     # action stats + slot, accumulator r/w, record + cell r/w
+              + 76 * U                         # belief LSE / rows / parents, accumulator r/w
+              + psi_b * A * F)                 # full-row LSE (ill-conditioned incremental sums)
     return search, backup
 
 
@@ -440,11 +446,13 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
         return out
 
     roof_search = roof("search", "k_search", b_search,
-                       "n S + psi_b|A| Unf + 48 P + 32 children + 16 NA + 40 NB + 12 L per pass (bench.algorithmic_bytes)")
+                       "n S + (rec + 8)(U + L) + psi_b|A| (D + M) + 48 P + 32 children + 24 NA + 40 NB + 12 L "
+                       "per pass (bench.algorithmic_bytes)")
     roof_backup = roof("backup", "k_backup", b_backup,
-                       "24 L + (52 + 2 psi_b) P + 76 U + psi_b|A| Unf per pass (bench.algorithmic_bytes)")
+                       "24 L + (56 + rec + 2 psi_b) P + 76 U + psi_b|A| F per pass (bench.algorithmic_bytes)")
     names = ["interior_beliefs", "actions_visited", "psi_rows_staged", "search_launches", "row_levels",
-             "new_actions", "new_beliefs", "leaves", "psi_rows_read"]
+             "new_actions", "new_beliefs", "leaves", "full_row_lse_reads", "overlay_draws", "dense_rows_made",
+             "dense_cdfs_built"]
     res.update({
         "roofline": {"search": roof_search, "backup": roof_backup}.get(top) or roof_search,
         "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},

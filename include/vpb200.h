@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 6
+#define VPB200_ABI_VERSION 7
 
 enum vp_status {
   VP_OK = 0,
@@ -49,6 +49,8 @@ enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
 
 #define VP_COUNTERS 64
 #define VP_COUNTER_ACTIONS 32
+#define VP_COUNTER_DENSE 48   /* dense PSI rows handed out (fast mode), own 128-B line */
+#define VP_OVERLAY_SLOTS 4    /* realised PSI cells a belief keeps inline before it gets a dense row */
 
 /* Device descriptor of a ProblemModel (core.py:84-142).  Passed by value to
  * every kernel; constant tables live in device memory. */
@@ -117,12 +119,24 @@ typedef struct vp_tree {
   int32_t* b_parent_belief;   /* = a_parent_belief[b_parent_action] (backup climbs without chasing) */
   int32_t* b_parent_act;      /* = a_action[b_parent_action]                  */
   int32_t* b_depth;
-  void* psi;                  /* [cap_beliefs * psi_stride] float or double */
+  void* psi;                  /* [cap_dense * psi_stride] float or double.  Parity mode
+                                 (exact): row b is belief b's row.  Fast mode: only beliefs
+                                 with more than VP_OVERLAY_SLOTS action children own a dense
+                                 row (b_rec.dense_row); every other belief's row is the initial
+                                 row overlaid with its realised cells (tree.py:247-253,
+                                 backup.py:107-108: PSI departs from init only where (b, a)
+                                 was backed up) */
   double* b_lse;              /* cached (1/eta) log sum exp(eta PSI[b])      */
   double* b_value;            /* leaf heuristic sum of the current pass      */
   int32_t* b_rows;            /* rows that reached b in the current pass     */
   void* b_acc;                /* backup accumulator, 16 B {f64 sum; u32 rows done; u32 N} */
-  uint32_t* b_flags;          /* bit0: PSI row lazily == init; bit1: row not written */
+  uint32_t* b_flags;          /* parity mode: bit0 PSI row lazily == init; bit1 row not written */
+  void* b_rec;                /* fast mode: [cap_beliefs] overlay record, 16-B aligned:
+                                 {u32 dense_pass (0: no dense row; else the search pass that
+                                 wrote it); u32 dense_row; u16 action + 1 [4] (0: empty);
+                                 PSI dtype value [4]} -- 32 B (fp32) / 48 B (fp64) */
+  int32_t* b_nact;            /* action children created so far: child k takes overlay slot k;
+                                 child VP_OVERLAY_SLOTS makes the row dense */
   uint64_t* b_ckey;           /* creation key (canonical order)              */
   /* action table A */
   int32_t* a_parent_belief;
@@ -132,6 +146,7 @@ typedef struct vp_tree {
   int32_t* a_rows;            /* rows through the action in the current pass */
   void* a_acc;                /* backup accumulator, 16 B {f64 sum V*N; u32 rows done; u32 sum N} */
   uint64_t* a_ckey;           /* creation key (canonical order)              */
+  int32_t* a_slot;            /* child index of the action within its parent (b_nact order) */
   /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */
   void* hash_b;               /* belief key (see bkey_mode) -> belief row    */
@@ -149,6 +164,10 @@ typedef struct vp_tree {
   int32_t bkey_mode;          /* belief-index key: 0 = (action row << 32 | obs); 1 = (belief << 32 |
                                  action << 20 | obs), needs |A| <= 4096 and obs < 2^20 -- both
                                  claims of a level can then be issued together */
+  int32_t cap_dense;          /* rows of psi                                 */
+  int32_t overlay_slots;      /* VP_OVERLAY_SLOTS in fast mode, 0 in parity mode */
+  int32_t init_uniform;       /* 1: every init_prefs entry is equal (the reference's uniform
+                                 reference policy): overlay LSEs have a closed form */
   double eta;
 } vp_tree;
 
@@ -165,8 +184,10 @@ typedef struct vp_work {
                                  0 interior beliefs backed up, 1 actions backed up,
                                  2 PSI rows staged by the sampler, 3 search launches,
                                  4 row-levels sampled, 5 new actions, 6 new beliefs,
-                                 7 leaves, 8 interior beliefs whose PSI row was not
-                                 lazily initial (rows the sampler must read) */
+                                 7 leaves, 8 interior beliefs whose LSE needed a full
+                                 row read, 9 overlay draws (rows drawn from a belief's
+                                 inline cells), 10 dense rows materialised, 11 CDFs built
+                                 into the per-pass cache (distinct dense rows sampled) */
   /* optional per-level traces (level-major, n each; device ids); NULL = off */
   int32_t* trace_action;
   uint32_t* trace_obs;

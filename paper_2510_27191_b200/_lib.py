@@ -20,8 +20,9 @@ VP_MODEL_CROWDNAV = 6
 CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 6
-VP_COUNTERS, VP_COUNTER_ACTIONS = 64, 32  # include/vpb200.h
+ABI_VERSION = 7
+VP_COUNTERS, VP_COUNTER_ACTIONS, VP_COUNTER_DENSE = 64, 32, 48  # include/vpb200.h
+VP_OVERLAY_SLOTS = 4
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (
     C.POINTER(C.c_int8), C.POINTER(C.c_int16), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
@@ -63,13 +64,15 @@ class VpTree(C.Structure):
         ("b_parent_action", C.c_void_p), ("b_parent_obs", C.c_void_p), ("b_parent_belief", C.c_void_p),
         ("b_parent_act", C.c_void_p), ("b_depth", C.c_void_p),
         ("psi", C.c_void_p), ("b_lse", C.c_void_p), ("b_value", C.c_void_p),
-        ("b_rows", C.c_void_p), ("b_acc", C.c_void_p), ("b_flags", C.c_void_p), ("b_ckey", C.c_void_p),
+        ("b_rows", C.c_void_p), ("b_acc", C.c_void_p), ("b_flags", C.c_void_p), ("b_rec", C.c_void_p),
+        ("b_nact", C.c_void_p), ("b_ckey", C.c_void_p),
         ("a_parent_belief", C.c_void_p), ("a_action", C.c_void_p), ("a_reward", C.c_void_p),
         ("a_visits", C.c_void_p), ("a_rows", C.c_void_p), ("a_acc", C.c_void_p), ("a_ckey", C.c_void_p),
+        ("a_slot", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p),
         ("cdf_cache", C.c_void_p), ("cdf_tag", C.c_void_p), ("cdf_slots", C.c_int32), ("bkey_mode", C.c_int32),
-        ("eta", C.c_double),
+        ("cap_dense", C.c_int32), ("overlay_slots", C.c_int32), ("init_uniform", C.c_int32), ("eta", C.c_double),
     ]
 
 
@@ -216,12 +219,13 @@ def layout_mismatches() -> list:
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
             VpModel.mars_gpow.offset, VpTree.cdf_tag.offset, VpModel.nav_log_miss.offset,
-            VpModel.crowd_heur.offset, CROWD_STATE_BYTES]
+            VpModel.crowd_heur.offset, CROWD_STATE_BYTES, VpTree.b_rec.offset, VpTree.a_slot.offset,
+            VpTree.cap_dense.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
              "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag", "vp_model.nav_log_miss",
-             "vp_model.crowd_heur", "sizeof(CrowdState)"]
+             "vp_model.crowd_heur", "sizeof(CrowdState)", "vp_tree.b_rec", "vp_tree.a_slot", "vp_tree.cap_dense"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

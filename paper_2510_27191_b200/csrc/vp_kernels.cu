@@ -46,6 +46,10 @@ __global__ void k_clear(vp_tree T) {
       T.b_rows[i] = 0;
       reinterpret_cast<Acc*>(T.b_acc)[i] = Acc{0.0, 0u, 0u};
       T.b_ckey[i] = ~0ull;
+      T.b_nact[i] = 0;
+      const int words = T.psi_dtype == VP_PSI_F32 ? 2 : 3;  // sizeof(Rec<PsiT>) / 16
+      uint4* rec = reinterpret_cast<uint4*>(T.b_rec) + (size_t)i * words;
+      for (int w = 0; w < words; ++w) rec[w] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (i < T.cdf_slots) T.cdf_tag[i] = 0;  // cached CDFs of the previous tree
     if (i < na) {
@@ -74,7 +78,7 @@ __global__ void k_eta_init_row(vp_tree T) {
   } else {
     for (int a = threadIdx.x; a < A; a += 32) cdf[a] = (PsiT)T.init_prefs[a];
     __syncwarp();
-    v = row_lse_fast<PsiT>(cdf, A, T.eta);
+    v = row_lse_f64<PsiT>(cdf, A, T.eta);
   }
   for (int a = threadIdx.x; a < A; a += 32) cdf[a] = (PsiT)T.init_prefs[a];
   __syncwarp();
@@ -90,7 +94,17 @@ __global__ void k_eta_rows(vp_tree T) {
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
     double v;
-    if (T.b_flags[b] & 1u) {
+    if constexpr (!Exact) {  // dense row, overlay row or the initial row
+      const Rec<PsiT> r = load_rec<PsiT>(T, b);
+      if (r.dense_pass) {
+        v = row_lse_f64<PsiT>(psi + (size_t)r.dense_row * T.psi_stride, T.action_count, T.eta);
+      } else if (rec_any(r)) {
+        v = lane_id() == 0 ? lse_overlay<PsiT>(T, b) : 0.0;
+        v = __shfl_sync(FULL, v, 0);
+      } else {
+        v = T.init_lse[0];
+      }
+    } else if (T.b_flags[b] & 1u) {
       v = T.init_lse[0];
     } else if constexpr (Exact) {
       v = 0.0;
@@ -823,6 +837,13 @@ __global__ void k_sample_rows(const PsiT* rows, int width, double eta, const dou
 
 using namespace vp;
 
+// The PSI layout the kernels are compiled for: parity mode keeps one row per belief,
+// fast mode dense rows for the busy beliefs plus overlay records.
+static bool tree_ok(const vp_tree& T) {
+  return T.action_count >= 1 && T.action_count < 65535 && T.b_rec && T.b_nact && T.a_slot && T.cap_dense >= 1 &&
+         T.overlay_slots == (T.exact ? 0 : VP_OVERLAY_SLOTS) && (!T.exact || T.cap_dense >= T.cap_beliefs);
+}
+
 extern "C" {
 
 int32_t vp_abi_version(void) { return VPB200_ABI_VERSION; }
@@ -889,7 +910,8 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_model, mars_gpow),
                        (int32_t)offsetof(vp_tree, cdf_tag),
                        (int32_t)offsetof(vp_model, nav_log_miss), (int32_t)offsetof(vp_model, crowd_heur),
-                       (int32_t)sizeof(CrowdState)};
+                       (int32_t)sizeof(CrowdState), (int32_t)offsetof(vp_tree, b_rec),
+                       (int32_t)offsetof(vp_tree, a_slot), (int32_t)offsetof(vp_tree, cap_dense)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];
@@ -897,7 +919,7 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
 }
 
 int32_t vp_tree_init(const vp_tree* t, void* stream) {
-  if (!t || t->action_count < 1) return VP_ERR_INVALID;
+  if (!t || !tree_ok(*t)) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(t->hash_a, 0xff, (t->hmask_a + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
   if (cudaMemsetAsync(t->hash_b, 0xff, (t->hmask_b + 1) * sizeof(Slot), st) != cudaSuccess) return VP_ERR_CUDA;
@@ -960,6 +982,7 @@ int32_t vp_draw_root_states(const vp_model* m, const vp_work* w, const void* par
 
 int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_search_args* a, void* stream) {
   if (!t || !m || !w || !a || !work_ok(*w)) return VP_ERR_INVALID;
+  if (!tree_ok(*t)) return VP_ERR_INVALID;
   if (a->depth0 < 0 || a->d_max < a->depth0 || a->d_max > w->max_levels || a->pass < 1) return VP_ERR_INVALID;
   if (a->particles && (!a->cum_weights || a->m < 1)) return VP_ERR_INVALID;
   if (a->mode < VP_SEARCH_FUSED || a->mode > VP_SEARCH_INSERT || a->row0 < 0) return VP_ERR_INVALID;
@@ -985,6 +1008,7 @@ int32_t vp_search(const vp_tree* t, const vp_model* m, const vp_work* w, const v
 
 int32_t vp_plan(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_plan_args* p, void* stream) {
   if (!t || !m || !w || !p || !work_ok(*w)) return VP_ERR_INVALID;
+  if (!tree_ok(*t)) return VP_ERR_INVALID;
   if (p->iterations < 1 || p->d_max_cap < 1 || p->m < 1 || !p->keys_dev || !p->particles_dev || !p->cumw_dev ||
       !p->out_dev || (p->mode != 0 && p->mode != 1))
     return VP_ERR_INVALID;
@@ -1006,6 +1030,7 @@ int32_t vp_plan(const vp_tree* t, const vp_model* m, const vp_work* w, const vp_
 
 int32_t vp_backup(const vp_tree* t, const vp_work* w, uint32_t pass, double gamma, void* stream) {
   if (!t || !w || !work_ok(*w) || pass < 1) return VP_ERR_INVALID;
+  if (!tree_ok(*t)) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   const vp_tree T = *t;
   const vp_work W = *w;
@@ -1079,6 +1104,10 @@ int32_t vp_sir_resample(const vp_model* mdl, const void* prop, const double* cum
 // Host-level tree mutation (tree.py:180-256 append_actions / append_beliefs):
 // one thread per edge, the search's claim / numbering / creation-key protocol,
 // so new nodes take reference ids n + rank in first-occurrence order at export.
+}  // extern "C"
+
+namespace vp {
+template <class PsiT>
 __global__ void k_append_actions(vp_tree T, const int32_t* beliefs, const int32_t* actions, const double* rewards,
                                  int n, u32 pass, int32_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1093,6 +1122,12 @@ __global__ void k_append_actions(vp_tree T, const int32_t* beliefs, const int32_
       T.a_parent_belief[x] = b;
       T.a_action[x] = a;
       red_min(&T.a_ckey[x], creation_key(pass, 0, i));
+      const int k = atomicAdd(&T.b_nact[b], 1);  // overlay slot (the search's protocol)
+      T.a_slot[x] = k;
+      if (T.overlay_slots && k == kOverlay) {
+        const Rec<PsiT> r = load_rec<PsiT, true>(T, b);
+        if (!r.dense_pass) materialise_dense<PsiT>(T, nullptr, b, r, nullptr, pass);
+      }
     } else {
       T.counters[2] = 1;
     }
@@ -1108,6 +1143,10 @@ __global__ void k_append_actions(vp_tree T, const int32_t* beliefs, const int32_
   }
   out[i] = x < T.cap_actions ? x : -1;
 }
+
+}  // namespace vp
+
+extern "C" {
 
 __global__ void k_append_beliefs(vp_tree T, const int32_t* anodes, const uint32_t* obs, int n, u32 pass, int32_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1146,7 +1185,12 @@ int32_t vp_tree_append_actions(const vp_tree* t, const int32_t* beliefs, const i
   if (!t || n < 0 || (n && (!beliefs || !actions || !rewards || !out)) || pass == 0) return VP_ERR_INVALID;
   if (!n) return VP_OK;
   Launch L_(KK_HOOK, (cudaStream_t)stream);
-  k_append_actions<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*t, beliefs, actions, rewards, n, pass, out);
+  if (t->psi_dtype == VP_PSI_F32)
+    k_append_actions<float><<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*t, beliefs, actions, rewards, n, pass,
+                                                                                   out);
+  else
+    k_append_actions<double><<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*t, beliefs, actions, rewards, n,
+                                                                                    pass, out);
   return check_launch();
 }
 

@@ -88,10 +88,15 @@ struct __align__(16) Acc {
 //    completing delivery, which reads the totals.
 // The path depends only on `target`, so all deliveries to a node agree on it.
 constexpr u32 kCasRows = 16;
+// Row counts are < 2^24 (n_parallel < 2^24): the top 8 bits of a delivery's row count are
+// free for flags that add up like a bit-or (each set by exactly one delivery of the pass) --
+// the overlay slots an action completion changed (kSlotBit << slot).
+constexpr u32 kRowsMask = 0xFFFFFFu;
+constexpr u32 kSlotBit = 1u << 24;
 
 __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 drows, u32 dcnt, u32 target,
                                             Acc& out) {
-  if (drows == target) {
+  if ((drows & kRowsMask) == target) {
     out = Acc{dsum, drows, dcnt};
     return true;
   }
@@ -105,7 +110,7 @@ __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 
       u64 olo, ohi;
       cas128(p, lo, hi, nlo, nhi, olo, ohi);
       if (olo == lo && ohi == hi) {
-        if (r != target) return false;
+        if ((r & kRowsMask) != target) return false;
         out = Acc{s, r, c};
         *p = Acc{0.0, 0u, 0u};
         return true;
@@ -116,12 +121,86 @@ __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 
   }
   red_add(&p->sum, dsum);
   red_add(reinterpret_cast<int*>(&p->cnt), (int)dcnt);
-  if ((u32)atom_add_acq_rel(reinterpret_cast<int*>(&p->rows), (int)drows) + drows != target) return false;
+  const u32 rows = (u32)atom_add_acq_rel(reinterpret_cast<int*>(&p->rows), (int)drows) + drows;
+  if ((rows & kRowsMask) != target) return false;
   out.sum = ld_relaxed_f64(&p->sum);
   out.cnt = ld_relaxed_u32(&p->cnt);
-  out.rows = target;
+  out.rows = rows;
   *p = Acc{0.0, 0u, 0u};
   return true;
+}
+
+// ------------------------------------------------------------------ overlay records (fast mode)
+// PSI[b, a] departs from init_prefs[a] only where (b, a) was backed up (tree.py:247-253,
+// backup.py:107-108).  In fast mode a belief's row is therefore the initial row overlaid with
+// its realised cells, kept inline in a 32-B record (one sector) -- child k of b owns slot k --
+// and only a belief with more than kOverlay action children gets a dense row (allocated from
+// its own pool, so PSI memory scales with the busy beliefs, not with every belief).  The
+// search reads records; the backup writes their cells; a dense row is written by the search
+// lane that creates the (kOverlay + 1)-th child and is used from the next pass on.
+constexpr int kOverlay = VP_OVERLAY_SLOTS;
+template <class PsiT>
+struct __align__(16) Rec {
+  u32 dense_pass;                // 0: no dense row; else the pass whose search wrote it
+  u32 dense_row;                 // row of T.psi
+  unsigned short act[kOverlay];  // action + 1; 0 = empty slot
+  PsiT val[kOverlay];            // PSI[b, act - 1]
+};
+static_assert(sizeof(Rec<float>) == 32 && sizeof(Rec<double>) == 48, "overlay record layout (vpb200.h)");
+
+template <class PsiT>
+__device__ __forceinline__ Rec<PsiT>* rec_ptr(const vp_tree& T, int b) {
+  return reinterpret_cast<Rec<PsiT>*>(T.b_rec) + b;
+}
+template <class PsiT, bool L2 = false>
+__device__ __forceinline__ Rec<PsiT> load_rec(const vp_tree& T, int b) {
+  const uint4* p = reinterpret_cast<const uint4*>(rec_ptr<PsiT>(T, b));
+  Rec<PsiT> r;
+  uint4* q = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Rec<PsiT>) / 16); ++i) q[i] = L2 ? __ldcg(p + i) : p[i];
+  return r;
+}
+template <class PsiT>
+__device__ __forceinline__ bool rec_any(const Rec<PsiT>& r) {
+  u32 any = 0;
+#pragma unroll
+  for (int k = 0; k < kOverlay; ++k) any |= r.act[k];
+  return any != 0;
+}
+
+// log(exp(a) + exp(b)) without overflow / underflow (fp64)
+__device__ __forceinline__ double log_add_exp(double a, double b) {
+  const double hi = a > b ? a : b, lo = a > b ? b : a;
+  return lo == -INFINITY ? hi : hi + log1p(exp(lo - hi));
+}
+
+// Delivery of a log-mass to an overlay belief (fast mode, at most kOverlay deliveries per pass:
+// one per action child): the accumulator's sum holds log sum exp of the delivered log-masses,
+// combined by CAS (an empty accumulator has rows == 0; every delivery carries >= 1 row).
+__device__ __forceinline__ bool acc_deliver_log(void* base, int i, double l, u32 drows, u32 dcnt, u32 target,
+                                                Acc& out) {
+  if ((drows & kRowsMask) == target) {
+    out = Acc{l, drows, dcnt};
+    return true;
+  }
+  Acc* p = reinterpret_cast<Acc*>(base) + i;
+  u64 lo = 0, hi = 0;
+  while (true) {
+    const double s = hi == 0 ? l : log_add_exp(__longlong_as_double((long long)lo), l);
+    const u32 r = (u32)hi + drows, c = (u32)(hi >> 32) + dcnt;
+    const u64 nlo = (u64)__double_as_longlong(s), nhi = (u64)r | ((u64)c << 32);
+    u64 olo, ohi;
+    cas128(p, lo, hi, nlo, nhi, olo, ohi);
+    if (olo == lo && ohi == hi) {
+      if ((r & kRowsMask) != target) return false;
+      out = Acc{s, r, c};
+      *p = Acc{0.0, 0u, 0u};
+      return true;
+    }
+    lo = olo;
+    hi = ohi;
+  }
 }
 
 // ------------------------------------------------------------------ exp helpers (fast mode)
@@ -231,6 +310,21 @@ __device__ double row_lse_fast(const PsiT* row, int A, double eta) {
   return out;
 }
 
+// LSE of a row in fp64 arithmetic by a full warp (returned on every lane).  Fast mode keeps
+// every cached LSE at fp64 accuracy whatever the PSI dtype: the incremental backup LSE
+// (1 + sum of changed terms) cancels terms of order 1, so LSE_pre must not carry the
+// ~1e-7 error of an fp32 evaluation.
+template <class PsiT, bool L2 = false>
+__device__ double row_lse_f64(const PsiT* row, int A, double eta) {
+  double m = -INFINITY;
+  for (int a = lane_id(); a < A; a += 32) m = fmax(m, eta * (double)ldp<L2>(row + a));
+  m = warp_max(m);
+  double s = 0.0;
+  for (int a = lane_id(); a < A; a += 32) s += exp(eta * (double)ldp<L2>(row + a) - m);
+  s = warp_sum(s);
+  return m / eta + log(s) / eta;
+}
+
 // numpy-order LSE for the fp64 parity mode: m/eta + log(pairwise sum)/eta.
 template <bool L2 = false>
 __device__ double lse_exact(const double* row, int A, double eta) {
@@ -276,6 +370,36 @@ __device__ __forceinline__ int search_cdf(const CT* cdf, int A, CT u) {
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (cdf[mid] > u) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo < A ? lo : A - 1;
+}
+
+// Draw from an overlay row (search.py:46-83 on init + realised cells): with the row's LSE,
+//   F(a) = s * initCDF(a) + sum_{k: a_k <= a} c_k,   s = exp(eta (LSE_init - LSE)),
+//   c_k = exp(eta (psi_k - LSE)) - exp(eta (init_{a_k} - LSE)),
+// is the row's CDF (the initial CDF rescaled, each realised cell's mass swapped in); the
+// first a with F(a) > u, clamped to |A| - 1.  Probabilities use the dense sampler's
+// arithmetic (exp2(fma(eta log2e, psi, -eta LSE log2e))).
+template <class PsiT>
+__device__ __forceinline__ int draw_overlay(const Rec<PsiT>& r, const PsiT* init_cdf, const PsiT* init_row, int A,
+                                            double eta, double lse, double lse_init, PsiT u) {
+  const PsiT e2 = (PsiT)(eta * kLog2eD), sh2 = (PsiT)(eta * lse * kLog2eD);
+  const PsiT s = (PsiT)exp(eta * (lse_init - lse));
+  int ak[kOverlay];
+  PsiT ck[kOverlay];
+#pragma unroll
+  for (int k = 0; k < kOverlay; ++k) {
+    ak[k] = r.act[k] ? (int)r.act[k] - 1 : A;
+    ck[k] = r.act[k] ? fexp2(ffma(e2, r.val[k], -sh2)) - fexp2(ffma(e2, init_row[ak[k]], -sh2)) : (PsiT)0;
+  }
+  int lo = 0, hi = A;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    PsiT f = s * init_cdf[mid];
+#pragma unroll
+    for (int k = 0; k < kOverlay; ++k) f += ak[k] <= mid ? ck[k] : (PsiT)0;
+    if (f > u) hi = mid;
     else lo = mid + 1;
   }
   return lo < A ? lo : A - 1;
@@ -432,6 +556,37 @@ __device__ __forceinline__ void materialise_rows(const vp_tree& T, const PsiT* i
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// Fast mode: belief b just got its (kOverlay + 1)-th action child -- give it a dense row:
+// the initial row (one TMA bulk store from the block's shared copy) with the record's
+// realised cells written over it (stable during the search: only the backup writes them),
+// then publish {row, pass}.  Draws of this pass keep using the record (dense_pass == pass).
+template <class PsiT>
+__device__ __noinline__ void materialise_dense(const vp_tree& T, unsigned long long* stats, int b,
+                                               const Rec<PsiT>& rec, const PsiT* init_row, u32 pass) {
+  const int r = atomicAdd(&T.counters[VP_COUNTER_DENSE], 1);
+  if (r >= T.cap_dense) {
+    T.counters[2] = 1;  // overflow: the host fails the plan loudly
+    return;
+  }
+  PsiT* row = reinterpret_cast<PsiT*>(T.psi) + (size_t)r * T.psi_stride;
+  const u32 bytes = (u32)(((size_t)T.action_count * sizeof(PsiT) + 15) & ~(size_t)15);
+  if (init_row) {
+    bulk_s2g(row, init_row, bytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  } else {
+    for (int a = 0; a < T.action_count; ++a) row[a] = (PsiT)T.init_prefs[a];
+  }
+#pragma unroll
+  for (int k = 0; k < kOverlay; ++k)
+    if (rec.act[k]) row[rec.act[k] - 1] = rec.val[k];
+  Rec<PsiT>* g = rec_ptr<PsiT>(T, b);
+  g->dense_row = (u32)r;
+  g->dense_pass = pass;
+  if (stats) atomicAdd(&stats[10], 1ull);
+}
+
 // Numbered-node allocation for the winners of a warp: one atomic per warp.
 __device__ __forceinline__ int warp_alloc(int* counter, bool won) {
   const u32 winners = __ballot_sync(FULL, won);
@@ -472,7 +627,7 @@ __device__ void block_tree_init(const vp_tree& T) {
       if (threadIdx.x == 0) v = lse_exact(reinterpret_cast<const double*>(psi), A, T.eta);
       v = __shfl_sync(FULL, v, 0);
     } else {
-      v = row_lse_fast<PsiT>(psi, A, T.eta);
+      v = row_lse_f64<PsiT>(psi, A, T.eta);
     }
     // normalised CDF of the initial row with the fast sampler's arithmetic (warp-parallel)
     PsiT* cdf = reinterpret_cast<PsiT*>(T.init_cdf);
@@ -493,6 +648,14 @@ __device__ void block_tree_init(const vp_tree& T) {
       reinterpret_cast<Acc*>(T.b_acc)[0] = Acc{0.0, 0u, 0u};
       T.b_flags[0] = 0;  // the root row is written (above), not lazy
       T.b_ckey[0] = 0;
+      T.b_nact[0] = 0;
+      if constexpr (!Exact) {  // the root owns dense row 0 from the start (it is the busiest row)
+        Rec<PsiT> r{};
+        r.dense_pass = 1;
+        r.dense_row = 0;
+        *rec_ptr<PsiT>(T, 0) = r;
+        T.counters[VP_COUNTER_DENSE] = 1;
+      }
       T.counters[0] = 1;
       T.counters[VP_COUNTER_ACTIONS] = 0;
       T.counters[2] = 0;
@@ -593,7 +756,8 @@ __device__ __forceinline__ void publish_pending_cdf(const vp_tree& T, int& pend,
 
 template <class PsiT, bool Exact>
 __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, Stage<PsiT>& sg, const PsiT* init_cdf,
-                                           int b, u32 fl, bool ok, double u, u32 pass, int& pend, int& pend_b) {
+                                           const PsiT* init_row, int b, u32 fl, const Rec<PsiT>& rec, double lse,
+                                           double lse_init, bool ok, double u, u32 pass, int& pend, int& pend_b) {
   const int A = T.action_count, lane = lane_id();
   const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
   PsiT* cache = reinterpret_cast<PsiT*>(T.cdf_cache);
@@ -609,9 +773,18 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
     // CDFs this lane built at the previous level: the bulk stores have long
     // completed; make them visible and stamp them with the pass
     publish_pending_cdf(T, pend, pend_b, pass);
-    const bool fresh = ok && (fl & 1u);
-    const bool need = ok && !fresh;
-    if (fresh) a = search_cdf(init_cdf, A, (PsiT)u);
+    // fast mode: a belief with a dense row written before this pass draws from that row
+    // (staged below); every other belief draws from its overlay record -- the initial CDF
+    // itself when no cell is realised yet
+    const bool need = ok && rec.dense_pass != 0 && rec.dense_pass < pass;
+    const bool ovl = ok && !need && rec_any(rec);
+    if (ok && !need)
+      a = ovl ? draw_overlay<PsiT>(rec, init_cdf, init_row, A, T.eta, lse, lse_init, (PsiT)u)
+              : search_cdf(init_cdf, A, (PsiT)u);
+    if (W.stats) {
+      const u32 om = __ballot_sync(FULL, ovl);
+      if (lane == 0 && om) atomicAdd(&W.stats[9], (unsigned long long)__popc(om));
+    }
     // Distinct non-fresh beliefs of the warp: one TMA bulk copy of each row into the
     // warp's stage -- the row's normalised CDF if some warp already built it this pass
     // (the PSI row is read-only during a pass), else its PSI row, which the warp turns
@@ -639,8 +812,12 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
                           cdf_tag(pass, b) | kCdfBuilding) == tag;
     }
     const u32 cmask = __ballot_sync(FULL, cached);
+    if (W.stats) {  // CDFs built this pass: ~ the distinct dense rows sampled (compulsory reads)
+      const u32 bm = __ballot_sync(FULL, claim);
+      if (lane == 0 && bm) atomicAdd(&W.stats[11], (unsigned long long)__popc(bm));
+    }
     if (cmask) asm volatile("fence.proxy.async.global;" ::: "memory");
-    const PsiT sh2 = lead && !cached ? (PsiT)(T.eta * T.b_lse[b] * kLog2eD) : (PsiT)0;
+    const PsiT sh2 = lead && !cached ? (PsiT)(T.eta * lse * kLog2eD) : (PsiT)0;
     for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
       const int cnt = min(sg.cfg.rows, K - s0);
       fence_async_smem();
@@ -649,8 +826,8 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
       const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
       PsiT* srow = sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride;
       if (mine && lane == my_leader)
-        bulk_g2s(srow, cached ? cache + (size_t)cslot * T.psi_stride : psi + (size_t)b * T.psi_stride, row_bytes,
-                 sg.bar);
+        bulk_g2s(srow, cached ? cache + (size_t)cslot * T.psi_stride : psi + (size_t)rec.dense_row * T.psi_stride,
+                 row_bytes, sg.bar);
       mbar_wait(sg.bar, sg.phase);
       sg.phase ^= 1u;
       u32 rem = leaders;
@@ -717,18 +894,27 @@ __device__ __forceinline__ int find_key(const Slot* tab, u64 mask, u64 key) {
 // initial -- so the trajectory is that of the fused search.
 template <class Model, class PsiT, bool Exact>
 __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
-                                Stage<PsiT>& sg, const PsiT* init_cdf, typename Model::State& st, int r, int rg,
-                                bool active, u64 skey) {
+                                Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, double lse_init,
+                                typename Model::State& st, int r, int rg, bool active, u64 skey) {
   const int n = W.n;
   const Slot* ha = slots(T.hash_a);
   const Slot* hb = slots(T.hash_b);
   int b = 0, pend = -1, pend_b = 0;
   bool known = active;  // the row's belief existed when the pass started
   u32 fl = known ? T.b_flags[0] : 1u;
+  Rec<PsiT> rec{};  // fast mode: the belief's overlay record (zero: initial row)
+  double lse = lse_init;
+  if constexpr (!Exact) {
+    if (known) {
+      rec = load_rec<PsiT>(T, 0);
+      lse = T.b_lse[0];
+    }
+  }
   for (int l = 0; l < S.d_max; ++l) {
     const u64 lkey = fold(skey, (u64)l);
     const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
-    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, known ? fl : 1u, active, u, S.pass, pend, pend_b);
+    const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, known ? fl : 1u, rec, lse, lse_init, active,
+                                           u, S.pass, pend, pend_b);
     u32 o = 0;
     double rw = 0.0;
     model_step<Model>(M, st, a, fold(lkey, 1), rg, active, o, rw);
@@ -745,6 +931,13 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
       if (known) {
         b = c;
         fl = T.b_flags[c];
+        if constexpr (!Exact) {
+          rec = load_rec<PsiT>(T, c);
+          lse = T.b_lse[c];
+        }
+      } else if constexpr (!Exact) {
+        rec = Rec<PsiT>{};  // off the tree: the initial row from here on
+        lse = lse_init;
       }
     }
   }
@@ -798,12 +991,23 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     }
   }
   if (S.mode == VP_SEARCH_TRAJECTORY) {
-    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, st, r, rg, active, skey);
+    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, T.init_lse[0], st, r, rg, active, skey);
     return;
   }
   int b = active ? (S.start_beliefs ? S.start_beliefs[r] : 0) : 0;
   bool ok = active;
-  u32 fl = ok ? T.b_flags[b] : 0u;  // flags of nodes older than this pass are stable here
+  u32 fl = Exact && ok ? T.b_flags[b] : 0u;  // flags of nodes older than this pass are stable here
+  // fast mode: the lane's view of its belief -- overlay record and cached LSE (stable during
+  // the search except a dense row's publication, which draws of this pass ignore)
+  const double lse_init = T.init_lse[0];
+  Rec<PsiT> rec{};
+  double lse = lse_init;
+  if constexpr (!Exact) {
+    if (ok) {
+      rec = load_rec<PsiT>(T, b);
+      lse = T.b_lse[b];
+    }
+  }
   u32 grp = __match_any_sync(FULL, ok ? (u32)b : 0xffffffffu);
   bool lead = ok && lane == __ffs(grp) - 1;
   arrive(T, W, leaf_count, b, grp, lead, depth0 == d);
@@ -822,9 +1026,9 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (ld) {
         red_add(&T.a_rows[x], __popc(g));
         red_add(&T.b_rows[p], __popc(g));
-        if (T.b_flags[p] & 2u) mat = atomicAnd(&T.b_flags[p], ~2u) & 2u;
+        if (Exact && (T.b_flags[p] & 2u)) mat = atomicAnd(&T.b_flags[p], ~2u) & 2u;
       }
-      materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), p);
+      if constexpr (Exact) materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), p);
       cur = p;
     }
   }
@@ -833,8 +1037,8 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   int pend = -1, pend_b = 0;   // CDF cache slot (and belief) this lane wrote, tag pending
   for (int l = depth0; l < d; ++l) {
     const u64 lkey = fold(skey, (u64)l);  // search.py:107
-    // ---- lazy rows: b is interior at this level; write its PSI row once
-    {
+    // ---- parity mode, lazy rows: b is interior at this level; write its PSI row once
+    if constexpr (Exact) {
       bool mat = made_interior;
       if (lead && !made_interior && (fl & 2u)) mat = atomicAnd(&T.b_flags[b], ~2u) & 2u;
       materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), b);
@@ -843,7 +1047,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
     int a = 0;
     if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
-    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, b, fl, ok, u, pass, pend, pend_b);
+    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, fl, rec, lse, lse_init, ok, u, pass, pend, pend_b);
     // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
     double rw = 0.0;
@@ -879,6 +1083,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     int id_a = 0, id_b = 0;
     warp_alloc2(&T.counters[VP_COUNTER_ACTIONS], cl_a.won, &T.counters[0], early && cl_b.won, id_a, id_b);
     int x = 0;
+    int kslot = 0;  // the new action's child index under b (overlay slot); consumed after the belief claim
     if (cl_a.won) {
       x = id_a;
       if (x < T.cap_actions) {
@@ -886,6 +1091,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         T.a_parent_belief[x] = b;
         T.a_action[x] = a;
         red_min(&T.a_ckey[x], creation_key(pass, l, rg));
+        kslot = atomicAdd(&T.b_nact[b], 1);
       } else {
         T.counters[2] = 1;  // overflow: the host fails the plan loudly
       }
@@ -961,6 +1167,12 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       }
     }
     ok = ok && c < T.cap_beliefs;
+    if (cl_a.won && x < T.cap_actions) {
+      T.a_slot[x] = kslot;
+      // fast mode: the (kOverlay + 1)-th child of b gives b a dense row
+      if constexpr (!Exact)
+        if (kslot == kOverlay && rec.dense_pass == 0) materialise_dense<PsiT>(T, W.stats, b, rec, init_row, pass);
+    }
     arrive(T, W, leaf_count, c, grp, lead && ok, !interior_next);
     if (active && W.trace_action) {
       const size_t t = (size_t)l * n + r;
@@ -970,7 +1182,16 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       W.trace_belief[t] = c;
     }
     b = c;
-    fl = c_new ? (interior_next ? 1u : 3u) : (ok ? T.b_flags[c] : 0u);
+    if constexpr (Exact) fl = c_new ? (interior_next ? 1u : 3u) : (ok ? T.b_flags[c] : 0u);
+    if constexpr (!Exact) {
+      if (c_new || !ok) {  // created this pass: the initial row
+        rec = Rec<PsiT>{};
+        lse = lse_init;
+      } else {
+        rec = load_rec<PsiT>(T, c);
+        lse = T.b_lse[c];
+      }
+    }
   }
 
   // ---- leaves: heuristic value (search.py:119), summed per leaf (backup.py:44-51)
@@ -1003,22 +1224,36 @@ __device__ __forceinline__ void lse_ready(const vp_tree& T, int ready, u32 rmask
   if constexpr (Exact) {
     if (ready >= 0) out[lane_id()] = lse_exact<true>(reinterpret_cast<const double*>(psi) + (size_t)ready * T.psi_stride,
                                                       A, T.eta);
-  } else {
-    with_group(A, [&](auto g) {
-      constexpr int G = decltype(g)::value;
-      constexpr int RPW = 32 / G;  // rows per warp per round
-      const int gl = lane_id() & (G - 1), gi = lane_id() / G;
-      const int k = __popc(rmask);
-      for (int p0 = 0; p0 < k; p0 += RPW) {
-        const int idx = p0 + gi;
-        const int owner = idx < k ? (int)__fns(rmask, 0, idx + 1) : -1;
-        const int bb = __shfl_sync(FULL, ready, owner < 0 ? 0 : owner);
-        const double v = lse_group<PsiT, G, true>(owner >= 0 ? psi + (size_t)bb * T.psi_stride : nullptr, A, T.eta);
-        if (owner >= 0 && gl == 0) out[owner] = v;
-      }
-    });
+  } else {  // the rare fallback of the incremental LSE: one row at a time, fp64 arithmetic
+    for (u32 m = rmask; m; m &= m - 1u) {
+      const int owner = __ffs(m) - 1;
+      const int row = __shfl_sync(FULL, ready, owner);
+      const double v = row_lse_f64<PsiT, true>(psi + (size_t)row * T.psi_stride, A, T.eta);
+      if (lane_id() == owner) out[owner] = v;
+    }
   }
   __syncwarp();
+}
+
+// LSE of an overlay row (initial row + the record's realised cells) by one lane in fp64:
+// the rare fallback of the incremental backup LSE.  The record is read from L2.
+template <class PsiT>
+__device__ __noinline__ double lse_overlay(const vp_tree& T, int b) {
+  const Rec<PsiT> r = load_rec<PsiT, true>(T, b);
+  const int A = T.action_count;
+  const double eta = T.eta;
+  auto val = [&](int a) -> double {
+    double v = (double)(PsiT)T.init_prefs[a];
+#pragma unroll
+    for (int k = 0; k < kOverlay; ++k)
+      if (r.act[k] == a + 1) v = (double)r.val[k];
+    return v;
+  };
+  double m = -INFINITY;
+  for (int a = 0; a < A; ++a) m = fmax(m, eta * val(a));
+  double s = 0.0;
+  for (int a = 0; a < A; ++a) s += exp(eta * val(a) - m);
+  return m / eta + log(s) / eta;
 }
 
 // One warp = up to 32 distinct leaves; each lane climbs while it is the last
@@ -1054,6 +1289,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0;
   while (__any_sync(FULL, live)) {
     int ready = -1, nx = -1, npb = -1, nact = 0;
+    int prow = -1;  // the PSI row of a completed belief's full-row fallback (-1: overlay row)
+    u32 slotbit = 0, bmask = 0;  // overlay slot this lane's action changed / all changed slots
+    Rec<PsiT> prec{};            // fast mode: the parent belief's overlay record
     double lse_pre = 0.0, bsum = 0.0;
     u32 bcnt = 0, btot = 0;
     bool fresh = false;
@@ -1061,15 +1299,24 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
       live = false;
       if (x >= 0) {
         // ONE round trip for everything a completing delivery needs -- the action's
-        // statistics, the parent belief's LSE / rows / flags, the PSI cell -- and the next
-        // level's pointers.  All of it is stable until this lane completes the nodes.
+        // statistics, the parent belief's LSE / rows, its PSI cell (parity mode) or overlay
+        // record + the action's slot (fast mode) -- and the next level's pointers.  All of it
+        // is stable until this lane completes the nodes.
         const int tot = T.a_rows[x], vis = T.a_visits[x];
         const double rew = T.a_reward[x];
         lse_pre = T.b_lse[pb];
         btot = (u32)T.b_rows[pb];
-        const u32 pflags = T.b_flags[pb];
-        PsiT* cell = psi + (size_t)pb * T.psi_stride + act;
-        const double old_v = (double)__ldcg(cell);
+        PsiT* cell = nullptr;
+        double old_v = 0.0, init_v = 0.0;
+        int slot = 0;
+        if constexpr (Exact) {
+          cell = psi + (size_t)pb * T.psi_stride + act;
+          old_v = (double)__ldcg(cell);
+        } else {
+          prec = load_rec<PsiT>(T, pb);  // slots untouched this pass are stable in this kernel
+          slot = T.a_slot[x];
+          init_v = T.init_prefs[act];
+        }
         nx = T.b_parent_action[pb];
         npb = T.b_parent_belief[pb];
         nact = T.b_parent_act[pb];
@@ -1079,46 +1326,102 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
           // last child: Q (backup.py:96-104) and PSI[b, a] += Q - LSE_pre(b) (:106-108)
           ++n_act;
           T.a_rows[x] = 0;
-          fresh = !Exact && (pflags & 1u);
           const double q = rew / (double)vis + (gamma * aa.sum) / (double)aa.cnt;
-          const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
-          *cell = new_v;
-          // a lazily-initial row (LSE_pre is its exact LSE): LSE_post follows from the
-          // changed cells, sum_a exp(eta (psi_a - LSE_pre)) = 1 + sum_changed (new - old)
           double term = 0.0;
-          if (fresh) term = exp(eta * ((double)new_v - lse_pre)) - exp(eta * (old_v - lse_pre));
-          else __threadfence();  // the full-row LSE of pb reads this cell from another SM
+          if constexpr (Exact) {
+            *cell = (PsiT)(old_v + (q - lse_pre));
+            __threadfence();  // the full-row LSE of pb reads this cell from another SM
+          } else {
+            // LSE_pre is the row's LSE, so LSE_post follows from the changed cells:
+            // sum_a exp(eta (psi_a - LSE_pre)) = 1 + sum_changed (new - old)
+            fresh = true;
+            const bool dense = prec.dense_pass != 0;
+            if (dense) {
+              prow = (int)prec.dense_row;
+              cell = psi + (size_t)prow * T.psi_stride + act;
+              old_v = (double)__ldcg(cell);
+            } else if (slot < kOverlay) {
+              old_v = prec.act[slot] ? (double)prec.val[slot] : (double)(PsiT)init_v;
+            } else {
+              T.counters[2] = 1;  // a child beyond the overlay without a dense row: fail loudly
+            }
+            const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
+            if (dense) {
+              term = exp(eta * ((double)new_v - lse_pre)) - exp(eta * (old_v - lse_pre));
+              *cell = new_v;
+              __threadfence();  // an ill-conditioned sum makes the completing lane read the row
+            } else if (slot < kOverlay) {
+              // overlay row: deliver the new cell's log-mass eta psi and flag its slot; the
+              // completing lane adds the unchanged cells (untouched slots + unrealised initial
+              // cells) in log space, so nothing cancels, overflows or underflows
+              term = eta * (double)new_v;
+              slotbit = kSlotBit << slot;
+              Rec<PsiT>* g = rec_ptr<PsiT>(T, pb);
+              g->val[slot] = new_v;
+              g->act[slot] = (unsigned short)(act + 1);
+              if (!T.init_uniform) __threadfence();  // the general LSE reads every cell
+            }
+          }
           // N(b) = lifetime visits of the valued actions (backup.py:110-114)
           Acc ba;
-          if (acc_deliver(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba)) {
+          const bool done = slotbit ? acc_deliver_log(T.b_acc, pb, term, (u32)tot | slotbit, (u32)vis, btot, ba)
+                                    : acc_deliver(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba);
+          if (done) {
             ready = pb;
             bsum = ba.sum;
             bcnt = ba.cnt;
+            bmask = ba.rows >> 24;
           }
         }
       }
     }
     if (__any_sync(FULL, ready >= 0)) {
       // last action of a belief: V = LSE_post (backup.py:109), cached as the next LSE_pre.
-      // Lazily-initial rows use the incremental sum; other rows (and tiny / overflowing
-      // incremental sums) are read in full by the warp.
+      // Fast mode uses the incremental sum; parity mode (and tiny / overflowing incremental
+      // sums) read the row in full -- the warp for PSI rows, the lane for an overlay row.
       bool full = ready >= 0;
-      if (fresh) {
-        const double sum = 1.0 + bsum;
-        if (sum > 1e-9 && sum < 1e300) {
-          V = lse_pre + log(sum) / eta;
+      bool ofull = false;
+      if constexpr (!Exact) {
+        if (fresh && prow < 0 && T.init_uniform) {
+          // overlay row: eta LSE = log sum_a exp(eta psi_a) = the changed cells (delivered, log
+          // space) (+) the slots untouched this pass (stable in this lane's record) (+) the
+          // unrealised initial cells, (|A| - filled) exp(eta init)
+          double l = bsum;
+          int filled = __popc(bmask);
+#pragma unroll
+          for (int k = 0; k < kOverlay; ++k)
+            if (!((bmask >> k) & 1u) && prec.act[k]) {
+              l = log_add_exp(l, eta * (double)prec.val[k]);
+              ++filled;
+            }
+          if (T.action_count > filled)
+            l = log_add_exp(l, eta * (double)(PsiT)T.init_prefs[0] + log((double)(T.action_count - filled)));
+          V = l / eta;
           full = false;
+        } else if (fresh && prow >= 0) {
+          // dense row: 1 + sum_changed (new - old); well conditioned unless the changed cells
+          // carried most of the mass -- then the warp reads the row
+          const double sum = 1.0 + bsum;
+          if (sum > 0.9 && sum < 1e300) {
+            V = lse_pre + log(sum) / eta;
+            full = false;
+          }
+        }
+        ofull = full && prow < 0;
+        if (ofull) {  // overlay row of a non-uniform initial row: every writer fenced
+          __threadfence();
+          V = lse_overlay<PsiT>(T, ready);
         }
       }
-      const u32 fmask = __ballot_sync(FULL, full);
+      const u32 fmask = __ballot_sync(FULL, full && !ofull);
       if (fmask) {
         __threadfence();
-        lse_ready<PsiT, Exact>(T, full ? ready : -1, fmask, s_v);
+        lse_ready<PsiT, Exact>(T, full && !ofull ? (Exact ? ready : prow) : -1, fmask, s_v);
       }
       if (ready >= 0) {
         ++n_bel;
         if (full) {
-          V = s_v[lane];
+          if (!ofull) V = s_v[lane];
           ++n_psi;
         }
         T.b_lse[ready] = V;

@@ -125,11 +125,14 @@ class Planner:
         return min(need, max(self.node_budget(A), 1 + n * levels)), levels
 
     def node_budget(self, A: int, fraction: float | None = None) -> int:
-        """Nodes (belief + action pairs) that fit in mem_fraction of the free HBM: a PSI row and
-        the B columns per belief, the A columns per action, and a 2x-oversized 16-B hash slot each."""
+        """Nodes (belief + action pairs) that fit in mem_fraction of the free HBM: the B columns
+        per belief (+ its overlay record), the A columns per action, a 2x-oversized 16-B hash
+        slot each, and PSI rows -- one per belief in parity mode, one per 5 actions at most in
+        fast mode (only beliefs with more than 4 action children own a dense row)."""
         torch = _torch()
         elem = 4 if self.precision == "fp32" else 8
-        per_pair = (A + 4) * elem + 60 + 48 + 2 * 2 * 16
+        per_row = (A + 4) * elem if self.exact else (A + 4) * elem // (_lib.VP_OVERLAY_SLOTS + 1) + 8 * elem + 8
+        per_pair = per_row + 60 + 52 + 2 * 2 * 16
         free, _ = torch.cuda.mem_get_info()
         return int(free * (self.mem_fraction if fraction is None else fraction)) // per_pair
 

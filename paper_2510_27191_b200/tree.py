@@ -4,9 +4,14 @@
 Layout (all device tensors, row-indexed):
 
     B   b_parent_action i32 | b_parent_obs u32 | b_depth i32 | b_ckey i64
-    PSI psi [cap_beliefs, stride] fp32 (fast) or fp64 (parity), row-major,
-        rows padded to 16 B; b_flags bit 0 = row still lazily equal to init,
-        bit 1 = row not yet written
+    PSI psi [cap_dense, stride] fp32 (fast) or fp64 (parity), row-major, rows
+        padded to 16 B.  Parity mode: row b is belief b's (b_flags bit 0 = row
+        still lazily equal to init, bit 1 = row not yet written).  Fast mode: a
+        belief's row is the initial row overlaid with <= 4 realised cells kept in
+        its 32-B record b_rec {dense_pass, dense_row, action+1 [4], value [4]};
+        only beliefs with more than 4 action children own a dense row
+        (cap_dense = cap_actions // 5 + 2 rows bound them); b_nact counts the
+        children, a_slot is an action's child index
         b_lse f64 (cached LSE of the row) | b_value f64, b_rows i32, b_acc 16 B (pass scratch)
     A   a_parent_belief i32 | a_action i32 | a_reward f64 | a_visits i32 | a_ckey i64
         a_rows i32, a_acc 16 B (pass scratch)
@@ -58,7 +63,7 @@ class DeviceTree:
     CDF_SLOTS = 1 << 16  # direct-mapped CDF cache rows (csrc draw_action)
 
     def __init__(self, action_count: int, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32",
-                 exact: bool = False, cap_beliefs: int = 4096, cap_actions: int = 4096):
+                 exact: bool = False, cap_beliefs: int = 4096, cap_actions: int = 4096, cap_dense: int = 0):
         if action_count < 1:
             raise ValueError("action_count must be >= 1")
         if precision not in PRECISIONS:
@@ -86,14 +91,24 @@ class DeviceTree:
         self._host_counts = (C.c_int32 * 3)()
         self.cap_beliefs = 0
         self.cap_actions = 0
-        self._allocate(max(16, cap_beliefs), max(16, cap_actions))
+        self.overlay_slots = 0 if self.exact else _lib.VP_OVERLAY_SLOTS
+        self._allocate(max(16, cap_beliefs), max(16, cap_actions), min_dense=cap_dense)
         self.reset(init_prefs, eta)
 
     # ------------------------------------------------------------------ storage
-    def _allocate(self, cap_b: int, cap_a: int, keep_b: int = 0, keep_a: int = 0):
+    def dense_rows_for(self, cap_b: int, cap_a: int) -> int:
+        """PSI rows the arena needs: one per belief in parity mode; in fast mode one per
+        belief with more than ``overlay_slots`` action children (each owns >= slots + 1 of
+        the cap_a actions) plus the root."""
+        return cap_b if self.exact else cap_a // (self.overlay_slots + 1) + 2
+
+    def _allocate(self, cap_b: int, cap_a: int, keep_b: int = 0, keep_a: int = 0, keep_dense: int = 0,
+                  min_dense: int = 0):
         torch = _torch()
         dev = "cuda"
         A = self.action_count
+        cap_d = max(self.dense_rows_for(cap_b, cap_a), min_dense, keep_dense, 1)
+        rec_words = 8 if self.precision == "fp32" else 12  # sizeof(Rec<PsiT>) / 4 (32 / 48 bytes)
 
         def col(old, shape, dtype, keep, fill=None):
             # accumulators start at zero and creation keys unset (-1 = ~0): node creation
@@ -110,12 +125,14 @@ class DeviceTree:
         self.b_parent_belief = col(g("b_parent_belief"), cap_b, torch.int32, keep_b)
         self.b_parent_act = col(g("b_parent_act"), cap_b, torch.int32, keep_b)
         self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
-        self.psi = col(g("psi"), (cap_b, self.psi_stride), self._psi_dtype, keep_b)
+        self.psi = col(g("psi"), (cap_d, self.psi_stride), self._psi_dtype, keep_b if self.exact else keep_dense)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
         self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b, 0)
         self.b_rows = col(g("b_rows"), cap_b, torch.int32, keep_b, 0)
         self.b_acc = col(g("b_acc"), (cap_b, 2), torch.int64, keep_b, 0)
         self.b_flags = col(g("b_flags"), cap_b, torch.int32, keep_b)
+        self.b_rec = col(g("b_rec"), (cap_b, rec_words), torch.int32, keep_b, 0)
+        self.b_nact = col(g("b_nact"), cap_b, torch.int32, keep_b, 0)
         self.b_ckey = col(g("b_ckey"), cap_b, torch.int64, keep_b, -1)
         slots = min(_pow2_at_least(cap_b), self.CDF_SLOTS)
         if getattr(self, "cdf_tag", None) is None or self.cdf_tag.numel() != slots:
@@ -128,11 +145,12 @@ class DeviceTree:
         self.a_rows = col(g("a_rows"), cap_a, torch.int32, keep_a, 0)
         self.a_acc = col(g("a_acc"), (cap_a, 2), torch.int64, keep_a, 0)
         self.a_ckey = col(g("a_ckey"), cap_a, torch.int64, keep_a, -1)
+        self.a_slot = col(g("a_slot"), cap_a, torch.int32, keep_a, 0)
         ha = _pow2_at_least(2 * cap_a)
         hb = _pow2_at_least(2 * cap_b)
         self.hash_a = torch.empty((ha, 2), dtype=torch.int64, device=dev)
         self.hash_b = torch.empty((hb, 2), dtype=torch.int64, device=dev)
-        self.cap_beliefs, self.cap_actions = cap_b, cap_a
+        self.cap_beliefs, self.cap_actions, self.cap_dense = cap_b, cap_a, cap_d
         s = _lib.VpTree()
         s.cap_beliefs, s.cap_actions, s.action_count = cap_b, cap_a, A
         s.psi_dtype = PRECISIONS[self.precision]
@@ -140,10 +158,12 @@ class DeviceTree:
         s.hmask_a, s.hmask_b = ha - 1, hb - 1
         s.psi_stride = self.psi_stride
         for name in ("b_parent_action", "b_parent_obs", "b_parent_belief", "b_parent_act", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
-                     "b_flags", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits", "a_rows", "a_acc",
-                     "a_ckey", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
+                     "b_flags", "b_rec", "b_nact", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits",
+                     "a_rows", "a_acc", "a_ckey", "a_slot", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.cdf_slots = self.cdf_tag.numel()
+        s.cap_dense = cap_d
+        s.overlay_slots = self.overlay_slots
         s.bkey_mode = getattr(self, "bkey_mode", 0)
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
@@ -188,6 +208,7 @@ class DeviceTree:
         if getattr(self, "init_prefs", None) is None or not np.array_equal(self.init_prefs, base):
             self._init_prefs.copy_(torch.from_numpy(base))
         self.init_prefs = base
+        self.struct.init_uniform = int(bool(np.all(base == base[0])))
         self.generation += 1
         self.pass_cursor = 0
         self._canon_cache = None
@@ -212,9 +233,15 @@ class DeviceTree:
         cap_a = max(self.cap_actions, 16)
         while cap_a < need_actions:
             cap_a *= 2
-        self._allocate(cap_b, cap_a, keep_b=nb, keep_a=na)
+        self._allocate(cap_b, cap_a, keep_b=nb, keep_a=na, keep_dense=self.n_dense())
         _lib.call("vp_tree_rehash", C.byref(self.struct), _stream())
         return True
+
+    def n_dense(self) -> int:
+        """PSI rows in use (parity mode: the belief count)."""
+        if self.exact:
+            return self.counts()[0]
+        return int(self._counters[_lib.VP_COUNTER_DENSE].item())
 
     def next_pass(self) -> int:
         """Pass number of the next search on this tree (ckey order, leaf-list parity)."""
@@ -364,7 +391,8 @@ class DeviceTree:
             raise ValueError("serialized tree must start with belief row 0")
         A = len(p_rows[0][1])
         nb, na = len(b_rows), len(a_rows)
-        tree = cls(A, eta=eta, precision=precision, cap_beliefs=max(16, nb), cap_actions=max(16, na))
+        tree = cls(A, eta=eta, precision=precision, cap_beliefs=max(16, nb), cap_actions=max(16, na),
+                   cap_dense=nb)
         prefs = np.zeros((nb, A))
         for row, vals in p_rows:
             prefs[row] = vals
@@ -383,6 +411,12 @@ class DeviceTree:
                               + np.log(np.exp(eta * prefs - np.max(eta * prefs, axis=1)[:, None]).sum(axis=1)) / eta,
                               torch.float64)
         tree.b_flags[:nb] = 0  # every row is written
+        if not tree.exact:  # fast mode: every belief owns its dense row (row = id)
+            tree.b_rec[:nb] = 0
+            tree.b_rec[:nb, 0] = 1
+            tree.b_rec[:nb, 1] = torch.arange(nb, device="cuda", dtype=torch.int32)
+            tree.b_nact[:nb] = tree.overlay_slots + 1
+            tree._counters[_lib.VP_COUNTER_DENSE] = nb
         tree.b_ckey[:nb] = torch.arange(nb, device="cuda", dtype=torch.int64)  # canonical order = ids
         if na:
             tree.a_parent_belief[:na] = dev(apb, torch.int32)
@@ -426,10 +460,7 @@ class DeviceTree:
         obs = self.b_parent_obs[:nb][border].cpu().numpy().view(np.uint32).astype(np.int64)
         if nb:
             obs[0] = ROOT_SENTINEL
-        fresh = (self.b_flags[:nb][border] & 1).bool()[:, None]
-        init = self._init_prefs.to(self._psi_dtype)[None, :]
-        # lazily initialised rows read as the initial row (tree.py:253)
-        prefs = torch.where(fresh, init, self.psi[:nb, : self.action_count][border]).cpu().numpy().astype(np.float64)
+        prefs = self._prefs_rows(nb)[border].cpu().numpy().astype(np.float64)
         apb = brank[self.a_parent_belief[:na].to(torch.int64)[aorder]] if na else torch.zeros(0, dtype=torch.int64)
         return {
             "parent_action": pa.cpu().numpy(),
@@ -442,6 +473,29 @@ class DeviceTree:
             "action_visits": self.a_visits[:na][aorder].cpu().numpy().astype(np.int64),
         }
 
+
+    def _prefs_rows(self, nb: int):
+        """[nb, |A|] PSI rows in device order, the dtype of the tree."""
+        torch = _torch()
+        A = self.action_count
+        init = self._init_prefs.to(self._psi_dtype)[None, :]
+        if self.exact:  # lazily initialised rows read as the initial row (tree.py:253)
+            fresh = (self.b_flags[:nb] & 1).bool()[:, None]
+            return torch.where(fresh, init, self.psi[:nb, :A])
+        rec = self.b_rec[:nb]
+        dense_pass, dense_row = rec[:, 0], rec[:, 1].to(torch.int64)
+        act = rec[:, 2:4].contiguous().view(torch.int16).to(torch.int64) & 0xFFFF  # action + 1, 0 = empty
+        val = rec[:, 4:].contiguous().view(self._psi_dtype)[:, : self.overlay_slots]
+        rows = init.expand(nb, A).clone()
+        dense = dense_pass != 0
+        if bool(dense.any()):
+            rows[dense] = self.psi[dense_row[dense], :A]
+        for k in range(self.overlay_slots):
+            m = (act[:, k] > 0) & ~dense
+            if bool(m.any()):
+                idx = torch.nonzero(m).squeeze(1)
+                rows[idx, act[idx, k] - 1] = val[idx, k]
+        return rows
 
     def root_prefs(self) -> np.ndarray:
         return self.psi[0, : self.action_count].cpu().numpy().astype(np.float64)

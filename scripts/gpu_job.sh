@@ -1,4 +1,7 @@
+#!/bin/bash
+# Ad-hoc GPU job: full -m gpu suite (no -x, failure summary), then optional extra command.
 cd "$GRAFT_REPO_ROOT" || cd /root/repo
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_acceptance.py -x -q -s -p no:cacheprovider > gpurun_out/acc.log 2>&1; echo "acc rc=$?"; tail -15 gpurun_out/acc.log
-timeout 900 bash scripts/ncu_capture.sh r02c2 7 > gpurun_out/ncu_r02c2.log 2>&1; echo "ncu rc=$?"
+timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -m gpu -q -p no:cacheprovider -x ${PYTEST_ARGS} > gpurun_out/gputest.log 2>&1
+echo "pytest rc=$?"; grep -E "passed|failed|FAILED|Error" gpurun_out/gputest.log | tail -25
+if [ -n "${EXTRA}" ]; then eval "${EXTRA}"; fi
