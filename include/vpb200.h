@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 7
+#define VPB200_ABI_VERSION 8
 
 enum vp_status {
   VP_OK = 0,
@@ -49,6 +49,9 @@ enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
 
 #define VP_COUNTERS 64
 #define VP_COUNTER_ACTIONS 32
+#define VP_COUNTER_LIVE_B 8     /* beliefs actually created (ids below [0] may be unused) */
+#define VP_COUNTER_LIVE_A 16    /* actions actually created */
+#define VP_COUNTER_DONE 24      /* search blocks finished (last one advances the id extents) */
 #define VP_COUNTER_DENSE 48   /* dense PSI rows handed out (fast mode), own 128-B line */
 #define VP_OVERLAY_SLOTS 4    /* realised PSI cells a belief keeps inline before it gets a dense row */
 
@@ -150,8 +153,10 @@ typedef struct vp_tree {
   /* open-addressing hash indexes, 16-byte slots {u64 key; u32 id; u32 pass} */
   void* hash_a;               /* (belief << 32 | action)  -> action row     */
   void* hash_b;               /* belief key (see bkey_mode) -> belief row    */
-  int32_t* counters;          /* [VP_COUNTERS]: [0] n_beliefs, [2] overflow, [VP_COUNTER_ACTIONS] n_actions
-                               (the two id counters on separate 128-B lines: every warp allocates from both) */
+  int32_t* counters;          /* [VP_COUNTERS]: [0] belief id extent, [2] overflow, [VP_COUNTER_ACTIONS] action id
+                               extent, [VP_COUNTER_LIVE_B/_A] live node counts.  A search pass numbers
+                               nodes statically -- row r creating at level l takes id extent + l n + r --
+                               so ids below the extents may be unused (creation key ~0) */
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
@@ -283,7 +288,8 @@ int32_t vp_tree_init(const vp_tree* tree, void* stream);
 int32_t vp_tree_set_eta(const vp_tree* tree, void* stream);
 /* Rebuild both hash indexes from the node columns (after capacity growth). */
 int32_t vp_tree_rehash(const vp_tree* tree, void* stream);
-/* Copy (n_beliefs, n_actions, overflow) to host memory (3 x int32). */
+/* Copy (n_beliefs, n_actions, overflow, belief id extent, action id extent) to host
+ * memory (5 x int32): live node counts and the id ranges the columns use. */
 int32_t vp_tree_counts(const vp_tree* tree, int32_t* host_out, void* stream);
 
 /* ---- planning step pieces ---------------------------------------------- */

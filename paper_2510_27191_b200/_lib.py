@@ -20,8 +20,9 @@ VP_MODEL_CROWDNAV = 6
 CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 7
+ABI_VERSION = 8
 VP_COUNTERS, VP_COUNTER_ACTIONS, VP_COUNTER_DENSE = 64, 32, 48  # include/vpb200.h
+VP_COUNTER_LIVE_B, VP_COUNTER_LIVE_A, VP_COUNTER_DONE = 8, 16, 24
 VP_OVERLAY_SLOTS = 4
 
 p_i8, p_i16, p_i32, p_u32, p_f64, p_u8, p_u64 = (

@@ -130,12 +130,14 @@ __global__ void k_rehash(vp_tree T) {
   const int na = T.counters[VP_COUNTER_ACTIONS], nb = T.counters[0];
   const int total = na + nb;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    // ids below the extents that no node took (static per-row numbering) keep ckey ~0
     if (i < na) {
+      if (T.a_ckey[i] == ~0ull) continue;
       const u64 key = ((u64)(u32)T.a_parent_belief[i] << 32) | (u32)T.a_action[i];
       put_final(slots(T.hash_a), T.hmask_a, key, (u32)i);
     } else {
       const int b = i - na;
-      if (b == 0) continue;
+      if (b == 0 || T.b_ckey[b] == ~0ull) continue;
       const u64 key = belief_key(T, T.b_parent_belief[b], T.b_parent_act[b], T.b_parent_action[b], T.b_parent_obs[b]);
       put_final(slots(T.hash_b), T.hmask_b, key, (u32)b);
     }
@@ -192,8 +194,22 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
   if (blockIdx.x == 0 && threadIdx.x == 0) W.leaf_count[(S.pass + 1u) & 1u] = 0;
   __syncthreads();
   const int wi = blockIdx.x * kSearchWarps + (threadIdx.x >> 5);
-  if (wi * rows_per_search_warp<Model>(S.mode, rows) >= W.n) return;
-  search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state, rows);
+  // node ids of this pass: extent + (level - depth0) n + row (read by every warp before the
+  // last block advances the extents)
+  const int base_b = T.counters[0], base_a = T.counters[VP_COUNTER_ACTIONS];
+  if (wi * rows_per_search_warp<Model>(S.mode, rows) < W.n)
+    search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state, rows, base_a, base_b);
+  if (S.mode == VP_SEARCH_TRAJECTORY) return;  // creates no nodes
+  // the last warp to finish advances the extents (every warp has used its base by then)
+  __syncwarp();
+  if (lane_id() == 0) {
+    if (atomicAdd(&T.counters[VP_COUNTER_DONE], 1) == (int)(gridDim.x * kSearchWarps) - 1) {
+      const long long span = (long long)W.n * (S.d_max - S.depth0);
+      T.counters[0] = (int)min((long long)base_b + span, (long long)INT_MAX);
+      T.counters[VP_COUNTER_ACTIONS] = (int)min((long long)base_a + span, (long long)INT_MAX);
+      T.counters[VP_COUNTER_DONE] = 0;
+    }
+  }
 }
 
 template <class PsiT, bool Exact>
@@ -210,8 +226,10 @@ __global__ void k_root_argmax(vp_tree T, int* out) {
   warp_root_argmax<PsiT>(T, out);
 }
 
+// (live beliefs, live actions, overflow) after the chosen action
 __global__ void k_copy_counters(vp_tree T, int* out) {
-  if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[threadIdx.x == 1 ? VP_COUNTER_ACTIONS : threadIdx.x];
+  const int idx[3] = {VP_COUNTER_LIVE_B, VP_COUNTER_LIVE_A, 2};
+  if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[idx[threadIdx.x]];
 }
 
 // ================================================================== host side
@@ -954,8 +972,8 @@ int32_t vp_tree_rehash(const vp_tree* t, void* stream) {
 int32_t vp_tree_counts(const vp_tree* t, int32_t* host_out, void* stream) {
   if (!t || !host_out) return VP_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  const int idx[3] = {0, VP_COUNTER_ACTIONS, 2};
-  for (int k = 0; k < 3; ++k)
+  const int idx[5] = {VP_COUNTER_LIVE_B, VP_COUNTER_LIVE_A, 2, 0, VP_COUNTER_ACTIONS};
+  for (int k = 0; k < 5; ++k)
     if (cudaMemcpyAsync(host_out + k, t->counters + idx[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
         cudaSuccess)
       return VP_ERR_CUDA;
@@ -1118,6 +1136,7 @@ __global__ void k_append_actions(vp_tree T, const int32_t* beliefs, const int32_
   int x;
   if (cl.won) {
     x = atomicAdd(&T.counters[VP_COUNTER_ACTIONS], 1);
+    red_add(&T.counters[VP_COUNTER_LIVE_A], 1);
     if (x < T.cap_actions) {
       T.a_parent_belief[x] = b;
       T.a_action[x] = a;
@@ -1158,6 +1177,7 @@ __global__ void k_append_beliefs(vp_tree T, const int32_t* anodes, const uint32_
   int c;
   if (cl.won) {
     c = atomicAdd(&T.counters[0], 1);
+    red_add(&T.counters[VP_COUNTER_LIVE_B], 1);
     if (c < T.cap_beliefs) {
       const int pb = T.a_parent_belief[x];
       T.b_parent_action[c] = x;

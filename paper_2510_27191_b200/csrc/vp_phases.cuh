@@ -57,6 +57,23 @@ __device__ __forceinline__ ClaimTry claim_try(Slot* tab, u64 mask, u64 key, bool
   if (go) cas128(&tab[t.h], kEmptyKey, ~0ull, key, ~0ull, t.old_key, t.old_word);
   return t;
 }
+// Claims that insert the creator's id with the key ({key, pass << 32 | id} in the CAS): the id
+// is known before the claim (static per-row numbering), so a slot is never unpublished and a
+// hit returns the node in the same round trip.
+__device__ __forceinline__ ClaimTry claim_try_id(Slot* tab, u64 mask, u64 key, u64 word, bool go) {
+  ClaimTry t{slot_hash(key) & mask, kEmptyKey, ~0ull};
+  if (go) cas128(&tab[t.h], kEmptyKey, ~0ull, key, word, t.old_key, t.old_word);
+  return t;
+}
+__device__ __forceinline__ Claim claim_finish_id(Slot* tab, u64 mask, u64 key, u64 word, ClaimTry t) {
+  u64 h = t.h, old_key = t.old_key, old_word = t.old_word;
+  while (true) {
+    if (old_key == kEmptyKey) return Claim{(u32)h, true, word};
+    if (old_key == key) return Claim{(u32)h, false, old_word};
+    h = (h + 1) & mask;
+    cas128(&tab[h], kEmptyKey, ~0ull, key, word, old_key, old_word);
+  }
+}
 __device__ __forceinline__ Claim claim_finish(Slot* tab, u64 mask, u64 key, ClaimTry t) {
   u64 h = t.h, old_key = t.old_key, old_word = t.old_word;
   while (true) {
@@ -658,6 +675,9 @@ __device__ void block_tree_init(const vp_tree& T) {
       }
       T.counters[0] = 1;
       T.counters[VP_COUNTER_ACTIONS] = 0;
+      T.counters[VP_COUNTER_LIVE_B] = 1;
+      T.counters[VP_COUNTER_LIVE_A] = 0;
+      T.counters[VP_COUNTER_DONE] = 0;
       T.counters[2] = 0;
       T.counters[3] = 0;
     }
@@ -949,7 +969,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
 template <class Model, class PsiT, bool Exact>
 __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                             Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index,
-                            typename Model::State* shared_state, int rows) {
+                            typename Model::State* shared_state, int rows, int base_a, int base_b) {
   typedef typename Model::State State;
   constexpr bool kCoop = coop_trait<Model>::value;
   const int kRows = rows_per_search_warp<Model>(S.mode, rows);
@@ -1035,6 +1055,10 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
 
   bool made_interior = false;  // this lane created b at the previous level and it is interior now
   int pend = -1, pend_b = 0;   // CDF cache slot (and belief) this lane wrote, tag pending
+  // fast mode: the action this lane created at the previous level (its overlay slot is stored
+  // one level later) and a belief owed a dense row (written after the levels)
+  int pend_x = -1, pend_k = 0, pend_bel = -1, pend_mat = -1, pend_mat_prev = -1;
+  int won_a = 0, won_b = 0;    // nodes this lane created (live counts, one reduction per warp)
   for (int l = depth0; l < d; ++l) {
     const u64 lkey = fold(skey, (u64)l);  // search.py:107
     // ---- parity mode, lazy rows: b is interior at this level; write its PSI row once
@@ -1061,54 +1085,69 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     }
 
     // ---- action node (b, a) and belief node: append_actions / append_beliefs (tree.py:180-256)
-    // With (belief, action, obs) belief keys (bkey_mode 1) the belief claim does not wait for
-    // the action's row: the first CAS of both claims and both id atomics go out together.
+    // Ids are static: row r creating at this level takes extent + (l - depth0) n + r in each
+    // table, so a claim is ONE 128-bit CAS that inserts {key, pass | id} -- no id atomic, no
+    // publication, no spinning on another row's claim.  With (belief, action, obs) belief keys
+    // (bkey_mode 1) the two claims of a level are in flight together.
     const bool early = T.bkey_mode != 0;
     const bool interior_next = l + 1 < d;
+    const long long id_off = (long long)(l - depth0) * n + r;
+    const long long my_a = (long long)base_a + id_off, my_b = (long long)base_b + id_off;
     const u64 key_a = ((u64)(u32)b << 32) | (u32)a;
     const u32 grp_a = __match_any_sync(FULL, ok ? key_a : kEmptyKey);
     const int leader_a = __ffs(grp_a) - 1;
-    const bool lead_a = ok && lane == leader_a;
+    bool lead_a = ok && lane == leader_a;
     u64 key_b = early ? belief_key(T, b, a, 0, o) : 0ull;
     u32 grp_b = early ? __match_any_sync(FULL, ok ? key_b : kEmptyKey) : 0u;
     int leader_b = early ? __ffs(grp_b) - 1 : 0;
     bool lead_b = early && ok && lane == leader_b;
+    if ((lead_a && my_a >= T.cap_actions) || (lead_b && my_b >= T.cap_beliefs)) {
+      T.counters[2] = 1;  // overflow: the host fails the plan loudly
+      lead_a = lead_b = false;
+    }
+    const u64 word_a = ((u64)pass << 32) | (u64)(u32)my_a, word_b = ((u64)pass << 32) | (u64)(u32)my_b;
     Claim cl_a{0, false, 0}, cl_b{0, false, 0};
     {
-      ClaimTry ta = claim_try(ha, T.hmask_a, key_a, lead_a);
-      ClaimTry tb = claim_try(hb, T.hmask_b, key_b, lead_b);  // in flight together with ta
-      if (lead_a) cl_a = claim_finish(ha, T.hmask_a, key_a, ta);
-      if (lead_b) cl_b = claim_finish(hb, T.hmask_b, key_b, tb);
+      ClaimTry ta = claim_try_id(ha, T.hmask_a, key_a, word_a, lead_a);
+      ClaimTry tb = claim_try_id(hb, T.hmask_b, key_b, word_b, lead_b);  // in flight together with ta
+      if (lead_a) cl_a = claim_finish_id(ha, T.hmask_a, key_a, word_a, ta);
+      if (lead_b) cl_b = claim_finish_id(hb, T.hmask_b, key_b, word_b, tb);
     }
-    int id_a = 0, id_b = 0;
-    warp_alloc2(&T.counters[VP_COUNTER_ACTIONS], cl_a.won, &T.counters[0], early && cl_b.won, id_a, id_b);
+    // deferred from the previous level: the overlay slot of the action this lane created there
+    // (its atomic has had a whole level to return)
+    if (pend_x >= 0) {
+      T.a_slot[pend_x] = pend_k;
+      if (!Exact && pend_k == kOverlay && pend_bel >= 0) pend_mat = pend_bel;  // dense row: after the levels
+      pend_x = -1;
+    }
+    if (pend_mat >= 0 && pend_mat_prev >= 0) {  // a second one before the end: write the first now
+      materialise_dense<PsiT>(T, W.stats, pend_mat_prev, load_rec<PsiT>(T, pend_mat_prev), init_row, pass);
+      pend_mat_prev = -1;
+    }
+    if (pend_mat >= 0) {
+      pend_mat_prev = pend_mat;
+      pend_mat = -1;
+    }
     int x = 0;
-    int kslot = 0;  // the new action's child index under b (overlay slot); consumed after the belief claim
-    if (cl_a.won) {
-      x = id_a;
-      if (x < T.cap_actions) {
-        // accumulators are zero (cleared at tree reset); the key is a min-reduction
-        T.a_parent_belief[x] = b;
-        T.a_action[x] = a;
-        red_min(&T.a_ckey[x], creation_key(pass, l, rg));
-        kslot = atomicAdd(&T.b_nact[b], 1);
-      } else {
-        T.counters[2] = 1;  // overflow: the host fails the plan loudly
-      }
-      publish(ha, cl_a.slot, (u32)x, pass);
-    }
-    __syncwarp();  // every creator of the warp has published before any lane spins
-    if (lead_a && !cl_a.won) {
-      const u64 w = wait_published(ha, cl_a.slot, cl_a.word);
+    if (lead_a) {
+      const u64 w = wait_published(ha, cl_a.slot, cl_a.word);  // (append kernels publish late)
       x = (int)(u32)w;
-      if ((u32)(w >> 32) == pass && x < T.cap_actions) red_min(&T.a_ckey[x], creation_key(pass, l, rg));
+      if ((u32)(w >> 32) == pass) red_min(&T.a_ckey[x], creation_key(pass, l, rg));
+    }
+    if (cl_a.won) {
+      // accumulators are zero (cleared at tree reset); the key is a min-reduction (above)
+      T.a_parent_belief[x] = b;
+      T.a_action[x] = a;
+      pend_x = x;
+      pend_bel = rec.dense_pass == 0 ? b : -1;
+      if constexpr (!Exact) pend_k = atomicAdd(&T.b_nact[b], 1);  // consumed next level
+      ++won_a;
     }
     x = __shfl_sync(FULL, x, leader_a);
     if (W.stats) {
       const u32 wn = __ballot_sync(FULL, cl_a.won);
       if (lane == 0 && wn) atomicAdd(&W.stats[5], (unsigned long long)__popc(wn));
     }
-    ok = ok && x < T.cap_actions;
     // rewards and visits (tree.py:216-217); rows through x for the backup
     {
       const double sum = group_sum(rw, grp_a, ok);
@@ -1119,13 +1158,18 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         red_add(&T.a_rows[x], cnt);
       }
     }
+    const bool led_a = __shfl_sync(FULL, (int)lead_a, leader_a) != 0;  // (every lane shuffles)
+    ok = ok && led_a;
     if (!early) {  // (action row, obs) keys: the belief claim needs x
       key_b = belief_key(T, b, a, x, o);
       grp_b = __match_any_sync(FULL, ok ? key_b : kEmptyKey);
       leader_b = __ffs(grp_b) - 1;
       lead_b = ok && lane == leader_b;
-      if (lead_b) cl_b = claim_key(hb, T.hmask_b, key_b);
-      id_b = warp_alloc(&T.counters[0], cl_b.won);
+      if (lead_b && my_b >= T.cap_beliefs) {
+        T.counters[2] = 1;
+        lead_b = false;
+      }
+      if (lead_b) cl_b = claim_finish_id(hb, T.hmask_b, key_b, word_b, claim_try_id(hb, T.hmask_b, key_b, word_b, true));
     }
     grp = grp_b;
     lead = lead_b;
@@ -1133,46 +1177,33 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     bool c_new = false;
     {
       u32 cpass = 0;
-      if (cl_b.won) {
-        c = id_b;
-        cpass = pass;
-        if (c < T.cap_beliefs) {
-          T.b_parent_action[c] = x;
-          T.b_parent_obs[c] = o;
-          T.b_parent_belief[c] = b;
-          T.b_parent_act[c] = a;
-          T.b_depth[c] = l + 1;
-          T.b_lse[c] = T.init_lse[0];
-          // fresh (PSI == init); an interior node's row is written by its creator next level
-          T.b_flags[c] = interior_next ? 1u : 3u;
-          red_min(&T.b_ckey[c], creation_key(pass, l, rg));
-        } else {
-          T.counters[2] = 1;
-        }
-        publish(hb, cl_b.slot, (u32)c, pass);
-      }
-      __syncwarp();
-      if (lead_b && !cl_b.won) {
+      if (lead_b) {
         const u64 w = wait_published(hb, cl_b.slot, cl_b.word);
         c = (int)(u32)w;
         cpass = (u32)(w >> 32);
-        if (cpass == pass && c < T.cap_beliefs) red_min(&T.b_ckey[c], creation_key(pass, l, rg));
+        if (cpass == pass) red_min(&T.b_ckey[c], creation_key(pass, l, rg));
+      }
+      if (cl_b.won) {
+        T.b_parent_action[c] = x;
+        T.b_parent_obs[c] = o;
+        T.b_parent_belief[c] = b;
+        T.b_parent_act[c] = a;
+        T.b_depth[c] = l + 1;
+        T.b_lse[c] = lse_init;
+        // fresh (PSI == init); an interior node's row is written by its creator next level
+        T.b_flags[c] = interior_next ? 1u : 3u;
+        ++won_b;
       }
       c = __shfl_sync(FULL, c, leader_b);
       c_new = __shfl_sync(FULL, cpass, leader_b) == pass;
-      made_interior = cl_b.won && interior_next && c < T.cap_beliefs;
+      made_interior = cl_b.won && interior_next;
       if (W.stats) {
         const u32 wn = __ballot_sync(FULL, cl_b.won);
         if (lane == 0 && wn) atomicAdd(&W.stats[6], (unsigned long long)__popc(wn));
       }
     }
-    ok = ok && c < T.cap_beliefs;
-    if (cl_a.won && x < T.cap_actions) {
-      T.a_slot[x] = kslot;
-      // fast mode: the (kOverlay + 1)-th child of b gives b a dense row
-      if constexpr (!Exact)
-        if (kslot == kOverlay && rec.dense_pass == 0) materialise_dense<PsiT>(T, W.stats, b, rec, init_row, pass);
-    }
+    const bool led_b = __shfl_sync(FULL, (int)lead_b, leader_b) != 0;
+    ok = ok && led_b;
     arrive(T, W, leaf_count, c, grp, lead && ok, !interior_next);
     if (active && W.trace_action) {
       const size_t t = (size_t)l * n + r;
@@ -1192,6 +1223,21 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         lse = T.b_lse[c];
       }
     }
+  }
+
+  if (pend_x >= 0) {
+    T.a_slot[pend_x] = pend_k;
+    if (!Exact && pend_k == kOverlay && pend_bel >= 0) pend_mat = pend_bel;
+  }
+  if constexpr (!Exact) {
+    if (pend_mat_prev >= 0) materialise_dense<PsiT>(T, W.stats, pend_mat_prev, load_rec<PsiT>(T, pend_mat_prev), init_row, pass);
+    if (pend_mat >= 0) materialise_dense<PsiT>(T, W.stats, pend_mat, load_rec<PsiT>(T, pend_mat), init_row, pass);
+  }
+  won_a = warp_sum(won_a);
+  won_b = warp_sum(won_b);
+  if (lane == 0) {
+    if (won_a) red_add(&T.counters[VP_COUNTER_LIVE_A], won_a);
+    if (won_b) red_add(&T.counters[VP_COUNTER_LIVE_B], won_b);
   }
 
   // ---- leaves: heuristic value (search.py:119), summed per leaf (backup.py:44-51)
@@ -1386,17 +1432,24 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
           // overlay row: eta LSE = log sum_a exp(eta psi_a) = the changed cells (delivered, log
           // space) (+) the slots untouched this pass (stable in this lane's record) (+) the
           // unrealised initial cells, (|A| - filled) exp(eta init)
-          double l = bsum;
+          // (one max shift, then a sum of at most kOverlay + 2 exponentials and one log)
+          double lk[kOverlay];
+          double m = bsum;
           int filled = __popc(bmask);
 #pragma unroll
-          for (int k = 0; k < kOverlay; ++k)
-            if (!((bmask >> k) & 1u) && prec.act[k]) {
-              l = log_add_exp(l, eta * (double)prec.val[k]);
-              ++filled;
-            }
-          if (T.action_count > filled)
-            l = log_add_exp(l, eta * (double)(PsiT)T.init_prefs[0] + log((double)(T.action_count - filled)));
-          V = l / eta;
+          for (int k = 0; k < kOverlay; ++k) {
+            const bool keep = !((bmask >> k) & 1u) && prec.act[k];
+            lk[k] = keep ? eta * (double)prec.val[k] : -INFINITY;
+            m = fmax(m, lk[k]);
+            filled += keep;
+          }
+          const double li = eta * (double)(PsiT)T.init_prefs[0];
+          const int rest = T.action_count - filled;
+          if (rest > 0) m = fmax(m, li);
+          double sum = exp(bsum - m) + (rest > 0 ? (double)rest * exp(li - m) : 0.0);
+#pragma unroll
+          for (int k = 0; k < kOverlay; ++k) sum += exp(lk[k] - m);
+          V = (m + log(sum)) / eta;
           full = false;
         } else if (fresh && prow >= 0) {
           // dense row: 1 + sum_changed (new - old); well conditioned unless the changed cells

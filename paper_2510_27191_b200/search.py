@@ -164,7 +164,7 @@ def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inje
     if work is None or not work.fits(n, levels, dm.state_bytes, trace):
         work = Workspace(n, levels, dm.state_bytes, trace)
         tree._api_work = work
-    nb, na, _ = tree.counts()
+    nb, na = tree.extent()
     grow = n * (d_max - batch.depth)
     tree.ensure_capacity(nb + grow, na + grow)
     rec = dm.pack(batch.states)
@@ -212,7 +212,7 @@ def search_recorded(tree, model, actions, observations, rewards, leaf_values) ->
     if work is None or not work.fits(n, d, dm.state_bytes, False):
         work = Workspace(n, d, dm.state_bytes, False)
         tree._api_work = work
-    nb, na, _ = tree.counts()
+    nb, na = tree.extent()
     tree.ensure_capacity(nb + n * d, na + n * d)
     dev = {k: torch.from_numpy(v.reshape(-1)).cuda() for k, v in
            (("a", act), ("o", obs.astype(np.uint32).view(np.int32)), ("r", rew), ("h", leaf))}

@@ -191,7 +191,7 @@ class ShardedPlanner(Planner):
         for (_, e0), (name, e1) in zip(ev, ev[1:]):
             if name != "start":
                 self.phase_ms[name] = self.phase_ms.get(name, 0.0) + e0.elapsed_time(e1)
-        nb, na, overflow = (int(v) for v in tree._host_counts)
+        nb, na, overflow = (int(v) for v in tree._host_counts[:3])
         if overflow:
             raise _lib.CapacityError("device tree overflowed its arena during plan()")
         held = tree if keep_tree else TreeHandle(tree)

@@ -304,7 +304,7 @@ class Planner:
         while True:
             it_key = fold(key, done)
             if ub_b + n * d_max > tree.cap_beliefs or ub_a + n * d_max > tree.cap_actions:
-                nb, na, _ = tree.counts()
+                nb, na = tree.extent()
                 ub_b, ub_a = nb, na
                 need_b, need_a = nb + n * d_max, na + n * d_max
                 if done and (need_b > tree.cap_beliefs or need_a > tree.cap_actions):
@@ -349,7 +349,7 @@ class Planner:
         _lib.call("vp_root_argmax", C.byref(tree.struct), self._out.data_ptr(), stream)
         _lib.call("vp_tree_counts", C.byref(tree.struct), tree._host_counts, stream)  # syncs once
         chosen = int(self._out.item())
-        nb, na, overflow = (int(v) for v in tree._host_counts)
+        nb, na, overflow = (int(v) for v in tree._host_counts[:3])
         if overflow:
             raise _lib.CapacityError("device tree overflowed its arena during plan()")
         held = tree if keep_tree else TreeHandle(tree)

@@ -88,7 +88,7 @@ class DeviceTree:
         per16 = 4 if precision == "fp32" else 2
         self.psi_stride = (action_count + per16 - 1) // per16 * per16
         self._init_cdf = torch.zeros(action_count, dtype=self._psi_dtype, device="cuda")
-        self._host_counts = (C.c_int32 * 3)()
+        self._host_counts = (C.c_int32 * 5)()  # live b, live a, overflow, id extents
         self.cap_beliefs = 0
         self.cap_actions = 0
         self.overlay_slots = 0 if self.exact else _lib.VP_OVERLAY_SLOTS
@@ -222,11 +222,18 @@ class DeviceTree:
         _lib.call("vp_tree_counts", C.byref(self.struct), self._host_counts, _stream())
         return int(self._host_counts[0]), int(self._host_counts[1]), int(self._host_counts[2])
 
+    def extent(self):
+        """(belief, action) id extents: the device columns in use.  A search numbers nodes
+        statically (row r creating at level l takes extent + l n + r), so ids below the
+        extents that no node took are holes (creation key ~0)."""
+        self.counts()
+        return int(self._host_counts[3]), int(self._host_counts[4])
+
     def ensure_capacity(self, need_beliefs: int, need_actions: int):
         """Grow (geometric, tree.py:90-97) so the next search cannot overflow."""
         if need_beliefs <= self.cap_beliefs and need_actions <= self.cap_actions:
             return False
-        nb, na, _ = self.counts()
+        nb, na = self.extent()
         cap_b = max(self.cap_beliefs, 16)
         while cap_b < need_beliefs:
             cap_b *= 2
@@ -240,7 +247,7 @@ class DeviceTree:
     def n_dense(self) -> int:
         """PSI rows in use (parity mode: the belief count)."""
         if self.exact:
-            return self.counts()[0]
+            return self.extent()[0]
         return int(self._counters[_lib.VP_COUNTER_DENSE].item())
 
     def next_pass(self) -> int:
@@ -253,7 +260,7 @@ class DeviceTree:
         """Zero the per-pass counters after a search that was never backed up."""
         if not self._scratch_dirty:
             return
-        nb, na, _ = self.counts()
+        nb, na = self.extent()
         for t in (self.b_rows, self.b_value, self.b_acc):
             t[:nb].zero_()
         for t in (self.a_rows, self.a_acc):
@@ -264,14 +271,16 @@ class DeviceTree:
         """(b_order, b_rank, a_order, a_rank) device tensors: ``order[k]`` is the
         device row of reference id k, ``rank[row]`` its reference id."""
         nb, na, _ = self.counts()
-        key = (self.generation, self.pass_cursor, nb, na)
+        hb, ha = int(self._host_counts[3]), int(self._host_counts[4])
+        key = (self.generation, self.pass_cursor, nb, na, hb, ha)
         if self._canon_cache is not None and self._canon_cache[0] == key:
             return self._canon_cache[1]
         torch = _torch()
         out = []
-        for ck, cnt in ((self.b_ckey, nb), (self.a_ckey, na)):
-            order = torch.argsort(ck[:cnt], stable=True).to(torch.int64)
-            rank = torch.empty_like(order)
+        for ck, cnt, ext in ((self.b_ckey, nb, hb), (self.a_ckey, na, ha)):
+            # holes keep ckey ~0 (-1 as int64) and sort first; live keys are >= 0
+            order = torch.argsort(ck[:ext], stable=True).to(torch.int64)[ext - cnt:]
+            rank = torch.full((ext,), -1, device=order.device, dtype=torch.int64)
             rank[order] = torch.arange(cnt, device=order.device, dtype=torch.int64)
             out += [order, rank]
         self._canon_cache = (key, tuple(out))
@@ -425,6 +434,7 @@ class DeviceTree:
             tree.a_visits[:na] = dev([r[4] for r in a_rows], torch.int32)
             tree.a_ckey[:na] = torch.arange(na, device="cuda", dtype=torch.int64)
         tree._counters[0], tree._counters[_lib.VP_COUNTER_ACTIONS], tree._counters[2] = nb, na, 0
+        tree._counters[_lib.VP_COUNTER_LIVE_B], tree._counters[_lib.VP_COUNTER_LIVE_A] = nb, na
         _lib.call("vp_tree_rehash", C.byref(tree.struct), _stream())
         tree.pass_cursor = 1
         tree._canon_cache = None
@@ -455,22 +465,23 @@ class DeviceTree:
         torch = _torch()
         nb, na, _ = self.counts()
         border, brank, aorder, arank = self.canonical()
-        pa = self.b_parent_action[:nb].to(torch.int64)[border]
+        hb, ha = int(self._host_counts[3]), int(self._host_counts[4])  # (canonical() refreshed them)
+        pa = self.b_parent_action[:hb].to(torch.int64)[border]
         pa = torch.where(pa >= 0, arank[pa.clamp(min=0)], pa)
-        obs = self.b_parent_obs[:nb][border].cpu().numpy().view(np.uint32).astype(np.int64)
+        obs = self.b_parent_obs[:hb][border].cpu().numpy().view(np.uint32).astype(np.int64)
         if nb:
             obs[0] = ROOT_SENTINEL
-        prefs = self._prefs_rows(nb)[border].cpu().numpy().astype(np.float64)
-        apb = brank[self.a_parent_belief[:na].to(torch.int64)[aorder]] if na else torch.zeros(0, dtype=torch.int64)
+        prefs = self._prefs_rows(hb)[border].cpu().numpy().astype(np.float64)
+        apb = brank[self.a_parent_belief[:ha].to(torch.int64)[aorder]] if na else torch.zeros(0, dtype=torch.int64)
         return {
             "parent_action": pa.cpu().numpy(),
             "parent_obs": obs,
-            "depth": self.b_depth[:nb][border].cpu().numpy().astype(np.int64),
+            "depth": self.b_depth[:hb][border].cpu().numpy().astype(np.int64),
             "prefs": prefs,
             "action_parent_belief": apb.cpu().numpy().astype(np.int64),
-            "action_id": self.a_action[:na][aorder].cpu().numpy().astype(np.int64),
-            "action_reward_sum": self.a_reward[:na][aorder].cpu().numpy().copy(),
-            "action_visits": self.a_visits[:na][aorder].cpu().numpy().astype(np.int64),
+            "action_id": self.a_action[:ha][aorder].cpu().numpy().astype(np.int64),
+            "action_reward_sum": self.a_reward[:ha][aorder].cpu().numpy().copy(),
+            "action_visits": self.a_visits[:ha][aorder].cpu().numpy().astype(np.int64),
         }
 
 
