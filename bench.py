@@ -452,7 +452,7 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
                        "24 L + (56 + rec + 2 psi_b) P + 76 U + psi_b|A| F per pass (bench.algorithmic_bytes)")
     names = ["interior_beliefs", "actions_visited", "psi_rows_staged", "search_launches", "row_levels",
              "new_actions", "new_beliefs", "leaves", "full_row_lse_reads", "overlay_draws", "dense_rows_made",
-             "dense_cdfs_built"]
+             "dense_cdfs_built", "overlay_lse_fallbacks"]
     res.update({
         "roofline": {"search": roof_search, "backup": roof_backup}.get(top) or roof_search,
         "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},

@@ -160,12 +160,12 @@ typedef struct vp_tree {
   const double* init_prefs;   /* [|A|] initial PSI row                      */
   double* init_lse;           /* [1] LSE of the initial row (set by init)   */
   void* init_cdf;             /* [|A|] CDF of softmax(eta init) (PSI dtype) */
-  void* cdf_cache;            /* [cdf_slots * psi_stride] normalised softmax CDFs of non-lazy rows,
-                                 direct-mapped by belief id, built once per pass by the first
-                                 warp that samples the row */
-  uint64_t* cdf_tag;          /* [cdf_slots] pass << 32 | belief of the slot's CDF (bit 31 of the
-                                 low word: being written); cleared at tree reset */
-  int32_t cdf_slots;          /* power of two                                */
+  void* psi_cdf;              /* [cap_dense * psi_stride] normalised softmax CDF of each dense PSI row
+                                 (fast mode), rebuilt by the backup whenever it completes the row's
+                                 belief: the search reads it with one TMA copy per distinct row */
+  void* dense_meta;           /* [cap_dense] {double lse, uint32 pass, pad}: a backup that changes a
+                                 dense row stamps it with its pass and the row's new LSE; the CDF
+                                 kernel after the backup rebuilds the stamped rows' CDFs */
   int32_t bkey_mode;          /* belief-index key: 0 = (action row << 32 | obs); 1 = (belief << 32 |
                                  action << 20 | obs), needs |A| <= 4096 and obs < 2^20 -- both
                                  claims of a level can then be issued together */
@@ -191,8 +191,9 @@ typedef struct vp_work {
                                  4 row-levels sampled, 5 new actions, 6 new beliefs,
                                  7 leaves, 8 interior beliefs whose LSE needed a full
                                  row read, 9 overlay draws (rows drawn from a belief's
-                                 inline cells), 10 dense rows materialised, 11 CDFs built
-                                 into the per-pass cache (distinct dense rows sampled) */
+                                 inline cells), 10 dense rows materialised, 11 dense rows
+                                 whose CDF a backup rebuilt, 12 overlay records whose LSE
+                                 needed the closed-form fallback */
   /* optional per-level traces (level-major, n each; device ids); NULL = off */
   int32_t* trace_action;
   uint32_t* trace_obs;
@@ -286,6 +287,9 @@ int32_t vp_tree_init(const vp_tree* tree, void* stream);
 /* tree->eta changed on a live tree (search.py:86 / backup.py:75 take eta per call): recompute the
  * initial row's LSE and CDF and every live row's cached LSE. */
 int32_t vp_tree_set_eta(const vp_tree* tree, void* stream);
+/* Rebuild the CDF row of every dense PSI row from its cached LSE (fast mode; after
+ * host-level edits -- append_actions, deserialize -- that create dense rows outside a pass). */
+int32_t vp_tree_build_cdfs(const vp_tree* tree, void* stream);
 /* Rebuild both hash indexes from the node columns (after capacity growth). */
 int32_t vp_tree_rehash(const vp_tree* tree, void* stream);
 /* Copy (n_beliefs, n_actions, overflow, belief id extent, action id extent) to host

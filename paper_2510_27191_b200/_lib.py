@@ -72,7 +72,7 @@ class VpTree(C.Structure):
         ("a_slot", C.c_void_p),
         ("hash_a", C.c_void_p), ("hash_b", C.c_void_p), ("counters", C.c_void_p),
         ("init_prefs", C.c_void_p), ("init_lse", C.c_void_p), ("init_cdf", C.c_void_p),
-        ("cdf_cache", C.c_void_p), ("cdf_tag", C.c_void_p), ("cdf_slots", C.c_int32), ("bkey_mode", C.c_int32),
+        ("psi_cdf", C.c_void_p), ("dense_meta", C.c_void_p), ("bkey_mode", C.c_int32),
         ("cap_dense", C.c_int32), ("overlay_slots", C.c_int32), ("init_uniform", C.c_int32), ("eta", C.c_double),
     ]
 
@@ -121,6 +121,7 @@ _SIGNATURES = [
     ("vp_launch_count", C.c_int64, []),
     ("vp_tree_init", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_rehash", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
+    ("vp_tree_build_cdfs", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_tree_set_eta", C.c_int32, [C.POINTER(VpTree), C.c_void_p]),
     ("vp_probe_latency", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
     ("vp_tree_counts", C.c_int32, [C.POINTER(VpTree), p_i32, C.c_void_p]),
@@ -219,13 +220,13 @@ def layout_mismatches() -> list:
             VpModel.tab_states.offset, VpModel.ld_bins.offset, VpTree.eta.offset,
             VpWork.trace_belief.offset, VpSearchArgs.start_beliefs.offset, 16, C.sizeof(VpPlanArgs),
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
-            VpModel.mars_gpow.offset, VpTree.cdf_tag.offset, VpModel.nav_log_miss.offset,
+            VpModel.mars_gpow.offset, VpTree.psi_cdf.offset, VpModel.nav_log_miss.offset,
             VpModel.crowd_heur.offset, CROWD_STATE_BYTES, VpTree.b_rec.offset, VpTree.a_slot.offset,
             VpTree.cap_dense.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
-             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.cdf_tag", "vp_model.nav_log_miss",
+             "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.psi_cdf", "vp_model.nav_log_miss",
              "vp_model.crowd_heur", "sizeof(CrowdState)", "vp_tree.b_rec", "vp_tree.a_slot", "vp_tree.cap_dense"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 

@@ -39,7 +39,8 @@ __global__ void k_tree_init(vp_tree T) {
 // in that state since allocation).  Part 2 (k_tree_init) rewrites the root.
 __global__ void k_clear(vp_tree T) {
   const int nb = min(T.counters[0], T.cap_beliefs), na = min(T.counters[VP_COUNTER_ACTIONS], T.cap_actions);
-  const int total = max(max(nb, na), T.cdf_slots);
+  const int nd = T.exact ? 0 : min(T.counters[VP_COUNTER_DENSE], T.cap_dense);
+  const int total = max(max(nb, na), nd);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i < nb) {
       T.b_value[i] = 0.0;
@@ -51,7 +52,7 @@ __global__ void k_clear(vp_tree T) {
       uint4* rec = reinterpret_cast<uint4*>(T.b_rec) + (size_t)i * words;
       for (int w = 0; w < words; ++w) rec[w] = make_uint4(0u, 0u, 0u, 0u);
     }
-    if (i < T.cdf_slots) T.cdf_tag[i] = 0;  // cached CDFs of the previous tree
+    if (i < nd) reinterpret_cast<uint4*>(T.dense_meta)[i] = make_uint4(0u, 0u, 0u, 0u);  // no CDF requests
     if (i < na) {
       T.a_reward[i] = 0.0;
       T.a_visits[i] = 0;
@@ -114,6 +115,22 @@ __global__ void k_eta_rows(vp_tree T) {
       v = row_lse_fast<PsiT>(psi + (size_t)b * T.psi_stride, T.action_count, T.eta);
     }
     if (lane_id() == 0) T.b_lse[b] = v;
+  }
+}
+
+// Fast mode: the CDF row of every dense PSI row from the belief's cached LSE (one warp per
+// belief) -- after host-level edits and eta changes; a pass keeps them current itself.
+template <class PsiT>
+__global__ void k_dense_cdfs(vp_tree T) {
+  const int nb = min(T.counters[0], T.cap_beliefs);
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+  PsiT* cdf = reinterpret_cast<PsiT*>(T.psi_cdf);
+  for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+    const int r = dense_row_of<PsiT>(T, b);
+    if (r >= 0)
+      build_cdf_row<PsiT, false>(psi + (size_t)r * T.psi_stride, cdf + (size_t)r * T.psi_stride, T.action_count,
+                                 T.eta, T.b_lse[b]);
   }
 }
 
@@ -219,6 +236,11 @@ __global__ void __launch_bounds__(kBackupWarps * 32) k_backup(vp_tree T, vp_work
   const int wi = blockIdx.x * kBackupWarps + warp;
   if (wi * rpw >= W.leaf_count[pass & 1u]) return;
   backup_warp<PsiT, Exact>(T, W, pass, gamma, wi, s_v[warp], rpw);
+}
+
+template <class PsiT>
+__global__ void __launch_bounds__(256) k_cdf_rows(vp_tree T, u32 pass) {
+  cdf_rows_warp<PsiT>(T, pass);
 }
 
 template <class PsiT>
@@ -449,6 +471,10 @@ static int32_t launch_backup(const vp_tree& T, const vp_work& W, u32 pass, doubl
   {
     Launch L_(KK_BACKUP, st);
     k_backup<PsiT, Exact><<<grid, kBackupWarps * 32, 0, st>>>(T, W, pass, gamma, rpw);
+  }
+  if constexpr (!Exact) {  // the CDFs of the dense rows this backup changed
+    Launch L_(KK_BACKUP, st);
+    k_cdf_rows<PsiT><<<num_sms() * 4, 256, 0, st>>>(T, pass);
   }
   return check_launch();
 }
@@ -926,7 +952,7 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, a_ckey),
                        (int32_t)offsetof(vp_search_args, m),
                        (int32_t)offsetof(vp_model, mars_gpow),
-                       (int32_t)offsetof(vp_tree, cdf_tag),
+                       (int32_t)offsetof(vp_tree, psi_cdf),
                        (int32_t)offsetof(vp_model, nav_log_miss), (int32_t)offsetof(vp_model, crowd_heur),
                        (int32_t)sizeof(CrowdState), (int32_t)offsetof(vp_tree, b_rec),
                        (int32_t)offsetof(vp_tree, a_slot), (int32_t)offsetof(vp_tree, cap_dense)};
@@ -956,6 +982,18 @@ int32_t vp_tree_set_eta(const vp_tree* t, void* stream) {
     constexpr bool E = decltype(ex)::value;
     { Launch L_(KK_TREE_INIT, st); k_eta_init_row<PsiT, E><<<1, 32, 0, st>>>(T); }
     { Launch L_(KK_TREE_INIT, st); k_eta_rows<PsiT, E><<<num_sms() * 8, 256, 0, st>>>(T); }
+    if (!E) { Launch L_(KK_TREE_INIT, st); k_dense_cdfs<PsiT><<<num_sms() * 8, 256, 0, st>>>(T); }
+    return check_launch();
+  });
+}
+
+int32_t vp_tree_build_cdfs(const vp_tree* t, void* stream) {
+  if (!t || t->action_count < 1) return VP_ERR_INVALID;
+  if (t->exact) return VP_OK;  // parity mode samples its PSI rows directly
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_tree T = *t;
+  return dispatch_psi(T.psi_dtype, 0, [&](auto z, auto) -> int32_t {
+    { Launch L_(KK_TREE_INIT, st); k_dense_cdfs<decltype(z)><<<num_sms() * 8, 256, 0, st>>>(T); }
     return check_launch();
   });
 }
@@ -1244,6 +1282,16 @@ int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, cons
       keep_hi / 8);
   return check_launch();
 }
+
+#ifdef VP_PHASE_CLOCKS
+// measurement builds: read (and clear) the per-phase cycle sums of the search
+int32_t vp_debug_phases(unsigned long long* host_out) {
+  if (cudaMemcpyFromSymbol(host_out, vp::g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return VP_ERR_CUDA;
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(vp::g_phase_cycles, z, sizeof(z)) == cudaSuccess ? VP_OK : VP_ERR_CUDA;
+}
+#endif
 
 int32_t vp_probe_latency(const uint64_t* next, int32_t hops, int32_t atomic, uint64_t start, double* out,
                          void* stream) {

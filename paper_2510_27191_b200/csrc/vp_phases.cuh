@@ -30,6 +30,23 @@
 namespace vp {
 
 constexpr int kSearchWarps = 2;   // warps per search block
+
+// Measurement builds only (-DVP_PHASE_CLOCKS, scripts/phase_clocks.sh): SM cycles per search
+// phase summed over warps (lane 0), read back with vp_debug_phases.
+#ifdef VP_PHASE_CLOCKS
+__device__ unsigned long long g_phase_cycles[16];
+#define VP_PH_INIT() long long ph_t0 = clock64(); unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define VP_PH(k) { const long long t_ = clock64(); ph_acc[k] += (unsigned long long)(t_ - ph_t0); ph_t0 = t_; }
+#define VP_PH_FLUSH() if (lane_id() == 0) for (int k_ = 0; k_ < 8; ++k_) atomicAdd(&g_phase_cycles[k_], ph_acc[k_]);
+#define VP_DR_INIT() long long dr_t0 = clock64();
+#define VP_DR(k) { const long long t_ = clock64(); if (lane_id() == 0) atomicAdd(&g_phase_cycles[8 + k], (unsigned long long)(t_ - dr_t0)); dr_t0 = clock64(); }
+#else
+#define VP_DR_INIT()
+#define VP_DR(k)
+#define VP_PH_INIT()
+#define VP_PH(k)
+#define VP_PH_FLUSH()
+#endif
 constexpr int kBackupWarps = 8;   // warps per backup block
 
 __device__ __forceinline__ Slot* slots(void* p) { return reinterpret_cast<Slot*>(p); }
@@ -111,6 +128,20 @@ constexpr u32 kCasRows = 16;
 constexpr u32 kRowsMask = 0xFFFFFFu;
 constexpr u32 kSlotBit = 1u << 24;
 
+__device__ __forceinline__ void cas128_acq_rel(void* p, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64& old_lo,
+                                               u64& old_hi) {
+  asm volatile(
+      "{\n .reg .b128 c, n, d;\n mov.b128 c, {%2, %3};\n mov.b128 n, {%4, %5};\n"
+      " atom.acq_rel.gpu.global.cas.b128 d, [%6], c, n;\n mov.b128 {%0, %1}, d;\n}\n"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(p)
+      : "memory");
+}
+
+// `ordered`: the deliveries also publish the deliverer's earlier stores to the completing one
+// (a dense PSI cell its full-row fallback may read): the CAS path then runs acq_rel; the busy
+// path's row-count add is acq_rel anyway, and a lone delivery is its own completer.
+template <bool ordered = false>
 __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 drows, u32 dcnt, u32 target,
                                             Acc& out) {
   if ((drows & kRowsMask) == target) {
@@ -125,7 +156,8 @@ __device__ __forceinline__ bool acc_deliver(void* base, int i, double dsum, u32 
       const u32 r = (u32)hi + drows, c = (u32)(hi >> 32) + dcnt;
       const u64 nlo = (u64)__double_as_longlong(s), nhi = (u64)r | ((u64)c << 32);
       u64 olo, ohi;
-      cas128(p, lo, hi, nlo, nhi, olo, ohi);
+      if (ordered) cas128_acq_rel(p, lo, hi, nlo, nhi, olo, ohi);
+      else cas128(p, lo, hi, nlo, nhi, olo, ohi);
       if (olo == lo && ohi == hi) {
         if ((r & kRowsMask) != target) return false;
         out = Acc{s, r, c};
@@ -177,6 +209,19 @@ __device__ __forceinline__ Rec<PsiT> load_rec(const vp_tree& T, int b) {
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(Rec<PsiT>) / 16); ++i) q[i] = L2 ? __ldcg(p + i) : p[i];
   return r;
+}
+// Per dense row: the LSE and pass of the backup that last changed it (CDF rebuild requests).
+struct __align__(16) DenseMeta {
+  double lse;
+  u32 pass;
+  u32 pad;
+};
+
+// The dense PSI row of belief b, or -1 while it keeps an overlay record (one 8-B load).
+template <class PsiT>
+__device__ __forceinline__ int dense_row_of(const vp_tree& T, int b) {
+  const uint2 w = *reinterpret_cast<const uint2*>(rec_ptr<PsiT>(T, b));
+  return w.x ? (int)w.y : -1;
 }
 template <class PsiT>
 __device__ __forceinline__ bool rec_any(const Rec<PsiT>& r) {
@@ -484,6 +529,29 @@ __device__ __forceinline__ PsiT row_cdf_inplace(PsiT* row, int A, PsiT e2, PsiT 
   return total;
 }
 
+// The normalised softmax CDF of a PSI row into global memory (search.py:46-54, 77-79):
+// p_a = exp(eta (psi_a - lse)), running sums divided by their total.  A full warp; lane j owns
+// the contiguous columns [j C, j C + C), C = ceil(|A| / 32), and the row is read twice (total,
+// then the stored sums), so any |A| fits without staging.  L2: the row was written by other
+// SMs inside this kernel.
+template <class PsiT, bool L2>
+__device__ void build_cdf_row(const PsiT* row, PsiT* cdf, int A, double eta, double lse) {
+  const PsiT e2 = (PsiT)(eta * kLog2eD), sh2 = (PsiT)(eta * lse * kLog2eD);
+  const int C = (A + 31) >> 5;
+  const int lo = lane_id() * C, hi = min(A, lo + C);
+  PsiT loc = 0;
+  for (int c = lo; c < hi; ++c) loc += fexp2(ffma(e2, ldp<L2>(row + c), -sh2));
+  const PsiT incl = warp_inclusive_scan(loc);
+  const PsiT up = __shfl_up_sync(FULL, incl, 1);
+  const PsiT excl = lane_id() ? up : (PsiT)0;
+  const PsiT scale = (PsiT)1 / __shfl_sync(FULL, incl, 31);
+  loc = 0;
+  for (int c = lo; c < hi; ++c) {
+    loc += fexp2(ffma(e2, ldp<L2>(row + c), -sh2));
+    cdf[c] = (loc + excl) * scale;
+  }
+}
+
 // ------------------------------------------------------------------ TMA bulk staging
 
 __device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -652,6 +720,8 @@ __device__ void block_tree_init(const vp_tree& T) {
     __syncwarp();
     const PsiT total = row_cdf_inplace(cdf, A, (PsiT)(T.eta * kLog2eD), (PsiT)(T.eta * v * kLog2eD));
     for (int a = threadIdx.x; a < A; a += 32) cdf[a] = cdf[a] / total;
+    if constexpr (!Exact)  // the root's dense row 0 is the initial row: its CDF row too
+      build_cdf_row<PsiT, false>(psi, reinterpret_cast<PsiT*>(T.psi_cdf), A, T.eta, v);
     if (threadIdx.x == 0) {
       T.init_lse[0] = v;
       T.b_lse[0] = v;
@@ -757,45 +827,29 @@ __device__ __forceinline__ void model_step(const vp_model& M, typename Model::St
 
 // ------------------------------------------------------------------ search
 
-// Softmax draw of one action per lane (search.py:46-83) from the PSI row of
-// belief b (or the initial row when flags bit 0 says it is lazily initial).
-// Called by all 32 lanes; lanes with ok == false return 0.
-// CDF cache tags: pass << 32 | belief; kCdfBuilding marks a slot being written.
-constexpr u64 kCdfBuilding = 0x80000000ull;
-__device__ __forceinline__ u64 cdf_tag(u32 pass, int b) { return ((u64)pass << 32) | (u32)b; }
-
-// Publish the CDF this lane bulk-stored into cache slot `pend` for belief
-// `pend_b`: once the store has completed, release the slot's tag.
-__device__ __forceinline__ void publish_pending_cdf(const vp_tree& T, int& pend, int pend_b, u32 pass) {
-  if (pend < 0) return;
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(T.cdf_tag + pend), "l"(cdf_tag(pass, pend_b)) : "memory");
-  pend = -1;
-}
-
+// Softmax draw of one action per lane (search.py:46-83) from the PSI row of belief b.  Called by
+// all 32 lanes; lanes with ok == false return 0.
+//  * parity mode: numpy-order inverse CDF of the row (the initial row while lazily initial);
+//  * fast mode: a belief with an overlay record draws from the shared initial CDF corrected by
+//    its realised cells; a belief with a dense row draws from that row's CDF, which the backup
+//    that last changed the row rebuilt (PSI is read-only during a pass): the warp's distinct
+//    dense beliefs get ONE TMA bulk copy each into the warp's stage, then every lane
+//    binary-searches its row.
 template <class PsiT, bool Exact>
 __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, Stage<PsiT>& sg, const PsiT* init_cdf,
                                            const PsiT* init_row, int b, u32 fl, const Rec<PsiT>& rec, double lse,
-                                           double lse_init, bool ok, double u, u32 pass, int& pend, int& pend_b) {
+                                           double lse_init, bool ok, double u, u32 pass) {
   const int A = T.action_count, lane = lane_id();
-  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
-  PsiT* cache = reinterpret_cast<PsiT*>(T.cdf_cache);
-  const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
-  const PsiT e2 = (PsiT)(T.eta * kLog2eD);
   int a = 0;
   if constexpr (Exact) {
     if (ok) {
-      const double* row = (fl & 1u) ? T.init_prefs : reinterpret_cast<const double*>(psi) + (size_t)b * T.psi_stride;
+      const double* row =
+          (fl & 1u) ? T.init_prefs : reinterpret_cast<const double*>(T.psi) + (size_t)b * T.psi_stride;
       a = sample_exact(row, A, T.eta, u);
     }
   } else {
-    // CDFs this lane built at the previous level: the bulk stores have long
-    // completed; make them visible and stamp them with the pass
-    publish_pending_cdf(T, pend, pend_b, pass);
-    // fast mode: a belief with a dense row written before this pass draws from that row
-    // (staged below); every other belief draws from its overlay record -- the initial CDF
-    // itself when no cell is realised yet
+    VP_DR_INIT();
+    // a dense row written before this pass (one written during it is used from the next pass)
     const bool need = ok && rec.dense_pass != 0 && rec.dense_pass < pass;
     const bool ovl = ok && !need && rec_any(rec);
     if (ok && !need)
@@ -805,12 +859,7 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
       const u32 om = __ballot_sync(FULL, ovl);
       if (lane == 0 && om) atomicAdd(&W.stats[9], (unsigned long long)__popc(om));
     }
-    // Distinct non-fresh beliefs of the warp: one TMA bulk copy of each row into the
-    // warp's stage -- the row's normalised CDF if some warp already built it this pass
-    // (the PSI row is read-only during a pass), else its PSI row, which the warp turns
-    // into the CDF in place (lane j owns a contiguous ceil(|A|/32)-column chunk, one
-    // shuffle scan, p = e / sum e, search.py:51-54) and publishes for the other warps.
-    // Every lane then binary-searches its row.
+    VP_DR(1);
     const u32 g = __match_any_sync(FULL, need ? (u32)b : 0xffffffffu);
     const int my_leader = __ffs(g) - 1;
     const bool lead = need && lane == my_leader;
@@ -818,58 +867,24 @@ __device__ __forceinline__ int draw_action(const vp_tree& T, const vp_work& W, S
     const int K = __popc(leaders);
     if (W.stats && lane == 0 && K) atomicAdd(&W.stats[2], (unsigned long long)K);
     const int my_slot = need ? __popc(leaders & ((1u << my_leader) - 1u)) : -1;
-    // direct-mapped cache slot of b: a hit when it holds b's CDF of this pass; otherwise the
-    // builder claims the slot (one writer per slot and pass) unless it holds this pass's CDF
-    // of another row
-    bool cached = false, claim = false;
-    const int cslot = b & (T.cdf_slots - 1);
-    if (lead) {
-      u64 tag;
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(tag) : "l"(T.cdf_tag + cslot) : "memory");
-      cached = tag == cdf_tag(pass, b);
-      if (!cached && (u32)(tag >> 32) != pass)
-        claim = atomicCAS(reinterpret_cast<unsigned long long*>(T.cdf_tag + cslot), tag,
-                          cdf_tag(pass, b) | kCdfBuilding) == tag;
-    }
-    const u32 cmask = __ballot_sync(FULL, cached);
-    if (W.stats) {  // CDFs built this pass: ~ the distinct dense rows sampled (compulsory reads)
-      const u32 bm = __ballot_sync(FULL, claim);
-      if (lane == 0 && bm) atomicAdd(&W.stats[11], (unsigned long long)__popc(bm));
-    }
-    if (cmask) asm volatile("fence.proxy.async.global;" ::: "memory");
-    const PsiT sh2 = lead && !cached ? (PsiT)(T.eta * lse * kLog2eD) : (PsiT)0;
+    const PsiT* cdf = reinterpret_cast<const PsiT*>(T.psi_cdf);
+    const u32 row_bytes = (u32)(((size_t)A * sizeof(PsiT) + 15) & ~(size_t)15);
     for (int s0 = 0; s0 < K; s0 += sg.cfg.rows) {
       const int cnt = min(sg.cfg.rows, K - s0);
-      fence_async_smem();
+      fence_async_smem();  // the stage's previous rows were read by the generic proxy
       if (lane == 0) mbar_expect_tx(sg.bar, row_bytes * (u32)cnt);
       __syncwarp();
       const bool mine = need && my_slot >= s0 && my_slot < s0 + cnt;
-      PsiT* srow = sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride;
+      const PsiT* srow = sg.buf + (size_t)(my_slot - s0) * sg.cfg.stride;
       if (mine && lane == my_leader)
-        bulk_g2s(srow, cached ? cache + (size_t)cslot * T.psi_stride : psi + (size_t)rec.dense_row * T.psi_stride,
-                 row_bytes, sg.bar);
+        bulk_g2s(const_cast<PsiT*>(srow), cdf + (size_t)rec.dense_row * T.psi_stride, row_bytes, sg.bar);
+      VP_DR(3);
       mbar_wait(sg.bar, sg.phase);
       sg.phase ^= 1u;
-      u32 rem = leaders;
-      for (int k = 0; k < s0; ++k) rem &= rem - 1u;
-      for (int k = 0; k < cnt; ++k) {
-        const int src = __ffs(rem) - 1;
-        rem &= rem - 1u;
-        if (!((cmask >> src) & 1u))
-          row_cdf_inplace<PsiT, true>(sg.buf + (size_t)k * sg.cfg.stride, A, e2, __shfl_sync(FULL, sh2, src));
-      }
-      if (claim && mine) {  // publish the normalised CDF: one bulk store from the stage
-        fence_async_smem();
-        bulk_s2g(cache + (size_t)cslot * T.psi_stride, srow, row_bytes);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        pend = cslot;
-        pend_b = b;
-      }
-      __syncwarp();
+      VP_DR(4);
       if (mine) a = search_cdf(srow, A, (PsiT)u);
-      // the stage is refilled next: the bulk stores must have read it
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
+      VP_DR(6);
     }
   }
   return a;
@@ -919,7 +934,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
   const int n = W.n;
   const Slot* ha = slots(T.hash_a);
   const Slot* hb = slots(T.hash_b);
-  int b = 0, pend = -1, pend_b = 0;
+  int b = 0;
   bool known = active;  // the row's belief existed when the pass started
   u32 fl = known ? T.b_flags[0] : 1u;
   Rec<PsiT> rec{};  // fast mode: the belief's overlay record (zero: initial row)
@@ -934,7 +949,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     const u64 lkey = fold(skey, (u64)l);
     const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
     const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, known ? fl : 1u, rec, lse, lse_init, active,
-                                           u, S.pass, pend, pend_b);
+                                           u, S.pass);
     u32 o = 0;
     double rw = 0.0;
     model_step<Model>(M, st, a, fold(lkey, 1), rg, active, o, rw);
@@ -962,7 +977,6 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
     }
   }
   if (active) W.leaf_value[r] = Model::heuristic(M, st);
-  publish_pending_cdf(T, pend, pend_b, S.pass);
 }
 
 // The search kernel body for one warp = 32 consecutive rows.
@@ -1054,11 +1068,11 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   }
 
   bool made_interior = false;  // this lane created b at the previous level and it is interior now
-  int pend = -1, pend_b = 0;   // CDF cache slot (and belief) this lane wrote, tag pending
   // fast mode: the action this lane created at the previous level (its overlay slot is stored
   // one level later) and a belief owed a dense row (written after the levels)
   int pend_x = -1, pend_k = 0, pend_bel = -1, pend_mat = -1, pend_mat_prev = -1;
   int won_a = 0, won_b = 0;    // nodes this lane created (live counts, one reduction per warp)
+  VP_PH_INIT();
   for (int l = depth0; l < d; ++l) {
     const u64 lkey = fold(skey, (u64)l);  // search.py:107
     // ---- parity mode, lazy rows: b is interior at this level; write its PSI row once
@@ -1067,11 +1081,15 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (lead && !made_interior && (fl & 2u)) mat = atomicAnd(&T.b_flags[b], ~2u) & 2u;
       materialise_rows<PsiT>(T, init_row, __ballot_sync(FULL, mat), b);
     }
+#ifdef VP_PHASE_CLOCKS
+    { u32 w_; asm volatile("mov.b32 %0, %1;" : "=r"(w_) : "r"(rec.dense_pass)); (void)w_; }
+    VP_PH(0);
+#endif
     // ---- softmax draw (search.py:108-112)
     const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
     int a = 0;
     if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
-    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, fl, rec, lse, lse_init, ok, u, pass, pend, pend_b);
+    else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, fl, rec, lse, lse_init, ok, u, pass);
     // ---- generative model (search.py:113-115), state stays in registers
     u32 o = 0;
     double rw = 0.0;
@@ -1081,7 +1099,9 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         rw = S.inject_reward[(size_t)l * n + r];
       }
     } else {
+      VP_PH(1);
       model_step<Model>(M, st, a, fold(lkey, 1), rg, ok, o, rw);  // level_rng.derive(1)
+      VP_PH(2);
     }
 
     // ---- action node (b, a) and belief node: append_actions / append_beliefs (tree.py:180-256)
@@ -1113,6 +1133,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (lead_a) cl_a = claim_finish_id(ha, T.hmask_a, key_a, word_a, ta);
       if (lead_b) cl_b = claim_finish_id(hb, T.hmask_b, key_b, word_b, tb);
     }
+    VP_PH(3);
     // deferred from the previous level: the overlay slot of the action this lane created there
     // (its atomic has had a whole level to return)
     if (pend_x >= 0) {
@@ -1171,6 +1192,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       }
       if (lead_b) cl_b = claim_finish_id(hb, T.hmask_b, key_b, word_b, claim_try_id(hb, T.hmask_b, key_b, word_b, true));
     }
+    VP_PH(4);
     grp = grp_b;
     lead = lead_b;
     int c = 0;
@@ -1204,6 +1226,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     }
     const bool led_b = __shfl_sync(FULL, (int)lead_b, leader_b) != 0;
     ok = ok && led_b;
+    VP_PH(5);
     arrive(T, W, leaf_count, c, grp, lead && ok, !interior_next);
     if (active && W.trace_action) {
       const size_t t = (size_t)l * n + r;
@@ -1240,6 +1263,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     if (won_b) red_add(&T.counters[VP_COUNTER_LIVE_B], won_b);
   }
 
+  VP_PH(6);
   // ---- leaves: heuristic value (search.py:119), summed per leaf (backup.py:44-51)
   double h = 0.0;
   if (active) {
@@ -1251,7 +1275,8 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   const double sum = group_sum(h, grp, ok);
   if (ok && lane == __ffs(grp) - 1) red_add(&T.b_value[b], sum);
   bulk_store_drain();
-  publish_pending_cdf(T, pend, pend_b, pass);
+  VP_PH(7);
+  VP_PH_FLUSH();
   if (W.stats && threadIdx.x == 0 && blockIdx.x == 0) {
     atomicAdd(&W.stats[3], 1ull);
     atomicAdd(&W.stats[4], (unsigned long long)n * (unsigned long long)(d - depth0));
@@ -1332,7 +1357,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
     pb = T.b_parent_belief[c];
     act = T.b_parent_act[c];
   }
-  unsigned long long n_act = 0, n_bel = 0, n_psi = 0;
+  unsigned long long n_act = 0, n_bel = 0, n_psi = 0, n_cdf = 0, n_ovf = 0;
   while (__any_sync(FULL, live)) {
     int ready = -1, nx = -1, npb = -1, nact = 0;
     int prow = -1;  // the PSI row of a completed belief's full-row fallback (-1: overlay row)
@@ -1394,8 +1419,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
             const PsiT new_v = (PsiT)(old_v + (q - lse_pre));
             if (dense) {
               term = exp(eta * ((double)new_v - lse_pre)) - exp(eta * (old_v - lse_pre));
-              *cell = new_v;
-              __threadfence();  // an ill-conditioned sum makes the completing lane read the row
+              *cell = new_v;  // published to the completer by the ordered delivery below
             } else if (slot < kOverlay) {
               // overlay row: deliver the new cell's log-mass eta psi and flag its slot; the
               // completing lane adds the unchanged cells (untouched slots + unrealised initial
@@ -1411,7 +1435,8 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
           // N(b) = lifetime visits of the valued actions (backup.py:110-114)
           Acc ba;
           const bool done = slotbit ? acc_deliver_log(T.b_acc, pb, term, (u32)tot | slotbit, (u32)vis, btot, ba)
-                                    : acc_deliver(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba);
+                            : prow >= 0 ? acc_deliver<true>(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba)
+                                        : acc_deliver(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba);
           if (done) {
             ready = pb;
             bsum = ba.sum;
@@ -1476,7 +1501,15 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         if (full) {
           if (!ofull) V = s_v[lane];
           ++n_psi;
+          n_ovf += ofull;
         }
+        if constexpr (!Exact)
+          if (prow >= 0) {  // a changed dense row: the CDF kernel after this one rebuilds its CDF
+            DenseMeta* dm = reinterpret_cast<DenseMeta*>(T.dense_meta) + prow;
+            dm->lse = V;
+            dm->pass = pass;
+            ++n_cdf;
+          }
         T.b_lse[ready] = V;
         T.b_flags[ready] = 0u;
         T.b_rows[ready] = 0;
@@ -1494,12 +1527,34 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
     n_act = warp_sum(n_act);
     n_bel = warp_sum(n_bel);
     n_psi = warp_sum(n_psi);
+    n_cdf = warp_sum(n_cdf);
+    n_ovf = warp_sum(n_ovf);
     if (lane == 0) {
       if (n_bel) atomicAdd(&W.stats[0], n_bel);
       if (n_psi) atomicAdd(&W.stats[8], n_psi);
       if (n_act) atomicAdd(&W.stats[1], n_act);
+      if (n_cdf) atomicAdd(&W.stats[11], n_cdf);
+      if (n_ovf) atomicAdd(&W.stats[12], n_ovf);
       if (i < cnt) atomicAdd(&W.stats[7], (unsigned long long)min(rpw, cnt - warp_index * rpw));
     }
+  }
+}
+
+// The dense rows a backup changed get their softmax CDF rebuilt for the next pass's draws, one
+// warp per row over the whole GPU (off the backup's climb; the kernel boundary makes every new
+// cell visible).
+template <class PsiT>
+__device__ void cdf_rows_warp(const vp_tree& T, u32 pass) {
+  const int nd = min(T.counters[VP_COUNTER_DENSE], T.cap_dense);
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const PsiT* psi = reinterpret_cast<const PsiT*>(T.psi);
+  PsiT* cdf = reinterpret_cast<PsiT*>(T.psi_cdf);
+  const DenseMeta* meta = reinterpret_cast<const DenseMeta*>(T.dense_meta);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nd; r += warps) {
+    const DenseMeta m = meta[r];
+    if (m.pass == pass)
+      build_cdf_row<PsiT, false>(psi + (size_t)r * T.psi_stride, cdf + (size_t)r * T.psi_stride, T.action_count,
+                                 T.eta, m.lse);
   }
 }
 

@@ -60,8 +60,6 @@ def _stream():
 class DeviceTree:
     """B / A / PSI tables of one planning step on the current CUDA device."""
 
-    CDF_SLOTS = 1 << 16  # direct-mapped CDF cache rows (csrc draw_action)
-
     def __init__(self, action_count: int, init_prefs=None, *, eta: float = 2.0, precision: str = "fp32",
                  exact: bool = False, cap_beliefs: int = 4096, cap_actions: int = 4096, cap_dense: int = 0):
         if action_count < 1:
@@ -126,6 +124,10 @@ class DeviceTree:
         self.b_parent_act = col(g("b_parent_act"), cap_b, torch.int32, keep_b)
         self.b_depth = col(g("b_depth"), cap_b, torch.int32, keep_b)
         self.psi = col(g("psi"), (cap_d, self.psi_stride), self._psi_dtype, keep_b if self.exact else keep_dense)
+        # fast mode: the softmax CDF of each dense row (rebuilt by the backup)
+        self.psi_cdf = col(g("psi_cdf"), (1 if self.exact else cap_d, self.psi_stride), self._psi_dtype,
+                           0 if self.exact else keep_dense)
+        self.dense_meta = col(g("dense_meta"), (1 if self.exact else cap_d, 2), torch.int64, 0, 0)
         self.b_lse = col(g("b_lse"), cap_b, torch.float64, keep_b)
         self.b_value = col(g("b_value"), cap_b, torch.float64, keep_b, 0)
         self.b_rows = col(g("b_rows"), cap_b, torch.int32, keep_b, 0)
@@ -134,10 +136,6 @@ class DeviceTree:
         self.b_rec = col(g("b_rec"), (cap_b, rec_words), torch.int32, keep_b, 0)
         self.b_nact = col(g("b_nact"), cap_b, torch.int32, keep_b, 0)
         self.b_ckey = col(g("b_ckey"), cap_b, torch.int64, keep_b, -1)
-        slots = min(_pow2_at_least(cap_b), self.CDF_SLOTS)
-        if getattr(self, "cdf_tag", None) is None or self.cdf_tag.numel() != slots:
-            self.cdf_cache = torch.empty((slots, self.psi_stride), dtype=self._psi_dtype, device=dev)
-            self.cdf_tag = torch.zeros(slots, dtype=torch.int64, device=dev)  # pass 0: empty
         self.a_parent_belief = col(g("a_parent_belief"), cap_a, torch.int32, keep_a)
         self.a_action = col(g("a_action"), cap_a, torch.int32, keep_a)
         self.a_reward = col(g("a_reward"), cap_a, torch.float64, keep_a, 0)
@@ -159,9 +157,8 @@ class DeviceTree:
         s.psi_stride = self.psi_stride
         for name in ("b_parent_action", "b_parent_obs", "b_parent_belief", "b_parent_act", "b_depth", "psi", "b_lse", "b_value", "b_rows", "b_acc",
                      "b_flags", "b_rec", "b_nact", "b_ckey", "a_parent_belief", "a_action", "a_reward", "a_visits",
-                     "a_rows", "a_acc", "a_ckey", "a_slot", "hash_a", "hash_b", "cdf_cache", "cdf_tag"):
+                     "a_rows", "a_acc", "a_ckey", "a_slot", "hash_a", "hash_b", "psi_cdf", "dense_meta"):
             setattr(s, name, getattr(self, name).data_ptr())
-        s.cdf_slots = self.cdf_tag.numel()
         s.cap_dense = cap_d
         s.overlay_slots = self.overlay_slots
         s.bkey_mode = getattr(self, "bkey_mode", 0)
@@ -341,6 +338,7 @@ class DeviceTree:
                            torch.from_numpy(r).cuda(), len(b))
         if self.counts()[2]:
             raise _lib.CapacityError("action table overflow")
+        _lib.call("vp_tree_build_cdfs", C.byref(self.struct), _stream())  # rows made dense by the edit
         return self.to_reference_actions(out.to(torch.int64)).cpu().numpy()
 
     def append_beliefs(self, action_node_indices, observations) -> np.ndarray:
@@ -436,6 +434,7 @@ class DeviceTree:
         tree._counters[0], tree._counters[_lib.VP_COUNTER_ACTIONS], tree._counters[2] = nb, na, 0
         tree._counters[_lib.VP_COUNTER_LIVE_B], tree._counters[_lib.VP_COUNTER_LIVE_A] = nb, na
         _lib.call("vp_tree_rehash", C.byref(tree.struct), _stream())
+        _lib.call("vp_tree_build_cdfs", C.byref(tree.struct), _stream())  # every row is dense here
         tree.pass_cursor = 1
         tree._canon_cache = None
         return tree

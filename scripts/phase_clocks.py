@@ -1,0 +1,35 @@
+"""Per-phase cycles of the search kernel (measurement build, see phase_clocks.sh)."""
+import argparse
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2510_27191_b200 as vp  # noqa: E402
+from paper_2510_27191_b200 import _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=11)
+ap.add_argument("--n-parallel", type=int, default=16384)
+ap.add_argument("--iterations", type=int, default=10)
+a = ap.parse_args()
+model = vp.MarsModel(a.n, a.n, layout_seed=1000)
+belief = vp.ParticleBelief.from_model(model, 10_000, vp.RowRng.from_seed(1000).derive(3))
+cfg = vp.SolverConfig(n_parallel=a.n_parallel, iterations=a.iterations)
+lib = _lib.load()
+buf = (C.c_ulonglong * 16)()
+for t in range(3):
+    vp.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, t))
+torch.cuda.synchronize()
+lib.vp_debug_phases(buf)
+names = ["rec wait", "draw", "model", "claims", "post-action", "belief-post", "arrive+tail", "leaf"]
+tot = sum(buf[:8])
+warps = (a.n_parallel + 31) // 32
+levels = sum(min(i + 1, 50) for i in range(a.iterations)) * 3
+for k in range(8):
+    print(f"{names[k]:16s} {100.0 * buf[k] / tot:5.1f}%  {buf[k] / warps / levels:8.0f} cycles per warp-level")
+dr = ["publish prev CDF", "init/overlay draw", "tag+claim", "stage issue", "TMA wait", "CDF build", "store+bsearch"]
+for k in range(7):
+    print(f"  draw.{dr[k]:18s} {buf[8 + k] / warps / levels:8.0f} cycles per warp-level")

@@ -10,7 +10,7 @@ seed, MARS(15,15) 65 536 x 10).
   within 1e-5 (scale-aware) of the fp64 values.  C2 injects the oracle's streams; C3 injects the
   streams of the fp64 parity plan, whose tree digests equal the reference's.
 * the fp32 sampler at a pass that samples more than 65 536 distinct non-fresh beliefs, so the
-  direct-mapped per-pass CDF cache (64k slots) must evict: every draw equals the inverse CDF of
+  dense rows' CDF rows rebuilt by the backups: every draw equals the inverse CDF of
   softmax(eta PSI) of the tree at the start of the pass, up to fp32 CDF-edge flips.
 """
 
@@ -118,16 +118,12 @@ def test_fp32_injected_streams_c3_chain():
     assert _scale_close(got["prefs"], want["prefs"], 1e-5)
 
 
-@pytest.mark.parametrize("kind,n,k,slots", [("synthetic", 131072, 12, None), ("mars11_11", 16384, 10, 64)])
-def test_fp32_sampler_with_cdf_cache_eviction(kind, n, k, slots, monkeypatch):
-    """Passes that sample more distinct non-fresh beliefs than the per-pass CDF cache has slots,
-    so the direct-mapped cache must evict: Synthetic at 131 072 rows x 12 iterations samples
-    ~95k distinct existing beliefs in its last pass (64k slots); MARS(11,11) at C2 with the cache
-    cut to 64 slots.  Every draw is the inverse CDF of softmax(eta PSI) of the tree at the start
-    of the pass, except fp32 CDF-edge flips."""
-    if slots:
-        monkeypatch.setattr(vp.tree.DeviceTree, "CDF_SLOTS", slots)
-    cache_slots = slots or vp.tree.DeviceTree.CDF_SLOTS
+@pytest.mark.parametrize("kind,n,k", [("synthetic", 131072, 12), ("mars11_11", 16384, 10)])
+def test_fp32_sampler_at_scale(kind, n, k):
+    """fp32 draws at scale: Synthetic at 131 072 rows x 12 iterations samples ~95k distinct
+    existing beliefs in its last pass (overlay records and dense rows, whose CDF rows the
+    previous backup rebuilt); MARS(11,11) at the C2 workload.  Every draw is the inverse CDF of
+    softmax(eta PSI) of the tree at the start of the pass, except fp32 CDF-edge flips."""
     model = vp.SyntheticModel(n_actions=16, n_obs=8, seed=3) if kind == "synthetic" else vp.MarsModel(11, 11,
                                                                                                       layout_seed=3)
     belief = vp.ParticleBelief.from_model(model, 10_000, vp.RowRng.from_seed(3).derive(3))
@@ -136,7 +132,6 @@ def test_fp32_sampler_with_cdf_cache_eviction(kind, n, k, slots, monkeypatch):
                                      keep_tree=True).tree.tables()
     out = vp.Planner("fp32").plan(belief, model, vp.SolverConfig(n_parallel=n, iterations=k), rng,
                                   keep_tree=True, trace=True)
-    assert out.tree.cdf_tag.numel() == min(cache_slots, out.tree.cdf_tag.numel())
     prefs = before["prefs"]
     nb, A = prefs.shape
     search_rng = rng.derive(k - 1).derive(1)
@@ -159,5 +154,6 @@ def test_fp32_sampler_with_cdf_cache_eviction(kind, n, k, slots, monkeypatch):
         mism += len(bad)
         total += n
         ids = tr["next_beliefs"]
-    assert len(distinct_known) > out.tree.cdf_tag.numel(), (len(distinct_known), out.tree.cdf_tag.numel())
+    if kind == "synthetic":
+        assert len(distinct_known) > 65536, len(distinct_known)
     assert mism <= max(3, 1e-3 * total), (mism, total)
