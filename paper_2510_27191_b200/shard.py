@@ -82,9 +82,12 @@ def all_gather_blocks(local, world: int, group, torch):
     """torch.distributed all-gather of equal-shape trajectory blocks, rank-major."""
     import torch.distributed as dist
 
+    dev = local.device
+    if dev.type == "cuda" and dist.get_backend(group) == "gloo":  # gloo moves host tensors (CPU tests)
+        local = local.cpu()
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local.contiguous(), group=group)
-    return gather_blocks(parts, torch)
+    return gather_blocks(parts, torch).to(dev)
 
 
 class ShardedPlanner(Planner):

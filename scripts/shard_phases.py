@@ -24,8 +24,9 @@ ap.add_argument("--iterations", type=int, default=10)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--problem", default="mars", choices=["mars", "crowdnav"])
 ap.add_argument("--particles", type=int, default=10_000)
+ap.add_argument("--board", type=int, default=11, help="MARS board size (11: C2, 15: C3)")
 a = ap.parse_args()
-model = vp.MarsModel(11, 11, layout_seed=1000) if a.problem == "mars" else vp.CrowdNavModel()
+model = vp.MarsModel(a.board, a.board, layout_seed=1000) if a.problem == "mars" else vp.CrowdNavModel()
 belief = vp.ParticleBelief.from_model(model, a.particles, vp.RowRng.from_seed(1000).derive(3))
 
 

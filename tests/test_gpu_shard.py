@@ -60,3 +60,57 @@ def test_sharded_rejects_uneven_rows():
     with pytest.raises(ValueError):
         vp.ShardedPlanner(world=3).plan(belief, om, oracle.SolverConfig(n_parallel=100, iterations=2),
                                         oracle.RowRng.from_seed(0))
+
+
+def _rank_worker(rank, world, port, name, q):
+    """One process of a world-2 job on the same GPU: gloo carries the exchange (the code path
+    NCCL drives on a multi-GPU box)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        case = manifest()["plans"][name]
+        g = load(name)
+        planner = vp.ShardedPlanner(world=world, rank=rank, group=dist.group.WORLD, precision="fp64", exact=True)
+        ok = True
+        for run in case["runs"]:
+            s = run["seed"]
+            om, belief, cfg, rng = plan_inputs(case, s)
+            out = planner.plan(belief, om, cfg, rng, keep_tree=True)
+            t = out.tree.tables()
+            ok &= out.tree_stats == run["tree_stats"] and out.chosen_action == run["chosen_action"]
+            ok &= all(np.array_equal(t[k], g[f"s{s}_{k}"].astype(np.int64)) for k in INT_COLUMNS)
+            ok &= bool(np.allclose(t["prefs"].sum(axis=1), g[f"s{s}_prefs_row_sum"], rtol=1e-9, atol=1e-8))
+        q.put((rank, bool(ok)))
+    except Exception as e:  # noqa: BLE001 -- reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["plan_mars7_8_c1", "plan_synthetic"])
+def test_sharded_planner_two_processes_gloo(name):
+    """ShardedPlanner across two real processes (torch.distributed, gloo, 127.0.0.1) on one GPU:
+    both replicas must equal the reference's golden trees in fp64 parity mode."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+    res = sorted(q.get() for _ in range(2))
+    assert res == [(0, True), (1, True)], res
