@@ -1286,9 +1286,9 @@ int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, cons
 #ifdef VP_PHASE_CLOCKS
 // measurement builds: read (and clear) the per-phase cycle sums of the search
 int32_t vp_debug_phases(unsigned long long* host_out) {
-  if (cudaMemcpyFromSymbol(host_out, vp::g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess)
+  if (cudaMemcpyFromSymbol(host_out, vp::g_phase_cycles, 24 * sizeof(unsigned long long)) != cudaSuccess)
     return VP_ERR_CUDA;
-  unsigned long long z[16] = {0};
+  unsigned long long z[24] = {0};
   return cudaMemcpyToSymbol(vp::g_phase_cycles, z, sizeof(z)) == cudaSuccess ? VP_OK : VP_ERR_CUDA;
 }
 #endif

@@ -34,15 +34,19 @@ constexpr int kSearchWarps = 2;   // warps per search block
 // Measurement builds only (-DVP_PHASE_CLOCKS, scripts/phase_clocks.sh): SM cycles per search
 // phase summed over warps (lane 0), read back with vp_debug_phases.
 #ifdef VP_PHASE_CLOCKS
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[24];
 #define VP_PH_INIT() long long ph_t0 = clock64(); unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define VP_PH(k) { const long long t_ = clock64(); ph_acc[k] += (unsigned long long)(t_ - ph_t0); ph_t0 = t_; }
 #define VP_PH_FLUSH() if (lane_id() == 0) for (int k_ = 0; k_ < 8; ++k_) atomicAdd(&g_phase_cycles[k_], ph_acc[k_]);
+#define VP_BK(k) { const long long t_ = clock64(); if (lane_id() == 0) atomicAdd(&g_phase_cycles[16 + k], (unsigned long long)(t_ - bk_t0)); bk_t0 = clock64(); }
+#define VP_BK_INIT() long long bk_t0 = clock64();
 #define VP_DR_INIT() long long dr_t0 = clock64();
 #define VP_DR(k) { const long long t_ = clock64(); if (lane_id() == 0) atomicAdd(&g_phase_cycles[8 + k], (unsigned long long)(t_ - dr_t0)); dr_t0 = clock64(); }
 #else
 #define VP_DR_INIT()
 #define VP_DR(k)
+#define VP_BK_INIT()
+#define VP_BK(k)
 #define VP_PH_INIT()
 #define VP_PH(k)
 #define VP_PH_FLUSH()
@@ -1358,7 +1362,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
     act = T.b_parent_act[c];
   }
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0, n_cdf = 0, n_ovf = 0;
+  VP_BK_INIT();
   while (__any_sync(FULL, live)) {
+    VP_BK(0);
     int ready = -1, nx = -1, npb = -1, nact = 0;
     int prow = -1;  // the PSI row of a completed belief's full-row fallback (-1: overlay row)
     u32 slotbit = 0, bmask = 0;  // overlay slot this lane's action changed / all changed slots
@@ -1446,6 +1452,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         }
       }
     }
+    VP_BK(1);
     if (__any_sync(FULL, ready >= 0)) {
       // last action of a belief: V = LSE_post (backup.py:109), cached as the next LSE_pre.
       // Fast mode uses the incremental sum; parity mode (and tiny / overflowing incremental
@@ -1453,27 +1460,38 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
       bool full = ready >= 0;
       bool ofull = false;
       if constexpr (!Exact) {
-        if (fresh && prow < 0 && T.init_uniform) {
-          // overlay row: eta LSE = log sum_a exp(eta psi_a) = the changed cells (delivered, log
-          // space) (+) the slots untouched this pass (stable in this lane's record) (+) the
-          // unrealised initial cells, (|A| - filled) exp(eta init)
-          // (one max shift, then a sum of at most kOverlay + 2 exponentials and one log)
-          double lk[kOverlay];
-          double m = bsum;
-          int filled = __popc(bmask);
+        // overlay row (uniform initial row): eta LSE = log sum_a exp(eta psi_a) = the changed
+        // cells (delivered, log space) (+) the slots untouched this pass (stable in this lane's
+        // record) (+) the unrealised initial cells, (|A| - filled) exp(eta init): one max shift,
+        // then only the exponentials some lane of the warp needs (the max term is exactly 1 --
+        // typically one exponential and one log per belief)
+        const bool ovl = ready >= 0 && fresh && prow < 0 && T.init_uniform;
+        double lk[kOverlay];
+        double m = ovl ? bsum : 0.0;
+        int filled = __popc(bmask);
 #pragma unroll
-          for (int k = 0; k < kOverlay; ++k) {
-            const bool keep = !((bmask >> k) & 1u) && prec.act[k];
-            lk[k] = keep ? eta * (double)prec.val[k] : -INFINITY;
-            m = fmax(m, lk[k]);
-            filled += keep;
+        for (int k = 0; k < kOverlay; ++k) {
+          const bool keep = ovl && !((bmask >> k) & 1u) && prec.act[k];
+          lk[k] = keep ? eta * (double)prec.val[k] : -INFINITY;
+          m = fmax(m, lk[k]);
+          filled += keep;
+        }
+        const double li = eta * (double)(PsiT)T.init_prefs[0];
+        const int rest = T.action_count - filled;
+        if (ovl && rest > 0) m = fmax(m, li);
+        auto term = [&](bool use, double x) -> double {  // exp(x - m) for the lanes that use it
+          const bool need = use && x != m;
+          double t = use ? 1.0 : 0.0;
+          if (__any_sync(FULL, need)) {
+            const double e = exp(x - m);
+            if (need) t = e;
           }
-          const double li = eta * (double)(PsiT)T.init_prefs[0];
-          const int rest = T.action_count - filled;
-          if (rest > 0) m = fmax(m, li);
-          double sum = exp(bsum - m) + (rest > 0 ? (double)rest * exp(li - m) : 0.0);
+          return t;
+        };
+        double sum = term(ovl, bsum) + (double)rest * term(ovl && rest > 0, li);
 #pragma unroll
-          for (int k = 0; k < kOverlay; ++k) sum += exp(lk[k] - m);
+        for (int k = 0; k < kOverlay; ++k) sum += term(lk[k] > -INFINITY, lk[k]);
+        if (ovl) {
           V = (m + log(sum)) / eta;
           full = false;
         } else if (fresh && prow >= 0) {
@@ -1523,6 +1541,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
       }
     }
   }
+  VP_BK(2);
   if (W.stats) {
     n_act = warp_sum(n_act);
     n_bel = warp_sum(n_bel);

@@ -19,7 +19,7 @@ model = vp.MarsModel(a.n, a.n, layout_seed=1000)
 belief = vp.ParticleBelief.from_model(model, 10_000, vp.RowRng.from_seed(1000).derive(3))
 cfg = vp.SolverConfig(n_parallel=a.n_parallel, iterations=a.iterations)
 lib = _lib.load()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 24)()
 for t in range(3):
     vp.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, t))
 torch.cuda.synchronize()
@@ -30,6 +30,9 @@ warps = (a.n_parallel + 31) // 32
 levels = sum(min(i + 1, 50) for i in range(a.iterations)) * 3
 for k in range(8):
     print(f"{names[k]:16s} {100.0 * buf[k] / tot:5.1f}%  {buf[k] / warps / levels:8.0f} cycles per warp-level")
-dr = ["publish prev CDF", "init/overlay draw", "tag+claim", "stage issue", "TMA wait", "CDF build", "store+bsearch"]
-for k in range(7):
+dr = ["-", "init/overlay draw", "-", "stage issue", "TMA wait", "-", "bsearch"]
+for k in (1, 3, 4, 6):
     print(f"  draw.{dr[k]:18s} {buf[8 + k] / warps / levels:8.0f} cycles per warp-level")
+bk = ["belief completion (prev) + loop test", "climb step (loads, deliveries, Q)", "final completion"]
+for k in range(3):
+    print(f"  backup.{bk[k]:34s} {buf[16 + k] / 1e6:8.2f} Mcycles (warp sum)")
