@@ -206,16 +206,17 @@ class ClockSampler:
 
 
 def algorithmic_bytes(st, n, S, A, psi_b, passes):
-    """Compulsory HBM bytes of the search and backup kernels summed over `passes` passes, from
-    the device traffic counters (adapted to the fused design: states and
-    frontier ids stay in registers across levels; node fields at element granularity, hash
+    """Compulsory HBM bytes of the search, backup and CDF kernels summed over `passes` passes,
+    from the device traffic counters (adapted to the fused design: states
+    and frontier ids stay in registers across levels; node fields at element granularity, hash
     probes at 32-B sector granularity; fast-mode PSI: a belief is its overlay record -- one
     record + its cached LSE per distinct belief visited -- and only beliefs with more than 4
-    action children own a dense row, read once per pass when sampled).
+    action children own a dense row, whose CDF row the search reads once per pass when sampled).
 
     U   interior beliefs backed up (= distinct beliefs sampled from), P distinct action nodes
-        visited, L distinct leaves, NA / NB new action / belief nodes, D distinct dense rows
-        sampled (CDFs built), M dense rows materialised, F full-row LSE reads (fallback).
+        visited, L distinct leaves, NA / NB new action / belief nodes, D dense rows changed by
+        a backup (their CDF rows rebuilt; ~ the distinct dense rows the next pass samples),
+        M dense rows materialised, F full-row LSE reads (fallback), R dense rows in use.
     """
     U, P, L, NA, NB = st[0], st[1], st[7], st[5], st[6]
     D, M, F = st[11], st[10], st[8]
@@ -223,7 +224,7 @@ def algorithmic_bytes(st, n, S, A, psi_b, passes):
     children = (U - passes) + L  # distinct (a, o) probes: every visited non-root belief
     search = (n * passes * S                   # root-state gather
               + (rec + 8) * (U + L)            # record + cached LSE of every distinct belief reached
-              + psi_b * A * D                  # dense PSI row per distinct dense belief sampled
+              + psi_b * A * D                  # CDF row per distinct dense belief sampled
               + 32 * (P + children)            # one hash sector per distinct probe (claims)
               + 16 * P                         # reward / visit / row reductions per action
               + 24 * NA + 40 * NB              # new node columns (+ child count, overlay slot)
@@ -232,14 +233,17 @@ def algorithmic_bytes(st, n, S, A, psi_b, passes):
     backup = (24 * L                           # leaf (rows, value) read + reset
               + (56 + rec + 2 * psi_b) * P     # action stats + slot, accumulator r/w, record + cell r/w
               + 76 * U                         # belief LSE / rows / parents, accumulator r/w
-              + psi_b * A * F)                 # full-row LSE (ill-conditioned incremental sums)
-    return search, backup
+              + psi_b * A * F                  # full-row LSE (ill-conditioned incremental sums)
+              + 16 * D)                        # CDF rebuild request (LSE, pass) per changed dense row
+    cdf = 2 * psi_b * A * D                    # k_cdf_rows: the changed rows read, their CDFs written
+    return search, backup, cdf
 
 
 # dependent global round trips on a warp's critical path per level:
-# search = PSI-row / CDF-tag fetch + child flags (loads), (b,a)+(a,o) claim CAS + id allocation
-# (atomics); backup = node fetch (load) + delivery to the parent (atomic)
-ROUND_TRIPS = {"search": {"load": 2, "atomic": 2}, "backup": {"load": 1, "atomic": 1}}
+# search = the child's overlay record + a dense row's CDF (TMA) (loads), the (b,a) and (a,o)
+# claims issued together, ids static (one atomic); backup = node fetch (load) + delivery to
+# the parent (atomic)
+ROUND_TRIPS = {"search": {"load": 2, "atomic": 1}, "backup": {"load": 1, "atomic": 1}}
 
 
 def probe_latency(vp_lib, torch) -> dict:
@@ -408,7 +412,7 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
     psi_b = 4 if args.precision == "fp32" else 8
     S = dm.state_bytes
     passes = prof_steps * args.iterations
-    b_search, b_backup = algorithmic_bytes(st, args.n_parallel, S, A, psi_b, passes)
+    b_search, b_backup, b_cdf = algorithmic_bytes(st, args.n_parallel, S, A, psi_b, passes)
     levels_per_pass = st[4] / max(1.0, args.n_parallel * passes)
 
     # measured DRAM bytes per launch of the same workload (ncu launch list, scripts/ncu_capture.sh +
@@ -435,7 +439,7 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
                "bytes_per_launch": round(per_launch),
                "avg_launch_us": round(avg_ms * 1e3, 2), "share_of_step": round(ms / total_ms, 3),
                "algorithmic_bytes": formula, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
-        if latency:
+        if latency and kind in ROUND_TRIPS:
             rt = ROUND_TRIPS[kind]
             lvl_ns = rt["load"] * latency["l2_load"]["ns"] + rt["atomic"] * latency["l2_atomic"]["ns"]
             floor_us = levels_per_pass * lvl_ns / 1e3
@@ -449,13 +453,14 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
                        "n S + (rec + 8)(U + L) + psi_b|A| (D + M) + 48 P + 32 children + 24 NA + 40 NB + 12 L "
                        "per pass (bench.algorithmic_bytes)")
     roof_backup = roof("backup", "k_backup", b_backup,
-                       "24 L + (56 + rec + 2 psi_b) P + 76 U + psi_b|A| F per pass (bench.algorithmic_bytes)")
+                       "24 L + (56 + rec + 2 psi_b) P + 76 U + psi_b|A| F + 16 D per pass (bench.algorithmic_bytes)")
+    roof_cdf = roof("cdf_rows", "k_cdf_rows", b_cdf, "2 psi_b|A| D per pass (bench.algorithmic_bytes)")
     names = ["interior_beliefs", "actions_visited", "psi_rows_staged", "search_launches", "row_levels",
              "new_actions", "new_beliefs", "leaves", "full_row_lse_reads", "overlay_draws", "dense_rows_made",
              "dense_cdfs_built", "overlay_lse_fallbacks"]
     res.update({
         "roofline": {"search": roof_search, "backup": roof_backup}.get(top) or roof_search,
-        "roofline_other": {"k_search": roof_search, "k_backup": roof_backup},
+        "roofline_other": {"k_search": roof_search, "k_backup": roof_backup, "k_cdf_rows": roof_cdf},
         "kernels": {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] // prof_steps}
                     for k, v in kinds.items()},
         "dominant_kernel": top,

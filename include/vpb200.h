@@ -272,8 +272,8 @@ int32_t vp_last_cuda_error(void);
 int32_t vp_abi_layout(int32_t* out, int32_t n);
 
 /* ---- measurement -------------------------------------------------------- */
-/* Kernel kinds, in order: draw, search, backup, tree_init, rehash, argmax, hooks. */
-#define VP_KERNEL_KINDS 7
+/* Kernel kinds, in order: draw, search, backup, tree_init, rehash, argmax, hooks, cdf_rows. */
+#define VP_KERNEL_KINDS 8
 /* on != 0: clear and start recording a CUDA-event pair around every launch. */
 int32_t vp_profile_enable(int32_t on);
 /* Sum recorded durations (ms) and launch counts per kind; returns #kinds. */

@@ -159,7 +159,7 @@ _SIGNATURES = [
 
 EXPORTED_SYMBOLS = tuple(name for name, _, _ in _SIGNATURES)
 
-KERNEL_KINDS = ("draw", "search", "backup", "tree_init", "rehash", "argmax", "hooks")
+KERNEL_KINDS = ("draw", "search", "backup", "tree_init", "rehash", "argmax", "hooks", "cdf_rows")
 
 
 def profile_enable(on: bool):

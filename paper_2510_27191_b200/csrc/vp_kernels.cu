@@ -268,7 +268,7 @@ static int32_t check_launch() {
 }
 
 // ---- per-launch accounting: launch counter + optional CUDA-event timing by kernel kind
-enum KernelKind { KK_DRAW = 0, KK_SEARCH, KK_BACKUP, KK_TREE_INIT, KK_REHASH, KK_ARGMAX, KK_HOOK, KK_COUNT };
+enum KernelKind { KK_DRAW = 0, KK_SEARCH, KK_BACKUP, KK_TREE_INIT, KK_REHASH, KK_ARGMAX, KK_HOOK, KK_CDF, KK_COUNT };
 static_assert(KK_COUNT == VP_KERNEL_KINDS, "kernel kinds out of sync with vpb200.h");
 struct ProfRec {
   int kind;
@@ -473,7 +473,7 @@ static int32_t launch_backup(const vp_tree& T, const vp_work& W, u32 pass, doubl
     k_backup<PsiT, Exact><<<grid, kBackupWarps * 32, 0, st>>>(T, W, pass, gamma, rpw);
   }
   if constexpr (!Exact) {  // the CDFs of the dense rows this backup changed
-    Launch L_(KK_BACKUP, st);
+    Launch L_(KK_CDF, st);
     k_cdf_rows<PsiT><<<num_sms() * 4, 256, 0, st>>>(T, pass);
   }
   return check_launch();
