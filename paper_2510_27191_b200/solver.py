@@ -124,14 +124,16 @@ class Planner:
         need = 1 + n * total
         return min(need, max(self.node_budget(A), 1 + n * levels)), levels
 
-    def node_budget(self, A: int, fraction: float | None = None) -> int:
+    def node_budget(self, A: int, fraction: float | None = None, dense: bool = True) -> int:
         """Nodes (belief + action pairs) that fit in mem_fraction of the free HBM: the B columns
         per belief (+ its overlay record), the A columns per action, a 2x-oversized 16-B hash
         slot each, and PSI rows -- one per belief in parity mode, one per 5 actions at most in
-        fast mode (only beliefs with more than 4 action children own a dense row)."""
+        fast mode (only beliefs with more than 4 action children own a dense row; ``dense=False``:
+        the pool is grown on demand and budgeted separately, Planner.run)."""
         torch = _torch()
         elem = 4 if self.precision == "fp32" else 8
-        per_row = (A + 4) * elem if self.exact else (A + 4) * elem // (_lib.VP_OVERLAY_SLOTS + 1) + 8 * elem + 8
+        per_row = (A + 4) * elem if self.exact else \
+            (2 * (A + 4) * elem // (_lib.VP_OVERLAY_SLOTS + 1) if dense else 0) + 8 * elem + 8
         per_pair = per_row + 60 + 52 + 2 * 2 * 16
         free, _ = torch.cuda.mem_get_info()
         return int(free * (self.mem_fraction if fraction is None else fraction)) // per_pair
@@ -224,6 +226,9 @@ class Planner:
             tree.reset(tree.init_prefs, config.eta)  # device reset for the iterative path
             fixed = False
         if fixed:
+            if not tree.exact:  # the fixed graph cannot grow the dense pool: its worst case
+                need = 1 + config.n_parallel * sum(min(i + 1, config.d_max_cap) for i in range(config.iterations))
+                tree.ensure_dense(need // (_lib.VP_OVERLAY_SLOTS + 1) + 2)
             if isinstance(belief, DeviceBelief):
                 _, _, m = self.upload_belief(dm, belief)
                 return self.run_fixed(dm, tree, work, m, model.spec, config, key_of(rng), from_host=False,
@@ -297,6 +302,10 @@ class Planner:
         n = config.n_parallel
         stream = torch.cuda.current_stream().cuda_stream
         ub_b, ub_a = 1, 0
+        # fast mode: the dense PSI pool grows on demand (a pass makes at most one dense row per
+        # new action), separately from the node columns
+        tree.dense_on_demand = not tree.exact
+        ub_d = tree.n_dense() if not tree.exact else 0
         d_max, done, last = 1, 0, 0
         stopped = None
         traces = [] if trace else None
@@ -314,7 +323,7 @@ class Planner:
                     grown = max(tree.cap_beliefs, tree.cap_actions, 16)
                     while grown < max(need_b, need_a):
                         grown *= 2
-                    if grown > self.node_budget(tree.action_count, fraction=0.85):
+                    if grown > self.node_budget(tree.action_count, fraction=0.85, dense=tree.exact):
                         if config.iterations is not None:  # the reference always runs `iterations`
                             raise _lib.CapacityError(
                                 f"a {config.iterations}-iteration plan does not fit in HBM after "
@@ -322,6 +331,21 @@ class Planner:
                         stopped = "memory"
                         break
                 tree.ensure_capacity(need_b, need_a)
+            if not tree.exact and ub_d + n * d_max > tree.cap_dense:
+                ub_d = tree.n_dense()
+                need_d = ub_d + n * d_max
+                if need_d > tree.cap_dense:
+                    grown = max(tree.cap_dense, 16)
+                    while grown < need_d:
+                        grown *= 2
+                    free, _ = torch.cuda.mem_get_info()
+                    if done and (grown - tree.cap_dense) * tree.dense_bytes_per_row() > 0.85 * free:
+                        if config.iterations is not None:
+                            raise _lib.CapacityError(f"the dense PSI pool of a {config.iterations}-iteration plan "
+                                                     f"does not fit in HBM after {done} iterations")
+                        stopped = "memory"
+                        break
+                    tree.ensure_dense(need_d)
             inject = None
             if inject_actions is not None:
                 arr = np.asarray(inject_actions[done], dtype=np.int32).reshape(d_max, n)
@@ -336,6 +360,7 @@ class Planner:
                                "heuristic_values": work.leaf_value.cpu().numpy().copy()})
             ub_b += n * d_max
             ub_a += n * d_max
+            ub_d += n * d_max
             done += 1
             last = d_max
             if config.iterations is not None:

@@ -105,7 +105,10 @@ class DeviceTree:
         torch = _torch()
         dev = "cuda"
         A = self.action_count
-        cap_d = max(self.dense_rows_for(cap_b, cap_a), min_dense, keep_dense, 1)
+        if getattr(self, "dense_on_demand", False) and getattr(self, "cap_dense", 0):
+            cap_d = max(self.cap_dense, min_dense, keep_dense, 1)  # grown separately (ensure_dense)
+        else:
+            cap_d = max(self.dense_rows_for(cap_b, cap_a), min_dense, keep_dense, 1)
         rec_words = 8 if self.precision == "fp32" else 12  # sizeof(Rec<PsiT>) / 4 (32 / 48 bytes)
 
         def col(old, shape, dtype, keep, fill=None):
@@ -228,6 +231,8 @@ class DeviceTree:
 
     def ensure_capacity(self, need_beliefs: int, need_actions: int):
         """Grow (geometric, tree.py:90-97) so the next search cannot overflow."""
+        if getattr(self, "dense_on_demand", False) and not self.exact:  # one dense row per new action at most
+            self.ensure_dense(self.n_dense() + max(0, need_actions - self.extent()[1]))
         if need_beliefs <= self.cap_beliefs and need_actions <= self.cap_actions:
             return False
         nb, na = self.extent()
@@ -240,6 +245,31 @@ class DeviceTree:
         self._allocate(cap_b, cap_a, keep_b=nb, keep_a=na, keep_dense=self.n_dense())
         _lib.call("vp_tree_rehash", C.byref(self.struct), _stream())
         return True
+
+    def ensure_dense(self, need_rows: int) -> bool:
+        """Fast mode, iterative plans: grow the dense PSI pool (rows, their CDF rows and CDF
+        requests; geometric) so the next pass cannot run out -- a pass makes at most one dense
+        row per new action node.  Only the pool is reallocated."""
+        if self.exact or need_rows <= self.cap_dense:
+            return False
+        torch = _torch()
+        used = self.n_dense()
+        cap = max(self.cap_dense, 16)
+        while cap < need_rows:
+            cap *= 2
+        for name, width, dt in (("psi", self.psi_stride, self._psi_dtype), ("psi_cdf", self.psi_stride, self._psi_dtype),
+                                ("dense_meta", 2, torch.int64)):
+            old = getattr(self, name)
+            new = torch.zeros((cap, width), dtype=dt, device="cuda") if name == "dense_meta" else \
+                torch.empty((cap, width), dtype=dt, device="cuda")
+            new[:used] = old[:used]
+            setattr(self, name, new)
+            setattr(self.struct, name, new.data_ptr())
+        self.cap_dense = self.struct.cap_dense = cap
+        return True
+
+    def dense_bytes_per_row(self) -> int:
+        return 2 * self.psi_stride * self._psi_dtype.itemsize + 16
 
     def n_dense(self) -> int:
         """PSI rows in use (parity mode: the belief count)."""
