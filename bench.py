@@ -309,8 +309,10 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
     belief = vp.ParticleBelief.from_model(model, WORKLOAD["particles"], vp.RowRng.from_seed(seed).derive(3))
     n_rows = args.n_parallel * (world if sharded else 1)
     cfg = vp.SolverConfig(eta=WORKLOAD["eta"], n_parallel=n_rows, iterations=args.iterations)
+    # single GPU: the planner the public vp.plan() uses, so the device-timed and the e2e steps
+    # share one tree arena (large configs only fit once)
     planner = vp.ShardedPlanner(world, rank, group=dist.group.WORLD, precision=args.precision) if sharded \
-        else vp.Planner(args.precision)
+        else vp.solver.get_planner(args.precision, False)
     dm = vp.device_model(model)
     particles, cumw, m = planner.upload_belief(dm, belief)
     rngs = [vp.RowRng.from_seed(seed).derive(1, t) for t in range(args.warmup + args.steps)]

@@ -122,7 +122,9 @@ class Planner:
             total = sum(min(i + 1, cap_levels) for i in range(16))
             levels = cap_levels
         need = 1 + n * total
-        return min(need, max(self.node_budget(A), 1 + n * levels)), levels
+        # a fixed budget cannot grow inside its CUDA graph: give it up to 85 % of the free HBM
+        frac = 0.85 if config.iterations is not None else None
+        return min(need, max(self.node_budget(A, fraction=frac), 1 + n * levels)), levels
 
     def node_budget(self, A: int, fraction: float | None = None, dense: bool = True) -> int:
         """Nodes (belief + action pairs) that fit in mem_fraction of the free HBM: the B columns
@@ -134,7 +136,7 @@ class Planner:
         elem = 4 if self.precision == "fp32" else 8
         per_row = (A + 4) * elem if self.exact else \
             (2 * (A + 4) * elem // (_lib.VP_OVERLAY_SLOTS + 1) if dense else 0) + 8 * elem + 8
-        per_pair = per_row + 60 + 52 + 2 * 2 * 16
+        per_pair = per_row + 60 + 52 + 2 * 4 * 16  # hash: 2^k >= 2 cap slots, up to 4 per node
         free, _ = torch.cuda.mem_get_info()
         return int(free * (self.mem_fraction if fraction is None else fraction)) // per_pair
 
@@ -307,6 +309,9 @@ class Planner:
         tree.dense_on_demand = not tree.exact
         ub_d = tree.n_dense() if not tree.exact else 0
         d_max, done, last = 1, 0, 0
+        # a fixed budget's whole id range (static per-row ids: exact); growth never goes past it
+        total = (1 + n * sum(min(i + 1, config.d_max_cap) for i in range(config.iterations))
+                 if config.iterations is not None else None)
         stopped = None
         traces = [] if trace else None
         t0 = time.perf_counter()
@@ -323,6 +328,8 @@ class Planner:
                     grown = max(tree.cap_beliefs, tree.cap_actions, 16)
                     while grown < max(need_b, need_a):
                         grown *= 2
+                    if total is not None:
+                        grown = max(min(grown, total), need_b, need_a)
                     if grown > self.node_budget(tree.action_count, fraction=0.85, dense=tree.exact):
                         if config.iterations is not None:  # the reference always runs `iterations`
                             raise _lib.CapacityError(
@@ -330,7 +337,7 @@ class Planner:
                                 f"{done} iterations ({nb} beliefs, {na} actions)")
                         stopped = "memory"
                         break
-                tree.ensure_capacity(need_b, need_a)
+                tree.ensure_capacity(need_b, need_a, limit=total)
             if not tree.exact and ub_d + n * d_max > tree.cap_dense:
                 ub_d = tree.n_dense()
                 need_d = ub_d + n * d_max

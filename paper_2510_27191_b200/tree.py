@@ -229,7 +229,7 @@ class DeviceTree:
         self.counts()
         return int(self._host_counts[3]), int(self._host_counts[4])
 
-    def ensure_capacity(self, need_beliefs: int, need_actions: int):
+    def ensure_capacity(self, need_beliefs: int, need_actions: int, limit: int | None = None):
         """Grow (geometric, tree.py:90-97) so the next search cannot overflow."""
         if getattr(self, "dense_on_demand", False) and not self.exact:  # one dense row per new action at most
             self.ensure_dense(self.n_dense() + max(0, need_actions - self.extent()[1]))
@@ -242,6 +242,8 @@ class DeviceTree:
         cap_a = max(self.cap_actions, 16)
         while cap_a < need_actions:
             cap_a *= 2
+        if limit is not None:  # never past what the caller can still use (a fixed budget's total)
+            cap_b, cap_a = max(min(cap_b, limit), need_beliefs), max(min(cap_a, limit), need_actions)
         self._allocate(cap_b, cap_a, keep_b=nb, keep_a=na, keep_dense=self.n_dense())
         _lib.call("vp_tree_rehash", C.byref(self.struct), _stream())
         return True
