@@ -1291,6 +1291,19 @@ int32_t vp_debug_phases(unsigned long long* host_out) {
   unsigned long long z[24] = {0};
   return cudaMemcpyToSymbol(vp::g_phase_cycles, z, sizeof(z)) == cudaSuccess ? VP_OK : VP_ERR_CUDA;
 }
+// the backup completion trace out (returns the entry count), then reset
+int32_t vp_debug_trace(unsigned long long* host_out, int32_t max_n) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, vp::g_trace_n, sizeof(n)) != cudaSuccess) return -1;
+  n = std::min<unsigned int>(n, 1u << 21);
+  if (host_out && n &&
+      cudaMemcpyFromSymbol(host_out, vp::g_trace, sizeof(unsigned long long) * std::min<unsigned>(n, (unsigned)max_n)) !=
+          cudaSuccess)
+    return -1;
+  const unsigned int z = 0;
+  cudaMemcpyToSymbol(vp::g_trace_n, &z, sizeof(z));
+  return (int32_t)n;
+}
 #endif
 
 int32_t vp_probe_latency(const uint64_t* next, int32_t hops, int32_t atomic, uint64_t start, double* out,

@@ -35,6 +35,22 @@ constexpr int kSearchWarps = 2;   // warps per search block
 // phase summed over warps (lane 0), read back with vp_debug_phases.
 #ifdef VP_PHASE_CLOCKS
 __device__ unsigned long long g_phase_cycles[24];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// completion trace: (globaltimer mod 2^48) << 16 | pass << 8 | depth, buffered per warp in shared
+// memory and flushed once per warp (no contended atomics on the climb)
+__device__ unsigned long long g_trace[1 << 21];
+__device__ unsigned int g_trace_n;
+#define VP_WAVE_DECL() __shared__ unsigned long long s_tr[8][256]; __shared__ int s_trn[8]; \
+  const int w_tr = threadIdx.x >> 5; if (lane_id() == 0) s_trn[w_tr] = 0; __syncwarp();
+#define VP_WAVE(pass, depth) { const int k_ = atomicAdd(&s_trn[w_tr], 1); \
+  if (k_ < 256) s_tr[w_tr][k_] = ((gtimer() & ((1ull << 48) - 1)) << 16) | (((pass) & 255u) << 8) | (unsigned)(depth); }
+#define VP_WAVE_FLUSH() { __syncwarp(); const int n_ = min(s_trn[w_tr], 256); unsigned b_ = 0; \
+  if (lane_id() == 0) b_ = atomicAdd(&g_trace_n, (unsigned)n_); b_ = __shfl_sync(FULL, b_, 0); \
+  for (int i_ = lane_id(); i_ < n_; i_ += 32) if (b_ + i_ < (1u << 21)) g_trace[b_ + i_] = s_tr[w_tr][i_]; }
 #define VP_PH_INIT() long long ph_t0 = clock64(); unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define VP_PH(k) { const long long t_ = clock64(); ph_acc[k] += (unsigned long long)(t_ - ph_t0); ph_t0 = t_; }
 #define VP_PH_FLUSH() if (lane_id() == 0) for (int k_ = 0; k_ < 8; ++k_) atomicAdd(&g_phase_cycles[k_], ph_acc[k_]);
@@ -45,6 +61,9 @@ __device__ unsigned long long g_phase_cycles[24];
 #else
 #define VP_DR_INIT()
 #define VP_DR(k)
+#define VP_WAVE(pass, depth)
+#define VP_WAVE_DECL()
+#define VP_WAVE_FLUSH()
 #define VP_BK_INIT()
 #define VP_BK(k)
 #define VP_PH_INIT()
@@ -1363,6 +1382,8 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   }
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0, n_cdf = 0, n_ovf = 0;
   VP_BK_INIT();
+  VP_WAVE_DECL();
+  if (lane == 0) VP_WAVE(pass, 255);
   while (__any_sync(FULL, live)) {
     VP_BK(0);
     int ready = -1, nx = -1, npb = -1, nact = 0;
@@ -1495,10 +1516,14 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
           V = (m + log(sum)) / eta;
           full = false;
         } else if (fresh && prow >= 0) {
-          // dense row: 1 + sum_changed (new - old); well conditioned unless the changed cells
-          // carried most of the mass -- then the warp reads the row
+          // dense row: 1 + sum_changed (new - old) relative to its exact (fp64-maintained) LSE.
+          // Each term carries the rounding of eta (psi - LSE) (~|A| ulp(|psi|) in all), so the
+          // sum's relative error is ~|A| ulp(|psi|) / sum: trusted down to 1e-3 for fp32 storage
+          // (<= 1e-8 relative, far inside its 1e-5 contract) and 0.9 for fp64 (1e-10 contract);
+          // below that the warp reads the row
+          constexpr double kTrust = sizeof(PsiT) == 4 ? 1e-3 : 0.9;
           const double sum = 1.0 + bsum;
-          if (sum > 0.9 && sum < 1e300) {
+          if (sum > kTrust && sum < 1e300) {
             V = lse_pre + log(sum) / eta;
             full = false;
           }
@@ -1528,6 +1553,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
             dm->pass = pass;
             ++n_cdf;
           }
+        VP_WAVE(pass, min(T.b_depth[ready], 64));
         T.b_lse[ready] = V;
         T.b_flags[ready] = 0u;
         T.b_rows[ready] = 0;
@@ -1542,6 +1568,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
     }
   }
   VP_BK(2);
+  VP_WAVE_FLUSH();
   if (W.stats) {
     n_act = warp_sum(n_act);
     n_bel = warp_sum(n_bel);

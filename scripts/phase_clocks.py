@@ -36,3 +36,22 @@ for k in (1, 3, 4, 6):
 bk = ["belief completion (prev) + loop test", "climb step (loads, deliveries, Q)", "final completion"]
 for k in range(3):
     print(f"  backup.{bk[k]:34s} {buf[16 + k] / 1e6:8.2f} Mcycles (warp sum)")
+# the backup completion wave of one planning step: per pass and depth, when completions happened
+import numpy as np  # noqa: E402
+buf_t = (C.c_ulonglong * (1 << 21))()
+lib.vp_debug_trace(None, 0)
+vp.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, 99))
+torch.cuda.synchronize()
+cnt = lib.vp_debug_trace(buf_t, 1 << 21)
+tr = np.frombuffer(buf_t, dtype=np.uint64, count=cnt)
+t = (tr >> np.uint64(16)).astype(np.int64)
+ps = ((tr >> np.uint64(8)) & np.uint64(255)).astype(np.int64)
+dp = (tr & np.uint64(255)).astype(np.int64)
+for p in sorted(set(ps.tolist())):
+    m = ps == p
+    t0 = t[m & (dp == 255)].min()
+    parts = []
+    for d in sorted(set(dp[m].tolist()) - {255}):
+        x = (t[m & (dp == d)] - t0) / 1e3
+        parts.append(f"d{d}:{np.percentile(x, 50):.1f}/{np.percentile(x, 90):.1f}/{x.max():.1f}(n={len(x)})")
+    print(f"  backup pass {p} completion us p50/p90/max after the first warp:", " ".join(parts))
