@@ -47,7 +47,8 @@ __device__ unsigned int g_trace_n;
 #define VP_WAVE_DECL() __shared__ unsigned long long s_tr[8][256]; __shared__ int s_trn[8]; \
   const int w_tr = threadIdx.x >> 5; if (lane_id() == 0) s_trn[w_tr] = 0; __syncwarp();
 #define VP_WAVE(pass, depth) { const int k_ = atomicAdd(&s_trn[w_tr], 1); \
-  if (k_ < 256) s_tr[w_tr][k_] = ((gtimer() & ((1ull << 48) - 1)) << 16) | (((pass) & 255u) << 8) | (unsigned)(depth); }
+  if (k_ < 256) s_tr[w_tr][k_] = ((gtimer() & ((1ull << 40) - 1)) << 24) | (((pass) & 63u) << 18) | \
+      ((unsigned)(depth) << 12) | ((blockIdx.x * 8 + w_tr) & 4095u); }
 #define VP_WAVE_FLUSH() { __syncwarp(); const int n_ = min(s_trn[w_tr], 256); unsigned b_ = 0; \
   if (lane_id() == 0) b_ = atomicAdd(&g_trace_n, (unsigned)n_); b_ = __shfl_sync(FULL, b_, 0); \
   for (int i_ = lane_id(); i_ < n_; i_ += 32) if (b_ + i_ < (1u << 21)) g_trace[b_ + i_] = s_tr[w_tr][i_]; }
@@ -393,6 +394,31 @@ __device__ double row_lse_fast(const PsiT* row, int A, double eta) {
     out = __shfl_sync(FULL, v, 0);
   });
   return out;
+}
+
+// Streaming log-sum-exp of the elements start, start + stride, ... of an L2-resident row in fp64:
+// mx = max eta psi, sm = sum exp(eta psi - mx) over them.  Batches of 8 independent loads, the
+// running sum rescaled once per batch.
+template <class PsiT>
+__device__ __forceinline__ void lse_online_f64(const PsiT* r, int A, int start, int stride, double eta, double& mx,
+                                               double& sm) {
+  for (int a0 = start; a0 < A; a0 += 8 * stride) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int a = a0 + j * stride;
+      v[j] = a < A ? eta * (double)__ldcg(r + a) : -INFINITY;
+    }
+    double mb = v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) mb = fmax(mb, v[j]);
+    const double mn = fmax(mx, mb);
+    double acc = mx == -INFINITY ? 0.0 : sm * exp(mx - mn);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += v[j] == -INFINITY ? 0.0 : exp(v[j] - mn);
+    sm = acc;
+    mx = mn;
+  }
 }
 
 // LSE of a row in fp64 arithmetic by a full warp (returned on every lane).  Fast mode keeps
@@ -1318,13 +1344,32 @@ __device__ __forceinline__ void lse_ready(const vp_tree& T, int ready, u32 rmask
   if constexpr (Exact) {
     if (ready >= 0) out[lane_id()] = lse_exact<true>(reinterpret_cast<const double*>(psi) + (size_t)ready * T.psi_stride,
                                                       A, T.eta);
-  } else {  // the rare fallback of the incremental LSE: one row at a time, fp64 arithmetic
-    for (u32 m = rmask; m; m &= m - 1u) {
-      const int owner = __ffs(m) - 1;
-      const int row = __shfl_sync(FULL, ready, owner);
-      const double v = row_lse_f64<PsiT, true>(psi + (size_t)row * T.psi_stride, A, T.eta);
-      if (lane_id() == owner) out[owner] = v;
+  } else {
+    // the fallback of the incremental LSE, fp64 arithmetic: the k rows are read in parallel,
+    // each by a group of G = 32 / 2^ceil(log2 k) lanes (the completions that need it cluster
+    // at the busy top levels, where a row-at-a-time loop put k full reads on the critical path)
+    const int k = __popc(rmask);
+    const int G = k <= 1 ? 32 : k <= 2 ? 16 : k <= 4 ? 8 : k <= 8 ? 4 : k <= 16 ? 2 : 1;
+    const int lane = lane_id(), grp = lane / G, gl = lane % G;
+    int owner = -1;  // the grp-th lane of rmask
+    {
+      u32 m = rmask;
+      for (int i = 0; i < grp && m; ++i) m &= m - 1u;
+      if (grp < k) owner = __ffs(m) - 1;
     }
+    const int row = __shfl_sync(FULL, ready, owner >= 0 ? owner : 0);
+    const PsiT* r = owner >= 0 ? psi + (size_t)row * T.psi_stride : nullptr;
+    // one pass over the row, 8 loads in flight per lane, online max rescaling (the row lives
+    // in L2: a load-then-use loop would pay one L2 round trip per element)
+    double mx = -INFINITY, sm = 0.0;
+    if (r) lse_online_f64<PsiT>(r, A, gl, G, T.eta, mx, sm);
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double m2 = __shfl_xor_sync(FULL, mx, o), s2 = __shfl_xor_sync(FULL, sm, o);
+      const double mn = fmax(mx, m2);
+      sm = (mx == -INFINITY ? 0.0 : sm * exp(mx - mn)) + (m2 == -INFINITY ? 0.0 : s2 * exp(m2 - mn));
+      mx = mn;
+    }
+    if (owner >= 0 && gl == 0) out[owner] = mx / T.eta + log(sm) / T.eta;
   }
   __syncwarp();
 }
@@ -1383,7 +1428,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   unsigned long long n_act = 0, n_bel = 0, n_psi = 0, n_cdf = 0, n_ovf = 0;
   VP_BK_INIT();
   VP_WAVE_DECL();
-  if (lane == 0) VP_WAVE(pass, 255);
+  if (lane == 0) VP_WAVE(pass, 63);
   while (__any_sync(FULL, live)) {
     VP_BK(0);
     int ready = -1, nx = -1, npb = -1, nact = 0;
@@ -1553,7 +1598,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
             dm->pass = pass;
             ++n_cdf;
           }
-        VP_WAVE(pass, min(T.b_depth[ready], 64));
+        VP_WAVE(pass, min(T.b_depth[ready], 62));
         T.b_lse[ready] = V;
         T.b_flags[ready] = 0u;
         T.b_rows[ready] = 0;

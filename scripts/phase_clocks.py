@@ -44,14 +44,21 @@ vp.plan(belief, model, cfg, vp.RowRng.from_seed(1000).derive(1, 99))
 torch.cuda.synchronize()
 cnt = lib.vp_debug_trace(buf_t, 1 << 21)
 tr = np.frombuffer(buf_t, dtype=np.uint64, count=cnt)
-t = (tr >> np.uint64(16)).astype(np.int64)
-ps = ((tr >> np.uint64(8)) & np.uint64(255)).astype(np.int64)
-dp = (tr & np.uint64(255)).astype(np.int64)
+t = (tr >> np.uint64(24)).astype(np.int64)
+ps = ((tr >> np.uint64(18)) & np.uint64(63)).astype(np.int64)
+dp = ((tr >> np.uint64(12)) & np.uint64(63)).astype(np.int64)
+wp = (tr & np.uint64(4095)).astype(np.int64)
 for p in sorted(set(ps.tolist())):
     m = ps == p
-    t0 = t[m & (dp == 255)].min()
+    t0 = t[m & (dp == 63)].min()
     parts = []
-    for d in sorted(set(dp[m].tolist()) - {255}):
+    for d in sorted(set(dp[m].tolist()) - {63}):
         x = (t[m & (dp == d)] - t0) / 1e3
         parts.append(f"d{d}:{np.percentile(x, 50):.1f}/{np.percentile(x, 90):.1f}/{x.max():.1f}(n={len(x)})")
     print(f"  backup pass {p} completion us p50/p90/max after the first warp:", " ".join(parts))
+    if p == max(ps.tolist()):  # the last pass: the critical path's warps
+        sel = np.flatnonzero(m & (dp != 63))
+        late = sel[np.argsort(t[sel])[-40:]]
+        print("   last completions (us, depth, warp):", [(round((t[i] - t0) / 1e3, 1), int(dp[i]), int(wp[i])) for i in late])
+        starts = {int(wp[i]): round((t[i] - t0) / 1e3, 1) for i in np.flatnonzero(m & (dp == 63))}
+        print("   those warps started at:", {w: starts.get(w) for w in sorted(set(int(wp[i]) for i in late))})
