@@ -588,6 +588,26 @@ __device__ void build_cdf_row(const PsiT* row, PsiT* cdf, int A, double eta, dou
   const PsiT e2 = (PsiT)(eta * kLog2eD), sh2 = (PsiT)(eta * lse * kLog2eD);
   const int C = (A + 31) >> 5;
   const int lo = lane_id() * C, hi = min(A, lo + C);
+  constexpr int R = 16;
+  if (C <= R) {  // |A| <= 512: the lane's chunk in registers, all its loads in flight at once
+    PsiT v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = lo + j < hi ? ldp<L2>(row + lo + j) : (PsiT)0;
+    PsiT loc = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      loc += lo + j < hi ? fexp2(ffma(e2, v[j], -sh2)) : (PsiT)0;
+      v[j] = loc;
+    }
+    const PsiT incl = warp_inclusive_scan(loc);
+    const PsiT up = __shfl_up_sync(FULL, incl, 1);
+    const PsiT excl = lane_id() ? up : (PsiT)0;
+    const PsiT scale = (PsiT)1 / __shfl_sync(FULL, incl, 31);
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (lo + j < hi) cdf[lo + j] = (v[j] + excl) * scale;
+    return;
+  }
   PsiT loc = 0;
   for (int c = lo; c < hi; ++c) loc += fexp2(ffma(e2, ldp<L2>(row + c), -sh2));
   const PsiT incl = warp_inclusive_scan(loc);
