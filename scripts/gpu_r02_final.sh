@@ -13,3 +13,6 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r02_bench.csv \
     python bench.py --steps 2 --warmup 1 --no-secondary --no-cpu-baseline --episodes 0 > gpurun_out/ncu_bench.log 2>&1
 echo "ncu bench rc=$?"
+timeout 500 python scripts/shard_phases.py > gpurun_out/shard_c2.json 2> gpurun_out/shard_c2.err
+timeout 600 python scripts/shard_phases.py --board 15 --rows-per-gpu 65536 > gpurun_out/shard_c3.json 2> gpurun_out/shard_c3.err
+echo "shard rc=$?"
