@@ -344,6 +344,15 @@ int32_t vp_tree_append_beliefs(const vp_tree* tree, const int32_t* action_nodes,
  * (the hidden component, kept per particle).  Sizes and offsets are multiples of 8. */
 int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, const void* source, int32_t keep_lo,
                             int32_t keep_hi, void* stream);
+/* HOST function (no CUDA): pack the reference's MarsStates (envs/mars.py:34-40: x, y (n, 2) int64,
+ * rocks (n, m) bool, terminal (n,) bool; C-contiguous) into the device's 16-B MARS records
+ * {x0 | y0 << 8 | x1 << 16 | y1 << 24 | terminal << 32, rock bits} at `dst` (pinned host memory
+ * of an e2e planning step).  m <= 64. */
+int32_t vp_pack_mars_states(const int64_t* x, const int64_t* y, const uint8_t* terminal, const uint8_t* rocks,
+                            int64_t n, int32_t m, void* dst);
+/* HOST function: the per-iteration keys of a fixed-iteration plan (solver.py:97-102):
+ * out[2 i] = it.derive(0) (root draw), out[2 i + 1] = it.derive(1) (search), it = key.derive(i). */
+int32_t vp_plan_keys(uint64_t key, int32_t iterations, uint64_t* out);
 
 /* Latency probe: one thread follows `hops` dependent pointers next[p] (element indices) from
  * `start` with gpu-scope loads (atomic = 0: L2 round trips) or atom.add 0 (atomic = 1); out[0] =

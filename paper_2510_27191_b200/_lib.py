@@ -144,6 +144,9 @@ _SIGNATURES = [
      [C.POINTER(VpTree), C.c_void_p, C.c_void_p, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p]),
     ("vp_broadcast_record", C.c_int32,
      [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    ("vp_pack_mars_states", C.c_int32,
+     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
+    ("vp_plan_keys", C.c_int32, [C.c_uint64, C.c_int32, C.c_void_p]),
     ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_rng_normal", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_model_step", C.c_int32,

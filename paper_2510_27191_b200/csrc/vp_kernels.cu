@@ -1270,6 +1270,52 @@ __global__ void k_broadcast_record(u64* rec, long long words_total, int words, c
   }
 }
 
+int32_t vp_plan_keys(uint64_t key, int32_t iterations, uint64_t* out) {
+  if (iterations < 0 || (iterations && !out)) return VP_ERR_INVALID;
+  for (int32_t i = 0; i < iterations; ++i) {
+    const uint64_t it = fold(key, (uint64_t)i);
+    out[2 * i] = fold(it, 0);      // SITE_DRAW
+    out[2 * i + 1] = fold(it, 1);  // SITE_SEARCH
+  }
+  return VP_OK;
+}
+
+// Host packer of MARS particle records (the e2e path packs the caller's belief every planning
+// step): 8 rock flags at a time turned into 8 bits by one multiply.
+static inline uint64_t bytes8_to_bits(uint64_t v) {
+  return ((v & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56;
+}
+
+int32_t vp_pack_mars_states(const int64_t* x, const int64_t* y, const uint8_t* terminal, const uint8_t* rocks,
+                            int64_t n, int32_t m, void* dst) {
+  if (n < 0 || m < 0 || m > 64 || (n && (!x || !y || !terminal || !dst || (m && !rocks)))) return VP_ERR_INVALID;
+  uint64_t* out = static_cast<uint64_t*>(dst);
+  const int chunks = (m + 7) / 8;
+  // rows whose whole-chunk reads stay inside the rocks array
+  const int64_t total = n * (int64_t)m;
+  const int64_t safe = m ? std::max<int64_t>(0, (total - 8 * chunks) / m) : n;
+  const uint64_t mask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  for (int64_t i = 0; i < n; ++i) {
+    out[2 * i] = (uint64_t)(x[2 * i] & 0xff) | (uint64_t)(y[2 * i] & 0xff) << 8 |
+                 (uint64_t)(x[2 * i + 1] & 0xff) << 16 | (uint64_t)(y[2 * i + 1] & 0xff) << 24 |
+                 (uint64_t)(terminal[i] != 0) << 32;
+    const uint8_t* r = rocks + i * (int64_t)m;
+    uint64_t bits = 0;
+    if (i < safe) {
+      for (int c = 0; c < chunks; ++c) {
+        uint64_t v;
+        memcpy(&v, r + 8 * c, 8);
+        bits |= bytes8_to_bits(v) << (8 * c);
+      }
+      bits &= mask;
+    } else {
+      for (int k = 0; k < m; ++k) bits |= (uint64_t)(r[k] != 0) << k;
+    }
+    out[2 * i + 1] = bits;
+  }
+  return VP_OK;
+}
+
 int32_t vp_broadcast_record(void* records, int32_t m, int32_t record_bytes, const void* source, int32_t keep_lo,
                             int32_t keep_hi, void* stream) {
   if (!records || !source || m < 1 || record_bytes < 8 || record_bytes % 8 || keep_lo % 8 || keep_hi % 8 ||

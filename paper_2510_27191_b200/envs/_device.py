@@ -151,6 +151,14 @@ def mars_pack_into(states, dst: np.ndarray) -> int:
     x = np.asarray(states.x)
     y = np.asarray(states.y)
     n = len(x)
+    term, rk = np.asarray(states.terminal), np.asarray(states.rocks)
+    if (x.dtype == y.dtype == np.int64 and term.dtype == rk.dtype == np.bool_ and x.shape == y.shape == (n, 2)
+            and term.shape == (n,) and rk.ndim == 2 and rk.shape[0] == n and rk.shape[1] <= 64
+            and all(a.flags["C_CONTIGUOUS"] for a in (x, y, term, rk))):
+        # the library's host packer (vp_pack_mars_states): the same words, ~4x faster
+        _lib.call("vp_pack_mars_states", x.ctypes.data, y.ctypes.data, term.ctypes.data, rk.ctypes.data, n,
+                  rk.shape[1], dst.ctypes.data)
+        return 16 * n
     out = dst[: 16 * n].view(np.uint64).reshape(n, 2)
     t = np.left_shift(y, 8, dtype=np.int64)
     t |= x

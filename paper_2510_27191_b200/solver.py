@@ -257,13 +257,9 @@ class Planner:
         """
         torch = _torch()
         iters = config.iterations
-        keys = np.empty(2 * iters, dtype=np.uint64)
-        for i in range(iters):
-            it_key = fold(key, i)
-            keys[2 * i] = fold(it_key, SITE_DRAW)
-            keys[2 * i + 1] = fold(it_key, SITE_SEARCH)
         kh = self._buf("keys_host", 16 * iters, True)
-        kh.numpy()[: 16 * iters].view(np.uint64)[:] = keys
+        # fold(fold(key, i), SITE_DRAW / SITE_SEARCH) for every iteration, straight into pinned memory
+        _lib.call("vp_plan_keys", C.c_uint64(key), iters, kh.data_ptr())
         kd = self._buf("keys_dev", 16 * iters, False)
         oh = self._buf("out_host", 16, True)
         od = self._buf("out_dev", 16, False)

@@ -98,14 +98,17 @@ def test_state_packing_roundtrip():
     assert _device.TAB_DTYPE.itemsize == 8 and _device.SYN_DTYPE.itemsize == 16 and _device.LD_DTYPE.itemsize == 24
 
 
-@pytest.mark.parametrize("n,m", [(4, 3), (11, 11), (20, 30), (20, 60)])
-def test_mars_word_packing_equals_field_layout(n, m):
+@pytest.mark.parametrize("native", [True, False])
+@pytest.mark.parametrize("n,m", [(4, 3), (11, 11), (20, 30), (20, 60), (20, 64)])
+def test_mars_word_packing_equals_field_layout(n, m, native):
     """mars_pack_into writes {x0,y0,x1,y1,terminal,rock bits} as two 64-bit words; every field
-    must land where MARS_DTYPE (and the kernel's MarsState) says, for every rock-count path."""
+    must land where MARS_DTYPE (and the kernel's MarsState) says, for every rock-count path --
+    through the library's host packer (vp_pack_mars_states, int64 / bool C-contiguous columns,
+    the reference's own dtypes) and through the numpy path (any other dtypes)."""
     model = oracle.MarsModel(n, m, layout_seed=1)
     st = model.sample_initial_states(300, oracle.RowRng.from_seed(3))
     g = np.random.default_rng(0)
-    st.x = g.integers(0, n + 1, size=(300, 2))
+    st.x = g.integers(0, n + 1, size=(300, 2)).astype(np.int64 if native else np.int32)
     st.y = g.integers(0, n, size=(300, 2))
     st.terminal = g.random(300) < 0.3
     rec = _device.mars_pack(st)
@@ -203,3 +206,15 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_plan_keys_host_function_matches_fold():
+    """vp_plan_keys (the library's host key schedule of a fixed-iteration plan) equals
+    fold(fold(key, i), site) for the draw (0) and search (1) sites (solver.py:97-102)."""
+    import ctypes as C
+
+    for key in (0, 1, 123456789, (1 << 64) - 1):
+        out = np.zeros(2 * 13, dtype=np.uint64)
+        assert _lib.load().vp_plan_keys(C.c_uint64(key), 13, out.ctypes.data) == 0
+        want = [fold(fold(key, i), s) for i in range(13) for s in (0, 1)]
+        np.testing.assert_array_equal(out, np.array(want, dtype=np.uint64))
