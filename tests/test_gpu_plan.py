@@ -179,6 +179,33 @@ def test_capacity_growth_matches_preallocated():
     assert out.tree.cap_beliefs >= len(got["depth"])
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fast_mode_growth_of_nodes_and_dense_pool_matches_graph_plan(precision):
+    """Fast mode through the growing path (capacity forced small: node columns regrown and
+    rehashed with static-id holes, the dense PSI pool grown on demand) equals the one-graph fixed
+    plan of the same key: the same structure bit for bit, PSI up to the arrival order of the fp64
+    L2 reductions (an ulp)."""
+    case = manifest()["plans"]["plan_mars7_8_small"]
+    s = case["runs"][0]["seed"]
+    om, belief, cfg, rng = plan_inputs(case, s)
+    base = vp.Planner(precision).plan(belief, om, cfg, rng, keep_tree=True)
+    planner = vp.Planner(precision)
+    planner._capacity = lambda n, config, A: (64, config.iterations)
+    orig = vp.DeviceTree.dense_rows_for
+    vp.DeviceTree.dense_rows_for = lambda self, cb, ca: 2  # a two-row pool: grown on demand
+    try:
+        out = planner.plan(belief, om, cfg, rng, keep_tree=True, trace=True)  # trace: the growing path
+    finally:
+        vp.DeviceTree.dense_rows_for = orig
+    assert out.tree.cap_dense > 2 and out.tree.n_dense() > 2
+    assert out.tree_stats == base.tree_stats and out.chosen_action == base.chosen_action
+    got, want = out.tree.tables(), base.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    np.testing.assert_allclose(got["prefs"], want["prefs"], rtol=1e-12, atol=1e-12)
+    out.tree.validate()
+
+
 def test_search_backup_api_from_interior_frontier():
     """Reference API: search from depth-1 beliefs, then backup to the root."""
     om = oracle.MarsModel(4, 3, layout_seed=0)
