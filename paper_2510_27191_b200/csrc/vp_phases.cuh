@@ -1565,11 +1565,15 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         const double li = eta * (double)(PsiT)T.init_prefs[0];
         const int rest = T.action_count - filled;
         if (ovl && rest > 0) m = fmax(m, li);
+        // fp32 storage: the terms lie in (0, 1] and the sum in [1, |A| + 4], so fp32 exp / log
+        // (MUFU) give the LSE to ~1e-7 of its scale -- inside the 1e-5 scale-aware contract
+        // and at the accuracy of the stored cells themselves; fp64 storage keeps fp64 math
+        constexpr bool kF32 = sizeof(PsiT) == 4;
         auto term = [&](bool use, double x) -> double {  // exp(x - m) for the lanes that use it
           const bool need = use && x != m;
           double t = use ? 1.0 : 0.0;
           if (__any_sync(FULL, need)) {
-            const double e = exp(x - m);
+            const double e = kF32 ? (double)__expf((float)(x - m)) : exp(x - m);
             if (need) t = e;
           }
           return t;
@@ -1578,7 +1582,7 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
 #pragma unroll
         for (int k = 0; k < kOverlay; ++k) sum += term(lk[k] > -INFINITY, lk[k]);
         if (ovl) {
-          V = (m + log(sum)) / eta;
+          V = (m + (kF32 ? (double)__logf((float)sum) : log(sum))) / eta;
           full = false;
         } else if (fresh && prow >= 0) {
           // dense row: 1 + sum_changed (new - old) relative to its exact (fp64-maintained) LSE.
