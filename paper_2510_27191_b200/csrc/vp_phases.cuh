@@ -1489,7 +1489,11 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
           // last child: Q (backup.py:96-104) and PSI[b, a] += Q - LSE_pre(b) (:106-108)
           ++n_act;
           T.a_rows[x] = 0;
-          const double q = rew / (double)vis + (gamma * aa.sum) / (double)aa.cnt;
+          // fp32 storage: Q enters a cell rounded to fp32 anyway -- fp32 reciprocals (MUFU) suffice
+          const double q = sizeof(PsiT) == 4 && !Exact
+                               ? (double)__fdividef((float)rew, (float)vis) +
+                                     (double)__fdividef((float)(gamma * aa.sum), (float)aa.cnt)
+                               : rew / (double)vis + (gamma * aa.sum) / (double)aa.cnt;
           double term = 0.0;
           if constexpr (Exact) {
             *cell = (PsiT)(old_v + (q - lse_pre));
