@@ -58,10 +58,11 @@ __device__ __forceinline__ double normal_j(u64 key, u64 row, u64 j) {
 // ---------------------------------------------------------------- hashing
 
 // 16-byte slot of an open-addressing index.  Empty slots are all-ones (one
-// memset).  A claim is ONE 128-bit CAS {empty, unpublished} -> {key,
-// unpublished}: the winner numbers the node and publishes {id, pass} with a
-// 64-bit store; a loser gets the whole slot back from the failed CAS, so a
-// hit on a published node costs one L2 round trip.
+// memset).  A claim is ONE 128-bit CAS on an empty slot: the search inserts
+// {key, pass | id} at once (its ids are static, known before the claim); the
+// host-level append kernels insert {key, unpublished}, number the node and
+// publish {id, pass} with a 64-bit store.  A loser gets the whole slot back
+// from the failed CAS, so a hit costs one L2 round trip.
 struct __align__(16) Slot {
   u64 key;
   u32 id;    // node id, kUnpublished while the winner is still numbering it

@@ -1,25 +1,26 @@
 // vp_phases.cuh -- device code of one PORPP planning pass (sm_100a).
 //
-// A pass is TWO kernels and no grid barrier:
+// A pass is three kernels and no grid barrier:
 //
 //   search  (search.py:86-119)  each warp carries its 32 rows through every
-//           level: softmax draw from the belief's PSI row (TMA-staged into
-//           shared memory), G(s,a) in registers, the (b,a) and (a,o) hash
-//           claims (one 128-bit CAS each), reward / visit / row-count
-//           reductions -- then the leaf heuristic.  Ids come from one atomic
-//           per warp, so a row never waits for rows of other warps except for
-//           the few cycles between a creator's CAS and its publish.
+//           level: softmax draw (the shared initial CDF, an overlay record's
+//           corrected CDF, or a dense row's CDF row TMA-staged into shared
+//           memory), G(s,a) in registers, the (b,a) and (b,a,o) hash claims --
+//           one 128-bit CAS each, issued together, inserting the creator's
+//           static id -- and reward / visit / row-count reductions; then the
+//           leaf heuristic.  A row never waits for rows of other warps.
 //   backup  (backup.py:75-114)  a bottom-up completion wave: every distinct
 //           leaf delivers (V, N) to its parent action; the delivery that
 //           brings an action's delivered-row count to its row count completes
-//           the action (Q, PSI scatter), and the action completion that does
-//           the same for its belief completes the belief (LSE over the row,
-//           computed by the warp) and delivers it upward.
+//           the action (Q, PSI update), and the action completion that does
+//           the same for its belief completes the belief (LSE_post without
+//           reading the row, save ill-conditioned dense rows) and climbs on.
+//   cdf rows  the dense rows the backup changed get their softmax CDF rows.
 //
-// Node ids are therefore assigned in completion order.  Each node stores the
-// key (pass, level, first row) under which the reference would have created
-// it; the host sorts by it when exporting, which reproduces the reference's
-// first-occurrence numbering (tree.py:10-12) exactly.
+// Node ids are static: row r creating at level l takes id extent + l n + r.
+// Each node stores the key (pass, level, first row) under which the reference
+// would have created it; the host sorts by it when exporting, which
+// reproduces the reference's first-occurrence numbering (tree.py:10-12).
 #pragma once
 
 #include <type_traits>
@@ -739,31 +740,6 @@ __device__ __noinline__ void materialise_dense(const vp_tree& T, unsigned long l
   g->dense_row = (u32)r;
   g->dense_pass = pass;
   if (stats) atomicAdd(&stats[10], 1ull);
-}
-
-// Numbered-node allocation for the winners of a warp: one atomic per warp.
-__device__ __forceinline__ int warp_alloc(int* counter, bool won) {
-  const u32 winners = __ballot_sync(FULL, won);
-  if (!winners) return 0;
-  const int first = __ffs(winners) - 1;
-  int base = 0;
-  if (lane_id() == first) base = atomicAdd(counter, __popc(winners));
-  base = __shfl_sync(FULL, base, first);
-  return base + __popc(winners & ((1u << lane_id()) - 1u));
-}
-
-// Two tables' allocations of a warp with both atomics in flight together.
-__device__ __forceinline__ void warp_alloc2(int* ca, bool wa, int* cb, bool wb, int& ida, int& idb) {
-  const u32 ma = __ballot_sync(FULL, wa), mb = __ballot_sync(FULL, wb);
-  const int fa = ma ? __ffs(ma) - 1 : 0, fb = mb ? __ffs(mb) - 1 : 0;
-  int ba = 0, bb = 0;
-  if (ma && lane_id() == fa) ba = atomicAdd(ca, __popc(ma));
-  if (mb && lane_id() == fb) bb = atomicAdd(cb, __popc(mb));
-  ba = __shfl_sync(FULL, ba, fa);
-  bb = __shfl_sync(FULL, bb, fb);
-  const u32 below = (1u << lane_id()) - 1u;
-  ida = ba + __popc(ma & below);
-  idb = bb + __popc(mb & below);
 }
 
 // ------------------------------------------------------------------ tree init (one block)

@@ -165,6 +165,7 @@ class DeviceTree:
         s.cap_dense = cap_d
         s.overlay_slots = self.overlay_slots
         s.bkey_mode = getattr(self, "bkey_mode", 0)
+        s.init_uniform = getattr(self, "_init_uniform", 0)  # (a regrown arena keeps it)
         s.counters = self._counters.data_ptr()
         s.init_prefs = self._init_prefs.data_ptr()
         s.init_lse = self._init_lse.data_ptr()
@@ -208,7 +209,7 @@ class DeviceTree:
         if getattr(self, "init_prefs", None) is None or not np.array_equal(self.init_prefs, base):
             self._init_prefs.copy_(torch.from_numpy(base))
         self.init_prefs = base
-        self.struct.init_uniform = int(bool(np.all(base == base[0])))
+        self._init_uniform = self.struct.init_uniform = int(bool(np.all(base == base[0])))
         self.generation += 1
         self.pass_cursor = 0
         self._canon_cache = None
