@@ -317,7 +317,9 @@ class Planner:
                 nb, na = tree.extent()
                 ub_b, ub_a = nb, na
                 need_b, need_a = nb + n * d_max, na + n * d_max
-                if done and (need_b > tree.cap_beliefs or need_a > tree.cap_actions):
+                if not done or not (need_b > tree.cap_beliefs or need_a > tree.cap_actions):
+                    tree.ensure_capacity(need_b, need_a, limit=total)
+                else:
                     # growth allocates the doubled arena beside the old one: stop deepening when
                     # it would not fit in HBM (a memory-bounded budget; the reference would
                     # exhaust host memory the same way, only later)
@@ -326,14 +328,21 @@ class Planner:
                         grown *= 2
                     if total is not None:
                         grown = max(min(grown, total), need_b, need_a)
-                    if grown > self.node_budget(tree.action_count, fraction=0.85, dense=tree.exact):
+                    budget = self.node_budget(tree.action_count, fraction=0.85, dense=tree.exact)
+                    if grown > budget:
+                        # near the memory bound: grow by what the next few iterations need
+                        # rather than doubling (deeper trees before the bound)
+                        grown = max(need_b, need_a) + 4 * n * min(d_max + 4, config.d_max_cap)
+                        if total is not None:
+                            grown = min(grown, total)
+                    if grown > budget:
                         if config.iterations is not None:  # the reference always runs `iterations`
                             raise _lib.CapacityError(
                                 f"a {config.iterations}-iteration plan does not fit in HBM after "
                                 f"{done} iterations ({nb} beliefs, {na} actions)")
                         stopped = "memory"
                         break
-                tree.ensure_capacity(need_b, need_a, limit=total)
+                    tree.ensure_capacity(need_b, need_a, limit=grown)
             if not tree.exact and ub_d + n * d_max > tree.cap_dense:
                 ub_d = tree.n_dense()
                 need_d = ub_d + n * d_max
