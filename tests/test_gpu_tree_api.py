@@ -105,3 +105,38 @@ def test_aggregate_leaves_and_q_values_equal_oracle():
     np.testing.assert_allclose(qd, qo, rtol=1e-13, atol=1e-13)
     with pytest.raises(ValueError):
         vp.action_q_values(dt, [0], ld, 0.95)  # the root's first action has no valued child here
+
+
+def _dense_cdf_errors(tree, eta):
+    """Max |psi_cdf - normalised cumsum(softmax(eta psi))| over every dense row of a fast-mode tree,
+    with the cached LSE of the row's belief (what the next pass's draws read)."""
+    import torch
+
+    nb = tree.extent()[0]
+    rec = tree.b_rec[:nb]
+    dense = torch.nonzero(rec[:, 0] != 0).squeeze(1)
+    rows = rec[dense, 1].to(torch.int64)
+    A = tree.action_count
+    psi = tree.psi[rows, :A].double()
+    lse = tree.b_lse[dense]
+    p = torch.exp(eta * (psi - lse[:, None]))
+    want = torch.cumsum(p, dim=1) / p.sum(dim=1, keepdim=True)
+    got = tree.psi_cdf[rows, :A].double()
+    return len(rows), float((got - want).abs().max()) if len(rows) else 0.0
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_dense_rows_cdf_rows_are_current(precision):
+    """After a fast-mode plan every dense PSI row's CDF row (rebuilt by the CDF kernel after each
+    backup that changed the row) is the softmax CDF of the row under its cached LSE; after
+    deserialize / append_actions (host-level edits) vp_tree_build_cdfs makes them so."""
+    model = vp.MarsModel(7, 8, layout_seed=1)
+    belief = vp.ParticleBelief.from_model(model, 500, vp.RowRng.from_seed(1).derive(3))
+    out = vp.plan(belief, model, vp.SolverConfig(n_parallel=2048, iterations=6), vp.RowRng.from_seed(1),
+                  precision=precision, keep_tree=True)
+    n, err = _dense_cdf_errors(out.tree, 2.0)
+    assert n > 10
+    assert err < (1e-5 if precision == "fp32" else 1e-12), err
+    back = vp.DeviceTree.deserialize(out.tree.serialize(), precision=precision)
+    n2, err2 = _dense_cdf_errors(back, back.eta)
+    assert n2 == len(back.tables()["depth"]) and err2 < (1e-5 if precision == "fp32" else 1e-12), err2
