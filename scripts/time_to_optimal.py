@@ -30,13 +30,14 @@ ap.add_argument("--budgets", default="0.001,0.003,0.01,0.03,0.1")
 ap.add_argument("--n", type=int, default=11)
 ap.add_argument("--m", type=int, default=11)
 ap.add_argument("--n-parallel", type=int, default=16_384)
+ap.add_argument("--problem", default="mars", choices=["mars", "navigation", "tiger", "lightdark"])
 ap.add_argument("--out", default=None)
 ap.add_argument("--cpu-runs", type=int, default=0,
                 help="also run the CPU reference algorithm (oracle/ port) at its smallest budget")
 a = ap.parse_args()
 rows = []
 for b in [float(x) for x in a.budgets.split(",")]:
-    cfg = CampaignConfig(problem="mars", problem_params={"n": a.n, "m": a.m},
+    cfg = CampaignConfig(problem=a.problem, problem_params={"n": a.n, "m": a.m} if a.problem == "mars" else {},
                          solver=SolverConfig(n_parallel=a.n_parallel, planning_seconds=b), runs=a.runs)
     t0 = time.perf_counter()
     recs, summ = run_campaign(cfg)
@@ -45,18 +46,18 @@ for b in [float(x) for x in a.budgets.split(",")]:
            "mean_steps": round(summ["metrics"]["steps"]["mean"], 2),
            "mean_plan_seconds": round(summ["metrics"]["plan_seconds"]["mean"], 5),
            "campaign_wall_s": round(time.perf_counter() - t0, 1)}
-    if b in PAPER and (a.n, a.m) == (20, 20):
+    if b in PAPER and (a.n, a.m) == (20, 20) and a.problem == "mars":
         row["paper_laptop_gpu"] = {"mean_return": PAPER[b][0], "ci95": PAPER[b][1]}
     rows.append(row)
     print(json.dumps(row), flush=True)
 best = max(rows, key=lambda r: r["mean_return"])
 near = min((r for r in rows if r["mean_return"] >= best["mean_return"] - best["ci95"]),
            key=lambda r: r["planning_seconds"])
-res = {"problem": f"MARS({a.n},{a.m})", "n_parallel": a.n_parallel, "eta": 2.0, "budgets": rows,
+res = {"problem": f"MARS({a.n},{a.m})" if a.problem == "mars" else a.problem, "n_parallel": a.n_parallel, "eta": 2.0, "budgets": rows,
        "time_to_near_optimal_s": near["planning_seconds"],
        "definition": "smallest planning_seconds whose mean return lies within the 95% CI of the best mean (SURVEY 8d)",
        "runs_per_budget": a.runs}
-if a.cpu_runs:
+if a.cpu_runs and a.problem == "mars":
     # the reference always completes its first iteration (solver.py:106-110), so on the CPU the
     # smallest achievable planning step is one iteration of n_parallel rows
     import oracle  # CPU baseline only
