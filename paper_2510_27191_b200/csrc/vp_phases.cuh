@@ -1194,6 +1194,28 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       pend_mat_prev = pend_mat;
       pend_mat = -1;
     }
+    // (belief, action, obs) keys: the child is known now -- resolve it and start loading its
+    // record and LSE, so the action's bookkeeping below hides the load
+    int c = 0;
+    u32 cpass = 0;
+    bool c_new = false, led_b = false;
+    Rec<PsiT> rec_n{};
+    double lse_n = lse_init;
+    if (early) {
+      if (lead_b) {
+        const u64 w = wait_published(hb, cl_b.slot, cl_b.word);
+        c = (int)(u32)w;
+        cpass = (u32)(w >> 32);
+      }
+      c = __shfl_sync(FULL, c, leader_b);
+      c_new = __shfl_sync(FULL, cpass, leader_b) == pass;
+      led_b = __shfl_sync(FULL, (int)lead_b, leader_b) != 0;
+      if constexpr (!Exact)
+        if (ok && led_b && !c_new) {
+          rec_n = load_rec<PsiT>(T, c);
+          lse_n = T.b_lse[c];
+        }
+    }
     int x = 0;
     if (lead_a) {
       const u64 w = wait_published(ha, cl_a.slot, cl_a.word);  // (append kernels publish late)
@@ -1240,14 +1262,13 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     VP_PH(4);
     grp = grp_b;
     lead = lead_b;
-    int c = 0;
-    bool c_new = false;
     {
-      u32 cpass = 0;
       if (lead_b) {
-        const u64 w = wait_published(hb, cl_b.slot, cl_b.word);
-        c = (int)(u32)w;
-        cpass = (u32)(w >> 32);
+        if (!early) {
+          const u64 w = wait_published(hb, cl_b.slot, cl_b.word);
+          c = (int)(u32)w;
+          cpass = (u32)(w >> 32);
+        }
         if (cpass == pass) red_min(&T.b_ckey[c], creation_key(pass, l, rg));
       }
       if (cl_b.won) {
@@ -1261,15 +1282,17 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
         T.b_flags[c] = interior_next ? 1u : 3u;
         ++won_b;
       }
-      c = __shfl_sync(FULL, c, leader_b);
-      c_new = __shfl_sync(FULL, cpass, leader_b) == pass;
+      if (!early) {
+        c = __shfl_sync(FULL, c, leader_b);
+        c_new = __shfl_sync(FULL, cpass, leader_b) == pass;
+      }
       made_interior = cl_b.won && interior_next;
       if (W.stats) {
         const u32 wn = __ballot_sync(FULL, cl_b.won);
         if (lane == 0 && wn) atomicAdd(&W.stats[6], (unsigned long long)__popc(wn));
       }
     }
-    const bool led_b = __shfl_sync(FULL, (int)lead_b, leader_b) != 0;
+    if (!early) led_b = __shfl_sync(FULL, (int)lead_b, leader_b) != 0;
     ok = ok && led_b;
     VP_PH(5);
     arrive(T, W, leaf_count, c, grp, lead && ok, !interior_next);
@@ -1286,6 +1309,9 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (c_new || !ok) {  // created this pass: the initial row
         rec = Rec<PsiT>{};
         lse = lse_init;
+      } else if (early) {  // loaded during this level's bookkeeping
+        rec = rec_n;
+        lse = lse_n;
       } else {
         rec = load_rec<PsiT>(T, c);
         lse = T.b_lse[c];
