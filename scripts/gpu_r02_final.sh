@@ -16,3 +16,5 @@ echo "ncu bench rc=$?"
 timeout 500 python scripts/shard_phases.py > gpurun_out/shard_c2.json 2> gpurun_out/shard_c2.err
 timeout 600 python scripts/shard_phases.py --board 15 --rows-per-gpu 65536 > gpurun_out/shard_c3.json 2> gpurun_out/shard_c3.err
 echo "shard rc=$?"
+timeout 300 python scripts/crowdnav_step.py > gpurun_out/crowdnav_step.json 2> gpurun_out/crowdnav_step.err
+echo "crowdnav rc=$?"
