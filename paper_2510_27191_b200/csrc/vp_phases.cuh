@@ -1454,6 +1454,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
   while (__any_sync(FULL, live)) {
     VP_BK(0);
     int ready = -1, nx = -1, npb = -1, nact = 0;
+#ifdef VP_PHASE_CLOCKS
+    int bdel_pb = -1;
+#endif
     int prow = -1;  // the PSI row of a completed belief's full-row fallback (-1: overlay row)
     u32 slotbit = 0, bmask = 0;  // overlay slot this lane's action changed / all changed slots
     Rec<PsiT> prec{};            // fast mode: the parent belief's overlay record
@@ -1531,6 +1534,9 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
             }
           }
           // N(b) = lifetime visits of the valued actions (backup.py:110-114)
+#ifdef VP_PHASE_CLOCKS
+          if ((u32)tot != btot) bdel_pb = pb;
+#endif
           Acc ba;
           const bool done = slotbit ? acc_deliver_log(T.b_acc, pb, term, (u32)tot | slotbit, (u32)vis, btot, ba)
                             : prow >= 0 ? acc_deliver<true>(T.b_acc, pb, term, (u32)tot, (u32)vis, btot, ba)
@@ -1544,6 +1550,17 @@ __device__ void backup_warp(const vp_tree& T, const vp_work& W, u32 pass, double
         }
       }
     }
+#ifdef VP_PHASE_CLOCKS
+    {  // how many multi-delivery belief deliveries of this iteration share their belief in the warp
+      const u32 g_ = __match_any_sync(FULL, bdel_pb);
+      const bool d_ = bdel_pb >= 0, l_ = d_ && lane == __ffs(g_) - 1;
+      const u32 nd_ = __popc(__ballot_sync(FULL, d_)), ng_ = __popc(__ballot_sync(FULL, l_));
+      if (lane == 0 && nd_) {
+        atomicAdd(&g_phase_cycles[20], (unsigned long long)nd_);
+        atomicAdd(&g_phase_cycles[21], (unsigned long long)ng_);
+      }
+    }
+#endif
     VP_BK(1);
     if (__any_sync(FULL, ready >= 0)) {
       // last action of a belief: V = LSE_post (backup.py:109), cached as the next LSE_pre.

@@ -62,3 +62,4 @@ for p in sorted(set(ps.tolist())):
         print("   last completions (us, depth, warp):", [(round((t[i] - t0) / 1e3, 1), int(dp[i]), int(wp[i])) for i in late])
         starts = {int(wp[i]): round((t[i] - t0) / 1e3, 1) for i in np.flatnonzero(m & (dp == 63))}
         print("   those warps started at:", {w: starts.get(w) for w in sorted(set(int(wp[i]) for i in late))})
+print(f"  backup multi-delivery belief deliveries: {buf[20]}, distinct (warp, iteration, belief) groups: {buf[21]}")
