@@ -248,5 +248,27 @@ def check(status: int, what: str = ""):
     raise RuntimeError(msg)
 
 
+_FNS: dict = {}
+
+
 def call(name: str, *args):
-    check(getattr(load(), name)(*args), name)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(load(), name)
+    check(fn(*args), name)
+
+
+_CUDA_OK = False
+
+
+def torch_cuda():
+    """torch, once a CUDA device is known to be present (checked until it is: the product path
+    raises rather than fall back to the CPU)."""
+    global _CUDA_OK
+    import torch
+
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        _CUDA_OK = True
+    return torch

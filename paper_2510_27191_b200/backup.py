@@ -20,11 +20,7 @@ from . import _lib
 
 
 def _torch():
-    import torch
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
-    return torch
+    return _lib.torch_cuda()
 
 
 def run_backup(tree, work, pass_: int, gamma: float):

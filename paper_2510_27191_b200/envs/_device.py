@@ -41,11 +41,7 @@ CROWD_DTYPE = np.dtype([("robot", "<f8", (2,)), ("prev", "<f8", (8,)), ("code", 
 
 
 def _torch():
-    import torch
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
-    return torch
+    return _lib.torch_cuda()
 
 
 class DeviceModel:

@@ -23,11 +23,7 @@ SITE_MODEL = 1
 
 
 def _torch():
-    import torch
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
-    return torch
+    return _lib.torch_cuda()
 
 
 class Workspace:

@@ -29,14 +29,11 @@ from .tree import DeviceTree, TreeHandle
 
 NS_ENV, NS_PLAN, NS_SIR, NS_INIT_BELIEF = 0, 1, 2, 3
 SITE_DRAW, SITE_SEARCH = 0, 1
+_BKEY_MODE_MAX = int(os.environ.get("VP_BKEY_MODE", "1"))  # measurement only
 
 
 def _torch():
-    import torch
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
-    return torch
+    return _lib.torch_cuda()
 
 
 @dataclass(frozen=True)
@@ -163,7 +160,7 @@ class Planner:
                 t.reset(init, config.eta, device_init=device_init)
         # (belief, action, obs) belief keys when the action and observation codes fit
         mode = 1 if A <= 4096 and model.spec.observation_arity + 1 <= (1 << 20) else 0
-        t.set_belief_key_mode(min(mode, int(os.environ.get("VP_BKEY_MODE", "1"))))  # env: measurement only
+        t.set_belief_key_mode(min(mode, _BKEY_MODE_MAX))
         w = self.work
         if w is None or not w.fits(n, levels, dm.state_bytes, trace):
             w = self.work = Workspace(n, levels, dm.state_bytes, trace)

@@ -39,11 +39,7 @@ PRECISIONS = {"fp32": _lib.VP_PSI_F32, "fp64": _lib.VP_PSI_F64}
 
 
 def _torch():
-    import torch
-
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_27191_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
-    return torch
+    return _lib.torch_cuda()
 
 
 def _pow2_at_least(x: int) -> int:
