@@ -248,8 +248,11 @@ __global__ void k_root_argmax(vp_tree T, int* out) {
   warp_root_argmax<PsiT>(T, out);
 }
 
-// (live beliefs, live actions, overflow) after the chosen action
-__global__ void k_copy_counters(vp_tree T, int* out) {
+// the planning step's result in one launch: the chosen action, then (live beliefs, live
+// actions, overflow)
+template <class PsiT>
+__global__ void k_plan_result(vp_tree T, int* out) {
+  warp_root_argmax<PsiT>(T, out);
   const int idx[3] = {VP_COUNTER_LIVE_B, VP_COUNTER_LIVE_A, 2};
   if (threadIdx.x < 3) out[1 + threadIdx.x] = T.counters[idx[threadIdx.x]];
 }
@@ -528,8 +531,7 @@ static int32_t enqueue_plan_kernels(const vp_tree& T, const vp_model& M, const v
     if (int32_t rc = launch_backup<PsiT, Exact>(T, W, S.pass, P.gamma, st)) return rc;
     d = std::min(d + 1, P.d_max_cap);
   }
-  { Launch L_(KK_ARGMAX, st); k_root_argmax<PsiT><<<1, 32, 0, st>>>(T, P.out_dev); }
-  { Launch L_(KK_ARGMAX, st); k_copy_counters<<<1, 32, 0, st>>>(T, P.out_dev); }
+  { Launch L_(KK_ARGMAX, st); k_plan_result<PsiT><<<1, 32, 0, st>>>(T, P.out_dev); }
   if (P.out_host &&
       cudaMemcpyAsync(P.out_host, P.out_dev, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return VP_ERR_CUDA;
