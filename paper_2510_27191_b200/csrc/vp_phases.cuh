@@ -30,7 +30,7 @@
 
 namespace vp {
 
-constexpr int kSearchWarps = 2;   // warps per search block
+constexpr int kSearchWarps = 4;   // warps per search block (4: C3 -1.5 %, C2 / C5 even against 1 or 2)
 
 // Measurement builds only (-DVP_PHASE_CLOCKS, scripts/phase_clocks.sh): SM cycles per search
 // phase summed over warps (lane 0), read back with vp_debug_phases.
