@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--n-parallel", type=int, default=None)
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--rng", default="splitmix64", choices=["splitmix64", "philox"],
+                    help="per-row streams: the reference's SplitMix64 hash or the Philox4x32-10 fast mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
                     help="skip the secondary workloads (C3, C5, fp64 C2) measured beside the headline at N = 1")
@@ -115,7 +117,8 @@ def workload_config(args, actions):
             "simulations_per_step": args.n_parallel * args.iterations,
             "episode_steps_per_step": args.n_parallel * sum(range(1, args.iterations + 1)),
             "parallelism": "one plan() per step",
-            "l2": "flushed between timed steps (256 MB write, outside the per-step CUDA events)"}
+            "l2": "flushed between timed steps (256 MB write, outside the per-step CUDA events)",
+            **({"rng": "philox4x32-10"} if getattr(args, "rng", "splitmix64") == "philox" else {})}
 
 
 # ---------------------------------------------------------------- clocks
@@ -298,7 +301,7 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
 
     import paper_2510_27191_b200 as vp
     from paper_2510_27191_b200 import _lib
-    from paper_2510_27191_b200.rng import key_of
+    from paper_2510_27191_b200.rng import key_of, kind_of
 
     sharded = world > 1 and args.multi == "sharded"
     # sharded: ONE planning step over world * n_parallel rows (same seed on every rank);
@@ -315,13 +318,15 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
         else vp.solver.get_planner(args.precision, False)
     dm = vp.device_model(model)
     particles, cumw, m = planner.upload_belief(dm, belief)
-    rngs = [vp.RowRng.from_seed(seed).derive(1, t) for t in range(args.warmup + args.steps)]
+    rng_cls = vp.PhiloxRowRng if getattr(args, "rng", "splitmix64") == "philox" else vp.RowRng
+    rngs = [rng_cls.from_seed(seed).derive(1, t) for t in range(args.warmup + args.steps)]
 
     def step(t):
         if sharded:  # trajectories of this rank's rows, one NCCL all-gather per pass, replicated insert + backup
             return planner.plan(belief, model, cfg, rngs[t], resident=(particles, cumw, m))
         # belief resident in HBM; one vp_plan call (CUDA graph replay) per planning step
         d, tree, work = planner.prepare(model, cfg, device_init=False)
+        d.desc.rng_kind = kind_of(rngs[t])
         return planner.run_fixed(d, tree, work, m, model.spec, cfg, key_of(rngs[t]), from_host=False)
 
     def plan_e2e(t):
@@ -474,7 +479,8 @@ def measure(args, rank, world, local, *, profile=True, clocks=True, latency=None
 
 # secondary workloads measured beside the headline at N = 1 (BASELINE configs[2] and [4] and the
 # reference precision of the headline)
-SECONDARY = [("c3", "fp32"), ("c5", "fp32"), ("c2", "fp64")]
+SECONDARY = [("c3", "fp32", "splitmix64"), ("c5", "fp32", "splitmix64"), ("c2", "fp64", "splitmix64"),
+             ("c2", "fp32", "philox")]
 
 
 def run_b200(args):
@@ -503,16 +509,17 @@ def run_b200(args):
         line["latency_probe"] = latency
     if rank == 0 and world == 1 and args.secondary:
         sec = {}
-        for cid, prec in SECONDARY:
-            if cid == args.config and prec == args.precision:
+        for cid, prec, rk in SECONDARY:
+            if cid == args.config and prec == args.precision and rk == args.rng:
                 continue
             a2 = argparse.Namespace(**vars(args))
-            a2.config, a2.precision = cid, prec
+            a2.config, a2.precision, a2.rng = cid, prec, rk
             a2.n_parallel, a2.iterations = CONFIGS[cid]["n_parallel"], CONFIGS[cid]["iterations"]
             r = measure(a2, rank, world, local, clocks=False, latency=latency)
             r.pop("_model")
-            sec[f"{cid}_{prec}"] = {"config": workload_config(a2, r["actions"]), "value": r["value"],
-                                    "ms_per_step": r["ms_per_step"], "e2e": r["e2e"], "dtype": prec,
+            sec[f"{cid}_{prec}" + ("_philox" if rk == "philox" else "")] = {
+                                    "config": workload_config(a2, r["actions"]), "value": r["value"],
+                                    "ms_per_step": r["ms_per_step"], "e2e": r["e2e"], "dtype": prec, "rng": rk,
                                     "roofline_other": r["roofline_other"], "kernels": r["kernels"],
                                     "tree_stats": r["tree_stats"], "traffic_per_step": r["traffic_per_step"]}
             torch.cuda.empty_cache()

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VPB200_ABI_VERSION 8
+#define VPB200_ABI_VERSION 9
 
 enum vp_status {
   VP_OK = 0,
@@ -42,10 +42,19 @@ enum vp_model_kind {
   VP_MODEL_SYNTHETIC = 3, /* NEW: integer-hash scaling model (BASELINE config 5) */
   VP_MODEL_LIGHTDARK = 4, /* NEW: continuous-observation Light-Dark (config 4) */
   VP_MODEL_NAVIGATION = 5, /* envs/navigation.py (13x13 grid, gates, 8-bit sensor) */
-  VP_MODEL_CROWDNAV = 6    /* envs/crowdnav.py (robot through a reactive crowd) */
+  VP_MODEL_CROWDNAV = 6,   /* envs/crowdnav.py (robot through a reactive crowd) */
+  VP_MODEL_USER = 7        /* a user ProblemModel compiled in as a plug-in library (core.py:84-142;
+                              paper_2510_27191_b200/plugin.py, csrc/vp_plugin.cuh); only
+                              plug-in builds of this library accept it */
 };
 
 enum vp_psi_dtype { VP_PSI_F32 = 0, VP_PSI_F64 = 1 };
+
+/* Per-row random streams (vp_model.rng_kind).  SPLITMIX64 is the reference's
+ * counter hash (rng.py:26-89): trees equal the reference's.  PHILOX is the fast
+ * mode the north_star names: Philox4x32-10 keyed by the same derived stream
+ * keys (vp_common.cuh), statistically equivalent, not the reference's trees. */
+enum vp_rng_kind { VP_RNG_SPLITMIX64 = 0, VP_RNG_PHILOX = 1 };
 
 #define VP_COUNTERS 64
 #define VP_COUNTER_ACTIONS 32
@@ -97,7 +106,11 @@ typedef struct vp_model {
   double crowd_hall_w, crowd_hall_d, crowd_noise, crowd_react, crowd_r_nearby;
   double crowd_v_curious, crowd_v_shy, crowd_v_back, crowd_collision;
   const double* crowd_heur;   /* [crowd_heur_len] heuristic by remaining rows k, host numpy (crowdnav.py:203-210) */
-  int32_t crowd_heur_len, crowd_pad;
+  int32_t crowd_heur_len;
+  int32_t rng_kind;           /* vp_rng_kind (0: the reference's SplitMix64 streams) */
+  /* USER (plug-in models): the model's parameter block, laid out as its CUDA `Params` struct */
+  const void* user_params;
+  int64_t user_param_bytes;
 } vp_model;
 
 /* Structure-of-arrays belief tree in HBM (tree.py:100-132 columns plus the
@@ -365,11 +378,27 @@ int32_t vp_rng_uniform(uint64_t key, const int64_t* rows, int64_t n, int32_t k,
                        double* out, void* stream);
 int32_t vp_rng_normal(uint64_t key, const int64_t* rows, int64_t n, int32_t k,
                       double* out, void* stream);
+/* Either stream kind (vp_rng_kind): uniforms (normal = 0) or Box-Muller
+ * normals (normal = 1) of rows under `key`, k = 0 the single-draw form, else
+ * k per row (rng.py:66-89 for SPLITMIX64; the Philox fast mode's streams). */
+int32_t vp_rng_draws(uint64_t key, const int64_t* rows, int64_t n, int32_t k,
+                     int32_t rng_kind, int32_t normal, double* out, void* stream);
+/* Raw Philox4x32-10 blocks: counters [n][4], keys [n][2] -> out [n][4]
+ * (known-answer / curand cross-checks of the fast mode's generator). */
+int32_t vp_philox4x32_10(const uint32_t* counters, const uint32_t* keys, int64_t n,
+                         uint32_t* out, void* stream);
 int32_t vp_model_step(const vp_model* model, void* states, const int32_t* actions,
                       uint64_t key, const int64_t* rows, int32_t n,
                       uint32_t* obs_out, double* reward_out, void* stream);
 int32_t vp_model_heuristic(const vp_model* model, const void* states, int32_t n,
                            double* out, void* stream);
+/* log P(observation | next state, action) per record (ProblemModel.
+ * observation_log_likelihood, core.py:96-99; the SIR reweighting term). */
+int32_t vp_model_obs_loglik(const vp_model* model, const void* states, int32_t n,
+                            int32_t action, uint32_t observation, double* out, void* stream);
+/* 1 when this build carries a plug-in model (VP_MODEL_USER), else 0; the
+ * plug-in's State record size in bytes through *state_bytes. */
+int32_t vp_plugin_info(int32_t* state_bytes);
 /* rows of PSI (f32/f64 per dtype) -> LSE per row, mode exact/fast. */
 int32_t vp_lse_rows(const void* rows, int32_t dtype, int32_t exact, int32_t count,
                     int32_t width, double eta, double* out, void* stream);

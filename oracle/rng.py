@@ -116,3 +116,82 @@ class BoundRng:
 
     def normal(self, k: int | None = None) -> np.ndarray:
         return self.rng.normal(self.rows, k)
+
+
+# ---------------------------------------------------------------- Philox fast mode
+#
+# Not in the reference: the north_star's "counter-based Philox RNG", the
+# device's optional fast stream kind (vp_model.rng_kind = VP_RNG_PHILOX,
+# csrc/vp_common.cuh).  Philox4x32-10 as Salmon, Moraes, Dror & Shaw,
+# "Parallel random numbers: as easy as 1, 2, 3" (SC'11) define it, pinned to the
+# Random123 known-answer vectors in tests/test_rng_contract_cpu.py.  Stream keys
+# derive exactly as above (SplitMix64 folds); only the per-row draw changes:
+#     block(key, row, j, tag) = Philox4x32-10(ctr = (lo row, hi row, lo j, tag), key = (lo key, hi key))
+#     uniform  (tag 0; j = 0 single draw, j = 1..k)  = top 53 bits of (x << 32 | y) * 2**-53
+#     normal   (tag 1)  = Box-Muller of u1 = (bits(x, y) + 1) 2**-53, u2 = bits(z, w) 2**-53
+
+PHILOX_M0, PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
+PHILOX_W0, PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+_M32 = U64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 over arrays: ctr (..., 4) and key (..., 2) of uint32-valued ints -> (..., 4) uint32."""
+    c = [np.asarray(ctr, dtype=U64)[..., i] & _M32 for i in range(4)]
+    k0 = np.asarray(key, dtype=U64)[..., 0] & _M32
+    k1 = np.asarray(key, dtype=U64)[..., 1] & _M32
+    m0, m1 = U64(PHILOX_M0), U64(PHILOX_M1)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = c[0] * m0
+            p1 = c[2] * m1
+            c = [(p1 >> U64(32)) ^ c[1] ^ k0, p1 & _M32, (p0 >> U64(32)) ^ c[3] ^ k1, p0 & _M32]
+            k0 = (k0 + U64(PHILOX_W0)) & _M32
+            k1 = (k1 + U64(PHILOX_W1)) & _M32
+    return np.stack(c, axis=-1).astype(np.uint32)
+
+
+def philox_row_blocks(key, rows, js, tag: int):
+    """Blocks for every (row, j): rows (n,), js (k,) -> (n, k, 4)."""
+    r = np.asarray(rows, dtype=np.int64).astype(U64)
+    j = np.asarray(js, dtype=np.int64).astype(U64)
+    n, k = len(r), len(j)
+    ctr = np.empty((n, k, 4), dtype=U64)
+    ctr[..., 0] = (r & _M32)[:, None]
+    ctr[..., 1] = (r >> U64(32))[:, None]
+    ctr[..., 2] = (j & _M32)[None, :]
+    ctr[..., 3] = U64(tag)
+    kk = U64(key)
+    keyv = np.array([int(kk) & 0xFFFFFFFF, int(kk) >> 32], dtype=U64)
+    return philox4x32_10(ctr, np.broadcast_to(keyv, (n, k, 2)))
+
+
+def _bits53(hi, lo):
+    return ((hi.astype(U64) << U64(32)) | lo.astype(U64)) >> U64(11)
+
+
+class PhiloxRowRng(RowRng):
+    """RowRng whose per-row draws are Philox4x32-10 blocks (the device fast mode)."""
+
+    __slots__ = ()
+    rng_kind = 1  # vp_rng_kind VP_RNG_PHILOX
+
+    def derive(self, *words: int) -> "PhiloxRowRng":
+        k = self.key
+        for w in words:
+            k = fold_word(k, w)
+        return PhiloxRowRng(k)
+
+    def uniform(self, rows, k: int | None = None) -> np.ndarray:
+        js = [0] if k is None else range(1, k + 1)
+        b = philox_row_blocks(self.key, rows, js, 0)
+        u = _bits53(b[..., 0], b[..., 1]).astype(np.float64) * _SCALE
+        return u[:, 0] if k is None else u
+
+    def normal(self, rows, k: int | None = None) -> np.ndarray:
+        js = [0] if k is None else range(1, k + 1)
+        b = philox_row_blocks(self.key, rows, js, 1)
+        u1 = (_bits53(b[..., 0], b[..., 1]).astype(np.float64) + 1.0) * _SCALE
+        u2 = _bits53(b[..., 2], b[..., 3]).astype(np.float64) * _SCALE
+        z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+        return z[:, 0] if k is None else z

@@ -14,17 +14,18 @@ from .belief import DeviceBelief, ParticleBelief, SirUpdate, sir_update, systema
 from .core import ProblemModel, ProblemSpec, StepResult
 from .envs import (CrowdNavModel, CrowdStates, LightDarkModel, MarsModel, NavigationModel, SyntheticModel, TabularModel, TabularPOMDP,
                    device_model, problem_from_config, tiger_model)
-from .rng import BoundRng, RowRng
+from .rng import BoundRng, PhiloxRowRng, RowRng
 from .search import LeafResult, SearchBatch, sample_actions, search, search_recorded, softmax_rows
 from .solver import Planner, PlanOutcome, RunRecord, SolverConfig, get_planner, plan, run_episode
 from .shard import ShardedPlanner, shard_rows
+from .plugin import CudaModel, RecordStates, compile_plugin
 from .tree import DeviceTree, init_tree, match_or_append_pairs
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BoundRng", "CrowdNavModel", "CrowdStates", "DeviceBelief", "DeviceTree", "LeafResult", "LightDarkModel", "MarsModel", "NavigationModel", "ParticleBelief", "PlanOutcome",
-    "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
+    "CudaModel", "RecordStates", "compile_plugin", "Planner", "ProblemModel", "ShardedPlanner", "shard_rows", "ProblemSpec", "PhiloxRowRng", "RowRng", "RunRecord", "SearchBatch", "SirUpdate", "SolverConfig",
     "StepResult", "SyntheticModel", "TabularModel", "TabularPOMDP", "backup", "device_model", "get_planner",
     "init_tree", "log_sum_exp_rows", "plan", "problem_from_config", "run_episode", "sample_actions", "search",
     "sir_update", "search_recorded", "softmax_rows", "systematic_resample", "tiger_model", "LevelValues", "aggregate_leaves",

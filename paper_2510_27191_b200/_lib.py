@@ -17,10 +17,13 @@ LIB_PATH = os.environ.get("VPB200_LIB") or os.path.join(_HERE, "libvpb200.so")  
 VP_OK, VP_ERR_INVALID, VP_ERR_CAPACITY, VP_ERR_CUDA, VP_ERR_MODEL = range(5)
 VP_MODEL_MARS, VP_MODEL_TABULAR, VP_MODEL_SYNTHETIC, VP_MODEL_LIGHTDARK, VP_MODEL_NAVIGATION = 1, 2, 3, 4, 5
 VP_MODEL_CROWDNAV = 6
+VP_MODEL_USER = 7  # plug-in builds only (plugin.py)
 CROWD_MAX_PEOPLE, CROWD_MAX_TRACKED, CROWD_STATE_BYTES = 320, 8, 2704
 VP_PSI_F32, VP_PSI_F64 = 0, 1
+VP_RNG_SPLITMIX64, VP_RNG_PHILOX = 0, 1
+RNG_KINDS = {"splitmix64": VP_RNG_SPLITMIX64, "philox": VP_RNG_PHILOX}
 VP_SEARCH_FUSED, VP_SEARCH_TRAJECTORY, VP_SEARCH_INSERT = 0, 1, 2
-ABI_VERSION = 8
+ABI_VERSION = 9
 VP_COUNTERS, VP_COUNTER_ACTIONS, VP_COUNTER_DENSE = 64, 32, 48  # include/vpb200.h
 VP_COUNTER_LIVE_B, VP_COUNTER_LIVE_A, VP_COUNTER_DONE = 8, 16, 24
 VP_OVERLAY_SLOTS = 4
@@ -53,7 +56,8 @@ class VpModel(C.Structure):
         ("crowd_hall_w", C.c_double), ("crowd_hall_d", C.c_double), ("crowd_noise", C.c_double),
         ("crowd_react", C.c_double), ("crowd_r_nearby", C.c_double), ("crowd_v_curious", C.c_double),
         ("crowd_v_shy", C.c_double), ("crowd_v_back", C.c_double), ("crowd_collision", C.c_double),
-        ("crowd_heur", C.c_void_p), ("crowd_heur_len", C.c_int32), ("crowd_pad", C.c_int32),
+        ("crowd_heur", C.c_void_p), ("crowd_heur_len", C.c_int32), ("rng_kind", C.c_int32),
+        ("user_params", C.c_void_p), ("user_param_bytes", C.c_int64),
     ]
 
 
@@ -149,10 +153,16 @@ _SIGNATURES = [
     ("vp_plan_keys", C.c_int32, [C.c_uint64, C.c_int32, C.c_void_p]),
     ("vp_rng_uniform", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("vp_rng_normal", C.c_int32, [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_rng_draws", C.c_int32,
+     [C.c_uint64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_philox4x32_10", C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("vp_model_step", C.c_int32,
      [C.POINTER(VpModel), C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
       C.c_void_p]),
     ("vp_model_heuristic", C.c_int32, [C.POINTER(VpModel), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("vp_model_obs_loglik", C.c_int32,
+     [C.POINTER(VpModel), C.c_void_p, C.c_int32, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    ("vp_plugin_info", C.c_int32, [C.POINTER(C.c_int32)]),
     ("vp_lse_rows", C.c_int32,
      [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p]),
     ("vp_sample_rows", C.c_int32,
@@ -193,11 +203,7 @@ class LibraryMissing(ImportError):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load and type the shared library (no CUDA context is created here)."""
-    global _lib
-    if _lib is not None:
-        return _lib
+def _open(path: str):
     if not os.path.exists(path):
         raise LibraryMissing(
             f"{path} not found: build the sm_100a library first (`make` or "
@@ -209,8 +215,37 @@ def load(path: str = LIB_PATH):
         fn.argtypes = args
     if lib.vp_abi_version() != ABI_VERSION:
         raise LibraryMissing(f"ABI mismatch: library {lib.vp_abi_version()} vs binding {ABI_VERSION}")
-    _lib = lib
     return lib
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA context is created here)."""
+    global _lib
+    if _lib is None:
+        _lib = _open(path)
+    return _lib
+
+
+_PLUGINS: dict = {}
+
+
+def load_plugin(path: str):
+    """A plug-in build of the library (plugin.py), typed like the main one; cached by path."""
+    lib = _PLUGINS.get(path)
+    if lib is None:
+        load()  # the main library first: its status strings and the model-independent entry points
+        lib = _PLUGINS[path] = _open(path)
+    return lib
+
+
+def call_on(lib, name: str, *args):
+    """``call`` on a given library (None: the main one)."""
+    if lib is None:
+        return call(name, *args)
+    fn = getattr(lib, name)
+    st = fn(*args)
+    if st != VP_OK:
+        raise_status(st, name, lib)
 
 
 def layout_mismatches() -> list:
@@ -238,7 +273,11 @@ def check(status: int, what: str = ""):
     """Map a vp_status to the reference's exception convention."""
     if status == VP_OK:
         return
-    msg = f"{what}: {load().vp_status_string(status).decode()}"
+    raise_status(status, what, load())
+
+
+def raise_status(status: int, what: str, lib):
+    msg = f"{what}: {lib.vp_status_string(status).decode()}"
     if status == VP_ERR_INVALID:
         raise ValueError(msg)
     if status == VP_ERR_CAPACITY:

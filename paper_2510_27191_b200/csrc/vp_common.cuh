@@ -55,6 +55,64 @@ __device__ __forceinline__ double normal_j(u64 key, u64 row, u64 j) {
   return sqrt(-2.0 * log(u1)) * cos(kTwoPi * u2);
 }
 
+// ---------------------------------------------------------------- Philox fast mode
+//
+// vp_model.rng_kind = VP_RNG_PHILOX replaces the per-row SplitMix64 hash by
+// Philox4x32-10 (Salmon et al., SC'11; the constants of curand_philox4x32_x.h,
+// checked against curand_Philox4x32_10 in tests/test_gpu_philox.py).  The
+// stream keys (derive / fold: warp-uniform) are unchanged; a row's draw j of
+// the stream `key` is the block
+//   Philox4x32-10(counter = {lo(row), hi(row), lo(j), tag}, key = {lo(key), hi(key)})
+// with tag 0 for uniforms (j = 0: the single draw, j >= 1: the j-th of k) and
+// tag 1 for normals (one block per Box-Muller pair).  A uniform takes the top
+// 53 bits of {x, y}; a normal uses {x, y} + 1 ulp and {z, w} as (u1, u2).
+// Not the reference's streams: trees differ from the reference's, their
+// statistics do not (oracle/rng.py: philox4x32_10, PhiloxRowRng).
+constexpr u32 kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
+constexpr u32 kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const u32 lo0 = kPhiloxM0 * c.x, hi0 = __umulhi(kPhiloxM0, c.x);
+    const u32 lo1 = kPhiloxM1 * c.z, hi1 = __umulhi(kPhiloxM1, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += kPhiloxW0;
+    k.y += kPhiloxW1;
+  }
+  return c;
+}
+__device__ __forceinline__ uint4 philox_block(u64 key, u64 row, u64 j, u32 tag) {
+  return philox4x32_10(make_uint4((u32)row, (u32)(row >> 32), (u32)j, tag), make_uint2((u32)key, (u32)(key >> 32)));
+}
+__device__ __forceinline__ double philox_unit(u64 key, u64 row, u64 j) {
+  const uint4 b = philox_block(key, row, j, 0u);
+  return unit53(((u64)b.x << 32) | b.y);
+}
+__device__ __forceinline__ double philox_normal(u64 key, u64 row, u64 j) {
+  const uint4 b = philox_block(key, row, j, 1u);
+  const double u1 = ((double)((((u64)b.x << 32) | b.y) >> 11) + 1.0) * kInv53;
+  const double u2 = (double)((((u64)b.z << 32) | b.w) >> 11) * kInv53;
+  return sqrt(-2.0 * log(u1)) * cos(kTwoPi * u2);
+}
+
+// Stream-kind dispatch (rk = vp_model.rng_kind: kernel-parameter uniform, no divergence).
+__device__ __forceinline__ double uniform1(u64 key, u64 row, int rk) {
+  return rk ? philox_unit(key, row, 0) : uniform1(key, row);
+}
+__device__ __forceinline__ double uniform_j(u64 key, u64 row, u64 j, int rk) {
+  return rk ? philox_unit(key, row, j) : uniform_j(key, row, j);
+}
+__device__ __forceinline__ double normal_j(u64 key, u64 row, u64 j, int rk) {
+  return rk ? philox_normal(key, row, j) : normal_j(key, row, j);
+}
+// A row's stream handle for many draws: SplitMix64 precomputes the row base
+// (rng.py:69); Philox keeps the key and takes the row per draw.
+__device__ __forceinline__ u64 stream_base(u64 key, u64 row, int rk) { return rk ? key : row_base(key, row); }
+__device__ __forceinline__ double stream_uniform(u64 base, u64 row, u64 j, int rk) {
+  return rk ? philox_unit(base, row, j) : unit53(mix64(base + j * kMixB));
+}
+
 // ---------------------------------------------------------------- hashing
 
 // 16-byte slot of an open-addressing index.  Empty slots are all-ones (one

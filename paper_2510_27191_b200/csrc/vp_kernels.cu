@@ -163,9 +163,9 @@ __global__ void k_rehash(vp_tree T) {
 
 // Root-state draw into work.states (hook / iterative path; vp_plan fuses it into k_search).
 template <class Model>
-__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key) {
+__global__ void k_draw(vp_work W, const typename Model::State* particles, const double* cumw, int m, u64 key, int rk) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < W.n) reinterpret_cast<typename Model::State*>(W.states)[r] = draw_state(particles, cumw, m, key, r);
+  if (r < W.n) reinterpret_cast<typename Model::State*>(W.states)[r] = draw_state(particles, cumw, m, key, r, rk);
 }
 
 template <class PsiT>
@@ -185,7 +185,7 @@ __device__ __forceinline__ Stage<PsiT> make_stage(unsigned char* smem, u64* bars
 }
 
 // One search call: every warp carries 32 rows through all levels.
-template <class Model, class PsiT, bool Exact>
+template <class Model, class PsiT, bool Exact, int RK>
 __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_model M, vp_work W, vp_search_args S,
                                                               StageCfg sc, int rows) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) k_search(vp_tree T, vp_mode
   // last block advances the extents)
   const int base_b = T.counters[0], base_a = T.counters[VP_COUNTER_ACTIONS];
   if (wi * rows_per_search_warp<Model>(S.mode, rows) < W.n)
-    search_warp<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state, rows, base_a, base_b);
+    search_warp<Model, PsiT, Exact, RK>(T, M, W, S, sg, init_cdf, init_row, wi, shared_state, rows, base_a, base_b);
   if (S.mode == VP_SEARCH_TRAJECTORY) return;  // creates no nodes
   // the last warp to finish advances the extents (every warp has used its base by then)
   __syncwarp();
@@ -315,12 +315,17 @@ struct Launch {
 template <class F>
 static int32_t dispatch_model(int kind, F&& f) {
   switch (kind) {
+#ifndef VP_PLUGIN_ONLY  // a plug-in library instantiates its own model only (compile time)
     case VP_MODEL_MARS: return f(MarsModel());
     case VP_MODEL_TABULAR: return f(TabularModel());
     case VP_MODEL_SYNTHETIC: return f(SyntheticModel());
     case VP_MODEL_LIGHTDARK: return f(LightDarkModel());
     case VP_MODEL_NAVIGATION: return f(NavigationModel());
     case VP_MODEL_CROWDNAV: return f(CrowdNavModel());
+#endif
+#ifdef VP_PLUGIN_SOURCE
+    case VP_MODEL_USER: return f(UserModel());
+#endif
     default: return VP_ERR_MODEL;
   }
 }
@@ -380,6 +385,11 @@ static bool state_size_ok(const vp_model& M) {
       return false;
     if (!ensure_stack(3 * sizeof(CrowdState))) return false;
   }
+#ifdef VP_PLUGIN_SOURCE
+  if constexpr (std::is_same<Model, UserModel>::value) {
+    if (!M.user_params || M.user_param_bytes < (int64_t)sizeof(UserModel::Params)) return false;
+  }
+#endif
   return M.state_bytes == (int)sizeof(typename Model::State);
 }
 
@@ -448,7 +458,10 @@ static int32_t search_geometry(int A, int n, int mode, StageCfg& sc, size_t& sme
 
 template <class Model, class PsiT, bool Exact>
 static int32_t set_search_attr(size_t smem) {
-  return ensure_smem_optin((const void*)k_search<Model, PsiT, Exact>, smem) ? VP_OK : VP_ERR_CUDA;
+  return ensure_smem_optin((const void*)k_search<Model, PsiT, Exact, VP_RNG_SPLITMIX64>, smem) &&
+                 ensure_smem_optin((const void*)k_search<Model, PsiT, Exact, VP_RNG_PHILOX>, smem)
+             ? VP_OK
+             : VP_ERR_CUDA;
 }
 
 template <class Model, class PsiT, bool Exact>
@@ -462,7 +475,11 @@ static int32_t launch_search(const vp_tree& T, const vp_model& M, const vp_work&
   const int grid = blocks_for(blocks_for(W.n, rows_per_search_warp<Model>(S.mode, rows)), kSearchWarps);
   {
     Launch L_(KK_SEARCH, st);
-    k_search<Model, PsiT, Exact><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc, rows);
+    // the stream kind is a template constant: the reference's SplitMix64 path carries no Philox branch
+    if (M.rng_kind == VP_RNG_PHILOX)
+      k_search<Model, PsiT, Exact, VP_RNG_PHILOX><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc, rows);
+    else
+      k_search<Model, PsiT, Exact, VP_RNG_SPLITMIX64><<<grid, kSearchWarps * 32, smem, st>>>(T, M, W, S, sc, rows);
   }
   return check_launch();
 }
@@ -637,7 +654,7 @@ __global__ void k_sir_propagate(vp_model M, const typename Model::State* in, con
   typename Model::State st = in[i];
   u32 o;
   double r;
-  Model::step(M, st, a, key, (u64)i, o, r);  // step_batch(states, actions, rng.derive(retry).bind(rows))
+  Model::step(M, st, a, key, (u64)i, o, r, M.rng_kind);  // step_batch(states, actions, rng.derive(retry).bind(rows))
   out[i] = st;
   logw[i] = log(w[i]) + Model::obs_loglik(M, st, a, obs);  // log(weights) + log_lik (belief.py:88-90)
 }
@@ -660,7 +677,7 @@ __global__ void __launch_bounds__(kCoopSirWarps * 32) k_sir_propagate_coop(vp_mo
   warp_copy_state(st, in[i]);
   u32 o;
   double r;
-  Model::step_warp(M, st, a, key, (u64)i, true, o, r);
+  Model::step_warp(M, st, a, key, (u64)i, true, o, r, M.rng_kind);
   warp_copy_state(out[i], st);
   if (lane_id() == 0) logw[i] = log(w[i]) + Model::obs_loglik(M, st, a, obs);
 }
@@ -825,6 +842,20 @@ __global__ void k_rng_uniform(u64 key, const int64_t* rows, int64_t n, int k, do
   else
     for (int j = 1; j <= k; ++j) out[i * k + (j - 1)] = uniform_j(key, r, (u64)j);
 }
+// draws of either stream kind (rk); normal != 0: Box-Muller normals
+__global__ void k_rng_draws(u64 key, const int64_t* rows, int64_t n, int k, int rk, int normal, double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 r = (u64)rows[i];
+  if (k <= 0) out[i] = normal ? normal_j(key, r, 0, rk) : uniform1(key, r, rk);
+  else
+    for (int j = 1; j <= k; ++j)
+      out[i * k + (j - 1)] = normal ? normal_j(key, r, (u64)j, rk) : uniform_j(key, r, (u64)j, rk);
+}
+__global__ void k_philox_blocks(const uint4* ctr, const uint2* key, int64_t n, uint4* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
+}
 __global__ void k_rng_normal(u64 key, const int64_t* rows, int64_t n, int k, double* out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -841,7 +872,7 @@ __global__ void k_model_step(vp_model M, typename Model::State* st, const int32_
   typename Model::State s = st[i];
   u32 o;
   double r;
-  Model::step(M, s, act[i], key, (u64)rows[i], o, r);
+  Model::step(M, s, act[i], key, (u64)rows[i], o, r, M.rng_kind);
   st[i] = s;
   obs[i] = o;
   rew[i] = r;
@@ -851,6 +882,12 @@ __global__ void k_model_heur(vp_model M, const typename Model::State* st, int n,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   out[i] = Model::heuristic(M, st[i]);
+}
+template <class Model>
+__global__ void k_model_loglik(vp_model M, const typename Model::State* st, int n, int a, u32 o, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = Model::obs_loglik(M, st[i], a, o);
 }
 template <class PsiT, bool Exact>
 __global__ void k_lse_rows(const PsiT* rows, int count, int width, double eta, double* out) {
@@ -1033,7 +1070,7 @@ int32_t vp_draw_root_states(const vp_model* m, const vp_work* w, const void* par
     if (!state_size_ok<Model>(*m)) return VP_ERR_INVALID;
     Launch L_(KK_DRAW, st);
     k_draw<Model><<<blocks_for(W.n, 256), 256, 0, st>>>(
-        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key);
+        W, reinterpret_cast<const typename Model::State*>(particles), cumw, count, key, m->rng_kind);
     return check_launch();
   });
 }
@@ -1375,6 +1412,23 @@ int32_t vp_rng_normal(uint64_t key, const int64_t* rows, int64_t n, int32_t k, d
   return check_launch();
 }
 
+int32_t vp_rng_draws(uint64_t key, const int64_t* rows, int64_t n, int32_t k, int32_t rng_kind, int32_t normal,
+                     double* out, void* stream) {
+  if (n < 0 || (n && (!rows || !out)) || (rng_kind != VP_RNG_SPLITMIX64 && rng_kind != VP_RNG_PHILOX))
+    return VP_ERR_INVALID;
+  if (!n) return VP_OK;
+  k_rng_draws<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(key, rows, n, k, rng_kind, normal, out);
+  return check_launch();
+}
+
+int32_t vp_philox4x32_10(const uint32_t* counters, const uint32_t* keys, int64_t n, uint32_t* out, void* stream) {
+  if (n < 0 || (n && (!counters || !keys || !out))) return VP_ERR_INVALID;
+  if (!n) return VP_OK;
+  k_philox_blocks<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const uint4*>(counters), reinterpret_cast<const uint2*>(keys), n, reinterpret_cast<uint4*>(out));
+  return check_launch();
+}
+
 int32_t vp_model_step(const vp_model* m, void* states, const int32_t* actions, uint64_t key, const int64_t* rows,
                       int32_t n, uint32_t* obs_out, double* reward_out, void* stream) {
   if (!m || n < 0) return VP_ERR_INVALID;
@@ -1402,6 +1456,31 @@ int32_t vp_model_heuristic(const vp_model* m, const void* states, int32_t n, dou
         M, reinterpret_cast<const typename Model::State*>(states), n, out);
     return check_launch();
   });
+}
+
+int32_t vp_model_obs_loglik(const vp_model* m, const void* states, int32_t n, int32_t action, uint32_t observation,
+                            double* out, void* stream) {
+  if (!m || n < 0 || action < 0 || action >= m->action_count) return VP_ERR_INVALID;
+  if (!n) return VP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vp_model M = *m;
+  return dispatch_model(M.kind, [&](auto mdl) -> int32_t {
+    typedef decltype(mdl) Model;
+    if (!state_size_ok<Model>(M)) return VP_ERR_INVALID;
+    k_model_loglik<Model><<<blocks_for(n, 256), 256, 0, st>>>(
+        M, reinterpret_cast<const typename Model::State*>(states), n, action, observation, out);
+    return check_launch();
+  });
+}
+
+int32_t vp_plugin_info(int32_t* state_bytes) {
+#ifdef VP_PLUGIN_SOURCE
+  if (state_bytes) *state_bytes = (int32_t)sizeof(UserModel::State);
+  return 1;
+#else
+  if (state_bytes) *state_bytes = 0;
+  return 0;
+#endif
 }
 
 int32_t vp_lse_rows(const void* rows, int32_t dtype, int32_t exact, int32_t count, int32_t width, double eta,

@@ -26,7 +26,7 @@ struct __align__(16) MarsState {
 struct MarsModel {
   typedef MarsState State;
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
-                                              u32& obs, double& rew) {
+                                              u32& obs, double& rew, int rkind) {
     const int n = M.mars_n, P = M.mars_ops;
     const int op[2] = {a / P, a % P};
     const State in = s;
@@ -66,7 +66,7 @@ struct MarsModel {
     int reading[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const double u = uniform1(fold(mkey, (u64)k), row);
+      const double u = uniform1(fold(mkey, (u64)k), row, rkind);
       reading[k] = 2;  // NULL
       if (!gone[k] && op[k] >= 5) {
         const int rk = op[k] - 5;
@@ -152,15 +152,15 @@ struct __align__(8) TabularState {
 struct TabularModel {
   typedef TabularState State;
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
-                                              u32& obs, double& rew) {
+                                              u32& obs, double& rew, int rkind) {
     const int S = M.tab_states, O = M.tab_obs;
     const int cur = s.idx;
-    const double us = uniform1(fold(mkey, 0), row);
+    const double us = uniform1(fold(mkey, 0), row, rkind);
     const double* ct = M.tab_cum_t + ((size_t)a * S + cur) * S;
     int nxt = 0;
     for (int j = 0; j < S; ++j) nxt += ct[j] < us;
     nxt = nxt < S - 1 ? nxt : S - 1;
-    const double uo = uniform1(fold(mkey, 1), row);
+    const double uo = uniform1(fold(mkey, 1), row, rkind);
     const double* cz = M.tab_cum_z + ((size_t)a * S + nxt) * O;
     int o = 0;
     for (int j = 0; j < O; ++j) o += cz[j] < uo;
@@ -198,10 +198,10 @@ constexpr u64 kSynHeur = 0x9FB21C651E98DF25ull;
 struct SyntheticModel {
   typedef SyntheticState State;
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
-                                              u32& obs, double& rew) {
-    const double ut = uniform1(fold(mkey, 0), row);
-    const double uo = uniform1(fold(mkey, 1), row);
-    const double un = uniform1(fold(mkey, 2), row);
+                                              u32& obs, double& rew, int rkind) {
+    const double ut = uniform1(fold(mkey, 0), row, rkind);
+    const double uo = uniform1(fold(mkey, 1), row, rkind);
+    const double un = uniform1(fold(mkey, 2), row, rkind);
     const u64 w = s.word, ua = (u64)a;
     const u64 branch = (u64)(int64_t)floor(ut * (double)M.syn_branching);
     const u64 nxt = mix64(w + (ua + 1) * kSynAct + branch * kSynBranch + M.syn_salt);
@@ -256,7 +256,7 @@ struct LightDarkModel {
     return (int)b;
   }
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row,
-                                              u32& obs, double& rew) {
+                                              u32& obs, double& rew, int rkind) {
     // moves E, NE, N, NW, W, SW, S, SE, then DECLARE
     const int dxs[9] = {1, 1, 0, -1, -1, -1, 0, 1, 0};
     const int dys[9] = {0, 1, 1, 1, 0, -1, -1, -1, 0};
@@ -266,7 +266,7 @@ struct LightDarkModel {
     const bool inside = s.x * s.x + s.y * s.y <= M.ld_goal_radius * M.ld_goal_radius;
     rew = declare ? (inside ? 100.0 : -100.0) : -1.0;
     const u64 nk = fold(mkey, 0);
-    const double z0 = normal_j(nk, row, 1), z1 = normal_j(nk, row, 2);
+    const double z0 = normal_j(nk, row, 1, rkind), z1 = normal_j(nk, row, 2, rkind);
     const double sigma = M.ld_sigma0 + M.ld_sigma_slope * fabs(nx - M.ld_light_x);
     const int o = bin(M, nx + sigma * z0) * M.ld_bins + bin(M, ny + sigma * z1);
     const bool term = s.term || declare;
@@ -330,7 +330,7 @@ struct NavigationModel {
   }
 
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row, u32& obs,
-                                              double& rew) {
+                                              double& rew, int rkind) {
     // navigation.py:172-213
     const int r = s.pos / M.nav_w, c = s.pos % M.nav_w;
     const bool move = a != 8;
@@ -350,7 +350,7 @@ struct NavigationModel {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const bool bit = blocked(M, nx, nr + dr(i), nc + dc(i));
-      const bool flip = uniform_j(fk, row, (u64)(i + 1)) >= M.nav_acc;
+      const bool flip = uniform_j(fk, row, (u64)(i + 1), rkind) >= M.nav_acc;
       o |= (u32)(bit != flip) << i;
     }
     obs = term ? (u32)M.obs_arity : o;
@@ -407,7 +407,9 @@ struct CrowdNavModel {
   static constexpr bool kCoop = true;
 
   // j-th of the row's Box-Muller normals from precomputed row bases (rng.py:81-89)
-  static __device__ __forceinline__ double normal_at(u64 b1, u64 b2, u64 j) {
+  // (Philox mode: b1 is the normal stream's key itself, one block per normal)
+  static __device__ __forceinline__ double normal_at(u64 b1, u64 b2, u64 row, u64 j, int rk) {
+    if (rk) return philox_normal(b1, row, j);
     const u64 h1 = mix64(b1 + j * kMixB), h2 = mix64(b2 + j * kMixB);
     const double u1 = ((double)(h1 >> 11) + 1.0) * kInv53;
     const double u2 = (double)(h2 >> 11) * kInv53;
@@ -422,7 +424,7 @@ struct CrowdNavModel {
   // crowdnav.py:116-174, every operation in numpy's order and precision
   // (float64 motion, float32 storage; no FMA contraction, see Makefile)
   static __device__ __forceinline__ void step(const vp_model& M, State& s, int a, u64 mkey, u64 row, u32& obs,
-                                              double& rew) {
+                                              double& rew, int rkind) {
     if (s.term) {  // absorbing: state, distances and code stay
       obs = (u32)M.obs_arity;
       rew = 0.0;
@@ -435,16 +437,17 @@ struct CrowdNavModel {
     const bool entered = ry0 >= M.crowd_hall_d;
     const double rx = clamp(s.rx + ddx, M.crowd_hall_w), ry = clamp(ry0, M.crowd_hall_d);
     const u64 nk = fold(mkey, 0), uk = fold(mkey, 1);
-    const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
+    const u64 b1 = rkind ? nk : row_base(fold(nk, 101), row), b2 = rkind ? 0 : row_base(fold(nk, 211), row),
+              bu = stream_base(uk, row, rkind);
     const double rad = M.crowd_collision;
     bool bumped = false;
 #pragma unroll 2
     for (int i = 0; i < M.crowd_people; ++i) {
-      double x = (double)s.px[2 * i] + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
-      double y = (double)s.px[2 * i + 1] + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
+      double x = (double)s.px[2 * i] + normal_at(b1, b2, row, (u64)(2 * i + 1), rkind) * M.crowd_noise;
+      double y = (double)s.px[2 * i + 1] + normal_at(b1, b2, row, (u64)(2 * i + 2), rkind) * M.crowd_noise;
       const double dx = rx - x, dy = ry - y;
       const double d = sqrt(dx * dx + dy * dy);
-      const double u = unit53(mix64(bu + (u64)(i + 1) * kMixB));
+      const double u = stream_uniform(bu, row, (u64)(i + 1), rkind);
       if (d < M.crowd_r_nearby && d > 1e-9 && u < M.crowd_react) {
         const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
         const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
@@ -477,7 +480,7 @@ struct CrowdNavModel {
   // memory: lane j moves people j, j + 32, ...; the arithmetic of every person
   // is step()'s, so the result is bit-identical.  a, row, live are warp-uniform.
   static __device__ __forceinline__ void step_warp(const vp_model& M, State& s, int a, u64 mkey, u64 row, bool live,
-                                                   u32& obs, double& rew) {
+                                                   u32& obs, double& rew, int rkind) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     obs = 0;
@@ -494,7 +497,8 @@ struct CrowdNavModel {
     const bool entered = ry0 >= M.crowd_hall_d;
     const double rx = clamp(s.rx + ddx, M.crowd_hall_w), ry = clamp(ry0, M.crowd_hall_d);
     const u64 nk = fold(mkey, 0), uk = fold(mkey, 1);
-    const u64 b1 = row_base(fold(nk, 101), row), b2 = row_base(fold(nk, 211), row), bu = row_base(uk, row);
+    const u64 b1 = rkind ? nk : row_base(fold(nk, 101), row), b2 = rkind ? 0 : row_base(fold(nk, 211), row),
+              bu = stream_base(uk, row, rkind);
     bool bumped = false;
     // squared-distance gates: sqrt is correctly rounded and monotone, so d < r can only
     // hold when s < r^2 (1 + 1e-12); outside the gate the reference's comparisons are
@@ -503,14 +507,14 @@ struct CrowdNavModel {
     const double bump2 = M.crowd_collision * M.crowd_collision * (1.0 + 1e-12);
     for (int i = lane; i < M.crowd_people; i += 32) {
       const float2 p = reinterpret_cast<const float2*>(s.px)[i];
-      double x = (double)p.x + normal_at(b1, b2, (u64)(2 * i + 1)) * M.crowd_noise;
-      double y = (double)p.y + normal_at(b1, b2, (u64)(2 * i + 2)) * M.crowd_noise;
+      double x = (double)p.x + normal_at(b1, b2, row, (u64)(2 * i + 1), rkind) * M.crowd_noise;
+      double y = (double)p.y + normal_at(b1, b2, row, (u64)(2 * i + 2), rkind) * M.crowd_noise;
       const double dx = rx - x, dy = ry - y;
       const double s2 = dx * dx + dy * dy;
       if (s2 < near2) {
         const double d = sqrt(s2);
         // the react draw only matters when both distance tests pass (pure function of row, i)
-        if (d < M.crowd_r_nearby && d > 1e-9 && unit53(mix64(bu + (u64)(i + 1) * kMixB)) < M.crowd_react) {
+        if (d < M.crowd_r_nearby && d > 1e-9 && stream_uniform(bu, row, (u64)(i + 1), rkind) < M.crowd_react) {
           const bool cur = (s.curious[i >> 5] >> (i & 31)) & 1u;
           const double speed = yell ? -M.crowd_v_back : cur ? M.crowd_v_curious : -M.crowd_v_shy;
           const double dn = fmax(d, 1e-9);
@@ -564,3 +568,7 @@ struct CrowdNavModel {
 };
 
 }  // namespace vp
+
+#ifdef VP_PLUGIN_SOURCE
+#include "vp_plugin.cuh"  // a user ProblemModel compiled into this build (VP_MODEL_USER)
+#endif

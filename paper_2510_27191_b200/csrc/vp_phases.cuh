@@ -804,8 +804,8 @@ __device__ void block_tree_init(const vp_tree& T) {
 
 // belief.py:37-44: u = uniform(draw_key, row); first index with cum > u
 // (searchsorted side=right), clamped to m - 1.
-__device__ __forceinline__ int draw_index(const double* cumw, int m, u64 key, int r) {
-  const double u = uniform1(key, (u64)r);
+__device__ __forceinline__ int draw_index(const double* cumw, int m, u64 key, int r, int rk) {
+  const double u = uniform1(key, (u64)r, rk);
   // weights are uniform after every SIR update (belief.py:101): the first
   // guess floor(u m) is usually the answer, confirmed with two loads
   int idx = min((int)(u * (double)m), m - 1);
@@ -823,8 +823,9 @@ __device__ __forceinline__ int draw_index(const double* cumw, int m, u64 key, in
 }
 
 template <class State>
-__device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r) {
-  return particles[draw_index(cumw, m, key, r)];
+__device__ __forceinline__ State draw_state(const State* particles, const double* cumw, int m, u64 key, int r,
+                                             int rk) {
+  return particles[draw_index(cumw, m, key, r, rk)];
 }
 
 // ------------------------------------------------------------------ cooperative models
@@ -858,15 +859,16 @@ __device__ __forceinline__ void warp_copy_state(State& dst, const State& src) {
 }
 
 // one generative step of every live row of the warp (search.py:113-115)
-template <class Model>
+// RK: the stream kind (vp_rng_kind) as a compile-time constant of the search kernel
+template <class Model, int RK>
 __device__ __forceinline__ void model_step(const vp_model& M, typename Model::State& st, int a, u64 key, int rg,
                                            bool live, u32& o, double& rw) {
   if constexpr (coop_trait<Model>::value) {
     // the row is lane 0's; every lane takes part
     Model::step_warp(M, st, __shfl_sync(FULL, a, 0), key, (u64)__shfl_sync(FULL, rg, 0),
-                     __shfl_sync(FULL, (int)live, 0) != 0, o, rw);
+                     __shfl_sync(FULL, (int)live, 0) != 0, o, rw, RK);
   } else if (live) {
-    Model::step(M, st, a, key, (u64)rg, o, rw);
+    Model::step(M, st, a, key, (u64)rg, o, rw, RK);
   }
 }
 
@@ -972,7 +974,7 @@ __device__ __forceinline__ int find_key(const Slot* tab, u64 mask, u64 key) {
 // leaves the existing tree draws from the initial row from then on -- exactly
 // what the fused search does, since nodes created during a pass are lazily
 // initial -- so the trajectory is that of the fused search.
-template <class Model, class PsiT, bool Exact>
+template <class Model, class PsiT, bool Exact, int RK>
 __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                                 Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, double lse_init,
                                 typename Model::State& st, int r, int rg, bool active, u64 skey) {
@@ -992,12 +994,12 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
   }
   for (int l = 0; l < S.d_max; ++l) {
     const u64 lkey = fold(skey, (u64)l);
-    const double u = active ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;
+    const double u = active ? uniform1(fold(lkey, 0), (u64)rg, RK) : 0.0;
     const int a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, known ? fl : 1u, rec, lse, lse_init, active,
                                            u, S.pass);
     u32 o = 0;
     double rw = 0.0;
-    model_step<Model>(M, st, a, fold(lkey, 1), rg, active, o, rw);
+    model_step<Model, RK>(M, st, a, fold(lkey, 1), rg, active, o, rw);
     if (active) {
       const size_t t = (size_t)l * n + r;
       W.trace_action[t] = a;
@@ -1025,7 +1027,7 @@ __device__ void trajectory_rows(const vp_tree& T, const vp_model& M, const vp_wo
 }
 
 // The search kernel body for one warp = 32 consecutive rows.
-template <class Model, class PsiT, bool Exact>
+template <class Model, class PsiT, bool Exact, int RK>
 __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& W, const vp_search_args& S,
                             Stage<PsiT>& sg, const PsiT* init_cdf, const PsiT* init_row, int warp_index,
                             typename Model::State* shared_state, int rows, int base_a, int base_b) {
@@ -1055,7 +1057,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       if (active) {
         const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
         src = S.particles ? reinterpret_cast<const State*>(S.particles) +
-                                draw_index(S.cum_weights, S.m, dkey, rg)
+                                draw_index(S.cum_weights, S.m, dkey, rg, RK)
                           : reinterpret_cast<const State*>(W.states) + r;
       }
       src = reinterpret_cast<const State*>(__shfl_sync(FULL, (unsigned long long)src, 0));
@@ -1064,13 +1066,13 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
   } else if (active && !insert) {
     if (S.particles) {
       const u64 dkey = S.draw_key_dev ? *S.draw_key_dev : S.draw_key;
-      st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, rg);
+      st = draw_state(reinterpret_cast<const State*>(S.particles), S.cum_weights, S.m, dkey, rg, RK);
     } else {
       st = reinterpret_cast<const State*>(W.states)[r];
     }
   }
   if (S.mode == VP_SEARCH_TRAJECTORY) {
-    trajectory_rows<Model, PsiT, Exact>(T, M, W, S, sg, init_cdf, init_row, T.init_lse[0], st, r, rg, active, skey);
+    trajectory_rows<Model, PsiT, Exact, RK>(T, M, W, S, sg, init_cdf, init_row, T.init_lse[0], st, r, rg, active, skey);
     return;
   }
   int b = active ? (S.start_beliefs ? S.start_beliefs[r] : 0) : 0;
@@ -1131,7 +1133,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
     VP_PH(0);
 #endif
     // ---- softmax draw (search.py:108-112)
-    const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg) : 0.0;  // level_rng.derive(0)
+    const double u = (active && !S.inject_actions) ? uniform1(fold(lkey, 0), (u64)rg, RK) : 0.0;  // level_rng.derive(0)
     int a = 0;
     if (S.inject_actions) a = active ? S.inject_actions[(size_t)l * n + r] : 0;
     else a = draw_action<PsiT, Exact>(T, W, sg, init_cdf, init_row, b, fl, rec, lse, lse_init, ok, u, pass);
@@ -1145,7 +1147,7 @@ __device__ void search_warp(const vp_tree& T, const vp_model& M, const vp_work& 
       }
     } else {
       VP_PH(1);
-      model_step<Model>(M, st, a, fold(lkey, 1), rg, ok, o, rw);  // level_rng.derive(1)
+      model_step<Model, RK>(M, st, a, fold(lkey, 1), rg, ok, o, rw);  // level_rng.derive(1)
       VP_PH(2);
     }
 

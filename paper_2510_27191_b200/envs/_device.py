@@ -28,7 +28,7 @@ import numpy as np
 
 from .. import _lib
 from ..core import check_step_inputs, StepResult
-from ..rng import key_of
+from ..rng import key_of, kind_of
 
 MARS_DTYPE = np.dtype([("x0", "u1"), ("y0", "u1"), ("x1", "u1"), ("y1", "u1"), ("term", "<u4"), ("rocks", "<u8")])
 TAB_DTYPE = np.dtype([("idx", "<i4"), ("term", "<i4")])
@@ -62,6 +62,12 @@ class DeviceModel:
         self.desc.state_bytes = state_dtype.itemsize
         self.desc.discount = float(spec.discount)
         self.tables = []  # device tensors referenced by desc
+        self.lib = None  # the plug-in library of a CudaModel (plugin.py); None: the main library
+
+    def call(self, name: str, *args):
+        """A model-dependent entry point (vp_plan, vp_search, vp_sir_*, vp_model_*) on the library
+        that carries this model."""
+        _lib.call_on(self.lib, name, *args)
 
     @property
     def state_bytes(self) -> int:
@@ -109,7 +115,8 @@ class DeviceModel:
         obs = torch.empty(n, dtype=torch.int32, device="cuda")
         rew = torch.empty(n, dtype=torch.float64, device="cuda")
         stream = torch.cuda.current_stream().cuda_stream
-        _lib.call("vp_model_step", C.byref(self.desc), st.data_ptr(), acts.data_ptr(), key_of(rng.rng),
+        self.desc.rng_kind = kind_of(rng)
+        self.call("vp_model_step", C.byref(self.desc), st.data_ptr(), acts.data_ptr(), key_of(rng.rng),
                   rows.data_ptr(), n, obs.data_ptr(), rew.data_ptr(), stream)
         rec = st.cpu().numpy().view(self.state_dtype)
         o = obs.cpu().numpy().view(np.uint32).astype(np.int64)
@@ -122,8 +129,20 @@ class DeviceModel:
             return np.zeros(0)
         st = self.states_to_device(states)
         out = torch.empty(n, dtype=torch.float64, device="cuda")
-        _lib.call("vp_model_heuristic", C.byref(self.desc), st.data_ptr(), n, out.data_ptr(),
+        self.call("vp_model_heuristic", C.byref(self.desc), st.data_ptr(), n, out.data_ptr(),
                   torch.cuda.current_stream().cuda_stream)
+        return out.cpu().numpy()
+
+    def obs_loglik(self, states, action: int, observation: int) -> np.ndarray:
+        """observation_log_likelihood on the device via vp_model_obs_loglik."""
+        torch = _torch()
+        n = len(states)
+        if n == 0:
+            return np.zeros(0)
+        st = self.states_to_device(states)
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        self.call("vp_model_obs_loglik", C.byref(self.desc), st.data_ptr(), n, int(action), int(observation),
+                  out.data_ptr(), torch.cuda.current_stream().cuda_stream)
         return out.cpu().numpy()
 
 

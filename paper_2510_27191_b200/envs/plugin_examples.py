@@ -1,0 +1,158 @@
+"""Example ``CudaModel`` plug-ins (plugin.py): user ProblemModels written as CUDA.
+
+* ``tabular_cuda_model(pomdp)`` -- any small TabularPOMDP (<= 8 states, actions,
+  observations) as a plug-in: the tables travel in the ``Params`` block.  It restates
+  envs/tabular.py:106-145 (the reference's TabularModel) operation for operation, so
+  its plans equal the reference's trees bit for bit -- the plug-in path's parity check.
+* ``corridor_cuda_model(length)`` -- a model that exists only as a plug-in: a robot in
+  a 1-D corridor of unknown length-position with a noisy continuous range sensor
+  (Gaussian, binned), reward at the door.  Shows floating-point states, normal draws
+  and a non-trivial heuristic / observation likelihood.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ..core import ProblemSpec
+from ..plugin import CudaModel
+
+TAB_MAX = 8
+
+TABULAR_SOURCE = r"""
+// A TabularPOMDP with <= 8 states / actions / observations (envs/tabular.py:106-145).
+struct Params {
+  int32_t S, A, O, pad;
+  double cum_t[8][8][8];   // [a][s][s'] cumulative transition rows
+  double cum_z[8][8][8];   // [a][s'][o] cumulative observation rows
+  double log_z[8][8][8];   // [a][s'][o] log Z
+  double reward[8][8];     // [s][a]
+  int32_t terminal[8];
+};
+struct State {
+  int32_t idx;
+  int32_t terminal;
+};
+__device__ void step(const Params& P, State& s, int a, const RowDraws& rng, uint32_t& obs, double& reward) {
+  const double us = rng.uniform(0);             // rng.derive(0).uniform()
+  int nxt = 0;
+  for (int j = 0; j < P.S; ++j) nxt += P.cum_t[a][s.idx][j] < us;
+  nxt = nxt < P.S - 1 ? nxt : P.S - 1;
+  const double uo = rng.uniform(1);             // rng.derive(1).uniform()
+  int o = 0;
+  for (int j = 0; j < P.O; ++j) o += P.cum_z[a][nxt][j] < uo;
+  o = o < P.O - 1 ? o : P.O - 1;
+  reward = P.reward[s.idx][a];
+  const bool term = P.terminal[nxt] || s.terminal;
+  obs = term ? (uint32_t)P.O : (uint32_t)o;     // the terminal observation code is |O|
+  if (s.terminal) {                             // absorbing
+    reward = 0.0;
+    return;
+  }
+  s.idx = nxt;
+  s.terminal = term ? 1 : 0;
+}
+__device__ double heuristic(const Params&, const State&) { return 0.0; }
+__device__ double obs_log_likelihood(const Params& P, const State& s, int a, uint32_t obs) {
+  if (obs == (uint32_t)P.O) return s.terminal ? 0.0 : -INFINITY;
+  if (s.terminal) return -INFINITY;
+  return P.log_z[a][s.idx][obs];
+}
+"""
+
+TAB_STATE = np.dtype([("idx", "<i4"), ("terminal", "<i4")])
+TAB_PARAMS = np.dtype([("S", "<i4"), ("A", "<i4"), ("O", "<i4"), ("pad", "<i4"),
+                       ("cum_t", "<f8", (8, 8, 8)), ("cum_z", "<f8", (8, 8, 8)), ("log_z", "<f8", (8, 8, 8)),
+                       ("reward", "<f8", (8, 8)), ("terminal", "<i4", (8,))])
+
+
+def tabular_cuda_model(pomdp) -> CudaModel:
+    """A plug-in CudaModel of a TabularPOMDP (the reference's or ours)."""
+    t = np.asarray(pomdp.transitions, dtype=np.float64)
+    z = np.asarray(pomdp.observations, dtype=np.float64)
+    A, S, O = t.shape[0], t.shape[1], z.shape[2]
+    if max(A, S, O) > TAB_MAX:
+        raise ValueError(f"the tabular plug-in holds <= {TAB_MAX} states / actions / observations")
+    p = np.zeros((), dtype=TAB_PARAMS)
+    p["S"], p["A"], p["O"] = S, A, O
+    p["cum_t"][:A, :S, :S] = np.cumsum(t, axis=2)
+    p["cum_z"][:A, :S, :O] = np.cumsum(z, axis=2)
+    with np.errstate(divide="ignore"):
+        p["log_z"][:A, :S, :O] = np.log(z)
+    p["reward"][:S, :A] = np.asarray(pomdp.rewards, dtype=np.float64)
+    term = np.asarray(pomdp.terminal_states, dtype=bool)
+    p["terminal"][:S] = term
+    init = np.cumsum(np.asarray(pomdp.initial_belief, dtype=np.float64))
+
+    def initial_states(n, rng):  # tabular.py sample_initial_states
+        u = rng.uniform(np.arange(n, dtype=np.int64))
+        idx = np.minimum(np.searchsorted(init, u, side="right"), len(init) - 1)
+        out = np.zeros(n, dtype=TAB_STATE)
+        out["idx"], out["terminal"] = idx, term[idx]
+        return out
+
+    spec = ProblemSpec(f"{pomdp.name}-cuda", A, O, float(pomdp.discount), int(pomdp.max_steps))
+    return CudaModel(spec, TAB_STATE, TABULAR_SOURCE, p, initial_states=initial_states)
+
+
+CORRIDOR_SOURCE = r"""
+// 1-D corridor: position x in [0, L), door at L - 1.  Actions: 0 left, 1 right, 2 open door.
+// Motion noise N(0, 0.1) per move; the range sensor reads the distance to the door plus
+// N(0, sigma) noise, binned into nbins bins of width bin_w.
+struct Params {
+  double length, sigma, bin_w, move_noise;
+  int32_t nbins, pad;
+};
+struct State {
+  double x;
+  int32_t terminal, pad;
+};
+__device__ int bin_of(const Params& P, double d) {
+  int b = (int)floor(d / P.bin_w);
+  return b < 0 ? 0 : (b >= P.nbins ? P.nbins - 1 : b);
+}
+__device__ void step(const Params& P, State& s, int a, const RowDraws& rng, uint32_t& obs, double& reward) {
+  if (s.terminal) { obs = (uint32_t)P.nbins; reward = 0.0; return; }
+  if (a == 2) {                                     // open: +10 at the door, -5 elsewhere; ends
+    const bool at_door = fabs(s.x - (P.length - 1.0)) < 0.5;
+    reward = at_door ? 10.0 : -5.0;
+    s.terminal = 1;
+    obs = (uint32_t)P.nbins;
+    return;
+  }
+  const double dx = (a == 1 ? 1.0 : -1.0) + P.move_noise * rng.normal(0);
+  s.x = fmin(fmax(s.x + dx, 0.0), P.length - 1.0);
+  reward = -0.1;
+  const double reading = (P.length - 1.0 - s.x) + P.sigma * rng.normal(1);
+  obs = (uint32_t)bin_of(P, reading);
+}
+__device__ double heuristic(const Params& P, const State& s) {
+  return s.terminal ? 0.0 : 10.0 * pow(0.95, fabs(P.length - 1.0 - s.x));
+}
+__device__ double obs_log_likelihood(const Params& P, const State& s, int, uint32_t obs) {
+  if (obs == (uint32_t)P.nbins) return s.terminal ? 0.0 : -INFINITY;
+  if (s.terminal) return -INFINITY;
+  // mass of the reading's bin under N(distance, sigma); the end bins are open
+  const double mu = P.length - 1.0 - s.x, k = 1.0 / (P.sigma * sqrt(2.0));
+  const double lo = obs == 0 ? -INFINITY : obs * P.bin_w, hi = (int)obs == P.nbins - 1 ? INFINITY : (obs + 1) * P.bin_w;
+  const double m = 0.5 * (erf((hi - mu) * k) - erf((lo - mu) * k));
+  return m > 0.0 ? log(m) : -INFINITY;
+}
+"""
+
+CORRIDOR_STATE = np.dtype([("x", "<f8"), ("terminal", "<i4"), ("pad", "<i4")])
+CORRIDOR_PARAMS = np.dtype([("length", "<f8"), ("sigma", "<f8"), ("bin_w", "<f8"), ("move_noise", "<f8"),
+                            ("nbins", "<i4"), ("pad", "<i4")])
+
+
+def corridor_cuda_model(length: float = 20.0, sigma: float = 1.5, nbins: int = 16) -> CudaModel:
+    p = np.zeros((), dtype=CORRIDOR_PARAMS)
+    p["length"], p["sigma"], p["bin_w"], p["move_noise"], p["nbins"] = length, sigma, length / nbins, 0.1, nbins
+
+    def initial_states(n, rng):  # x ~ U[0, L/2)
+        out = np.zeros(n, dtype=CORRIDOR_STATE)
+        out["x"] = rng.derive(0).uniform(np.arange(n, dtype=np.int64)) * (length / 2.0)
+        return out
+
+    spec = ProblemSpec("corridor-cuda", 3, nbins, 0.95, 60)
+    return CudaModel(spec, CORRIDOR_STATE, CORRIDOR_SOURCE, p, initial_states=initial_states)

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 from .envs._device import device_model
-from .rng import key_of
+from .rng import key_of, kind_of
 
 SITE_ACTION = 0
 SITE_MODEL = 1
@@ -131,7 +131,7 @@ def run_search(tree, dm, work: Workspace, search_key: int, depth0: int, d_max: i
         work.leaf_count.zero_()  # the leaf-list parity chain restarts (fresh tree or another tree)
     work.last_pass = pass_
     stream = _torch().cuda.current_stream().cuda_stream
-    _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args), stream)
+    dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args), stream)
     tree._scratch_dirty = True
 
 
@@ -172,6 +172,7 @@ def search(tree, model, batch: SearchBatch, d_max: int, eta: float, rng, *, inje
         arr[: d_max] = np.asarray(inject_actions, dtype=np.int32).reshape(d_max, n)
         inject = torch.from_numpy(arr.reshape(-1)).cuda()
     pass_ = tree.next_pass()
+    dm.desc.rng_kind = kind_of(rng)
     run_search(tree, dm, work, key_of(rng), batch.depth, d_max, pass_, inject, start)
     leaves = LeafResult(tree, work, batch.depth, d_max, pass_, tree.generation)
     tree.last_search = leaves
@@ -222,7 +223,7 @@ def search_recorded(tree, model, actions, observations, rewards, leaf_values) ->
         work.leaf_count.zero_()
     work.last_pass = pass_
     stream = torch.cuda.current_stream()
-    _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
+    dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
               stream.cuda_stream)
     stream.synchronize()  # the injected columns are temporaries
     tree._scratch_dirty = True

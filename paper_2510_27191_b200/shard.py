@@ -32,7 +32,7 @@ import ctypes as C
 
 from . import _lib
 from .backup import run_backup
-from .rng import fold, key_of
+from .rng import fold, key_of, kind_of
 from .search import Workspace
 from .solver import SITE_DRAW, SITE_SEARCH, Planner, PlanOutcome, _validate_config
 from .tree import TreeHandle
@@ -131,6 +131,7 @@ class ShardedPlanner(Planner):
             tw = self._traj_work = Workspace(m_rows, levels, dm.state_bytes, trace=True)
         particles, cumw, m = resident if resident is not None else self.upload_belief(dm, belief)
         key = key_of(rng)
+        dm.desc.rng_kind = kind_of(rng)
         stream = torch.cuda.current_stream().cuda_stream
         d_max = 1
         ev = []
@@ -154,7 +155,7 @@ class ShardedPlanner(Planner):
                 args.mode, args.row0 = _lib.VP_SEARCH_TRAJECTORY, row0
                 args.particles, args.cum_weights, args.m = particles.data_ptr(), cumw.data_ptr(), m
                 args.draw_key = fold(it_key, SITE_DRAW)
-                _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(tw.struct), C.byref(args),
+                dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(tw.struct), C.byref(args),
                           stream)
                 a = tw.trace_action[: d_max * cnt].view(d_max, cnt)
                 o = tw.trace_obs[: d_max * cnt].view(d_max, cnt)
@@ -177,7 +178,7 @@ class ShardedPlanner(Planner):
             if pass_ != work.last_pass + 1:
                 work.leaf_count.zero_()
             work.last_pass = pass_
-            _lib.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
+            dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
                       stream)
             tree._scratch_dirty = True
             mark("insert")

@@ -23,7 +23,7 @@ from . import _lib
 from .backup import run_backup
 from .belief import DeviceBelief, ParticleBelief, sir_update, uniform_cum
 from .envs._device import device_model
-from .rng import RowRng, fold, key_of
+from .rng import PhiloxRowRng, RowRng, fold, key_of, kind_of
 from .search import Workspace, run_search
 from .tree import DeviceTree, TreeHandle
 
@@ -221,6 +221,7 @@ class Planner:
         _validate_config(config)
         fixed = config.iterations is not None and inject_actions is None and not trace
         dm, tree, work = self.prepare(model, config, trace, device_init=not fixed)
+        dm.desc.rng_kind = kind_of(rng)  # the stream kind of the caller's rng (PhiloxRowRng: fast mode)
         if fixed and not self.fits_fixed(tree, config):
             tree.reset(tree.init_prefs, config.eta)  # device reset for the iterative path
             fixed = False
@@ -275,7 +276,7 @@ class Planner:
         a.keys_host, a.keys_dev = kh.data_ptr(), kd.data_ptr()
         a.out_host, a.out_dev = oh.data_ptr(), od.data_ptr()
         stream = torch.cuda.current_stream()
-        _lib.call("vp_plan", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(a),
+        dm.call("vp_plan", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(a),
                   stream.cuda_stream)
         stream.synchronize()
         tree.pass_cursor = iters  # vp_plan numbers its passes 1..iterations on the fresh tree
@@ -440,15 +441,19 @@ def _identity_hooks(model) -> bool:
 
 
 def run_episode(model, config, seed: int, run_index: int = 0, *, precision: str = "fp32",
-                exact: bool = False, device_belief: bool | None = None) -> RunRecord:
+                exact: bool = False, device_belief: bool | None = None, rng_kind: str = "splitmix64") -> RunRecord:
     """Plan / execute / filter loop (solver.py:130-194) around the device plan.
 
     ``device_belief`` (default: fast mode with identity belief hooks) keeps the
     particles in HBM and runs the SIR update on the device (belief.py:47-102);
     otherwise the update runs through the model's host step_batch, as the
-    reference does (the fp64 parity mode reproduces the reference's episodes)."""
+    reference does (the fp64 parity mode reproduces the reference's episodes).
+    ``rng_kind="philox"`` draws every stream of the episode from Philox4x32-10
+    (the fast mode; statistically, not bitwise, the reference's episodes)."""
     spec = model.spec
-    root = RowRng.from_seed(seed)
+    if rng_kind not in ("splitmix64", "philox"):
+        raise ValueError(f"rng_kind must be 'splitmix64' or 'philox', got {rng_kind!r}")
+    root = (PhiloxRowRng if rng_kind == "philox" else RowRng).from_seed(seed)
     env_rng = root.derive(NS_ENV)
     env_state = model.sample_initial_states(1, env_rng.derive(0))
     belief = ParticleBelief.from_model(model, config.particles, root.derive(NS_INIT_BELIEF))
