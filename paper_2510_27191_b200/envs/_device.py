@@ -451,7 +451,8 @@ def device_model(model) -> DeviceModel:
         # e.g. with another reference policy, keep their device layout)
         known = next((i for i, c in enumerate(mro) if c.__name__ in _BY_NAME), None)
         if known is None:
-            raise TypeError(f"no device model for {type(model).__name__}; supported: {sorted(_BY_NAME)}")
+            raise TypeError(f"no device model for {type(model).__name__}; supported: {sorted(_BY_NAME)} -- or state "
+                            f"its dynamics in CUDA as a paper_2510_27191_b200.CudaModel plug-in")
     # a subclass that changes the dynamics the device runs (the generative step, the leaf
     # heuristic, the SIR likelihood) must not silently plan with its base's device model
     for c in mro[:known]:

@@ -118,3 +118,42 @@ def test_plugin_only_model_plans_and_runs():
     assert np.isfinite(rec.discounted_return) and rec.steps >= 1
     p = vp.run_episode(m, vp.SolverConfig(n_parallel=4096, iterations=8, particles=2000), seed=3, rng_kind="philox")
     assert np.isfinite(p.discounted_return)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_plugin_sharded_plan_equals_reference(tiger, world):
+    """The sharded planner routes the plug-in's trajectory / insert passes to its library too."""
+    case = manifest()["plans"]["plan_tiger"]
+    g = load("plan_tiger")
+    run = case["runs"][0]
+    s = run["seed"]
+    om, belief, cfg, rng = plan_inputs(case, s)
+    out = vp.ShardedPlanner(world=world, precision="fp64", exact=True).plan(belief, tiger, cfg, rng, keep_tree=True)
+    assert out.tree_stats == run["tree_stats"]
+    t = out.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(t[k], g[f"s{s}_{k}"].astype(np.int64), err_msg=k)
+    assert out.chosen_action == run["chosen_action"]
+
+
+def test_plugin_with_reference_policy(tiger):
+    """reference_log_probs (core.py:109-112) of a plug-in shape the initial PSI rows like a built-in's."""
+    om = oracle.tiger_model()
+    logp = np.log(np.array([0.6, 0.2, 0.2]))
+    biased = vp.CudaModel(tiger.spec, tiger.state_dtype, tiger.source, tiger.params,
+                          reference_log_probs=logp)
+
+    class BiasedTiger(oracle.TabularModel):
+        def reference_log_probs(self):
+            return logp.copy()
+
+    ob = BiasedTiger(om.pomdp)
+    belief = oracle.ParticleBelief.from_model(om, 1000, oracle.RowRng.from_seed(6).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=512, iterations=6)
+    rng = oracle.RowRng.from_seed(6).derive(1, 0)
+    want = oracle.plan(belief, ob, cfg, rng)
+    out = vp.plan(belief, biased, cfg, rng, precision="fp64", exact=True, keep_tree=True)
+    assert out.tree_stats == want.tree_stats and out.chosen_action == want.chosen_action
+    t, w = out.tree.tables(), want.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(t[k], np.asarray(w[k]).astype(np.int64), err_msg=k)
