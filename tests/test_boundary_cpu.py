@@ -218,3 +218,15 @@ def test_plan_keys_host_function_matches_fold():
         assert _lib.load().vp_plan_keys(C.c_uint64(key), 13, out.ctypes.data) == 0
         want = [fold(fold(key, i), s) for i in range(13) for s in (0, 1)]
         np.testing.assert_array_equal(out, np.array(want, dtype=np.uint64))
+
+
+# vecpomdp/__init__.py:10-48 __all__ (the reference's public names)
+REFERENCE_ALL = ['BeliefTree', 'BoundRng', 'LeafResult', 'LevelValues', 'ParticleBelief', 'PlanOutcome', 'ProblemModel', 'ProblemSpec', 'RowRng', 'RunRecord', 'SearchBatch', 'SirUpdate', 'SolverConfig', 'StateBatch', 'StepResult', 'action_q_values', 'aggregate_leaves', 'backup', 'init_tree', 'log_sum_exp_rows', 'match_or_append_pairs', 'plan', 'run_episode', 'sample_actions', 'search', 'sir_update', 'softmax_rows', 'systematic_resample']
+
+
+def test_every_reference_public_name_is_exported():
+    missing = [n for n in REFERENCE_ALL if not hasattr(vp, n) or n not in vp.__all__]
+    assert missing == []
+    envs = ["CrowdNavModel", "MarsModel", "NavigationModel", "TabularModel", "TabularPOMDP", "tiger_model",
+            "problem_from_config"]  # vecpomdp/envs/__init__.py __all__
+    assert [n for n in envs if not hasattr(vp.envs, n)] == []
