@@ -74,11 +74,13 @@ def compile_plugin(source: str, *, verbose: bool = False) -> str:
         if not os.path.exists(nvcc):
             raise _lib.LibraryMissing("compiling a CudaModel needs nvcc (CUDA 12.9); there is no CPU fallback")
         os.makedirs(PLUGIN_DIR, exist_ok=True)
-        stem = path[:-3]
+        # per-process temporaries, published with an atomic rename: concurrent builders of the
+        # same source (e.g. torchrun ranks) never read a half-written file
+        stem = f"{path[:-3]}.{os.getpid()}"
         src = stem + ".cuh"
         with open(src, "w") as f:
             f.write(source)
-        tmp = f"{stem}.{os.getpid()}.tmp.so"
+        tmp = stem + ".tmp.so"
         cmd = [nvcc, *NVCC_FLAGS, f'-DVP_PLUGIN_SOURCE="{src}"', "-DVP_PLUGIN_ONLY", "-o", tmp,
                os.path.join(CSRC, "vp_kernels.cu")]
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -87,6 +89,7 @@ def compile_plugin(source: str, *, verbose: bool = False) -> str:
             raise RuntimeError(f"CudaModel source failed to compile:\n{res.stderr[-4000:]}")
         if verbose:
             print(res.stderr)
+        os.replace(src, path[:-3] + ".cuh")  # kept beside the library (its -lineinfo source)
         os.replace(tmp, path)
     return path
 
