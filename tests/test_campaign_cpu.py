@@ -92,3 +92,12 @@ def test_campaign_runs_split_over_ranks_gloo():
     want_mean = np.mean([i * 1.5 - 2.0 for i in range(7)])
     for rank, idx, mean in res:
         assert idx == list(range(7)) and mean == pytest.approx(want_mean)
+
+
+def test_cli_stream_kind():
+    cfg = config_from_args(build_parser().parse_args(["--problem", "tiger", "--iterations", "2", "--rng", "philox"]))
+    assert cfg.rng_kind == "philox" and cfg.to_dict()["rng_kind"] == "philox"
+    cfg = config_from_args(build_parser().parse_args(["--problem", "tiger", "--iterations", "2"]))
+    assert cfg.rng_kind == "splitmix64"
+    with pytest.raises(SystemExit):
+        build_parser().parse_args(["--problem", "tiger", "--rng", "xorshift"])
