@@ -20,6 +20,8 @@ Cases (see SURVEY.md section 4 "parity ladder" and Appendix C):
 * acceptance  -- the reference's acceptance oracles (oracle.py; SPEC.md ACCEPTANCE 1, 4, 5):
                  serial_backup on random trees, exact_value_iteration on Tiger,
                  exact_bayes_filter on random 2-state chains
+* serial_search -- SPEC.md ACCEPTANCE 2: the reference's serial_search_backup trees
+                 (width-1 episodes, 4x4 MARS toys, d_max <= 4) as to_text() dumps
 """
 
 from __future__ import annotations
@@ -300,6 +302,29 @@ ACCEPT_HORIZONS = (1, 2, 3, 5, 8)  # Tiger exact value iteration
 ACCEPT_FILTERS = 10      # random 2-state chains x 10 (a, o) steps
 
 
+# SPEC #2 (oracle equivalence -- search): width-1 episodes on a 4x4 MARS toy, the reference's
+# serial_search_backup (oracle.py:176-206) building the tree episode by episode
+SERIAL_CASES = [(4, 3, 5, 2, 30, 0.05), (4, 3, 6, 3, 30, 0.1), (4, 4, 7, 4, 40, 0.05)]  # n, m, seed, d cap, episodes, eta
+
+
+def gen_serial_search():
+    from vecpomdp import oracle as ro
+
+    out = {}
+    for n, m, seed, dcap, episodes, eta in SERIAL_CASES:
+        model = MarsModel(n=n, m=m, layout_seed=seed)
+        belief = ref.ParticleBelief.from_model(model, 200, ref.RowRng.from_seed(seed).derive(3))
+        tree = ro.SerialTree(model.spec.action_count)
+        for e in range(episodes):
+            it = ref.RowRng.from_seed(seed).derive(1, e)
+            state = belief.sample_states(1, it.derive(0))
+            ro.serial_search_backup(model, state, it.derive(1), min(e + 1, dcap), eta, model.spec.discount,
+                                    tree=tree)
+        out[f"mars{n}_{m}_s{seed}"] = np.array(tree.to_text())
+    np.savez_compressed(os.path.join(HERE, "serial_search.npz"), **out)
+    print("serial_search:", list(out))
+
+
 def two_state_chain(g):
     """A random 2-state, 2-action, 2-observation tabular chain (SPEC #5)."""
     t = g.dirichlet([2.0, 2.0], size=(2, 2))
@@ -371,6 +396,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["acceptance"]:
         gen_acceptance()
         sys.exit(0)
+    if sys.argv[1:] == ["serial"]:
+        gen_serial_search()
+        sys.exit(0)
     if sys.argv[1:] == ["large"]:
         with open(os.path.join(HERE, "manifest.json")) as f:
             manifest = json.load(f)
@@ -392,6 +420,7 @@ if __name__ == "__main__":
     gen_rng()
     gen_formulas()
     gen_acceptance()
+    gen_serial_search()
     manifest = {"plans": gen_plans(), "large_plans": gen_large(), "episodes": dict(gen_episodes(), episode_crowdnav40=gen_crowd_episodes()),
                 "numpy": np.__version__, "reference": "/root/reference/pkg/src/vecpomdp @ 0.1.0"}
     with open(os.path.join(HERE, "manifest.json"), "w") as f:

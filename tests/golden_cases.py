@@ -68,3 +68,39 @@ def tree_columns(tables: dict) -> dict:
     out["prefs_row_sum"] = prefs.sum(axis=1)
     out["prefs_root"] = prefs[0]
     return out
+
+
+# SPEC.md ACCEPTANCE 2 (make_golden.gen_serial_search): n, m, seed, d_max cap, episodes, eta
+SERIAL_CASES = [(4, 3, 5, 2, 30, 0.05), (4, 3, 6, 3, 30, 0.1), (4, 4, 7, 4, 40, 0.05)]
+
+
+def serial_search_build(vpmod, case, make_tree, **plan_kw):
+    """Width-1 episodes through ``vpmod``'s search + backup (the vectorized path at n_p = 1),
+    episode e from rng.derive(1, e) exactly as the reference's serial_search_backup builds it."""
+    n, m, seed, dcap, episodes, eta = case
+    model = vpmod.MarsModel(n=n, m=m, layout_seed=seed)
+    belief = vpmod.ParticleBelief.from_model(model, 200, oracle.RowRng.from_seed(seed).derive(3))
+    tree = make_tree(model)
+    for e in range(episodes):
+        it = oracle.RowRng.from_seed(seed).derive(1, e)
+        state = belief.sample_states(1, it.derive(0))
+        d = min(e + 1, dcap)
+        leaves = vpmod.search(tree, model, vpmod.SearchBatch(np.zeros(1, dtype=np.int64), state), d, eta, it.derive(1))
+        vpmod.backup(tree, leaves, d, eta, model.spec.discount)
+    return tree
+
+
+def parse_tree_text(text):
+    """to_text() / serialize() dump -> (integer rows, float rows) for tolerance comparisons."""
+    ints, floats = [], []
+    for line in text.splitlines():
+        f = line.split("\t")
+        if f[0] == "B":
+            ints.append(tuple(int(x) for x in f[1:]))
+        elif f[0] == "A":
+            ints.append((int(f[1]), int(f[2]), int(f[3]), int(f[5])))
+            floats.append(float(f[4]))
+        elif f[0] == "P":
+            ints.append((int(f[1]), int(f[2])))
+            floats.extend(float(x) for x in f[3:])
+    return ints, np.array(floats)

@@ -88,3 +88,17 @@ def test_exact_bayes_filter_equals_reference():
         p = oracle.TabularPOMDP(np.ones((1, 2, 2)) / 2, z, np.zeros((2, 1)), np.array([0.5, 0.5]), 0.9,
                                 np.array([False, False]))
         acc.exact_bayes_filter(p, [0.5, 0.5], 0, 1)
+
+
+@pytest.mark.parametrize("case", __import__("golden_cases").SERIAL_CASES)
+def test_oracle_width1_search_equals_reference_serial_search(case):
+    """SPEC ACCEPTANCE 2 for the oracle: its vectorized search + backup at n_p = 1 rebuild the
+    reference's serial_search_backup tree (integer fields exact, floats within 1e-9)."""
+    from golden_cases import parse_tree_text, serial_search_build
+
+    n, m, seed = case[:3]
+    want_i, want_f = parse_tree_text(str(load("serial_search")[f"mars{n}_{m}_s{seed}"]))
+    tree = serial_search_build(oracle, case, lambda model: oracle.tree.init_tree(model.spec))
+    got_i, got_f = parse_tree_text(tree.serialize())
+    assert got_i == want_i
+    np.testing.assert_allclose(got_f, want_f, rtol=0, atol=1e-9)

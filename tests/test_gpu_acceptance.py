@@ -147,3 +147,23 @@ def test_spec5_device_sir_matches_exact_bayes_filter(exact):
             worst = max(worst, float(np.abs(est - b).max()))
     print(f"SIR vs exact filter: worst |posterior error| {worst:.4f} over 50 x 10 updates")
     assert worst <= 0.01
+
+
+@pytest.mark.parametrize("case", __import__("golden_cases").SERIAL_CASES)
+@pytest.mark.parametrize("precision,exact", [("fp64", True), ("fp64", False), ("fp32", False)])
+def test_width1_device_search_equals_reference_serial_search(case, precision, exact):
+    """SPEC ACCEPTANCE 2: with n_p = 1, fixed seeds, d_max <= 4, on 4x4 MARS toys, the device
+    search + backup (one width-1 pass per episode) rebuild the reference's serial_search_backup
+    tree: integer fields bit-identical, floats within 1e-9 (fp64; fp32 storage: 1e-5 relative)."""
+    from golden_cases import parse_tree_text, serial_search_build
+
+    n, m, seed = case[:3]
+    want_i, want_f = parse_tree_text(str(load("serial_search")[f"mars{n}_{m}_s{seed}"]))
+    tree = serial_search_build(vp, case, lambda model: vp.init_tree(model.spec, eta=case[5], precision=precision,
+                                                                     exact=exact))
+    got_i, got_f = parse_tree_text(tree.serialize())
+    assert got_i == want_i
+    if precision == "fp64":
+        np.testing.assert_allclose(got_f, want_f, rtol=0, atol=1e-9)
+    else:
+        np.testing.assert_allclose(got_f, want_f, rtol=1e-5, atol=1e-5 * np.abs(want_f).max())
