@@ -167,3 +167,37 @@ def test_width1_device_search_equals_reference_serial_search(case, precision, ex
         np.testing.assert_allclose(got_f, want_f, rtol=0, atol=1e-9)
     else:
         np.testing.assert_allclose(got_f, want_f, rtol=1e-5, atol=1e-5 * np.abs(want_f).max())
+
+
+@pytest.mark.parametrize("precision,exact", [("fp64", True), ("fp64", False), ("fp32", False)])
+def test_formula_checks_spec3(precision, exact):
+    """SPEC ACCEPTANCE 3 (Eq. 3 / Eq. 6 properties) on the device LSE: max <= LSE <= max + log|A|/eta
+    on 10^5 random rows; constant-row LSE = c + log|A|/eta within 1e-12 (fp64); the softmax built
+    from it sums to 1 within 1e-9 and is shift-invariant."""
+    g = np.random.default_rng(11)
+    eta = 2.0
+    for A in (2, 9, 64, 256):
+        rows = g.normal(size=(100_000 // A * 4 if A > 16 else 100_000, A)) * 5.0
+        if precision == "fp32":
+            rows = rows.astype(np.float32).astype(np.float64)
+        lse = vp.log_sum_exp_rows(rows, eta, precision=precision, exact=exact)
+        mx = rows.max(axis=1)
+        slack = 1e-12 if precision == "fp64" else 1e-5 * np.maximum(np.abs(mx), 1.0)
+        assert np.all(lse >= mx - slack) and np.all(lse <= mx + np.log(A) / eta + slack)
+        p = np.exp(eta * (rows - lse[:, None]))
+        tol = 1e-9 if precision == "fp64" else 1e-5
+        assert np.all(np.abs(p.sum(axis=1) - 1.0) <= tol)
+        shift = g.normal(size=(len(rows), 1)) * 3.0
+        if precision == "fp32":
+            shift = np.round(shift * 8) / 8  # exactly representable shifts keep fp32 rows exact
+        lse2 = vp.log_sum_exp_rows(rows + shift, eta, precision=precision, exact=exact)
+        p2 = np.exp(eta * (rows + shift - lse2[:, None]))
+        np.testing.assert_allclose(p2, p, rtol=0, atol=tol)
+        c = g.normal(size=(1000, 1)) * 10.0
+        const = np.repeat(c, A, axis=1)
+        lc = vp.log_sum_exp_rows(const, eta, precision=precision, exact=exact)
+        want = c[:, 0] + np.log(A) / eta
+        if precision == "fp64":
+            np.testing.assert_allclose(lc, want, rtol=0, atol=1e-12)
+        else:
+            np.testing.assert_allclose(lc, want, rtol=1e-6, atol=1e-5)
