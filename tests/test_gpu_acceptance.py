@@ -201,3 +201,33 @@ def test_formula_checks_spec3(precision, exact):
             np.testing.assert_allclose(lc, want, rtol=0, atol=1e-12)
         else:
             np.testing.assert_allclose(lc, want, rtol=1e-6, atol=1e-5)
+
+
+def test_batch_scaling_sanity_spec10():
+    """SPEC ACCEPTANCE 10: episodes simulated per second at n_p = 32 768 are >= 8x those at
+    n_p = 1 024 (RockSample(7,8), 8 iterations, belief resident, median of 5 planning steps)."""
+    import torch
+    from paper_2510_27191_b200.rng import key_of
+
+    model = vp.MarsModel(7, 8, layout_seed=1)
+    belief = vp.ParticleBelief.from_model(model, 2000, vp.RowRng.from_seed(1).derive(3))
+    rate = {}
+    for n in (1024, 32768):
+        cfg = vp.SolverConfig(n_parallel=n, iterations=8)
+        planner = vp.Planner("fp32")
+        dm = vp.device_model(model)
+        _, _, m = planner.upload_belief(dm, belief)
+        ms = []
+        for t in range(8):
+            d, tree, work = planner.prepare(model, cfg, device_init=False)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            planner.run_fixed(d, tree, work, m, model.spec, cfg, key_of(vp.RowRng.from_seed(1).derive(1, t)),
+                              from_host=False)
+            e1.record()
+            torch.cuda.synchronize()
+            if t >= 3:
+                ms.append(e0.elapsed_time(e1))
+        rate[n] = n * sum(range(1, 9)) / sorted(ms)[len(ms) // 2]
+    assert rate[32768] >= 8.0 * rate[1024], rate
