@@ -128,7 +128,9 @@ class BoundRng:
 # derive exactly as above (SplitMix64 folds); only the per-row draw changes:
 #     block(key, row, j, tag) = Philox4x32-10(ctr = (lo row, hi row, lo j, tag), key = (lo key, hi key))
 #     uniform  (tag 0; j = 0 single draw, j = 1..k)  = top 53 bits of (x << 32 | y) * 2**-53
-#     normal   (tag 1)  = Box-Muller of u1 = (bits(x, y) + 1) 2**-53, u2 = bits(z, w) 2**-53
+#     normal   (tag 1)  = Box-Muller pairs: block b = (j + 1) // 2, u1 = (bits(x, y) + 1) 2**-53,
+#                         u2 = bits(z, w) 2**-53, R = sqrt(-2 log u1); normal j = R cos(2 pi u2) for
+#                         odd j (and j = 0), R sin(2 pi u2) for even j
 
 PHILOX_M0, PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
 PHILOX_W0, PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
@@ -189,9 +191,10 @@ class PhiloxRowRng(RowRng):
         return u[:, 0] if k is None else u
 
     def normal(self, rows, k: int | None = None) -> np.ndarray:
-        js = [0] if k is None else range(1, k + 1)
-        b = philox_row_blocks(self.key, rows, js, 1)
+        js = np.array([0] if k is None else range(1, k + 1), dtype=np.int64)
+        b = philox_row_blocks(self.key, rows, (js + 1) // 2, 1)
         u1 = (_bits53(b[..., 0], b[..., 1]).astype(np.float64) + 1.0) * _SCALE
         u2 = _bits53(b[..., 2], b[..., 3]).astype(np.float64) * _SCALE
-        z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+        r = np.sqrt(-2.0 * np.log(u1))
+        z = np.where(((js == 0) | (js % 2 == 1))[None, :], r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2))
         return z[:, 0] if k is None else z

@@ -58,14 +58,16 @@ __device__ __forceinline__ double normal_j(u64 key, u64 row, u64 j) {
 // ---------------------------------------------------------------- Philox fast mode
 //
 // vp_model.rng_kind = VP_RNG_PHILOX replaces the per-row SplitMix64 hash by
-// Philox4x32-10 (Salmon et al., SC'11; the constants of curand_philox4x32_x.h,
-// checked against curand_Philox4x32_10 in tests/test_gpu_philox.py).  The
+// Philox4x32-10 (Salmon et al., SC'11; the constants of curand_philox4x32_x.h;
+// pinned to the Random123 known-answer vectors, tests/test_gpu_philox.py).  The
 // stream keys (derive / fold: warp-uniform) are unchanged; a row's draw j of
 // the stream `key` is the block
 //   Philox4x32-10(counter = {lo(row), hi(row), lo(j), tag}, key = {lo(key), hi(key)})
 // with tag 0 for uniforms (j = 0: the single draw, j >= 1: the j-th of k) and
-// tag 1 for normals (one block per Box-Muller pair).  A uniform takes the top
-// 53 bits of {x, y}; a normal uses {x, y} + 1 ulp and {z, w} as (u1, u2).
+// tag 1 for normals.  A uniform takes the top 53 bits of {x, y}.  Normals come
+// in Box-Muller pairs: block b = (j + 1) / 2 gives u1 = bits{x, y} + 1 ulp,
+// u2 = bits{z, w}, R = sqrt(-2 log u1); normal j is R cos(2 pi u2) for odd j (and
+// j = 0), R sin(2 pi u2) for even j -- one block, one log and one sqrt per pair.
 // Not the reference's streams: trees differ from the reference's, their
 // statistics do not (oracle/rng.py: philox4x32_10, PhiloxRowRng).
 constexpr u32 kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
@@ -89,11 +91,17 @@ __device__ __forceinline__ double philox_unit(u64 key, u64 row, u64 j) {
   const uint4 b = philox_block(key, row, j, 0u);
   return unit53(((u64)b.x << 32) | b.y);
 }
+// the pair of block b: (R cos, R sin)
+__device__ __forceinline__ double2 philox_normal_pair(u64 key, u64 row, u64 b) {
+  const uint4 h = philox_block(key, row, b, 1u);
+  const double u1 = ((double)((((u64)h.x << 32) | h.y) >> 11) + 1.0) * kInv53;
+  const double u2 = (double)((((u64)h.z << 32) | h.w) >> 11) * kInv53;
+  const double r = sqrt(-2.0 * log(u1));
+  return make_double2(r * cos(kTwoPi * u2), r * sin(kTwoPi * u2));
+}
 __device__ __forceinline__ double philox_normal(u64 key, u64 row, u64 j) {
-  const uint4 b = philox_block(key, row, j, 1u);
-  const double u1 = ((double)((((u64)b.x << 32) | b.y) >> 11) + 1.0) * kInv53;
-  const double u2 = (double)((((u64)b.z << 32) | b.w) >> 11) * kInv53;
-  return sqrt(-2.0 * log(u1)) * cos(kTwoPi * u2);
+  const double2 z = philox_normal_pair(key, row, (j + 1) >> 1);
+  return (j == 0 || (j & 1)) ? z.x : z.y;
 }
 
 // Stream-kind dispatch (rk = vp_model.rng_kind: kernel-parameter uniform, no divergence).

@@ -266,7 +266,15 @@ struct LightDarkModel {
     const bool inside = s.x * s.x + s.y * s.y <= M.ld_goal_radius * M.ld_goal_radius;
     rew = declare ? (inside ? 100.0 : -100.0) : -1.0;
     const u64 nk = fold(mkey, 0);
-    const double z0 = normal_j(nk, row, 1, rkind), z1 = normal_j(nk, row, 2, rkind);
+    double z0, z1;  // rng.derive(0).normal(2): one Box-Muller pair in Philox mode
+    if (rkind) {
+      const double2 z = philox_normal_pair(nk, row, 1);
+      z0 = z.x;
+      z1 = z.y;
+    } else {
+      z0 = normal_j(nk, row, 1);
+      z1 = normal_j(nk, row, 2);
+    }
     const double sigma = M.ld_sigma0 + M.ld_sigma_slope * fabs(nx - M.ld_light_x);
     const int o = bin(M, nx + sigma * z0) * M.ld_bins + bin(M, ny + sigma * z1);
     const bool term = s.term || declare;
@@ -408,6 +416,17 @@ struct CrowdNavModel {
 
   // j-th of the row's Box-Muller normals from precomputed row bases (rng.py:81-89)
   // (Philox mode: b1 is the normal stream's key itself, one block per normal)
+  // person i's (x, y) motion normals, draws 2i+1 and 2i+2 (Philox: one Box-Muller pair)
+  static __device__ __forceinline__ void normal_xy(u64 b1, u64 b2, u64 row, int i, int rk, double& zx, double& zy) {
+    if (rk) {
+      const double2 z = philox_normal_pair(b1, row, (u64)(i + 1));
+      zx = z.x;
+      zy = z.y;
+    } else {
+      zx = normal_at(b1, b2, row, (u64)(2 * i + 1), 0);
+      zy = normal_at(b1, b2, row, (u64)(2 * i + 2), 0);
+    }
+  }
   static __device__ __forceinline__ double normal_at(u64 b1, u64 b2, u64 row, u64 j, int rk) {
     if (rk) return philox_normal(b1, row, j);
     const u64 h1 = mix64(b1 + j * kMixB), h2 = mix64(b2 + j * kMixB);
@@ -443,8 +462,10 @@ struct CrowdNavModel {
     bool bumped = false;
 #pragma unroll 2
     for (int i = 0; i < M.crowd_people; ++i) {
-      double x = (double)s.px[2 * i] + normal_at(b1, b2, row, (u64)(2 * i + 1), rkind) * M.crowd_noise;
-      double y = (double)s.px[2 * i + 1] + normal_at(b1, b2, row, (u64)(2 * i + 2), rkind) * M.crowd_noise;
+      double zx, zy;
+      normal_xy(b1, b2, row, i, rkind, zx, zy);
+      double x = (double)s.px[2 * i] + zx * M.crowd_noise;
+      double y = (double)s.px[2 * i + 1] + zy * M.crowd_noise;
       const double dx = rx - x, dy = ry - y;
       const double d = sqrt(dx * dx + dy * dy);
       const double u = stream_uniform(bu, row, (u64)(i + 1), rkind);
@@ -507,8 +528,10 @@ struct CrowdNavModel {
     const double bump2 = M.crowd_collision * M.crowd_collision * (1.0 + 1e-12);
     for (int i = lane; i < M.crowd_people; i += 32) {
       const float2 p = reinterpret_cast<const float2*>(s.px)[i];
-      double x = (double)p.x + normal_at(b1, b2, row, (u64)(2 * i + 1), rkind) * M.crowd_noise;
-      double y = (double)p.y + normal_at(b1, b2, row, (u64)(2 * i + 2), rkind) * M.crowd_noise;
+      double zx, zy;
+      normal_xy(b1, b2, row, i, rkind, zx, zy);
+      double x = (double)p.x + zx * M.crowd_noise;
+      double y = (double)p.y + zy * M.crowd_noise;
       const double dx = rx - x, dy = ry - y;
       const double s2 = dx * dx + dy * dy;
       if (s2 < near2) {

@@ -28,6 +28,7 @@ ap.add_argument("--particles", type=int, default=2000)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--rng", default="splitmix64", choices=["splitmix64", "philox"])
 ap.add_argument("--cpu", action="store_true", help="also time the oracle port on the host (one plan)")
 a = ap.parse_args()
 
@@ -37,11 +38,13 @@ cfg = vp.SolverConfig(n_parallel=a.n_parallel, iterations=a.iterations)
 planner = vp.Planner(a.precision)
 dm = vp.device_model(model)
 particles, cumw, m = planner.upload_belief(dm, belief)
-rngs = [vp.RowRng.from_seed(1000).derive(1, t) for t in range(a.warmup + a.steps)]
+rng_cls = vp.PhiloxRowRng if a.rng == "philox" else vp.RowRng
+rngs = [rng_cls.from_seed(1000).derive(1, t) for t in range(a.warmup + a.steps)]
 
 
 def step(t):
     d, tree, work = planner.prepare(model, cfg, device_init=False)
+    d.desc.rng_kind = 1 if a.rng == "philox" else 0
     return planner.run_fixed(d, tree, work, m, model.spec, cfg, key_of(rngs[t]), from_host=False)
 
 
@@ -68,7 +71,7 @@ prof = _lib.profile_read()
 _lib.profile_enable(False)
 sims = a.n_parallel * a.iterations
 res = {"workload": f"crowdnav {a.people} people, {a.n_parallel} rows x {a.iterations} iterations, "
-                   f"{a.particles} particles, {a.precision}",
+                   f"{a.particles} particles, {a.precision}, {a.rng} streams",
        "state_bytes": dm.state_bytes, "ms_per_step": ms, "sims_per_s": sims / (ms / 1e3),
        "e2e_ms_per_step": e2e_ms, "e2e_sims_per_s": sims / (e2e_ms / 1e3),
        "kernel_ms_per_step": {k: v[0] / 2 for k, v in prof.items() if v[1]},
