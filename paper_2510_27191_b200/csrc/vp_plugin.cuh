@@ -15,6 +15,8 @@
 //                        uint32_t& obs, double& reward);          // G(s, a), in place
 //   __device__ double heuristic(const Params&, const State&);     // leaf value, 0 on terminal
 //   __device__ double obs_log_likelihood(const Params&, const State& next, int a, uint32_t obs);
+// The source is included inside namespace vp_user after the library's headers: it must
+// not #include anything itself (<cstdint> types, CUDA math and the runtime are in scope).
 // RowDraws is the row's BoundRng (rng.py:96-120): rng.uniform(site) is
 // rng.derive(site).uniform(), rng.uniform(site, j) the j-th (1-based) of
 // rng.derive(site).uniform(k), and likewise normal(); either stream kind.

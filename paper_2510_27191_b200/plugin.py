@@ -17,7 +17,9 @@ model-independent and stay on the main library.
     model = vp.CudaModel(spec, state_dtype, source, params, initial_states=sampler)
     vp.plan(belief, model, SolverConfig(...), rng)
 
-``state_dtype`` is a numpy structured dtype laid out like the source's ``State``
+The source is compiled inside ``namespace vp_user`` and must not ``#include`` anything
+(fixed-width integer types and CUDA math are in scope).  ``state_dtype`` is a numpy
+structured dtype laid out like the source's ``State``
 struct and must have a ``terminal`` field; ``params`` (a structured scalar or raw
 bytes) is laid out like ``Params``.  There is no CPU fallback: without nvcc (the
 first use of a new source compiles) or a GPU the calls raise.
