@@ -14,6 +14,16 @@ for om, n, it in ((oracle.MarsModel(7, 8, layout_seed=1), 96, 4), (oracle.Synthe
         out.tree.validate()
     db = vp.DeviceBelief.from_host(b, om)
     vp.sir_update(db, om, 0, 0, oracle.RowRng.from_seed(5))
+    # Philox streams (fast mode) on the same plan
+    vp.plan(b, om, oracle.SolverConfig(n_parallel=n, iterations=it), vp.PhiloxRowRng.from_seed(1)).tree_stats
+# a user-model plug-in (CudaModel): plan + SIR through its plug-in build
+from paper_2510_27191_b200.envs.plugin_examples import corridor_cuda_model
+pm = corridor_cuda_model()
+pb = vp.ParticleBelief.from_model(pm, 200, vp.RowRng.from_seed(1).derive(3))
+for prec, exact in (("fp32", False), ("fp64", True)):
+    vp.plan(pb, pm, vp.SolverConfig(n_parallel=64, iterations=4), vp.RowRng.from_seed(1), precision=prec,
+            exact=exact, keep_tree=True).tree.validate()
+vp.sir_update(vp.DeviceBelief.from_host(pb, pm), pm, 1, 3, vp.RowRng.from_seed(5))
 print("plans ok")
 PY
 for tool in memcheck racecheck synccheck; do
