@@ -224,7 +224,7 @@ def search_recorded(tree, model, actions, observations, rewards, leaf_values) ->
     work.last_pass = pass_
     stream = torch.cuda.current_stream()
     dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
-              stream.cuda_stream)
+            stream.cuda_stream)
     stream.synchronize()  # the injected columns are temporaries
     tree._scratch_dirty = True
     leaves = LeafResult(tree, work, 0, d, pass_, tree.generation)

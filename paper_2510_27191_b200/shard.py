@@ -156,7 +156,7 @@ class ShardedPlanner(Planner):
                 args.particles, args.cum_weights, args.m = particles.data_ptr(), cumw.data_ptr(), m
                 args.draw_key = fold(it_key, SITE_DRAW)
                 dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(tw.struct), C.byref(args),
-                          stream)
+                        stream)
                 a = tw.trace_action[: d_max * cnt].view(d_max, cnt)
                 o = tw.trace_obs[: d_max * cnt].view(d_max, cnt)
                 r = tw.trace_reward[: d_max * cnt].view(d_max, cnt)
@@ -179,7 +179,7 @@ class ShardedPlanner(Planner):
                 work.leaf_count.zero_()
             work.last_pass = pass_
             dm.call("vp_search", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(args),
-                      stream)
+                    stream)
             tree._scratch_dirty = True
             mark("insert")
             run_backup(tree, work, pass_, model.spec.discount)

@@ -277,7 +277,7 @@ class Planner:
         a.out_host, a.out_dev = oh.data_ptr(), od.data_ptr()
         stream = torch.cuda.current_stream()
         dm.call("vp_plan", C.byref(tree.struct), C.byref(dm.desc), C.byref(work.struct), C.byref(a),
-                  stream.cuda_stream)
+                stream.cuda_stream)
         stream.synchronize()
         tree.pass_cursor = iters  # vp_plan numbers its passes 1..iterations on the fresh tree
         work.last_pass = iters
