@@ -1,7 +1,7 @@
 """Example ``CudaModel`` plug-ins (plugin.py): user ProblemModels written as CUDA.
 
-* ``tabular_cuda_model(pomdp)`` -- any small TabularPOMDP (<= 8 states, actions,
-  observations) as a plug-in: the tables travel in the ``Params`` block.  It restates
+* ``tabular_cuda_model(pomdp)`` -- any TabularPOMDP as a plug-in: its tables are uploaded
+  to HBM once (``CudaModel(tables=...)``) and reached through pointers in ``Params``.  It restates
   envs/tabular.py:106-145 (the reference's TabularModel) operation for operation, so
   its plans equal the reference's trees bit for bit -- the plug-in path's parity check.
 * ``corridor_cuda_model(length)`` -- a model that exists only as a plug-in: a robot in
@@ -17,17 +17,15 @@ import numpy as np
 from ..core import ProblemSpec
 from ..plugin import CudaModel
 
-TAB_MAX = 8
-
 TABULAR_SOURCE = r"""
-// A TabularPOMDP with <= 8 states / actions / observations (envs/tabular.py:106-145).
+// A TabularPOMDP of any size (envs/tabular.py:106-145); the tables live in HBM (CudaModel tables=).
 struct Params {
   int32_t S, A, O, pad;
-  double cum_t[8][8][8];   // [a][s][s'] cumulative transition rows
-  double cum_z[8][8][8];   // [a][s'][o] cumulative observation rows
-  double log_z[8][8][8];   // [a][s'][o] log Z
-  double reward[8][8];     // [s][a]
-  int32_t terminal[8];
+  const double* cum_t;      // [a][s][s'] cumulative transition rows
+  const double* cum_z;      // [a][s'][o] cumulative observation rows
+  const double* log_z;      // [a][s'][o] log Z
+  const double* reward;     // [s][a]
+  const int32_t* terminal;  // [s]
 };
 struct State {
   int32_t idx;
@@ -35,14 +33,16 @@ struct State {
 };
 __device__ void step(const Params& P, State& s, int a, const RowDraws& rng, uint32_t& obs, double& reward) {
   const double us = rng.uniform(0);             // rng.derive(0).uniform()
+  const double* ct = P.cum_t + ((size_t)a * P.S + s.idx) * P.S;
   int nxt = 0;
-  for (int j = 0; j < P.S; ++j) nxt += P.cum_t[a][s.idx][j] < us;
+  for (int j = 0; j < P.S; ++j) nxt += ct[j] < us;
   nxt = nxt < P.S - 1 ? nxt : P.S - 1;
   const double uo = rng.uniform(1);             // rng.derive(1).uniform()
+  const double* cz = P.cum_z + ((size_t)a * P.S + nxt) * P.O;
   int o = 0;
-  for (int j = 0; j < P.O; ++j) o += P.cum_z[a][nxt][j] < uo;
+  for (int j = 0; j < P.O; ++j) o += cz[j] < uo;
   o = o < P.O - 1 ? o : P.O - 1;
-  reward = P.reward[s.idx][a];
+  reward = P.reward[(size_t)s.idx * P.A + a];
   const bool term = P.terminal[nxt] || s.terminal;
   obs = term ? (uint32_t)P.O : (uint32_t)o;     // the terminal observation code is |O|
   if (s.terminal) {                             // absorbing
@@ -56,32 +56,28 @@ __device__ double heuristic(const Params&, const State&) { return 0.0; }
 __device__ double obs_log_likelihood(const Params& P, const State& s, int a, uint32_t obs) {
   if (obs == (uint32_t)P.O) return s.terminal ? 0.0 : -INFINITY;
   if (s.terminal) return -INFINITY;
-  return P.log_z[a][s.idx][obs];
+  return P.log_z[((size_t)a * P.S + s.idx) * P.O + obs];
 }
 """
 
 TAB_STATE = np.dtype([("idx", "<i4"), ("terminal", "<i4")])
-TAB_PARAMS = np.dtype([("S", "<i4"), ("A", "<i4"), ("O", "<i4"), ("pad", "<i4"),
-                       ("cum_t", "<f8", (8, 8, 8)), ("cum_z", "<f8", (8, 8, 8)), ("log_z", "<f8", (8, 8, 8)),
-                       ("reward", "<f8", (8, 8)), ("terminal", "<i4", (8,))])
+TAB_PARAMS = np.dtype([("S", "<i4"), ("A", "<i4"), ("O", "<i4"), ("pad", "<i4"), ("cum_t", "<u8"), ("cum_z", "<u8"),
+                       ("log_z", "<u8"), ("reward", "<u8"), ("terminal", "<u8")])
 
 
 def tabular_cuda_model(pomdp) -> CudaModel:
-    """A plug-in CudaModel of a TabularPOMDP (the reference's or ours)."""
+    """A plug-in CudaModel of a TabularPOMDP (the reference's or ours), any size."""
     t = np.asarray(pomdp.transitions, dtype=np.float64)
     z = np.asarray(pomdp.observations, dtype=np.float64)
     A, S, O = t.shape[0], t.shape[1], z.shape[2]
-    if max(A, S, O) > TAB_MAX:
-        raise ValueError(f"the tabular plug-in holds <= {TAB_MAX} states / actions / observations")
     p = np.zeros((), dtype=TAB_PARAMS)
     p["S"], p["A"], p["O"] = S, A, O
-    p["cum_t"][:A, :S, :S] = np.cumsum(t, axis=2)
-    p["cum_z"][:A, :S, :O] = np.cumsum(z, axis=2)
     with np.errstate(divide="ignore"):
-        p["log_z"][:A, :S, :O] = np.log(z)
-    p["reward"][:S, :A] = np.asarray(pomdp.rewards, dtype=np.float64)
+        log_z = np.log(z)
     term = np.asarray(pomdp.terminal_states, dtype=bool)
-    p["terminal"][:S] = term
+    tables = {"cum_t": np.cumsum(t, axis=2).reshape(-1), "cum_z": np.cumsum(z, axis=2).reshape(-1),
+              "log_z": log_z.reshape(-1), "reward": np.asarray(pomdp.rewards, dtype=np.float64).reshape(-1),
+              "terminal": term.astype(np.int32)}
     init = np.cumsum(np.asarray(pomdp.initial_belief, dtype=np.float64))
 
     def initial_states(n, rng):  # tabular.py sample_initial_states
@@ -92,7 +88,7 @@ def tabular_cuda_model(pomdp) -> CudaModel:
         return out
 
     spec = ProblemSpec(f"{pomdp.name}-cuda", A, O, float(pomdp.discount), int(pomdp.max_steps))
-    return CudaModel(spec, TAB_STATE, TABULAR_SOURCE, p, initial_states=initial_states)
+    return CudaModel(spec, TAB_STATE, TABULAR_SOURCE, p, initial_states=initial_states, tables=tables)
 
 
 CORRIDOR_SOURCE = r"""

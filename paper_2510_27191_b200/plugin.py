@@ -129,10 +129,13 @@ class CudaModel(ProblemModel):
     (numpy structured scalar / array / bytes).  ``initial_states(n, rng)``: host sampler
     returning a structured array of ``state_dtype`` (sample_initial_states, core.py:101).
     ``reference_log_probs``: optional log pi0 per action (default uniform).
+    ``tables``: {field: numpy array} uploaded to HBM once per model; the device address of each
+    is written into the ``Params`` field of that name (a pointer in the CUDA struct, a ``<u8``
+    field of a structured ``params``) -- constant tables of any size (maps, matrices).
     """
 
     def __init__(self, spec, state_dtype, source: str, params=None, initial_states=None,
-                 reference_log_probs=None):
+                 reference_log_probs=None, tables=None):
         self.spec = spec
         self.state_dtype = np.dtype(state_dtype)
         if not self.state_dtype.names or "terminal" not in self.state_dtype.names:
@@ -145,6 +148,13 @@ class CudaModel(ProblemModel):
         else:
             raw = np.ascontiguousarray(np.asarray(params)).view(np.uint8).reshape(-1)
         self.params = raw.copy()
+        self.tables = {k: np.ascontiguousarray(v) for k, v in (tables or {}).items()}
+        if self.tables:
+            names = getattr(np.asarray(params), "dtype", np.dtype([])).names or ()
+            missing = [k for k in self.tables if k not in names or np.asarray(params).dtype[k] != np.dtype("<u8")]
+            if missing:
+                raise ValueError(f"tables {missing} need '<u8' (pointer) fields of the same name in a structured params")
+            self._params_dtype = np.asarray(params).dtype
         self._initial = initial_states
         self._ref_logp = None if reference_log_probs is None else np.asarray(reference_log_probs, np.float64)
         self._lib = None
@@ -168,7 +178,13 @@ class CudaModel(ProblemModel):
         lib = self.library()
         dm = DeviceModel(_lib.VP_MODEL_USER, self.spec, self.state_dtype, self.pack, unpack=RecordStates)
         dm.lib = lib
-        dm.desc.user_params = dm.upload(self.params)
+        raw = self.params
+        if self.tables:  # device addresses of the uploaded tables into their pointer fields
+            p = raw.view(self._params_dtype)[0].copy()
+            for k, v in self.tables.items():
+                p[k] = dm.upload(v)
+            raw = np.frombuffer(p.tobytes(), dtype=np.uint8).copy()
+        dm.desc.user_params = dm.upload(raw)
         dm.desc.user_param_bytes = len(self.params)
         return dm
 

@@ -140,8 +140,10 @@ def test_plugin_with_reference_policy(tiger):
     """reference_log_probs (core.py:109-112) of a plug-in shape the initial PSI rows like a built-in's."""
     om = oracle.tiger_model()
     logp = np.log(np.array([0.6, 0.2, 0.2]))
-    biased = vp.CudaModel(tiger.spec, tiger.state_dtype, tiger.source, tiger.params,
-                          reference_log_probs=logp)
+    from paper_2510_27191_b200.envs.plugin_examples import TAB_PARAMS
+
+    biased = vp.CudaModel(tiger.spec, tiger.state_dtype, tiger.source, tiger.params.view(TAB_PARAMS),
+                          reference_log_probs=logp, tables=tiger.tables)
 
     class BiasedTiger(oracle.TabularModel):
         def reference_log_probs(self):
@@ -155,5 +157,43 @@ def test_plugin_with_reference_policy(tiger):
     out = vp.plan(belief, biased, cfg, rng, precision="fp64", exact=True, keep_tree=True)
     assert out.tree_stats == want.tree_stats and out.chosen_action == want.chosen_action
     t, w = out.tree.tables(), want.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(t[k], np.asarray(w[k]).astype(np.int64), err_msg=k)
+
+
+def _random_pomdp(S, A, O, seed):
+    g = np.random.default_rng(seed)
+    t = g.dirichlet(np.ones(S) * 0.3, size=(A, S))
+    z = g.dirichlet(np.ones(O) * 0.5, size=(A, S))
+    term = np.zeros(S, dtype=bool)
+    term[-1] = True
+    t[:, -1, :] = 0.0
+    t[:, -1, -1] = 1.0
+    b0 = np.ones(S) / (S - 1)
+    b0[-1] = 0.0
+    return oracle.TabularPOMDP(t, z, g.normal(size=(S, A)), b0, 0.95, term, "random", 60)
+
+
+def test_large_tabular_plugin_with_hbm_tables_equals_oracle():
+    """Tables of any size travel as HBM arrays behind Params pointers (CudaModel tables=)."""
+    pomdp = _random_pomdp(40, 6, 7, 3)
+    om = oracle.TabularModel(pomdp)
+    pm = tabular_cuda_model(pomdp)
+    g = np.random.default_rng(4)
+    n = 8192
+    states = om.states_from_indices(g.integers(0, 40, n))
+    acts = g.integers(0, 6, n)
+    rng = oracle.RowRng.from_seed(2).derive(5).bind(np.arange(n))
+    want, got = om.step_batch(states, acts, rng), pm.step_batch(states, acts, rng)
+    np.testing.assert_array_equal(got.next_states.idx, want.next_states.idx)
+    np.testing.assert_array_equal(got.observations, want.observations)
+    np.testing.assert_array_equal(got.rewards, want.rewards)
+    belief = oracle.ParticleBelief.from_model(om, 2000, oracle.RowRng.from_seed(9).derive(3))
+    cfg = oracle.SolverConfig(n_parallel=1024, iterations=6)
+    rng = oracle.RowRng.from_seed(9).derive(1, 0)
+    ref = oracle.plan(belief, om, cfg, rng)
+    out = vp.plan(belief, pm, cfg, rng, precision="fp64", exact=True, keep_tree=True)
+    assert out.tree_stats == ref.tree_stats and out.chosen_action == ref.chosen_action
+    t, w = out.tree.tables(), ref.tree.tables()
     for k in INT_COLUMNS:
         np.testing.assert_array_equal(t[k], np.asarray(w[k]).astype(np.int64), err_msg=k)

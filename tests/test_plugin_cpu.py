@@ -54,9 +54,12 @@ def test_state_size_mismatch_is_refused(tiger):
 def test_model_validation():
     with pytest.raises(ValueError, match="terminal"):
         vp.CudaModel(vp.ProblemSpec("x", 2, 2, 0.9, 10), np.dtype([("idx", "<i4")]), "")
-    with pytest.raises(ValueError):
-        tabular_cuda_model(oracle.TabularPOMDP(np.ones((9, 2, 2)) / 2, np.ones((9, 2, 2)) / 2, np.zeros((2, 9)),
-                                               np.array([0.5, 0.5]), 0.9, np.array([False, False])))
+    spec = vp.ProblemSpec("x", 2, 2, 0.9, 10)
+    with pytest.raises(ValueError, match="pointer"):  # a table needs a '<u8' field of its name in params
+        vp.CudaModel(spec, TAB_STATE, "", np.zeros((), dtype=[("S", "<i4"), ("cum_t", "<f8")]),
+                     tables={"cum_t": np.zeros(4)})
+    with pytest.raises(ValueError, match="pointer"):
+        vp.CudaModel(spec, TAB_STATE, "", b"\0" * 16, tables={"cum_t": np.zeros(4)})
 
 
 def test_record_states_and_packing(tiger):
