@@ -386,6 +386,11 @@ static bool state_size_ok(const vp_model& M) {
     if (!ensure_stack(3 * sizeof(CrowdState))) return false;
   }
 #ifdef VP_PLUGIN_SOURCE
+  if constexpr (std::is_same<Model, UserModel>::value && coop_trait<Model>::value) {
+    if (!ensure_stack(3 * sizeof(typename Model::State))) return false;
+  }
+#endif
+#ifdef VP_PLUGIN_SOURCE
   if constexpr (std::is_same<Model, UserModel>::value) {
     if (!M.user_params || M.user_param_bytes < (int64_t)sizeof(UserModel::Params)) return false;
   }

@@ -15,6 +15,14 @@
 //                        uint32_t& obs, double& reward);          // G(s, a), in place
 //   __device__ double heuristic(const Params&, const State&);     // leaf value, 0 on terminal
 //   __device__ double obs_log_likelihood(const Params&, const State& next, int a, uint32_t obs);
+// A model whose record is too large for one lane (CrowdNav-sized) also defines
+//   #define VP_USER_COOP 1
+//   __device__ void step_warp(const Params&, State& s, int a, const RowDraws& rng, bool live,
+//                             uint32_t& obs, double& reward);
+// called by all 32 lanes of a warp with warp-uniform (a, rng, live) and s in shared memory;
+// the lanes split the record, every lane returns the same (obs, reward), and the result must
+// equal step()'s (the search and the device SIR step one row per warp with it; the
+// environment step and vp_model_step use step()).
 // The source is included inside namespace vp_user after the library's headers: it must
 // not #include anything itself (<cstdint> types, CUDA math and the runtime are in scope).
 // RowDraws is the row's BoundRng (rng.py:96-120): rng.uniform(site) is
@@ -59,6 +67,21 @@ struct UserModel {
     obs = o;
     rew = w;
   }
+#ifdef VP_USER_COOP
+  static constexpr bool kCoop = true;
+  static __device__ __forceinline__ void step_warp(const vp_model& M, State& s, int a, u64 mkey, u64 row, bool live,
+                                                   u32& obs, double& rew, int rk) {
+    obs = 0;
+    rew = 0.0;
+    if (!live) return;
+    const RowDraws r{mkey, row, rk};
+    u32 o = 0;
+    double w = 0.0;
+    vp_user::step_warp(params(M), s, a, r, live, o, w);
+    obs = o;
+    rew = w;
+  }
+#endif
   static __device__ __forceinline__ double heuristic(const vp_model& M, const State& s) {
     return vp_user::heuristic(params(M), s);
   }

@@ -152,3 +152,99 @@ def corridor_cuda_model(length: float = 20.0, sigma: float = 1.5, nbins: int = 1
 
     spec = ProblemSpec("corridor-cuda", 3, nbins, 0.95, 60)
     return CudaModel(spec, CORRIDOR_STATE, CORRIDOR_SOURCE, p, initial_states=initial_states)
+
+
+LEVELS_SOURCE = r"""
+// "Levels": k hidden gauges (floats) drift with the action plus per-gauge Gaussian noise;
+// the observation counts the gauges above 0, the reward is minus the gauges outside [-1, 1].
+// A 520-byte record: the search steps it with a whole warp (VP_USER_COOP build, step_warp).
+struct Params {
+  int32_t k, horizon;
+  double noise;
+};
+struct State {
+  float level[128];
+  int32_t t, terminal;
+};
+__device__ __forceinline__ double levels_delta(int a) { return a == 0 ? -0.5 : a == 1 ? -0.1 : a == 2 ? 0.1 : 0.5; }
+__device__ __forceinline__ float levels_next(const Params& P, float v, int a, const RowDraws& rng, int i) {
+  return (float)((double)v + levels_delta(a) + P.noise * rng.normal(0, (uint64_t)(i + 1)));
+}
+__device__ void step(const Params& P, State& s, int a, const RowDraws& rng, uint32_t& obs, double& reward) {
+  if (s.terminal) { obs = (uint32_t)(P.k + 1); reward = 0.0; return; }
+  int above = 0, out = 0;
+  for (int i = 0; i < P.k; ++i) {
+    const float v = levels_next(P, s.level[i], a, rng, i);
+    s.level[i] = v;
+    above += v > 0.0f;
+    out += fabsf(v) > 1.0f;
+  }
+  s.t += 1;
+  s.terminal = s.t >= P.horizon;
+  reward = -(double)out;
+  obs = s.terminal ? (uint32_t)(P.k + 1) : (uint32_t)above;
+}
+__device__ double heuristic(const Params& P, const State& s) {
+  if (s.terminal) return 0.0;
+  int out = 0;
+  for (int i = 0; i < P.k; ++i) out += fabsf(s.level[i]) > 1.0f;
+  return -0.5 * (double)out * (double)(P.horizon - s.t);
+}
+__device__ double obs_log_likelihood(const Params& P, const State& s, int, uint32_t obs) {
+  if (obs == (uint32_t)(P.k + 1)) return s.terminal ? 0.0 : -INFINITY;
+  if (s.terminal) return -INFINITY;
+  int above = 0;
+  for (int i = 0; i < P.k; ++i) above += s.level[i] > 0.0f;
+  return (uint32_t)above == obs ? 0.0 : -INFINITY;
+}
+"""
+
+LEVELS_COOP = r"""
+#define VP_USER_COOP 1
+""" + LEVELS_SOURCE + r"""
+// the same step with the 32 lanes splitting the gauges (integer counts: any order is exact)
+__device__ void step_warp(const Params& P, State& s, int a, const RowDraws& rng, bool, uint32_t& obs, double& reward) {
+  const int lane = threadIdx.x & 31;
+  const bool was_terminal = s.terminal;
+  __syncwarp();
+  if (was_terminal) { obs = (uint32_t)(P.k + 1); reward = 0.0; return; }
+  int above = 0, out = 0;
+  for (int i = lane; i < P.k; i += 32) {
+    const float v = levels_next(P, s.level[i], a, rng, i);
+    s.level[i] = v;
+    above += v > 0.0f;
+    out += fabsf(v) > 1.0f;
+  }
+  for (int o = 16; o; o >>= 1) {
+    above += __shfl_xor_sync(0xffffffffu, above, o);
+    out += __shfl_xor_sync(0xffffffffu, out, o);
+  }
+  __syncwarp();
+  const int t = s.t + 1;
+  const bool term = t >= P.horizon;
+  if (lane == 0) { s.t = t; s.terminal = term; }
+  __syncwarp();
+  reward = -(double)out;
+  obs = term ? (uint32_t)(P.k + 1) : (uint32_t)above;
+}
+"""
+
+LEVELS_STATE = np.dtype([("level", "<f4", (128,)), ("t", "<i4"), ("terminal", "<i4")])
+LEVELS_PARAMS = np.dtype([("k", "<i4"), ("horizon", "<i4"), ("noise", "<f8")])
+
+
+def levels_cuda_model(k: int = 96, horizon: int = 20, noise: float = 0.3, coop: bool = True) -> CudaModel:
+    """A large-record plug-in (520 B): ``coop`` builds the warp-cooperative form (one row per warp,
+    the record in shared memory); ``coop=False`` the same dynamics one row per lane."""
+    if not 1 <= k <= 128:
+        raise ValueError("k must be in [1, 128]")
+    p = np.zeros((), dtype=LEVELS_PARAMS)
+    p["k"], p["horizon"], p["noise"] = k, horizon, noise
+
+    def initial_states(n, rng):  # gauges ~ U[-1, 1)
+        out = np.zeros(n, dtype=LEVELS_STATE)
+        out["level"][:, :k] = (rng.derive(0).uniform(np.arange(n, dtype=np.int64), k) * 2.0 - 1.0).astype(np.float32)
+        return out
+
+    spec = ProblemSpec("levels-cuda", 4, k + 1, 0.95, horizon)
+    return CudaModel(spec, LEVELS_STATE, LEVELS_COOP if coop else LEVELS_SOURCE, p, initial_states=initial_states)

@@ -197,3 +197,45 @@ def test_large_tabular_plugin_with_hbm_tables_equals_oracle():
     t, w = out.tree.tables(), ref.tree.tables()
     for k in INT_COLUMNS:
         np.testing.assert_array_equal(t[k], np.asarray(w[k]).astype(np.int64), err_msg=k)
+
+
+@pytest.mark.parametrize("precision,exact", [("fp64", True), ("fp32", False)])
+def test_cooperative_plugin_equals_single_lane_form(precision, exact):
+    """A large-record plug-in (520 B) built warp-cooperative (VP_USER_COOP: one row per warp, the
+    lanes splitting the record) plans exactly like its one-row-per-lane build."""
+    from paper_2510_27191_b200.envs.plugin_examples import levels_cuda_model
+
+    coop, lane = levels_cuda_model(coop=True), levels_cuda_model(coop=False)
+    belief = vp.ParticleBelief.from_model(lane, 500, vp.RowRng.from_seed(2).derive(3))
+    cfg = vp.SolverConfig(n_parallel=1024, iterations=6)
+    rng = vp.RowRng.from_seed(2).derive(1, 0)
+    a = vp.plan(belief, coop, cfg, rng, precision=precision, exact=exact, keep_tree=True)
+    b = vp.plan(belief, lane, cfg, rng, precision=precision, exact=exact, keep_tree=True)
+    assert a.tree_stats == b.tree_stats and a.chosen_action == b.chosen_action
+    ta, tb = a.tree.tables(), b.tree.tables()
+    for k in INT_COLUMNS:
+        np.testing.assert_array_equal(ta[k], tb[k], err_msg=k)
+    # values: the backup's L2 reductions sum in arrival order (1 ulp apart between runs)
+    tol = 1e-12 if precision == "fp64" else 1e-5
+    np.testing.assert_allclose(ta["prefs"], tb["prefs"], rtol=tol, atol=tol * np.abs(tb["prefs"]).max())
+    assert a.tree_stats["belief_rows"] > 100
+
+
+def test_cooperative_plugin_sir_and_episode():
+    from paper_2510_27191_b200.envs.plugin_examples import levels_cuda_model
+
+    coop, lane = levels_cuda_model(coop=True), levels_cuda_model(coop=False)
+    belief = vp.ParticleBelief.from_model(lane, 2000, vp.RowRng.from_seed(4).derive(3))
+    env = lane.sample_initial_states(1, vp.RowRng.from_seed(4).derive(0, 0))
+    res = lane.step_batch(env, np.array([2]), vp.RowRng.from_seed(4).derive(0, 1).bind([0]))
+    o = int(res.observations[0])
+    rng = vp.RowRng.from_seed(4).derive(2, 1)
+    x = vp.sir_update(vp.DeviceBelief.from_host(belief, coop), coop, 2, o, rng, max_retries=3)
+    y = vp.sir_update(vp.DeviceBelief.from_host(belief, lane), lane, 2, o, rng, max_retries=3)
+    assert (x.retries, x.degenerate) == (y.retries, y.degenerate)
+    np.testing.assert_array_equal(x.belief.records.cpu().numpy(), y.belief.records.cpu().numpy())
+    cfg = vp.SolverConfig(n_parallel=512, iterations=4, particles=500)
+    ea = vp.run_episode(coop, cfg, seed=1, precision="fp64")
+    eb = vp.run_episode(lane, cfg, seed=1, precision="fp64")
+    assert (ea.steps, ea.terminal_reason) == (eb.steps, eb.terminal_reason)
+    assert ea.discounted_return == pytest.approx(eb.discounted_return, abs=1e-12)
