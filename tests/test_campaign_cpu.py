@@ -101,3 +101,11 @@ def test_cli_stream_kind():
     assert cfg.rng_kind == "splitmix64"
     with pytest.raises(SystemExit):
         build_parser().parse_args(["--problem", "tiger", "--rng", "xorshift"])
+
+
+def test_cli_plugin_problems():
+    """The example CudaModel plug-ins are campaign problems like the built-in ones."""
+    for name in ("corridor", "levels"):
+        cfg = config_from_args(build_parser().parse_args(["--problem", name, "--iterations", "3"]))
+        model = cfg.model_for(0)
+        assert type(model).__name__ == "CudaModel" and cfg.solver.n_parallel > 0
