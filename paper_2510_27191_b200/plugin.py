@@ -44,7 +44,8 @@ CSRC = os.path.join(_HERE, "csrc")
 PLUGIN_DIR = os.environ.get("VP_PLUGIN_DIR") or os.path.join(_HERE, "plugins")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
               "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr", "-shared"]
-_BUILD_LOCK = threading.Lock()
+_LOCKS_GUARD = threading.Lock()
+_BUILD_LOCKS: dict = {}  # one lock per plug-in path: different plug-ins build in parallel
 
 
 def _library_digest() -> str:
@@ -69,7 +70,9 @@ def compile_plugin(source: str, *, verbose: bool = False) -> str:
     path = plugin_path(source)
     if os.path.exists(path):
         return path
-    with _BUILD_LOCK:
+    with _LOCKS_GUARD:
+        lock = _BUILD_LOCKS.setdefault(path, threading.Lock())
+    with lock:
         if os.path.exists(path):
             return path
         nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
