@@ -260,12 +260,14 @@ def layout_mismatches() -> list:
             VpPlanArgs.out_dev.offset, VpTree.init_cdf.offset, VpTree.a_ckey.offset, VpSearchArgs.m.offset,
             VpModel.mars_gpow.offset, VpTree.psi_cdf.offset, VpModel.nav_log_miss.offset,
             VpModel.crowd_heur.offset, CROWD_STATE_BYTES, VpTree.b_rec.offset, VpTree.a_slot.offset,
-            VpTree.cap_dense.offset]
+            VpTree.cap_dense.offset, VpModel.rng_kind.offset, VpModel.user_params.offset,
+            VpModel.user_param_bytes.offset]
     names = ["sizeof(vp_model)", "sizeof(vp_tree)", "sizeof(vp_work)", "sizeof(vp_search_args)",
              "vp_model.tab_states", "vp_model.ld_bins", "vp_tree.eta", "vp_work.trace_belief",
              "vp_search_args.start_beliefs", "sizeof(Slot)", "sizeof(vp_plan_args)", "vp_plan_args.out_dev",
              "vp_tree.init_cdf", "vp_tree.a_ckey", "vp_search_args.m", "vp_model.mars_gpow", "vp_tree.psi_cdf", "vp_model.nav_log_miss",
-             "vp_model.crowd_heur", "sizeof(CrowdState)", "vp_tree.b_rec", "vp_tree.a_slot", "vp_tree.cap_dense"]
+             "vp_model.crowd_heur", "sizeof(CrowdState)", "vp_tree.b_rec", "vp_tree.a_slot", "vp_tree.cap_dense",
+             "vp_model.rng_kind", "vp_model.user_params", "vp_model.user_param_bytes"]
     return [(nm, a, b) for nm, a, b in zip(names, list(buf), mine) if a != b]
 
 

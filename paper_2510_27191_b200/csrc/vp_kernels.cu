@@ -999,7 +999,9 @@ int32_t vp_abi_layout(int32_t* out, int32_t n) {
                        (int32_t)offsetof(vp_tree, psi_cdf),
                        (int32_t)offsetof(vp_model, nav_log_miss), (int32_t)offsetof(vp_model, crowd_heur),
                        (int32_t)sizeof(CrowdState), (int32_t)offsetof(vp_tree, b_rec),
-                       (int32_t)offsetof(vp_tree, a_slot), (int32_t)offsetof(vp_tree, cap_dense)};
+                       (int32_t)offsetof(vp_tree, a_slot), (int32_t)offsetof(vp_tree, cap_dense),
+                       (int32_t)offsetof(vp_model, rng_kind), (int32_t)offsetof(vp_model, user_params),
+                       (int32_t)offsetof(vp_model, user_param_bytes)};
   const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
   if (!out) return m;
   for (int32_t i = 0; i < n && i < m; ++i) out[i] = v[i];
