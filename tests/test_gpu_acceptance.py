@@ -231,3 +231,30 @@ def test_batch_scaling_sanity_spec10():
                 ms.append(e0.elapsed_time(e1))
         rate[n] = n * sum(range(1, 9)) / sorted(ms)[len(ms) // 2]
     assert rate[32768] >= 8.0 * rate[1024], rate
+
+
+@pytest.mark.parametrize("model_name", ["mars", "crowdnav"])
+def test_structural_invariants_through_a_campaign_spec9(model_name):
+    """SPEC ACCEPTANCE 9: through a closed loop (device belief, device SIR), every planning step's
+    tree has unique A-pairs and B-pairs and conserves visits (sum of visits = rows x levels
+    expanded), and every belief update leaves normalised weights."""
+    import torch
+
+    model = vp.MarsModel(7, 8, layout_seed=3) if model_name == "mars" else vp.CrowdNavModel(n_people=40)
+    cfg = vp.SolverConfig(n_parallel=1024, iterations=6, particles=1000)
+    root = vp.RowRng.from_seed(11)
+    env = model.sample_initial_states(1, root.derive(0, 0))
+    belief = vp.DeviceBelief.from_host(vp.ParticleBelief.from_model(model, cfg.particles, root.derive(3)), model)
+    for t in range(8):
+        out = vp.plan(belief, model, cfg, root.derive(1, t), keep_tree=True)
+        out.tree.validate()  # unique (belief, action) and (action, observation) edges, depth chain
+        visits = out.tree.tables()["action_visits"].sum()
+        assert visits == cfg.n_parallel * sum(min(i + 1, cfg.d_max_cap) for i in range(cfg.iterations))
+        res = model.step_batch(env, np.array([out.chosen_action]), root.derive(2, t).bind([0]))
+        if bool(res.next_states.terminal[0]):
+            break
+        upd = vp.sir_update(belief, model, out.chosen_action, int(res.observations[0]), root.derive(4, t),
+                            exact=False)
+        w = upd.belief.weights_dev.double()
+        assert torch.isfinite(w).all() and abs(float(w.sum()) - 1.0) < 1e-9
+        env, belief = res.next_states, upd.belief
